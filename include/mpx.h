@@ -1,0 +1,215 @@
+/* libmpx — B200 (sm_100a) kernels for the secret-shared fixed-point engine.
+ *
+ * Drop-in boundary for the hot path of arXiv 2402.02320's reference package
+ * `mpfix` (/root/reference/pkg/src/mpfix). The reference is pure Python +
+ * numpy; its "FFI" for this path is the Python operator API
+ * (protocols/__init__.py:1-30, nonlinear.py, nn.py). This C ABI is what the
+ * Python host mirror (paper_2402_02320_b200/) binds through ctypes; each entry
+ * point names the reference code it replaces.
+ *
+ * Conventions
+ *  - Every function returns MPX_OK (0) or a negative MPX_ERR_* code, never
+ *    allocates or frees, never synchronizes, and runs on `stream`
+ *    (a cudaStream_t passed as void*; NULL = legacy default stream).
+ *  - Pointers are DEVICE pointers unless the parameter name ends in `_host`.
+ *  - Ring elements: uint64 words masked to `width` (w in 1..64), Z_2^w
+ *    arithmetic wraps (ring.py:20-62).
+ *  - Share arrays hold L local parties, party-major and contiguous:
+ *    element i of local party l is at [l * n + i]. Sim mode puts all n
+ *    parties on one GPU (L = n); party mode runs one process per party per
+ *    GPU (L = 1).
+ *  - Dealer material arrays carry their own party stride `*_ps` (elements or
+ *    words) and the host passes pointers already advanced to the store cursor
+ *    (preprocessing.py:281-291). Bit material is a flat packed bit stream per
+ *    party (bit t = item t) and is addressed by absolute bit offset `*_bit`.
+ *  - Binary shares are row-packed: one uint64 word per row, low `m` bits are
+ *    the row's trailing bit axis, LSB first (ring.py:110-114).
+ *  - `p0` = local slot of party 0, or -1 when party 0 is not local: public
+ *    constants land on party 0 only (sharing.py:99-121).
+ */
+#ifndef MPX_H_
+#define MPX_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPX_OK 0
+#define MPX_ERR_ARG (-1)
+#define MPX_ERR_CUDA (-2)
+#define MPX_ERR_UNSUPPORTED (-3)
+
+/* bit-op codes for mpx_bits_op */
+#define MPX_BITS_XOR 0      /* out = a ^ b                                   */
+#define MPX_BITS_AND 1      /* out = a & b                                   */
+#define MPX_BITS_AND_PUB 2  /* out = a & pub[row]        (sharing.py:84-86)  */
+#define MPX_BITS_XOR_PUB 3  /* out = a ^ [p0] pub[row]   (sharing.py:99-103) */
+#define MPX_BITS_XOR_SHR1 4 /* out = a ^ (a >> 1)        (derived.py:148)    */
+#define MPX_BITS_PARITY 5   /* out = popcount(a & mask(m)) & 1 (nonlinear.py:243) */
+#define MPX_BITS_SIGNFOLD 6 /* out = (a & mask(m)) ^ (bit m of a ? mask(m):0) (nonlinear.py:162) */
+#define MPX_BITS_SHL_OR 7   /* out = (a & mask(imm)) | (b << imm)  (bit-axis concat) */
+#define MPX_BITS_BCAST_PUB 8 /* out = a ^ [p0] pub[0]  (public constant pattern) */
+
+/* Library identity / diagnostics. */
+const char* mpx_version(void);
+int mpx_last_cuda_error(void);
+const char* mpx_cuda_error_string(int code);
+int mpx_device_sm_count(int device);
+
+/* ---- local ring arithmetic (ring.py:44-62, sharing.py:37-56,99-121) ---- */
+/* out[l][i] = ka*a[l][i] + kb*b[l][i] + [l==p0](c0 + cv[i % cv_len])  mod 2^w.
+ * b and cv may be NULL. Covers add/sub/neg/mul_public/add_public/add_const/
+ * scale_fixed (derived.py:73-83) and narrow/cast_down (nn.py:68-74). */
+int mpx_ring_lin(uint64_t* out, const uint64_t* a, uint64_t ka, const uint64_t* b, uint64_t kb,
+                 uint64_t c0, const uint64_t* cv, int64_t cv_len, int L, int64_t n, int width, int p0,
+                 void* stream);
+/* out[i] = a[i] * b[i] mod 2^w (public elementwise product; dealer c = a*b,
+ * preprocessing.py:141). */
+int mpx_ring_mul(uint64_t* out, const uint64_t* a, const uint64_t* b, int64_t n, int width, void* stream);
+/* out[l][r] = sum_j wts[j] * x[l][r][j] mod 2^w; wts NULL = all ones.
+ * Row sums (nn.py:134), compose weights (basic.py:193-195), one-hot
+ * contractions (nonlinear.py:117-122, 252-256). */
+int mpx_ring_rowdot(uint64_t* out, const uint64_t* x, const uint64_t* wts, int L, int64_t rows,
+                    int64_t cols, int width, void* stream);
+
+/* ---- fixed-point codec (ring.py:76-89) ---- */
+int mpx_encode(uint64_t* out, const double* in, int64_t n, int width, int frac, void* stream);
+int mpx_decode(double* out, const uint64_t* in, int64_t n, int width, int frac, void* stream);
+
+/* ---- openings: local-party reduction of one round (session.py:71-115) ----
+ * Sim mode: the reduction over all L parties IS the opening. Party mode: the
+ * partial is all-reduced (sum) / all-gathered (xor) over NCCL by the host. */
+int mpx_open_sum(uint64_t* out, const uint64_t* x, int L, int64_t n, int width, void* stream);
+int mpx_open_xor(uint64_t* out, const uint64_t* x, int L, int64_t n, void* stream);
+/* out[i] = sum_l (x[l][i] - a[l][i]) mod 2^w: the masked opening of Beaver
+ * mul/matmul (basic.py:36, :66) and decompose (basic.py:211). */
+int mpx_mask_sub(uint64_t* out, const uint64_t* x, const uint64_t* a, int64_t a_ps, int L, int64_t n,
+                 int width, void* stream);
+
+/* ---- Beaver multiplication (basic.py:27-42) ----
+ * z_l = c_l + d*b_l + e*a_l + [l==p0] d*e. */
+int mpx_mul_finish(uint64_t* z, const uint64_t* d, const uint64_t* e, const uint64_t* a,
+                   const uint64_t* b, const uint64_t* c, int64_t t_ps, int L, int64_t n, int width,
+                   int p0, void* stream);
+/* Fused sim-mode round (L parties on this GPU, no peer): mask, open and
+ * finish in one pass. */
+int mpx_mul_fused(uint64_t* z, const uint64_t* x, const uint64_t* y, const uint64_t* a,
+                  const uint64_t* b, const uint64_t* c, int64_t t_ps, int L, int64_t n, int width,
+                  int p0, void* stream);
+
+/* ---- probabilistic truncation (derived.py:20-70) ----
+ * mask: out[i] = sum_l (x + r_lo + 2^f r_hi + [l==p0] bias)   (r_hi may be NULL)
+ * finish: z_l = -r_hi_l + [l==p0]((c >> f) - unbias)            mod 2^w */
+int mpx_trunc_mask(uint64_t* out, const uint64_t* x, const uint64_t* r_lo, int64_t lo_ps,
+                   const uint64_t* r_hi, int64_t hi_ps, int L, int64_t n, int width, int f,
+                   uint64_t bias, int p0, void* stream);
+int mpx_trunc_finish(uint64_t* z, const uint64_t* c, const uint64_t* r_hi, int64_t hi_ps, int L,
+                     int64_t n, int width, int f, uint64_t unbias, int p0, void* stream);
+int mpx_trunc_fused(uint64_t* z, const uint64_t* x, const uint64_t* r_lo, int64_t lo_ps,
+                    const uint64_t* r_hi, int64_t hi_ps, int L, int64_t n, int width, int f,
+                    uint64_t bias, uint64_t unbias, int p0, void* stream);
+
+/* ---- binary Beaver AND on row-packed bits (basic.py:82-95) ----
+ * triple for (row r, bit j) = bit (t_bit + r*m + j) of the bintriple stream. */
+int mpx_and_mask(uint64_t* d, uint64_t* e, const uint64_t* x, const uint64_t* y, const uint64_t* ta,
+                 const uint64_t* tb, int64_t t_ps, int64_t t_bit, int L, int64_t rows, int m,
+                 void* stream);
+int mpx_and_finish(uint64_t* z, const uint64_t* d, const uint64_t* e, const uint64_t* ta,
+                   const uint64_t* tb, const uint64_t* tc, int64_t t_ps, int64_t t_bit, int L,
+                   int64_t rows, int m, int p0, void* stream);
+
+/* ---- Kogge-Stone carry level (basic.py:98-129) at shift s over m bits ----
+ * Non-final level: one AND call on [p_hi|p_hi] & [g_lo|p_lo] (row width
+ * 2(m-s)); final level: p_hi & g_lo (row width m-s). G, P updated in place.
+ * dg/eg/dp/ep: opened masked words (dp/ep unused on the final level). */
+int mpx_carry_mask(uint64_t* dg, uint64_t* eg, uint64_t* dp, uint64_t* ep, const uint64_t* G,
+                   const uint64_t* P, const uint64_t* ta, const uint64_t* tb, int64_t t_ps,
+                   int64_t t_bit, int L, int64_t rows, int m, int s, int last, void* stream);
+int mpx_carry_finish(uint64_t* G, uint64_t* P, const uint64_t* dg, const uint64_t* eg,
+                     const uint64_t* dp, const uint64_t* ep, const uint64_t* ta, const uint64_t* tb,
+                     const uint64_t* tc, int64_t t_ps, int64_t t_bit, int L, int64_t rows, int m,
+                     int s, int last, int p0, void* stream);
+int mpx_carry_fused(uint64_t* G, uint64_t* P, const uint64_t* ta, const uint64_t* tb,
+                    const uint64_t* tc, int64_t t_ps, int64_t t_bit, int L, int64_t rows, int m,
+                    int s, int last, int p0, void* stream);
+/* Public-operand adder set-up (basic.py:139-152): G = x & pub, P = P0 = x ^ [p0] pub.
+ * x comes from `x` (row words, L x rows) or, when x == NULL, from the edaBit
+ * bit stream xb (bit xb_bit + r*m + j) as in decompose (basic.py:199-214). */
+int mpx_pubadd_init(uint64_t* G, uint64_t* P, uint64_t* P0, const uint64_t* pub, const uint64_t* x,
+                    const uint64_t* xb, int64_t xb_ps, int64_t xb_bit, int L, int64_t rows, int m,
+                    int p0, void* stream);
+/* sum = P0 ^ (carries << 1)  (basic.py:132-136) */
+int mpx_sum_from_carries(uint64_t* out, const uint64_t* P0, const uint64_t* G, int L, int64_t rows,
+                         int m, void* stream);
+
+/* ---- leftmost-one suffix-OR level (derived.py:131-149) ----
+ * lo = Y[:m-s], hi = Y[s:]; Y[:m-s] = lo ^ hi ^ AND(lo, hi). */
+int mpx_lmo_mask(uint64_t* d, uint64_t* e, const uint64_t* Y, const uint64_t* ta, const uint64_t* tb,
+                 int64_t t_ps, int64_t t_bit, int L, int64_t rows, int m, int s, void* stream);
+int mpx_lmo_finish(uint64_t* Y, const uint64_t* d, const uint64_t* e, const uint64_t* ta,
+                   const uint64_t* tb, const uint64_t* tc, int64_t t_ps, int64_t t_bit, int L,
+                   int64_t rows, int m, int s, int p0, void* stream);
+int mpx_lmo_fused(uint64_t* Y, const uint64_t* ta, const uint64_t* tb, const uint64_t* tc,
+                  int64_t t_ps, int64_t t_bit, int L, int64_t rows, int m, int s, int p0,
+                  void* stream);
+
+/* ---- daBit conversion (basic.py:164-196) ----
+ * mask: c[r] = xor_l (b_l[r] ^ rbits_l(r)) ; daBit (r, j) = bit rb_bit + r*m + j.
+ * finish: z = r_arith*(1-2c) + [p0] c ; mode 0 writes z as (L, rows, m),
+ * mode 1 writes sum_j wts[j]*z (L, rows) (compose). */
+int mpx_bit2a_mask(uint64_t* c, const uint64_t* b, const uint64_t* rbits, int64_t rb_ps,
+                   int64_t rb_bit, int L, int64_t rows, int m, void* stream);
+int mpx_bit2a_finish(uint64_t* out, const uint64_t* c, const uint64_t* rarith, int64_t ra_ps, int L,
+                     int64_t rows, int m, int width, int p0, const uint64_t* wts, int mode,
+                     void* stream);
+
+/* ---- local bit manipulation on row-packed words ---- */
+int mpx_bits_op(uint64_t* out, const uint64_t* a, const uint64_t* b, int op, int L, int64_t rows,
+                int m, int p0, int imm, void* stream);
+/* out[i] bit t = in[i] bit src_host[t] (src < 0 -> 0), t < k. Slicing,
+ * reversal and bit selection of the trailing axis (nonlinear.py:170,199,344). */
+int mpx_bits_gather(uint64_t* out, const uint64_t* in, const int8_t* src_host, int k, int64_t nwords,
+                    void* stream);
+/* uint8-per-bit (rows, m) <-> row-packed words (BShare layout conversion). */
+int mpx_bits_pack(uint64_t* out, const uint8_t* in, int64_t rows, int m, void* stream);
+int mpx_bits_unpack(uint8_t* out, const uint64_t* in, int64_t rows, int m, void* stream);
+/* Flat bit stream (bit t) -> row words (m bits per row) and back. */
+int mpx_bits_flat_to_rows(uint64_t* out, const uint64_t* flat, int64_t flat_bit, int64_t rows, int m,
+                          void* stream);
+int mpx_bits_rows_to_flat(uint64_t* flat, const uint64_t* rows_in, int64_t rows, int m, void* stream);
+
+/* ---- Z_2^64 GEMM (ring.py:60-62; basic.py:72-75; nn.py:193) ----
+ * C[b] (+)= A[b] @ B[b] mod 2^w, row-major, A: MxK, B: KxN, C: MxN,
+ * batch strides sA/sB/sC in elements (0 broadcasts). */
+int mpx_gemm(uint64_t* C, const uint64_t* A, const uint64_t* B, int64_t batch, int64_t M, int64_t K,
+             int64_t N, int64_t sA, int64_t sB, int64_t sC, int accumulate, int width, void* stream);
+/* Same contract, forced onto the exact 64-bit SIMT tiles (reference shape). */
+int mpx_gemm_simt(uint64_t* C, const uint64_t* A, const uint64_t* B, int64_t batch, int64_t M,
+                  int64_t K, int64_t N, int64_t sA, int64_t sB, int64_t sC, int accumulate, int width,
+                  void* stream);
+
+/* ---- trusted dealer (preprocessing.py:121-174; ring.py:124-134) ----
+ * Philox4x64-10 keyed (k0, k1) exactly as numpy; the byte stream is read as
+ * u32 words from u32 index `u32_off` (Generator.bytes semantics). */
+int mpx_philox_elems(uint64_t* out, uint64_t k0, uint64_t k1, int64_t u32_off, int64_t count,
+                     int width, void* stream);
+int mpx_philox_bits(uint64_t* out_words, uint64_t k0, uint64_t k1, int64_t u32_off, int64_t count,
+                    void* stream);
+/* Additive shares of `secret` (count elems) for global parties p_lo..p_lo+L-1:
+ * party p < n-1 gets draw p (u32 offset u32_base + p*2*count), the last party
+ * gets secret - sum(draws) (sharing.py:124-133). */
+int mpx_deal_share_arith(uint64_t* out, int64_t out_ps, const uint64_t* secret, uint64_t k0,
+                         uint64_t k1, int64_t u32_base, int64_t count, int n, int p_lo, int L,
+                         int width, void* stream);
+/* XOR shares of a packed bit stream `secret_words` (count bits); draw k at
+ * u32 offset u32_base + k*ceil(count/4) (sharing.py:144-152). */
+int mpx_deal_share_bits(uint64_t* out, int64_t out_ps, const uint64_t* secret_words, uint64_t k0,
+                        uint64_t k1, int64_t u32_base, int64_t count, int n, int p_lo, int L,
+                        void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPX_H_ */

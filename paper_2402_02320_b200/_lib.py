@@ -1,0 +1,132 @@
+"""ctypes binding of libmpx.so (the C ABI declared in include/mpx.h).
+
+The shared library is built in-tree (``__graft_entry__.build()``). There is
+no CPU fallback: if the library is missing or a call fails the product path
+raises ``MpxError``. Tensors cross the ABI as raw device pointers; the
+launching stream is torch's current CUDA stream.
+
+Dry runs (``DemandCounter`` sessions, preprocessing.py:369-403) allocate
+``meta`` tensors; every wrapper skips the launch when its output is meta, so
+the same protocol code sizes the dealer material without touching a GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmpx.so")
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_L = ctypes.c_int64
+_U = ctypes.c_uint64
+
+_SIGS = {
+    "mpx_ring_lin": [_P, _P, _U, _P, _U, _U, _P, _L, _I, _L, _I, _I, _P],
+    "mpx_ring_mul": [_P, _P, _P, _L, _I, _P],
+    "mpx_ring_rowdot": [_P, _P, _P, _I, _L, _L, _I, _P],
+    "mpx_encode": [_P, _P, _L, _I, _I, _P],
+    "mpx_decode": [_P, _P, _L, _I, _I, _P],
+    "mpx_open_sum": [_P, _P, _I, _L, _I, _P],
+    "mpx_open_xor": [_P, _P, _I, _L, _P],
+    "mpx_mask_sub": [_P, _P, _P, _L, _I, _L, _I, _P],
+    "mpx_mul_finish": [_P, _P, _P, _P, _P, _P, _L, _I, _L, _I, _I, _P],
+    "mpx_mul_fused": [_P, _P, _P, _P, _P, _P, _L, _I, _L, _I, _I, _P],
+    "mpx_trunc_mask": [_P, _P, _P, _L, _P, _L, _I, _L, _I, _I, _U, _I, _P],
+    "mpx_trunc_finish": [_P, _P, _P, _L, _I, _L, _I, _I, _U, _I, _P],
+    "mpx_trunc_fused": [_P, _P, _P, _L, _P, _L, _I, _L, _I, _I, _U, _U, _I, _P],
+    "mpx_and_mask": [_P, _P, _P, _P, _P, _P, _L, _L, _I, _L, _I, _P],
+    "mpx_and_finish": [_P, _P, _P, _P, _P, _P, _L, _L, _I, _L, _I, _I, _P],
+    "mpx_carry_mask": [_P, _P, _P, _P, _P, _P, _P, _P, _L, _L, _I, _L, _I, _I, _I, _P],
+    "mpx_carry_finish": [_P, _P, _P, _P, _P, _P, _P, _P, _P, _L, _L, _I, _L, _I, _I, _I, _I, _P],
+    "mpx_carry_fused": [_P, _P, _P, _P, _P, _L, _L, _I, _L, _I, _I, _I, _I, _P],
+    "mpx_pubadd_init": [_P, _P, _P, _P, _P, _P, _L, _L, _I, _L, _I, _I, _P],
+    "mpx_sum_from_carries": [_P, _P, _P, _I, _L, _I, _P],
+    "mpx_lmo_mask": [_P, _P, _P, _P, _P, _L, _L, _I, _L, _I, _I, _P],
+    "mpx_lmo_finish": [_P, _P, _P, _P, _P, _P, _L, _L, _I, _L, _I, _I, _I, _P],
+    "mpx_lmo_fused": [_P, _P, _P, _P, _L, _L, _I, _L, _I, _I, _I, _P],
+    "mpx_bit2a_mask": [_P, _P, _P, _L, _L, _I, _L, _I, _P],
+    "mpx_bit2a_finish": [_P, _P, _P, _L, _I, _L, _I, _I, _I, _P, _I, _P],
+    "mpx_bits_op": [_P, _P, _P, _I, _I, _L, _I, _I, _I, _P],
+    "mpx_bits_gather": [_P, _P, _P, _I, _L, _P],
+    "mpx_bits_pack": [_P, _P, _L, _I, _P],
+    "mpx_bits_unpack": [_P, _P, _L, _I, _P],
+    "mpx_bits_flat_to_rows": [_P, _P, _L, _L, _I, _P],
+    "mpx_bits_rows_to_flat": [_P, _P, _L, _I, _P],
+    "mpx_gemm": [_P, _P, _P, _L, _L, _L, _L, _L, _L, _L, _I, _I, _P],
+    "mpx_gemm_simt": [_P, _P, _P, _L, _L, _L, _L, _L, _L, _L, _I, _I, _P],
+    "mpx_philox_elems": [_P, _U, _U, _L, _L, _I, _P],
+    "mpx_philox_bits": [_P, _U, _U, _L, _L, _P],
+    "mpx_deal_share_arith": [_P, _L, _P, _U, _U, _L, _L, _I, _I, _I, _I, _P],
+    "mpx_deal_share_bits": [_P, _L, _P, _U, _U, _L, _L, _I, _I, _I, _P],
+    "mpx_last_cuda_error": [],
+    "mpx_device_sm_count": [_I],
+}
+
+BITS_XOR, BITS_AND, BITS_AND_PUB, BITS_XOR_PUB, BITS_XOR_SHR1, BITS_PARITY, BITS_SIGNFOLD, \
+    BITS_SHL_OR, BITS_BCAST_PUB = range(9)
+
+
+class MpxError(RuntimeError):
+    """A libmpx call failed (bad argument or CUDA error)."""
+
+
+_lib = None
+
+
+def exported_symbols() -> list[str]:
+    return sorted(list(_SIGS) + ["mpx_version", "mpx_cuda_error_string"])
+
+
+def load() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise MpxError(f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                       "(the B200 path has no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, args in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    lib.mpx_version.restype = ctypes.c_char_p
+    lib.mpx_version.argtypes = []
+    lib.mpx_cuda_error_string.restype = ctypes.c_char_p
+    lib.mpx_cuda_error_string.argtypes = [_I]
+    _lib = lib
+    return lib
+
+
+def version() -> str:
+    return load().mpx_version().decode()
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t) -> int | None:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def call(name: str, *args) -> None:
+    """Invoke one libmpx entry point; raise MpxError on a non-zero return."""
+    lib = load()
+    rc = getattr(lib, name)(*args, stream_ptr())
+    if rc != 0:
+        if rc == -2:
+            code = lib.mpx_last_cuda_error()
+            msg = lib.mpx_cuda_error_string(code).decode()
+            raise MpxError(f"{name}: CUDA error {code} ({msg})")
+        raise MpxError(f"{name}: returned {rc} (invalid argument)")
+
+
+def is_dry(*tensors) -> bool:
+    return any(t is not None and t.is_meta for t in tensors)

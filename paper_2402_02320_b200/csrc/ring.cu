@@ -1,0 +1,351 @@
+// Local ring arithmetic, codec, openings and bit-layout kernels.
+//
+// These are the HBM-bound elementwise pieces of the path (SURVEY §2.2 K3,
+// K11, K12, K14): one pass, 64-bit words, grid-stride over all local
+// parties. Reference: ring.py:20-134, sharing.py:37-121, session.py:71-115.
+#include "common.cuh"
+
+// --------------------------------------------------------------------------
+// out = ka*a + kb*b + [l==p0](c0 + cv[i % cv_len])
+
+__global__ void k_ring_lin(u64* __restrict__ out, const u64* __restrict__ a, u64 ka,
+                           const u64* __restrict__ b, u64 kb, u64 c0, const u64* __restrict__ cv,
+                           i64 cv_len, int L, i64 n, u64 msk, int p0) {
+  const i64 total = (i64)L * n;
+  GRID_STRIDE(t, total) {
+    const i64 l = t / n;
+    const i64 i = t - l * n;
+    u64 v = a ? a[t] * ka : 0ull;
+    if (b) v += b[t] * kb;
+    if (l == p0) {
+      v += c0;
+      if (cv) v += cv[cv_len == n ? i : i % cv_len];
+    }
+    out[t] = v & msk;
+  }
+}
+
+extern "C" int mpx_ring_lin(uint64_t* out, const uint64_t* a, uint64_t ka, const uint64_t* b,
+                            uint64_t kb, uint64_t c0, const uint64_t* cv, int64_t cv_len, int L,
+                            int64_t n, int width, int p0, void* stream) {
+  CHECK_ARG(out && L >= 1 && n >= 0 && width >= 1 && width <= 64);
+  CHECK_ARG(!cv || cv_len >= 1);
+  if (n == 0) return MPX_OK;
+  k_ring_lin<<<grid_for((i64)L * n), MPX_THREADS, 0, (cudaStream_t)stream>>>(
+      out, a, ka, b, kb, c0, cv, cv_len, L, n, ring_mask(width), p0);
+  return launch_status();
+}
+
+__global__ void k_ring_mul(u64* __restrict__ out, const u64* __restrict__ a, const u64* __restrict__ b,
+                           i64 n, u64 msk) {
+  GRID_STRIDE(i, n) { out[i] = (a[i] * b[i]) & msk; }
+}
+
+extern "C" int mpx_ring_mul(uint64_t* out, const uint64_t* a, const uint64_t* b, int64_t n, int width,
+                            void* stream) {
+  CHECK_ARG(out && a && b && n >= 0 && width >= 1 && width <= 64);
+  if (n == 0) return MPX_OK;
+  k_ring_mul<<<grid_for(n), MPX_THREADS, 0, (cudaStream_t)stream>>>(out, a, b, n, ring_mask(width));
+  return launch_status();
+}
+
+// --------------------------------------------------------------------------
+// Row dot with public weights: one warp per row, lanes stride the row
+// (coalesced), u64 shuffle reduction. K12 (row sums) and compose contractions.
+
+__global__ void k_ring_rowdot(u64* __restrict__ out, const u64* __restrict__ x,
+                              const u64* __restrict__ wts, i64 nrows, i64 cols, u64 msk) {
+  const int lane = threadIdx.x & 31;
+  const i64 warp = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 r = warp; r < nrows; r += nwarps) {
+    const u64* row = x + r * cols;
+    u64 acc = 0;
+    for (i64 j = lane; j < cols; j += 32) acc += wts ? row[j] * wts[j] : row[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) out[r] = acc & msk;
+  }
+}
+
+// Short rows: one thread per row (cols <= 8 keeps the loads in a few sectors).
+__global__ void k_ring_rowdot_small(u64* __restrict__ out, const u64* __restrict__ x,
+                                    const u64* __restrict__ wts, i64 nrows, i64 cols, u64 msk) {
+  GRID_STRIDE(r, nrows) {
+    const u64* row = x + r * cols;
+    u64 acc = 0;
+    for (i64 j = 0; j < cols; ++j) acc += wts ? row[j] * wts[j] : row[j];
+    out[r] = acc & msk;
+  }
+}
+
+extern "C" int mpx_ring_rowdot(uint64_t* out, const uint64_t* x, const uint64_t* wts, int L,
+                               int64_t rows, int64_t cols, int width, void* stream) {
+  CHECK_ARG(out && x && L >= 1 && rows >= 0 && cols >= 1 && width >= 1 && width <= 64);
+  const i64 nrows = (i64)L * rows;
+  if (nrows == 0) return MPX_OK;
+  if (cols <= 8)
+    k_ring_rowdot_small<<<grid_for(nrows), MPX_THREADS, 0, (cudaStream_t)stream>>>(
+        out, x, wts, nrows, cols, ring_mask(width));
+  else
+    k_ring_rowdot<<<grid_for(nrows * 32), MPX_THREADS, 0, (cudaStream_t)stream>>>(
+        out, x, wts, nrows, cols, ring_mask(width));
+  return launch_status();
+}
+
+// --------------------------------------------------------------------------
+// Codec: floor(x * 2^f) as int64, two's complement into Z_2^w (ring.py:76-89)
+
+__global__ void k_encode(u64* __restrict__ out, const double* __restrict__ in, i64 n, double scale,
+                         u64 msk) {
+  GRID_STRIDE(i, n) {
+    const double s = floor(in[i] * scale);
+    out[i] = ((u64)(long long)s) & msk;
+  }
+}
+
+__global__ void k_decode(double* __restrict__ out, const u64* __restrict__ in, i64 n, int w,
+                         double inv_scale) {
+  GRID_STRIDE(i, n) {
+    u64 v = in[i] & ring_mask(w);
+    long long s;
+    if (w == 64) {
+      s = (long long)v;
+    } else {
+      const u64 sign = 1ull << (w - 1);
+      s = (v & sign) ? (long long)(v | ~ring_mask(w)) : (long long)v;
+    }
+    out[i] = (double)s * inv_scale;
+  }
+}
+
+extern "C" int mpx_encode(uint64_t* out, const double* in, int64_t n, int width, int frac,
+                          void* stream) {
+  CHECK_ARG(out && in && n >= 0 && width >= 1 && width <= 64 && frac >= 0 && frac < 64);
+  if (n == 0) return MPX_OK;
+  k_encode<<<grid_for(n), MPX_THREADS, 0, (cudaStream_t)stream>>>(out, in, n, ldexp(1.0, frac),
+                                                                   ring_mask(width));
+  return launch_status();
+}
+
+extern "C" int mpx_decode(double* out, const uint64_t* in, int64_t n, int width, int frac,
+                          void* stream) {
+  CHECK_ARG(out && in && n >= 0 && width >= 1 && width <= 64 && frac >= 0 && frac < 64);
+  if (n == 0) return MPX_OK;
+  k_decode<<<grid_for(n), MPX_THREADS, 0, (cudaStream_t)stream>>>(out, in, n, width,
+                                                                   ldexp(1.0, -frac));
+  return launch_status();
+}
+
+// --------------------------------------------------------------------------
+// Openings (session.py:87-115): reduce the local parties' contributions.
+
+__global__ void k_open_sum(u64* __restrict__ out, const u64* __restrict__ x, int L, i64 n, u64 msk) {
+  GRID_STRIDE(i, n) {
+    u64 s = 0;
+    for (int l = 0; l < L; ++l) s += x[(i64)l * n + i];
+    out[i] = s & msk;
+  }
+}
+
+__global__ void k_open_xor(u64* __restrict__ out, const u64* __restrict__ x, int L, i64 n) {
+  GRID_STRIDE(i, n) {
+    u64 s = 0;
+    for (int l = 0; l < L; ++l) s ^= x[(i64)l * n + i];
+    out[i] = s;
+  }
+}
+
+__global__ void k_mask_sub(u64* __restrict__ out, const u64* __restrict__ x, const u64* __restrict__ a,
+                           i64 a_ps, int L, i64 n, u64 msk) {
+  GRID_STRIDE(i, n) {
+    u64 s = 0;
+    for (int l = 0; l < L; ++l) s += x[(i64)l * n + i] - a[(i64)l * a_ps + i];
+    out[i] = s & msk;
+  }
+}
+
+extern "C" int mpx_open_sum(uint64_t* out, const uint64_t* x, int L, int64_t n, int width,
+                            void* stream) {
+  CHECK_ARG(out && x && L >= 1 && n >= 0 && width >= 1 && width <= 64);
+  if (n == 0) return MPX_OK;
+  k_open_sum<<<grid_for(n), MPX_THREADS, 0, (cudaStream_t)stream>>>(out, x, L, n, ring_mask(width));
+  return launch_status();
+}
+
+extern "C" int mpx_open_xor(uint64_t* out, const uint64_t* x, int L, int64_t n, void* stream) {
+  CHECK_ARG(out && x && L >= 1 && n >= 0);
+  if (n == 0) return MPX_OK;
+  k_open_xor<<<grid_for(n), MPX_THREADS, 0, (cudaStream_t)stream>>>(out, x, L, n);
+  return launch_status();
+}
+
+extern "C" int mpx_mask_sub(uint64_t* out, const uint64_t* x, const uint64_t* a, int64_t a_ps, int L,
+                            int64_t n, int width, void* stream) {
+  CHECK_ARG(out && x && a && L >= 1 && n >= 0 && width >= 1 && width <= 64);
+  if (n == 0) return MPX_OK;
+  k_mask_sub<<<grid_for(n), MPX_THREADS, 0, (cudaStream_t)stream>>>(out, x, a, a_ps, L, n,
+                                                                     ring_mask(width));
+  return launch_status();
+}
+
+// --------------------------------------------------------------------------
+// Local bit ops on row-packed words.
+
+__global__ void k_bits_op(u64* __restrict__ out, const u64* __restrict__ a, const u64* __restrict__ b,
+                          int op, int L, i64 rows, int m, int p0, int imm) {
+  const i64 total = (i64)L * rows;
+  const u64 mm = low_bits(m);
+  GRID_STRIDE(t, total) {
+    const i64 l = t / rows;
+    const i64 r = t - l * rows;
+    const u64 x = a[t];
+    u64 v;
+    switch (op) {
+      case MPX_BITS_XOR: v = x ^ b[t]; break;
+      case MPX_BITS_AND: v = x & b[t]; break;
+      case MPX_BITS_AND_PUB: v = x & b[r]; break;
+      case MPX_BITS_XOR_PUB: v = (l == p0) ? (x ^ b[r]) : x; break;
+      case MPX_BITS_XOR_SHR1: v = x ^ ((x & mm) >> 1); break;
+      case MPX_BITS_PARITY: v = (u64)(__popcll(x & mm) & 1); break;
+      case MPX_BITS_SIGNFOLD: v = (x & mm) ^ (((x >> m) & 1ull) ? mm : 0ull); break;
+      case MPX_BITS_SHL_OR: v = (x & low_bits(imm)) | (b[t] << imm); break;
+      case MPX_BITS_BCAST_PUB: v = (l == p0) ? (x ^ b[0]) : x; break;
+      default: v = 0; break;
+    }
+    out[t] = (op == MPX_BITS_SIGNFOLD || op == MPX_BITS_PARITY) ? v : (v & mm);
+  }
+}
+
+extern "C" int mpx_bits_op(uint64_t* out, const uint64_t* a, const uint64_t* b, int op, int L,
+                           int64_t rows, int m, int p0, int imm, void* stream) {
+  CHECK_ARG(out && a && L >= 1 && rows >= 0 && m >= 1 && m <= 64 && op >= 0 && op <= 8);
+  CHECK_ARG(b || op == MPX_BITS_XOR_SHR1 || op == MPX_BITS_PARITY || op == MPX_BITS_SIGNFOLD);
+  CHECK_ARG(op != MPX_BITS_SIGNFOLD || m < 64);
+  CHECK_ARG(op != MPX_BITS_SHL_OR || (imm >= 0 && imm < 64));
+  if (rows == 0) return MPX_OK;
+  k_bits_op<<<grid_for((i64)L * rows), MPX_THREADS, 0, (cudaStream_t)stream>>>(out, a, b, op, L, rows,
+                                                                                m, p0, imm);
+  return launch_status();
+}
+
+struct GatherSpec {
+  int8_t src[64];
+};
+
+__global__ void k_bits_gather(u64* __restrict__ out, const u64* __restrict__ in, GatherSpec g, int k,
+                              i64 n) {
+  GRID_STRIDE(i, n) {
+    const u64 x = in[i];
+    u64 v = 0;
+    for (int t = 0; t < k; ++t) {
+      const int s = g.src[t];
+      if (s >= 0) v |= ((x >> s) & 1ull) << t;
+    }
+    out[i] = v;
+  }
+}
+
+extern "C" int mpx_bits_gather(uint64_t* out, const uint64_t* in, const int8_t* src_host, int k,
+                               int64_t nwords, void* stream) {
+  CHECK_ARG(out && in && src_host && k >= 1 && k <= 64 && nwords >= 0);
+  GatherSpec g;
+  for (int t = 0; t < 64; ++t) g.src[t] = t < k ? src_host[t] : (int8_t)-1;
+  for (int t = 0; t < k; ++t) CHECK_ARG(g.src[t] < 64);
+  if (nwords == 0) return MPX_OK;
+  k_bits_gather<<<grid_for(nwords), MPX_THREADS, 0, (cudaStream_t)stream>>>(out, in, g, k, nwords);
+  return launch_status();
+}
+
+__global__ void k_bits_pack(u64* __restrict__ out, const uint8_t* __restrict__ in, i64 rows, int m) {
+  GRID_STRIDE(r, rows) {
+    const uint8_t* row = in + r * m;
+    u64 v = 0;
+    for (int j = 0; j < m; ++j) v |= (u64)(row[j] & 1u) << j;
+    out[r] = v;
+  }
+}
+
+__global__ void k_bits_unpack(uint8_t* __restrict__ out, const u64* __restrict__ in, i64 rows, int m) {
+  const i64 total = rows * m;
+  GRID_STRIDE(t, total) {
+    const i64 r = t / m;
+    const int j = (int)(t - r * m);
+    out[t] = (uint8_t)((in[r] >> j) & 1ull);
+  }
+}
+
+extern "C" int mpx_bits_pack(uint64_t* out, const uint8_t* in, int64_t rows, int m, void* stream) {
+  CHECK_ARG(out && in && rows >= 0 && m >= 1 && m <= 64);
+  if (rows == 0) return MPX_OK;
+  k_bits_pack<<<grid_for(rows), MPX_THREADS, 0, (cudaStream_t)stream>>>(out, in, rows, m);
+  return launch_status();
+}
+
+extern "C" int mpx_bits_unpack(uint8_t* out, const uint64_t* in, int64_t rows, int m, void* stream) {
+  CHECK_ARG(out && in && rows >= 0 && m >= 1 && m <= 64);
+  if (rows == 0) return MPX_OK;
+  k_bits_unpack<<<grid_for(rows * m), MPX_THREADS, 0, (cudaStream_t)stream>>>(out, in, rows, m);
+  return launch_status();
+}
+
+__global__ void k_bits_flat_to_rows(u64* __restrict__ out, const u64* __restrict__ flat, i64 flat_bit,
+                                    i64 rows, int m) {
+  GRID_STRIDE(r, rows) { out[r] = load_bits(flat, flat_bit + r * (i64)m, m); }
+}
+
+// One thread per output word of the flat stream: bit t = row t/m, bit t%m.
+__global__ void k_bits_rows_to_flat(u64* __restrict__ flat, const u64* __restrict__ rin, i64 rows,
+                                    int m) {
+  const i64 nbits = rows * m;
+  const i64 nw = (nbits + 63) >> 6;
+  GRID_STRIDE(w, nw) {
+    u64 v = 0;
+    const i64 t0 = w << 6;
+    i64 r = t0 / m;
+    int j = (int)(t0 - r * m);
+    for (int b = 0; b < 64 && t0 + b < nbits; ++b) {
+      v |= ((rin[r] >> j) & 1ull) << b;
+      if (++j == m) {
+        j = 0;
+        ++r;
+      }
+    }
+    flat[w] = v;
+  }
+}
+
+extern "C" int mpx_bits_flat_to_rows(uint64_t* out, const uint64_t* flat, int64_t flat_bit,
+                                     int64_t rows, int m, void* stream) {
+  CHECK_ARG(out && flat && flat_bit >= 0 && rows >= 0 && m >= 1 && m <= 64);
+  if (rows == 0) return MPX_OK;
+  k_bits_flat_to_rows<<<grid_for(rows), MPX_THREADS, 0, (cudaStream_t)stream>>>(out, flat, flat_bit,
+                                                                                 rows, m);
+  return launch_status();
+}
+
+extern "C" int mpx_bits_rows_to_flat(uint64_t* flat, const uint64_t* rows_in, int64_t rows, int m,
+                                     void* stream) {
+  CHECK_ARG(flat && rows_in && rows >= 0 && m >= 1 && m <= 64);
+  if (rows == 0) return MPX_OK;
+  const i64 nw = (rows * m + 63) >> 6;
+  k_bits_rows_to_flat<<<grid_for(nw), MPX_THREADS, 0, (cudaStream_t)stream>>>(flat, rows_in, rows, m);
+  return launch_status();
+}
+
+// --------------------------------------------------------------------------
+// Diagnostics
+
+extern "C" const char* mpx_version(void) { return "libmpx 0.1 sm_100a"; }
+
+extern "C" int mpx_last_cuda_error(void) { return (int)cudaGetLastError(); }
+
+extern "C" const char* mpx_cuda_error_string(int code) {
+  return cudaGetErrorString((cudaError_t)code);
+}
+
+extern "C" int mpx_device_sm_count(int device) {
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+  return v;
+}

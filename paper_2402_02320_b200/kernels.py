@@ -1,0 +1,296 @@
+"""Typed launch wrappers over the libmpx C ABI (one per entry point).
+
+Every wrapper takes torch int64 tensors (uint64 words) already laid out as
+include/mpx.h describes, skips the launch when its output is a ``meta``
+tensor (dry run), and raises ``MpxError`` on failure.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import call, ptr
+
+_M64 = (1 << 64) - 1
+
+
+def _u(v: int) -> int:
+    return int(v) & _M64
+
+
+def _dry(*ts) -> bool:
+    return _lib.is_dry(*ts)
+
+
+# ---- local ring ----------------------------------------------------------
+
+def ring_lin(out, a, ka, b, kb, c0, cv, L, n, width, p0):
+    if _dry(out):
+        return out
+    call("mpx_ring_lin", ptr(out), ptr(a), _u(ka), ptr(b), _u(kb), _u(c0), ptr(cv),
+         int(cv.numel()) if cv is not None else 0, L, n, width, p0)
+    return out
+
+
+def ring_mul(out, a, b, n, width):
+    if _dry(out):
+        return out
+    call("mpx_ring_mul", ptr(out), ptr(a), ptr(b), n, width)
+    return out
+
+
+def ring_rowdot(out, x, wts, L, rows, cols, width):
+    if _dry(out):
+        return out
+    call("mpx_ring_rowdot", ptr(out), ptr(x), ptr(wts), L, rows, cols, width)
+    return out
+
+
+def encode(out, x_f64, n, width, frac):
+    if _dry(out):
+        return out
+    call("mpx_encode", ptr(out), ptr(x_f64), n, width, frac)
+    return out
+
+
+def decode(out_f64, x, n, width, frac):
+    if _dry(out_f64):
+        return out_f64
+    call("mpx_decode", ptr(out_f64), ptr(x), n, width, frac)
+    return out_f64
+
+
+# ---- openings ------------------------------------------------------------
+
+def open_sum(out, x, L, n, width):
+    if _dry(out):
+        return out
+    call("mpx_open_sum", ptr(out), ptr(x), L, n, width)
+    return out
+
+
+def open_xor(out, x, L, n):
+    if _dry(out):
+        return out
+    call("mpx_open_xor", ptr(out), ptr(x), L, n)
+    return out
+
+
+def mask_sub(out, x, a_ptr, a_ps, L, n, width):
+    if _dry(out):
+        return out
+    call("mpx_mask_sub", ptr(out), ptr(x), a_ptr, a_ps, L, n, width)
+    return out
+
+
+# ---- Beaver arithmetic ----------------------------------------------------
+
+def mul_finish(z, d, e, a, b, c, t_ps, L, n, width, p0):
+    if _dry(z):
+        return z
+    call("mpx_mul_finish", ptr(z), ptr(d), ptr(e), a, b, c, t_ps, L, n, width, p0)
+    return z
+
+
+def mul_fused(z, x, y, a, b, c, t_ps, L, n, width, p0):
+    if _dry(z):
+        return z
+    call("mpx_mul_fused", ptr(z), ptr(x), ptr(y), a, b, c, t_ps, L, n, width, p0)
+    return z
+
+
+def trunc_mask(out, x, r_lo, lo_ps, r_hi, hi_ps, L, n, width, f, bias, p0):
+    if _dry(out):
+        return out
+    call("mpx_trunc_mask", ptr(out), ptr(x), r_lo, lo_ps, r_hi, hi_ps, L, n, width, f, _u(bias), p0)
+    return out
+
+
+def trunc_finish(z, c, r_hi, hi_ps, L, n, width, f, unbias, p0):
+    if _dry(z):
+        return z
+    call("mpx_trunc_finish", ptr(z), ptr(c), r_hi, hi_ps, L, n, width, f, _u(unbias), p0)
+    return z
+
+
+def trunc_fused(z, x, r_lo, lo_ps, r_hi, hi_ps, L, n, width, f, bias, unbias, p0):
+    if _dry(z):
+        return z
+    call("mpx_trunc_fused", ptr(z), ptr(x), r_lo, lo_ps, r_hi, hi_ps, L, n, width, f, _u(bias),
+         _u(unbias), p0)
+    return z
+
+
+# ---- binary circuits -------------------------------------------------------
+
+def and_mask(d, e, x, y, t, L, rows, m):
+    if _dry(d):
+        return
+    call("mpx_and_mask", ptr(d), ptr(e), ptr(x), ptr(y), t.a_ptr, t.b_ptr, t.ps, t.bit, L, rows, m)
+
+
+def and_finish(z, d, e, t, L, rows, m, p0):
+    if _dry(z):
+        return
+    call("mpx_and_finish", ptr(z), ptr(d), ptr(e), t.a_ptr, t.b_ptr, t.c_ptr, t.ps, t.bit, L, rows, m, p0)
+
+
+def carry_mask(dg, eg, dp, ep, G, P, t, L, rows, m, s, last):
+    if _dry(dg):
+        return
+    call("mpx_carry_mask", ptr(dg), ptr(eg), ptr(dp), ptr(ep), ptr(G), ptr(P), t.a_ptr, t.b_ptr, t.ps,
+         t.bit, L, rows, m, s, int(last))
+
+
+def carry_finish(G, P, dg, eg, dp, ep, t, L, rows, m, s, last, p0):
+    if _dry(G):
+        return
+    call("mpx_carry_finish", ptr(G), ptr(P), ptr(dg), ptr(eg), ptr(dp), ptr(ep), t.a_ptr, t.b_ptr,
+         t.c_ptr, t.ps, t.bit, L, rows, m, s, int(last), p0)
+
+
+def carry_fused(G, P, t, L, rows, m, s, last, p0):
+    if _dry(G):
+        return
+    call("mpx_carry_fused", ptr(G), ptr(P), t.a_ptr, t.b_ptr, t.c_ptr, t.ps, t.bit, L, rows, m, s,
+         int(last), p0)
+
+
+def pubadd_init(G, P, P0, pub, x, xb_ptr, xb_ps, xb_bit, L, rows, m, p0):
+    if _dry(G):
+        return
+    call("mpx_pubadd_init", ptr(G), ptr(P), ptr(P0), ptr(pub), ptr(x), xb_ptr, xb_ps, xb_bit, L, rows,
+         m, p0)
+
+
+def sum_from_carries(out, P0, G, L, rows, m):
+    if _dry(out):
+        return out
+    call("mpx_sum_from_carries", ptr(out), ptr(P0), ptr(G), L, rows, m)
+    return out
+
+
+def lmo_mask(d, e, Y, t, L, rows, m, s):
+    if _dry(d):
+        return
+    call("mpx_lmo_mask", ptr(d), ptr(e), ptr(Y), t.a_ptr, t.b_ptr, t.ps, t.bit, L, rows, m, s)
+
+
+def lmo_finish(Y, d, e, t, L, rows, m, s, p0):
+    if _dry(Y):
+        return
+    call("mpx_lmo_finish", ptr(Y), ptr(d), ptr(e), t.a_ptr, t.b_ptr, t.c_ptr, t.ps, t.bit, L, rows, m, s,
+         p0)
+
+
+def lmo_fused(Y, t, L, rows, m, s, p0):
+    if _dry(Y):
+        return
+    call("mpx_lmo_fused", ptr(Y), t.a_ptr, t.b_ptr, t.c_ptr, t.ps, t.bit, L, rows, m, s, p0)
+
+
+def bit2a_mask(c, b, rb_ptr, rb_ps, rb_bit, L, rows, m):
+    if _dry(c):
+        return c
+    call("mpx_bit2a_mask", ptr(c), ptr(b), rb_ptr, rb_ps, rb_bit, L, rows, m)
+    return c
+
+
+def bit2a_finish(out, c, ra_ptr, ra_ps, L, rows, m, width, p0, wts=None, mode=0):
+    if _dry(out):
+        return out
+    call("mpx_bit2a_finish", ptr(out), ptr(c), ra_ptr, ra_ps, L, rows, m, width, p0, ptr(wts), mode)
+    return out
+
+
+def bits_op(out, a, b, op, L, rows, m, p0=-1, imm=0):
+    if _dry(out):
+        return out
+    call("mpx_bits_op", ptr(out), ptr(a), ptr(b), op, L, rows, m, p0, imm)
+    return out
+
+
+def bits_gather(out, x, src, nwords):
+    if _dry(out):
+        return out
+    k = len(src)
+    arr = (ctypes.c_int8 * 64)(*([int(s) for s in src] + [-1] * (64 - k)))
+    call("mpx_bits_gather", ptr(out), ptr(x), ctypes.cast(arr, ctypes.c_void_p), k, nwords)
+    return out
+
+
+def bits_pack(out, x_u8, rows, m):
+    if _dry(out):
+        return out
+    call("mpx_bits_pack", ptr(out), ptr(x_u8), rows, m)
+    return out
+
+
+def bits_unpack(out_u8, x, rows, m):
+    if _dry(out_u8):
+        return out_u8
+    call("mpx_bits_unpack", ptr(out_u8), ptr(x), rows, m)
+    return out_u8
+
+
+def bits_flat_to_rows(out, flat_ptr, flat_bit, rows, m):
+    if _dry(out):
+        return out
+    call("mpx_bits_flat_to_rows", ptr(out), flat_ptr, flat_bit, rows, m)
+    return out
+
+
+def bits_rows_to_flat(flat, rows_in, rows, m):
+    if _dry(flat):
+        return flat
+    call("mpx_bits_rows_to_flat", ptr(flat), ptr(rows_in), rows, m)
+    return flat
+
+
+# ---- GEMM -------------------------------------------------------------------
+
+def gemm(C, A, B, batch, M, K, N, sA, sB, sC, accumulate, width, simt=False):
+    if _dry(C):
+        return C
+    call("mpx_gemm_simt" if simt else "mpx_gemm", ptr(C), A if isinstance(A, int) else ptr(A),
+         B if isinstance(B, int) else ptr(B), batch, M, K, N, sA, sB, sC, int(accumulate), width)
+    return C
+
+
+# ---- dealer -----------------------------------------------------------------
+
+def philox_elems(out, key, u32_off, count, width):
+    if _dry(out):
+        return out
+    call("mpx_philox_elems", ptr(out), _u(key[0]), _u(key[1]), u32_off, count, width)
+    return out
+
+
+def philox_bits(out, key, u32_off, count):
+    if _dry(out):
+        return out
+    call("mpx_philox_bits", ptr(out), _u(key[0]), _u(key[1]), u32_off, count)
+    return out
+
+
+def deal_share_arith(out, secret, key, u32_base, count, n, p_lo, L, width):
+    if _dry(out):
+        return out
+    call("mpx_deal_share_arith", ptr(out), out.stride(0), ptr(secret), _u(key[0]), _u(key[1]), u32_base,
+         count, n, p_lo, L, width)
+    return out
+
+
+def deal_share_bits(out, secret, key, u32_base, count, n, p_lo, L):
+    if _dry(out):
+        return out
+    call("mpx_deal_share_bits", ptr(out), out.stride(0), ptr(secret), _u(key[0]), _u(key[1]), u32_base,
+         count, n, p_lo, L)
+    return out
+
+
+def empty(shape, like: torch.Tensor):
+    return torch.empty(shape, dtype=torch.int64, device=like.device)

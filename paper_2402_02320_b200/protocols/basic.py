@@ -1,0 +1,232 @@
+"""Core interactive protocols (reference: protocols/basic.py:1-239).
+
+Same names, argument meaning, round counts, material consumption order and
+ledger entries as the reference; every local step runs in a libmpx kernel.
+In sim mode (``session.fused``) a round's mask, opening and finish collapse
+into one kernel; in party mode the mask kernel's partial goes through an
+NCCL collective before the finish kernel.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .. import _lib
+from .. import kernels as K
+from ..ring import bits_of_np, encode, encode_scalar
+from ..sharing import AShare, BShare, add_public, public_bits_words
+from ..session import arith_payload, bits_payload
+
+
+def _check_same(x, y):
+    if x.shape != y.shape:
+        raise ValueError(f"shape mismatch {x.shape} vs {y.shape}")
+
+
+def mul(session, x: AShare, y: AShare) -> AShare:
+    """Element-wise Beaver product, one triple per element (basic.py:27-42)."""
+    _check_same(x, y)
+    if x.width != y.width:
+        raise ValueError(f"width mismatch {x.width} vs {y.width}")
+    w, n, L = x.width, x.size, session.L
+    a, b, c = session.store.take_triples(w, n)
+    z = session.alloc((L,) + x.shape)
+    if session.fused:
+        K.mul_fused(z, x.values, y.values, a.ptr, b.ptr, c.ptr, a.ps, L, n, w, session.p0)
+        session.exchange(payload=2 * arith_payload(w, n))
+    else:
+        d, e = session.alloc((n,)), session.alloc((n,))
+        K.mask_sub(d, x.values, a.ptr, a.ps, L, n, w)
+        K.mask_sub(e, y.values, b.ptr, b.ps, L, n, w)
+        d, e = session.exchange(arith=[(d, w), (e, w)])
+        K.mul_finish(z, d, e, a.ptr, b.ptr, c.ptr, a.ps, L, n, w, session.p0)
+    session.metrics.count(mul_count=1, mul_elems=n)
+    return AShare(z, w, x.frac + y.frac, session.parties)
+
+
+def matmul(session, x: AShare, y: AShare) -> AShare:
+    return batch_matmul(session, [(x, y)])[0]
+
+
+def batch_matmul(session, pairs) -> list[AShare]:
+    """Independent matrix products in one round, one matrix triple each (basic.py:45-79).
+
+    Z_l = C_l + D @ B_l + A_l @ E + [l==p0] D @ E, on the Z_2^64 GEMM kernel.
+    """
+    L = session.L
+    trip, masked = [], []
+    for x, y in pairs:
+        if len(x.shape) != 2 or len(y.shape) != 2 or x.shape[1] != y.shape[0]:
+            raise ValueError(f"bad matmul shapes {x.shape} @ {y.shape}")
+        w = x.width
+        m, k = x.shape
+        r = y.shape[1]
+        A, B, C = session.store.take_matrix_triple(w, m, k, r)
+        D, E = session.alloc((m * k,)), session.alloc((k * r,))
+        K.mask_sub(D, x.values, A.data_ptr(), A.stride(0), L, m * k, w)
+        K.mask_sub(E, y.values, B.data_ptr(), B.stride(0), L, k * r, w)
+        trip.append((A, B, C))
+        masked += [(D, w), (E, w)]
+    opened = session.exchange(arith=masked)
+    out = []
+    for i, (x, y) in enumerate(pairs):
+        w = x.width
+        m, k = x.shape
+        r = y.shape[1]
+        A, B, C = trip[i]
+        D, E = opened[2 * i], opened[2 * i + 1]
+        Z = session.alloc((L, m, r))
+        if not session.dry:
+            Z.copy_(C)
+        K.gemm(Z, D, B.data_ptr(), L, m, k, r, 0, B.stride(0), m * r, True, w)
+        K.gemm(Z, A.data_ptr(), E, L, m, k, r, A.stride(0), 0, m * r, True, w)
+        if session.p0 >= 0:
+            K.gemm(Z[session.p0], D, E, 1, m, k, r, 0, 0, 0, True, w)
+        session.metrics.count(matmul_count=1, matmul_macs=m * k * r)
+        out.append(AShare(Z, w, x.frac + y.frac, session.parties))
+    return out
+
+
+def and_gate(session, x: BShare, y: BShare) -> BShare:
+    """Bitwise AND, one binary triple per bit (basic.py:82-95)."""
+    _check_same(x, y)
+    y = y.like_layout(x)
+    L, rows, m = session.L, x.rows, x.m
+    t = session.store.take_bin_triples(x.size)
+    d, e = session.alloc((rows,)), session.alloc((rows,))
+    K.and_mask(d, e, x.words, y.words, t, L, rows, m)
+    d, e = session.exchange(bits=[d, e], payload=2 * bits_payload(x.size))
+    z = session.alloc(x.words.shape)
+    K.and_finish(z, d, e, t, L, rows, m, session.p0)
+    session.metrics.count(and_count=1, and_elems=x.size)
+    return x._new(z)
+
+
+def _carry_prefix(session, G: torch.Tensor, P: torch.Tensor, m: int, rows: int) -> None:
+    """Kogge-Stone carries over the m-bit rows of G, P in place (basic.py:98-129).
+
+    One AND round per level; level s consumes rows*2(m-s) bintriples laid
+    out [G-part | P-part] per row (rows*(m-s) on the final level).
+    """
+    L = session.L
+    s = 1
+    while s < m:
+        last = 2 * s >= m
+        W = m - s
+        cnt = rows * (W if last else 2 * W)
+        t = session.store.take_bin_triples(cnt)
+        if session.fused:
+            K.carry_fused(G, P, t, L, rows, m, s, last, session.p0)
+            session.exchange(payload=2 * bits_payload(cnt))
+        else:
+            dg, eg = session.alloc((rows,)), session.alloc((rows,))
+            dp = None if last else session.alloc((rows,))
+            ep = None if last else session.alloc((rows,))
+            K.carry_mask(dg, eg, dp, ep, G, P, t, L, rows, m, s, last)
+            parts = [dg, eg] if last else [dg, eg, dp, ep]
+            got = session.exchange(bits=parts, payload=2 * bits_payload(cnt))
+            if last:
+                dg, eg = got
+            else:
+                dg, eg, dp, ep = got
+            K.carry_finish(G, P, dg, eg, dp, ep, t, L, rows, m, s, last, session.p0)
+        session.metrics.count(and_count=1, and_elems=cnt)
+        s *= 2
+
+
+def _sum_bits(session, P0, G, m, rows, like: BShare) -> BShare:
+    out = session.alloc(P0.shape)
+    K.sum_from_carries(out, P0, G, session.L, rows, m)
+    return BShare(out, m, True, session.parties)
+
+
+def public_add_bits(session, pub_bits, x: BShare) -> BShare:
+    """Bits of (public + shared) mod 2^m; the generate layer is local (basic.py:139-152)."""
+    if isinstance(pub_bits, torch.Tensor) and pub_bits.dtype == torch.int64:
+        pub = pub_bits      # already row words
+    else:
+        pub = public_bits_words(pub_bits, x)
+    x = x.as_rows()
+    L, rows, m = session.L, x.rows, x.m
+    G, P, P0 = (session.alloc(x.words.shape) for _ in range(3))
+    K.pubadd_init(G, P, P0, pub, x.words, None, 0, 0, L, rows, m, session.p0)
+    _carry_prefix(session, G, P, m, rows)
+    return _sum_bits(session, P0, G, m, rows, x)
+
+
+def binary_add(session, x: BShare, y: BShare) -> BShare:
+    """Bits of (x + y) mod 2^m for two shared values (basic.py:155-161)."""
+    g = and_gate(session, x.as_rows(), y.as_rows())
+    p = x.as_rows() ^ y.as_rows()
+    P0 = p.words
+    P = P0.clone()
+    G = g.words.clone()
+    _carry_prefix(session, G, P, p.m, p.rows)
+    return _sum_bits(session, P0, G, p.m, p.rows, p)
+
+
+def _bit2a_round(session, b: BShare, width: int):
+    L, rows, m = session.L, b.rows, b.m
+    r_a, r_b = session.store.take_dabits(width, b.size)
+    c = session.alloc((rows,))
+    K.bit2a_mask(c, b.words, r_b.ptr, r_b.ps, r_b.bit, L, rows, m)
+    (c,) = session.exchange(bits=[c], payload=bits_payload(b.size))
+    session.metrics.count(bit2a_elems=b.size)
+    return c, r_a
+
+
+def bit2a(session, b: BShare, width: int) -> AShare:
+    """XOR-shared bits -> additive shares in Z_2^width via daBits (basic.py:164-184)."""
+    c, r_a = _bit2a_round(session, b, width)
+    out = session.alloc((session.L,) + b.shape)
+    K.bit2a_finish(out, c, r_a.ptr, r_a.ps, session.L, b.rows, b.m, width, session.p0, None, 0)
+    return AShare(out, width, 0, session.parties)
+
+
+def compose(session, bits: BShare, width: int, frac: int = 0) -> AShare:
+    """sum_i 2^i * bit_i over the trailing axis, one round (basic.py:187-196).
+
+    The per-bit conversions are reduced inside the finish kernel (no
+    intermediate (..., m) tensor)."""
+    bits = bits.as_rows()
+    c, r_a = _bit2a_round(session, bits, width)
+    out = session.alloc((session.L,) + bits.rows_shape)
+    K.bit2a_finish(out, c, r_a.ptr, r_a.ps, session.L, bits.rows, bits.m, width, session.p0, None, 1)
+    return AShare(out, width, frac, session.parties)
+
+
+def decompose(session, x: AShare) -> BShare:
+    """Bit decomposition (trailing axis of x.width bits) via a full-width edaBit
+    (basic.py:199-214): open x - r, then add the public difference onto the
+    shared bits of r with the carry tree."""
+    w, n, L = x.width, x.size, session.L
+    r_a, r_b = session.store.take_edabits(w, w, n)
+    c = session.alloc((n,))
+    K.mask_sub(c, x.values, r_a.ptr, r_a.ps, L, n, w)
+    (c,) = session.exchange(arith=[(c, w)])
+    G, P, P0 = (session.alloc((L,) + x.shape) for _ in range(3))
+    K.pubadd_init(G, P, P0, c, None, r_b.ptr, r_b.ps, r_b.bit, L, n, w, session.p0)
+    _carry_prefix(session, G, P, w, n)
+    return _sum_bits(session, P0, G, w, n, None)
+
+
+def gt(session, x: AShare, y: AShare) -> BShare:
+    """Strict x > y: sign bit of y - x (basic.py:217-225)."""
+    diff = y - x
+    return decompose(session, diff)[..., diff.width - 1]
+
+
+def const_share(session, value, width: int, frac: int, shape=()) -> AShare:
+    """Fixed-point public constant as a degenerate sharing (basic.py:228-233)."""
+    shape = tuple(shape)
+    enc = encode(np.broadcast_to(np.asarray(value, np.float64), shape), width, frac, session.device)
+    vals = session.alloc((session.L,) + shape)
+    K.ring_lin(vals, None, 0, None, 0, 0, enc.reshape(-1) if enc.numel() else None,
+               session.L, max(1, int(np.prod(shape))) if shape else 1, width, session.p0)
+    return AShare(vals, width, frac, session.parties)
+
+
+def add_const(session, x: AShare, value: float) -> AShare:
+    """Add a public fixed-point constant at party 0 (basic.py:236-239)."""
+    return add_public(x, encode_scalar(value, x.width, x.frac))
