@@ -1,0 +1,463 @@
+#!/usr/bin/env python
+"""Benchmark: secure fixed-point Reciprocal (paper Alg. 1) on 2^24 elements,
+the BASELINE.json cfg-5 party-scaling workload, on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+* N = 1: the 1-GPU all-parties-simulated run (2 parties on cuda:0).
+* N > 1 (torchrun, one rank per GPU): one party per GPU, openings over NCCL.
+* ``--impl reference``: the reference algorithm's CPU implementation (the
+  numpy oracle port under ``oracle/``; the Python reference itself cannot
+  travel to the GPU box) on the host cores, same metric, bounded sample.
+
+A step = one online-phase secure reciprocal over the whole batch. The trusted
+dealer (on-device Philox, bit-exact with the reference's numpy dealer) deals
+fresh single-use material before every step, outside the timed region, and
+is reported separately (the reference and the paper time the online phase).
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import math
+import multiprocessing as mp
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "secure Reciprocal throughput, online phase (cfg5 party-scaling sweep)"
+UNIT = "elements/s"
+SEED = 7
+FRAC = 23
+WIDTH = 64
+
+
+def label_key(label: str):
+    """scenarios.py:48-51: Philox key = sha256(f"{seed}:{label}")[:16] as two LE u64."""
+    tag = hashlib.sha256(f"{SEED}:{label}".encode()).digest()
+    return [int.from_bytes(tag[:8], "little"), int.from_bytes(tag[8:16], "little")]
+
+
+def workload_inputs(n_elems: int) -> np.ndarray:
+    """x = +-2^U(-8, 8), random sign (SURVEY §8d cfg 5), deterministic."""
+    rng = np.random.default_rng(20240202)
+    mags = np.exp2(rng.uniform(-8.0, 8.0, n_elems))
+    return mags * rng.choice(np.array([-1.0, 1.0]), n_elems)
+
+
+def encode_np(x, width=WIDTH, frac=FRAC):
+    s = np.floor(np.asarray(x, dtype=np.float64) * float(1 << frac)).astype(np.int64)
+    return s.view(np.uint64)
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm / cpu_baseline: the oracle port, one process per core
+
+
+def _cpu_worker(args):
+    chunk, n_parties, seed = args
+    import oracle as O
+    xs = workload_inputs(chunk)
+    enc = encode_np(xs)
+
+    def fn(s):
+        x = O.AShare(O.deal_inputs_arith(enc, n_parties, WIDTH, label_key("share:x")), WIDTH, FRAC)
+        return O.reciprocal(s, x)
+
+    dry = O.Sim(n_parties, O.Demand(n_parties))
+    fn(dry)
+    live = O.Sim(n_parties, O.Store(seed, n_parties, dry.store.demands))
+    x = O.AShare(O.deal_inputs_arith(enc, n_parties, WIDTH, label_key("share:x")), WIDTH, FRAC)
+    t0 = time.perf_counter()
+    O.reciprocal(live, x)
+    return time.perf_counter() - t0
+
+
+def cpu_reference(sample: int, n_parties: int, cores: int | None = None, reps: int = 1):
+    """Online reciprocal on `sample` elements split over all host cores.
+    Returns (elements/s, cores, seconds)."""
+    cores = cores or os.cpu_count() or 1
+    chunk = max(1024, sample // cores)
+    tasks = [(chunk, n_parties, 11 + i) for i in range(cores)]
+    ctx = mp.get_context("fork")
+    best = None
+    with ctx.Pool(cores) as pool:
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            times = pool.map(_cpu_worker, tasks)
+            wall = time.perf_counter() - t0
+            online = max(times)  # all workers run concurrently; slowest bounds
+            rate = chunk * cores / online
+            best = rate if best is None else max(best, rate)
+    return best, cores, online
+
+
+# ---------------------------------------------------------------------------
+# clocks
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.fh.close()
+        sms, maxes, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sms.append(float(parts[1]))
+                maxes.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": float(np.median(sms)) if sms else None,
+                "sm_max_mhz": max(maxes) if maxes else None,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes per launch (what the kernel must move)
+
+
+def alg_bytes(name, a):
+    L = None
+    try:
+        if name == "mpx_carry_fused":
+            L, rows, m, s, last = a[7], a[8], a[9], a[10], a[11]
+            W = m - s
+            rw = W if last else 2 * W
+            return L * rows * (16 + (8 if last else 16)) + 3 * L * rows * rw // 8
+        if name == "mpx_lmo_fused":
+            L, rows, m, s = a[6], a[7], a[8], a[9]
+            return L * rows * 16 + 3 * L * rows * (m - s) // 8
+        if name == "mpx_mul_fused":
+            L, n = a[7], a[8]
+            return 6 * L * n * 8
+        if name == "mpx_trunc_fused":
+            L, n = a[6], a[7]
+            return (3 + (1 if a[4] else 0)) * L * n * 8
+        if name == "mpx_bit2a_mask":
+            L, rows, m = a[5], a[6], a[7]
+            return L * rows * 8 + L * rows * m // 8 + rows * 8
+        if name == "mpx_bit2a_finish":
+            L, rows, m, mode = a[4], a[5], a[6], a[10]
+            return rows * 8 + L * rows * m * 8 + (L * rows * m * 8 if mode == 0 else L * rows * 8)
+        if name == "mpx_mask_sub":
+            L, n = a[4], a[5]
+            return 2 * L * n * 8 + n * 8
+        if name == "mpx_pubadd_init":
+            L, rows, m = a[8], a[9], a[10]
+            return rows * 8 + L * rows * m // 8 + 3 * L * rows * 8
+        if name == "mpx_sum_from_carries":
+            L, rows = a[3], a[4]
+            return 3 * L * rows * 8
+        if name == "mpx_ring_lin":
+            L, n = a[8], a[9]
+            return ((1 if a[1] else 0) + (1 if a[3] else 0) + 1) * L * n * 8
+        if name == "mpx_bits_op":
+            L, rows = a[4], a[5]
+            return (2 + (1 if a[2] else 0)) * L * rows * 8
+        if name == "mpx_ring_rowdot":
+            L, rows, cols = a[3], a[4], a[5]
+            return L * rows * cols * 8 + L * rows * 8
+        if name == "mpx_bits_gather":
+            return 16 * a[4]
+    except (IndexError, TypeError):
+        return None
+    return None
+
+
+def _read_peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2402_02320_b200 as G
+    from paper_2402_02320_b200 import _lib
+    from paper_2402_02320_b200.preprocessing import DemandCounter, device_store
+    from paper_2402_02320_b200.session import PartySession, SimSession
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        # before CUDA initialisation: the pool forks numpy-only workers
+        rate, cores, secs = cpu_reference(args.cpu_sample, 2)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"oracle/ numpy port of the reference, online reciprocal on {args.cpu_sample} "
+                         f"elements (n=2) split over {cores} processes, slowest {secs:.2f} s"}
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n_parties = 2 if world == 1 else world
+    parties = tuple(range(n_parties)) if world == 1 else (rank,)
+    N = args.elems
+    xs = workload_inputs(N)
+    enc = encode_np(xs)
+    key = label_key("share:x")
+
+    def make_session(store):
+        if world == 1:
+            return SimSession(n_parties, store, device=dev)
+        return PartySession(rank, n_parties, None, store, device=dev)
+
+    # dry run (meta tensors): exact demand
+    counter = DemandCounter(parties, n_parties)
+    s_dry = make_session(counter)
+    G.reciprocal(s_dry, s_dry.share_ring(enc, WIDTH, FRAC, key))
+
+    def deal(step):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        st = device_store(1000 + step, n_parties, counter.demands, parties=parties, device=dev,
+                          needs_bits=counter.needs_bits)
+        torch.cuda.synchronize()
+        return st, time.perf_counter() - t0
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # input shares (device) + pinned host copies for the e2e leg
+    s0 = make_session(None)
+    x_sh = s0.share_ring(enc, WIDTH, FRAC, key)
+    torch.cuda.synchronize()
+    x_host = x_sh.values.cpu().pin_memory()
+
+    online_ms, dealer_s = [], []
+    clocks = ClockSampler(local)
+    store = None
+    launches_timed = 0
+    for step in range(args.warmup + args.steps):
+        del store
+        store, dt = deal(step)
+        dealer_s.append(dt)
+        sess = make_session(store)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        torch.cuda.synchronize()
+        timed = step >= args.warmup
+        if timed and step == args.warmup:
+            clocks.start()
+        l0 = _lib.LAUNCHES
+        ev0.record()
+        y = G.reciprocal(sess, x_sh)
+        ev1.record()
+        torch.cuda.synchronize()
+        barrier()
+        if timed:
+            online_ms.append(ev0.elapsed_time(ev1))
+            launches_timed += _lib.LAUNCHES - l0
+    clk = clocks.stop()
+    total_ms = float(sum(online_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = N * args.steps / (total_ms / 1e3)
+
+    # correctness spot check on the last step (opened vs float reference)
+    y_open = sess.open_fixed(y)
+    xq = encode_np(xs).view(np.int64) / float(1 << FRAC)
+    rel = float(np.max(np.abs(y_open - 1 / xq) * np.abs(xq)))
+
+    # profiled pass: per-kernel CUDA-event times over one more online step
+    del store
+    store, _ = deal(10_000)
+    sess = make_session(store)
+    torch.cuda.synchronize()
+    _lib.PROFILE = []
+    G.reciprocal(sess, x_sh)
+    torch.cuda.synchronize()
+    prof = _lib.PROFILE
+    _lib.PROFILE = None
+    per = {}
+    for name, a, e0, e1 in prof:
+        d = per.setdefault(name, {"ms": 0.0, "n": 0, "bytes": 0, "bytes_known": True})
+        d["ms"] += e0.elapsed_time(e1)
+        d["n"] += 1
+        b = alg_bytes(name, a)
+        if b is None:
+            d["bytes_known"] = False
+        else:
+            d["bytes"] += b
+    step_ms = sum(d["ms"] for d in per.values())
+    dom_name = max(per, key=lambda k: per[k]["ms"])
+    dom = per[dom_name]
+    peak, peak_kind = _read_peaks()
+    achieved = dom["bytes"] / (dom["ms"] / 1e3) / 1e9 if dom["bytes_known"] else None
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom_name)
+        except ValueError:
+            traffic = None
+    roofline = {"kernel": dom_name, "bound": "hbm", "achieved": achieved, "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None,
+                "traffic": traffic, "launches": dom["n"],
+                "avg_launch_us": 1e3 * dom["ms"] / dom["n"],
+                "alg_bytes_per_launch": dom["bytes"] // dom["n"],
+                "share_of_step": dom["ms"] / step_ms}
+    all_bytes = sum(d["bytes"] for d in per.values() if d["bytes_known"])
+    kernels = {k: {"ms": round(v["ms"], 3), "launches": v["n"],
+                   "GBps": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1) if v["bytes_known"] and v["ms"] else None}
+               for k, v in sorted(per.items(), key=lambda kv: -kv[1]["ms"])}
+
+    # e2e through the public API with host buffers: H2D shares -> reciprocal -> D2H
+    e2e_ms = []
+    store = None
+    for step in range(args.warmup + args.steps):
+        del store
+        store, _ = deal(20_000 + step)
+        sess = make_session(store)
+        barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        xv = x_host.to(dev, non_blocking=True)
+        yy = G.reciprocal(sess, G.AShare(xv, WIDTH, FRAC, parties))
+        y_host = yy.values.to("cpu")
+        ev1.record()
+        torch.cuda.synchronize()
+        barrier()
+        if step >= args.warmup:
+            e2e_ms.append(ev0.elapsed_time(ev1))
+    e2e_total = float(sum(e2e_ms))
+    if world > 1:
+        t = torch.tensor([e2e_total], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    h2d = int(x_host.numel() * 8)
+    d2h = int(y_host.numel() * 8)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64 (Z_2^64 ring)",
+            "data": "synthetic x = +-2^U(-8,8), fixed seed",
+            "config": {"workload": "cfg5 party-scaling sweep: secure Reciprocal (Alg. 1) on 2^24 elements",
+                       "elements": N, "ring_width": WIDTH, "frac": FRAC, "parties": n_parties,
+                       "mode": "sim: all parties on 1 GPU" if world == 1 else "one party per GPU, NCCL",
+                       "rounds_per_step": 37,
+                       "l2": "no flush needed: shares + dealer material ~40 GB per step >> 126 MB L2",
+                       "dealer": "fresh on-device material before every step, outside the timed region"},
+            "e2e": {"value": N * args.steps / (e2e_total / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_total / args.steps},
+            "gpu_launches": launches_timed,
+            "clocks": clk,
+            "roofline": roofline,
+            "alg_bytes_per_step": all_bytes,
+            "step_hbm_GBps": all_bytes / (step_ms / 1e3) / 1e9,
+            "dealer_ms_per_step": 1e3 * float(np.mean(dealer_s)),
+            "max_rel_err": rel,
+            "kernels": kernels,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n_parties = 2 if world == 1 else world
+    rates = []
+    cores = None
+    for step in range(args.warmup + args.steps):
+        rate, cores, secs = cpu_reference(args.cpu_sample, n_parties)
+        if step >= args.warmup:
+            rates.append(rate)
+    value = float(np.mean(rates))
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * (1 << 24) / value, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64 (Z_2^64 ring)", "impl": "reference",
+            "data": "synthetic x = +-2^U(-8,8), fixed seed",
+            "config": {"workload": "cfg5 party-scaling sweep: secure Reciprocal (Alg. 1) on 2^24 elements",
+                       "elements": 1 << 24, "ring_width": WIDTH, "frac": FRAC, "parties": n_parties,
+                       "mode": "CPU: reference algorithm (numpy oracle port), all host cores"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{args.cpu_sample} elements per step (bounded sample of the 2^24 "
+                                       f"workload), online phase, n={n_parties}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--elems", type=int, default=1 << 24)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 20)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -116,10 +116,26 @@ def ptr(t) -> int | None:
     return t.data_ptr()
 
 
+# Launch accounting for the benchmark harness: LAUNCHES counts libmpx entry
+# calls; when PROFILE is a list, each call is bracketed by CUDA events.
+LAUNCHES = 0
+PROFILE = None
+
+
 def call(name: str, *args) -> None:
     """Invoke one libmpx entry point; raise MpxError on a non-zero return."""
+    global LAUNCHES
     lib = load()
-    rc = getattr(lib, name)(*args, stream_ptr())
+    LAUNCHES += 1
+    if PROFILE is not None:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        rc = getattr(lib, name)(*args, stream_ptr())
+        ev1.record()
+        PROFILE.append((name, args, ev0, ev1))
+    else:
+        rc = getattr(lib, name)(*args, stream_ptr())
     if rc != 0:
         if rc == -2:
             code = lib.mpx_last_cuda_error()
