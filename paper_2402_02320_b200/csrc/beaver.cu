@@ -610,29 +610,53 @@ __global__ void k_bit2a_expand(u64* __restrict__ out, const u64* __restrict__ c,
   }
 }
 
-// mode 1: one warp per (l, r) row, lanes over j, weighted u64 reduction.
-__global__ void k_bit2a_compose(u64* __restrict__ out, const u64* __restrict__ c,
-                                const u64* __restrict__ ra, i64 ra_ps, int L, i64 rows, int m, u64 msk,
-                                int p0, const u64* __restrict__ wts) {
-  const int lane = threadIdx.x & 31;
-  const i64 warp = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
-  const i64 total = (i64)L * rows;
-  for (i64 t = warp; t < total; t += nwarps) {
-    const i64 l = t / rows;
-    const i64 r = t - l * rows;
-    const u64 cw = c[r];
-    const u64* row = ra + l * ra_ps + r * (i64)m;
-    u64 acc = 0;
-    for (int j = lane; j < m; j += 32) {
-      const u64 cj = (cw >> j) & 1ull;
-      u64 v = row[j] * (1ull - 2ull * cj);
-      if (l == p0) v += cj;
-      acc += (v & msk) * (wts ? wts[j] : (1ull << j));
+// mode 1 (compose): rows tiled through shared memory. A block stages the
+// contiguous r_arith slab of B2A_ROWS rows (coalesced 16-byte loads), then 4
+// threads per row reduce the weighted conversions with two shuffles.
+#define B2A_ROWS 64
+__global__ void __launch_bounds__(256) k_bit2a_compose(u64* __restrict__ out, const u64* __restrict__ c,
+                                                       const u64* __restrict__ ra, i64 ra_ps, int L,
+                                                       i64 rows, int m, u64 msk, int p0,
+                                                       const u64* __restrict__ wts) {
+  __shared__ __align__(16) u64 slab[B2A_ROWS * 64];
+  __shared__ u64 wsh[64];
+  if (threadIdx.x < 64) wsh[threadIdx.x] = wts ? (threadIdx.x < m ? wts[threadIdx.x] : 0ull)
+                                               : (threadIdx.x < 64 ? (1ull << threadIdx.x) : 0ull);
+  const i64 tiles = (rows + B2A_ROWS - 1) / B2A_ROWS;
+  const i64 total = (i64)L * tiles;
+  const int sub = threadIdx.x & 3;
+  const int lr = threadIdx.x >> 2;  // local row 0..63
+  for (i64 t = blockIdx.x; t < total; t += gridDim.x) {
+    const i64 l = t / tiles;
+    const i64 r0 = (t - l * tiles) * B2A_ROWS;
+    const int nr = (int)min((i64)B2A_ROWS, rows - r0);
+    const u64* src = ra + l * ra_ps + r0 * (i64)m;
+    const int nel = nr * m;
+    __syncthreads();
+    if ((((uintptr_t)src) & 15) == 0) {
+      const int nv = nel >> 1;
+      const ulonglong2* s2 = reinterpret_cast<const ulonglong2*>(src);
+      ulonglong2* d2 = reinterpret_cast<ulonglong2*>(slab);
+      for (int i = threadIdx.x; i < nv; i += blockDim.x) d2[i] = __ldcs(s2 + i);
+      if ((nel & 1) && threadIdx.x == 0) slab[nel - 1] = src[nel - 1];
+    } else {
+      for (int i = threadIdx.x; i < nel; i += blockDim.x) slab[i] = __ldcs(src + i);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) out[t] = acc & msk;
+    __syncthreads();
+    u64 acc = 0;
+    if (lr < nr) {
+      const u64 cw = c[r0 + lr];
+      const u64* row = slab + lr * m;
+      for (int j = sub; j < m; j += 4) {
+        const u64 cj = (cw >> j) & 1ull;
+        u64 v = row[j] * (1ull - 2ull * cj);
+        if (l == p0) v += cj;
+        acc += (v & msk) * wsh[j];
+      }
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (sub == 0 && lr < nr) out[l * rows + r0 + lr] = acc & msk;
   }
 }
 
@@ -648,7 +672,10 @@ extern "C" int mpx_bit2a_finish(uint64_t* out, const uint64_t* c, const uint64_t
     k_bit2a_expand<<<grid_for((i64)L * rows * m), MPX_THREADS, 0, s>>>(out, c, rarith, ra_ps, L, rows, m,
                                                                         msk, p0);
   else
-    k_bit2a_compose<<<grid_for((i64)L * rows * 32), MPX_THREADS, 0, s>>>(out, c, rarith, ra_ps, L, rows,
-                                                                          m, msk, p0, wts);
+  {
+    i64 tiles = (i64)L * ((rows + B2A_ROWS - 1) / B2A_ROWS);
+    unsigned g = (unsigned)(tiles < 148 * 8 ? tiles : 148 * 8);
+    k_bit2a_compose<<<g, 256, 0, s>>>(out, c, rarith, ra_ps, L, rows, m, msk, p0, wts);
+  }
   return launch_status();
 }

@@ -233,17 +233,75 @@ struct GatherSpec {
   int8_t src[64];
 };
 
+// General bit gather (arbitrary source list).
 __global__ void k_bits_gather(u64* __restrict__ out, const u64* __restrict__ in, GatherSpec g, int k,
                               i64 n) {
   GRID_STRIDE(i, n) {
     const u64 x = in[i];
     u64 v = 0;
+#pragma unroll 8
     for (int t = 0; t < k; ++t) {
       const int s = g.src[t];
       if (s >= 0) v |= ((x >> s) & 1ull) << t;
     }
     out[i] = v;
   }
+}
+
+// Fast paths: up to 3 runs, each a contiguous ascending (shift + mask) or
+// descending (bit reverse) source range; -1 padding runs produce zeros.
+struct RunSpec {
+  int nruns;
+  int src0[3], len[3], dst0[3], dir[3];  // dir: +1 ascending, -1 descending, 0 zeros
+};
+
+__global__ void k_bits_runs(u64* __restrict__ out, const u64* __restrict__ in, RunSpec rs, i64 n) {
+  GRID_STRIDE(i, n) {
+    const u64 x = in[i];
+    u64 v = 0;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      if (q >= rs.nruns) break;
+      const int len = rs.len[q];
+      if (rs.dir[q] > 0) {
+        v |= ((x >> rs.src0[q]) & low_bits(len)) << rs.dst0[q];
+      } else if (rs.dir[q] < 0) {
+        // bits src0, src0-1, ..., src0-len+1 -> dst0, dst0+1, ...
+        const u64 seg = (x >> (rs.src0[q] - len + 1)) & low_bits(len);
+        v |= (__brevll(seg) >> (64 - len)) << rs.dst0[q];
+      }
+    }
+    out[i] = v;
+  }
+}
+
+static bool make_runs(const GatherSpec& g, int k, RunSpec& rs) {
+  rs.nruns = 0;
+  int t = 0;
+  while (t < k) {
+    if (rs.nruns == 3) return false;
+    const int q = rs.nruns++;
+    rs.dst0[q] = t;
+    rs.src0[q] = g.src[t];
+    if (g.src[t] < 0) {
+      int e = t;
+      while (e < k && g.src[e] < 0) ++e;
+      rs.len[q] = e - t;
+      rs.dir[q] = 0;
+      t = e;
+      continue;
+    }
+    int e = t + 1;
+    int dir = 0;
+    if (e < k && g.src[e] == g.src[t] + 1) dir = 1;
+    else if (e < k && g.src[e] == g.src[t] - 1) dir = -1;
+    else dir = 1;
+    while (e < k && g.src[e] >= 0 && g.src[e] == g.src[e - 1] + dir) ++e;
+    rs.len[q] = e - t;
+    rs.dir[q] = dir;
+    t = e;
+  }
+  return true;
 }
 
 extern "C" int mpx_bits_gather(uint64_t* out, const uint64_t* in, const int8_t* src_host, int k,
@@ -253,7 +311,11 @@ extern "C" int mpx_bits_gather(uint64_t* out, const uint64_t* in, const int8_t* 
   for (int t = 0; t < 64; ++t) g.src[t] = t < k ? src_host[t] : (int8_t)-1;
   for (int t = 0; t < k; ++t) CHECK_ARG(g.src[t] < 64);
   if (nwords == 0) return MPX_OK;
-  k_bits_gather<<<grid_for(nwords), MPX_THREADS, 0, (cudaStream_t)stream>>>(out, in, g, k, nwords);
+  RunSpec rs;
+  if (make_runs(g, k, rs))
+    k_bits_runs<<<grid_for(nwords), MPX_THREADS, 0, (cudaStream_t)stream>>>(out, in, rs, nwords);
+  else
+    k_bits_gather<<<grid_for(nwords), MPX_THREADS, 0, (cudaStream_t)stream>>>(out, in, g, k, nwords);
   return launch_status();
 }
 
