@@ -252,34 +252,92 @@ class SimSession(_Session):
         self.party = None
 
 
+class DistComm:
+    """Collectives over a torch.distributed group: NCCL over NVLink on B200
+    (gloo on CPU for host-logic tests). Communication only - no arithmetic."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def allreduce_sum_(self, flat: torch.Tensor) -> None:
+        """In-place int64 sum over ranks; two's-complement wrap = Z_2^64."""
+        self.dist.all_reduce(flat, op=self.dist.ReduceOp.SUM, group=self.group)
+
+    def allgather(self, flat: torch.Tensor) -> torch.Tensor:
+        out = torch.empty((self.world, flat.numel()), dtype=flat.dtype, device=flat.device)
+        if flat.is_cuda:
+            self.dist.all_gather_into_tensor(out, flat, group=self.group)
+        else:
+            self.dist.all_gather(list(out.unbind(0)), flat, group=self.group)
+        return out
+
+
+class ThreadHub:
+    """Test harness: n party threads on ONE GPU exchanging partial openings by
+    host rendezvous (no device-side waiting). Emulates the NCCL party layer so
+    the per-round mask -> exchange -> finish path runs bit-exactly on 1 GPU."""
+
+    def __init__(self, n: int):
+        import threading
+        self.n = n
+        self.barrier = threading.Barrier(n)
+        self.slots = [None] * n
+
+    def comm(self, rank: int) -> "ThreadComm":
+        return ThreadComm(self, rank)
+
+
+class ThreadComm:
+    def __init__(self, hub: ThreadHub, rank: int):
+        self.hub, self.rank, self.world = hub, rank, hub.n
+
+    def allgather(self, flat: torch.Tensor) -> torch.Tensor:
+        torch.cuda.current_stream().synchronize()
+        self.hub.slots[self.rank] = flat
+        self.hub.barrier.wait()
+        out = torch.stack(self.hub.slots)
+        torch.cuda.current_stream().synchronize()
+        self.hub.barrier.wait()
+        return out
+
+    def allreduce_sum_(self, flat: torch.Tensor) -> None:
+        g = self.allgather(flat)
+        K.open_sum(flat, g, self.world, flat.numel(), 64)
+
+
 class PartySession(_Session):
-    """One party per process/GPU; openings are NCCL collectives over the group.
+    """One party per process/GPU; openings are collectives over the party group.
 
     Signature mirrors the reference's ``PartySession(party, n_parties, mesh,
-    store, rng, metrics)`` (session.py:53-64); ``mesh`` is the
-    torch.distributed process group (None = default group).
+    store, rng, metrics)`` (session.py:53-64). ``mesh`` is the communicator:
+    None = the default torch.distributed group over NCCL (``DistComm``), or
+    any object with ``world``, ``allreduce_sum_`` and ``allgather``.
     """
 
     def __init__(self, party: int, n_parties: int, mesh=None, store=None, rng=None,
                  metrics: CommMetrics | None = None, device=None):
-        import torch.distributed as dist
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() \
                 else torch.device("cpu")
         super().__init__((party,), n_parties, store, metrics, device)
         self.party = party
-        self.group = mesh
-        self.dist = dist
-        self.world = dist.get_world_size(mesh) if dist.is_initialized() else 1
+        if mesh is None:
+            import torch.distributed as dist
+            mesh = DistComm() if dist.is_available() and dist.is_initialized() else None
+        self.comm = mesh
+        self.world = mesh.world if mesh is not None else 1
         if self.world not in (1, n_parties):
             raise ValueError("one rank per party expected")
 
     def _collective(self, arith, bits):
-        dist = self.dist
         outs = []
         if arith:
             flat = torch.cat([t.reshape(-1) for t in arith]) if len(arith) > 1 else arith[0].reshape(-1)
-            dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=self.group)
+            self.comm.allreduce_sum_(flat)
             self.metrics.physical_bytes += flat.numel() * 8
             off = 0
             for t in arith:
@@ -287,8 +345,7 @@ class PartySession(_Session):
                 off += t.numel()
         if bits:
             flat = torch.cat([t.reshape(-1) for t in bits]) if len(bits) > 1 else bits[0].reshape(-1)
-            gathered = torch.empty((self.world, flat.numel()), dtype=torch.int64, device=flat.device)
-            dist.all_gather_into_tensor(gathered, flat, group=self.group)
+            gathered = self.comm.allgather(flat)
             self.metrics.physical_bytes += flat.numel() * 8 * (self.world - 1)
             red = torch.empty_like(flat)
             K.open_xor(red, gathered, self.world, flat.numel())
@@ -325,4 +382,4 @@ def demands_by_name(counter: DemandCounter) -> dict[str, int]:
     return {k.name(): c for k, c in sorted(counter.demands.items(), key=lambda kv: kv[0].name()) if c > 0}
 
 
-__all__ = ["SimSession", "PartySession", "run_sim", "dry_run", "demands_by_name", "MaterialKey"]
+__all__ = ["SimSession", "PartySession", "DistComm", "ThreadHub", "run_sim", "dry_run", "demands_by_name", "MaterialKey"]

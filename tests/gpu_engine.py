@@ -83,3 +83,42 @@ class GpuEngine:
         info = {"demands": demands_by_name(counter), "total": m.total.as_dict(),
                 "ledger": {k: v.as_dict() for k, v in sorted(m.ledger.items())}}
         return res, info, sess
+
+
+def run_party_threads(engine, fn, n, seed=11):
+    """Party mode on one GPU: n threads, one PartySession (L=1) each, partial
+    openings exchanged through a ThreadHub; returns per-party shares stacked
+    on a leading party axis plus party 0's ledger."""
+    import threading
+
+    from paper_2402_02320_b200.session import PartySession, ThreadHub
+
+    counter = dry_run(lambda s: fn(engine, s), n)
+    hub = ThreadHub(n)
+    hub.barrier = threading.Barrier(n, timeout=120)
+    outs, errs, sessions = {}, {}, {}
+
+    def worker(p):
+        try:
+            torch.cuda.set_device(0)
+            store = device_store(seed, n, counter.demands, parties=(p,), needs_bits=counter.needs_bits)
+            s = PartySession(p, n, hub.comm(p), store, device=torch.device("cuda", 0))
+            sessions[p] = s
+            outs[p] = fn(engine, s)
+            torch.cuda.synchronize()
+        except BaseException as e:  # noqa: BLE001
+            errs[p] = e
+            hub.barrier.abort()
+
+    ts = [threading.Thread(target=worker, args=(p,)) for p in range(n)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errs:
+        raise errs[min(errs)]
+    res = {k: np.concatenate([GpuEngine.export(outs[p][k]) for p in range(n)]) for k in outs[0]}
+    m = sessions[0].metrics
+    info = {"demands": demands_by_name(counter), "total": m.total.as_dict(),
+            "ledger": {k: v.as_dict() for k, v in sorted(m.ledger.items())}}
+    return res, info, sessions
