@@ -190,6 +190,20 @@ int mpx_gemm_simt(uint64_t* C, const uint64_t* A, const uint64_t* B, int64_t bat
                   int64_t K, int64_t N, int64_t sA, int64_t sB, int64_t sC, int accumulate, int width,
                   void* stream);
 
+/* ---- tcgen05 int8-limb Z_2^64 GEMM (gemm_tc.cu) ----
+ * Limb split of a row-major u64 matrix into 8 u8 planes (plane stride
+ * `plane`, row pitch `pitch`, column offset `coff` bytes): trans = 0 writes
+ * plane[i][r][coff + c], trans = 1 writes plane[i][c][coff + r] (K-major B). */
+int mpx_limb_split(uint8_t* out, const uint64_t* A, int64_t rows, int64_t cols, int64_t lda,
+                   int64_t plane, int64_t pitch, int64_t coff, int trans, void* stream);
+/* C[z] (+)= sum_{i+j<=7} 2^(8(i+j)) A8[z][i] @ B8[z][j]^T mod 2^w on tcgen05
+ * kind::i8 with per-diagonal TMEM accumulators, TMA-fed (128B swizzle).
+ * A8: [batch][8][Mpad][Kpad], B8: [batch][8][Npad][Kpad] u8, zero padded;
+ * Mpad % 128 == 0, Npad % 64 == 0, Kpad % 128 == 0, Kpad <= 16384. */
+int mpx_gemm_limbs(uint64_t* C, const uint8_t* A8, const uint8_t* B8, int64_t batch, int64_t M,
+                   int64_t N, int64_t Mpad, int64_t Npad, int64_t Kpad, int64_t ldc, int64_t sC,
+                   int accumulate, int width, void* stream);
+
 /* ---- trusted dealer (preprocessing.py:121-174; ring.py:124-134) ----
  * Philox4x64-10 keyed (k0, k1) exactly as numpy; the byte stream is read as
  * u32 words from u32 index `u32_off` (Generator.bytes semantics). */

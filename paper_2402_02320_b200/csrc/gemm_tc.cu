@@ -1,7 +1,426 @@
-// tcgen05 int8-limb Z_2^64 GEMM (placeholder until the tensor-core kernel lands).
+// Z_2^64 GEMM on the 5th-gen tensor cores (tcgen05, kind::i8, TMEM, TMA).
+//
+// A 64-bit ring product is exact from 8-bit limbs: with A = sum_i 2^(8i) A_i,
+// B = sum_j 2^(8j) B_j (u8 limb planes),
+//     A @ B mod 2^64 = sum_{d=0..7} 2^(8d) * sum_{i+j=d} A_i @ B_j   (mod 2^64)
+// i.e. 36 u8 x u8 -> s32 limb products, accumulated per diagonal d in its own
+// TMEM accumulator. Diagonal d only matters mod 2^(64-8d): d >= 4 needs 32
+// bits (wrap-around harmless), d <= 3 stays below 2^32 while K <= 16384
+// ((d+1) * K * 255^2 < 2^32), so the u32 reading of each s32 accumulator
+// recombines exactly (SURVEY §7 hard part 1, checked on all-0xFF inputs in
+// tests/test_gemm_tc.py).
+//
+// CTA tile 128 (M) x 64 (N): 8 accumulators x 64 columns = all 512 TMEM
+// columns. Per k-block of 128 bytes: all 8 B-limb tiles stay resident (double
+// buffered) while the 8 A-limb tiles stream through a 4-stage ring; A_i meets
+// B_0..B_{7-i}. Warp roles: w0 TMA producer, w1 MMA issuer (+TMEM owner),
+// w2..w5 epilogue (TMEM -> registers -> limb recombination -> global).
+// Operand tiles are TMA-loaded with 128-byte swizzle; UMMA smem descriptors
+// are K-major SWIZZLE_128B.
+#include <cuda.h>
+
 #include "common.cuh"
+
+#define TC_BM 128
+#define TC_BN 64
+#define TC_BK 128
+#define TC_ASTAGES 4
+#define TC_BSTAGES 2
+#define TC_A_TILE (TC_BM * TC_BK)          // 16 KB
+#define TC_B_TILE (TC_BN * TC_BK)          // 8 KB
+#define TC_B_STAGE (8 * TC_B_TILE)         // 64 KB
+#define TC_SMEM_BYTES (TC_ASTAGES * TC_A_TILE + TC_BSTAGES * TC_B_STAGE + 1024 + 256)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  const uint32_t z = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(z), "r"(z), "r"(z), "r"(z));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+// K-major, 128-byte swizzle UMMA shared-memory descriptor (version 1 = sm100).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                 // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;       // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                 // version
+  d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
+  return d;
+}
+
+#define TMEM_LD32(taddr, v)                                                                              \
+  asm volatile(                                                                                          \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"   \
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                        \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), \
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),        \
+        "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),      \
+        "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),      \
+        "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                                           \
+      : "r"(taddr))
+
+struct TcArgs {
+  u64* C;
+  i64 ldc;
+  i64 sC;        // batch stride of C (elements)
+  int M, N;      // true output extent
+  int Mpad, Npad;
+  int nk;        // k-blocks of TC_BK bytes
+  int accumulate;
+  u64 msk;
+};
+
+__global__ void __launch_bounds__(192, 1)
+    k_gemm_limbs_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                    TcArgs args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + TC_ASTAGES * TC_A_TILE;
+  uint64_t* bars = (uint64_t*)(sB + TC_BSTAGES * TC_B_STAGE);
+  uint64_t* fullA = bars;
+  uint64_t* emptyA = bars + TC_ASTAGES;
+  uint64_t* fullB = bars + 2 * TC_ASTAGES;
+  uint64_t* emptyB = bars + 2 * TC_ASTAGES + TC_BSTAGES;
+  uint64_t* tmem_full = bars + 2 * TC_ASTAGES + 2 * TC_BSTAGES;
+  uint32_t* tmem_holder = (uint32_t*)(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * TC_BM;
+  const int n0 = blockIdx.x * TC_BN;
+  const int z = blockIdx.z;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TC_ASTAGES; ++s) {
+      mbar_init(&fullA[s], 1);
+      mbar_init(&emptyA[s], 1);
+    }
+    for (int s = 0; s < TC_BSTAGES; ++s) {
+      mbar_init(&fullB[s], 1);
+      mbar_init(&emptyB[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      int as = 0;
+      uint32_t aph = 0;
+      for (int kb = 0; kb < args.nk; ++kb) {
+        const int bs = kb & 1;
+        const uint32_t bph = (uint32_t)((kb >> 1) & 1);
+        mbar_wait(&emptyB[bs], bph ^ 1);
+        mbar_expect_tx(&fullB[bs], TC_B_STAGE);
+        for (int j = 0; j < 8; ++j)
+          tma_load_2d(sB + bs * TC_B_STAGE + j * TC_B_TILE, &mapB, &fullB[bs], kb * TC_BK,
+                      (z * 8 + j) * args.Npad + n0);
+        for (int i = 0; i < 8; ++i) {
+          mbar_wait(&emptyA[as], aph ^ 1);
+          mbar_expect_tx(&fullA[as], TC_A_TILE);
+          tma_load_2d(sA + as * TC_A_TILE, &mapA, &fullA[as], kb * TC_BK, (z * 8 + i) * args.Mpad + m0);
+          if (++as == TC_ASTAGES) {
+            as = 0;
+            aph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      const uint32_t idesc = (2u << 4) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+      int as = 0;
+      uint32_t aph = 0;
+      for (int kb = 0; kb < args.nk; ++kb) {
+        const int bs = kb & 1;
+        const uint32_t bph = (uint32_t)((kb >> 1) & 1);
+        mbar_wait(&fullB[bs], bph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t b_base = smem_u32(sB + bs * TC_B_STAGE);
+        for (int i = 0; i < 8; ++i) {
+          mbar_wait(&fullA[as], aph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a_base = smem_u32(sA + as * TC_A_TILE);
+          for (int j = 0; j <= 7 - i; ++j) {
+            const uint32_t d_tmem = tmem_base + (uint32_t)((i + j) * TC_BN);
+#pragma unroll
+            for (int kk = 0; kk < TC_BK / 32; ++kk) {
+              const uint64_t ad = umma_desc_sw128(a_base + kk * 32);
+              const uint64_t bd = umma_desc_sw128(b_base + j * TC_B_TILE + kk * 32);
+              const uint32_t acc = (kb > 0 || i > 0 || kk > 0) ? 1u : 0u;
+              mma_i8(d_tmem, ad, bd, idesc, acc);
+            }
+          }
+          umma_commit(&emptyA[as]);  // slot free once these MMAs retire
+          if (++as == TC_ASTAGES) {
+            as = 0;
+            aph ^= 1;
+          }
+        }
+        umma_commit(&emptyB[bs]);
+      }
+      umma_commit(tmem_full);
+    }
+  } else {
+    // ---------------- epilogue: warps 2..5 ----------------
+    const int sp = warp & 3;  // TMEM sub-partition this warp may access
+    const int row = m0 + sp * 32 + lane;
+    mbar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    u64* Crow = args.C + (i64)z * args.sC + (i64)row * args.ldc;
+    for (int c = 0; c < TC_BN / 32; ++c) {
+      u64 res[32];
+#pragma unroll
+      for (int t = 0; t < 32; ++t) res[t] = 0;
+#pragma unroll
+      for (int d = 0; d < 8; ++d) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem_base + ((uint32_t)(sp * 32) << 16) + (uint32_t)(d * TC_BN + c * 32);
+        TMEM_LD32(taddr, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int t = 0; t < 32; ++t) res[t] += (u64)v[t] << (8 * d);
+      }
+      if (row < args.M) {
+        const int cbase = n0 + c * 32;
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const int col = cbase + t;
+          if (col < args.N) {
+            u64 v = res[t];
+            if (args.accumulate) v += Crow[col];
+            Crow[col] = v & args.msk;
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+  }
+}
+
+// --------------------------------------------------------------------------
+// Limb split: u64 matrix -> 8 u8 planes. `trans` = 0: plane[i][r][coff + c];
+// trans = 1: plane[i][c][coff + r] (K-major operand from a row-major KxN).
+
+__device__ __forceinline__ void bytes_transpose8(const u64 (&w)[8], u64 (&p)[8]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    u64 v = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v |= ((w[c] >> (8 * i)) & 0xFFull) << (8 * c);
+    p[i] = v;
+  }
+}
+
+// non-transposed: each thread takes 8 consecutive columns of one row
+__global__ void k_limb_split(uint8_t* __restrict__ out, const u64* __restrict__ A, i64 rows, i64 cols, i64 lda,
+                             i64 plane, i64 pitch, i64 coff) {
+  const i64 groups_per_row = (cols + 7) / 8;
+  const i64 total = rows * groups_per_row;
+  GRID_STRIDE(t, total) {
+    const i64 r = t / groups_per_row;
+    const i64 c0 = (t - r * groups_per_row) * 8;
+    u64 w[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) w[c] = (c0 + c < cols) ? A[r * lda + c0 + c] : 0ull;
+    u64 p[8];
+    bytes_transpose8(w, p);
+    uint8_t* dst = out + r * pitch + coff + c0;
+    if (c0 + 8 <= cols && (((uintptr_t)dst) & 7) == 0) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) *reinterpret_cast<u64*>(dst + i * plane) = p[i];
+    } else {
+      for (int i = 0; i < 8; ++i)
+        for (int c = 0; c < 8 && c0 + c < cols; ++c) dst[i * plane + c] = (uint8_t)(p[i] >> (8 * c));
+    }
+  }
+}
+
+// transposed via a 64 (k) x 32 (n) smem tile
+__global__ void __launch_bounds__(256) k_limb_split_t(uint8_t* __restrict__ out, const u64* __restrict__ A,
+                                                      i64 rows, i64 cols, i64 lda, i64 plane, i64 pitch,
+                                                      i64 coff) {
+  __shared__ u64 tile[64][33];
+  const i64 k0 = (i64)blockIdx.y * 64;
+  const i64 n0 = (i64)blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int kk = ty; kk < 64; kk += 8) {
+    const i64 k = k0 + kk, n = n0 + tx;
+    tile[kk][tx] = (k < rows && n < cols) ? A[k * lda + n] : 0ull;
+  }
+  __syncthreads();
+  const int n = tx;
+  const int g = ty;  // 8 groups of 8 k's
+  const i64 gn = n0 + n;
+  const i64 gk = k0 + g * 8;
+  if (gn < cols && gk < rows) {
+    u64 w[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) w[c] = tile[g * 8 + c][n];
+    u64 p[8];
+    bytes_transpose8(w, p);
+    uint8_t* dst = out + gn * pitch + coff + gk;
+    if (gk + 8 <= rows && (((uintptr_t)dst) & 7) == 0) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) *reinterpret_cast<u64*>(dst + i * plane) = p[i];
+    } else {
+      for (int i = 0; i < 8; ++i)
+        for (int c = 0; c < 8 && gk + c < rows; ++c) dst[i * plane + c] = (uint8_t)(p[i] >> (8 * c));
+    }
+  }
+}
+
+extern "C" int mpx_limb_split(uint8_t* out, const uint64_t* A, int64_t rows, int64_t cols, int64_t lda,
+                              int64_t plane, int64_t pitch, int64_t coff, int trans, void* stream) {
+  CHECK_ARG(out && A && rows >= 0 && cols >= 0 && lda >= cols);
+  if (rows == 0 || cols == 0) return MPX_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!trans) {
+    k_limb_split<<<grid_for(rows * ((cols + 7) / 8)), MPX_THREADS, 0, s>>>(out, A, rows, cols, lda, plane,
+                                                                           pitch, coff);
+  } else {
+    dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 63) / 64));
+    CHECK_ARG(grid.y <= 65535);
+    k_limb_split_t<<<grid, 256, 0, s>>>(out, A, rows, cols, lda, plane, pitch, coff);
+  }
+  return launch_status();
+}
+
+// --------------------------------------------------------------------------
+// Host: tensor maps + launch
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                    CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                    CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_encodeTiled)p;
+  }
+  return fn;
+}
+
+static int make_map(CUtensorMap* map, const uint8_t* base, i64 rows, i64 kbytes, int box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return MPX_ERR_CUDA;
+  cuuint64_t dims[2] = {(cuuint64_t)kbytes, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)kbytes};
+  cuuint32_t box[2] = {TC_BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? MPX_OK : MPX_ERR_CUDA;
+}
+
+// C[z] (+)= sum_{i+j<=7} 2^(8(i+j)) A8[z][i] @ B8[z][j]^T  (mod 2^width)
+// A8: [batch][8][Mpad][Kpad] u8, B8: [batch][8][Npad][Kpad] u8, zero padded;
+// Mpad % 128 == 0, Npad % 64 == 0, Kpad % 128 == 0, Kpad <= 16384.
+extern "C" int mpx_gemm_limbs(uint64_t* C, const uint8_t* A8, const uint8_t* B8, int64_t batch, int64_t M,
+                              int64_t N, int64_t Mpad, int64_t Npad, int64_t Kpad, int64_t ldc, int64_t sC,
+                              int accumulate, int width, void* stream) {
+  CHECK_ARG(C && A8 && B8 && batch >= 1 && batch <= 65535 && M >= 1 && N >= 1 && width >= 1 && width <= 64);
+  CHECK_ARG(Mpad % TC_BM == 0 && Npad % TC_BN == 0 && Kpad % TC_BK == 0 && Kpad >= TC_BK && Kpad <= 16384);
+  CHECK_ARG(M <= Mpad && N <= Npad && ldc >= N);
+  CHECK_ARG(batch * 8 * Mpad < (1ll << 31) && batch * 8 * Npad < (1ll << 31));
+  CUtensorMap mapA, mapB;
+  if (make_map(&mapA, A8, batch * 8 * Mpad, Kpad, TC_BM) != MPX_OK) return MPX_ERR_CUDA;
+  if (make_map(&mapB, B8, batch * 8 * Npad, Kpad, TC_BN) != MPX_OK) return MPX_ERR_CUDA;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(k_gemm_limbs_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES) !=
+        cudaSuccess)
+      return MPX_ERR_CUDA;
+    attr_set = true;
+  }
+  TcArgs a;
+  a.C = C;
+  a.ldc = ldc;
+  a.sC = sC;
+  a.M = (int)M;
+  a.N = (int)N;
+  a.Mpad = (int)Mpad;
+  a.Npad = (int)Npad;
+  a.nk = (int)(Kpad / TC_BK);
+  a.accumulate = accumulate;
+  a.msk = ring_mask(width);
+  dim3 grid((unsigned)(Npad / TC_BN), (unsigned)(Mpad / TC_BM), (unsigned)batch);
+  k_gemm_limbs_tc<<<grid, 192, TC_SMEM_BYTES, (cudaStream_t)stream>>>(mapA, mapB, a);
+  return launch_status();
+}
 
 int mpx_gemm_tc(uint64_t*, const uint64_t*, const uint64_t*, int64_t, int64_t, int64_t, int64_t, int64_t,
                 int64_t, int64_t, int, int, cudaStream_t) {
-  return MPX_ERR_UNSUPPORTED;
+  return MPX_ERR_UNSUPPORTED;  // the u64 entry point needs caller scratch: see mpx_gemm_limbs
 }

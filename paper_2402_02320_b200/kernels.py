@@ -255,8 +255,59 @@ def bits_rows_to_flat(flat, rows_in, rows, m):
 def gemm(C, A, B, batch, M, K, N, sA, sB, sC, accumulate, width, simt=False):
     if _dry(C):
         return C
+    if not simt and M * K * N >= TC_MIN_MACS and M >= 64 and N >= 32 and K >= 64:
+        return gemm_tc(C, A, B, batch, M, K, N, sA, sB, sC, accumulate, width)
     call("mpx_gemm_simt" if simt else "mpx_gemm", ptr(C), A if isinstance(A, int) else ptr(A),
          B if isinstance(B, int) else ptr(B), batch, M, K, N, sA, sB, sC, int(accumulate), width)
+    return C
+
+
+TC_MIN_MACS = 1 << 22   # below this the SIMT tiles win (launch + split overhead)
+TC_MAX_K = 16384        # exactness bound of the u32 diagonal accumulators
+
+
+def _rup(x, m):
+    return (x + m - 1) // m * m
+
+
+def limb_split(out, A, rows, cols, lda, plane, pitch, coff, trans):
+    if _dry(out):
+        return out
+    call("mpx_limb_split", ptr(out), A if isinstance(A, int) else ptr(A), rows, cols, lda, plane, pitch,
+         coff, int(trans))
+    return out
+
+
+def gemm_limbs(C, A8, B8, batch, M, N, Mpad, Npad, Kpad, ldc, sC, accumulate, width):
+    if _dry(C):
+        return C
+    call("mpx_gemm_limbs", ptr(C), ptr(A8), ptr(B8), batch, M, N, Mpad, Npad, Kpad, ldc, sC,
+         int(accumulate), width)
+    return C
+
+
+def gemm_tc(C, A, B, batch, M, K, N, sA, sB, sC, accumulate, width):
+    """u64 GEMM on the tcgen05 limb kernel: split operands into u8 limb planes
+    (scratch from the caching allocator), K chunked to <= TC_MAX_K."""
+    if _dry(C):
+        return C
+    dev = C.device
+    Mpad, Npad = _rup(M, 128), _rup(N, 64)
+    a_ptr = A if isinstance(A, int) else ptr(A)
+    b_ptr = B if isinstance(B, int) else ptr(B)
+    k0 = 0
+    first = True
+    while k0 < K:
+        kc = min(TC_MAX_K, K - k0)
+        Kpad = _rup(kc, 128)
+        A8 = torch.zeros((batch, 8, Mpad, Kpad), dtype=torch.uint8, device=dev)
+        B8 = torch.zeros((batch, 8, Npad, Kpad), dtype=torch.uint8, device=dev)
+        for z in range(batch):
+            limb_split(A8[z], a_ptr + 8 * (z * sA + k0), M, kc, K, Mpad * Kpad, Kpad, 0, False)
+            limb_split(B8[z], b_ptr + 8 * (z * sB + k0 * N), kc, N, N, Npad * Kpad, Kpad, 0, True)
+        gemm_limbs(C, A8, B8, batch, M, N, Mpad, Npad, Kpad, N, sC, accumulate or not first, width)
+        first = False
+        k0 += kc
     return C
 
 
