@@ -214,6 +214,95 @@ def _read_peaks():
 
 
 # ---------------------------------------------------------------------------
+# cfg-5 sweep entries (secondary): Exp / Log on 2^24, Beaver matmul 4096^2
+
+
+def int8_peak_tops(torch, n=8192, iters=10):
+    """cuBLASLt int8 GEMM (torch._int_mm) burst rate: the tensor-pipe roofline
+    denominator for int8 (MEASURED_PEAKS.json only carries bf16)."""
+    a = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda")
+    b = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda")
+    for _ in range(3):
+        torch._int_mm(a, b)
+    torch.cuda.synchronize()
+    best = None
+    for _ in range(iters):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch._int_mm(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    return 2 * n ** 3 / (best / 1e3) / 1e12
+
+
+def sweep_entry(torch, G, make_session, parties, n_parties, dev, name, steps=2, warmup=1):
+    from paper_2402_02320_b200 import _lib
+    from paper_2402_02320_b200.preprocessing import DemandCounter, device_store
+    from paper_2402_02320_b200.protocols import batch_matmul
+    N = 1 << 24
+    rng = np.random.default_rng(7)
+    if name == "matmul":
+        D = 4096
+        a = rng.integers(0, 1 << 64, (D, D), dtype=np.uint64)
+        b = rng.integers(0, 1 << 64, (D, D), dtype=np.uint64)
+
+        def inputs(s):
+            return s.share_ring(a, 64, 0, label_key("share:mm_a")), s.share_ring(b, 64, 0, label_key("share:mm_b"))
+
+        def op(s, x, y):
+            return batch_matmul(s, [(x, y)])[0]
+    else:
+        xs = rng.uniform(-16, 16, N) if name == "exp" else np.exp2(rng.uniform(-8, 8, N))
+        enc = encode_np(xs)
+
+        def inputs(s):
+            x = s.share_ring(enc, WIDTH, FRAC, label_key(f"share:{name}"))
+            return x, None
+
+        def op(s, x, y):
+            return G.exponentiation(s, x) if name == "exp" else G.logarithm(s, x)
+    counter = DemandCounter(parties, n_parties)
+    sd = make_session(counter)
+    op(sd, *inputs(sd))
+    x, y = inputs(make_session(None))
+    times, prof_ms = [], {}
+    store = None
+    for step in range(warmup + steps):
+        del store
+        store = device_store(500 + step, n_parties, counter.demands, parties=parties, device=dev,
+                             needs_bits=counter.needs_bits)
+        sess = make_session(store)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if step == warmup + steps - 1:
+            _lib.PROFILE = []
+        e0.record()
+        op(sess, x, y)
+        e1.record()
+        torch.cuda.synchronize()
+        if _lib.PROFILE is not None:
+            for nm, _a, p0, p1 in _lib.PROFILE:
+                prof_ms[nm] = prof_ms.get(nm, 0.0) + p0.elapsed_time(p1)
+            _lib.PROFILE = None
+        if step >= warmup:
+            times.append(e0.elapsed_time(e1))
+    del store
+    ms = float(np.mean(times))
+    out = {"ms_per_op": ms, "steps": steps}
+    if name == "matmul":
+        macs = len(parties) * D * (2 * D) * D          # [D|A_l] @ [B_l';E] per local party
+        tc_ms = prof_ms.get("mpx_gemm_limbs", 0.0)
+        out.update({"shape": [D, D, D], "ring_GMAC_per_s": macs / (ms / 1e3) / 1e9,
+                    "gemm_kernel_ms": tc_ms,
+                    "gemm_int8_TOPS": 36 * 2 * macs / (tc_ms / 1e3) / 1e12 if tc_ms else None})
+    else:
+        out.update({"elements": N, "elements_per_s": N / (ms / 1e3)})
+    return out
+
+
+# ---------------------------------------------------------------------------
 # B200 arm
 
 
@@ -387,6 +476,19 @@ def run_b200(args):
     h2d = int(x_host.numel() * 8)
     d2h = int(y_host.numel() * 8)
 
+    sweep = {}
+    if not args.no_sweep:
+        for nm in ("exp", "log", "matmul"):
+            sweep[nm] = sweep_entry(torch, G, make_session, parties, n_parties, dev, nm)
+        if world == 1:
+            pk = int8_peak_tops(torch)
+            mm = sweep["matmul"]
+            mm["roofline"] = {"bound": "tensor", "kernel": "mpx_gemm_limbs (tcgen05 kind::i8)",
+                              "achieved": mm["gemm_kernel_ms"] and mm["gemm_int8_TOPS"], "peak": pk,
+                              "peak_kind": "measured in-run: torch._int_mm int8 8192^3 (cuBLASLt), burst",
+                              "unit": "TOPS int8",
+                              "frac": (mm["gemm_int8_TOPS"] / pk) if mm.get("gemm_int8_TOPS") else None}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -411,6 +513,7 @@ def run_b200(args):
             "max_rel_err": rel,
             "kernels": kernels,
             "cpu_baseline": cpu,
+            "sweep": sweep,
         }
         print(json.dumps(line))
     if world > 1:
@@ -453,6 +556,7 @@ def main():
     ap.add_argument("--elems", type=int, default=1 << 24)
     ap.add_argument("--cpu-sample", type=int, default=1 << 20)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -79,13 +79,40 @@ def batch_matmul(session, pairs) -> list[AShare]:
         Z = session.alloc((L, m, r))
         if not session.dry:
             Z.copy_(C)
-        K.gemm(Z, D, B.data_ptr(), L, m, k, r, 0, B.stride(0), m * r, True, w)
-        K.gemm(Z, A.data_ptr(), E, L, m, k, r, A.stride(0), 0, m * r, True, w)
-        if session.p0 >= 0:
-            K.gemm(Z[session.p0], D, E, 1, m, k, r, 0, 0, 0, True, w)
+        if not session.dry and _use_tc(m, k, r):
+            _beaver_matmul_tc(session, Z, D, E, A, B, L, m, k, r, w)
+        else:
+            K.gemm(Z, D, B.data_ptr(), L, m, k, r, 0, B.stride(0), m * r, True, w, simt=True)
+            K.gemm(Z, A.data_ptr(), E, L, m, k, r, A.stride(0), 0, m * r, True, w, simt=True)
+            if session.p0 >= 0:
+                K.gemm(Z[session.p0], D, E, 1, m, k, r, 0, 0, 0, True, w, simt=True)
         session.metrics.count(matmul_count=1, matmul_macs=m * k * r)
         out.append(AShare(Z, w, x.frac + y.frac, session.parties))
     return out
+
+
+def _use_tc(m, k, r) -> bool:
+    return m * k * r >= K.TC_MIN_MACS and m >= 64 and r >= 32 and 2 * k <= K.TC_MAX_K
+
+
+def _beaver_matmul_tc(session, Z, D, E, A, B, L, m, k, r, w):
+    """Z_l += [D | A_l] @ [B_l + [l==p0] E ; E] as ONE tcgen05 limb GEMM per party
+    (K doubled), so D@E at party 0 folds into its B operand (basic.py:72-75)."""
+    Mp, Np, Kp = K._rup(m, 128), K._rup(r, 64), K._rup(2 * k, 128)
+    A8 = torch.zeros((L, 8, Mp, Kp), dtype=torch.uint8, device=Z.device)
+    B8 = torch.zeros((L, 8, Np, Kp), dtype=torch.uint8, device=Z.device)
+    bp = None
+    for l in range(L):
+        K.limb_split(A8[l], D, m, k, k, Mp * Kp, Kp, 0, False)
+        K.limb_split(A8[l], A[l].data_ptr(), m, k, k, Mp * Kp, Kp, k, False)
+        if l == session.p0:
+            bp = torch.empty((k, r), dtype=torch.int64, device=Z.device)
+            K.ring_lin(bp, B[l], 1, E, 1, 0, None, 1, k * r, 64, -1)
+            K.limb_split(B8[l], bp, k, r, r, Np * Kp, Kp, 0, True)
+        else:
+            K.limb_split(B8[l], B[l].data_ptr(), k, r, r, Np * Kp, Kp, 0, True)
+        K.limb_split(B8[l], E, k, r, r, Np * Kp, Kp, k, True)
+    K.gemm_limbs(Z, A8, B8, L, m, r, Mp, Np, Kp, r, m * r, True, w)
 
 
 def and_gate(session, x: BShare, y: BShare) -> BShare:

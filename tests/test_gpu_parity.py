@@ -93,6 +93,17 @@ def big_matmul(M, s):
     return {"z": M.batch_matmul(s, [(M.deal_arith(s, a, 64, tag=0), M.deal_arith(s, b, 64, tag=1))])[0]}
 
 
+def tc_matmul(M, s):
+    rng = np.random.default_rng(16)
+    a = rng.integers(0, 1 << 64, (256, 320), dtype=np.uint64)
+    b = rng.integers(0, 1 << 64, (320, 192), dtype=np.uint64)
+    c = rng.integers(0, 1 << 64, (130, 256), dtype=np.uint64)
+    d = rng.integers(0, 1 << 64, (256, 96), dtype=np.uint64)
+    return {f"z{i}": z for i, z in enumerate(M.batch_matmul(s, [
+        (M.deal_arith(s, a, 64, tag=0), M.deal_arith(s, b, 64, tag=1)),
+        (M.deal_arith(s, c, 64, tag=2), M.deal_arith(s, d, 64, tag=3))]))}
+
+
 def big_decompose(M, s):
     rng = np.random.default_rng(7)
     xs = rng.integers(0, 1 << 64, 20000, dtype=np.uint64)
@@ -131,10 +142,11 @@ def big_attention(M, s):
     return {"o": M.attention_block(s, heads, optimized=True)}
 
 
-@pytest.mark.parametrize("fn,n", [(big_mul, 3), (big_matmul, 2), (big_decompose, 4),
+@pytest.mark.parametrize("fn,n", [(big_mul, 3), (big_matmul, 2), (tc_matmul, 2), (tc_matmul, 3),
+                                  (big_decompose, 4),
                                   (big_reciprocal, 2), (big_exp, 3), (big_log, 2),
                                   (big_softmax, 2), (big_attention, 2)],
-                         ids=["mul65536_n3", "matmul96x160x72", "decompose20000_n4", "reciprocal4096",
+                         ids=["mul65536_n3", "matmul96x160x72", "tc_matmul_n2", "tc_matmul_n3", "decompose20000_n4", "reciprocal4096",
                               "exp4096_n3", "log4096", "softmax16x128", "attention2h32"])
 def test_larger_sizes_vs_oracle(engine, oracle_engine, fn, n):
     _compare(engine, oracle_engine, fn, n)
