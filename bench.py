@@ -107,7 +107,7 @@ def cpu_reference(sample: int, n_parties: int, cores: int | None = None, reps: i
 
 
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -125,30 +125,38 @@ class ClockSampler:
         except OSError:
             self.proc = None
 
-    def stop(self) -> dict:
+    def stop(self, window=None) -> dict:
+        """Median SM clock and active throttle reasons over the samples taken
+        inside ``window`` (host epoch seconds of the timed region)."""
+        import datetime
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
         self.proc.wait()
         self.fh.close()
-        sms, maxes, reasons = [], [], set()
+        rows = []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 9:
+            if len(parts) < 10:
                 continue
             try:
-                sms.append(float(parts[1]))
-                maxes.append(float(parts[2]))
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(parts[2]), float(parts[3]), parts[6:10]))
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[5:9]):
+        os.unlink(self.path)
+        inside = [r for r in rows if window and window[0] - 0.05 <= r[0] <= window[1] + 0.05]
+        use = inside or rows
+        reasons = set()
+        for r in use:
+            for nm, v in zip(names, r[3]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
-        os.unlink(self.path)
-        return {"sm_mhz": float(np.median(sms)) if sms else None,
-                "sm_max_mhz": max(maxes) if maxes else None,
-                "reasons": sorted(reasons), "samples": len(sms)}
+        return {"sm_mhz": float(np.median([r[1] for r in use])) if use else None,
+                "sm_max_mhz": max(r[2] for r in use) if use else None,
+                "reasons": sorted(reasons), "samples": len(use),
+                "window": "timed region" if inside else "whole run (no sample fell inside the timed region)"}
 
 
 # ---------------------------------------------------------------------------
@@ -368,8 +376,10 @@ def run_b200(args):
 
     online_ms, dealer_s = [], []
     clocks = ClockSampler(local)
+    clocks.start()
     store = None
     launches_timed = 0
+    t_window = [None, None]
     for step in range(args.warmup + args.steps):
         del store
         store, dt = deal(step)
@@ -379,8 +389,8 @@ def run_b200(args):
         barrier()
         torch.cuda.synchronize()
         timed = step >= args.warmup
-        if timed and step == args.warmup:
-            clocks.start()
+        if timed and t_window[0] is None:
+            t_window[0] = time.time()
         l0 = _lib.LAUNCHES
         ev0.record()
         y = G.reciprocal(sess, x_sh)
@@ -390,7 +400,8 @@ def run_b200(args):
         if timed:
             online_ms.append(ev0.elapsed_time(ev1))
             launches_timed += _lib.LAUNCHES - l0
-    clk = clocks.stop()
+            t_window[1] = time.time()
+    clk = clocks.stop(t_window)
     total_ms = float(sum(online_ms))
     if world > 1:
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
