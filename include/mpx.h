@@ -204,6 +204,20 @@ int mpx_gemm_limbs(uint64_t* C, const uint8_t* A8, const uint8_t* B8, int64_t ba
                    int64_t N, int64_t Mpad, int64_t Npad, int64_t Kpad, int64_t ldc, int64_t sC,
                    int accumulate, int width, void* stream);
 
+/* ---- sim-mode whole-op fused kernels (fused_ops.cu) ----
+ * All L parties on this GPU: the whole Reciprocal / Exp / Log protocol
+ * (nonlinear.py:146-267) runs in one kernel, one thread per element, shares
+ * in registers. `tape_host` points to a host `Tape` (one MatRef per dealer
+ * take, in protocol order) and `params_host` to `FusedParams`; layouts are
+ * reported by mpx_fused_abi_sizes. */
+int mpx_reciprocal_fused(uint64_t* y, const uint64_t* x, int64_t n, const void* tape_host,
+                         const void* params_host, void* stream);
+int mpx_exp_fused(uint64_t* y, const uint64_t* x, int64_t n, const void* tape_host,
+                  const void* params_host, void* stream);
+int mpx_log_fused(uint64_t* y, const uint64_t* x, int64_t n, const void* tape_host,
+                  const void* params_host, void* stream);
+int mpx_fused_abi_sizes(int64_t* matref, int64_t* tape, int64_t* params, int64_t* tape_max);
+
 /* ---- trusted dealer (preprocessing.py:121-174; ring.py:124-134) ----
  * Philox4x64-10 keyed (k0, k1) exactly as numpy; the byte stream is read as
  * u32 words from u32 index `u32_off` (Generator.bytes semantics). */

@@ -1,0 +1,501 @@
+// Whole-op fused kernels for the all-parties-on-one-GPU deployment (sim mode).
+//
+// With every party's shares on this GPU an opening needs no communication, so
+// the 23-37 rounds of Exp / Log / Reciprocal can run inside ONE kernel: each
+// thread owns one element and keeps all L parties' shares in registers from
+// the input to the output, reading each item of its dealer material exactly
+// once. The protocol is the reference's, step for step (nonlinear.py:146-267,
+// basic.py:27-214, derived.py:20-149); the host records the exact sequence of
+// material takes (a "tape": one MatRef per take, pointers already advanced to
+// the store cursor) by running the Python protocol as a dry pass over the real
+// store, so material order and the ledger are identical to the per-round path.
+// Element e of a take that hands out `per` items per element reads items
+// [e*per, e*per + per) — the reference's flattened C order.
+#include "common.cuh"
+
+#define TAPE_MAX 64
+
+struct MatRef {
+  const u64* p0;  // triple a | bintriple a | dabit/edabit arithmetic part
+  const u64* p1;  // triple b | bintriple b | dabit/edabit bit stream
+  const u64* p2;  // triple c | bintriple c
+  i64 ps0, ps1, ps2;
+  i64 off;        // bit offset of the cursor (bit material)
+};
+
+struct Tape {
+  MatRef m[TAPE_MAX];
+  int n;
+};
+
+struct FusedParams {
+  int w, p, iters, bias, c;
+  int L, p0;
+  u64 log2e_p;      // enc(log2 e, w, p)
+  u64 bias_2p;      // enc(bias, w, 2p)
+  u64 one_p;        // enc(1.0, w, p)
+  u64 m1_p;         // enc(-1.0, w, p)
+  u64 ln2_p;        // enc(ln 2, w, p)
+  u64 coef_p[5];    // enc(c_i, w, p), i = 1..4 (scale_fixed)
+  u64 coef0_2p;     // enc(c_0, w, 2p) (add_const at doubled precision)
+  int coef_nz[5];
+};
+
+template <int L>
+struct Sh {
+  u64 v[L];
+};
+
+template <int L>
+__device__ __forceinline__ Sh<L> sh_lin(const Sh<L>& a, u64 ka, const Sh<L>& b, u64 kb, u64 c0, int p0, u64 msk) {
+  Sh<L> o;
+#pragma unroll
+  for (int l = 0; l < L; ++l) o.v[l] = (a.v[l] * ka + b.v[l] * kb + (l == p0 ? c0 : 0ull)) & msk;
+  return o;
+}
+
+template <int L>
+__device__ __forceinline__ Sh<L> sh_scale(const Sh<L>& a, u64 ka, u64 c0, int p0, u64 msk) {
+  Sh<L> o;
+#pragma unroll
+  for (int l = 0; l < L; ++l) o.v[l] = (a.v[l] * ka + (l == p0 ? c0 : 0ull)) & msk;
+  return o;
+}
+
+// Beaver mul (basic.py:27-42), triple item e of the take
+template <int L>
+__device__ __forceinline__ Sh<L> d_mul(const Sh<L>& x, const Sh<L>& y, const MatRef& t, i64 e, int p0, u64 msk) {
+  u64 a[L], b[L];
+  u64 d = 0, f = 0;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    a[l] = __ldcs(t.p0 + l * t.ps0 + e);
+    b[l] = __ldcs(t.p1 + l * t.ps1 + e);
+    d += x.v[l] - a[l];
+    f += y.v[l] - b[l];
+  }
+  Sh<L> z;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    u64 v = __ldcs(t.p2 + l * t.ps2 + e) + d * b[l] + f * a[l];
+    if (l == p0) v += d * f;
+    z.v[l] = v & msk;
+  }
+  return z;
+}
+
+// probabilistic truncation (derived.py:20-70); lo/hi = edaBit(w, f), edaBit(w, w-1-f)
+template <int L>
+__device__ __forceinline__ Sh<L> d_trunc(const Sh<L>& x, const MatRef& lo, const MatRef* hi, i64 e, int f,
+                                         bool sgn, int w, int p0, u64 msk) {
+  const u64 bias = sgn ? (1ull << (w - 2)) : 0ull;
+  const u64 unbias = sgn ? (1ull << (w - 2 - f)) : 0ull;
+  u64 h[L];
+  u64 s = 0;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    h[l] = hi ? __ldcs(hi->p0 + l * hi->ps0 + e) : 0ull;
+    u64 v = x.v[l] + __ldcs(lo.p0 + l * lo.ps0 + e) + (h[l] << f);
+    if (l == p0) v += bias;
+    s += v;
+  }
+  const u64 chi = (s & msk) >> f;
+  Sh<L> z;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    u64 v = 0ull - h[l];
+    if (l == p0) v += chi - unbias;
+    z.v[l] = v & msk;
+  }
+  return z;
+}
+
+// Kogge-Stone carries over m-bit words (basic.py:98-136), consuming one tape
+// entry per level; returns the sum bits P0 ^ (G << 1).
+template <int L>
+__device__ __forceinline__ void d_carry_sum(u64 (&G)[L], u64 (&P)[L], const u64 (&P0)[L], int m, const Tape& tape,
+                                            int& ti, i64 e, int p0, Sh<L>& out) {
+  for (int s = 1; s < m; s *= 2) {
+    const MatRef& t = tape.m[ti++];
+    const bool last = 2 * s >= m;
+    const int W = m - s;
+    const int RW = last ? W : 2 * W;
+    const u64 hi = low_bits(m) & ~low_bits(s);
+    const i64 bit = t.off + e * (i64)RW;
+    u64 ag[L], bg[L], ap[L], bp[L];
+    u64 dg = 0, eg = 0, dp = 0, ep = 0;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      ag[l] = load_bits(t.p0 + l * t.ps0, bit, W) << s;
+      bg[l] = load_bits(t.p1 + l * t.ps1, bit, W) << s;
+      const u64 left = P[l] & hi;
+      dg ^= left ^ ag[l];
+      eg ^= ((G[l] << s) & hi) ^ bg[l];
+      if (!last) {
+        ap[l] = load_bits(t.p0 + l * t.ps0, bit + W, W) << s;
+        bp[l] = load_bits(t.p1 + l * t.ps1, bit + W, W) << s;
+        dp ^= left ^ ap[l];
+        ep ^= ((P[l] << s) & hi) ^ bp[l];
+      }
+    }
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      u64 zg = (load_bits(t.p2 + l * t.ps2, bit, W) << s) ^ (dg & bg[l]) ^ (eg & ag[l]);
+      if (l == p0) zg ^= dg & eg;
+      G[l] ^= zg;
+      if (!last) {
+        u64 zp = (load_bits(t.p2 + l * t.ps2, bit + W, W) << s) ^ (dp & bp[l]) ^ (ep & ap[l]);
+        if (l == p0) zp ^= dp & ep;
+        P[l] = (P[l] & low_bits(s)) | zp;
+      }
+    }
+  }
+#pragma unroll
+  for (int l = 0; l < L; ++l) out.v[l] = (P0[l] ^ (G[l] << 1)) & low_bits(m);
+}
+
+// bit decomposition (basic.py:199-214): edaBit(w, w) then the carry tree
+template <int L>
+__device__ __forceinline__ Sh<L> d_decompose(const Sh<L>& x, int w, const Tape& tape, int& ti, i64 e, int p0) {
+  const MatRef& t = tape.m[ti++];
+  const u64 msk = ring_mask(w);
+  u64 c = 0;
+  u64 rb[L];
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    c += x.v[l] - __ldcs(t.p0 + l * t.ps0 + e);
+    rb[l] = load_bits(t.p1 + l * t.ps1, t.off + e * (i64)w, w);
+  }
+  c &= msk;
+  u64 G[L], P[L], P0[L];
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    G[l] = rb[l] & c;
+    P[l] = (l == p0) ? (rb[l] ^ c) : rb[l];
+    P0[l] = P[l];
+  }
+  Sh<L> out;
+  d_carry_sum<L>(G, P, P0, w, tape, ti, e, p0, out);
+  return out;
+}
+
+// leftmost one (derived.py:131-149)
+template <int L>
+__device__ __forceinline__ Sh<L> d_lmo(const Sh<L>& bits, int m, const Tape& tape, int& ti, i64 e, int p0) {
+  u64 Y[L];
+#pragma unroll
+  for (int l = 0; l < L; ++l) Y[l] = bits.v[l];
+  for (int s = 1; s < m; s *= 2) {
+    const MatRef& t = tape.m[ti++];
+    const int W = m - s;
+    const u64 mw = low_bits(W);
+    const i64 bit = t.off + e * (i64)W;
+    u64 a[L], b[L];
+    u64 d = 0, f = 0;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      a[l] = load_bits(t.p0 + l * t.ps0, bit, W);
+      b[l] = load_bits(t.p1 + l * t.ps1, bit, W);
+      d ^= (Y[l] & mw) ^ a[l];
+      f ^= ((Y[l] >> s) & mw) ^ b[l];
+    }
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      u64 z = load_bits(t.p2 + l * t.ps2, bit, W) ^ (d & b[l]) ^ (f & a[l]);
+      if (l == p0) z ^= d & f;
+      const u64 lo = Y[l] & mw, hi = (Y[l] >> s) & mw;
+      Y[l] = (Y[l] & ~mw) | ((lo ^ hi ^ z) & mw);
+    }
+  }
+  Sh<L> o;
+#pragma unroll
+  for (int l = 0; l < L; ++l) o.v[l] = Y[l] ^ (Y[l] >> 1);
+  return o;
+}
+
+// bit2a opening of an m-bit row (basic.py:164-184): returns the opened c word
+template <int L>
+__device__ __forceinline__ u64 d_bit2a_open(const Sh<L>& b, int m, const MatRef& t, i64 e) {
+  u64 c = 0;
+#pragma unroll
+  for (int l = 0; l < L; ++l) c ^= b.v[l] ^ load_bits(t.p1 + l * t.ps1, t.off + e * (i64)m, m);
+  return c & low_bits(m);
+}
+
+// converted bit j of the row: r_arith * (1 - 2c_j) + [p0] c_j
+template <int L>
+__device__ __forceinline__ Sh<L> d_bit2a_get(u64 c, int j, int m, const MatRef& t, i64 e, int p0, u64 msk) {
+  const u64 cj = (c >> j) & 1ull;
+  Sh<L> z;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    u64 v = __ldcs(t.p0 + l * t.ps0 + e * (i64)m + j) * (1ull - 2ull * cj);
+    if (l == p0) v += cj;
+    z.v[l] = v & msk;
+  }
+  return z;
+}
+
+// polynomial at precision p (derived.py:86-108), coefficients pre-encoded
+template <int L>
+__device__ __forceinline__ Sh<L> d_poly4(const Sh<L>& x, const FusedParams& P, const Tape& tape, int& ti, i64 e,
+                                         u64 msk) {
+  Sh<L> pw[5];
+  pw[1] = x;
+  for (int i = 2; i <= 4; ++i) {
+    const MatRef& tm = tape.m[ti++];
+    Sh<L> prod = d_mul<L>(pw[i - 1], x, tm, e, P.p0, msk);
+    const MatRef& lo = tape.m[ti++];
+    const MatRef& hi = tape.m[ti++];
+    pw[i] = d_trunc<L>(prod, lo, &hi, e, P.p, true, P.w, P.p0, msk);
+  }
+  Sh<L> acc;
+#pragma unroll
+  for (int l = 0; l < L; ++l) acc.v[l] = 0;
+  for (int i = 1; i <= 4; ++i) {
+    if (!P.coef_nz[i]) continue;
+#pragma unroll
+    for (int l = 0; l < L; ++l) acc.v[l] += pw[i].v[l] * P.coef_p[i];
+  }
+#pragma unroll
+  for (int l = 0; l < L; ++l) acc.v[l] = (acc.v[l] + (l == P.p0 ? P.coef0_2p : 0ull)) & msk;
+  const MatRef& lo = tape.m[ti++];
+  const MatRef& hi = tape.m[ti++];
+  return d_trunc<L>(acc, lo, &hi, e, P.p, true, P.w, P.p0, msk);
+}
+
+template <int L>
+__device__ __forceinline__ Sh<L> load_sh(const u64* x, i64 n, i64 e) {
+  Sh<L> s;
+#pragma unroll
+  for (int l = 0; l < L; ++l) s.v[l] = __ldcs(x + l * n + e);
+  return s;
+}
+
+template <int L>
+__device__ __forceinline__ void store_sh(u64* y, i64 n, i64 e, const Sh<L>& s) {
+#pragma unroll
+  for (int l = 0; l < L; ++l) __stcs(y + l * n + e, s.v[l]);
+}
+
+// ---------------------------------------------------------------------------
+// Reciprocal, paper Alg. 1 (nonlinear.py:146-176)
+
+template <int L>
+__global__ void __launch_bounds__(128) k_reciprocal_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
+                                                          const __grid_constant__ Tape tape, FusedParams P) {
+  const int w = P.w, p = P.p, p0 = P.p0;
+  const u64 msk = ring_mask(w);
+  GRID_STRIDE(e, n) {
+    int ti = 0;
+    const Sh<L> x = load_sh<L>(xin, n, e);
+    const Sh<L> bits = d_decompose<L>(x, w, tape, ti, e, p0);
+    Sh<L> sign, mag;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      sign.v[l] = (bits.v[l] >> (w - 1)) & 1ull;
+      const u64 mm = low_bits(w - 1);
+      mag.v[l] = (bits.v[l] & mm) ^ (sign.v[l] ? mm : 0ull);
+    }
+    const MatRef& tsg = tape.m[ti++];
+    const u64 csg = d_bit2a_open<L>(sign, 1, tsg, e);
+    const Sh<L> s = d_bit2a_get<L>(csg, 0, 1, tsg, e, p0, msk);
+    const Sh<L> sx = d_mul<L>(s, x, tape.m[ti++], e, p0, msk);
+    const Sh<L> x_pos = sh_lin<L>(x, 1, sx, 0ull - 2ull, 0, p0, msk);
+    const Sh<L> onehot = d_lmo<L>(mag, w - 1, tape, ti, e, p0);
+    // reversed low 2p window -> compose (basic.py:187-196)
+    Sh<L> window;
+#pragma unroll
+    for (int l = 0; l < L; ++l) window.v[l] = __brevll(onehot.v[l] & low_bits(2 * p)) >> (64 - 2 * p);
+    const MatRef& tc = tape.m[ti++];
+    const u64 cw = d_bit2a_open<L>(window, 2 * p, tc, e);
+    Sh<L> t;
+#pragma unroll
+    for (int l = 0; l < L; ++l) t.v[l] = 0;
+    for (int j = 0; j < 2 * p; ++j) {
+      const Sh<L> zj = d_bit2a_get<L>(cw, j, 2 * p, tc, e, p0, msk);
+#pragma unroll
+      for (int l = 0; l < L; ++l) t.v[l] += zj.v[l] << j;
+    }
+#pragma unroll
+    for (int l = 0; l < L; ++l) t.v[l] &= msk;
+    Sh<L> z = d_mul<L>(t, x_pos, tape.m[ti], e, p0, msk);
+    z = d_trunc<L>(z, tape.m[ti + 1], &tape.m[ti + 2], e, p, true, w, p0, msk);
+    ti += 3;
+    // Newton product (nonlinear.py:134-143)
+    Sh<L> q = sh_scale<L>(z, 0ull - 1ull, P.one_p, p0, msk);
+    Sh<L> acc = sh_scale<L>(q, 1, P.one_p, p0, msk);
+    for (int it = 1; it < P.iters; ++it) {
+      q = d_mul<L>(q, q, tape.m[ti], e, p0, msk);
+      q = d_trunc<L>(q, tape.m[ti + 1], &tape.m[ti + 2], e, p, true, w, p0, msk);
+      ti += 3;
+      const Sh<L> q1 = sh_scale<L>(q, 1, P.one_p, p0, msk);
+      acc = d_mul<L>(acc, q1, tape.m[ti], e, p0, msk);
+      acc = d_trunc<L>(acc, tape.m[ti + 1], &tape.m[ti + 2], e, p, true, w, p0, msk);
+      ti += 3;
+    }
+    Sh<L> yv = d_mul<L>(t, acc, tape.m[ti], e, p0, msk);
+    yv = d_trunc<L>(yv, tape.m[ti + 1], &tape.m[ti + 2], e, p, true, w, p0, msk);
+    ti += 3;
+    const Sh<L> sy = d_mul<L>(s, yv, tape.m[ti++], e, p0, msk);
+    store_sh<L>(y, n, e, sh_lin<L>(yv, 1, sy, 0ull - 2ull, 0, p0, msk));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Exponentiation, paper Alg. 2 (nonlinear.py:179-213)
+
+template <int L>
+__global__ void __launch_bounds__(128) k_exp_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
+                                                   const __grid_constant__ Tape tape, FusedParams P) {
+  const int w = P.w, p = P.p, p0 = P.p0, c = P.c, bias = P.bias;
+  const u64 msk = ring_mask(w);
+  GRID_STRIDE(e, n) {
+    int ti = 0;
+    const Sh<L> x = load_sh<L>(xin, n, e);
+    const Sh<L> xb = sh_scale<L>(x, P.log2e_p, P.bias_2p, p0, msk);
+    const Sh<L> bits = d_decompose<L>(xb, w, tape, ti, e, p0);
+    const int k = p + c + 1;
+    Sh<L> seg;
+#pragma unroll
+    for (int l = 0; l < L; ++l)
+      seg.v[l] = ((bits.v[l] >> p) & low_bits(p + c)) | (((bits.v[l] >> (w - 1)) & 1ull) << (p + c));
+    const MatRef& tc = tape.m[ti++];
+    const u64 cw = d_bit2a_open<L>(seg, k, tc, e);
+    Sh<L> t;
+#pragma unroll
+    for (int l = 0; l < L; ++l) t.v[l] = 0;
+    for (int j = 0; j < p; ++j) {
+      const Sh<L> zj = d_bit2a_get<L>(cw, j, k, tc, e, p0, msk);
+#pragma unroll
+      for (int l = 0; l < L; ++l) t.v[l] += zj.v[l] << j;
+    }
+#pragma unroll
+    for (int l = 0; l < L; ++l) t.v[l] &= msk;
+    // 2^int as a product of (2^(2^i) b_i - b_i + 1) (nonlinear.py:125-131)
+    Sh<L> pw = sh_scale<L>(d_bit2a_get<L>(cw, p, k, tc, e, p0, msk), 1ull, 1ull, p0, msk);
+    for (int i = 1; i < c; ++i) {
+      const Sh<L> bi = d_bit2a_get<L>(cw, p + i, k, tc, e, p0, msk);
+      const u64 kf = (1ull << (1 << i)) - 1ull;
+      pw = d_mul<L>(pw, sh_scale<L>(bi, kf, 1ull, p0, msk), tape.m[ti++], e, p0, msk);
+    }
+    const Sh<L> sgn = d_bit2a_get<L>(cw, p + c, k, tc, e, p0, msk);
+    const Sh<L> poly = d_poly4<L>(t, P, tape, ti, e, msk);
+    const Sh<L> yv = d_mul<L>(pw, poly, tape.m[ti++], e, p0, msk);
+    const Sh<L> s1 = sh_scale<L>(sgn, 0ull - 1ull, 1ull, p0, msk);
+    Sh<L> out = d_mul<L>(s1, yv, tape.m[ti], e, p0, msk);
+    const MatRef* hi = (w - 1 - bias > 0) ? &tape.m[ti + 2] : nullptr;
+    out = d_trunc<L>(out, tape.m[ti + 1], hi, e, bias, true, w, p0, msk);
+    store_sh<L>(y, n, e, out);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Logarithm, paper Alg. 3 without the big-input pre-shift (nonlinear.py:216-267)
+
+template <int L>
+__global__ void __launch_bounds__(128) k_log_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
+                                                   const __grid_constant__ Tape tape, FusedParams P) {
+  const int w = P.w, p = P.p, p0 = P.p0;
+  const u64 msk = ring_mask(w);
+  const int m2 = 2 * p;
+  GRID_STRIDE(e, n) {
+    int ti = 0;
+    const Sh<L> x = load_sh<L>(xin, n, e);
+    const Sh<L> bits = d_decompose<L>(x, w, tape, ti, e, p0);
+    Sh<L> window;
+#pragma unroll
+    for (int l = 0; l < L; ++l) window.v[l] = bits.v[l] & low_bits(m2);
+    const Sh<L> onehot = d_lmo<L>(window, m2, tape, ti, e, p0);
+    // paired = AND(window, below) (basic.py:82-95), one bintriple per bit
+    const MatRef& ta = tape.m[ti++];
+    u64 a[L], b[L];
+    u64 d = 0, f = 0;
+    const i64 bit = ta.off + e * (i64)m2;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      a[l] = load_bits(ta.p0 + l * ta.ps0, bit, m2);
+      b[l] = load_bits(ta.p1 + l * ta.ps1, bit, m2);
+      const u64 below = onehot.v[l] >> 1;
+      d ^= window.v[l] ^ a[l];
+      f ^= below ^ b[l];
+    }
+    Sh<L> seg;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      u64 z = load_bits(ta.p2 + l * ta.ps2, bit, m2) ^ (d & b[l]) ^ (f & a[l]);
+      if (l == p0) z ^= d & f;
+      const u64 r_bit = (u64)(__popcll(z & low_bits(m2)) & 1);
+      seg.v[l] = (onehot.v[l] & low_bits(m2)) | (r_bit << m2);
+    }
+    const int k = m2 + 1;
+    const MatRef& tc = tape.m[ti++];
+    const u64 cw = d_bit2a_open<L>(seg, k, tc, e);
+    Sh<L> yl, mm;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      yl.v[l] = 0;
+      mm.v[l] = 0;
+    }
+    for (int j = 0; j < m2; ++j) {
+      const Sh<L> zj = d_bit2a_get<L>(cw, j, k, tc, e, p0, msk);
+      const u64 wl = (u64)(long long)(j - p);
+      const u64 wm = 1ull << (m2 - 1 - j);
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        yl.v[l] += zj.v[l] * wl;
+        mm.v[l] += zj.v[l] * wm;
+      }
+    }
+    const Sh<L> r = d_bit2a_get<L>(cw, m2, k, tc, e, p0, msk);
+    const Sh<L> xr = d_mul<L>(x, r, tape.m[ti++], e, p0, msk);
+    const Sh<L> doubled = sh_lin<L>(x, 2, xr, 0ull - 1ull, 0, p0, msk);
+    Sh<L> t = d_mul<L>(doubled, sh_scale<L>(mm, 1, 0, p0, msk), tape.m[ti], e, p0, msk);
+    t = d_trunc<L>(t, tape.m[ti + 1], &tape.m[ti + 2], e, p, true, w, p0, msk);
+    ti += 3;
+    t = sh_scale<L>(t, 1, P.m1_p, p0, msk);
+    const Sh<L> yr = d_poly4<L>(t, P, tape, ti, e, msk);
+    Sh<L> pre;
+#pragma unroll
+    for (int l = 0; l < L; ++l) pre.v[l] = (yr.v[l] + (yl.v[l] << p) + (r.v[l] << p)) & msk;
+    Sh<L> out = sh_scale<L>(pre, P.ln2_p, 0, p0, msk);
+    out = d_trunc<L>(out, tape.m[ti], &tape.m[ti + 1], e, p, true, w, p0, msk);
+    store_sh<L>(y, n, e, out);
+  }
+}
+
+// ---------------------------------------------------------------------------
+
+template <template <int> class KERN>
+struct Dispatch;
+
+#define DEFINE_LAUNCH(NAME, KFN)                                                                             \
+  extern "C" int NAME(uint64_t* y, const uint64_t* x, int64_t n, const void* tape_host,                    \
+                      const void* params_host, void* stream) {                                             \
+    CHECK_ARG(y && x && n >= 0 && tape_host && params_host);                                               \
+    const Tape& tp = *(const Tape*)tape_host;                                                              \
+    const FusedParams& P = *(const FusedParams*)params_host;                                               \
+    CHECK_ARG(tp.n >= 1 && tp.n <= TAPE_MAX && P.w >= 8 && P.w <= 64 && P.L >= 1 && P.L <= 4);            \
+    if (n == 0) return MPX_OK;                                                                             \
+    cudaStream_t s = (cudaStream_t)stream;                                                                 \
+    const unsigned g = grid_for(n, 128);                                                                   \
+    switch (P.L) {                                                                                         \
+      case 1: KFN<1><<<g, 128, 0, s>>>(y, x, n, tp, P); break;                                             \
+      case 2: KFN<2><<<g, 128, 0, s>>>(y, x, n, tp, P); break;                                             \
+      case 3: KFN<3><<<g, 128, 0, s>>>(y, x, n, tp, P); break;                                             \
+      default: KFN<4><<<g, 128, 0, s>>>(y, x, n, tp, P); break;                                            \
+    }                                                                                                      \
+    return launch_status();                                                                                \
+  }
+
+DEFINE_LAUNCH(mpx_reciprocal_fused, k_reciprocal_fused)
+DEFINE_LAUNCH(mpx_exp_fused, k_exp_fused)
+DEFINE_LAUNCH(mpx_log_fused, k_log_fused)
+
+extern "C" int mpx_fused_abi_sizes(int64_t* matref, int64_t* tape, int64_t* params, int64_t* tape_max) {
+  *matref = sizeof(MatRef);
+  *tape = sizeof(Tape);
+  *params = sizeof(FusedParams);
+  *tape_max = TAPE_MAX;
+  return MPX_OK;
+}

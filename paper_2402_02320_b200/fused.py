@@ -1,0 +1,175 @@
+"""Sim-mode whole-op fusion: record the material tape, launch one kernel.
+
+When all parties live on this GPU (``SimSession``) the openings of a
+non-linear function need no communication, so Exp / Log / Reciprocal run as
+ONE kernel (csrc/fused_ops.cu). The exact sequence of dealer-material takes
+is recorded by running the Python protocol once as a dry pass whose store
+forwards every ``take_*`` to the real store (advancing the real cursors, as
+the per-round path would) and logs the resulting views; the same pass
+records the op/communication ledger into the live session's metrics. The
+kernel then consumes the tape in order. Bit-exactness against the per-round
+path and the reference is covered by tests/test_gpu_parity.py and
+tests/test_fused_ops.py.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import torch
+
+from . import _lib
+from .preprocessing import ArithMat, BitMat, BitTriples
+from .ring import encode_scalar
+from .sharing import AShare
+
+TAPE_MAX = 64
+
+
+class MatRef(ctypes.Structure):
+    _fields_ = [("p0", ctypes.c_void_p), ("p1", ctypes.c_void_p), ("p2", ctypes.c_void_p),
+                ("ps0", ctypes.c_int64), ("ps1", ctypes.c_int64), ("ps2", ctypes.c_int64),
+                ("off", ctypes.c_int64)]
+
+
+class Tape(ctypes.Structure):
+    _fields_ = [("m", MatRef * TAPE_MAX), ("n", ctypes.c_int)]
+
+
+class FusedParams(ctypes.Structure):
+    _fields_ = [("w", ctypes.c_int), ("p", ctypes.c_int), ("iters", ctypes.c_int), ("bias", ctypes.c_int),
+                ("c", ctypes.c_int), ("L", ctypes.c_int), ("p0", ctypes.c_int),
+                ("log2e_p", ctypes.c_uint64), ("bias_2p", ctypes.c_uint64), ("one_p", ctypes.c_uint64),
+                ("m1_p", ctypes.c_uint64), ("ln2_p", ctypes.c_uint64), ("coef_p", ctypes.c_uint64 * 5),
+                ("coef0_2p", ctypes.c_uint64), ("coef_nz", ctypes.c_int * 5)]
+
+
+class TapeStore:
+    """Dry-run store that forwards takes to the real store and logs them."""
+
+    dry = True
+
+    def __init__(self, real):
+        self.real = real
+        self.parties = real.parties
+        self.n_parties = real.n_parties
+        self.tape: list[tuple] = []
+
+    @property
+    def L(self):
+        return len(self.parties)
+
+    def _m(self, *shape):
+        return torch.empty(shape, dtype=torch.int64, device="meta")
+
+    def take_triples(self, width, count):
+        a, b, c = self.real.take_triples(width, count)
+        self.tape.append((a.ptr, b.ptr, c.ptr, a.ps, b.ps, c.ps, 0))
+        return tuple(ArithMat(self._m(self.L, count)) for _ in range(3))
+
+    def take_bin_triples(self, count):
+        t = self.real.take_bin_triples(count)
+        self.tape.append((t.a_ptr, t.b_ptr, t.c_ptr, t.ps, t.ps, t.ps, t.bit))
+        z = self._m(self.L, 1)
+        return BitTriples(z, z, z, 0)
+
+    def take_dabits(self, width, count):
+        ra, rb = self.real.take_dabits(width, count)
+        self.tape.append((ra.ptr, rb.ptr, 0, ra.ps, rb.ps, 0, rb.bit))
+        return ArithMat(self._m(self.L, count)), BitMat(self._m(self.L, 1), 0)
+
+    def take_edabits(self, width, m, count, need_bits: bool = True):
+        ra, rb = self.real.take_edabits(width, m, count, need_bits)
+        self.tape.append((ra.ptr, rb.ptr if rb else 0, 0, ra.ps, rb.ps if rb else 0, 0, rb.bit if rb else 0))
+        return ArithMat(self._m(self.L, count)), (BitMat(self._m(self.L, 1), 0) if need_bits else None)
+
+    def take_matrix_triple(self, width, m, k, r):
+        raise NotImplementedError("matrix triples are not fused")
+
+
+_ENTRY = {"reciprocal": "mpx_reciprocal_fused", "exp": "mpx_exp_fused", "log": "mpx_log_fused"}
+_SIG_SET = False
+
+
+def _bind():
+    global _SIG_SET
+    lib = _lib.load()
+    if not _SIG_SET:
+        for nm in _ENTRY.values():
+            fn = getattr(lib, nm)
+            fn.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                           ctypes.c_void_p]
+            fn.restype = ctypes.c_int
+        lib.mpx_fused_abi_sizes.argtypes = [ctypes.POINTER(ctypes.c_int64)] * 4
+        sizes = [ctypes.c_int64() for _ in range(4)]
+        lib.mpx_fused_abi_sizes(*[ctypes.byref(s) for s in sizes])
+        want = (ctypes.sizeof(MatRef), ctypes.sizeof(Tape), ctypes.sizeof(FusedParams), TAPE_MAX)
+        if tuple(s.value for s in sizes) != want:
+            raise _lib.MpxError(f"fused ABI layout mismatch: C {[s.value for s in sizes]} vs ctypes {want}")
+        _SIG_SET = True
+    return lib
+
+
+def fusable(session, x: AShare) -> bool:
+    return (getattr(session, "fused", False) and getattr(session, "fuse_ops", True)
+            and x.width == 64 and 1 <= session.L <= 4 and 2 * x.frac <= 62 and x.size > 0)
+
+
+def params_for(kind: str, session, x: AShare, params) -> FusedParams:
+    w, p = x.width, x.frac
+    P = FusedParams()
+    P.w, P.p, P.L, P.p0 = w, p, session.L, session.p0
+    P.iters = params.newton_iters
+    coeffs = None
+    if kind == "exp":
+        P.bias = min(p, 38 - p)
+        P.c = max(1, (w - p - 1 - 1).bit_length())
+        P.log2e_p = encode_scalar(math.log2(math.e), w, p)
+        P.bias_2p = encode_scalar(float(P.bias), w, 2 * p)
+        coeffs = params.exp_coeffs
+    elif kind == "log":
+        P.m1_p = encode_scalar(-1.0, w, p)
+        P.ln2_p = encode_scalar(math.log(2.0), w, p)
+        coeffs = params.log_coeffs
+    P.one_p = encode_scalar(1.0, w, p)
+    if coeffs is not None:
+        if len(coeffs) != 5:
+            raise ValueError("fused kernels evaluate degree-4 polynomials")
+        for i in range(1, 5):
+            P.coef_p[i] = encode_scalar(coeffs[i], w, p)
+            P.coef_nz[i] = int(coeffs[i] != 0)
+        P.coef0_2p = encode_scalar(float(coeffs[0]), w, 2 * p)
+    return P
+
+
+def run_fused(kind: str, session, x: AShare, params, protocol) -> AShare | None:
+    """Record the tape with a dry pass of ``protocol`` and launch the fused
+    kernel. Returns None (caller falls back) if the tape does not fit."""
+    from .session import SimSession
+    lib = _bind()
+    store = TapeStore(session.store)
+    ts = SimSession(session.n_parties, store, metrics=session.metrics)
+    xm = AShare(torch.empty(x.values.shape, dtype=torch.int64, device="meta"), x.width, x.frac, x.parties)
+    ym = protocol(ts, xm)
+    if len(store.tape) > TAPE_MAX:
+        raise _lib.MpxError(f"{kind}: tape of {len(store.tape)} takes exceeds {TAPE_MAX}")
+    tape = Tape()
+    for i, ent in enumerate(store.tape):
+        tape.m[i] = MatRef(*ent)
+    tape.n = len(store.tape)
+    P = params_for(kind, session, x, params)
+    y = session.alloc(ym.values.shape)
+    xv = x.values.contiguous()
+    _lib.LAUNCHES += 1
+    if _lib.PROFILE is not None:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+    rc = getattr(lib, _ENTRY[kind])(y.data_ptr(), xv.data_ptr(), x.size, ctypes.addressof(tape),
+                                    ctypes.addressof(P), _lib.stream_ptr())
+    if _lib.PROFILE is not None:
+        ev1.record()
+        _lib.PROFILE.append((_ENTRY[kind], (x.size, session.L, tuple(store.tape)), ev0, ev1))
+    if rc != 0:
+        raise _lib.MpxError(f"{_ENTRY[kind]} returned {rc}")
+    return AShare(y, ym.width, ym.frac, session.parties)

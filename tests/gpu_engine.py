@@ -72,10 +72,11 @@ class GpuEngine:
             return v.values.cpu().numpy().view(np.uint64).copy()
         return v.bits.cpu().numpy().copy()
 
-    def run(self, fn, n, seed=11):
+    def run(self, fn, n, seed=11, fuse=True):
         counter = dry_run(lambda s: fn(self, s), n)
         store = device_store(seed, n, counter.demands, needs_bits=counter.needs_bits)
         sess = SimSession(n, store)
+        sess.fuse_ops = fuse
         out = fn(self, sess)
         torch.cuda.synchronize()
         res = {k: self.export(v) for k, v in out.items()}
