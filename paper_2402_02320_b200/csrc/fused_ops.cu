@@ -236,6 +236,40 @@ __device__ __forceinline__ Sh<L> d_bit2a_get(u64 c, int j, int m, const MatRef& 
   return z;
 }
 
+// Stream a whole converted row z_0..z_{m-1} (per party) through `f(l, j, z)`.
+// Each party's m daBit words are contiguous (items e*m .. e*m+m-1): read them
+// with back-to-back 16-byte L1-cached vector loads so every sector is used.
+template <int L, class F>
+__device__ __forceinline__ void d_bit2a_row(u64 c, int m, const MatRef& t, i64 e, int p0, u64 msk, F&& f) {
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    const u64* row = t.p0 + l * t.ps0 + e * (i64)m;
+    int j = 0;
+    auto emit = [&](int jj, u64 r) {
+      const u64 cj = (c >> jj) & 1ull;
+      u64 v = r * (1ull - 2ull * cj);
+      if (l == p0) v += cj;
+      f(l, jj, v & msk);
+    };
+    if (((uintptr_t)row & 15) != 0 && m > 0) {
+      emit(0, __ldg(row));
+      j = 1;
+    }
+    for (; j + 8 <= m; j += 8) {
+      const ulonglong2* r2 = reinterpret_cast<const ulonglong2*>(row + j);
+      const ulonglong2 v0 = __ldg(r2), v1 = __ldg(r2 + 1), v2 = __ldg(r2 + 2), v3 = __ldg(r2 + 3);
+      emit(j, v0.x); emit(j + 1, v0.y); emit(j + 2, v1.x); emit(j + 3, v1.y);
+      emit(j + 4, v2.x); emit(j + 5, v2.y); emit(j + 6, v3.x); emit(j + 7, v3.y);
+    }
+    for (; j + 2 <= m; j += 2) {
+      const ulonglong2 v0 = __ldg(reinterpret_cast<const ulonglong2*>(row + j));
+      emit(j, v0.x);
+      emit(j + 1, v0.y);
+    }
+    if (j < m) emit(j, __ldg(row + j));
+  }
+}
+
 // polynomial at precision p (derived.py:86-108), coefficients pre-encoded
 template <int L>
 __device__ __forceinline__ Sh<L> d_poly4(const Sh<L>& x, const FusedParams& P, const Tape& tape, int& ti, i64 e,
@@ -312,11 +346,7 @@ __global__ void __launch_bounds__(128) k_reciprocal_fused(u64* __restrict__ y, c
     Sh<L> t;
 #pragma unroll
     for (int l = 0; l < L; ++l) t.v[l] = 0;
-    for (int j = 0; j < 2 * p; ++j) {
-      const Sh<L> zj = d_bit2a_get<L>(cw, j, 2 * p, tc, e, p0, msk);
-#pragma unroll
-      for (int l = 0; l < L; ++l) t.v[l] += zj.v[l] << j;
-    }
+    d_bit2a_row<L>(cw, 2 * p, tc, e, p0, msk, [&](int l, int j, u64 z) { t.v[l] += z << j; });
 #pragma unroll
     for (int l = 0; l < L; ++l) t.v[l] &= msk;
     Sh<L> z = d_mul<L>(t, x_pos, tape.m[ti], e, p0, msk);
@@ -362,24 +392,27 @@ __global__ void __launch_bounds__(128) k_exp_fused(u64* __restrict__ y, const u6
       seg.v[l] = ((bits.v[l] >> p) & low_bits(p + c)) | (((bits.v[l] >> (w - 1)) & 1ull) << (p + c));
     const MatRef& tc = tape.m[ti++];
     const u64 cw = d_bit2a_open<L>(seg, k, tc, e);
-    Sh<L> t;
+    Sh<L> t, sgn;
+    Sh<L> ib[8];
 #pragma unroll
     for (int l = 0; l < L; ++l) t.v[l] = 0;
-    for (int j = 0; j < p; ++j) {
-      const Sh<L> zj = d_bit2a_get<L>(cw, j, k, tc, e, p0, msk);
+    d_bit2a_row<L>(cw, k, tc, e, p0, msk, [&](int l, int j, u64 z) {
+      if (j < p) t.v[l] += z << j;
+      else if (j < p + c) {
 #pragma unroll
-      for (int l = 0; l < L; ++l) t.v[l] += zj.v[l] << j;
-    }
+        for (int i = 0; i < 8; ++i)
+          if (j - p == i) ib[i].v[l] = z;
+      }
+      else sgn.v[l] = z;
+    });
 #pragma unroll
     for (int l = 0; l < L; ++l) t.v[l] &= msk;
     // 2^int as a product of (2^(2^i) b_i - b_i + 1) (nonlinear.py:125-131)
-    Sh<L> pw = sh_scale<L>(d_bit2a_get<L>(cw, p, k, tc, e, p0, msk), 1ull, 1ull, p0, msk);
+    Sh<L> pw = sh_scale<L>(ib[0], 1ull, 1ull, p0, msk);
     for (int i = 1; i < c; ++i) {
-      const Sh<L> bi = d_bit2a_get<L>(cw, p + i, k, tc, e, p0, msk);
       const u64 kf = (1ull << (1 << i)) - 1ull;
-      pw = d_mul<L>(pw, sh_scale<L>(bi, kf, 1ull, p0, msk), tape.m[ti++], e, p0, msk);
+      pw = d_mul<L>(pw, sh_scale<L>(ib[i], kf, 1ull, p0, msk), tape.m[ti++], e, p0, msk);
     }
-    const Sh<L> sgn = d_bit2a_get<L>(cw, p + c, k, tc, e, p0, msk);
     const Sh<L> poly = d_poly4<L>(t, P, tape, ti, e, msk);
     const Sh<L> yv = d_mul<L>(pw, poly, tape.m[ti++], e, p0, msk);
     const Sh<L> s1 = sh_scale<L>(sgn, 0ull - 1ull, 1ull, p0, msk);
@@ -431,23 +464,20 @@ __global__ void __launch_bounds__(128) k_log_fused(u64* __restrict__ y, const u6
     const int k = m2 + 1;
     const MatRef& tc = tape.m[ti++];
     const u64 cw = d_bit2a_open<L>(seg, k, tc, e);
-    Sh<L> yl, mm;
+    Sh<L> yl, mm, r;
 #pragma unroll
     for (int l = 0; l < L; ++l) {
       yl.v[l] = 0;
       mm.v[l] = 0;
     }
-    for (int j = 0; j < m2; ++j) {
-      const Sh<L> zj = d_bit2a_get<L>(cw, j, k, tc, e, p0, msk);
-      const u64 wl = (u64)(long long)(j - p);
-      const u64 wm = 1ull << (m2 - 1 - j);
-#pragma unroll
-      for (int l = 0; l < L; ++l) {
-        yl.v[l] += zj.v[l] * wl;
-        mm.v[l] += zj.v[l] * wm;
+    d_bit2a_row<L>(cw, k, tc, e, p0, msk, [&](int l, int j, u64 z) {
+      if (j < m2) {
+        yl.v[l] += z * (u64)(long long)(j - p);
+        mm.v[l] += z << (m2 - 1 - j);
+      } else {
+        r.v[l] = z;
       }
-    }
-    const Sh<L> r = d_bit2a_get<L>(cw, m2, k, tc, e, p0, msk);
+    });
     const Sh<L> xr = d_mul<L>(x, r, tape.m[ti++], e, p0, msk);
     const Sh<L> doubled = sh_lin<L>(x, 2, xr, 0ull - 1ull, 0, p0, msk);
     Sh<L> t = d_mul<L>(doubled, sh_scale<L>(mm, 1, 0, p0, msk), tape.m[ti], e, p0, msk);

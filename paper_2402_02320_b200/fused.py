@@ -45,6 +45,23 @@ class FusedParams(ctypes.Structure):
                 ("coef0_2p", ctypes.c_uint64), ("coef_nz", ctypes.c_int * 5)]
 
 
+def _take_ref(store, method: str, args: tuple) -> tuple:
+    """Perform one take on the real store; return its MatRef fields."""
+    if method == "take_triples":
+        a, b, c = store.take_triples(*args)
+        return (a.ptr, b.ptr, c.ptr, a.ps, b.ps, c.ps, 0)
+    if method == "take_bin_triples":
+        t = store.take_bin_triples(*args)
+        return (t.a_ptr, t.b_ptr, t.c_ptr, t.ps, t.ps, t.ps, t.bit)
+    if method == "take_dabits":
+        ra, rb = store.take_dabits(*args)
+        return (ra.ptr, rb.ptr, 0, ra.ps, rb.ps, 0, rb.bit)
+    if method == "take_edabits":
+        ra, rb = store.take_edabits(*args)
+        return (ra.ptr, rb.ptr if rb else 0, 0, ra.ps, rb.ps if rb else 0, 0, rb.bit if rb else 0)
+    raise NotImplementedError(f"{method} is not fused")
+
+
 class TapeStore:
     """Dry-run store that forwards takes to the real store and logs them."""
 
@@ -55,6 +72,7 @@ class TapeStore:
         self.parties = real.parties
         self.n_parties = real.n_parties
         self.tape: list[tuple] = []
+        self.calls: list[tuple] = []
 
     @property
     def L(self):
@@ -63,29 +81,50 @@ class TapeStore:
     def _m(self, *shape):
         return torch.empty(shape, dtype=torch.int64, device="meta")
 
+    def _rec(self, method, args):
+        self.calls.append((method, args))
+        self.tape.append(_take_ref(self.real, method, args))
+
     def take_triples(self, width, count):
-        a, b, c = self.real.take_triples(width, count)
-        self.tape.append((a.ptr, b.ptr, c.ptr, a.ps, b.ps, c.ps, 0))
+        self._rec("take_triples", (width, count))
         return tuple(ArithMat(self._m(self.L, count)) for _ in range(3))
 
     def take_bin_triples(self, count):
-        t = self.real.take_bin_triples(count)
-        self.tape.append((t.a_ptr, t.b_ptr, t.c_ptr, t.ps, t.ps, t.ps, t.bit))
+        self._rec("take_bin_triples", (count,))
         z = self._m(self.L, 1)
         return BitTriples(z, z, z, 0)
 
     def take_dabits(self, width, count):
-        ra, rb = self.real.take_dabits(width, count)
-        self.tape.append((ra.ptr, rb.ptr, 0, ra.ps, rb.ps, 0, rb.bit))
+        self._rec("take_dabits", (width, count))
         return ArithMat(self._m(self.L, count)), BitMat(self._m(self.L, 1), 0)
 
     def take_edabits(self, width, m, count, need_bits: bool = True):
-        ra, rb = self.real.take_edabits(width, m, count, need_bits)
-        self.tape.append((ra.ptr, rb.ptr if rb else 0, 0, ra.ps, rb.ps if rb else 0, 0, rb.bit if rb else 0))
+        self._rec("take_edabits", (width, m, count, need_bits))
         return ArithMat(self._m(self.L, count)), (BitMat(self._m(self.L, 1), 0) if need_bits else None)
 
     def take_matrix_triple(self, width, m, k, r):
         raise NotImplementedError("matrix triples are not fused")
+
+
+def _merge_metrics(dst, src) -> None:
+    """Add a scoped ledger recorded from an empty scope stack under dst's
+    current scope path."""
+    from .metrics import OpCounters
+    prefix = "/".join(dst._stack)
+    for key, e in src.ledger.items():
+        full = (prefix or "(root)") if key == "(root)" else (f"{prefix}/{key}" if prefix else key)
+        entry = dst.ledger.get(full)
+        if entry is None:
+            entry = dst.ledger[full] = OpCounters()
+        entry.add(e)
+    dst.total.add(src.total)
+    for peer, b in src.bytes_per_peer.items():
+        dst.bytes_per_peer[peer] += b
+    dst.physical_bytes += src.physical_bytes
+
+
+# (kind, shape, width, frac, params, L, n, p0) -> (take calls, ledger, out width, out frac)
+_SCHEDULES: dict = {}
 
 
 _ENTRY = {"reciprocal": "mpx_reciprocal_fused", "exp": "mpx_exp_fused", "log": "mpx_log_fused"}
@@ -143,23 +182,40 @@ def params_for(kind: str, session, x: AShare, params) -> FusedParams:
     return P
 
 
-def run_fused(kind: str, session, x: AShare, params, protocol) -> AShare | None:
-    """Record the tape with a dry pass of ``protocol`` and launch the fused
-    kernel. Returns None (caller falls back) if the tape does not fit."""
+def run_fused(kind: str, session, x: AShare, params, protocol) -> AShare:
+    """Launch the fused kernel for ``protocol`` on ``x``.
+
+    The first call for a (kind, shape, params, party layout) records the
+    schedule of material takes and the ledger with a dry pass of the Python
+    protocol over the real store; later calls replay the takes on the store
+    (same cursors as the per-round path) and merge the cached ledger.
+    """
+    from .metrics import CommMetrics
     from .session import SimSession
     lib = _bind()
-    store = TapeStore(session.store)
-    ts = SimSession(session.n_parties, store, metrics=session.metrics)
-    xm = AShare(torch.empty(x.values.shape, dtype=torch.int64, device="meta"), x.width, x.frac, x.parties)
-    ym = protocol(ts, xm)
-    if len(store.tape) > TAPE_MAX:
-        raise _lib.MpxError(f"{kind}: tape of {len(store.tape)} takes exceeds {TAPE_MAX}")
+    key = (kind, x.shape, x.width, x.frac, params, session.L, session.n_parties, session.p0)
+    sched = _SCHEDULES.get(key)
+    if sched is None:
+        store = TapeStore(session.store)
+        tmp = CommMetrics(session.metrics.party, session.n_parties)
+        ts = SimSession(session.n_parties, store, metrics=tmp)
+        xm = AShare(torch.empty(x.values.shape, dtype=torch.int64, device="meta"), x.width, x.frac, x.parties)
+        ym = protocol(ts, xm)
+        if len(store.tape) > TAPE_MAX:
+            raise _lib.MpxError(f"{kind}: tape of {len(store.tape)} takes exceeds {TAPE_MAX}")
+        sched = (tuple(store.calls), tmp, ym.width, ym.frac)
+        _SCHEDULES[key] = sched
+        entries = store.tape
+    else:
+        entries = [_take_ref(session.store, m, a) for m, a in sched[0]]
+    calls, ledger, out_w, out_f = sched
+    _merge_metrics(session.metrics, ledger)
     tape = Tape()
-    for i, ent in enumerate(store.tape):
+    for i, ent in enumerate(entries):
         tape.m[i] = MatRef(*ent)
-    tape.n = len(store.tape)
+    tape.n = len(entries)
     P = params_for(kind, session, x, params)
-    y = session.alloc(ym.values.shape)
+    y = session.alloc(x.values.shape)
     xv = x.values.contiguous()
     _lib.LAUNCHES += 1
     if _lib.PROFILE is not None:
@@ -169,7 +225,7 @@ def run_fused(kind: str, session, x: AShare, params, protocol) -> AShare | None:
                                     ctypes.addressof(P), _lib.stream_ptr())
     if _lib.PROFILE is not None:
         ev1.record()
-        _lib.PROFILE.append((_ENTRY[kind], (x.size, session.L, tuple(store.tape)), ev0, ev1))
+        _lib.PROFILE.append((_ENTRY[kind], (kind, x.size, session.L, tuple(entries)), ev0, ev1))
     if rc != 0:
         raise _lib.MpxError(f"{_ENTRY[kind]} returned {rc}")
-    return AShare(y, ym.width, ym.frac, session.parties)
+    return AShare(y, out_w, out_f, session.parties)
