@@ -229,7 +229,7 @@ __device__ __forceinline__ Sh<L> d_bit2a_get(u64 c, int j, int m, const MatRef& 
   Sh<L> z;
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    u64 v = __ldcs(t.p0 + l * t.ps0 + e * (i64)m + j) * (1ull - 2ull * cj);
+    u64 v = __ldg(t.p0 + l * t.ps0 + e * (i64)m + j) * (1ull - 2ull * cj);
     if (l == p0) v += cj;
     z.v[l] = v & msk;
   }
@@ -392,27 +392,21 @@ __global__ void __launch_bounds__(128) k_exp_fused(u64* __restrict__ y, const u6
       seg.v[l] = ((bits.v[l] >> p) & low_bits(p + c)) | (((bits.v[l] >> (w - 1)) & 1ull) << (p + c));
     const MatRef& tc = tape.m[ti++];
     const u64 cw = d_bit2a_open<L>(seg, k, tc, e);
-    Sh<L> t, sgn;
-    Sh<L> ib[8];
+    Sh<L> t;
 #pragma unroll
     for (int l = 0; l < L; ++l) t.v[l] = 0;
-    d_bit2a_row<L>(cw, k, tc, e, p0, msk, [&](int l, int j, u64 z) {
-      if (j < p) t.v[l] += z << j;
-      else if (j < p + c) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          if (j - p == i) ib[i].v[l] = z;
-      }
-      else sgn.v[l] = z;
-    });
+    // fraction window: first p converted bits, streamed; the row stays in L1
+    d_bit2a_row<L>(cw, p, tc, e, p0, msk, [&](int l, int j, u64 z) { t.v[l] += z << j; });
 #pragma unroll
     for (int l = 0; l < L; ++l) t.v[l] &= msk;
     // 2^int as a product of (2^(2^i) b_i - b_i + 1) (nonlinear.py:125-131)
-    Sh<L> pw = sh_scale<L>(ib[0], 1ull, 1ull, p0, msk);
+    Sh<L> pw = sh_scale<L>(d_bit2a_get<L>(cw, p, k, tc, e, p0, msk), 1ull, 1ull, p0, msk);
     for (int i = 1; i < c; ++i) {
+      const Sh<L> bi = d_bit2a_get<L>(cw, p + i, k, tc, e, p0, msk);
       const u64 kf = (1ull << (1 << i)) - 1ull;
-      pw = d_mul<L>(pw, sh_scale<L>(ib[i], kf, 1ull, p0, msk), tape.m[ti++], e, p0, msk);
+      pw = d_mul<L>(pw, sh_scale<L>(bi, kf, 1ull, p0, msk), tape.m[ti++], e, p0, msk);
     }
+    const Sh<L> sgn = d_bit2a_get<L>(cw, p + c, k, tc, e, p0, msk);
     const Sh<L> poly = d_poly4<L>(t, P, tape, ti, e, msk);
     const Sh<L> yv = d_mul<L>(pw, poly, tape.m[ti++], e, p0, msk);
     const Sh<L> s1 = sh_scale<L>(sgn, 0ull - 1ull, 1ull, p0, msk);
