@@ -240,10 +240,11 @@ __device__ __forceinline__ Sh<L> d_bit2a_get(u64 c, int j, int m, const MatRef& 
 // Each party's m daBit words are contiguous (items e*m .. e*m+m-1): read them
 // with back-to-back 16-byte L1-cached vector loads so every sector is used.
 template <int L, class F>
-__device__ __forceinline__ void d_bit2a_row(u64 c, int m, const MatRef& t, i64 e, int p0, u64 msk, F&& f) {
+__device__ __forceinline__ void d_bit2a_row(u64 c, int m, int stride, const MatRef& t, i64 e, int p0, u64 msk,
+                                            F&& f) {
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    const u64* row = t.p0 + l * t.ps0 + e * (i64)m;
+    const u64* row = t.p0 + l * t.ps0 + e * (i64)stride;
     int j = 0;
     auto emit = [&](int jj, u64 r) {
       const u64 cj = (c >> jj) & 1ull;
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(128) k_reciprocal_fused(u64* __restrict__ y, c
     Sh<L> t;
 #pragma unroll
     for (int l = 0; l < L; ++l) t.v[l] = 0;
-    d_bit2a_row<L>(cw, 2 * p, tc, e, p0, msk, [&](int l, int j, u64 z) { t.v[l] += z << j; });
+    d_bit2a_row<L>(cw, 2 * p, 2 * p, tc, e, p0, msk, [&](int l, int j, u64 z) { t.v[l] += z << j; });
 #pragma unroll
     for (int l = 0; l < L; ++l) t.v[l] &= msk;
     Sh<L> z = d_mul<L>(t, x_pos, tape.m[ti], e, p0, msk);
@@ -396,7 +397,7 @@ __global__ void __launch_bounds__(128) k_exp_fused(u64* __restrict__ y, const u6
 #pragma unroll
     for (int l = 0; l < L; ++l) t.v[l] = 0;
     // fraction window: first p converted bits, streamed; the row stays in L1
-    d_bit2a_row<L>(cw, p, tc, e, p0, msk, [&](int l, int j, u64 z) { t.v[l] += z << j; });
+    d_bit2a_row<L>(cw, p, k, tc, e, p0, msk, [&](int l, int j, u64 z) { t.v[l] += z << j; });
 #pragma unroll
     for (int l = 0; l < L; ++l) t.v[l] &= msk;
     // 2^int as a product of (2^(2^i) b_i - b_i + 1) (nonlinear.py:125-131)
@@ -464,7 +465,7 @@ __global__ void __launch_bounds__(128) k_log_fused(u64* __restrict__ y, const u6
       yl.v[l] = 0;
       mm.v[l] = 0;
     }
-    d_bit2a_row<L>(cw, k, tc, e, p0, msk, [&](int l, int j, u64 z) {
+    d_bit2a_row<L>(cw, k, k, tc, e, p0, msk, [&](int l, int j, u64 z) {
       if (j < m2) {
         yl.v[l] += z * (u64)(long long)(j - p);
         mm.v[l] += z << (m2 - 1 - j);
