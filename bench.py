@@ -206,6 +206,10 @@ def alg_bytes(name, a):
             return L * rows * cols * 8 + L * rows * 8
         if name == "mpx_bits_gather":
             return 16 * a[4]
+        if name in ("mpx_reciprocal_fused", "mpx_exp_fused", "mpx_log_fused"):
+            from paper_2402_02320_b200.fused import material_bytes
+            kind, n, L, calls = a
+            return material_bytes(calls, L) + 2 * 8 * L * n   # material + x in + y out
     except (IndexError, TypeError):
         return None
     return None

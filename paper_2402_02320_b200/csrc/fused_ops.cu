@@ -21,12 +21,58 @@ struct MatRef {
   const u64* p2;  // triple c | bintriple c
   i64 ps0, ps1, ps2;
   i64 off;        // bit offset of the cursor (bit material)
+  int kind;       // 0: arithmetic triple, 1: bit triple, 2: daBit/edaBit
+  int per0;       // items per element in p0 (words; bits for kind 1)
+  int per1;       // bits per element in p1 (kind 2)
+  int pad;
 };
 
 struct Tape {
   MatRef m[TAPE_MAX];
   int n;
 };
+
+#ifndef MPX_PREFETCH_DIST
+#define MPX_PREFETCH_DIST 3
+#endif
+
+__device__ __forceinline__ void pf_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+// Pull take `t`'s slice for element e towards L2 (no registers held).
+template <int L>
+__device__ __forceinline__ void prefetch_take(const MatRef& t, i64 e) {
+  if (t.kind == 0) {
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      pf_l2(t.p0 + l * t.ps0 + e);
+      pf_l2(t.p1 + l * t.ps1 + e);
+      pf_l2(t.p2 + l * t.ps2 + e);
+    }
+  } else if (t.kind == 1) {
+    const i64 w = (t.off + e * (i64)t.per0) >> 6;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      pf_l2(t.p0 + l * t.ps0 + w);
+      pf_l2(t.p1 + l * t.ps1 + w);
+      pf_l2(t.p2 + l * t.ps2 + w);
+    }
+  } else {
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      const u64* row = t.p0 + l * t.ps0 + e * (i64)t.per0;
+      for (int q = 0; q < t.per0; q += 16) pf_l2(row + q);
+      if (t.p1) pf_l2(t.p1 + l * t.ps1 + ((t.off + e * (i64)t.per1) >> 6));
+    }
+  }
+}
+
+// Consume the next tape entry, prefetching the one MPX_PREFETCH_DIST ahead.
+template <int L>
+__device__ __forceinline__ const MatRef& next_take(const Tape& tape, int& ti, i64 e) {
+  const int ahead = ti + MPX_PREFETCH_DIST;
+  if (ahead < tape.n) prefetch_take<L>(tape.m[ahead], e);
+  return tape.m[ti++];
+}
 
 struct FusedParams {
   int w, p, iters, bias, c;
@@ -84,6 +130,23 @@ __device__ __forceinline__ Sh<L> d_mul(const Sh<L>& x, const Sh<L>& y, const Mat
   return z;
 }
 
+template <int L>
+__device__ __forceinline__ Sh<L> d_mul(const Sh<L>& x, const Sh<L>& y, const MatRef& t, i64 e, int p0, u64 msk);
+template <int L>
+__device__ __forceinline__ Sh<L> d_trunc(const Sh<L>& x, const MatRef& lo, const MatRef* hi, i64 e, int f,
+                                         bool sgn, int w, int p0, u64 msk);
+
+// truncate(mul(x, y), f) consuming triple, edaBit(w, f), edaBit(w, w-1-f) in order
+template <int L>
+__device__ __forceinline__ Sh<L> d_mul_trunc(const Sh<L>& x, const Sh<L>& y, const Tape& tape, int& ti, i64 e,
+                                             int f, int w, int p0, u64 msk) {
+  const MatRef& tm = next_take<L>(tape, ti, e);
+  const Sh<L> z = d_mul<L>(x, y, tm, e, p0, msk);
+  const MatRef& lo = next_take<L>(tape, ti, e);
+  const MatRef* hi = (w - 1 - f > 0) ? &next_take<L>(tape, ti, e) : nullptr;
+  return d_trunc<L>(z, lo, hi, e, f, true, w, p0, msk);
+}
+
 // probabilistic truncation (derived.py:20-70); lo/hi = edaBit(w, f), edaBit(w, w-1-f)
 template <int L>
 __device__ __forceinline__ Sh<L> d_trunc(const Sh<L>& x, const MatRef& lo, const MatRef* hi, i64 e, int f,
@@ -116,7 +179,7 @@ template <int L>
 __device__ __forceinline__ void d_carry_sum(u64 (&G)[L], u64 (&P)[L], const u64 (&P0)[L], int m, const Tape& tape,
                                             int& ti, i64 e, int p0, Sh<L>& out) {
   for (int s = 1; s < m; s *= 2) {
-    const MatRef& t = tape.m[ti++];
+    const MatRef& t = next_take<L>(tape, ti, e);
     const bool last = 2 * s >= m;
     const int W = m - s;
     const int RW = last ? W : 2 * W;
@@ -157,7 +220,7 @@ __device__ __forceinline__ void d_carry_sum(u64 (&G)[L], u64 (&P)[L], const u64 
 // bit decomposition (basic.py:199-214): edaBit(w, w) then the carry tree
 template <int L>
 __device__ __forceinline__ Sh<L> d_decompose(const Sh<L>& x, int w, const Tape& tape, int& ti, i64 e, int p0) {
-  const MatRef& t = tape.m[ti++];
+  const MatRef& t = next_take<L>(tape, ti, e);
   const u64 msk = ring_mask(w);
   u64 c = 0;
   u64 rb[L];
@@ -186,7 +249,7 @@ __device__ __forceinline__ Sh<L> d_lmo(const Sh<L>& bits, int m, const Tape& tap
 #pragma unroll
   for (int l = 0; l < L; ++l) Y[l] = bits.v[l];
   for (int s = 1; s < m; s *= 2) {
-    const MatRef& t = tape.m[ti++];
+    const MatRef& t = next_take<L>(tape, ti, e);
     const int W = m - s;
     const u64 mw = low_bits(W);
     const i64 bit = t.off + e * (i64)W;
@@ -277,16 +340,14 @@ __device__ __forceinline__ Sh<L> d_poly4(const Sh<L>& x, const FusedParams& P, c
                                          u64 msk) {
   Sh<L> pw[5];
   pw[1] = x;
+#pragma unroll
   for (int i = 2; i <= 4; ++i) {
-    const MatRef& tm = tape.m[ti++];
-    Sh<L> prod = d_mul<L>(pw[i - 1], x, tm, e, P.p0, msk);
-    const MatRef& lo = tape.m[ti++];
-    const MatRef& hi = tape.m[ti++];
-    pw[i] = d_trunc<L>(prod, lo, &hi, e, P.p, true, P.w, P.p0, msk);
+    pw[i] = d_mul_trunc<L>(pw[i - 1], x, tape, ti, e, P.p, P.w, P.p0, msk);
   }
   Sh<L> acc;
 #pragma unroll
   for (int l = 0; l < L; ++l) acc.v[l] = 0;
+#pragma unroll
   for (int i = 1; i <= 4; ++i) {
     if (!P.coef_nz[i]) continue;
 #pragma unroll
@@ -294,8 +355,8 @@ __device__ __forceinline__ Sh<L> d_poly4(const Sh<L>& x, const FusedParams& P, c
   }
 #pragma unroll
   for (int l = 0; l < L; ++l) acc.v[l] = (acc.v[l] + (l == P.p0 ? P.coef0_2p : 0ull)) & msk;
-  const MatRef& lo = tape.m[ti++];
-  const MatRef& hi = tape.m[ti++];
+  const MatRef& lo = next_take<L>(tape, ti, e);
+  const MatRef& hi = next_take<L>(tape, ti, e);
   return d_trunc<L>(acc, lo, &hi, e, P.p, true, P.w, P.p0, msk);
 }
 
@@ -332,17 +393,17 @@ __global__ void __launch_bounds__(128) k_reciprocal_fused(u64* __restrict__ y, c
       const u64 mm = low_bits(w - 1);
       mag.v[l] = (bits.v[l] & mm) ^ (sign.v[l] ? mm : 0ull);
     }
-    const MatRef& tsg = tape.m[ti++];
+    const MatRef& tsg = next_take<L>(tape, ti, e);
     const u64 csg = d_bit2a_open<L>(sign, 1, tsg, e);
     const Sh<L> s = d_bit2a_get<L>(csg, 0, 1, tsg, e, p0, msk);
-    const Sh<L> sx = d_mul<L>(s, x, tape.m[ti++], e, p0, msk);
+    const Sh<L> sx = d_mul<L>(s, x, next_take<L>(tape, ti, e), e, p0, msk);
     const Sh<L> x_pos = sh_lin<L>(x, 1, sx, 0ull - 2ull, 0, p0, msk);
     const Sh<L> onehot = d_lmo<L>(mag, w - 1, tape, ti, e, p0);
     // reversed low 2p window -> compose (basic.py:187-196)
     Sh<L> window;
 #pragma unroll
     for (int l = 0; l < L; ++l) window.v[l] = __brevll(onehot.v[l] & low_bits(2 * p)) >> (64 - 2 * p);
-    const MatRef& tc = tape.m[ti++];
+    const MatRef& tc = next_take<L>(tape, ti, e);
     const u64 cw = d_bit2a_open<L>(window, 2 * p, tc, e);
     Sh<L> t;
 #pragma unroll
@@ -350,25 +411,17 @@ __global__ void __launch_bounds__(128) k_reciprocal_fused(u64* __restrict__ y, c
     d_bit2a_row<L>(cw, 2 * p, 2 * p, tc, e, p0, msk, [&](int l, int j, u64 z) { t.v[l] += z << j; });
 #pragma unroll
     for (int l = 0; l < L; ++l) t.v[l] &= msk;
-    Sh<L> z = d_mul<L>(t, x_pos, tape.m[ti], e, p0, msk);
-    z = d_trunc<L>(z, tape.m[ti + 1], &tape.m[ti + 2], e, p, true, w, p0, msk);
-    ti += 3;
+    const Sh<L> z = d_mul_trunc<L>(t, x_pos, tape, ti, e, p, w, p0, msk);
     // Newton product (nonlinear.py:134-143)
     Sh<L> q = sh_scale<L>(z, 0ull - 1ull, P.one_p, p0, msk);
     Sh<L> acc = sh_scale<L>(q, 1, P.one_p, p0, msk);
     for (int it = 1; it < P.iters; ++it) {
-      q = d_mul<L>(q, q, tape.m[ti], e, p0, msk);
-      q = d_trunc<L>(q, tape.m[ti + 1], &tape.m[ti + 2], e, p, true, w, p0, msk);
-      ti += 3;
+      q = d_mul_trunc<L>(q, q, tape, ti, e, p, w, p0, msk);
       const Sh<L> q1 = sh_scale<L>(q, 1, P.one_p, p0, msk);
-      acc = d_mul<L>(acc, q1, tape.m[ti], e, p0, msk);
-      acc = d_trunc<L>(acc, tape.m[ti + 1], &tape.m[ti + 2], e, p, true, w, p0, msk);
-      ti += 3;
+      acc = d_mul_trunc<L>(acc, q1, tape, ti, e, p, w, p0, msk);
     }
-    Sh<L> yv = d_mul<L>(t, acc, tape.m[ti], e, p0, msk);
-    yv = d_trunc<L>(yv, tape.m[ti + 1], &tape.m[ti + 2], e, p, true, w, p0, msk);
-    ti += 3;
-    const Sh<L> sy = d_mul<L>(s, yv, tape.m[ti++], e, p0, msk);
+    const Sh<L> yv = d_mul_trunc<L>(t, acc, tape, ti, e, p, w, p0, msk);
+    const Sh<L> sy = d_mul<L>(s, yv, next_take<L>(tape, ti, e), e, p0, msk);
     store_sh<L>(y, n, e, sh_lin<L>(yv, 1, sy, 0ull - 2ull, 0, p0, msk));
   }
 }
@@ -391,7 +444,7 @@ __global__ void __launch_bounds__(128) k_exp_fused(u64* __restrict__ y, const u6
 #pragma unroll
     for (int l = 0; l < L; ++l)
       seg.v[l] = ((bits.v[l] >> p) & low_bits(p + c)) | (((bits.v[l] >> (w - 1)) & 1ull) << (p + c));
-    const MatRef& tc = tape.m[ti++];
+    const MatRef& tc = next_take<L>(tape, ti, e);
     const u64 cw = d_bit2a_open<L>(seg, k, tc, e);
     Sh<L> t;
 #pragma unroll
@@ -405,15 +458,13 @@ __global__ void __launch_bounds__(128) k_exp_fused(u64* __restrict__ y, const u6
     for (int i = 1; i < c; ++i) {
       const Sh<L> bi = d_bit2a_get<L>(cw, p + i, k, tc, e, p0, msk);
       const u64 kf = (1ull << (1 << i)) - 1ull;
-      pw = d_mul<L>(pw, sh_scale<L>(bi, kf, 1ull, p0, msk), tape.m[ti++], e, p0, msk);
+      pw = d_mul<L>(pw, sh_scale<L>(bi, kf, 1ull, p0, msk), next_take<L>(tape, ti, e), e, p0, msk);
     }
     const Sh<L> sgn = d_bit2a_get<L>(cw, p + c, k, tc, e, p0, msk);
     const Sh<L> poly = d_poly4<L>(t, P, tape, ti, e, msk);
-    const Sh<L> yv = d_mul<L>(pw, poly, tape.m[ti++], e, p0, msk);
+    const Sh<L> yv = d_mul<L>(pw, poly, next_take<L>(tape, ti, e), e, p0, msk);
     const Sh<L> s1 = sh_scale<L>(sgn, 0ull - 1ull, 1ull, p0, msk);
-    Sh<L> out = d_mul<L>(s1, yv, tape.m[ti], e, p0, msk);
-    const MatRef* hi = (w - 1 - bias > 0) ? &tape.m[ti + 2] : nullptr;
-    out = d_trunc<L>(out, tape.m[ti + 1], hi, e, bias, true, w, p0, msk);
+    const Sh<L> out = d_mul_trunc<L>(s1, yv, tape, ti, e, bias, w, p0, msk);
     store_sh<L>(y, n, e, out);
   }
 }
@@ -436,7 +487,7 @@ __global__ void __launch_bounds__(128) k_log_fused(u64* __restrict__ y, const u6
     for (int l = 0; l < L; ++l) window.v[l] = bits.v[l] & low_bits(m2);
     const Sh<L> onehot = d_lmo<L>(window, m2, tape, ti, e, p0);
     // paired = AND(window, below) (basic.py:82-95), one bintriple per bit
-    const MatRef& ta = tape.m[ti++];
+    const MatRef& ta = next_take<L>(tape, ti, e);
     u64 a[L], b[L];
     u64 d = 0, f = 0;
     const i64 bit = ta.off + e * (i64)m2;
@@ -457,7 +508,7 @@ __global__ void __launch_bounds__(128) k_log_fused(u64* __restrict__ y, const u6
       seg.v[l] = (onehot.v[l] & low_bits(m2)) | (r_bit << m2);
     }
     const int k = m2 + 1;
-    const MatRef& tc = tape.m[ti++];
+    const MatRef& tc = next_take<L>(tape, ti, e);
     const u64 cw = d_bit2a_open<L>(seg, k, tc, e);
     Sh<L> yl, mm, r;
 #pragma unroll
@@ -473,18 +524,20 @@ __global__ void __launch_bounds__(128) k_log_fused(u64* __restrict__ y, const u6
         r.v[l] = z;
       }
     });
-    const Sh<L> xr = d_mul<L>(x, r, tape.m[ti++], e, p0, msk);
+    const Sh<L> xr = d_mul<L>(x, r, next_take<L>(tape, ti, e), e, p0, msk);
     const Sh<L> doubled = sh_lin<L>(x, 2, xr, 0ull - 1ull, 0, p0, msk);
-    Sh<L> t = d_mul<L>(doubled, sh_scale<L>(mm, 1, 0, p0, msk), tape.m[ti], e, p0, msk);
-    t = d_trunc<L>(t, tape.m[ti + 1], &tape.m[ti + 2], e, p, true, w, p0, msk);
-    ti += 3;
+    Sh<L> t = d_mul_trunc<L>(doubled, sh_scale<L>(mm, 1, 0, p0, msk), tape, ti, e, p, w, p0, msk);
     t = sh_scale<L>(t, 1, P.m1_p, p0, msk);
     const Sh<L> yr = d_poly4<L>(t, P, tape, ti, e, msk);
     Sh<L> pre;
 #pragma unroll
     for (int l = 0; l < L; ++l) pre.v[l] = (yr.v[l] + (yl.v[l] << p) + (r.v[l] << p)) & msk;
     Sh<L> out = sh_scale<L>(pre, P.ln2_p, 0, p0, msk);
-    out = d_trunc<L>(out, tape.m[ti], &tape.m[ti + 1], e, p, true, w, p0, msk);
+    {
+      const MatRef& lo = next_take<L>(tape, ti, e);
+      const MatRef& hi = next_take<L>(tape, ti, e);
+      out = d_trunc<L>(out, lo, &hi, e, p, true, w, p0, msk);
+    }
     store_sh<L>(y, n, e, out);
   }
 }

@@ -30,7 +30,8 @@ TAPE_MAX = 64
 class MatRef(ctypes.Structure):
     _fields_ = [("p0", ctypes.c_void_p), ("p1", ctypes.c_void_p), ("p2", ctypes.c_void_p),
                 ("ps0", ctypes.c_int64), ("ps1", ctypes.c_int64), ("ps2", ctypes.c_int64),
-                ("off", ctypes.c_int64)]
+                ("off", ctypes.c_int64), ("kind", ctypes.c_int), ("per0", ctypes.c_int),
+                ("per1", ctypes.c_int), ("pad", ctypes.c_int)]
 
 
 class Tape(ctypes.Structure):
@@ -45,20 +46,24 @@ class FusedParams(ctypes.Structure):
                 ("coef0_2p", ctypes.c_uint64), ("coef_nz", ctypes.c_int * 5)]
 
 
-def _take_ref(store, method: str, args: tuple) -> tuple:
-    """Perform one take on the real store; return its MatRef fields."""
+def _take_ref(store, method: str, args: tuple, n: int) -> tuple:
+    """Perform one take on the real store; return its MatRef fields (``n`` =
+    elements of the fused op, so per-element strides are count // n)."""
     if method == "take_triples":
         a, b, c = store.take_triples(*args)
-        return (a.ptr, b.ptr, c.ptr, a.ps, b.ps, c.ps, 0)
+        return (a.ptr, b.ptr, c.ptr, a.ps, b.ps, c.ps, 0, 0, args[1] // n, 0, 0)
     if method == "take_bin_triples":
         t = store.take_bin_triples(*args)
-        return (t.a_ptr, t.b_ptr, t.c_ptr, t.ps, t.ps, t.ps, t.bit)
+        return (t.a_ptr, t.b_ptr, t.c_ptr, t.ps, t.ps, t.ps, t.bit, 1, args[0] // n, 0, 0)
     if method == "take_dabits":
         ra, rb = store.take_dabits(*args)
-        return (ra.ptr, rb.ptr, 0, ra.ps, rb.ps, 0, rb.bit)
+        per = args[1] // n
+        return (ra.ptr, rb.ptr, 0, ra.ps, rb.ps, 0, rb.bit, 2, per, per, 0)
     if method == "take_edabits":
         ra, rb = store.take_edabits(*args)
-        return (ra.ptr, rb.ptr if rb else 0, 0, ra.ps, rb.ps if rb else 0, 0, rb.bit if rb else 0)
+        per = args[2] // n
+        return (ra.ptr, rb.ptr if rb else 0, 0, ra.ps, rb.ps if rb else 0, 0, rb.bit if rb else 0, 2, per,
+                per * args[1] if rb else 0, 0)
     raise NotImplementedError(f"{method} is not fused")
 
 
@@ -67,8 +72,9 @@ class TapeStore:
 
     dry = True
 
-    def __init__(self, real):
+    def __init__(self, real, n: int):
         self.real = real
+        self.n = n
         self.parties = real.parties
         self.n_parties = real.n_parties
         self.tape: list[tuple] = []
@@ -83,7 +89,7 @@ class TapeStore:
 
     def _rec(self, method, args):
         self.calls.append((method, args))
-        self.tape.append(_take_ref(self.real, method, args))
+        self.tape.append(_take_ref(self.real, method, args, self.n))
 
     def take_triples(self, width, count):
         self._rec("take_triples", (width, count))
@@ -150,6 +156,21 @@ def _bind():
     return lib
 
 
+def material_bytes(calls, L: int) -> int:
+    """Dealer bytes a fused op must read for one call (all L local parties)."""
+    tot = 0
+    for method, args in calls:
+        if method == "take_triples":
+            tot += 3 * 8 * args[1]
+        elif method == "take_bin_triples":
+            tot += 3 * args[0] / 8
+        elif method == "take_dabits":
+            tot += 8 * args[1] + args[1] / 8
+        elif method == "take_edabits":
+            tot += 8 * args[2] + (args[2] * args[1] / 8 if args[3] else 0)
+    return int(tot * L)
+
+
 def fusable(session, x: AShare) -> bool:
     return (getattr(session, "fused", False) and getattr(session, "fuse_ops", True)
             and x.width == 64 and 1 <= session.L <= 4 and 2 * x.frac <= 62 and x.size > 0)
@@ -196,7 +217,7 @@ def run_fused(kind: str, session, x: AShare, params, protocol) -> AShare:
     key = (kind, x.shape, x.width, x.frac, params, session.L, session.n_parties, session.p0)
     sched = _SCHEDULES.get(key)
     if sched is None:
-        store = TapeStore(session.store)
+        store = TapeStore(session.store, x.size)
         tmp = CommMetrics(session.metrics.party, session.n_parties)
         ts = SimSession(session.n_parties, store, metrics=tmp)
         xm = AShare(torch.empty(x.values.shape, dtype=torch.int64, device="meta"), x.width, x.frac, x.parties)
@@ -207,7 +228,7 @@ def run_fused(kind: str, session, x: AShare, params, protocol) -> AShare:
         _SCHEDULES[key] = sched
         entries = store.tape
     else:
-        entries = [_take_ref(session.store, m, a) for m, a in sched[0]]
+        entries = [_take_ref(session.store, m, a, x.size) for m, a in sched[0]]
     calls, ledger, out_w, out_f = sched
     _merge_metrics(session.metrics, ledger)
     tape = Tape()
@@ -225,7 +246,7 @@ def run_fused(kind: str, session, x: AShare, params, protocol) -> AShare:
                                     ctypes.addressof(P), _lib.stream_ptr())
     if _lib.PROFILE is not None:
         ev1.record()
-        _lib.PROFILE.append((_ENTRY[kind], (kind, x.size, session.L, tuple(entries)), ev0, ev1))
+        _lib.PROFILE.append((_ENTRY[kind], (kind, x.size, session.L, calls), ev0, ev1))
     if rc != 0:
         raise _lib.MpxError(f"{_ENTRY[kind]} returned {rc}")
     return AShare(y, out_w, out_f, session.parties)
