@@ -33,7 +33,7 @@ struct Tape {
 };
 
 #ifndef MPX_PREFETCH_DIST
-#define MPX_PREFETCH_DIST 3
+#define MPX_PREFETCH_DIST 0
 #endif
 
 __device__ __forceinline__ void pf_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
@@ -69,8 +69,10 @@ __device__ __forceinline__ void prefetch_take(const MatRef& t, i64 e) {
 // Consume the next tape entry, prefetching the one MPX_PREFETCH_DIST ahead.
 template <int L>
 __device__ __forceinline__ const MatRef& next_take(const Tape& tape, int& ti, i64 e) {
-  const int ahead = ti + MPX_PREFETCH_DIST;
-  if (ahead < tape.n) prefetch_take<L>(tape.m[ahead], e);
+  if (MPX_PREFETCH_DIST > 0) {
+    const int ahead = ti + MPX_PREFETCH_DIST;
+    if (ahead < tape.n) prefetch_take<L>(tape.m[ahead], e);
+  }
   return tape.m[ti++];
 }
 
@@ -334,30 +336,110 @@ __device__ __forceinline__ void d_bit2a_row(u64 c, int m, int stride, const MatR
   }
 }
 
+// Material of one truncate(mul(x, y), f) step: triple + edaBit(w,f) + edaBit(w,w-1-f).
+// Loads are independent of data, so chains of these steps are software
+// pipelined: step k+1's material is loaded while step k computes.
+template <int L>
+struct MTM {
+  u64 a[L], b[L], c[L], lo[L], hi[L];
+};
+
+template <int L>
+__device__ __forceinline__ void mt_load(MTM<L>& m, const Tape& tape, int& ti, i64 e, int f, int w) {
+  const MatRef& tm = next_take<L>(tape, ti, e);
+  const MatRef& lo = next_take<L>(tape, ti, e);
+  const bool has_hi = w - 1 - f > 0;
+  const MatRef* hi = has_hi ? &next_take<L>(tape, ti, e) : nullptr;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    m.a[l] = __ldcs(tm.p0 + l * tm.ps0 + e);
+    m.b[l] = __ldcs(tm.p1 + l * tm.ps1 + e);
+    m.c[l] = __ldcs(tm.p2 + l * tm.ps2 + e);
+    m.lo[l] = __ldcs(lo.p0 + l * lo.ps0 + e);
+    m.hi[l] = hi ? __ldcs(hi->p0 + l * hi->ps0 + e) : 0ull;
+  }
+}
+
+template <int L>
+__device__ __forceinline__ Sh<L> mt_compute(const Sh<L>& x, const Sh<L>& y, const MTM<L>& m, int f, int w, int p0,
+                                            u64 msk) {
+  u64 d = 0, g = 0;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    d += x.v[l] - m.a[l];
+    g += y.v[l] - m.b[l];
+  }
+  const u64 bias = 1ull << (w - 2), unbias = 1ull << (w - 2 - f);
+  u64 z[L];
+  u64 s = 0;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    u64 v = m.c[l] + d * m.b[l] + g * m.a[l];
+    if (l == p0) v += d * g;
+    z[l] = v & msk;
+    u64 t = z[l] + m.lo[l] + (m.hi[l] << f);
+    if (l == p0) t += bias;
+    s += t;
+  }
+  const u64 chi = (s & msk) >> f;
+  Sh<L> o;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    u64 v = 0ull - m.hi[l];
+    if (l == p0) v += chi - unbias;
+    o.v[l] = v & msk;
+  }
+  return o;
+}
+
 // polynomial at precision p (derived.py:86-108), coefficients pre-encoded
 template <int L>
 __device__ __forceinline__ Sh<L> d_poly4(const Sh<L>& x, const FusedParams& P, const Tape& tape, int& ti, i64 e,
                                          u64 msk) {
-  Sh<L> pw[5];
-  pw[1] = x;
+  // powers x^2..x^4: three pipelined mul+trunc steps, then the final truncation
+  MTM<L> A, B;
+  mt_load<L>(A, tape, ti, e, P.p, P.w);
+  mt_load<L>(B, tape, ti, e, P.p, P.w);
+  const Sh<L> x2 = mt_compute<L>(x, x, A, P.p, P.w, P.p0, msk);
+  mt_load<L>(A, tape, ti, e, P.p, P.w);
+  const Sh<L> x3 = mt_compute<L>(x2, x, B, P.p, P.w, P.p0, msk);
+  // final truncation's edaBits (no triple)
+  const MatRef& flo = next_take<L>(tape, ti, e);
+  const MatRef& fhi = next_take<L>(tape, ti, e);
+  u64 rlo[L], rhi[L];
 #pragma unroll
-  for (int i = 2; i <= 4; ++i) {
-    pw[i] = d_mul_trunc<L>(pw[i - 1], x, tape, ti, e, P.p, P.w, P.p0, msk);
+  for (int l = 0; l < L; ++l) {
+    rlo[l] = __ldcs(flo.p0 + l * flo.ps0 + e);
+    rhi[l] = __ldcs(fhi.p0 + l * fhi.ps0 + e);
   }
-  Sh<L> acc;
+  const Sh<L> x4 = mt_compute<L>(x3, x, A, P.p, P.w, P.p0, msk);
+  const Sh<L>* pw[5] = {nullptr, &x, &x2, &x3, &x4};
+  u64 acc[L];
 #pragma unroll
-  for (int l = 0; l < L; ++l) acc.v[l] = 0;
+  for (int l = 0; l < L; ++l) acc[l] = 0;
 #pragma unroll
   for (int i = 1; i <= 4; ++i) {
     if (!P.coef_nz[i]) continue;
 #pragma unroll
-    for (int l = 0; l < L; ++l) acc.v[l] += pw[i].v[l] * P.coef_p[i];
+    for (int l = 0; l < L; ++l) acc[l] += pw[i]->v[l] * P.coef_p[i];
   }
+  const u64 bias = 1ull << (P.w - 2), unbias = 1ull << (P.w - 2 - P.p);
+  u64 s = 0;
 #pragma unroll
-  for (int l = 0; l < L; ++l) acc.v[l] = (acc.v[l] + (l == P.p0 ? P.coef0_2p : 0ull)) & msk;
-  const MatRef& lo = next_take<L>(tape, ti, e);
-  const MatRef& hi = next_take<L>(tape, ti, e);
-  return d_trunc<L>(acc, lo, &hi, e, P.p, true, P.w, P.p0, msk);
+  for (int l = 0; l < L; ++l) {
+    u64 v = ((acc[l] + (l == P.p0 ? P.coef0_2p : 0ull)) & msk) + rlo[l] + (rhi[l] << P.p);
+    if (l == P.p0) v += bias;
+    s += v;
+  }
+  const u64 chi = (s & msk) >> P.p;
+  Sh<L> o;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    u64 v = 0ull - rhi[l];
+    if (l == P.p0) v += chi - unbias;
+    o.v[l] = v & msk;
+  }
+  return o;
 }
 
 template <int L>
@@ -411,16 +493,21 @@ __global__ void __launch_bounds__(128) k_reciprocal_fused(u64* __restrict__ y, c
     d_bit2a_row<L>(cw, 2 * p, 2 * p, tc, e, p0, msk, [&](int l, int j, u64 z) { t.v[l] += z << j; });
 #pragma unroll
     for (int l = 0; l < L; ++l) t.v[l] &= msk;
-    const Sh<L> z = d_mul_trunc<L>(t, x_pos, tape, ti, e, p, w, p0, msk);
-    // Newton product (nonlinear.py:134-143)
+    // z = trunc(t * x_pos), Newton product (nonlinear.py:134-143), y = trunc(t * acc):
+    // a chain of 2*iters mul+trunc steps, pipelined one step ahead (A/B)
+    MTM<L> A, B;
+    mt_load<L>(A, tape, ti, e, p, w);
+    mt_load<L>(B, tape, ti, e, p, w);
+    const Sh<L> z = mt_compute<L>(t, x_pos, A, p, w, p0, msk);
     Sh<L> q = sh_scale<L>(z, 0ull - 1ull, P.one_p, p0, msk);
     Sh<L> acc = sh_scale<L>(q, 1, P.one_p, p0, msk);
     for (int it = 1; it < P.iters; ++it) {
-      q = d_mul_trunc<L>(q, q, tape, ti, e, p, w, p0, msk);
-      const Sh<L> q1 = sh_scale<L>(q, 1, P.one_p, p0, msk);
-      acc = d_mul_trunc<L>(acc, q1, tape, ti, e, p, w, p0, msk);
+      mt_load<L>(A, tape, ti, e, p, w);
+      q = mt_compute<L>(q, q, B, p, w, p0, msk);
+      mt_load<L>(B, tape, ti, e, p, w);
+      acc = mt_compute<L>(acc, sh_scale<L>(q, 1, P.one_p, p0, msk), A, p, w, p0, msk);
     }
-    const Sh<L> yv = d_mul_trunc<L>(t, acc, tape, ti, e, p, w, p0, msk);
+    const Sh<L> yv = mt_compute<L>(t, acc, B, p, w, p0, msk);
     const Sh<L> sy = d_mul<L>(s, yv, next_take<L>(tape, ti, e), e, p0, msk);
     store_sh<L>(y, n, e, sh_lin<L>(yv, 1, sy, 0ull - 2ull, 0, p0, msk));
   }
