@@ -318,7 +318,39 @@ def sweep_entry(torch, G, make_session, parties, n_parties, dev, name, steps=2, 
 # B200 arm
 
 
-def run_b200(args):
+class DistGroup:
+    """torch.distributed over NCCL: one rank per GPU (torchrun)."""
+
+    def __init__(self, torch, dist):
+        self.torch, self.dist = torch, dist
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    def init(self, dev):
+        if self.world > 1:
+            self.dist.init_process_group("nccl", device_id=dev)
+
+    def comm(self):
+        return None            # PartySession default: DistComm over the NCCL group
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, v: float, dev) -> float:
+        if self.world == 1:
+            return v
+        t = self.torch.tensor([v], device=dev, dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+def run_b200(args, group=None):
     import torch
     import torch.distributed as dist
 
@@ -326,10 +358,10 @@ def run_b200(args):
     from paper_2402_02320_b200 import _lib
     from paper_2402_02320_b200.preprocessing import DemandCounter, device_store
     from paper_2402_02320_b200.session import PartySession, SimSession
+    from paper_2402_02320_b200.streaming import run_host
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    group = group or DistGroup(torch, dist)
+    world, rank, local = group.world, group.rank, group.local
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         # before CUDA initialisation: the pool forks numpy-only workers
@@ -341,8 +373,7 @@ def run_b200(args):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    group.init(dev)
     n_parties = 2 if world == 1 else world
     parties = tuple(range(n_parties)) if world == 1 else (rank,)
     N = args.elems
@@ -353,7 +384,10 @@ def run_b200(args):
     def make_session(store):
         if world == 1:
             return SimSession(n_parties, store, device=dev)
-        return PartySession(rank, n_parties, None, store, device=dev)
+        return PartySession(rank, n_parties, group.comm(), store, device=dev)
+
+    def barrier():
+        group.barrier()
 
     # dry run (meta tensors): exact demand
     counter = DemandCounter(parties, n_parties)
@@ -367,10 +401,6 @@ def run_b200(args):
                           needs_bits=counter.needs_bits)
         torch.cuda.synchronize()
         return st, time.perf_counter() - t0
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
 
     # input shares (device) + pinned host copies for the e2e leg
     s0 = make_session(None)
@@ -406,11 +436,7 @@ def run_b200(args):
             launches_timed += _lib.LAUNCHES - l0
             t_window[1] = time.time()
     clk = clocks.stop(t_window)
-    total_ms = float(sum(online_ms))
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = group.max(float(sum(online_ms)), dev)
     ms_per_step = total_ms / args.steps
     value = N * args.steps / (total_ms / 1e3)
 
@@ -463,7 +489,8 @@ def run_b200(args):
                    "GBps": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1) if v["bytes_known"] and v["ms"] else None}
                for k, v in sorted(per.items(), key=lambda kv: -kv[1]["ms"])}
 
-    # e2e through the public API with host buffers: H2D shares -> reciprocal -> D2H
+    # e2e through the public API with host buffers: streaming.run_host overlaps
+    # H2D of chunk k+1, the secure op on chunk k and D2H of chunk k-1
     e2e_ms = []
     store = None
     y_host = torch.empty(x_host.shape, dtype=torch.int64).pin_memory()
@@ -475,19 +502,13 @@ def run_b200(args):
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
-        xv = x_host.to(dev, non_blocking=True)
-        yy = G.reciprocal(sess, G.AShare(xv, WIDTH, FRAC, parties))
-        y_host.copy_(yy.values, non_blocking=True)
+        run_host(lambda s, x: G.reciprocal(s, x), sess, x_host, WIDTH, FRAC, chunks=args.chunks, y_host=y_host)
         ev1.record()
         torch.cuda.synchronize()
         barrier()
         if step >= args.warmup:
             e2e_ms.append(ev0.elapsed_time(ev1))
-    e2e_total = float(sum(e2e_ms))
-    if world > 1:
-        t = torch.tensor([e2e_total], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_total = float(t.item())
+    e2e_total = group.max(float(sum(e2e_ms)), dev)
     h2d = int(x_host.numel() * 8)
     d2h = int(y_host.numel() * 8)
 
@@ -518,7 +539,9 @@ def run_b200(args):
                        "dealer": "fresh on-device material before every step, outside the timed region"},
             "e2e": {"value": N * args.steps / (e2e_total / 1e3), "unit": UNIT,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": e2e_total / args.steps},
+                    "ms_per_step": e2e_total / args.steps,
+                    "how": f"streaming.run_host: pinned host shares, {args.chunks} chunks, H2D/compute/D2H "
+                           "overlapped on 3 CUDA streams, one protocol call per chunk"},
             "gpu_launches": launches_timed,
             "clocks": clk,
             "roofline": roofline,
@@ -531,8 +554,7 @@ def run_b200(args):
             "sweep": sweep,
         }
         print(json.dumps(line))
-    if world > 1:
-        dist.destroy_process_group()
+    group.close()
 
 
 def run_reference(args):
@@ -572,6 +594,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=1 << 20)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--chunks", type=int, default=8)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
