@@ -289,15 +289,14 @@ def sweep_entry(torch, G, make_session, parties, n_parties, dev, name, steps=2, 
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if step == warmup + steps - 1:
-            _lib.PROFILE = []
+            _lib.profile_begin()
         e0.record()
         op(sess, x, y)
         e1.record()
         torch.cuda.synchronize()
-        if _lib.PROFILE is not None:
-            for nm, _a, p0, p1 in _lib.PROFILE:
+        if _lib.profiling() is not None:
+            for nm, _a, p0, p1 in _lib.profile_end():
                 prof_ms[nm] = prof_ms.get(nm, 0.0) + p0.elapsed_time(p1)
-            _lib.PROFILE = None
         if step >= warmup:
             times.append(e0.elapsed_time(e1))
     del store
@@ -450,11 +449,10 @@ def run_b200(args, group=None):
     store, _ = deal(10_000)
     sess = make_session(store)
     torch.cuda.synchronize()
-    _lib.PROFILE = []
+    _lib.profile_begin()
     G.reciprocal(sess, x_sh)
     torch.cuda.synchronize()
-    prof = _lib.PROFILE
-    _lib.PROFILE = None
+    prof = _lib.profile_end()
     per = {}
     for name, a, e0, e1 in prof:
         d = per.setdefault(name, {"ms": 0.0, "n": 0, "bytes": 0, "bytes_known": True})

@@ -120,9 +120,26 @@ def ptr(t) -> int | None:
 
 
 # Launch accounting for the benchmark harness: LAUNCHES counts libmpx entry
-# calls; when PROFILE is a list, each call is bracketed by CUDA events.
+# calls; between profile_begin() and profile_end() every call of the calling
+# thread is bracketed by CUDA events on its stream.
+import threading
+
 LAUNCHES = 0
-PROFILE = None
+_TLS = threading.local()
+
+
+def profile_begin() -> None:
+    _TLS.prof = []
+
+
+def profile_end() -> list:
+    out = getattr(_TLS, "prof", None) or []
+    _TLS.prof = None
+    return out
+
+
+def profiling() -> list | None:
+    return getattr(_TLS, "prof", None)
 
 
 def call(name: str, *args) -> None:
@@ -130,13 +147,14 @@ def call(name: str, *args) -> None:
     global LAUNCHES
     lib = load()
     LAUNCHES += 1
-    if PROFILE is not None:
+    prof = getattr(_TLS, "prof", None)
+    if prof is not None:
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record()
         rc = getattr(lib, name)(*args, stream_ptr())
         ev1.record()
-        PROFILE.append((name, args, ev0, ev1))
+        prof.append((name, args, ev0, ev1))
     else:
         rc = getattr(lib, name)(*args, stream_ptr())
     if rc != 0:

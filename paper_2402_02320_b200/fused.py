@@ -239,14 +239,15 @@ def run_fused(kind: str, session, x: AShare, params, protocol) -> AShare:
     y = session.alloc(x.values.shape)
     xv = x.values.contiguous()
     _lib.LAUNCHES += 1
-    if _lib.PROFILE is not None:
+    prof = _lib.profiling()
+    if prof is not None:
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
     rc = getattr(lib, _ENTRY[kind])(y.data_ptr(), xv.data_ptr(), x.size, ctypes.addressof(tape),
                                     ctypes.addressof(P), _lib.stream_ptr())
-    if _lib.PROFILE is not None:
+    if prof is not None:
         ev1.record()
-        _lib.PROFILE.append((_ENTRY[kind], (kind, x.size, session.L, calls), ev0, ev1))
+        prof.append((_ENTRY[kind], (kind, x.size, session.L, calls), ev0, ev1))
     if rc != 0:
         raise _lib.MpxError(f"{_ENTRY[kind]} returned {rc}")
     return AShare(y, out_w, out_f, session.parties)
