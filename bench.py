@@ -551,8 +551,8 @@ def run_b200(args, group=None):
             "cpu_baseline": cpu,
             "sweep": sweep,
         }
-        print(json.dumps(line))
     group.close()
+    return line if rank == 0 else None
 
 
 def run_reference(args):
@@ -597,7 +597,9 @@ def main():
     if args.impl == "reference":
         run_reference(args)
     else:
-        run_b200(args)
+        line = run_b200(args)
+        if line is not None:
+            print(json.dumps(line))
 
 
 if __name__ == "__main__":

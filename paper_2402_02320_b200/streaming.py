@@ -14,6 +14,17 @@ import torch
 
 from .sharing import AShare
 
+_STREAMS: dict = {}
+
+
+def _streams(dev):
+    """Three long-lived side streams per device (the caching allocator keeps
+    per-stream pools, so fresh streams per call would force cudaMalloc)."""
+    key = torch.device(dev).index
+    if key not in _STREAMS:
+        _STREAMS[key] = tuple(torch.cuda.Stream(dev) for _ in range(3))
+    return _STREAMS[key]
+
 
 def run_host(op, session, x_host: torch.Tensor, width: int, frac: int, chunks: int = 8,
              y_host: torch.Tensor | None = None) -> torch.Tensor:
@@ -24,7 +35,7 @@ def run_host(op, session, x_host: torch.Tensor, width: int, frac: int, chunks: i
         y_host = torch.empty_like(x_host).pin_memory()
     chunks = max(1, min(chunks, N))
     bounds = [N * k // chunks for k in range(chunks + 1)]
-    h2d, comp, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    h2d, comp, d2h = _streams(dev)
     main = torch.cuda.current_stream(dev)
     h2d.wait_stream(main)
     comp.wait_stream(main)
