@@ -24,11 +24,12 @@
 #define TC_BM 128
 #define TC_BN 64
 #define TC_BK 128
-#define TC_ASTAGES 4
+#define TC_ASTAGES 6
 #define TC_BSTAGES 2
 #define TC_A_TILE (TC_BM * TC_BK)          // 16 KB
 #define TC_B_TILE (TC_BN * TC_BK)          // 8 KB
 #define TC_B_STAGE (8 * TC_B_TILE)         // 64 KB
+#define TC_GROUP_M 16
 #define TC_SMEM_BYTES (TC_ASTAGES * TC_A_TILE + TC_BSTAGES * TC_B_STAGE + 1024 + 256)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -132,8 +133,17 @@ __global__ void __launch_bounds__(192, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * TC_BM;
-  const int n0 = blockIdx.x * TC_BN;
+  // grouped rasterization: consecutive CTAs walk TC_GROUP_M row tiles of one
+  // column band, so a wave shares both A and B k-slabs through L2
+  const int tiles_m = args.Mpad / TC_BM, tiles_n = args.Npad / TC_BN;
+  const int lin = blockIdx.x;
+  const int per_group = TC_GROUP_M * tiles_n;
+  const int g = lin / per_group;
+  const int first_m = g * TC_GROUP_M;
+  const int gm = min(TC_GROUP_M, tiles_m - first_m);
+  const int in_g = lin - g * per_group;
+  const int m0 = (first_m + in_g % gm) * TC_BM;
+  const int n0 = (in_g / gm) * TC_BN;
   const int z = blockIdx.z;
 
   if (threadIdx.x == 0) {
@@ -415,7 +425,7 @@ extern "C" int mpx_gemm_limbs(uint64_t* C, const uint8_t* A8, const uint8_t* B8,
   a.nk = (int)(Kpad / TC_BK);
   a.accumulate = accumulate;
   a.msk = ring_mask(width);
-  dim3 grid((unsigned)(Npad / TC_BN), (unsigned)(Mpad / TC_BM), (unsigned)batch);
+  dim3 grid((unsigned)((Npad / TC_BN) * (Mpad / TC_BM)), 1, (unsigned)batch);
   k_gemm_limbs_tc<<<grid, 192, TC_SMEM_BYTES, (cudaStream_t)stream>>>(mapA, mapB, a);
   return launch_status();
 }
