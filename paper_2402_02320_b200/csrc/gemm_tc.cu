@@ -198,7 +198,11 @@ __global__ void __launch_bounds__(192, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
+      // Descriptors are precomputed: the start address is the low field, so
+      // advancing within shared memory is a plain add of (bytes >> 4).
       const uint32_t idesc = (2u << 4) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+      const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA));
+      const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sB));
       int as = 0;
       uint32_t aph = 0;
       for (int kb = 0; kb < args.nk; ++kb) {
@@ -206,20 +210,20 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t bph = (uint32_t)((kb >> 1) & 1);
         mbar_wait(&fullB[bs], bph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t b_base = smem_u32(sB + bs * TC_B_STAGE);
+        const uint64_t bd0 = b_desc0 + (uint64_t)((bs * TC_B_STAGE) >> 4);
+        const uint32_t first = kb == 0 ? 0u : 1u;
+#pragma unroll
         for (int i = 0; i < 8; ++i) {
           mbar_wait(&fullA[as], aph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t a_base = smem_u32(sA + as * TC_A_TILE);
+          const uint64_t ad = a_desc0 + (uint64_t)((as * TC_A_TILE) >> 4);
+#pragma unroll
           for (int j = 0; j <= 7 - i; ++j) {
             const uint32_t d_tmem = tmem_base + (uint32_t)((i + j) * TC_BN);
+            const uint64_t bd = bd0 + (uint64_t)((j * TC_B_TILE) >> 4);
 #pragma unroll
-            for (int kk = 0; kk < TC_BK / 32; ++kk) {
-              const uint64_t ad = umma_desc_sw128(a_base + kk * 32);
-              const uint64_t bd = umma_desc_sw128(b_base + j * TC_B_TILE + kk * 32);
-              const uint32_t acc = (kb > 0 || i > 0 || kk > 0) ? 1u : 0u;
-              mma_i8(d_tmem, ad, bd, idesc, acc);
-            }
+            for (int kk = 0; kk < TC_BK / 32; ++kk)
+              mma_i8(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, (i > 0 || kk > 0) ? 1u : first);
           }
           umma_commit(&emptyA[as]);  // slot free once these MMAs retire
           if (++as == TC_ASTAGES) {
