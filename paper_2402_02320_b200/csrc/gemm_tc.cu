@@ -328,8 +328,10 @@ __global__ void __launch_bounds__(256) k_limb_split_t(uint8_t* __restrict__ out,
     tile[kk][tx] = (k < rows && n < cols) ? A[k * lda + n] : 0ull;
   }
   __syncthreads();
-  const int n = tx;
-  const int g = ty;  // 8 groups of 8 k's
+  // 8 lanes cover one output row's 64 contiguous k-bytes (two full sectors)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = warp * 4 + (lane >> 3);
+  const int g = lane & 7;
   const i64 gn = n0 + n;
   const i64 gk = k0 + g * 8;
   if (gn < cols && gk < rows) {
