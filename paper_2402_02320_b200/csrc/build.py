@@ -27,7 +27,7 @@ def nvcc() -> str:
 def flags() -> list[str]:
     return ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
             "-Xcompiler", "-fPIC", "-Xptxas", "-v", f"-I{os.path.join(REPO, 'include')}",
-            "--expt-relaxed-constexpr"]
+            "--expt-relaxed-constexpr"] + os.environ.get("MPX_NVCC_EXTRA", "").split()
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

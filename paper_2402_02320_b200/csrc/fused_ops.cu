@@ -396,50 +396,44 @@ __device__ __forceinline__ Sh<L> mt_compute(const Sh<L>& x, const Sh<L>& y, cons
 template <int L>
 __device__ __forceinline__ Sh<L> d_poly4(const Sh<L>& x, const FusedParams& P, const Tape& tape, int& ti, i64 e,
                                          u64 msk) {
-  // powers x^2..x^4: three pipelined mul+trunc steps, then the final truncation
+#ifdef MPX_POLY_PIPELINED
   MTM<L> A, B;
   mt_load<L>(A, tape, ti, e, P.p, P.w);
   mt_load<L>(B, tape, ti, e, P.p, P.w);
   const Sh<L> x2 = mt_compute<L>(x, x, A, P.p, P.w, P.p0, msk);
   mt_load<L>(A, tape, ti, e, P.p, P.w);
   const Sh<L> x3 = mt_compute<L>(x2, x, B, P.p, P.w, P.p0, msk);
-  // final truncation's edaBits (no triple)
+  const Sh<L> x4 = mt_compute<L>(x3, x, A, P.p, P.w, P.p0, msk);
+#else
+  const Sh<L> x2 = d_mul_trunc<L>(x, x, tape, ti, e, P.p, P.w, P.p0, msk);
+  const Sh<L> x3 = d_mul_trunc<L>(x2, x, tape, ti, e, P.p, P.w, P.p0, msk);
+  const Sh<L> x4 = d_mul_trunc<L>(x3, x, tape, ti, e, P.p, P.w, P.p0, msk);
+#endif
   const MatRef& flo = next_take<L>(tape, ti, e);
   const MatRef& fhi = next_take<L>(tape, ti, e);
-  u64 rlo[L], rhi[L];
-#pragma unroll
-  for (int l = 0; l < L; ++l) {
-    rlo[l] = __ldcs(flo.p0 + l * flo.ps0 + e);
-    rhi[l] = __ldcs(fhi.p0 + l * fhi.ps0 + e);
-  }
-  const Sh<L> x4 = mt_compute<L>(x3, x, A, P.p, P.w, P.p0, msk);
-  const Sh<L>* pw[5] = {nullptr, &x, &x2, &x3, &x4};
   u64 acc[L];
 #pragma unroll
   for (int l = 0; l < L; ++l) acc[l] = 0;
+  if (P.coef_nz[1]) {
 #pragma unroll
-  for (int i = 1; i <= 4; ++i) {
-    if (!P.coef_nz[i]) continue;
-#pragma unroll
-    for (int l = 0; l < L; ++l) acc[l] += pw[i]->v[l] * P.coef_p[i];
+    for (int l = 0; l < L; ++l) acc[l] += x.v[l] * P.coef_p[1];
   }
-  const u64 bias = 1ull << (P.w - 2), unbias = 1ull << (P.w - 2 - P.p);
-  u64 s = 0;
+  if (P.coef_nz[2]) {
 #pragma unroll
-  for (int l = 0; l < L; ++l) {
-    u64 v = ((acc[l] + (l == P.p0 ? P.coef0_2p : 0ull)) & msk) + rlo[l] + (rhi[l] << P.p);
-    if (l == P.p0) v += bias;
-    s += v;
+    for (int l = 0; l < L; ++l) acc[l] += x2.v[l] * P.coef_p[2];
   }
-  const u64 chi = (s & msk) >> P.p;
-  Sh<L> o;
+  if (P.coef_nz[3]) {
 #pragma unroll
-  for (int l = 0; l < L; ++l) {
-    u64 v = 0ull - rhi[l];
-    if (l == P.p0) v += chi - unbias;
-    o.v[l] = v & msk;
+    for (int l = 0; l < L; ++l) acc[l] += x3.v[l] * P.coef_p[3];
   }
-  return o;
+  if (P.coef_nz[4]) {
+#pragma unroll
+    for (int l = 0; l < L; ++l) acc[l] += x4.v[l] * P.coef_p[4];
+  }
+  Sh<L> a;
+#pragma unroll
+  for (int l = 0; l < L; ++l) a.v[l] = (acc[l] + (l == P.p0 ? P.coef0_2p : 0ull)) & msk;
+  return d_trunc<L>(a, flo, &fhi, e, P.p, true, P.w, P.p0, msk);
 }
 
 template <int L>
