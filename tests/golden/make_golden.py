@@ -54,6 +54,25 @@ def save_dealer(eng):
     np.savez_compressed(os.path.join(HERE, "dealer.npz"), **arrays)
 
 
+def save_dealer_files(eng):
+    """Reference-written MPFXPRE1 files + manifest for the `reciprocal` and
+    `batch_matmul` cases (seed 11): dry run on the reference, then
+    preprocessing.dealer_generate / write_manifest (preprocessing.py:199-256)."""
+    import shutil
+    from mpfix.metrics import CommMetrics
+    from mpfix.preprocessing import DemandCounter, dealer_generate, write_manifest
+    from mpfix.session import PartySession
+    from mpfix.transport import NullMesh
+    for name in ("reciprocal", "batch_matmul"):
+        fn, n = CASES[name]
+        counter = DemandCounter(party=0)
+        fn(eng, PartySession(0, n, NullMesh(0, n), counter, metrics=CommMetrics(0, n)))
+        out = os.path.join(HERE, "files", name)
+        shutil.rmtree(out, ignore_errors=True)
+        dealer_generate(11, n, counter.demands, out)
+        write_manifest(os.path.join(out, "manifest.json"), counter.demands)
+
+
 def main(argv):
     eng = ReferenceEngine()
     names = argv or list(CASES)
@@ -62,7 +81,8 @@ def main(argv):
         print(f"{nm}: rounds={info['total']['rounds']} demands={len(info['demands'])}")
     if not argv:
         save_dealer(eng)
-        print("dealer fixture written")
+        save_dealer_files(eng)
+        print("dealer fixtures written")
 
 
 if __name__ == "__main__":
