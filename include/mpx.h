@@ -180,6 +180,14 @@ int mpx_bits_flat_to_rows(uint64_t* out, const uint64_t* flat, int64_t flat_bit,
                           void* stream);
 int mpx_bits_rows_to_flat(uint64_t* flat, const uint64_t* rows_in, int64_t rows, int m, void* stream);
 
+/* ---- convolution layout on shares (CNN layers) ----
+ * x: [L][B][C][H][W] -> cols: [L][B*OH*OW][C*K*K] (zero padding), and the
+ * adjoint scatter-add col2im (mod 2^w). Local: no communication. */
+int mpx_im2col(uint64_t* out, const uint64_t* x, int L, int64_t B, int C, int H, int W, int K, int stride,
+               int pad, void* stream);
+int mpx_col2im(uint64_t* dx, const uint64_t* cols, int L, int64_t B, int C, int H, int W, int K, int stride,
+               int pad, int width, void* stream);
+
 /* ---- Z_2^64 GEMM (ring.py:60-62; basic.py:72-75; nn.py:193) ----
  * C[b] (+)= A[b] @ B[b] mod 2^w, row-major, A: MxK, B: KxN, C: MxN,
  * batch strides sA/sB/sC in elements (0 broadcasts). */

@@ -1,0 +1,233 @@
+"""CPU oracle for secure training — TEST INFRASTRUCTURE ONLY.
+
+Restates ``paper_2402_02320_b200/train.py`` (Conv2d / AvgPool2d / ReLU /
+Linear / softmax-CE / SGD) over the oracle's primitives, which are pinned
+bit-exactly to the reference (``tests/test_oracle_golden.py``). The reference
+itself has no training or convolution code, so training parity
+is pinned per primitive; this restatement lets the tests check a whole GPU
+training step bit-for-bit on every party's shares.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+
+import numpy as np
+
+from . import mpc_sim as O
+
+U64 = np.uint64
+
+
+def im2col(x: np.ndarray, k: int, stride: int, pad: int) -> np.ndarray:
+    """x: (n, B, C, H, W) -> (n, B*OH*OW, C*k*k), zero padded."""
+    n, B, C, H, W = x.shape
+    OH, OW = (H + 2 * pad - k) // stride + 1, (W + 2 * pad - k) // stride + 1
+    xp = np.zeros((n, B, C, H + 2 * pad, W + 2 * pad), U64)
+    xp[:, :, :, pad:pad + H, pad:pad + W] = x
+    out = np.empty((n, B, OH, OW, C, k, k), U64)
+    for kh in range(k):
+        for kw in range(k):
+            out[:, :, :, :, :, kh, kw] = xp[:, :, :, kh:kh + stride * OH:stride,
+                                            kw:kw + stride * OW:stride].transpose(0, 1, 3, 4, 2)
+    return out.reshape(n, B * OH * OW, C * k * k)
+
+
+def col2im(cols: np.ndarray, shape, k: int, stride: int, pad: int, width: int) -> np.ndarray:
+    """Adjoint of im2col: scatter-add (mod 2^w) into (n, B, C, H, W)."""
+    n, B, C, H, W = shape
+    OH, OW = (H + 2 * pad - k) // stride + 1, (W + 2 * pad - k) // stride + 1
+    c = cols.reshape(n, B, OH, OW, C, k, k)
+    xp = np.zeros((n, B, C, H + 2 * pad, W + 2 * pad), U64)
+    with np.errstate(over="ignore"):
+        for kh in range(k):
+            for kw in range(k):
+                xp[:, :, :, kh:kh + stride * OH:stride, kw:kw + stride * OW:stride] += \
+                    c[:, :, :, :, :, kh, kw].transpose(0, 1, 4, 2, 3)
+    return O.wrap(xp[:, :, :, pad:pad + H, pad:pad + W].copy(), width)
+
+
+def _key(seed, label):
+    tag = hashlib.sha256(f"{seed}:param:{label}".encode()).digest()
+    return [int.from_bytes(tag[:8], "little"), int.from_bytes(tag[8:16], "little")]
+
+
+def share_fixed(s: O.Sim, floats, width, frac, key) -> O.AShare:
+    enc = O.encode(np.asarray(floats, np.float64), width, frac)
+    return O.AShare(O.deal_inputs_arith(enc, s.n, width, key), width, frac)
+
+
+def _T(x: O.AShare) -> O.AShare:
+    return O.AShare(np.ascontiguousarray(x.values.swapaxes(-1, -2)), x.width, x.frac)
+
+
+def _bcast_rows(b: O.AShare, rows) -> O.AShare:
+    return O.AShare(np.ascontiguousarray(np.broadcast_to(b.values[:, None, :], (b.values.shape[0], rows,
+                                                                               b.values.shape[1]))),
+                    b.width, b.frac)
+
+
+def _lift(x: O.AShare, p) -> O.AShare:
+    return x.mul_public(1 << p, frac_delta=p)
+
+
+def _colsum(z: O.AShare) -> O.AShare:
+    return O.AShare(O.rsum(z.values, z.width, axis=1), z.width, z.frac)
+
+
+class Conv2d:
+    def __init__(self, s, cin, cout, k, stride=1, pad=0, *, rng, name, seed, frac, width=64):
+        self.cin, self.cout, self.k, self.stride, self.pad, self.p = cin, cout, k, stride, pad, frac
+        fan_in = cin * k * k
+        self.W = share_fixed(s, rng.normal(0.0, math.sqrt(2.0 / fan_in), (fan_in, cout)), width, frac,
+                             _key(seed, name + ".W"))
+        self.b = share_fixed(s, np.zeros(cout), width, frac, _key(seed, name + ".b"))
+
+    def forward(self, s, x):
+        n, B, C, H, W = x.values.shape
+        self.in_shape = x.values.shape
+        self.cols = O.AShare(im2col(x.values, self.k, self.stride, self.pad), x.width, x.frac)
+        OH, OW = (H + 2 * self.pad - self.k) // self.stride + 1, (W + 2 * self.pad - self.k) // self.stride + 1
+        self.out_hw = (OH, OW)
+        z = O.batch_matmul(s, [(self.cols, self.W)])[0]
+        z = O.truncate(s, z + _bcast_rows(_lift(self.b, self.p), B * OH * OW), self.p)
+        v = z.values.reshape(n, B, OH, OW, self.cout).transpose(0, 1, 4, 2, 3)
+        return O.AShare(np.ascontiguousarray(v), z.width, z.frac)
+
+    def backward(self, s, dy, need_dx=True):
+        n, B, C, H, W = self.in_shape
+        OH, OW = self.out_hw
+        dz = O.AShare(np.ascontiguousarray(dy.values.transpose(0, 1, 3, 4, 2)).reshape(n, B * OH * OW, self.cout),
+                      dy.width, dy.frac)
+        pairs = [(_T(self.cols), dz)]
+        if need_dx:
+            pairs.append((dz, _T(self.W)))
+        outs = O.batch_matmul(s, pairs)
+        self.gW, self.gb = outs[0], _colsum(dz)
+        if not need_dx:
+            return None
+        dcols = O.truncate(s, outs[1], self.p)
+        return O.AShare(col2im(dcols.values, self.in_shape, self.k, self.stride, self.pad, dcols.width),
+                        dcols.width, dcols.frac)
+
+    def step(self, s, shift):
+        self.W = self.W - O.truncate(s, self.gW, self.p + shift, out_frac=self.p)
+        self.b = self.b - O.truncate(s, self.gb, shift, out_frac=self.p)
+
+
+class AvgPool2d:
+    def __init__(self, k=2):
+        self.k = k
+        self.shift = int(round(math.log2(k * k)))
+
+    def forward(self, s, x):
+        n, B, C, H, W = x.values.shape
+        k = self.k
+        self.in_shape = x.values.shape
+        v = x.values.reshape(n, B, C, H // k, k, W // k, k).transpose(0, 1, 2, 3, 5, 4, 6)
+        summed = O.rsum(v.reshape(n, B, C, H // k, W // k, k * k), x.width)
+        return O.truncate(s, O.AShare(summed, x.width, x.frac), self.shift, out_frac=x.frac)
+
+    def backward(self, s, dy, need_dx=True):
+        n, B, C, H, W = self.in_shape
+        k = self.k
+        d = O.truncate(s, dy, self.shift, out_frac=dy.frac)
+        v = np.broadcast_to(d.values.reshape(n, B, C, H // k, 1, W // k, 1), (n, B, C, H // k, k, W // k, k))
+        return O.AShare(np.ascontiguousarray(v).reshape(n, B, C, H, W), d.width, d.frac)
+
+
+class ReLU:
+    def forward(self, s, x):
+        zero = O.public_ashare(s.n, 0, x.width, x.frac, x.shape)
+        self.sign = O.bit2a(s, O.gt(s, x, zero), x.width)
+        return O.mul(s, self.sign, x)
+
+    def backward(self, s, dy, need_dx=True):
+        return O.mul(s, self.sign, dy)
+
+    def step(self, s, shift):
+        pass
+
+
+class Flatten:
+    def forward(self, s, x):
+        self.in_shape = x.shape
+        return x.reshape((x.shape[0], int(np.prod(x.shape[1:]))))
+
+    def backward(self, s, dy, need_dx=True):
+        return dy.reshape(self.in_shape)
+
+    def step(self, s, shift):
+        pass
+
+
+AvgPool2d.step = lambda self, s, shift: None
+
+
+class Linear:
+    def __init__(self, s, fin, fout, *, rng, name, seed, frac, width=64):
+        self.p = frac
+        self.W = share_fixed(s, rng.normal(0.0, math.sqrt(2.0 / fin), (fin, fout)), width, frac,
+                             _key(seed, name + ".W"))
+        self.b = share_fixed(s, np.zeros(fout), width, frac, _key(seed, name + ".b"))
+
+    def forward(self, s, x):
+        self.x = x
+        z = O.batch_matmul(s, [(x, self.W)])[0]
+        return O.truncate(s, z + _bcast_rows(_lift(self.b, self.p), x.shape[0]), self.p)
+
+    def backward(self, s, dy, need_dx=True):
+        pairs = [(_T(self.x), dy)]
+        if need_dx:
+            pairs.append((dy, _T(self.W)))
+        outs = O.batch_matmul(s, pairs)
+        self.gW, self.gb = outs[0], _colsum(dy)
+        return O.truncate(s, outs[1], self.p) if need_dx else None
+
+    def step(self, s, shift):
+        self.W = self.W - O.truncate(s, self.gW, self.p + shift, out_frac=self.p)
+        self.b = self.b - O.truncate(s, self.gb, shift, out_frac=self.p)
+
+
+class Model:
+    def __init__(self, layers):
+        self.layers = list(layers)
+
+    def forward(self, s, x):
+        for layer in self.layers:
+            x = layer.forward(s, x)
+        return x
+
+    def train_step(self, s, x, y, lr_shift):
+        B = x.shape[0]
+        bshift = int(round(math.log2(B)))
+        with s.scope("forward"):
+            logits = self.forward(s, x)
+        with s.scope("loss"):
+            dz = O.softmax(s, logits) - y
+        with s.scope("backward"):
+            g = dz
+            for i in range(len(self.layers) - 1, -1, -1):
+                g = self.layers[i].backward(s, g, need_dx=i > 0)
+        with s.scope("sgd"):
+            for layer in self.layers:
+                layer.step(s, lr_shift + bshift)
+        return logits
+
+
+def lenet(s, seed=7, frac=23):
+    rng = np.random.default_rng(seed)
+    kw = dict(seed=seed, frac=frac)
+    return Model([Conv2d(s, 1, 20, 5, rng=rng, name="conv1", **kw), AvgPool2d(2), ReLU(),
+                  Conv2d(s, 20, 50, 5, rng=rng, name="conv2", **kw), AvgPool2d(2), ReLU(), Flatten(),
+                  Linear(s, 800, 500, rng=rng, name="fc1", **kw), ReLU(),
+                  Linear(s, 500, 10, rng=rng, name="fc2", **kw)])
+
+
+def simple_mlp(s, seed=7, frac=23):
+    rng = np.random.default_rng(seed)
+    kw = dict(seed=seed, frac=frac)
+    return Model([Linear(s, 784, 128, rng=rng, name="fc1", **kw), ReLU(),
+                  Linear(s, 128, 128, rng=rng, name="fc2", **kw), ReLU(),
+                  Linear(s, 128, 10, rng=rng, name="fc3", **kw)])

@@ -411,3 +411,80 @@ extern "C" int mpx_device_sm_count(int device) {
   if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
   return v;
 }
+
+// --------------------------------------------------------------------------
+// Convolution layout ops on shares (local, linear): im2col gathers, col2im
+// scatter-adds mod 2^w. x: [L][B][C][H][W]; cols: [L][B*OH*OW][C*K*K].
+
+__global__ void k_im2col(u64* __restrict__ out, const u64* __restrict__ x, int L, i64 B, int C, int H, int W,
+                         int K, int S, int P, int OH, int OW) {
+  const i64 cols = (i64)C * K * K;
+  const i64 rows = B * OH * OW;
+  const i64 total = (i64)L * rows * cols;
+  GRID_STRIDE(t, total) {
+    const i64 col = t % cols;
+    const i64 rr = t / cols;
+    const i64 row = rr % rows;
+    const i64 l = rr / rows;
+    const int kw = (int)(col % K), kh = (int)((col / K) % K), c = (int)(col / ((i64)K * K));
+    const int ow = (int)(row % OW), oh = (int)((row / OW) % OH);
+    const i64 b = row / ((i64)OH * OW);
+    const int h = oh * S - P + kh, w = ow * S - P + kw;
+    u64 v = 0;
+    if (h >= 0 && h < H && w >= 0 && w < W) v = x[(((l * B + b) * C + c) * H + h) * (i64)W + w];
+    out[t] = v;
+  }
+}
+
+__global__ void k_col2im(u64* __restrict__ dx, const u64* __restrict__ colsb, int L, i64 B, int C, int H, int W,
+                         int K, int S, int P, int OH, int OW, u64 msk) {
+  const i64 cols = (i64)C * K * K;
+  const i64 rows = B * OH * OW;
+  const i64 total = (i64)L * B * C * H * W;
+  GRID_STRIDE(t, total) {
+    const int w = (int)(t % W);
+    const int h = (int)((t / W) % H);
+    const int c = (int)((t / ((i64)W * H)) % C);
+    const i64 bl = t / ((i64)W * H * C);
+    const i64 b = bl % B, l = bl / B;
+    u64 acc = 0;
+    for (int kh = 0; kh < K; ++kh) {
+      const int hh = h + P - kh;
+      if (hh < 0 || hh % S) continue;
+      const int oh = hh / S;
+      if (oh >= OH) continue;
+      for (int kw = 0; kw < K; ++kw) {
+        const int ww = w + P - kw;
+        if (ww < 0 || ww % S) continue;
+        const int ow = ww / S;
+        if (ow >= OW) continue;
+        const i64 row = (b * OH + oh) * OW + ow;
+        acc += colsb[(l * rows + row) * cols + ((i64)c * K + kh) * K + kw];
+      }
+    }
+    dx[t] = acc & msk;
+  }
+}
+
+extern "C" int mpx_im2col(uint64_t* out, const uint64_t* x, int L, int64_t B, int C, int H, int W, int K,
+                          int stride, int pad, void* stream) {
+  CHECK_ARG(out && x && L >= 1 && B >= 1 && C >= 1 && H >= 1 && W >= 1 && K >= 1 && stride >= 1 && pad >= 0);
+  const int OH = (H + 2 * pad - K) / stride + 1, OW = (W + 2 * pad - K) / stride + 1;
+  CHECK_ARG(OH >= 1 && OW >= 1);
+  const i64 total = (i64)L * B * OH * OW * C * K * K;
+  k_im2col<<<grid_for(total), MPX_THREADS, 0, (cudaStream_t)stream>>>(out, x, L, B, C, H, W, K, stride, pad, OH,
+                                                                        OW);
+  return launch_status();
+}
+
+extern "C" int mpx_col2im(uint64_t* dx, const uint64_t* cols, int L, int64_t B, int C, int H, int W, int K,
+                          int stride, int pad, int width, void* stream) {
+  CHECK_ARG(dx && cols && L >= 1 && B >= 1 && C >= 1 && H >= 1 && W >= 1 && K >= 1 && stride >= 1 && pad >= 0 &&
+            width >= 1 && width <= 64);
+  const int OH = (H + 2 * pad - K) / stride + 1, OW = (W + 2 * pad - K) / stride + 1;
+  CHECK_ARG(OH >= 1 && OW >= 1);
+  const i64 total = (i64)L * B * C * H * W;
+  k_col2im<<<grid_for(total), MPX_THREADS, 0, (cudaStream_t)stream>>>(dx, cols, L, B, C, H, W, K, stride, pad, OH,
+                                                                        OW, ring_mask(width));
+  return launch_status();
+}

@@ -250,6 +250,20 @@ def bits_rows_to_flat(flat, rows_in, rows, m):
     return flat
 
 
+def im2col(out, x, L, B, C, H, W, K, stride, pad):
+    if _dry(out):
+        return out
+    call("mpx_im2col", ptr(out), ptr(x), L, B, C, H, W, K, stride, pad)
+    return out
+
+
+def col2im(dx, cols, L, B, C, H, W, K, stride, pad, width):
+    if _dry(dx):
+        return dx
+    call("mpx_col2im", ptr(dx), ptr(cols), L, B, C, H, W, K, stride, pad, width)
+    return dx
+
+
 # ---- GEMM -------------------------------------------------------------------
 
 def gemm(C, A, B, batch, M, K, N, sA, sB, sC, accumulate, width, simt=False):

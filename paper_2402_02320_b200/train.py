@@ -1,0 +1,250 @@
+"""Secure CNN / MLP training on secret shares (BASELINE configs 0-2).
+
+The reference package has no training or convolution code; the
+paper trains Simple / LeNet / AlexNet / VGG16m with Piranha's recipe
+(layer tables :1289-1458). Everything here is a
+composition of the reference's pinned primitives, so parity is pinned per
+primitive (and the composition is restated in ``oracle/train_sim.py`` for a
+bit-exact end-to-end check):
+
+* weights and activations are additive shares at precision p (w = 64);
+* Conv2d = im2col (local kernel) + Beaver matmul with the secret weight
+  matrix (one matrix triple, ``basic.py:45-79``) + secret bias + truncation;
+* AvgPool2d (power-of-two window) = local window sum + truncation;
+* ReLU = gt / bit2a / mul (``nn.py:92-97``), keeping the converted sign bit
+  so the backward pass is one Beaver mul;
+* Linear = Beaver matmul with secret weights + secret bias + truncation;
+* softmax-cross-entropy gradient = softmax (``nn.py:139-147``) - one-hot;
+* SGD with lr = 2^-lr_shift and batch 2^b folds 1/B into one truncation of
+  the doubled-precision gradient: W -= trunc(dW_2p, p + lr_shift + b).
+
+Both backward matmuls of a layer (dW = X^T dZ, dX = dZ W^T) open in ONE round.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import kernels as K
+from .nn import softmax
+from .protocols import batch_matmul, bit2a, gt, mul, truncate
+from .sharing import AShare, public_ashare
+
+
+def _transpose(x: AShare) -> AShare:
+    return AShare(x.values.transpose(-1, -2).contiguous(), x.width, x.frac, x.parties)
+
+
+def _bcast_rows(b: AShare, rows: int) -> AShare:
+    """(C,) -> (rows, C) share broadcast (layout only)."""
+    v = b.values.unsqueeze(1).expand(b.L, rows, b.shape[0]).contiguous()
+    return AShare(v, b.width, b.frac, b.parties)
+
+
+def _colsum(session, z: AShare) -> AShare:
+    """sum over rows of a (rows, C) share -> (C,) (local ring sum)."""
+    t = _transpose(z)
+    c, r = t.shape
+    out = session.alloc((session.L, c))
+    K.ring_rowdot(out, t.values, None, session.L, c, r, z.width)
+    return AShare(out, z.width, z.frac, session.parties)
+
+
+def _lift(x: AShare, p: int) -> AShare:
+    """x at frac p -> same value at frac 2p (local shift by 2^p)."""
+    return x.mul_public(1 << p, frac_delta=p)
+
+
+@dataclass
+class InitSpec:
+    seed: int = 7
+    frac: int = 23
+    width: int = 64
+
+
+def _kaiming(rng, fan_in, shape):
+    return rng.normal(0.0, math.sqrt(2.0 / fan_in), size=shape)
+
+
+class Layer:
+    params: tuple = ()
+
+    def step(self, session, shift: int) -> None:
+        pass
+
+
+class Conv2d(Layer):
+    """(C_in -> C_out, K x K, stride, pad); weight matrix (C_in*K*K, C_out)."""
+
+    def __init__(self, session, cin, cout, k, stride=1, pad=0, *, rng, name, spec: InitSpec):
+        self.cin, self.cout, self.k, self.stride, self.pad = cin, cout, k, stride, pad
+        self.p = spec.frac
+        fan_in = cin * k * k
+        self.W = session.share_fixed(_kaiming(rng, fan_in, (fan_in, cout)), spec.width, spec.frac,
+                                     _key(spec, name + ".W"))
+        self.b = session.share_fixed(np.zeros(cout), spec.width, spec.frac, _key(spec, name + ".b"))
+
+    def forward(self, s, x: AShare) -> AShare:
+        B, C, H, W = x.shape
+        k, st, pd = self.k, self.stride, self.pad
+        OH, OW = (H + 2 * pd - k) // st + 1, (W + 2 * pd - k) // st + 1
+        rows, cols = B * OH * OW, C * k * k
+        cv = s.alloc((s.L, rows, cols))
+        K.im2col(cv, x.values, s.L, B, C, H, W, k, st, pd)
+        self.cols = AShare(cv, x.width, x.frac, s.parties)
+        self.in_shape = (B, C, H, W)
+        z = batch_matmul(s, [(self.cols, self.W)])[0]
+        z = truncate(s, z + _bcast_rows(_lift(self.b, self.p), rows), self.p)
+        self.out_hw = (OH, OW)
+        v = z.values.view(s.L, B, OH, OW, self.cout).permute(0, 1, 4, 2, 3).contiguous()
+        return AShare(v, z.width, z.frac, s.parties)
+
+    def backward(self, s, dy: AShare, need_dx: bool = True) -> AShare | None:
+        B, C, H, W = self.in_shape
+        OH, OW = self.out_hw
+        dz = AShare(dy.values.permute(0, 1, 3, 4, 2).reshape(s.L, B * OH * OW, self.cout).contiguous(),
+                    dy.width, dy.frac, s.parties)
+        pairs = [(_transpose(self.cols), dz)]
+        if need_dx:
+            pairs.append((dz, _transpose(self.W)))
+        outs = batch_matmul(s, pairs)
+        self.gW, self.gb = outs[0], _colsum(s, dz)
+        if not need_dx:
+            return None
+        dcols = truncate(s, outs[1], self.p)
+        dx = s.alloc((s.L, B, C, H, W))
+        K.col2im(dx, dcols.values, s.L, B, C, H, W, self.k, self.stride, self.pad, dcols.width)
+        return AShare(dx, dcols.width, dcols.frac, s.parties)
+
+    def step(self, s, shift: int) -> None:
+        self.W = self.W - truncate(s, self.gW, self.p + shift, out_frac=self.p)
+        self.b = self.b - truncate(s, self.gb, shift, out_frac=self.p)
+
+
+class AvgPool2d(Layer):
+    """Average pool with a power-of-two window (k x k, stride k)."""
+
+    def __init__(self, k: int = 2):
+        self.k = k
+        self.shift = int(round(math.log2(k * k)))
+        if (1 << self.shift) != k * k:
+            raise ValueError("AvgPool2d needs a power-of-two window area")
+
+    def forward(self, s, x: AShare) -> AShare:
+        B, C, H, W = x.shape
+        k = self.k
+        v = x.values.view(s.L, B, C, H // k, k, W // k, k).permute(0, 1, 2, 3, 5, 4, 6).contiguous()
+        out = s.alloc((s.L, B, C, H // k, W // k))
+        K.ring_rowdot(out, v, None, s.L, B * C * (H // k) * (W // k), k * k, x.width)
+        self.in_shape = (B, C, H, W)
+        return truncate(s, AShare(out, x.width, x.frac, s.parties), self.shift, out_frac=x.frac)
+
+    def backward(self, s, dy: AShare, need_dx: bool = True) -> AShare:
+        B, C, H, W = self.in_shape
+        k = self.k
+        d = truncate(s, dy, self.shift, out_frac=dy.frac)
+        v = d.values.view(s.L, B, C, H // k, 1, W // k, 1).expand(s.L, B, C, H // k, k, W // k, k)
+        return AShare(v.reshape(s.L, B, C, H, W).contiguous(), d.width, d.frac, s.parties)
+
+
+class ReLU(Layer):
+    def forward(self, s, x: AShare) -> AShare:
+        zero = public_ashare(0, x.width, x.frac, s, shape=x.shape)
+        self.sign = bit2a(s, gt(s, x, zero), x.width)
+        return mul(s, self.sign, x)
+
+    def backward(self, s, dy: AShare, need_dx: bool = True) -> AShare:
+        return mul(s, self.sign, dy)
+
+
+class Flatten(Layer):
+    def forward(self, s, x: AShare) -> AShare:
+        self.in_shape = x.shape
+        return x.reshape((x.shape[0], math.prod(x.shape[1:])))
+
+    def backward(self, s, dy: AShare, need_dx: bool = True) -> AShare:
+        return dy.reshape(self.in_shape)
+
+
+class Linear(Layer):
+    def __init__(self, session, fin, fout, *, rng, name, spec: InitSpec):
+        self.p = spec.frac
+        self.W = session.share_fixed(_kaiming(rng, fin, (fin, fout)), spec.width, spec.frac,
+                                     _key(spec, name + ".W"))
+        self.b = session.share_fixed(np.zeros(fout), spec.width, spec.frac, _key(spec, name + ".b"))
+
+    def forward(self, s, x: AShare) -> AShare:
+        self.x = x
+        z = batch_matmul(s, [(x, self.W)])[0]
+        return truncate(s, z + _bcast_rows(_lift(self.b, self.p), x.shape[0]), self.p)
+
+    def backward(self, s, dy: AShare, need_dx: bool = True) -> AShare | None:
+        pairs = [(_transpose(self.x), dy)]
+        if need_dx:
+            pairs.append((dy, _transpose(self.W)))
+        outs = batch_matmul(s, pairs)
+        self.gW, self.gb = outs[0], _colsum(s, dy)
+        return truncate(s, outs[1], self.p) if need_dx else None
+
+    def step(self, s, shift: int) -> None:
+        self.W = self.W - truncate(s, self.gW, self.p + shift, out_frac=self.p)
+        self.b = self.b - truncate(s, self.gb, shift, out_frac=self.p)
+
+
+def _key(spec: InitSpec, label: str):
+    import hashlib
+    tag = hashlib.sha256(f"{spec.seed}:param:{label}".encode()).digest()
+    return [int.from_bytes(tag[:8], "little"), int.from_bytes(tag[8:16], "little")]
+
+
+class Model:
+    """Sequential secure model with a softmax-cross-entropy head."""
+
+    def __init__(self, layers):
+        self.layers = list(layers)
+
+    def forward(self, s, x: AShare) -> AShare:
+        for layer in self.layers:
+            x = layer.forward(s, x)
+        return x
+
+    def train_step(self, s, x: AShare, y_onehot: AShare, lr_shift: int) -> AShare:
+        """One SGD step on a batch (batch size must be a power of two).
+        Returns the logits (shares) of the forward pass."""
+        B = x.shape[0]
+        bshift = int(round(math.log2(B)))
+        if (1 << bshift) != B:
+            raise ValueError("batch size must be a power of two")
+        with s.scope("forward"):
+            logits = self.forward(s, x)
+        with s.scope("loss"):
+            dz = softmax(s, logits) - y_onehot
+        with s.scope("backward"):
+            g = dz
+            for i in range(len(self.layers) - 1, -1, -1):
+                g = self.layers[i].backward(s, g, need_dx=i > 0)
+        with s.scope("sgd"):
+            for layer in self.layers:
+                layer.step(s, lr_shift + bshift)
+        return logits
+
+
+def lenet(session, spec: InitSpec = InitSpec()) -> Model:
+    """Paper Table 'LeNet': conv(20,5x5) pool ReLU conv(50,5x5) pool ReLU FC800x500 ReLU FC500x10."""
+    rng = np.random.default_rng(spec.seed)
+    return Model([Conv2d(session, 1, 20, 5, rng=rng, name="conv1", spec=spec), AvgPool2d(2), ReLU(),
+                  Conv2d(session, 20, 50, 5, rng=rng, name="conv2", spec=spec), AvgPool2d(2), ReLU(), Flatten(),
+                  Linear(session, 800, 500, rng=rng, name="fc1", spec=spec), ReLU(),
+                  Linear(session, 500, 10, rng=rng, name="fc2", spec=spec)])
+
+
+def simple_mlp(session, spec: InitSpec = InitSpec()) -> Model:
+    """Paper Table 'Simple network': 784-128-128-10 with ReLU."""
+    rng = np.random.default_rng(spec.seed)
+    return Model([Linear(session, 784, 128, rng=rng, name="fc1", spec=spec), ReLU(),
+                  Linear(session, 128, 128, rng=rng, name="fc2", spec=spec), ReLU(),
+                  Linear(session, 128, 10, rng=rng, name="fc3", spec=spec)])
