@@ -207,10 +207,13 @@ int mpx_limb_split(uint8_t* out, const uint64_t* A, int64_t rows, int64_t cols, 
 /* C[z] (+)= sum_{i+j<=7} 2^(8(i+j)) A8[z][i] @ B8[z][j]^T mod 2^w on tcgen05
  * kind::i8 with per-diagonal TMEM accumulators, TMA-fed (128B swizzle).
  * A8: [batch][8][Mpad][Kpad], B8: [batch][8][Npad][Kpad] u8, zero padded;
- * Mpad % 128 == 0, Npad % 64 == 0, Kpad % 128 == 0, Kpad <= 16384. */
+ * Mpad % 128 == 0, Npad % 64 == 0, Kpad % 128 == 0. `ksplit` CTAs share each
+ * output tile along K (each <= 16384 of K, the exactness bound) and add their
+ * u64 partials with wrapping atomics (width 64 only); ksplit = 1 needs
+ * Kpad <= 16384. */
 int mpx_gemm_limbs(uint64_t* C, const uint8_t* A8, const uint8_t* B8, int64_t batch, int64_t M,
                    int64_t N, int64_t Mpad, int64_t Npad, int64_t Kpad, int64_t ldc, int64_t sC,
-                   int accumulate, int width, void* stream);
+                   int accumulate, int width, int ksplit, void* stream);
 
 /* ---- sim-mode whole-op fused kernels (fused_ops.cu) ----
  * All L parties on this GPU: the whole Reciprocal / Exp / Log protocol

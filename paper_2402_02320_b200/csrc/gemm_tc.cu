@@ -111,7 +111,9 @@ struct TcArgs {
   i64 sC;        // batch stride of C (elements)
   int M, N;      // true output extent
   int Mpad, Npad;
-  int nk;        // k-blocks of TC_BK bytes
+  int nk;        // k-blocks of TC_BK bytes per CTA (split-K slice)
+  int nk_total;  // k-blocks of the whole reduction
+  int ksplit;    // CTAs per output tile along K; > 1 => wrapping atomic adds
   int accumulate;
   u64 msk;
 };
@@ -136,7 +138,10 @@ __global__ void __launch_bounds__(192, 1)
   // grouped rasterization: consecutive CTAs walk TC_GROUP_M row tiles of one
   // column band, so a wave shares both A and B k-slabs through L2
   const int tiles_m = args.Mpad / TC_BM, tiles_n = args.Npad / TC_BN;
-  const int lin = blockIdx.x;
+  const int ks = blockIdx.x % args.ksplit;            // split-K slice of this CTA
+  const int lin = blockIdx.x / args.ksplit;
+  const int kb0 = ks * args.nk;
+  const int nk = min(args.nk, args.nk_total - kb0);
   const int per_group = TC_GROUP_M * tiles_n;
   const int g = lin / per_group;
   const int first_m = g * TC_GROUP_M;
@@ -176,18 +181,18 @@ __global__ void __launch_bounds__(192, 1)
       // ---------------- TMA producer ----------------
       int as = 0;
       uint32_t aph = 0;
-      for (int kb = 0; kb < args.nk; ++kb) {
+      for (int kb = 0; kb < nk; ++kb) {
         const int bs = kb & 1;
         const uint32_t bph = (uint32_t)((kb >> 1) & 1);
         mbar_wait(&emptyB[bs], bph ^ 1);
         mbar_expect_tx(&fullB[bs], TC_B_STAGE);
         for (int j = 0; j < 8; ++j)
-          tma_load_2d(sB + bs * TC_B_STAGE + j * TC_B_TILE, &mapB, &fullB[bs], kb * TC_BK,
+          tma_load_2d(sB + bs * TC_B_STAGE + j * TC_B_TILE, &mapB, &fullB[bs], (kb0 + kb) * TC_BK,
                       (z * 8 + j) * args.Npad + n0);
         for (int i = 0; i < 8; ++i) {
           mbar_wait(&emptyA[as], aph ^ 1);
           mbar_expect_tx(&fullA[as], TC_A_TILE);
-          tma_load_2d(sA + as * TC_A_TILE, &mapA, &fullA[as], kb * TC_BK, (z * 8 + i) * args.Mpad + m0);
+          tma_load_2d(sA + as * TC_A_TILE, &mapA, &fullA[as], (kb0 + kb) * TC_BK, (z * 8 + i) * args.Mpad + m0);
           if (++as == TC_ASTAGES) {
             as = 0;
             aph ^= 1;
@@ -205,7 +210,7 @@ __global__ void __launch_bounds__(192, 1)
       const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sB));
       int as = 0;
       uint32_t aph = 0;
-      for (int kb = 0; kb < args.nk; ++kb) {
+      for (int kb = 0; kb < nk; ++kb) {
         const int bs = kb & 1;
         const uint32_t bph = (uint32_t)((kb >> 1) & 1);
         mbar_wait(&fullB[bs], bph);
@@ -261,9 +266,13 @@ __global__ void __launch_bounds__(192, 1)
         for (int t = 0; t < 32; ++t) {
           const int col = cbase + t;
           if (col < args.N) {
-            u64 v = res[t];
-            if (args.accumulate) v += Crow[col];
-            Crow[col] = v & args.msk;
+            if (args.ksplit > 1) {
+              atomicAdd(reinterpret_cast<unsigned long long*>(Crow + col), (unsigned long long)res[t]);
+            } else {
+              u64 v = res[t];
+              if (args.accumulate) v += Crow[col];
+              Crow[col] = v & args.msk;
+            }
           }
         }
       }
@@ -405,9 +414,24 @@ static int make_map(CUtensorMap* map, const uint8_t* base, i64 rows, i64 kbytes,
 // Mpad % 128 == 0, Npad % 64 == 0, Kpad % 128 == 0, Kpad <= 16384.
 extern "C" int mpx_gemm_limbs(uint64_t* C, const uint8_t* A8, const uint8_t* B8, int64_t batch, int64_t M,
                               int64_t N, int64_t Mpad, int64_t Npad, int64_t Kpad, int64_t ldc, int64_t sC,
-                              int accumulate, int width, void* stream) {
+                              int accumulate, int width, int ksplit, void* stream) {
   CHECK_ARG(C && A8 && B8 && batch >= 1 && batch <= 65535 && M >= 1 && N >= 1 && width >= 1 && width <= 64);
-  CHECK_ARG(Mpad % TC_BM == 0 && Npad % TC_BN == 0 && Kpad % TC_BK == 0 && Kpad >= TC_BK && Kpad <= 16384);
+  CHECK_ARG(Mpad % TC_BM == 0 && Npad % TC_BN == 0 && Kpad % TC_BK == 0 && Kpad >= TC_BK);
+  const int nk_total = (int)(Kpad / TC_BK);
+  if (ksplit < 1) ksplit = 1;
+  if (ksplit > nk_total) ksplit = nk_total;
+  int nk_per = (nk_total + ksplit - 1) / ksplit;
+  ksplit = (nk_total + nk_per - 1) / nk_per;
+  // exactness: each CTA's s32 diagonal accumulators see at most 16384 of K
+  CHECK_ARG((i64)nk_per * TC_BK <= 16384);
+  // split-K adds partials with wrapping 64-bit atomics: exact mod 2^64 only
+  CHECK_ARG(ksplit == 1 || width == 64);
+  if (ksplit > 1 && !accumulate) {
+    for (i64 z = 0; z < batch; ++z)
+      if (cudaMemset2DAsync(C + z * sC, (size_t)ldc * 8, 0, (size_t)N * 8, (size_t)M, (cudaStream_t)stream) !=
+          cudaSuccess)
+        return MPX_ERR_CUDA;
+  }
   CHECK_ARG(M <= Mpad && N <= Npad && ldc >= N);
   CHECK_ARG(batch * 8 * Mpad < (1ll << 31) && batch * 8 * Npad < (1ll << 31));
   CUtensorMap mapA, mapB;
@@ -428,10 +452,12 @@ extern "C" int mpx_gemm_limbs(uint64_t* C, const uint8_t* A8, const uint8_t* B8,
   a.N = (int)N;
   a.Mpad = (int)Mpad;
   a.Npad = (int)Npad;
-  a.nk = (int)(Kpad / TC_BK);
+  a.nk = nk_per;
+  a.nk_total = nk_total;
+  a.ksplit = ksplit;
   a.accumulate = accumulate;
   a.msk = ring_mask(width);
-  dim3 grid((unsigned)((Npad / TC_BN) * (Mpad / TC_BM)), 1, (unsigned)batch);
+  dim3 grid((unsigned)((Npad / TC_BN) * (Mpad / TC_BM) * ksplit), 1, (unsigned)batch);
   k_gemm_limbs_tc<<<grid, 192, TC_SMEM_BYTES, (cudaStream_t)stream>>>(mapA, mapB, a);
   return launch_status();
 }

@@ -267,9 +267,10 @@ def col2im(dx, cols, L, B, C, H, W, K, stride, pad, width):
 # ---- GEMM -------------------------------------------------------------------
 
 def gemm(C, A, B, batch, M, K, N, sA, sB, sC, accumulate, width, simt=False):
+    """C[b] (+)= A[b] @ B[b] mod 2^w: tcgen05 limb kernel for real work, SIMT tiles otherwise."""
     if _dry(C):
         return C
-    if not simt and M * K * N >= TC_MIN_MACS and M >= 64 and N >= 32 and K >= 64:
+    if not simt and tc_eligible(M, K, N, width):
         return gemm_tc(C, A, B, batch, M, K, N, sA, sB, sC, accumulate, width)
     call("mpx_gemm_simt" if simt else "mpx_gemm", ptr(C), A if isinstance(A, int) else ptr(A),
          B if isinstance(B, int) else ptr(B), batch, M, K, N, sA, sB, sC, int(accumulate), width)
@@ -277,7 +278,12 @@ def gemm(C, A, B, batch, M, K, N, sA, sB, sC, accumulate, width, simt=False):
 
 
 TC_MIN_MACS = 1 << 22   # below this the SIMT tiles win (launch + split overhead)
-TC_MAX_K = 16384        # exactness bound of the u32 diagonal accumulators
+TC_MAX_K = 16384        # exactness bound of the u32 diagonal accumulators (per CTA)
+NUM_SMS = 148
+
+
+def tc_eligible(M, K, N, width) -> bool:
+    return M * K * N >= TC_MIN_MACS and K >= 64 and (width == 64 or K <= TC_MAX_K or M * N >= 1 << 16)
 
 
 def _rup(x, m):
@@ -292,27 +298,39 @@ def limb_split(out, A, rows, cols, lda, plane, pitch, coff, trans):
     return out
 
 
-def gemm_limbs(C, A8, B8, batch, M, N, Mpad, Npad, Kpad, ldc, sC, accumulate, width):
+def auto_ksplit(tiles: int, batch: int, Kpad: int) -> int:
+    """Split K so small-output GEMMs still fill the SMs; every slice <= TC_MAX_K."""
+    nk = Kpad // 128
+    need = -(-Kpad // TC_MAX_K)
+    want = max(1, (2 * NUM_SMS) // max(1, tiles * batch))
+    return max(need, min(want, nk))
+
+
+def gemm_limbs(C, A8, B8, batch, M, N, Mpad, Npad, Kpad, ldc, sC, accumulate, width, ksplit=None):
     if _dry(C):
         return C
+    if ksplit is None:
+        ksplit = auto_ksplit((Mpad // 128) * (Npad // 64), batch, Kpad) if width == 64 else 1
     call("mpx_gemm_limbs", ptr(C), ptr(A8), ptr(B8), batch, M, N, Mpad, Npad, Kpad, ldc, sC,
-         int(accumulate), width)
+         int(accumulate), width, int(ksplit))
     return C
 
 
 def gemm_tc(C, A, B, batch, M, K, N, sA, sB, sC, accumulate, width):
     """u64 GEMM on the tcgen05 limb kernel: split operands into u8 limb planes
-    (scratch from the caching allocator), K chunked to <= TC_MAX_K."""
+    (scratch from the caching allocator). Width 64: one launch, split-K with
+    wrapping atomics; narrower rings: K chunks of <= TC_MAX_K accumulated."""
     if _dry(C):
         return C
     dev = C.device
     Mpad, Npad = _rup(M, 128), _rup(N, 64)
     a_ptr = A if isinstance(A, int) else ptr(A)
     b_ptr = B if isinstance(B, int) else ptr(B)
+    step = K if width == 64 else TC_MAX_K
     k0 = 0
     first = True
     while k0 < K:
-        kc = min(TC_MAX_K, K - k0)
+        kc = min(step, K - k0)
         Kpad = _rup(kc, 128)
         A8 = torch.zeros((batch, 8, Mpad, Kpad), dtype=torch.uint8, device=dev)
         B8 = torch.zeros((batch, 8, Npad, Kpad), dtype=torch.uint8, device=dev)

@@ -79,7 +79,7 @@ def batch_matmul(session, pairs) -> list[AShare]:
         Z = session.alloc((L, m, r))
         if not session.dry:
             Z.copy_(C)
-        if not session.dry and _use_tc(m, k, r):
+        if not session.dry and _use_tc(m, k, r, w):
             _beaver_matmul_tc(session, Z, D, E, A, B, L, m, k, r, w)
         else:
             K.gemm(Z, D, B.data_ptr(), L, m, k, r, 0, B.stride(0), m * r, True, w, simt=True)
@@ -91,8 +91,8 @@ def batch_matmul(session, pairs) -> list[AShare]:
     return out
 
 
-def _use_tc(m, k, r) -> bool:
-    return m * k * r >= K.TC_MIN_MACS and m >= 64 and r >= 32 and 2 * k <= K.TC_MAX_K
+def _use_tc(m, k, r, w=64) -> bool:
+    return K.tc_eligible(m, 2 * k, r, w) and (w == 64 or 2 * k <= K.TC_MAX_K)
 
 
 def _beaver_matmul_tc(session, Z, D, E, A, B, L, m, k, r, w):

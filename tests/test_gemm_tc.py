@@ -60,6 +60,17 @@ def test_all_ones_worst_case_k16384():
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("M,K,N", [(25, 147456, 20), (500, 16384, 50), (128, 40000, 10), (8, 3000, 700)])
+def test_split_k_skinny_shapes(M, K, N):
+    """conv-backward shapes: tiny M or N with long K, split-K atomics mod 2^64"""
+    rng = np.random.default_rng(M + K + N)
+    A = rng.integers(0, 1 << 64, (M, K), dtype=np.uint64)
+    B = rng.integers(0, 1 << 64, (K, N), dtype=np.uint64)
+    C0 = rng.integers(0, 1 << 64, (1, M, N), dtype=np.uint64)
+    assert np.array_equal(_run(A, B)[0], np.matmul(A, B))
+    assert np.array_equal(_run(A, B, acc=C0)[0], C0[0] + np.matmul(A, B))
+
+
 def test_k_chunking_beyond_16384():
     rng = np.random.default_rng(3)
     A = rng.integers(0, 1 << 64, (128, 20000), dtype=np.uint64)
