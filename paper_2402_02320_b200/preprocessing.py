@@ -176,6 +176,7 @@ class Dealer:
     def __init__(self, seed: int, n_parties: int, p_lo: int, L: int, device):
         self.seed, self.n, self.p_lo, self.L = seed, n_parties, p_lo, L
         self.device = torch.device(device)
+        self._out = None   # when set: write shares into these existing arrays
 
     def _e(self, *shape):
         return torch.empty(shape, dtype=torch.int64, device=self.device)
@@ -183,13 +184,18 @@ class Dealer:
     def _z(self, *shape):
         return torch.zeros(shape, dtype=torch.int64, device=self.device)
 
-    def _share_arith(self, secret, key, q, count, w):
-        out = self._e(self.L, count)
+    def _dst(self, name, shape, zero=False):
+        if self._out is not None and name in self._out:
+            return self._out[name]
+        return self._z(*shape) if zero else self._e(*shape)
+
+    def _share_arith(self, secret, key, q, count, w, name=None):
+        out = self._dst(name, (self.L, count))
         K.deal_share_arith(out, secret, key, q, count, self.n, self.p_lo, self.L, w)
         return out, q + (self.n - 1) * 2 * count
 
-    def _share_bits(self, secret, key, q, count):
-        out = self._z(self.L, _words(count))
+    def _share_bits(self, secret, key, q, count, name=None):
+        out = self._dst(name, (self.L, _words(count)), zero=True)
         K.deal_share_bits(out, secret, key, q, count, self.n, self.p_lo, self.L)
         return out, q + (self.n - 1) * ((count + 3) // 4)
 
@@ -203,7 +209,19 @@ class Dealer:
         K.philox_bits(out, key, q, count)
         return out, q + (count + 3) // 4
 
-    def generate(self, key: MaterialKey, count: int, need_bits: bool = True) -> dict:
+    def generate(self, key: MaterialKey, count: int, need_bits: bool = True, out: dict | None = None) -> dict:
+        """Deal ``count`` items of ``key``; with ``out`` (a previous result for
+        the same key and count) the shares are written in place, keeping
+        every device pointer stable (CUDA-graph replays)."""
+        if out is not None:
+            flat = {k: (v.view(self.L, -1) if k in ("a", "b", "c") and v.dim() > 2 else v) for k, v in out.items()}
+            self._out = flat
+        try:
+            return self._generate(key, count, need_bits)
+        finally:
+            self._out = None
+
+    def _generate(self, key: MaterialKey, count: int, need_bits: bool) -> dict:
         pk = dealer_philox_key(self.seed, key)
         w = key.width
         q = 0
@@ -212,9 +230,9 @@ class Dealer:
             b, q = self._elems(pk, q, count, w)
             c = self._e(count)
             K.ring_mul(c, a, b, count, w)
-            sa, q = self._share_arith(a, pk, q, count, w)
-            sb, q = self._share_arith(b, pk, q, count, w)
-            sc, q = self._share_arith(c, pk, q, count, w)
+            sa, q = self._share_arith(a, pk, q, count, w, "a")
+            sb, q = self._share_arith(b, pk, q, count, w, "b")
+            sc, q = self._share_arith(c, pk, q, count, w, "c")
             return {"a": sa, "b": sb, "c": sc}
         if key.kind == KIND_MATRIX_TRIPLE:                # preprocessing.py:146-152
             m, k, r = key.params
@@ -222,9 +240,9 @@ class Dealer:
             b, q = self._elems(pk, q, count * k * r, w)
             c = self._e(count * m * r)
             K.gemm(c, a, b, count, m, k, r, m * k, k * r, m * r, False, w)
-            sa, q = self._share_arith(a, pk, q, count * m * k, w)
-            sb, q = self._share_arith(b, pk, q, count * k * r, w)
-            sc, q = self._share_arith(c, pk, q, count * m * r, w)
+            sa, q = self._share_arith(a, pk, q, count * m * k, w, "a")
+            sb, q = self._share_arith(b, pk, q, count * k * r, w, "b")
+            sc, q = self._share_arith(c, pk, q, count * m * r, w, "c")
             L = self.L
             return {"a": sa.view(L, count, m, k), "b": sb.view(L, count, k, r),
                     "c": sc.view(L, count, m, r)}
@@ -233,27 +251,27 @@ class Dealer:
             b, q = self._bits(pk, q, count)
             c = self._z(a.numel())
             K.bits_op(c, a, b, 1, 1, a.numel(), 64)      # AND
-            sa, q = self._share_bits(a, pk, q, count)
-            sb, q = self._share_bits(b, pk, q, count)
-            sc, q = self._share_bits(c, pk, q, count)
+            sa, q = self._share_bits(a, pk, q, count, "a")
+            sb, q = self._share_bits(b, pk, q, count, "b")
+            sc, q = self._share_bits(c, pk, q, count, "c")
             return {"a": sa, "b": sb, "c": sc}
         if key.kind == KIND_DABIT:                        # preprocessing.py:160-164
             r, q = self._bits(pk, q, count)
             r_el = self._e(count)
             K.bits_flat_to_rows(r_el, r.data_ptr(), 0, count, 1)
-            arith, q = self._share_arith(r_el, pk, q, count, w)
-            bit, q = self._share_bits(r, pk, q, count)
+            arith, q = self._share_arith(r_el, pk, q, count, w, "arith")
+            bit, q = self._share_bits(r, pk, q, count, "bit")
             return {"arith": arith, "bit": bit}
         if key.kind == KIND_EDABIT:                       # preprocessing.py:165-170
             m = key.params[0]
             value, q = self._elems(pk, q, count, min(w, m))
-            arith, q = self._share_arith(value, pk, q, count, w)
-            out = {"arith": arith}
+            arith, q = self._share_arith(value, pk, q, count, w, "arith")
+            res = {"arith": arith}
             if need_bits:
                 flat = self._z(_words(count * m))
                 K.bits_rows_to_flat(flat, value, count, m)
-                out["bits"], q = self._share_bits(flat, pk, q, count * m)
-            return out
+                res["bits"], q = self._share_bits(flat, pk, q, count * m, "bits")
+            return res
         raise ValueError(f"unknown material kind {key.kind}")
 
 
@@ -377,16 +395,24 @@ class DemandCounter(MaterialStore):
 
 
 def device_store(seed: int, n_parties: int, demands: dict, parties=None, device="cuda",
-                 needs_bits: dict | None = None) -> MaterialStore:
-    """Deal every demanded key for the local ``parties`` (memory_stores, preprocessing.py:356-366)."""
+                 needs_bits: dict | None = None, into: MaterialStore | None = None) -> MaterialStore:
+    """Deal every demanded key for the local ``parties`` (memory_stores,
+    preprocessing.py:356-366). With ``into`` (a store dealt before for the same
+    demand) fresh material is written into its arrays in place and its
+    cursors are reset: every device pointer stays valid (CUDA graphs)."""
     parties = tuple(range(n_parties)) if parties is None else tuple(parties)
     if list(parties) != list(range(parties[0], parties[0] + len(parties))):
         raise ValueError("local parties must be contiguous")
-    store = MaterialStore(parties, n_parties, device)
+    store = into if into is not None else MaterialStore(parties, n_parties, device)
     dealer = Dealer(seed, n_parties, parties[0], len(parties), device)
     for key, count in sorted(demands.items(), key=lambda kv: kv[0].name()):
         if count <= 0:
             continue
         nb = True if needs_bits is None else needs_bits.get(key, key.kind != KIND_EDABIT)
-        store.add_material(key, count, dealer.generate(key, count, need_bits=nb))
+        if into is not None:
+            dealer.generate(key, count, need_bits=nb, out=into._arrays[key])
+        else:
+            store.add_material(key, count, dealer.generate(key, count, need_bits=nb))
+    if into is not None:
+        into.rewind()
     return store

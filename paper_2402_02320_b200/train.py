@@ -248,3 +248,54 @@ def simple_mlp(session, spec: InitSpec = InitSpec()) -> Model:
     return Model([Linear(session, 784, 128, rng=rng, name="fc1", spec=spec), ReLU(),
                   Linear(session, 128, 128, rng=rng, name="fc2", spec=spec), ReLU(),
                   Linear(session, 128, 10, rng=rng, name="fc3", spec=spec)])
+
+
+class GraphedStep:
+    """One secure training step captured in a CUDA graph and replayed.
+
+    The ~150 rounds / ~330 kernel launches of a LeNet step are issued once at
+    capture; a replay costs one graph launch. Every pointer the step touches is
+    stable: inputs and weights live in static buffers (updated weights are
+    copied back inside the graph), intermediates come from the graph's private
+    pool, and the dealer re-deals fresh material into the SAME store arrays
+    before each replay (``device_store(..., into=store)``, outside the graph).
+    """
+
+    def __init__(self, session, model: Model, x: AShare, y: AShare, lr_shift: int, demands: dict,
+                 needs_bits: dict, seed0: int):
+        from .preprocessing import device_store
+        self.s, self.model, self.lr_shift = session, model, lr_shift
+        self.demands, self.needs_bits = demands, needs_bits
+        self.params = [(layer, nm) for layer in model.layers for nm in ("W", "b") if hasattr(layer, nm)]
+        self.bufs = [getattr(layer, nm) for layer, nm in self.params]
+        self.x, self.y = x, y
+        session.store = device_store(seed0, session.n_parties, demands, parties=session.parties,
+                                     device=session.device, needs_bits=needs_bits)
+        # warm-up (eager) step: first-use work (attributes, schedules) happens here
+        side = torch.cuda.Stream(session.device)
+        side.wait_stream(torch.cuda.current_stream(session.device))
+        with torch.cuda.stream(side):
+            model.train_step(session, x, y, lr_shift)
+            self._writeback()
+        torch.cuda.current_stream(session.device).wait_stream(side)
+        torch.cuda.synchronize(session.device)
+        session.store.rewind()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.logits = model.train_step(session, x, y, lr_shift)
+            self._writeback()
+
+    def _writeback(self):
+        for (layer, nm), buf in zip(self.params, self.bufs):
+            cur = getattr(layer, nm)
+            if cur is not buf:
+                buf.values.copy_(cur.values)
+                setattr(layer, nm, buf)
+
+    def step(self, seed: int) -> AShare:
+        """Re-deal fresh material in place, replay the captured step."""
+        from .preprocessing import device_store
+        device_store(seed, self.s.n_parties, self.demands, parties=self.s.parties, device=self.s.device,
+                     needs_bits=self.needs_bits, into=self.s.store)
+        self.graph.replay()
+        return self.logits

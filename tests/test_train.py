@@ -153,3 +153,37 @@ def test_simple_mlp_training_tracks_plaintext():
     sec, pla = run_secure(), run_plain()
     assert sec[-1] < sec[0] * 0.7
     assert np.allclose(sec, pla, rtol=0.05, atol=0.05), (sec, pla)
+
+
+@pytest.mark.gpu
+def test_graphed_lenet_steps_equal_eager_steps():
+    """CUDA-graph replays (in-place re-dealt material) == eager steps, bit for bit."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2402_02320_b200 import train
+    from paper_2402_02320_b200.preprocessing import DemandCounter, device_store
+    from paper_2402_02320_b200.session import SimSession
+    n, B, T = 3, 8, 3
+    x, y = _data(B, (1, 28, 28))
+    c = DemandCounter(tuple(range(n)), n)
+    _gpu_lenet_step(SimSession(n, c), x, y, B)
+
+    s1 = SimSession(n, None)
+    m1 = train.lenet(s1)
+    xs1, ys1 = s1.share_fixed(x, 64, 23, _key("x")), s1.share_fixed(y, 64, 23, _key("y"))
+    for t in range(T + 1):
+        s1.store = device_store(40 + t, n, c.demands, needs_bits=c.needs_bits)
+        l1 = m1.train_step(s1, xs1, ys1, 5)
+
+    s2 = SimSession(n, None)
+    m2 = train.lenet(s2)
+    xs2, ys2 = s2.share_fixed(x, 64, 23, _key("x")), s2.share_fixed(y, 64, 23, _key("y"))
+    g = train.GraphedStep(s2, m2, xs2, ys2, 5, c.demands, c.needs_bits, seed0=40)
+    for t in range(1, T + 1):
+        l2 = g.step(40 + t)
+    torch.cuda.synchronize()
+    assert torch.equal(l1.values, l2.values)
+    for a, b in zip(m1.layers, m2.layers):
+        for nm in ("W", "b"):
+            if hasattr(a, nm):
+                assert torch.equal(getattr(a, nm).values, getattr(b, nm).values), (type(a).__name__, nm)

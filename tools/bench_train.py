@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--batch", type=int, default=128)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--profile", action="store_true")
+    ap.add_argument("--graph", action="store_true")
     a = ap.parse_args()
     n, B = a.parties, a.batch
     shape = (1, 28, 28) if a.model == "lenet" else (784,)
@@ -35,6 +36,26 @@ def main():
     model = build(s)
     xs, ys = s.share_fixed(x, 64, 23, [1, 2]), s.share_fixed(y, 64, 23, [3, 4])
     times, deal, host = [], [], []
+    if a.graph:
+        g = train.GraphedStep(s, model, xs, ys, 5, c.demands, c.needs_bits, seed0=50)
+        for t in range(a.steps + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            from paper_2402_02320_b200.preprocessing import device_store as _ds
+            _ds(60 + t, n, c.demands, needs_bits=c.needs_bits, into=s.store)
+            torch.cuda.synchronize()
+            deal.append(time.perf_counter() - t0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            h0 = time.perf_counter()
+            e0.record()
+            g.graph.replay()
+            e1.record()
+            h1 = time.perf_counter()
+            torch.cuda.synchronize()
+            if t:
+                times.append(e0.elapsed_time(e1))
+                host.append((h1 - h0) * 1e3)
+        a.steps = -1
     for t in range(a.steps + 1):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -53,10 +74,10 @@ def main():
         if t:
             times.append(e0.elapsed_time(e1))
             host.append((h1 - h0) * 1e3)
-    out = {"model": a.model, "parties": n, "batch": B, "ms_per_step": float(np.mean(times)),
+    out = {"graph": a.graph, "model": a.model, "parties": n, "batch": B, "ms_per_step": float(np.mean(times)),
            "steps_per_s": 1e3 / float(np.mean(times)), "host_issue_ms": float(np.mean(host)),
            "dealer_ms": 1e3 * float(np.mean(deal[1:])), "dry_run_s": dry_s,
-           "rounds_per_step": s.metrics.total.rounds // (a.steps + 1),
+           "rounds_per_step": s.metrics.total.rounds // max(1, a.steps + 1),
            "launches_per_step": None}
     if a.profile:
         prof = _lib.profile_end()
