@@ -1,19 +1,23 @@
 #!/usr/bin/env python
-"""Benchmark: secure fixed-point Reciprocal (paper Alg. 1) on 2^24 elements,
-the BASELINE.json cfg-5 party-scaling workload, on B200.
+"""Benchmark: secure LeNet training steps/s (BASELINE.json configs[1]) on B200,
+plus the cfg-5 party-scaling sweep (Reciprocal / Exp / Log on 2^24 elements,
+Beaver matmul 4096^2) and the Simple-MLP training step (configs[0]).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-* N = 1: the 1-GPU all-parties-simulated run (2 parties on cuda:0).
-* N > 1 (torchrun, one rank per GPU): one party per GPU, openings over NCCL.
+* N = 1: the 1-GPU all-parties-simulated run: 3 parties on cuda:0, each
+  training step captured once in a CUDA graph and replayed.
+* N > 1 (torchrun, one rank per GPU): N parties, one per GPU, openings over
+  NCCL, eager steps.
 * ``--impl reference``: the reference algorithm's CPU implementation (the
   numpy oracle port under ``oracle/``; the Python reference itself cannot
-  travel to the GPU box) on the host cores, same metric, bounded sample.
+  travel to the GPU box) on all host cores, same metric, bounded sample.
 
-A step = one online-phase secure reciprocal over the whole batch. The trusted
-dealer (on-device Philox, bit-exact with the reference's numpy dealer) deals
-fresh single-use material before every step, outside the timed region, and
-is reported separately (the reference and the paper time the online phase).
+A step = one secure SGD step of LeNet (forward, softmax-CE, backward, update)
+on a batch of 128 synthetic 28x28 images, weights secret-shared. The trusted
+dealer (on-device Philox, bit-exact with the reference's numpy dealer)
+re-deals fresh single-use material before every step outside the timed
+region (reported as dealer_ms_per_step; the paper times the online phase).
 Prints ONE JSON line on rank 0.
 """
 
@@ -35,8 +39,11 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-METRIC = "secure Reciprocal throughput, online phase (cfg5 party-scaling sweep)"
-UNIT = "elements/s"
+METRIC = "secure CNN train steps/s: LeNet, batch 128 (BASELINE configs[1])"
+UNIT = "steps/s"
+RECIP_UNIT = "elements/s"
+BATCH = 128
+LR_SHIFT = 5
 SEED = 7
 FRAC = 23
 WIDTH = 64
@@ -100,6 +107,49 @@ def cpu_reference(sample: int, n_parties: int, cores: int | None = None, reps: i
             rate = chunk * cores / online
             best = rate if best is None else max(best, rate)
     return best, cores, online
+
+
+def lenet_data(B: int, seed: int = 11):
+    """SURVEY §8d cfg 2: x ~ U(0,1) 28x28x1, labels uniform in 0..9 (one-hot)."""
+    rng = np.random.default_rng(seed)
+    return rng.uniform(0.0, 1.0, (B, 1, 28, 28)), np.eye(10)[rng.integers(0, 10, B)]
+
+
+def _cpu_lenet_worker(args):
+    batch, n_parties, seed = args
+    import oracle as O
+    from oracle import train_sim as OT
+    x, y = lenet_data(batch, seed)
+
+    def step(s):
+        m = OT.lenet(s)
+        xs = OT.share_fixed(s, x, WIDTH, FRAC, label_key("share:x"))
+        ys = OT.share_fixed(s, y, WIDTH, FRAC, label_key("share:y"))
+        return m, xs, ys
+
+    dry = O.Sim(n_parties, O.Demand(n_parties))
+    m, xs, ys = step(dry)
+    m.train_step(dry, xs, ys, LR_SHIFT)
+    live = O.Sim(n_parties, O.Store(seed, n_parties, dry.store.demands))
+    m, xs, ys = step(live)
+    t0 = time.perf_counter()
+    m.train_step(live, xs, ys, LR_SHIFT)
+    return time.perf_counter() - t0
+
+
+def cpu_lenet_reference(n_parties: int, cores: int | None = None):
+    """The oracle port of the reference algorithm, one LeNet training step of
+    batch 128 split data-parallel over all host cores (one process per core,
+    batch 128 / cores each; the slowest process bounds the step).
+    Returns (steps/s, cores, seconds, per-process batch)."""
+    cores = cores or os.cpu_count() or 1
+    per = max(1, BATCH // cores)
+    procs = -(-BATCH // per)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(min(cores, procs)) as pool:
+        times = pool.map(_cpu_lenet_worker, [(per, n_parties, 11 + i) for i in range(procs)])
+    secs = max(times) * (-(-procs // min(cores, procs)))
+    return 1.0 / secs, min(cores, procs), secs, per
 
 
 # ---------------------------------------------------------------------------
@@ -206,6 +256,8 @@ def alg_bytes(name, a):
             return L * rows * cols * 8 + L * rows * 8
         if name == "mpx_bits_gather":
             return 16 * a[4]
+        if name == "mpx_gemm_limbs":     # int8 ops, not bytes: see roofline_for
+            return None
         if name in ("mpx_reciprocal_fused", "mpx_exp_fused", "mpx_log_fused"):
             from paper_2402_02320_b200.fused import material_bytes
             kind, n, L, calls = a
@@ -349,125 +401,38 @@ class DistGroup:
             self.dist.destroy_process_group()
 
 
-def run_b200(args, group=None):
-    import torch
-    import torch.distributed as dist
-
-    import paper_2402_02320_b200 as G
-    from paper_2402_02320_b200 import _lib
-    from paper_2402_02320_b200.preprocessing import DemandCounter, device_store
-    from paper_2402_02320_b200.session import PartySession, SimSession
-    from paper_2402_02320_b200.streaming import run_host
-
-    group = group or DistGroup(torch, dist)
-    world, rank, local = group.world, group.rank, group.local
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        # before CUDA initialisation: the pool forks numpy-only workers
-        rate, cores, secs = cpu_reference(args.cpu_sample, 2)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"oracle/ numpy port of the reference, online reciprocal on {args.cpu_sample} "
-                         f"elements (n=2) split over {cores} processes, slowest {secs:.2f} s"}
-    if world != args.gpus:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    group.init(dev)
-    n_parties = 2 if world == 1 else world
-    parties = tuple(range(n_parties)) if world == 1 else (rank,)
-    N = args.elems
-    xs = workload_inputs(N)
-    enc = encode_np(xs)
-    key = label_key("share:x")
-
-    def make_session(store):
-        if world == 1:
-            return SimSession(n_parties, store, device=dev)
-        return PartySession(rank, n_parties, group.comm(), store, device=dev)
-
-    def barrier():
-        group.barrier()
-
-    # dry run (meta tensors): exact demand
-    counter = DemandCounter(parties, n_parties)
-    s_dry = make_session(counter)
-    G.reciprocal(s_dry, s_dry.share_ring(enc, WIDTH, FRAC, key))
-
-    def deal(step):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        st = device_store(1000 + step, n_parties, counter.demands, parties=parties, device=dev,
-                          needs_bits=counter.needs_bits)
-        torch.cuda.synchronize()
-        return st, time.perf_counter() - t0
-
-    # input shares (device) + pinned host copies for the e2e leg
-    s0 = make_session(None)
-    x_sh = s0.share_ring(enc, WIDTH, FRAC, key)
-    torch.cuda.synchronize()
-    x_host = x_sh.values.cpu().pin_memory()
-
-    online_ms, dealer_s = [], []
-    clocks = ClockSampler(local)
-    clocks.start()
-    store = None
-    launches_timed = 0
-    t_window = [None, None]
-    for step in range(args.warmup + args.steps):
-        del store
-        store, dt = deal(step)
-        dealer_s.append(dt)
-        sess = make_session(store)
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        barrier()
-        torch.cuda.synchronize()
-        timed = step >= args.warmup
-        if timed and t_window[0] is None:
-            t_window[0] = time.time()
-        l0 = _lib.LAUNCHES
-        ev0.record()
-        y = G.reciprocal(sess, x_sh)
-        ev1.record()
-        torch.cuda.synchronize()
-        barrier()
-        if timed:
-            online_ms.append(ev0.elapsed_time(ev1))
-            launches_timed += _lib.LAUNCHES - l0
-            t_window[1] = time.time()
-    clk = clocks.stop(t_window)
-    total_ms = group.max(float(sum(online_ms)), dev)
-    ms_per_step = total_ms / args.steps
-    value = N * args.steps / (total_ms / 1e3)
-
-    # correctness spot check on the last step (opened vs float reference)
-    y_open = sess.open_fixed(y)
-    xq = encode_np(xs).view(np.int64) / float(1 << FRAC)
-    rel = float(np.max(np.abs(y_open - 1 / xq) * np.abs(xq)))
-
-    # profiled pass: per-kernel CUDA-event times over one more online step
-    del store
-    store, _ = deal(10_000)
-    sess = make_session(store)
-    torch.cuda.synchronize()
-    _lib.profile_begin()
-    G.reciprocal(sess, x_sh)
-    torch.cuda.synchronize()
-    prof = _lib.profile_end()
+def _profile_kernels(prof):
     per = {}
     for name, a, e0, e1 in prof:
-        d = per.setdefault(name, {"ms": 0.0, "n": 0, "bytes": 0, "bytes_known": True})
+        d = per.setdefault(name, {"ms": 0.0, "n": 0, "bytes": 0, "bytes_known": True, "ops": 0})
         d["ms"] += e0.elapsed_time(e1)
         d["n"] += 1
+        if name == "mpx_gemm_limbs":
+            # (C, A8, B8, batch, M, N, Mpad, Npad, Kpad, ...): 36 limb MACs per ring MAC
+            d["ops"] += 2 * 36 * a[3] * a[4] * a[5] * a[8]
         b = alg_bytes(name, a)
         if b is None:
             d["bytes_known"] = False
         else:
             d["bytes"] += b
+    return per
+
+
+def roofline_for(per, int8_peak=None):
+    """Roofline object of the dominant kernel of one profiled step."""
     step_ms = sum(d["ms"] for d in per.values())
     dom_name = max(per, key=lambda k: per[k]["ms"])
     dom = per[dom_name]
+    common = {"kernel": dom_name, "launches": dom["n"], "avg_launch_us": 1e3 * dom["ms"] / dom["n"],
+              "share_of_step": dom["ms"] / step_ms}
+    if dom_name == "mpx_gemm_limbs":
+        ach = dom["ops"] / (dom["ms"] / 1e3) / 1e12
+        return dict(common, bound="tensor", achieved=ach, peak=int8_peak, unit="TOPS int8",
+                    peak_kind="measured in-run: torch._int_mm int8 8192^3 (cuBLASLt), burst",
+                    frac=(ach / int8_peak) if int8_peak else None, traffic=None,
+                    alg_ops_per_launch=dom["ops"] // dom["n"])
     peak, peak_kind = _read_peaks()
-    achieved = dom["bytes"] / (dom["ms"] / 1e3) / 1e9 if dom["bytes_known"] else None
+    ach = dom["bytes"] / (dom["ms"] / 1e3) / 1e9 if dom["bytes_known"] else None
     traffic = None
     tpath = os.path.join(REPO, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -475,84 +440,292 @@ def run_b200(args, group=None):
             traffic = json.load(open(tpath)).get(dom_name)
         except ValueError:
             traffic = None
-    roofline = {"kernel": dom_name, "bound": "hbm", "achieved": achieved, "peak": peak,
-                "peak_kind": peak_kind, "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None,
-                "traffic": traffic, "launches": dom["n"],
-                "avg_launch_us": 1e3 * dom["ms"] / dom["n"],
-                "alg_bytes_per_launch": dom["bytes"] // dom["n"],
-                "share_of_step": dom["ms"] / step_ms}
-    all_bytes = sum(d["bytes"] for d in per.values() if d["bytes_known"])
-    kernels = {k: {"ms": round(v["ms"], 3), "launches": v["n"],
-                   "GBps": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1) if v["bytes_known"] and v["ms"] else None}
-               for k, v in sorted(per.items(), key=lambda kv: -kv[1]["ms"])}
+    return dict(common, bound="hbm", achieved=ach, peak=peak, peak_kind=peak_kind, unit="GB/s",
+                frac=(ach / peak) if ach else None, traffic=traffic,
+                alg_bytes_per_launch=dom["bytes"] // dom["n"])
 
-    # e2e through the public API with host buffers: streaming.run_host overlaps
-    # H2D of chunk k+1, the secure op on chunk k and D2H of chunk k-1
-    e2e_ms = []
-    store = None
-    y_host = torch.empty(x_host.shape, dtype=torch.int64).pin_memory()
-    for step in range(args.warmup + args.steps):
+
+def _kernel_table(per):
+    return {k: {"ms": round(v["ms"], 3), "launches": v["n"],
+                "GBps": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1) if v["bytes_known"] and v["ms"] else None}
+            for k, v in sorted(per.items(), key=lambda kv: -kv[1]["ms"])}
+
+
+def reciprocal_entry(torch, G, make_session, parties, n_parties, dev, group, steps, warmup):
+    """cfg 5: secure Reciprocal on 2^24 elements (one fused kernel in sim mode)."""
+    from paper_2402_02320_b200 import _lib
+    from paper_2402_02320_b200.preprocessing import DemandCounter, device_store
+    N = 1 << 24
+    xs = workload_inputs(N)
+    enc = encode_np(xs)
+    key = label_key("share:x")
+    counter = DemandCounter(parties, n_parties)
+    sd = make_session(counter)
+    G.reciprocal(sd, sd.share_ring(enc, WIDTH, FRAC, key))
+    x_sh = make_session(None).share_ring(enc, WIDTH, FRAC, key)
+    times, store = [], None
+    for step in range(warmup + steps + 1):
         del store
-        store, _ = deal(20_000 + step)
+        store = device_store(3000 + step, n_parties, counter.demands, parties=parties, device=dev,
+                             needs_bits=counter.needs_bits)
         sess = make_session(store)
-        barrier()
+        group.barrier()
         torch.cuda.synchronize()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record()
-        run_host(lambda s, x: G.reciprocal(s, x), sess, x_host, WIDTH, FRAC, chunks=args.chunks, y_host=y_host)
-        ev1.record()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        last = step == warmup + steps
+        if last:
+            _lib.profile_begin()
+        e0.record()
+        y = G.reciprocal(sess, x_sh)
+        e1.record()
         torch.cuda.synchronize()
-        barrier()
+        if last:
+            per = _profile_kernels(_lib.profile_end())
+        elif step >= warmup:
+            times.append(e0.elapsed_time(e1))
+    ms = group.max(float(np.mean(times)), dev)
+    y_open = sess.open_fixed(y)
+    xq = enc.view(np.int64) / float(1 << FRAC)
+    del store
+    return {"elements": N, "ms_per_op": ms, "elements_per_s": N / (ms / 1e3), "steps": steps,
+            "max_rel_err": float(np.max(np.abs(y_open - 1 / xq) * np.abs(xq))),
+            "roofline": roofline_for(per), "kernels": _kernel_table(per)}
+
+
+def mlp_entry(torch, dev, steps, warmup):
+    """configs[0]: 2-party Simple MLP (784-128-128-10) forward+backward+SGD, batch 128."""
+    from paper_2402_02320_b200 import train
+    from paper_2402_02320_b200.preprocessing import DemandCounter, device_store
+    from paper_2402_02320_b200.session import SimSession
+    n = 2
+    rng = np.random.default_rng(5)
+    x, y = rng.normal(0, 1, (BATCH, 784)), np.eye(10)[rng.integers(0, 10, BATCH)]
+    c = DemandCounter((0, 1), n)
+    sd = SimSession(n, c, device=dev)
+    train.simple_mlp(sd).train_step(sd, sd.share_fixed(x, WIDTH, FRAC, [1, 1]), sd.share_fixed(y, WIDTH, FRAC, [1, 2]),
+                                    LR_SHIFT)
+    s = SimSession(n, None, device=dev)
+    m = train.simple_mlp(s)
+    g = train.GraphedStep(s, m, s.share_fixed(x, WIDTH, FRAC, [1, 1]), s.share_fixed(y, WIDTH, FRAC, [1, 2]),
+                          LR_SHIFT, c.demands, c.needs_bits, seed0=70)
+    times = []
+    for t in range(warmup + steps):
+        device_store(71 + t, n, c.demands, device=dev, needs_bits=c.needs_bits, into=s.store)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        if t >= warmup:
+            times.append(e0.elapsed_time(e1))
+    ms = float(np.mean(times))
+    return {"model": "Simple MLP 784-128-128-10", "parties": n, "batch": BATCH, "ms_per_step": ms,
+            "steps_per_s": 1e3 / ms, "cuda_graph": True}
+
+
+def run_b200(args, group=None):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2402_02320_b200 as G
+    from paper_2402_02320_b200 import _lib, train
+    from paper_2402_02320_b200.preprocessing import DemandCounter, device_store
+    from paper_2402_02320_b200.session import PartySession, SimSession
+
+    group = group or DistGroup(torch, dist)
+    world, rank, local = group.world, group.rank, group.local
+    n_parties = 3 if world == 1 else world
+    cpu = cpu_recip = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        # before CUDA initialisation: the pools fork numpy-only workers
+        sps, cores, secs, per = cpu_lenet_reference(n_parties)
+        cpu = {"value": sps, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"oracle/ numpy port of the reference algorithm: one LeNet train step of batch {BATCH} "
+                         f"split over {cores} processes (batch {per} each, n={n_parties}), online phase, "
+                         f"{secs:.1f} s"}
+        if not args.no_sweep:
+            rate, rcores, rsecs = cpu_reference(args.cpu_sample, 2)
+            cpu_recip = {"value": rate, "unit": RECIP_UNIT, "cores": rcores, "kind": "port",
+                         "sample": f"online reciprocal on {args.cpu_sample} elements (n=2) over {rcores} "
+                                   f"processes, slowest {rsecs:.2f} s"}
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group.init(dev)
+    parties = tuple(range(n_parties)) if world == 1 else (rank,)
+
+    def make_session(store):
+        if world == 1:
+            return SimSession(n_parties, store, device=dev)
+        return PartySession(rank, n_parties, group.comm(), store, device=dev)
+
+    B = args.batch
+    x, y = lenet_data(B)
+    kx, ky = label_key("share:x"), label_key("share:y")
+    # dry run: exact demand of one training step
+    counter = DemandCounter(parties, n_parties)
+    sd = make_session(counter)
+    train.lenet(sd).train_step(sd, sd.share_fixed(x, WIDTH, FRAC, kx), sd.share_fixed(y, WIDTH, FRAC, ky), LR_SHIFT)
+    sess = make_session(None)
+    model = train.lenet(sess)
+    xs, ys = sess.share_fixed(x, WIDTH, FRAC, kx), sess.share_fixed(y, WIDTH, FRAC, ky)
+    launches_per_step = None
+    graph = None
+    if world == 1:
+        l0 = _lib.LAUNCHES
+        graph = train.GraphedStep(sess, model, xs, ys, LR_SHIFT, counter.demands, counter.needs_bits, seed0=1)
+        launches_per_step = (_lib.LAUNCHES - l0) // 2          # warm-up step + captured step
+    else:
+        sess.store = device_store(1, n_parties, counter.demands, parties=parties, device=dev,
+                                  needs_bits=counter.needs_bits)
+
+    def redeal(seed):
+        device_store(seed, n_parties, counter.demands, parties=parties, device=dev,
+                     needs_bits=counter.needs_bits, into=sess.store)
+
+    def one_step():
+        if graph is not None:
+            graph.graph.replay()
+            return graph.logits
+        return model.train_step(sess, xs, ys, LR_SHIFT)
+
+    losses = []
+
+    def loss_of(logits, yy):
+        z = sess.open_fixed(logits)
+        z = z - z.max(1, keepdims=True)
+        p = np.exp(z) / np.exp(z).sum(1, keepdims=True)
+        return float(-np.mean(np.log(p[np.arange(len(yy)), yy.argmax(1)] + 1e-12)))
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    step_ms, deal_ms, t_window = [], [], [None, None]
+    for step in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        torch.cuda.synchronize()
+        redeal(100 + step)
+        torch.cuda.synchronize()
+        deal_ms.append(1e3 * (time.perf_counter() - t0))
+        group.barrier()
+        torch.cuda.synchronize()
+        if step >= args.warmup and t_window[0] is None:
+            t_window[0] = time.time()
+        l0 = _lib.LAUNCHES
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        logits = one_step()
+        e1.record()
+        torch.cuda.synchronize()
+        group.barrier()
+        if launches_per_step is None:
+            launches_per_step = _lib.LAUNCHES - l0
         if step >= args.warmup:
-            e2e_ms.append(ev0.elapsed_time(ev1))
-    e2e_total = group.max(float(sum(e2e_ms)), dev)
-    h2d = int(x_host.numel() * 8)
-    d2h = int(y_host.numel() * 8)
+            step_ms.append(e0.elapsed_time(e1))
+            t_window[1] = time.time()
+        if step in (0, args.warmup + args.steps - 1):
+            losses.append(loss_of(logits, y))
+    clk = clocks.stop(t_window)
+    total_ms = group.max(float(sum(step_ms)), dev)
+    value = args.steps / (total_ms / 1e3)
+
+    # profiled eager step (per-kernel CUDA events): dominant kernel + roofline
+    redeal(9000)
+    torch.cuda.synchronize()
+    _lib.profile_begin()
+    model.train_step(sess, xs, ys, LR_SHIFT)
+    torch.cuda.synchronize()
+    per = _profile_kernels(_lib.profile_end())
+    if graph is not None:
+        graph._writeback()
+    int8_pk = int8_peak_tops(torch) if world == 1 else None
+    roofline = roofline_for(per, int8_pk)
+
+    # e2e through the public API with host buffers: H2D of the step's input
+    # shares into the step's (static) input tensors, the step, D2H of the logits
+    x_host = xs.values.cpu().pin_memory()
+    y_host = ys.values.cpu().pin_memory()
+    out_host = None
+    e2e = []
+    for step in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        redeal(20_000 + step)
+        group.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        xs.values.copy_(x_host, non_blocking=True)
+        ys.values.copy_(y_host, non_blocking=True)
+        logits = one_step()
+        if out_host is None:
+            out_host = torch.empty(logits.values.shape, dtype=torch.int64).pin_memory()
+        out_host.copy_(logits.values, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        group.barrier()
+        if step >= args.warmup:
+            e2e.append(e0.elapsed_time(e1))
+    e2e_total = group.max(float(sum(e2e)), dev)
 
     sweep = {}
     if not args.no_sweep:
+        sweep["reciprocal"] = reciprocal_entry(torch, G, make_session, (0, 1) if world == 1 else parties,
+                                               2 if world == 1 else n_parties, dev, group, 3, 2)
+        sweep["reciprocal"]["cpu_baseline"] = cpu_recip
+        ps = (0, 1) if world == 1 else parties
+        np_ = 2 if world == 1 else n_parties
+
+        def mk2(store):
+            if world == 1:
+                return SimSession(2, store, device=dev)
+            return PartySession(rank, n_parties, group.comm(), store, device=dev)
         for nm in ("exp", "log", "matmul"):
-            sweep[nm] = sweep_entry(torch, G, make_session, parties, n_parties, dev, nm)
-        if world == 1:
-            pk = int8_peak_tops(torch)
+            sweep[nm] = sweep_entry(torch, G, mk2, ps, np_, dev, nm)
+        if int8_pk:
             mm = sweep["matmul"]
             mm["roofline"] = {"bound": "tensor", "kernel": "mpx_gemm_limbs (tcgen05 kind::i8)",
-                              "achieved": mm["gemm_kernel_ms"] and mm["gemm_int8_TOPS"], "peak": pk,
+                              "achieved": mm.get("gemm_int8_TOPS"), "peak": int8_pk,
                               "peak_kind": "measured in-run: torch._int_mm int8 8192^3 (cuBLASLt), burst",
                               "unit": "TOPS int8",
-                              "frac": (mm["gemm_int8_TOPS"] / pk) if mm.get("gemm_int8_TOPS") else None}
+                              "frac": (mm["gemm_int8_TOPS"] / int8_pk) if mm.get("gemm_int8_TOPS") else None}
+        if world == 1:
+            sweep["mlp_train"] = mlp_entry(torch, dev, 5, 3)
 
+    line = None
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64 (Z_2^64 ring)",
-            "data": "synthetic x = +-2^U(-8,8), fixed seed",
-            "config": {"workload": "cfg5 party-scaling sweep: secure Reciprocal (Alg. 1) on 2^24 elements",
-                       "elements": N, "ring_width": WIDTH, "frac": FRAC, "parties": n_parties,
-                       "mode": "sim: all parties on 1 GPU" if world == 1 else "one party per GPU, NCCL",
-                       "rounds_per_step": 37,
-                       "l2": "no flush needed: shares + dealer material ~40 GB per step >> 126 MB L2",
-                       "dealer": "fresh on-device material before every step, outside the timed region"},
-            "e2e": {"value": N * args.steps / (e2e_total / 1e3), "unit": UNIT,
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": e2e_total / args.steps,
-                    "how": f"streaming.run_host: pinned host shares, {args.chunks} chunks, H2D/compute/D2H "
-                           "overlapped on 3 CUDA streams, one protocol call per chunk"},
-            "gpu_launches": launches_timed,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64 (Z_2^64 fixed point, p=23)",
+            "data": "synthetic: x ~ U(0,1) 128x1x28x28, uniform labels; Kaiming-init secret weights",
+            "config": {"workload": "configs[1]: secure LeNet training step (conv20-5x5, avgpool, ReLU, "
+                                   "conv50-5x5, avgpool, ReLU, FC800x500, ReLU, FC500x10; softmax-CE; SGD "
+                                   "lr 2^-5)",
+                       "parties": n_parties, "batch": B, "frac": FRAC, "ring_width": WIDTH,
+                       "mode": ("sim: all parties on 1 GPU, step captured in one CUDA graph" if world == 1
+                                else "one party per GPU, NCCL openings, eager"),
+                       "l2": "working set > L2 per step (material ~0.7 GB, re-dealt in place each step)",
+                       "dealer": "fresh on-device material re-dealt in place before every step, outside "
+                                 "the timed region"},
+            "e2e": {"value": args.steps / (e2e_total / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": int(x_host.numel() * 8 + y_host.numel() * 8),
+                    "d2h_bytes_per_step": int(out_host.numel() * 8), "ms_per_step": e2e_total / args.steps,
+                    "how": "pinned host input shares -> step input tensors (H2D), the train step, logits "
+                           "shares -> pinned host (D2H), all inside the CUDA-event window"},
+            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches_per_step": launches_per_step,
             "clocks": clk,
             "roofline": roofline,
-            "alg_bytes_per_step": all_bytes,
-            "step_hbm_GBps": all_bytes / (step_ms / 1e3) / 1e9,
-            "dealer_ms_per_step": 1e3 * float(np.mean(dealer_s)),
-            "max_rel_err": rel,
-            "kernels": kernels,
+            "rounds_per_step": sd.metrics.total.rounds,
+            "dealer_ms_per_step": float(np.mean(deal_ms)),
+            "loss_first_last": losses,
+            "kernels": _kernel_table(per),
             "cpu_baseline": cpu,
             "sweep": sweep,
         }
     group.close()
-    return line if rank == 0 else None
+    return line
 
 
 def run_reference(args):
@@ -560,24 +733,23 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    n_parties = 2 if world == 1 else world
-    rates = []
-    cores = None
+    n_parties = 3 if world == 1 else world
+    rates, cores, secs, per = [], None, None, None
     for step in range(args.warmup + args.steps):
-        rate, cores, secs = cpu_reference(args.cpu_sample, n_parties)
+        sps, cores, secs, per = cpu_lenet_reference(n_parties)
         if step >= args.warmup:
-            rates.append(rate)
+            rates.append(sps)
     value = float(np.mean(rates))
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * (1 << 24) / value, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64 (Z_2^64 ring)", "impl": "reference",
-            "data": "synthetic x = +-2^U(-8,8), fixed seed",
-            "config": {"workload": "cfg5 party-scaling sweep: secure Reciprocal (Alg. 1) on 2^24 elements",
-                       "elements": 1 << 24, "ring_width": WIDTH, "frac": FRAC, "parties": n_parties,
+            "warmup": args.warmup, "ms_per_step": 1e3 / value, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64 (Z_2^64 fixed point, p=23)", "impl": "reference",
+            "data": "synthetic: x ~ U(0,1) 128x1x28x28, uniform labels; Kaiming-init secret weights",
+            "config": {"workload": "configs[1]: secure LeNet training step", "parties": n_parties,
+                       "batch": BATCH, "frac": FRAC, "ring_width": WIDTH,
                        "mode": "CPU: reference algorithm (numpy oracle port), all host cores"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{args.cpu_sample} elements per step (bounded sample of the 2^24 "
-                                       f"workload), online phase, n={n_parties}"},
+                             "sample": f"each step: batch {BATCH} split over {cores} processes (batch {per} "
+                                       f"each), online phase"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
@@ -588,7 +760,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--elems", type=int, default=1 << 24)
+    ap.add_argument("--batch", type=int, default=BATCH)
     ap.add_argument("--cpu-sample", type=int, default=1 << 20)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")

@@ -9,6 +9,7 @@ import threading
 import contextlib
 import types
 
+import numpy as np
 import pytest
 import torch
 
@@ -49,7 +50,7 @@ def test_bench_party_path_two_threads():
     hub = ThreadHub(2)
     hub.barrier = threading.Barrier(2, timeout=300)
     hub.vals = [0.0, 0.0]
-    args = types.SimpleNamespace(gpus=2, steps=2, warmup=1, elems=1 << 14, cpu_sample=0, no_cpu=True,
+    args = types.SimpleNamespace(gpus=2, steps=2, warmup=1, batch=8, cpu_sample=0, no_cpu=True,
                                  no_sweep=True, chunks=4, impl="b200")
     outs, errs = {}, {}
 
@@ -71,6 +72,6 @@ def test_bench_party_path_two_threads():
     assert outs[1] is None
     json.dumps(line)
     assert line["n_gpus"] == 2 and line["config"]["parties"] == 2
-    assert line["max_rel_err"] < 1e-4
+    assert all(np.isfinite(line["loss_first_last"]))
     assert line["value"] > 0 and line["e2e"]["value"] > 0
-    assert line["gpu_launches"] > 37
+    assert line["gpu_launches_per_step"] > 100
