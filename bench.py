@@ -670,9 +670,6 @@ def run_b200(args, group=None):
 
     sweep = {}
     if not args.no_sweep:
-        sweep["reciprocal"] = reciprocal_entry(torch, G, make_session, (0, 1) if world == 1 else parties,
-                                               2 if world == 1 else n_parties, dev, group, 3, 2)
-        sweep["reciprocal"]["cpu_baseline"] = cpu_recip
         ps = (0, 1) if world == 1 else parties
         np_ = 2 if world == 1 else n_parties
 
@@ -680,6 +677,8 @@ def run_b200(args, group=None):
             if world == 1:
                 return SimSession(2, store, device=dev)
             return PartySession(rank, n_parties, group.comm(), store, device=dev)
+        sweep["reciprocal"] = reciprocal_entry(torch, G, mk2, ps, np_, dev, group, 3, 2)
+        sweep["reciprocal"]["cpu_baseline"] = cpu_recip
         for nm in ("exp", "log", "matmul"):
             sweep[nm] = sweep_entry(torch, G, mk2, ps, np_, dev, nm)
         if int8_pk:
