@@ -204,6 +204,12 @@ int mpx_gemm_simt(uint64_t* C, const uint64_t* A, const uint64_t* B, int64_t bat
  * plane[i][r][coff + c], trans = 1 writes plane[i][c][coff + r] (K-major B). */
 int mpx_limb_split(uint8_t* out, const uint64_t* A, int64_t rows, int64_t cols, int64_t lda,
                    int64_t plane, int64_t pitch, int64_t coff, int trans, void* stream);
+/* Beaver matmul operands for all L parties in two launches: A8[l] = limbs
+ * of [D | A_l] (M x 2K), B8[l] = limbs of [B_l + [l==p0] E ; E]^T (N x 2K);
+ * A8 rows beyond M / B8 rows beyond N must be zero (caller zero-fills). */
+int mpx_beaver_limbs(uint8_t* A8, uint8_t* B8, const uint64_t* D, const uint64_t* E, const uint64_t* A,
+                     int64_t a_ps, const uint64_t* B, int64_t b_ps, int L, int64_t M, int64_t K, int64_t N,
+                     int64_t Mpad, int64_t Npad, int64_t Kpad, int p0, void* stream);
 /* C[z] (+)= sum_{i+j<=7} 2^(8(i+j)) A8[z][i] @ B8[z][j]^T mod 2^w on tcgen05
  * kind::i8 with per-diagonal TMEM accumulators, TMA-fed (128B swizzle).
  * A8: [batch][8][Mpad][Kpad], B8: [batch][8][Npad][Kpad] u8, zero padded;

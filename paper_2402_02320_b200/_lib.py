@@ -62,6 +62,7 @@ _SIGS = {
     "mpx_im2col": [_P, _P, _I, _L, _I, _I, _I, _I, _I, _I, _P],
     "mpx_col2im": [_P, _P, _I, _L, _I, _I, _I, _I, _I, _I, _I, _P],
     "mpx_limb_split": [_P, _P, _L, _L, _L, _L, _L, _L, _I, _P],
+    "mpx_beaver_limbs": [_P, _P, _P, _P, _P, _L, _P, _L, _I, _L, _L, _L, _L, _L, _L, _I, _P],
     "mpx_gemm_limbs": [_P, _P, _P, _L, _L, _L, _L, _L, _L, _L, _L, _I, _I, _I, _P],
     "mpx_philox_elems": [_P, _U, _U, _L, _L, _I, _P],
     "mpx_philox_bits": [_P, _U, _U, _L, _L, _P],

@@ -377,6 +377,96 @@ extern "C" int mpx_limb_split(uint8_t* out, const uint64_t* A, int64_t rows, int
 }
 
 // --------------------------------------------------------------------------
+// Beaver operand preparation (basic.py:72-75 as one K-concatenated GEMM per
+// party): A8[l] = limbs of [D | A_l] (M x 2K), B8[l] = limbs of
+// [B_l + [l==p0] E ; E]^T (N x 2K, K-major). One launch per side for all
+// parties; D and E are read once per party slice.
+
+__global__ void k_beaver_limbs_a(uint8_t* __restrict__ A8, const u64* __restrict__ D, const u64* __restrict__ A,
+                                 i64 a_ps, int L, i64 M, i64 Kd, i64 Mpad, i64 Kpad) {
+  const i64 gpr = Kpad / 8;  // 8-column groups per row (columns >= 2K are zero padding)
+  const i64 total = (i64)L * M * gpr;
+  GRID_STRIDE(t, total) {
+    const i64 g = t % gpr;
+    const i64 rl = t / gpr;
+    const i64 r = rl % M, l = rl / M;
+    const i64 c0 = g * 8;
+    u64 w[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const i64 cc = c0 + c;
+      w[c] = cc < Kd ? D[r * Kd + cc] : (cc < 2 * Kd ? A[l * a_ps + r * Kd + (cc - Kd)] : 0ull);
+    }
+    u64 pl[8];
+    bytes_transpose8(w, pl);
+    uint8_t* dst = A8 + (l * 8) * Mpad * Kpad + r * Kpad + c0;
+    const i64 plane = Mpad * Kpad;
+    if (c0 + 8 <= Kpad && (((uintptr_t)dst) & 7) == 0) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) *reinterpret_cast<u64*>(dst + i * plane) = pl[i];
+    } else {
+      for (int i = 0; i < 8; ++i)
+        for (int c = 0; c < 8 && c0 + c < Kpad; ++c) dst[i * plane + c] = (uint8_t)(pl[i] >> (8 * c));
+    }
+  }
+}
+
+// transposed side through a 64 (k) x 32 (n) smem tile; blockIdx.z = party
+__global__ void __launch_bounds__(256) k_beaver_limbs_b(uint8_t* __restrict__ B8, const u64* __restrict__ Bm,
+                                                        i64 b_ps, const u64* __restrict__ E, int p0, i64 Kd, i64 N,
+                                                        i64 Npad, i64 Kpad) {
+  __shared__ u64 tile[64][33];
+  const int l = blockIdx.z;
+  const i64 k0 = (i64)blockIdx.y * 64;  // over the concatenated 2K rows
+  const i64 n0 = (i64)blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int kk = ty; kk < 64; kk += 8) {
+    const i64 k = k0 + kk, n = n0 + tx;
+    u64 v = 0;
+    if (n < N) {
+      if (k < Kd) {
+        v = Bm[l * b_ps + k * N + n];
+        if (l == p0) v += E[k * N + n];
+      } else if (k < 2 * Kd) {
+        v = E[(k - Kd) * N + n];
+      }
+    }
+    tile[kk][tx] = v;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = warp * 4 + (lane >> 3);
+  const int g = lane & 7;
+  const i64 gn = n0 + n, gk = k0 + g * 8;
+  if (gn < Npad && gk < Kpad) {
+    u64 w[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) w[c] = tile[g * 8 + c][n];
+    u64 pl[8];
+    bytes_transpose8(w, pl);
+    uint8_t* dst = B8 + ((i64)l * 8) * Npad * Kpad + gn * Kpad + gk;
+    const i64 plane = Npad * Kpad;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) *reinterpret_cast<u64*>(dst + i * plane) = pl[i];
+  }
+}
+
+extern "C" int mpx_beaver_limbs(uint8_t* A8, uint8_t* B8, const uint64_t* D, const uint64_t* E, const uint64_t* A,
+                                int64_t a_ps, const uint64_t* B, int64_t b_ps, int L, int64_t M, int64_t K,
+                                int64_t N, int64_t Mpad, int64_t Npad, int64_t Kpad, int p0, void* stream) {
+  CHECK_ARG(A8 && B8 && D && E && A && B && L >= 1 && L <= 65535 && M >= 1 && K >= 1 && N >= 1);
+  CHECK_ARG(Mpad >= M && Npad >= N && Kpad >= 2 * K && Kpad % 64 == 0 && Kpad % 8 == 0);
+  cudaStream_t s = (cudaStream_t)stream;
+  const i64 ta = (i64)L * M * ((Kpad + 7) / 8);
+  // A side also zero-fills the K padding columns (groups beyond 2K read as 0)
+  k_beaver_limbs_a<<<grid_for(ta), MPX_THREADS, 0, s>>>(A8, D, A, a_ps, L, M, K, Mpad, Kpad);
+  dim3 grid((unsigned)((Npad + 31) / 32), (unsigned)(Kpad / 64), (unsigned)L);
+  CHECK_ARG(grid.y <= 65535);
+  k_beaver_limbs_b<<<grid, 256, 0, s>>>(B8, B, b_ps, E, p0, K, N, Npad, Kpad);
+  return launch_status();
+}
+
+// --------------------------------------------------------------------------
 // Host: tensor maps + launch
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

@@ -306,6 +306,13 @@ def auto_ksplit(tiles: int, batch: int, Kpad: int) -> int:
     return max(need, min(want, nk))
 
 
+def beaver_limbs(A8, B8, D, E, A_ptr, a_ps, B_ptr, b_ps, L, M, K, N, Mpad, Npad, Kpad, p0):
+    if _dry(A8):
+        return
+    call("mpx_beaver_limbs", ptr(A8), ptr(B8), ptr(D), ptr(E), A_ptr, a_ps, B_ptr, b_ps, L, M, K, N, Mpad, Npad,
+         Kpad, p0)
+
+
 def gemm_limbs(C, A8, B8, batch, M, N, Mpad, Npad, Kpad, ldc, sC, accumulate, width, ksplit=None):
     if _dry(C):
         return C

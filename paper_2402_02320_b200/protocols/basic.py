@@ -99,19 +99,12 @@ def _beaver_matmul_tc(session, Z, D, E, A, B, L, m, k, r, w):
     """Z_l += [D | A_l] @ [B_l + [l==p0] E ; E] as ONE tcgen05 limb GEMM per party
     (K doubled), so D@E at party 0 folds into its B operand (basic.py:72-75)."""
     Mp, Np, Kp = K._rup(m, 128), K._rup(r, 64), K._rup(2 * k, 128)
-    A8 = torch.zeros((L, 8, Mp, Kp), dtype=torch.uint8, device=Z.device)
-    B8 = torch.zeros((L, 8, Np, Kp), dtype=torch.uint8, device=Z.device)
-    bp = None
-    for l in range(L):
-        K.limb_split(A8[l], D, m, k, k, Mp * Kp, Kp, 0, False)
-        K.limb_split(A8[l], A[l].data_ptr(), m, k, k, Mp * Kp, Kp, k, False)
-        if l == session.p0:
-            bp = torch.empty((k, r), dtype=torch.int64, device=Z.device)
-            K.ring_lin(bp, B[l], 1, E, 1, 0, None, 1, k * r, 64, -1)
-            K.limb_split(B8[l], bp, k, r, r, Np * Kp, Kp, 0, True)
-        else:
-            K.limb_split(B8[l], B[l].data_ptr(), k, r, r, Np * Kp, Kp, 0, True)
-        K.limb_split(B8[l], E, k, r, r, Np * Kp, Kp, k, True)
+    A8 = torch.empty((L, 8, Mp, Kp), dtype=torch.uint8, device=Z.device)
+    B8 = torch.empty((L, 8, Np, Kp), dtype=torch.uint8, device=Z.device)
+    if Mp > m:
+        A8[:, :, m:, :].zero_()
+    K.beaver_limbs(A8, B8, D, E, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), L, m, k, r, Mp, Np, Kp,
+                   session.p0)
     K.gemm_limbs(Z, A8, B8, L, m, r, Mp, Np, Kp, r, m * r, True, w)
 
 
