@@ -15,10 +15,13 @@
 
 __global__ void __launch_bounds__(256) gemm_u64_simt(u64* __restrict__ C, const u64* __restrict__ A,
                                                      const u64* __restrict__ B, i64 M, i64 K, i64 N,
-                                                     i64 sA, i64 sB, i64 sC, int accumulate, u64 msk) {
+                                                     i64 sA, i64 sB, i64 sC, int accumulate, u64 msk,
+                                                     int ksplit, i64 kchunk) {
   __shared__ u64 As[GT_BK][GT_BM + 1];
   __shared__ u64 Bs[GT_BK][GT_BN];
-  const i64 bz = blockIdx.z;
+  const i64 bz = blockIdx.z / ksplit;
+  const int ks = blockIdx.z % ksplit;
+  const i64 kbeg = ks * kchunk, kend = min(K, kbeg + kchunk);
   A += bz * sA;
   B += bz * sB;
   C += bz * sC;
@@ -32,14 +35,14 @@ __global__ void __launch_bounds__(256) gemm_u64_simt(u64* __restrict__ C, const 
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0;
 
-  for (i64 k0 = 0; k0 < K; k0 += GT_BK) {
+  for (i64 k0 = kbeg; k0 < kend; k0 += GT_BK) {
     // A tile: 64 rows x 16 k = 1024 values, 4 per thread (k fastest for coalescing)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int idx = threadIdx.x + q * 256;
       const int r = idx / GT_BK, kk = idx % GT_BK;
       const i64 gr = row0 + r, gk = k0 + kk;
-      As[kk][r] = (gr < M && gk < K) ? A[gr * K + gk] : 0ull;
+      As[kk][r] = (gr < M && gk < kend) ? A[gr * K + gk] : 0ull;
     }
     // B tile: 16 k x 64 cols
 #pragma unroll
@@ -47,7 +50,7 @@ __global__ void __launch_bounds__(256) gemm_u64_simt(u64* __restrict__ C, const 
       const int idx = threadIdx.x + q * 256;
       const int kk = idx / GT_BN, c = idx % GT_BN;
       const i64 gk = k0 + kk, gc = col0 + c;
-      Bs[kk][c] = (gk < K && gc < N) ? B[gk * N + gc] : 0ull;
+      Bs[kk][c] = (gk < kend && gc < N) ? B[gk * N + gc] : 0ull;
     }
     __syncthreads();
 #pragma unroll
@@ -72,9 +75,13 @@ __global__ void __launch_bounds__(256) gemm_u64_simt(u64* __restrict__ C, const 
     for (int j = 0; j < 4; ++j) {
       const i64 gc = col0 + tx + 16 * j;
       if (gc >= N) continue;
-      u64 v = acc[i][j];
-      if (accumulate) v += C[gr * N + gc];
-      C[gr * N + gc] = v & msk;
+      if (ksplit > 1) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(C + gr * N + gc), (unsigned long long)acc[i][j]);
+      } else {
+        u64 v = acc[i][j];
+        if (accumulate) v += C[gr * N + gc];
+        C[gr * N + gc] = v & msk;
+      }
     }
   }
 }
@@ -90,10 +97,25 @@ extern "C" int mpx_gemm_simt(uint64_t* C, const uint64_t* A, const uint64_t* B, 
   CHECK_ARG(C && A && B && batch >= 1 && M >= 0 && K >= 0 && N >= 0 && width >= 1 && width <= 64);
   CHECK_ARG(batch <= 65535);
   if (M == 0 || N == 0) return MPX_OK;
-  dim3 grid((unsigned)((N + GT_BN - 1) / GT_BN), (unsigned)((M + GT_BM - 1) / GT_BM), (unsigned)batch);
+  const i64 tiles = ((N + GT_BN - 1) / GT_BN) * ((M + GT_BM - 1) / GT_BM) * batch;
+  // split K across CTAs when the output grid cannot fill the SMs (width 64:
+  // partial sums combine with wrapping 64-bit atomics)
+  int ksplit = 1;
+  if (width == 64 && tiles < 2 * 148 && K >= 4 * GT_BK) {
+    ksplit = (int)min((i64)(2 * 148 / tiles), (K + 2 * GT_BK - 1) / (2 * GT_BK));
+    if (ksplit < 1) ksplit = 1;
+  }
+  const i64 kchunk = ((K + ksplit - 1) / ksplit + GT_BK - 1) / GT_BK * GT_BK;
+  ksplit = (int)((K + kchunk - 1) / kchunk);
+  CHECK_ARG(batch * ksplit <= 65535);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (ksplit > 1 && !accumulate)
+    for (i64 z = 0; z < batch; ++z)
+      if (cudaMemsetAsync(C + z * sC, 0, (size_t)(M * N * 8), st) != cudaSuccess) return MPX_ERR_CUDA;
+  dim3 grid((unsigned)((N + GT_BN - 1) / GT_BN), (unsigned)((M + GT_BM - 1) / GT_BM), (unsigned)(batch * ksplit));
   CHECK_ARG(grid.y <= 65535);
-  gemm_u64_simt<<<grid, 256, 0, (cudaStream_t)stream>>>(C, A, B, M, K, N, sA, sB, sC, accumulate,
-                                                        ring_mask(width));
+  gemm_u64_simt<<<grid, 256, 0, st>>>(C, A, B, M, K, N, sA, sB, sC, accumulate, ring_mask(width), ksplit,
+                                      ksplit > 1 ? kchunk : K);
   return launch_status();
 }
 

@@ -1,0 +1,131 @@
+"""Secure Transformer inference (BASELINE.json configs[3]).
+
+The reference has ``attention_block`` (nn.py:150-186) but no full model; the
+paper's 18.9M-parameter workload (LeViT-256 block) is
+stood in for by a 6-layer encoder with d_model 512, 8 heads (d_head 64), FFN
+2048 and ReLU, seq 128, p = 14: 6 * (4 * 512^2 + 2 * 512 * 2048) =
+18,874,368 secret weights (SURVEY §8d cfg 4). Every product is a Beaver
+matmul with secret-shared weights (model privacy); attention is the
+reference's optimized ``attention_block`` with K pre-scaled by
+log2(e)/sqrt(d_head) in plaintext (nn.py:58-65 folding). LayerNorm is absent
+from the reference, so layers are residual without normalisation, with
+GPT-2-style scaled init N(0, 1/(fan_in * 2 * n_layers)) keeping the residual
+stream O(1) — accuracy of that choice is not pinned; parity is (per
+primitive, and end-to-end against ``oracle/transformer_sim.py``).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+
+import numpy as np
+import torch
+
+from .nn import attention_block, relu
+from .nonlinear import LOG2_E
+from .protocols import batch_matmul, truncate
+from .sharing import AShare
+
+
+def _key(seed, label):
+    tag = hashlib.sha256(f"{seed}:tparam:{label}".encode()).digest()
+    return [int.from_bytes(tag[:8], "little"), int.from_bytes(tag[8:16], "little")]
+
+
+def init_weights(layers, d, ffn, heads, seed=7):
+    """Plaintext init (float64), K projection pre-scaled by log2(e)/sqrt(d_head)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    scale = 1.0 / math.sqrt(2 * layers)
+    dh = d // heads
+    for _ in range(layers):
+        w = {nm: rng.normal(0.0, scale / math.sqrt(fi), (fi, fo)) for nm, fi, fo in
+             (("q", d, d), ("k", d, d), ("v", d, d), ("o", d, d), ("f1", d, ffn), ("f2", ffn, d))}
+        w["k"] = w["k"] * (LOG2_E / math.sqrt(dh))
+        out.append(w)
+    return out
+
+
+class Transformer:
+    def __init__(self, session, layers=6, d=512, heads=8, ffn=2048, frac=14, width=64, seed=7):
+        self.layers, self.d, self.heads, self.ffn, self.p = layers, d, heads, ffn, frac
+        self.plain = init_weights(layers, d, ffn, heads, seed)
+        self.W = [{nm: session.share_fixed(w, width, frac, _key(seed, f"{i}.{nm}")) for nm, w in lw.items()}
+                  for i, lw in enumerate(self.plain)]
+
+    @property
+    def n_params(self) -> int:
+        return sum(w.size for lw in self.plain for w in lw.values())
+
+    def _heads(self, t: AShare) -> list[AShare]:
+        S = t.shape[0]
+        dh = self.d // self.heads
+        v = t.values.view(t.L, S, self.heads, dh).permute(0, 2, 1, 3).contiguous()
+        return [AShare(v[:, h].contiguous(), t.width, t.frac, t.parties) for h in range(self.heads)]
+
+    def layer(self, s, i: int, x: AShare) -> AShare:
+        W, p = self.W[i], self.p
+        with s.scope(f"layer{i}"):
+            with s.scope("qkv"):
+                q, k, v = (truncate(s, z, p) for z in batch_matmul(s, [(x, W["q"]), (x, W["k"]), (x, W["v"])]))
+            with s.scope("attention"):
+                a = attention_block(s, list(zip(self._heads(q), self._heads(k), self._heads(v))), optimized=True)
+            S = x.shape[0]
+            a = AShare(a.values.permute(0, 2, 1, 3).reshape(a.L, S, self.d).contiguous(), a.width, a.frac,
+                       a.parties)
+            with s.scope("proj"):
+                h = x + truncate(s, batch_matmul(s, [(a, W["o"])])[0], p)
+            with s.scope("ffn"):
+                f = relu(s, truncate(s, batch_matmul(s, [(h, W["f1"])])[0], p))
+                return h + truncate(s, batch_matmul(s, [(f, W["f2"])])[0], p)
+
+    def forward(self, s, x: AShare) -> AShare:
+        for i in range(self.layers):
+            x = self.layer(s, i, x)
+        return x
+
+    def plaintext(self, x: np.ndarray) -> np.ndarray:
+        """float64 twin of forward (same folding) for accuracy checks."""
+        def softmax2(z):
+            z = z - z.max(-1, keepdims=True)
+            e = np.exp2(z)
+            return e / e.sum(-1, keepdims=True)
+        dh = self.d // self.heads
+        for w in self.plain:
+            q, k, v = x @ w["q"], x @ w["k"], x @ w["v"]
+            outs = []
+            for h in range(self.heads):
+                sl = slice(h * dh, (h + 1) * dh)
+                outs.append(softmax2(q[:, sl] @ k[:, sl].T) @ v[:, sl])
+            x = x + np.concatenate(outs, axis=1) @ w["o"]
+            x = x + np.maximum(x @ w["f1"], 0) @ w["f2"]
+        return x
+
+
+class GraphedInference:
+    """Forward pass captured in one CUDA graph; material re-dealt in place per call."""
+
+    def __init__(self, session, model: Transformer, x: AShare, demands, needs_bits, seed0: int):
+        from .preprocessing import device_store
+        self.s, self.model, self.x = session, model, x
+        self.demands, self.needs_bits = demands, needs_bits
+        session.store = device_store(seed0, session.n_parties, demands, parties=session.parties,
+                                     device=session.device, needs_bits=needs_bits)
+        side = torch.cuda.Stream(session.device)
+        side.wait_stream(torch.cuda.current_stream(session.device))
+        with torch.cuda.stream(side):
+            model.forward(session, x)
+        torch.cuda.current_stream(session.device).wait_stream(side)
+        torch.cuda.synchronize(session.device)
+        session.store.rewind()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.y = model.forward(session, x)
+
+    def run(self, seed: int) -> AShare:
+        from .preprocessing import device_store
+        device_store(seed, self.s.n_parties, self.demands, parties=self.s.parties, device=self.s.device,
+                     needs_bits=self.needs_bits, into=self.s.store)
+        self.graph.replay()
+        return self.y

@@ -100,3 +100,18 @@ def test_tc_matches_simt_path():
     K.gemm_tc(C1, _dev(A), _dev(B), 1, M, Kd, N, 0, 0, 0, False, 64)
     K.gemm(C2, _dev(A), _dev(B), 1, M, Kd, N, 0, 0, 0, False, 64, simt=True)
     assert torch.equal(C1, C2)
+
+
+@pytest.mark.parametrize("M,K,N,acc", [(128, 500, 10, False), (500, 128, 10, True), (3, 4000, 7, False),
+                                       (200, 300, 100, True)])
+def test_simt_split_k_exact(M, K, N, acc):
+    from paper_2402_02320_b200 import kernels as K_
+    rng = np.random.default_rng(M * K + N)
+    A = rng.integers(0, 1 << 64, (M, K), dtype=np.uint64)
+    B = rng.integers(0, 1 << 64, (K, N), dtype=np.uint64)
+    C0 = rng.integers(0, 1 << 64, (M, N), dtype=np.uint64)
+    C = _dev(C0) if acc else torch.zeros((M, N), dtype=torch.int64, device="cuda")
+    K_.gemm(C, _dev(A), _dev(B), 1, M, K, N, 0, 0, 0, acc, 64, simt=True)
+    torch.cuda.synchronize()
+    want = np.matmul(A, B) + (C0 if acc else np.uint64(0))
+    assert np.array_equal(_host(C), want)
