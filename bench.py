@@ -524,6 +524,40 @@ def mlp_entry(torch, dev, steps, warmup):
             "steps_per_s": 1e3 / ms, "cuda_graph": True}
 
 
+def transformer_entry(torch, dev, steps, warmup):
+    """configs[3]: 18.9M-parameter Transformer secure inference, seq 128, p = 14,
+    2 parties on one GPU, forward captured in one CUDA graph. Latency per
+    forward (lower is better)."""
+    from paper_2402_02320_b200.preprocessing import DemandCounter, device_store
+    from paper_2402_02320_b200.session import SimSession
+    from paper_2402_02320_b200.transformer import GraphedInference, Transformer
+    n, S = 2, 128
+    x = np.random.default_rng(3).normal(0, 1, (S, 512))
+    c = DemandCounter((0, 1), n)
+    sd = SimSession(n, c, device=dev)
+    Transformer(sd).forward(sd, sd.share_fixed(x, WIDTH, 14, [5, 5]))
+    s = SimSession(n, None, device=dev)
+    m = Transformer(s)
+    g = GraphedInference(s, m, s.share_fixed(x, WIDTH, 14, [5, 5]), c.demands, c.needs_bits, seed0=90)
+    times = []
+    for t in range(warmup + steps):
+        device_store(91 + t, n, c.demands, device=dev, needs_bits=c.needs_bits, into=s.store)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        if t >= warmup:
+            times.append(e0.elapsed_time(e1))
+    y = s.open_fixed(g.y)
+    xq = np.floor(x * (1 << 14)) / (1 << 14)
+    return {"model": "6-layer encoder d512 h8 ffn2048 (18,874,368 secret weights)", "seq": S, "parties": n,
+            "frac": 14, "latency_ms": float(np.mean(times)), "higher_is_better": False,
+            "rounds": sd.metrics.total.rounds, "cuda_graph": True,
+            "max_abs_err_vs_float64": float(np.abs(y - m.plaintext(xq)).max())}
+
+
 def run_b200(args, group=None):
     import torch
     import torch.distributed as dist
@@ -690,6 +724,7 @@ def run_b200(args, group=None):
                               "frac": (mm["gemm_int8_TOPS"] / int8_pk) if mm.get("gemm_int8_TOPS") else None}
         if world == 1:
             sweep["mlp_train"] = mlp_entry(torch, dev, 5, 3)
+            sweep["transformer"] = transformer_entry(torch, dev, 3, 2)
 
     line = None
     if rank == 0:
@@ -756,8 +791,8 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--batch", type=int, default=BATCH)
     ap.add_argument("--cpu-sample", type=int, default=1 << 20)
