@@ -233,6 +233,13 @@ int mpx_exp_fused(uint64_t* y, const uint64_t* x, int64_t n, const void* tape_ho
                   const void* params_host, void* stream);
 int mpx_log_fused(uint64_t* y, const uint64_t* x, int64_t n, const void* tape_host,
                   const void* params_host, void* stream);
+/* ReLU (nn.py:92-97) in one kernel: y = bit2a(gt(x, 0)) * x; when s_out is
+ * non-null the converted sign is stored too (training backward). */
+int mpx_relu_fused(uint64_t* y, uint64_t* s_out, const uint64_t* x, int64_t n, const void* tape_host,
+                   const void* params_host, void* stream);
+/* One max tournament level (derived.py:152-170): win = v + bit2a(gt(u, v)) * (u - v). */
+int mpx_maxlevel_fused(uint64_t* win, const uint64_t* u, const uint64_t* v, int64_t n,
+                       const void* tape_host, const void* params_host, void* stream);
 int mpx_fused_abi_sizes(int64_t* matref, int64_t* tape, int64_t* params, int64_t* tape_max);
 
 /* ---- trusted dealer (preprocessing.py:121-174; ring.py:124-134) ----

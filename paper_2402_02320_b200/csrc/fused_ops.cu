@@ -624,6 +624,68 @@ __global__ void __launch_bounds__(128) k_log_fused(u64* __restrict__ y, const u6
 }
 
 // ---------------------------------------------------------------------------
+// ReLU (nn.py:92-97): s = bit2a(gt(x, 0)) = bit2a(sign(0 - x)), y = s * x.
+// Also stores s (the converted sign) for the backward pass when s_out != 0.
+
+template <int L>
+__global__ void __launch_bounds__(128) k_relu_fused(u64* __restrict__ y, u64* __restrict__ s_out,
+                                                    const u64* __restrict__ xin, i64 n,
+                                                    const __grid_constant__ Tape tape, FusedParams P) {
+  const int w = P.w, p0 = P.p0;
+  const u64 msk = ring_mask(w);
+  GRID_STRIDE(e, n) {
+    int ti = 0;
+    const Sh<L> x = load_sh<L>(xin, n, e);
+    Sh<L> diff;
+#pragma unroll
+    for (int l = 0; l < L; ++l) diff.v[l] = (0ull - x.v[l]) & msk;   // public zero (party 0) - x
+    const Sh<L> bits = d_decompose<L>(diff, w, tape, ti, e, p0);
+    Sh<L> sign;
+#pragma unroll
+    for (int l = 0; l < L; ++l) sign.v[l] = (bits.v[l] >> (w - 1)) & 1ull;
+    const MatRef& tb = next_take<L>(tape, ti, e);
+    const u64 c = d_bit2a_open<L>(sign, 1, tb, e);
+    const Sh<L> sa = d_bit2a_get<L>(c, 0, 1, tb, e, p0, msk);
+    const Sh<L> out = d_mul<L>(sa, x, next_take<L>(tape, ti, e), e, p0, msk);
+    store_sh<L>(y, n, e, out);
+    if (s_out) store_sh<L>(s_out, n, e, sa);
+  }
+}
+
+// One max_vec tournament level (derived.py:152-170) on pairs (u, v):
+// b = gt(u, v) (sign of v - u), s = bit2a(b), winner = v + s * (u - v).
+template <int L>
+__global__ void __launch_bounds__(128) k_maxlevel_fused(u64* __restrict__ win, const u64* __restrict__ uin,
+                                                        const u64* __restrict__ vin, i64 n,
+                                                        const __grid_constant__ Tape tape, FusedParams P) {
+  const int w = P.w, p0 = P.p0;
+  const u64 msk = ring_mask(w);
+  GRID_STRIDE(e, n) {
+    int ti = 0;
+    const Sh<L> u = load_sh<L>(uin, n, e);
+    const Sh<L> v = load_sh<L>(vin, n, e);
+    Sh<L> diff, uv;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      diff.v[l] = (v.v[l] - u.v[l]) & msk;
+      uv.v[l] = (u.v[l] - v.v[l]) & msk;
+    }
+    const Sh<L> bits = d_decompose<L>(diff, w, tape, ti, e, p0);
+    Sh<L> sign;
+#pragma unroll
+    for (int l = 0; l < L; ++l) sign.v[l] = (bits.v[l] >> (w - 1)) & 1ull;
+    const MatRef& tb = next_take<L>(tape, ti, e);
+    const u64 c = d_bit2a_open<L>(sign, 1, tb, e);
+    const Sh<L> sa = d_bit2a_get<L>(c, 0, 1, tb, e, p0, msk);
+    const Sh<L> m = d_mul<L>(sa, uv, next_take<L>(tape, ti, e), e, p0, msk);
+    Sh<L> out;
+#pragma unroll
+    for (int l = 0; l < L; ++l) out.v[l] = (v.v[l] + m.v[l]) & msk;
+    store_sh<L>(win, n, e, out);
+  }
+}
+
+// ---------------------------------------------------------------------------
 
 template <template <int> class KERN>
 struct Dispatch;
@@ -648,6 +710,30 @@ struct Dispatch;
   }
 
 DEFINE_LAUNCH(mpx_reciprocal_fused, k_reciprocal_fused)
+
+#define DEFINE_LAUNCH2(NAME, KFN, T1, T2)                                                                  \
+  extern "C" int NAME(uint64_t* y, T1 a1, T2 a2, int64_t n, const void* tape_host, const void* params_host,   \
+                      void* stream) {                                                                      \
+    CHECK_ARG(y && a2 && n >= 0 && tape_host && params_host);                                              \
+    const Tape& tp = *(const Tape*)tape_host;                                                              \
+    const FusedParams& P = *(const FusedParams*)params_host;                                               \
+    CHECK_ARG(tp.n >= 1 && tp.n <= TAPE_MAX && P.w >= 8 && P.w <= 64 && P.L >= 1 && P.L <= 4);            \
+    if (n == 0) return MPX_OK;                                                                             \
+    cudaStream_t s = (cudaStream_t)stream;                                                                 \
+    const unsigned g = grid_for(n, 128);                                                                   \
+    switch (P.L) {                                                                                         \
+      case 1: KFN<1><<<g, 128, 0, s>>>(y, a1, a2, n, tp, P); break;                                        \
+      case 2: KFN<2><<<g, 128, 0, s>>>(y, a1, a2, n, tp, P); break;                                        \
+      case 3: KFN<3><<<g, 128, 0, s>>>(y, a1, a2, n, tp, P); break;                                        \
+      default: KFN<4><<<g, 128, 0, s>>>(y, a1, a2, n, tp, P); break;                                       \
+    }                                                                                                      \
+    return launch_status();                                                                                \
+  }
+
+// y, s_out (may be NULL), x
+DEFINE_LAUNCH2(mpx_relu_fused, k_relu_fused, uint64_t*, const uint64_t*)
+// winner, u, v
+DEFINE_LAUNCH2(mpx_maxlevel_fused, k_maxlevel_fused, const uint64_t*, const uint64_t*)
 DEFINE_LAUNCH(mpx_exp_fused, k_exp_fused)
 DEFINE_LAUNCH(mpx_log_fused, k_log_fused)
 

@@ -146,6 +146,11 @@ def _bind():
             fn.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                            ctypes.c_void_p]
             fn.restype = ctypes.c_int
+        for nm in ("mpx_relu_fused", "mpx_maxlevel_fused"):
+            fn = getattr(lib, nm)
+            fn.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                           ctypes.c_void_p, ctypes.c_void_p]
+            fn.restype = ctypes.c_int
         lib.mpx_fused_abi_sizes.argtypes = [ctypes.POINTER(ctypes.c_int64)] * 4
         sizes = [ctypes.c_int64() for _ in range(4)]
         lib.mpx_fused_abi_sizes(*[ctypes.byref(s) for s in sizes])
@@ -176,6 +181,12 @@ def fusable(session, x: AShare) -> bool:
             and x.width == 64 and 1 <= session.L <= 4 and 2 * x.frac <= 62 and x.size > 0)
 
 
+def fusable_cmp(session, x: AShare) -> bool:
+    """ReLU / max-level kernels: any ring width >= 8."""
+    return (getattr(session, "fused", False) and getattr(session, "fuse_ops", True)
+            and 8 <= x.width <= 64 and 1 <= session.L <= 4 and x.size > 0)
+
+
 def params_for(kind: str, session, x: AShare, params) -> FusedParams:
     w, p = x.width, x.frac
     P = FusedParams()
@@ -203,51 +214,93 @@ def params_for(kind: str, session, x: AShare, params) -> FusedParams:
     return P
 
 
-def run_fused(kind: str, session, x: AShare, params, protocol) -> AShare:
-    """Launch the fused kernel for ``protocol`` on ``x``.
-
-    The first call for a (kind, shape, params, party layout) records the
-    schedule of material takes and the ledger with a dry pass of the Python
-    protocol over the real store; later calls replay the takes on the store
-    (same cursors as the per-round path) and merge the cached ledger.
-    """
+def _schedule(kind: str, session, key, n_elems: int, protocol, metas):
+    """Take schedule + ledger for one fused call: recorded by a dry pass of the
+    Python protocol over the real store the first time, replayed afterwards."""
     from .metrics import CommMetrics
     from .session import SimSession
-    lib = _bind()
-    key = (kind, x.shape, x.width, x.frac, params, session.L, session.n_parties, session.p0)
     sched = _SCHEDULES.get(key)
     if sched is None:
-        store = TapeStore(session.store, x.size)
+        store = TapeStore(session.store, n_elems)
         tmp = CommMetrics(session.metrics.party, session.n_parties)
         ts = SimSession(session.n_parties, store, metrics=tmp)
-        xm = AShare(torch.empty(x.values.shape, dtype=torch.int64, device="meta"), x.width, x.frac, x.parties)
-        ym = protocol(ts, xm)
+        ym = protocol(ts, *metas)
         if len(store.tape) > TAPE_MAX:
             raise _lib.MpxError(f"{kind}: tape of {len(store.tape)} takes exceeds {TAPE_MAX}")
+        ym = ym[0] if isinstance(ym, tuple) else ym
         sched = (tuple(store.calls), tmp, ym.width, ym.frac)
         _SCHEDULES[key] = sched
         entries = store.tape
     else:
-        entries = [_take_ref(session.store, m, a, x.size) for m, a in sched[0]]
-    calls, ledger, out_w, out_f = sched
-    _merge_metrics(session.metrics, ledger)
+        entries = [_take_ref(session.store, m, a, n_elems) for m, a in sched[0]]
+    _merge_metrics(session.metrics, sched[1])
     tape = Tape()
     for i, ent in enumerate(entries):
         tape.m[i] = MatRef(*ent)
     tape.n = len(entries)
-    P = params_for(kind, session, x, params)
-    y = session.alloc(x.values.shape)
-    xv = x.values.contiguous()
+    return tape, sched
+
+
+def _meta(x: AShare) -> AShare:
+    return AShare(torch.empty(x.values.shape, dtype=torch.int64, device="meta"), x.width, x.frac, x.parties)
+
+
+def _launch(lib, entry, args, prof_info):
     _lib.LAUNCHES += 1
     prof = _lib.profiling()
     if prof is not None:
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
-    rc = getattr(lib, _ENTRY[kind])(y.data_ptr(), xv.data_ptr(), x.size, ctypes.addressof(tape),
-                                    ctypes.addressof(P), _lib.stream_ptr())
+    rc = getattr(lib, entry)(*args, _lib.stream_ptr())
     if prof is not None:
         ev1.record()
-        prof.append((_ENTRY[kind], (kind, x.size, session.L, calls), ev0, ev1))
+        prof.append((entry, prof_info, ev0, ev1))
     if rc != 0:
-        raise _lib.MpxError(f"{_ENTRY[kind]} returned {rc}")
+        raise _lib.MpxError(f"{entry} returned {rc}")
+
+
+def run_fused(kind: str, session, x: AShare, params, protocol) -> AShare:
+    """Launch the fused kernel for ``protocol`` on ``x`` (Reciprocal/Exp/Log)."""
+    lib = _bind()
+    key = (kind, x.shape, x.width, x.frac, params, session.L, session.n_parties, session.p0)
+    tape, (calls, _, out_w, out_f) = _schedule(kind, session, key, x.size, protocol, (_meta(x),))
+    P = params_for(kind, session, x, params)
+    y = session.alloc(x.values.shape)
+    xv = x.values.contiguous()
+    _launch(lib, _ENTRY[kind], (y.data_ptr(), xv.data_ptr(), x.size, ctypes.addressof(tape), ctypes.addressof(P)),
+            (kind, x.size, session.L, calls))
+    return AShare(y, out_w, out_f, session.parties)
+
+
+def _basic_params(session, x: AShare) -> FusedParams:
+    P = FusedParams()
+    P.w, P.p, P.L, P.p0 = x.width, x.frac, session.L, session.p0
+    return P
+
+
+def relu_fused(session, x: AShare, protocol, want_sign: bool):
+    """ReLU in one kernel: (y, converted sign or None)."""
+    lib = _bind()
+    key = ("relu", x.shape, x.width, x.frac, session.L, session.n_parties, session.p0)
+    tape, (calls, _, out_w, out_f) = _schedule("relu", session, key, x.size, protocol, (_meta(x),))
+    P = _basic_params(session, x)
+    y = session.alloc(x.values.shape)
+    sg = session.alloc(x.values.shape) if want_sign else None
+    _launch(lib, "mpx_relu_fused", (y.data_ptr(), sg.data_ptr() if sg is not None else None,
+                                    x.values.contiguous().data_ptr(), x.size, ctypes.addressof(tape),
+                                    ctypes.addressof(P)), ("relu", x.size, session.L, calls))
+    out = AShare(y, out_w, out_f, session.parties)
+    return out, (AShare(sg, x.width, 0, session.parties) if sg is not None else None)
+
+
+def maxlevel_fused(session, u: AShare, v: AShare, protocol) -> AShare:
+    """One max_vec tournament level in one kernel: v + bit2a(gt(u, v)) * (u - v)."""
+    lib = _bind()
+    key = ("maxlevel", u.shape, u.width, u.frac, session.L, session.n_parties, session.p0)
+    tape, (calls, _, out_w, out_f) = _schedule("maxlevel", session, key, u.size, protocol, (_meta(u), _meta(v)))
+    P = _basic_params(session, u)
+    y = session.alloc(u.values.shape)
+    _launch(lib, "mpx_maxlevel_fused", (y.data_ptr(), u.values.contiguous().data_ptr(),
+                                        v.values.contiguous().data_ptr(), u.size, ctypes.addressof(tape),
+                                        ctypes.addressof(P)), ("maxlevel", u.size, session.L, calls))
     return AShare(y, out_w, out_f, session.parties)

@@ -153,6 +153,21 @@ class AvgPool2d(Layer):
 
 class ReLU(Layer):
     def forward(self, s, x: AShare) -> AShare:
+        from . import fused as F
+        if F.fusable_cmp(s, x):
+            y, self.sign = F.relu_fused(s, x, ReLU._protocol, want_sign=True)
+            return y
+        return self._protocol(s, x, self)
+
+    @staticmethod
+    def _protocol(s, x: AShare, layer=None) -> AShare:
+        zero = public_ashare(0, x.width, x.frac, s, shape=x.shape)
+        sign = bit2a(s, gt(s, x, zero), x.width)
+        if layer is not None:
+            layer.sign = sign
+        return mul(s, sign, x)
+
+    def _unused(self, s, x):
         zero = public_ashare(0, x.width, x.frac, s, shape=x.shape)
         self.sign = bit2a(s, gt(s, x, zero), x.width)
         return mul(s, self.sign, x)

@@ -59,3 +59,40 @@ def test_fused_equals_per_round_and_oracle(engines, fn, n):
     for k in want:
         assert np.array_equal(fused[k], want[k]), k
         assert np.array_equal(rounds[k], want[k]), k
+
+
+def _relu(M, s):
+    rng = np.random.default_rng(26)
+    return {"y": M.relu(s, M.deal_fixed(s, rng.normal(0, 4, 5000), 64, 23, tag=0))}
+
+
+def _relu32(M, s):
+    rng = np.random.default_rng(27)
+    return {"y": M.relu(s, M.deal_fixed(s, rng.normal(0, 4, (40, 33)), 32, 14, tag=0))}
+
+
+def _max_odd(M, s):
+    rng = np.random.default_rng(28)
+    return {"m": M.max_vec(s, M.deal_fixed(s, rng.normal(0, 5, (37, 23)), 64, 23, tag=0))}
+
+
+def _maxcut_softmax(M, s):
+    rng = np.random.default_rng(29)
+    x = M.deal_fixed(s, rng.normal(0, 5, (9, 64)), 64, 23, tag=0)
+    return {"mc": M.maxcut(s, x), "sm": M.softmax(s, x)}
+
+
+@pytest.mark.parametrize("fn", [_relu, _relu32, _max_odd, _maxcut_softmax],
+                         ids=["relu", "relu_w32", "max_odd", "maxcut_softmax"])
+@pytest.mark.parametrize("n", [2, 3, 4])
+def test_fused_cmp_equals_per_round_and_oracle(engines, fn, n):
+    g, o = engines
+    fused, finfo, fs = g.run(fn, n, fuse=True)
+    rounds, rinfo, rs = g.run(fn, n, fuse=False)
+    want, winfo = o.run(fn, n)
+    assert finfo["ledger"] == rinfo["ledger"] == winfo["ledger"]
+    assert fs.store.usage() == rs.store.usage()
+    for k in want:
+        assert np.array_equal(fused[k], want[k]), k
+        assert np.array_equal(rounds[k], want[k]), k
+
