@@ -73,6 +73,15 @@ int mpx_ring_mul(uint64_t* out, const uint64_t* a, const uint64_t* b, int64_t n,
  * contractions (nonlinear.py:117-122, 252-256). */
 int mpx_ring_rowdot(uint64_t* out, const uint64_t* x, const uint64_t* wts, int L, int64_t rows,
                     int64_t cols, int width, void* stream);
+/* out[l][c] = sum_r x[l][r][c] mod 2^width, x: [L][rows][cols] (bias gradients). */
+int mpx_ring_colsum(uint64_t* out, const uint64_t* x, int L, int64_t rows, int64_t cols, int width,
+                    void* stream);
+/* k x k, stride-k window sums over [planes][H][W] -> [planes][H/k][W/k] (average pooling). */
+int mpx_ring_pool_sum(uint64_t* out, const uint64_t* x, int64_t planes, int64_t H, int64_t W, int64_t k,
+                      int width, void* stream);
+/* z[l][r][c] = z[l][r][c] + (b[l][c] << shift) mod 2^width, in place (bias rows). */
+int mpx_ring_add_rowvec(uint64_t* z, const uint64_t* b, int L, int64_t rows, int64_t cols, int shift,
+                        int width, void* stream);
 
 /* ---- fixed-point codec (ring.py:76-89) ---- */
 int mpx_encode(uint64_t* out, const double* in, int64_t n, int width, int frac, void* stream);
@@ -219,7 +228,17 @@ int mpx_beaver_limbs(uint8_t* A8, uint8_t* B8, const uint64_t* D, const uint64_t
  * Kpad <= 16384. */
 int mpx_gemm_limbs(uint64_t* C, const uint8_t* A8, const uint8_t* B8, int64_t batch, int64_t M,
                    int64_t N, int64_t Mpad, int64_t Npad, int64_t Kpad, int64_t ldc, int64_t sC,
-                   int accumulate, int width, int ksplit, void* stream);
+                   int accumulate, int width, int ksplit, const uint64_t* Cin, int64_t sCin,
+                   void* stream);
+
+/* Beaver matrix-product reconstruction in one launch (basic.py:72-75):
+ * Z_l = C_l + D @ (B_l + [l==p0] E) + A_l @ E mod 2^width for the L local
+ * parties (batch strides sZ, sC, sA, sB). Z, C: M x N; D, A: M x K; E, B:
+ * K x N, all row-major. SIMT u64 tiles sized to the output (thin layers),
+ * split-K with wrapping atomics for tiny outputs (width 64). */
+int mpx_beaver_gemm(uint64_t* Z, int64_t sZ, const uint64_t* C, int64_t sC, const uint64_t* D,
+                    const uint64_t* E, const uint64_t* A, int64_t sA, const uint64_t* B, int64_t sB,
+                    int L, int64_t M, int64_t K, int64_t N, int p0, int width, void* stream);
 
 /* ---- sim-mode whole-op fused kernels (fused_ops.cu) ----
  * All L parties on this GPU: the whole Reciprocal / Exp / Log protocol

@@ -63,7 +63,11 @@ _SIGS = {
     "mpx_col2im": [_P, _P, _I, _L, _I, _I, _I, _I, _I, _I, _I, _P],
     "mpx_limb_split": [_P, _P, _L, _L, _L, _L, _L, _L, _I, _P],
     "mpx_beaver_limbs": [_P, _P, _P, _P, _P, _L, _P, _L, _I, _L, _L, _L, _L, _L, _L, _I, _P],
-    "mpx_gemm_limbs": [_P, _P, _P, _L, _L, _L, _L, _L, _L, _L, _L, _I, _I, _I, _P],
+    "mpx_beaver_gemm": [_P, _L, _P, _L, _P, _P, _P, _L, _P, _L, _I, _L, _L, _L, _I, _I, _P],
+    "mpx_ring_colsum": [_P, _P, _I, _L, _L, _I, _P],
+    "mpx_ring_pool_sum": [_P, _P, _L, _L, _L, _L, _I, _P],
+    "mpx_ring_add_rowvec": [_P, _P, _I, _L, _L, _I, _I, _P],
+    "mpx_gemm_limbs": [_P, _P, _P, _L, _L, _L, _L, _L, _L, _L, _L, _I, _I, _I, _P, _L, _P],
     "mpx_philox_elems": [_P, _U, _U, _L, _L, _I, _P],
     "mpx_philox_bits": [_P, _U, _U, _L, _L, _P],
     "mpx_deal_share_arith": [_P, _L, _P, _U, _U, _L, _L, _I, _I, _I, _I, _P],

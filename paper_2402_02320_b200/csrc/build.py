@@ -13,7 +13,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 PKG = os.path.dirname(HERE)
 REPO = os.path.dirname(PKG)
-SOURCES = ["ring.cu", "beaver.cu", "gemm.cu", "gemm_tc.cu", "dealer.cu", "fused_ops.cu"]
+SOURCES = ["ring.cu", "beaver.cu", "gemm.cu", "gemm_tc.cu", "beaver_gemm.cu", "dealer.cu", "fused_ops.cu"]
 OUT = os.path.join(PKG, "libmpx.so")
 
 

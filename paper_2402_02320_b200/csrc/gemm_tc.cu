@@ -107,6 +107,8 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
 
 struct TcArgs {
   u64* C;
+  const u64* Cin;  // optional addend (C = Cin + A@B), same ldc as C
+  i64 sCin;
   i64 ldc;
   i64 sC;        // batch stride of C (elements)
   int M, N;      // true output extent
@@ -242,11 +244,16 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     // ---------------- epilogue: warps 2..5 ----------------
+    // TMEM lane = tile row, so a thread holds one row; the 32x32 u64 block is
+    // transposed through shared memory (the operand ring is idle once
+    // tmem_full fires) so global loads/stores run along rows, 256 B per warp.
     const int sp = warp & 3;  // TMEM sub-partition this warp may access
-    const int row = m0 + sp * 32 + lane;
     mbar_wait(tmem_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    u64* Crow = args.C + (i64)z * args.sC + (i64)row * args.ldc;
+    u64* stage = reinterpret_cast<u64*>(smem) + sp * (32 * 33);
+    const i64 rbase = (i64)m0 + sp * 32;
+    u64* Cz = args.C + (i64)z * args.sC;
+    const u64* Cin = args.Cin ? args.Cin + (i64)z * args.sCin : nullptr;
     for (int c = 0; c < TC_BN / 32; ++c) {
       u64 res[32];
 #pragma unroll
@@ -260,22 +267,27 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
         for (int t = 0; t < 32; ++t) res[t] += (u64)v[t] << (8 * d);
       }
-      if (row < args.M) {
-        const int cbase = n0 + c * 32;
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const int col = cbase + t;
-          if (col < args.N) {
-            if (args.ksplit > 1) {
-              atomicAdd(reinterpret_cast<unsigned long long*>(Crow + col), (unsigned long long)res[t]);
-            } else {
-              u64 v = res[t];
-              if (args.accumulate) v += Crow[col];
-              Crow[col] = v & args.msk;
-            }
+      for (int t = 0; t < 32; ++t) stage[lane * 33 + t] = res[t];
+      __syncwarp();
+      const int col = n0 + c * 32 + lane;
+      if (col < args.N) {
+        for (int r = 0; r < 32; ++r) {
+          const i64 row = rbase + r;
+          if (row >= args.M) break;
+          const u64 val = stage[r * 33 + lane];
+          u64* dst = Cz + row * args.ldc + col;
+          if (args.ksplit > 1) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(dst), (unsigned long long)val);
+          } else {
+            u64 v = val;
+            if (Cin) v += Cin[row * args.ldc + col];
+            else if (args.accumulate) v += *dst;
+            *dst = v & args.msk;
           }
         }
       }
+      __syncwarp();
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -504,7 +516,8 @@ static int make_map(CUtensorMap* map, const uint8_t* base, i64 rows, i64 kbytes,
 // Mpad % 128 == 0, Npad % 64 == 0, Kpad % 128 == 0, Kpad <= 16384.
 extern "C" int mpx_gemm_limbs(uint64_t* C, const uint8_t* A8, const uint8_t* B8, int64_t batch, int64_t M,
                               int64_t N, int64_t Mpad, int64_t Npad, int64_t Kpad, int64_t ldc, int64_t sC,
-                              int accumulate, int width, int ksplit, void* stream) {
+                              int accumulate, int width, int ksplit, const uint64_t* Cin, int64_t sCin,
+                              void* stream) {
   CHECK_ARG(C && A8 && B8 && batch >= 1 && batch <= 65535 && M >= 1 && N >= 1 && width >= 1 && width <= 64);
   CHECK_ARG(Mpad % TC_BM == 0 && Npad % TC_BN == 0 && Kpad % TC_BK == 0 && Kpad >= TC_BK);
   const int nk_total = (int)(Kpad / TC_BK);
@@ -516,7 +529,15 @@ extern "C" int mpx_gemm_limbs(uint64_t* C, const uint8_t* A8, const uint8_t* B8,
   CHECK_ARG((i64)nk_per * TC_BK <= 16384);
   // split-K adds partials with wrapping 64-bit atomics: exact mod 2^64 only
   CHECK_ARG(ksplit == 1 || width == 64);
-  if (ksplit > 1 && !accumulate) {
+  CHECK_ARG(!(Cin && accumulate));
+  if (ksplit > 1 && Cin) {
+    // partial sums land on a copy of the addend
+    for (i64 z = 0; z < batch; ++z)
+      if (cudaMemcpy2DAsync(C + z * sC, (size_t)ldc * 8, Cin + z * sCin, (size_t)ldc * 8, (size_t)N * 8,
+                            (size_t)M, cudaMemcpyDeviceToDevice, (cudaStream_t)stream) != cudaSuccess)
+        return MPX_ERR_CUDA;
+    Cin = nullptr;
+  } else if (ksplit > 1 && !accumulate) {
     for (i64 z = 0; z < batch; ++z)
       if (cudaMemset2DAsync(C + z * sC, (size_t)ldc * 8, 0, (size_t)N * 8, (size_t)M, (cudaStream_t)stream) !=
           cudaSuccess)
@@ -536,6 +557,8 @@ extern "C" int mpx_gemm_limbs(uint64_t* C, const uint8_t* A8, const uint8_t* B8,
   }
   TcArgs a;
   a.C = C;
+  a.Cin = Cin;
+  a.sCin = sCin;
   a.ldc = ldc;
   a.sC = sC;
   a.M = (int)M;

@@ -93,6 +93,117 @@ extern "C" int mpx_ring_rowdot(uint64_t* out, const uint64_t* x, const uint64_t*
   return launch_status();
 }
 
+// Column sums of [L][rows][cols] -> [L][cols] (the bias gradient: a sum over
+// the batch / spatial rows). Narrow tables (cols <= blockDim) tile a block as
+// (blockDim / cols) row lanes x cols, so consecutive threads read consecutive
+// words; partial sums meet in shared memory, then one wrapping atomic per
+// column and block. Wide tables walk columns directly.
+__global__ void k_ring_colsum(u64* __restrict__ out, const u64* __restrict__ x, i64 rows, int cols,
+                              i64 rows_per_block) {
+  extern __shared__ u64 part[];
+  const int l = blockIdx.y;
+  x += (i64)l * rows * cols;
+  out += (i64)l * cols;
+  const i64 r0 = (i64)blockIdx.x * rows_per_block;
+  const i64 r1 = min(rows, r0 + rows_per_block);
+  if (cols <= (int)blockDim.x) {
+    const int lanes = blockDim.x / cols;
+    const int col = threadIdx.x % cols, sub = threadIdx.x / cols;
+    for (int c = threadIdx.x; c < cols; c += blockDim.x) part[c] = 0;
+    __syncthreads();
+    if (sub < lanes) {
+      u64 acc = 0;
+      for (i64 r = r0 + sub; r < r1; r += lanes) acc += x[r * cols + col];
+      atomicAdd(reinterpret_cast<unsigned long long*>(&part[col]), (unsigned long long)acc);
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < cols; c += blockDim.x)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&out[c]), (unsigned long long)part[c]);
+  } else {
+    for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+      u64 acc = 0;
+      for (i64 r = r0; r < r1; ++r) acc += x[r * cols + c];
+      atomicAdd(reinterpret_cast<unsigned long long*>(&out[c]), (unsigned long long)acc);
+    }
+  }
+}
+
+__global__ void k_mask_inplace(u64* __restrict__ v, i64 n, u64 msk) {
+  GRID_STRIDE(i, n) v[i] &= msk;
+}
+
+extern "C" int mpx_ring_colsum(uint64_t* out, const uint64_t* x, int L, int64_t rows, int64_t cols, int width,
+                               void* stream) {
+  CHECK_ARG(out && x && L >= 1 && L <= 65535 && rows >= 0 && cols >= 1 && cols <= (1 << 20) && width >= 1 &&
+            width <= 64);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(out, 0, (size_t)L * cols * 8, s) != cudaSuccess) return MPX_ERR_CUDA;
+  if (rows == 0) return MPX_OK;
+  const int threads = 256;
+  // enough blocks to cover the SMs a few times, each a contiguous row band
+  const i64 lanes = cols <= threads ? threads / cols : 1;
+  i64 nblk = (4 * 148 + L - 1) / L;
+  const i64 min_rows = 4 * lanes;
+  nblk = max((i64)1, min(nblk, (rows + min_rows - 1) / min_rows));
+  const i64 rpb = (rows + nblk - 1) / nblk;
+  nblk = (rows + rpb - 1) / rpb;
+  const size_t sm = cols <= threads ? (size_t)cols * 8 : 0;
+  k_ring_colsum<<<dim3((unsigned)nblk, (unsigned)L), threads, sm, s>>>(out, x, rows, (int)cols, rpb);
+  if (width < 64) k_mask_inplace<<<grid_for((i64)L * cols), MPX_THREADS, 0, s>>>(out, (i64)L * cols, ring_mask(width));
+  return launch_status();
+}
+
+// z[l][r][c] += b[l][c] << shift (a bias row lifted to the product's
+// precision and broadcast over rows), in place.
+__global__ void k_ring_add_rowvec(u64* __restrict__ z, const u64* __restrict__ b, i64 rows, int cols, int shift,
+                                  u64 msk, i64 total) {
+  GRID_STRIDE(t, total) {
+    const i64 c = t % cols;
+    const i64 l = t / ((i64)rows * cols);
+    z[t] = (z[t] + (b[l * cols + c] << shift)) & msk;
+  }
+}
+
+extern "C" int mpx_ring_add_rowvec(uint64_t* z, const uint64_t* b, int L, int64_t rows, int64_t cols, int shift,
+                                   int width, void* stream) {
+  CHECK_ARG(z && b && L >= 1 && rows >= 0 && cols >= 1 && shift >= 0 && shift < 64 && width >= 1 && width <= 64);
+  const i64 total = (i64)L * rows * cols;
+  if (total == 0) return MPX_OK;
+  k_ring_add_rowvec<<<grid_for(total), MPX_THREADS, 0, (cudaStream_t)stream>>>(z, b, rows, (int)cols, shift,
+                                                                                ring_mask(width), total);
+  return launch_status();
+}
+
+// k x k window sums with stride k over [planes][H][W] -> [planes][H/k][W/k]
+// (average pooling before its power-of-two truncation).
+__global__ void k_ring_pool_sum(u64* __restrict__ out, const u64* __restrict__ x, i64 planes, int H, int W,
+                                int k, u64 msk) {
+  const int OH = H / k, OW = W / k;
+  const i64 n = planes * OH * OW;
+  GRID_STRIDE(i, n) {
+    const int oj = (int)(i % OW);
+    const i64 t = i / OW;
+    const int oi = (int)(t % OH);
+    const i64 p = t / OH;
+    const u64* src = x + (p * H + (i64)oi * k) * W + (i64)oj * k;
+    u64 acc = 0;
+    for (int a = 0; a < k; ++a)
+      for (int b = 0; b < k; ++b) acc += src[(i64)a * W + b];
+    out[i] = acc & msk;
+  }
+}
+
+extern "C" int mpx_ring_pool_sum(uint64_t* out, const uint64_t* x, int64_t planes, int64_t H, int64_t W,
+                                 int64_t k, int width, void* stream) {
+  CHECK_ARG(out && x && planes >= 0 && k >= 1 && H % k == 0 && W % k == 0 && H < (1 << 20) && W < (1 << 20) &&
+            width >= 1 && width <= 64);
+  const i64 n = planes * (H / k) * (W / k);
+  if (n == 0) return MPX_OK;
+  k_ring_pool_sum<<<grid_for(n), MPX_THREADS, 0, (cudaStream_t)stream>>>(out, x, planes, (int)H, (int)W, (int)k,
+                                                                          ring_mask(width));
+  return launch_status();
+}
+
 // --------------------------------------------------------------------------
 // Codec: floor(x * 2^f) as int64, two's complement into Z_2^w (ring.py:76-89)
 
@@ -416,50 +527,56 @@ extern "C" int mpx_device_sm_count(int device) {
 // Convolution layout ops on shares (local, linear): im2col gathers, col2im
 // scatter-adds mod 2^w. x: [L][B][C][H][W]; cols: [L][B*OH*OW][C*K*K].
 
-__global__ void k_im2col(u64* __restrict__ out, const u64* __restrict__ x, int L, i64 B, int C, int H, int W,
-                         int K, int S, int P, int OH, int OW) {
-  const i64 cols = (i64)C * K * K;
-  const i64 rows = B * OH * OW;
-  const i64 total = (i64)L * rows * cols;
-  GRID_STRIDE(t, total) {
-    const i64 col = t % cols;
-    const i64 rr = t / cols;
-    const i64 row = rr % rows;
-    const i64 l = rr / rows;
-    const int kw = (int)(col % K), kh = (int)((col / K) % K), c = (int)(col / ((i64)K * K));
-    const int ow = (int)(row % OW), oh = (int)((row / OW) % OH);
-    const i64 b = row / ((i64)OH * OW);
-    const int h = oh * S - P + kh, w = ow * S - P + kw;
+// Index math in IT (u32 whenever the tensor fits: 64-bit division costs
+// ~10x more and dominated these gathers).
+template <typename IT>
+__global__ void k_im2col(u64* __restrict__ out, const u64* __restrict__ x, IT B, IT C, IT H, IT W, IT K, IT S,
+                         IT P, IT OH, IT OW, IT total) {
+  const IT cols = C * K * K;
+  const IT rows = B * OH * OW;
+  for (IT t = (IT)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (IT)gridDim.x * blockDim.x) {
+    const IT col = t % cols;
+    const IT rr = t / cols;
+    const IT row = rr % rows;
+    const IT l = rr / rows;
+    const IT kw = col % K, ckh = col / K;
+    const IT kh = ckh % K, c = ckh / K;
+    const IT ow = row % OW, boh = row / OW;
+    const IT oh = boh % OH, b = boh / OH;
+    const long long h = (long long)(oh * S + kh) - (long long)P, w = (long long)(ow * S + kw) - (long long)P;
     u64 v = 0;
-    if (h >= 0 && h < H && w >= 0 && w < W) v = x[(((l * B + b) * C + c) * H + h) * (i64)W + w];
+    if (h >= 0 && h < (long long)H && w >= 0 && w < (long long)W)
+      v = x[(((i64)(l * B + b) * C + c) * H + h) * (i64)W + w];
     out[t] = v;
   }
 }
 
-__global__ void k_col2im(u64* __restrict__ dx, const u64* __restrict__ colsb, int L, i64 B, int C, int H, int W,
-                         int K, int S, int P, int OH, int OW, u64 msk) {
-  const i64 cols = (i64)C * K * K;
-  const i64 rows = B * OH * OW;
-  const i64 total = (i64)L * B * C * H * W;
-  GRID_STRIDE(t, total) {
-    const int w = (int)(t % W);
-    const int h = (int)((t / W) % H);
-    const int c = (int)((t / ((i64)W * H)) % C);
-    const i64 bl = t / ((i64)W * H * C);
-    const i64 b = bl % B, l = bl / B;
+template <typename IT>
+__global__ void k_col2im(u64* __restrict__ dx, const u64* __restrict__ colsb, IT B, IT C, IT H, IT W, IT K,
+                         IT S, IT P, IT OH, IT OW, IT total, u64 msk) {
+  const IT cols = C * K * K;
+  const IT rows = B * OH * OW;
+  for (IT t = (IT)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (IT)gridDim.x * blockDim.x) {
+    const IT w = t % W;
+    const IT t1 = t / W;
+    const IT h = t1 % H;
+    const IT t2 = t1 / H;
+    const IT c = t2 % C;
+    const IT bl = t2 / C;
+    const IT b = bl % B, l = bl / B;
     u64 acc = 0;
-    for (int kh = 0; kh < K; ++kh) {
-      const int hh = h + P - kh;
+    for (IT kh = 0; kh < K; ++kh) {
+      const long long hh = (long long)(h + P) - (long long)kh;
       if (hh < 0 || hh % S) continue;
-      const int oh = hh / S;
+      const IT oh = (IT)(hh / S);
       if (oh >= OH) continue;
-      for (int kw = 0; kw < K; ++kw) {
-        const int ww = w + P - kw;
+      for (IT kw = 0; kw < K; ++kw) {
+        const long long ww = (long long)(w + P) - (long long)kw;
         if (ww < 0 || ww % S) continue;
-        const int ow = ww / S;
+        const IT ow = (IT)(ww / S);
         if (ow >= OW) continue;
-        const i64 row = (b * OH + oh) * OW + ow;
-        acc += colsb[(l * rows + row) * cols + ((i64)c * K + kh) * K + kw];
+        const i64 row = ((i64)b * OH + oh) * OW + ow;
+        acc += colsb[((i64)l * rows + row) * cols + ((i64)c * K + kh) * K + kw];
       }
     }
     dx[t] = acc & msk;
@@ -472,8 +589,13 @@ extern "C" int mpx_im2col(uint64_t* out, const uint64_t* x, int L, int64_t B, in
   const int OH = (H + 2 * pad - K) / stride + 1, OW = (W + 2 * pad - K) / stride + 1;
   CHECK_ARG(OH >= 1 && OW >= 1);
   const i64 total = (i64)L * B * OH * OW * C * K * K;
-  k_im2col<<<grid_for(total), MPX_THREADS, 0, (cudaStream_t)stream>>>(out, x, L, B, C, H, W, K, stride, pad, OH,
-                                                                        OW);
+  if (total == 0) return MPX_OK;
+  if (total < (1ll << 31))
+    k_im2col<uint32_t><<<grid_for(total), MPX_THREADS, 0, (cudaStream_t)stream>>>(
+        out, x, (uint32_t)B, C, H, W, K, stride, pad, OH, OW, (uint32_t)total);
+  else
+    k_im2col<uint64_t><<<grid_for(total), MPX_THREADS, 0, (cudaStream_t)stream>>>(
+        out, x, (uint64_t)B, C, H, W, K, stride, pad, OH, OW, (uint64_t)total);
   return launch_status();
 }
 
@@ -484,7 +606,12 @@ extern "C" int mpx_col2im(uint64_t* dx, const uint64_t* cols, int L, int64_t B, 
   const int OH = (H + 2 * pad - K) / stride + 1, OW = (W + 2 * pad - K) / stride + 1;
   CHECK_ARG(OH >= 1 && OW >= 1);
   const i64 total = (i64)L * B * C * H * W;
-  k_col2im<<<grid_for(total), MPX_THREADS, 0, (cudaStream_t)stream>>>(dx, cols, L, B, C, H, W, K, stride, pad, OH,
-                                                                        OW, ring_mask(width));
+  if (total == 0) return MPX_OK;
+  if (total < (1ll << 31) && (i64)L * B * OH * OW * C * K * K < (1ll << 32))
+    k_col2im<uint32_t><<<grid_for(total), MPX_THREADS, 0, (cudaStream_t)stream>>>(
+        dx, cols, (uint32_t)B, C, H, W, K, stride, pad, OH, OW, (uint32_t)total, ring_mask(width));
+  else
+    k_col2im<uint64_t><<<grid_for(total), MPX_THREADS, 0, (cudaStream_t)stream>>>(
+        dx, cols, (uint64_t)B, C, H, W, K, stride, pad, OH, OW, (uint64_t)total, ring_mask(width));
   return launch_status();
 }

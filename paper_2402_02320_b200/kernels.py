@@ -306,6 +306,35 @@ def auto_ksplit(tiles: int, batch: int, Kpad: int) -> int:
     return max(need, min(want, nk))
 
 
+def ring_colsum(out, x, L, rows, cols, width):
+    if _dry(out):
+        return out
+    call("mpx_ring_colsum", ptr(out), ptr(x), L, rows, cols, width)
+    return out
+
+
+def ring_pool_sum(out, x, planes, H, W, k, width):
+    if _dry(out):
+        return out
+    call("mpx_ring_pool_sum", ptr(out), ptr(x), planes, H, W, k, width)
+    return out
+
+
+def ring_add_rowvec(z, b, L, rows, cols, shift, width):
+    if _dry(z):
+        return z
+    call("mpx_ring_add_rowvec", ptr(z), ptr(b), L, rows, cols, shift, width)
+    return z
+
+
+def beaver_gemm(Z, sZ, C_ptr, sC, D, E, A_ptr, sA, B_ptr, sB, L, M, K, N, p0, width):
+    """Z_l = C_l + D @ (B_l + [l==p0] E) + A_l @ E (one SIMT launch, all local parties)."""
+    if _dry(Z):
+        return Z
+    call("mpx_beaver_gemm", ptr(Z), sZ, C_ptr, sC, ptr(D), ptr(E), A_ptr, sA, B_ptr, sB, L, M, K, N, p0, width)
+    return Z
+
+
 def beaver_limbs(A8, B8, D, E, A_ptr, a_ps, B_ptr, b_ps, L, M, K, N, Mpad, Npad, Kpad, p0):
     if _dry(A8):
         return
@@ -313,13 +342,17 @@ def beaver_limbs(A8, B8, D, E, A_ptr, a_ps, B_ptr, b_ps, L, M, K, N, Mpad, Npad,
          Kpad, p0)
 
 
-def gemm_limbs(C, A8, B8, batch, M, N, Mpad, Npad, Kpad, ldc, sC, accumulate, width, ksplit=None):
+def gemm_limbs(C, A8, B8, batch, M, N, Mpad, Npad, Kpad, ldc, sC, accumulate, width, ksplit=None,
+               cin=None, s_cin=0):
+    """C[z] = (C[z] if accumulate) + (Cin[z] if cin) + limb product; ``cin`` is a
+    tensor or raw device address sharing C's row stride."""
     if _dry(C):
         return C
     if ksplit is None:
         ksplit = auto_ksplit((Mpad // 128) * (Npad // 64), batch, Kpad) if width == 64 else 1
+    cin_ptr = None if cin is None else (cin if isinstance(cin, int) else ptr(cin))
     call("mpx_gemm_limbs", ptr(C), ptr(A8), ptr(B8), batch, M, N, Mpad, Npad, Kpad, ldc, sC,
-         int(accumulate), width, int(ksplit))
+         int(accumulate), width, int(ksplit), cin_ptr, s_cin)
     return C
 
 

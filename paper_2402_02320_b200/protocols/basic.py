@@ -77,25 +77,26 @@ def batch_matmul(session, pairs) -> list[AShare]:
         A, B, C = trip[i]
         D, E = opened[2 * i], opened[2 * i + 1]
         Z = session.alloc((L, m, r))
-        if not session.dry:
-            Z.copy_(C)
         if not session.dry and _use_tc(m, k, r, w):
-            _beaver_matmul_tc(session, Z, D, E, A, B, L, m, k, r, w)
+            _beaver_matmul_tc(session, Z, D, E, A, B, C, L, m, k, r, w)
         else:
-            K.gemm(Z, D, B.data_ptr(), L, m, k, r, 0, B.stride(0), m * r, True, w, simt=True)
-            K.gemm(Z, A.data_ptr(), E, L, m, k, r, A.stride(0), 0, m * r, True, w, simt=True)
-            if session.p0 >= 0:
-                K.gemm(Z[session.p0], D, E, 1, m, k, r, 0, 0, 0, True, w, simt=True)
+            K.beaver_gemm(Z, m * r, C.data_ptr(), C.stride(0), D, E, A.data_ptr(), A.stride(0), B.data_ptr(),
+                          B.stride(0), L, m, k, r, session.p0, w)
         session.metrics.count(matmul_count=1, matmul_macs=m * k * r)
         out.append(AShare(Z, w, x.frac + y.frac, session.parties))
     return out
 
 
 def _use_tc(m, k, r, w=64) -> bool:
-    return K.tc_eligible(m, 2 * k, r, w) and (w == 64 or 2 * k <= K.TC_MAX_K)
+    """tcgen05 limb GEMM when the output fills its 128 x 64 tiles (padding
+    waste <= 1/3 on each side); thin or tiny products go to the SIMT kernel."""
+    if m < 96 or r < 48:
+        return False
+    waste = (K._rup(m, 128) / m) * (K._rup(r, 64) / r)
+    return waste <= 1.5 and K.tc_eligible(m, 2 * k, r, w) and (w == 64 or 2 * k <= K.TC_MAX_K)
 
 
-def _beaver_matmul_tc(session, Z, D, E, A, B, L, m, k, r, w):
+def _beaver_matmul_tc(session, Z, D, E, A, B, C, L, m, k, r, w):
     """Z_l += [D | A_l] @ [B_l + [l==p0] E ; E] as ONE tcgen05 limb GEMM per party
     (K doubled), so D@E at party 0 folds into its B operand (basic.py:72-75)."""
     Mp, Np, Kp = K._rup(m, 128), K._rup(r, 64), K._rup(2 * k, 128)
@@ -105,7 +106,7 @@ def _beaver_matmul_tc(session, Z, D, E, A, B, L, m, k, r, w):
         A8[:, :, m:, :].zero_()
     K.beaver_limbs(A8, B8, D, E, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), L, m, k, r, Mp, Np, Kp,
                    session.p0)
-    K.gemm_limbs(Z, A8, B8, L, m, r, Mp, Np, Kp, r, m * r, True, w)
+    K.gemm_limbs(Z, A8, B8, L, m, r, Mp, Np, Kp, r, m * r, False, w, cin=C.data_ptr(), s_cin=C.stride(0))
 
 
 def and_gate(session, x: BShare, y: BShare) -> BShare:

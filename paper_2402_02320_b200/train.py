@@ -39,24 +39,19 @@ def _transpose(x: AShare) -> AShare:
     return AShare(x.values.transpose(-1, -2).contiguous(), x.width, x.frac, x.parties)
 
 
-def _bcast_rows(b: AShare, rows: int) -> AShare:
-    """(C,) -> (rows, C) share broadcast (layout only)."""
-    v = b.values.unsqueeze(1).expand(b.L, rows, b.shape[0]).contiguous()
-    return AShare(v, b.width, b.frac, b.parties)
-
-
 def _colsum(session, z: AShare) -> AShare:
     """sum over rows of a (rows, C) share -> (C,) (local ring sum)."""
-    t = _transpose(z)
-    c, r = t.shape
+    r, c = z.shape
     out = session.alloc((session.L, c))
-    K.ring_rowdot(out, t.values, None, session.L, c, r, z.width)
+    K.ring_colsum(out, z.values.contiguous(), session.L, r, c, z.width)
     return AShare(out, z.width, z.frac, session.parties)
 
 
-def _lift(x: AShare, p: int) -> AShare:
-    """x at frac p -> same value at frac 2p (local shift by 2^p)."""
-    return x.mul_public(1 << p, frac_delta=p)
+def _add_bias(session, z: AShare, b: AShare, p: int) -> AShare:
+    """z + broadcast(b * 2^p) over rows, in place on the fresh product z."""
+    rows, cols = z.shape
+    K.ring_add_rowvec(z.values, b.values.contiguous(), session.L, rows, cols, p, z.width)
+    return z
 
 
 @dataclass
@@ -98,7 +93,7 @@ class Conv2d(Layer):
         self.cols = AShare(cv, x.width, x.frac, s.parties)
         self.in_shape = (B, C, H, W)
         z = batch_matmul(s, [(self.cols, self.W)])[0]
-        z = truncate(s, z + _bcast_rows(_lift(self.b, self.p), rows), self.p)
+        z = truncate(s, _add_bias(s, z, self.b, self.p), self.p)
         self.out_hw = (OH, OW)
         v = z.values.view(s.L, B, OH, OW, self.cout).permute(0, 1, 4, 2, 3).contiguous()
         return AShare(v, z.width, z.frac, s.parties)
@@ -137,9 +132,8 @@ class AvgPool2d(Layer):
     def forward(self, s, x: AShare) -> AShare:
         B, C, H, W = x.shape
         k = self.k
-        v = x.values.view(s.L, B, C, H // k, k, W // k, k).permute(0, 1, 2, 3, 5, 4, 6).contiguous()
         out = s.alloc((s.L, B, C, H // k, W // k))
-        K.ring_rowdot(out, v, None, s.L, B * C * (H // k) * (W // k), k * k, x.width)
+        K.ring_pool_sum(out, x.values.contiguous(), s.L * B * C, H, W, k, x.width)
         self.in_shape = (B, C, H, W)
         return truncate(s, AShare(out, x.width, x.frac, s.parties), self.shift, out_frac=x.frac)
 
@@ -167,11 +161,6 @@ class ReLU(Layer):
             layer.sign = sign
         return mul(s, sign, x)
 
-    def _unused(self, s, x):
-        zero = public_ashare(0, x.width, x.frac, s, shape=x.shape)
-        self.sign = bit2a(s, gt(s, x, zero), x.width)
-        return mul(s, self.sign, x)
-
     def backward(self, s, dy: AShare, need_dx: bool = True) -> AShare:
         return mul(s, self.sign, dy)
 
@@ -195,7 +184,7 @@ class Linear(Layer):
     def forward(self, s, x: AShare) -> AShare:
         self.x = x
         z = batch_matmul(s, [(x, self.W)])[0]
-        return truncate(s, z + _bcast_rows(_lift(self.b, self.p), x.shape[0]), self.p)
+        return truncate(s, _add_bias(s, z, self.b, self.p), self.p)
 
     def backward(self, s, dy: AShare, need_dx: bool = True) -> AShare | None:
         pairs = [(_transpose(self.x), dy)]

@@ -1,0 +1,136 @@
+"""GPU: the layer-plumbing kernels behind secure training, each against a
+numpy restatement on random Z_2^w data (bit-exact): the one-launch Beaver
+matrix-product reconstruction (every tile shape, split-K, narrow rings,
+party 0 local or not), the limb GEMM's C-addend epilogue, column sums,
+pooling window sums, bias-row adds, im2col / col2im."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import train_sim as OT
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def K():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2402_02320_b200 import kernels
+    return kernels
+
+
+def _rand(rng, shape, w):
+    v = rng.integers(0, 1 << 63, size=shape, dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, size=shape,
+                                                                                              dtype=np.uint64)
+    if w < 64:
+        v &= np.uint64((1 << w) - 1)
+    return v
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).cuda()
+
+
+def _host(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+def _mm(a, b):
+    """u64 matmul mod 2^64 (numpy uint64 wraps)."""
+    out = np.zeros((a.shape[0], b.shape[1]), dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        for k in range(a.shape[1]):
+            out += np.outer(a[:, k], b[k, :])
+    return out
+
+
+@pytest.mark.parametrize("L,M,Kd,N,p0,w", [
+    (3, 300, 25, 20, 0, 64),      # thin conv-like output: 128x32 tiles
+    (3, 25, 4000, 20, 0, 64),     # tiny output, long K: split-K atomics
+    (2, 130, 70, 130, 1, 64),     # 64x64 tiles
+    (1, 77, 33, 9, -1, 64),       # party mode, party 0 not local
+    (1, 77, 33, 9, 0, 64),
+    (4, 50, 40, 16, 2, 32),       # narrow ring: no split
+    (2, 3, 300, 5, 0, 64),
+])
+def test_beaver_gemm_matches_numpy(K, L, M, Kd, N, p0, w):
+    rng = np.random.default_rng(M * 7 + N)
+    D, E = _rand(rng, (M, Kd), w), _rand(rng, (Kd, N), w)
+    A, B, C = _rand(rng, (L, M, Kd), w), _rand(rng, (L, Kd, N), w), _rand(rng, (L, M, N), w)
+    Zd = torch.empty((L, M, N), dtype=torch.int64, device="cuda")
+    Cd, Ad, Bd = _dev(C), _dev(A), _dev(B)
+    K.beaver_gemm(Zd, M * N, Cd.data_ptr(), M * N, _dev(D), _dev(E), Ad.data_ptr(), M * Kd, Bd.data_ptr(), Kd * N,
+                  L, M, Kd, N, p0, w)
+    got = _host(Zd)
+    msk = np.uint64((1 << w) - 1) if w < 64 else np.uint64(0xFFFFFFFFFFFFFFFF)
+    with np.errstate(over="ignore"):
+        for l in range(L):
+            Bl = B[l] + (E if l == p0 else np.uint64(0))
+            want = (C[l] + _mm(D, Bl) + _mm(A[l], E)) & msk
+            assert np.array_equal(got[l], want), l
+
+
+def test_gemm_limbs_cin_epilogue(K):
+    rng = np.random.default_rng(3)
+    b, M, Kd, N = 2, 200, 96, 100
+    A, B, C = _rand(rng, (b, M, Kd), 64), _rand(rng, (b, Kd, N), 64), _rand(rng, (b, M, N), 64)
+    Mp, Np, Kp = K._rup(M, 128), K._rup(N, 64), K._rup(Kd, 128)
+    Ad, Bd, Cd = _dev(A), _dev(B), _dev(C)
+    for ks in (1, None):
+        A8 = torch.zeros((b, 8, Mp, Kp), dtype=torch.uint8, device="cuda")
+        B8 = torch.zeros((b, 8, Np, Kp), dtype=torch.uint8, device="cuda")
+        for z in range(b):
+            K.limb_split(A8[z], Ad.data_ptr() + 8 * z * M * Kd, M, Kd, Kd, Mp * Kp, Kp, 0, False)
+            K.limb_split(B8[z], Bd.data_ptr() + 8 * z * Kd * N, Kd, N, N, Np * Kp, Kp, 0, True)
+        Z = torch.full((b, M, N), 7, dtype=torch.int64, device="cuda")
+        K.gemm_limbs(Z, A8, B8, b, M, N, Mp, Np, Kp, N, M * N, False, 64, ksplit=ks, cin=Cd, s_cin=M * N)
+        got = _host(Z)
+        with np.errstate(over="ignore"):
+            for z in range(b):
+                assert np.array_equal(got[z], C[z] + _mm(A[z], B[z]))
+
+
+@pytest.mark.parametrize("L,rows,cols,w", [(3, 73728, 20, 64), (2, 1000, 500, 64), (1, 7, 3000, 32), (3, 5, 1, 64)])
+def test_colsum(K, L, rows, cols, w):
+    rng = np.random.default_rng(rows)
+    x = _rand(rng, (L, rows, cols), w)
+    out = torch.empty((L, cols), dtype=torch.int64, device="cuda")
+    K.ring_colsum(out, _dev(x), L, rows, cols, w)
+    with np.errstate(over="ignore"):
+        want = x.sum(axis=1, dtype=np.uint64)
+    if w < 64:
+        want &= np.uint64((1 << w) - 1)
+    assert np.array_equal(_host(out), want)
+
+
+def test_pool_sum_and_add_rowvec(K):
+    rng = np.random.default_rng(9)
+    x = _rand(rng, (3, 4, 5, 24, 24), 64)
+    out = torch.empty((3, 4, 5, 12, 12), dtype=torch.int64, device="cuda")
+    K.ring_pool_sum(out, _dev(x), 60, 24, 24, 2, 64)
+    with np.errstate(over="ignore"):
+        want = x.reshape(3, 4, 5, 12, 2, 12, 2).sum(axis=(4, 6), dtype=np.uint64)
+    assert np.array_equal(_host(out), want)
+    z, b = _rand(rng, (3, 50, 20), 64), _rand(rng, (3, 20), 64)
+    zd = _dev(z)
+    K.ring_add_rowvec(zd, _dev(b), 3, 50, 20, 23, 64)
+    with np.errstate(over="ignore"):
+        want = z + (b << np.uint64(23))[:, None, :]
+    assert np.array_equal(_host(zd), want)
+
+
+@pytest.mark.parametrize("Bn,C,H,k,st,pd", [(4, 3, 12, 5, 1, 0), (2, 2, 9, 3, 2, 1), (3, 1, 28, 5, 1, 0)])
+def test_im2col_col2im(K, Bn, C, H, k, st, pd):
+    rng = np.random.default_rng(H)
+    L = 2
+    x = _rand(rng, (L, Bn, C, H, H), 64)
+    OH = (H + 2 * pd - k) // st + 1
+    cols = torch.empty((L, Bn * OH * OH, C * k * k), dtype=torch.int64, device="cuda")
+    K.im2col(cols, _dev(x), L, Bn, C, H, H, k, st, pd)
+    assert np.array_equal(_host(cols), OT.im2col(x, k, st, pd))
+    g = _rand(rng, (L, Bn * OH * OH, C * k * k), 64)
+    dx = torch.empty((L, Bn, C, H, H), dtype=torch.int64, device="cuda")
+    K.col2im(dx, _dev(g), L, Bn, C, H, H, k, st, pd, 64)
+    assert np.array_equal(_host(dx), OT.col2im(g, (L, Bn, C, H, H), k, st, pd, 64))
