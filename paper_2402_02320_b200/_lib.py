@@ -18,7 +18,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmpx.so")
+LIB_PATH = os.environ.get("MPX_LIB") or os.path.join(_HERE, "libmpx.so")  # MPX_LIB: A/B builds
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int

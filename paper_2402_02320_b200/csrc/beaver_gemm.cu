@@ -13,12 +13,42 @@
 
 #define BG_BK 16
 
-template <int BM, int BN>
-__global__ void __launch_bounds__((BM / 4) * (BN / 4))
+// <= 128 registers per thread (a block occupies whole warps)
+constexpr int bg_min_blocks(int nt) { return 512 / (nt < 32 ? 32 : nt); }
+
+template <int BM, int BN, int TN, bool FULL>
+__device__ __forceinline__ void bg_tile_math(u64 (&acc)[4][TN], const u64 (*Ds)[BM + 1], const u64 (*As)[BM + 1],
+                                             const u64 (*Bs)[BN], const u64 (*Es)[BN], int tx, int ty, int kn) {
+  constexpr int TX = BN / TN, TY = BM / 4;
+#pragma unroll
+  for (int kk = 0; kk < BG_BK; ++kk) {
+    if (!FULL && kk >= kn) break;
+    u64 d[4], a[4], b[TN], e[TN];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      d[i] = Ds[kk][ty + TY * i];
+      a[i] = As[kk][ty + TY * i];
+    }
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      b[j] = Bs[kk][tx + TX * j];
+      e[j] = Es[kk][tx + TX * j];
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) acc[i][j] += d[i] * b[j] + a[i] * e[j];
+  }
+}
+
+// CTA tile BM x BN, each thread 4 rows x TN columns (strided by TY / TX so
+// shared-memory reads are conflict-free broadcasts / consecutive words).
+template <int BM, int BN, int TN>
+__global__ void __launch_bounds__((BM / 4) * (BN / TN), bg_min_blocks((BM / 4) * (BN / TN)))
     k_beaver_gemm(u64* __restrict__ Z, i64 sZ, const u64* __restrict__ C, i64 sC, const u64* __restrict__ D,
                   const u64* __restrict__ E, const u64* __restrict__ A, i64 sA, const u64* __restrict__ B,
                   i64 sB, int M, int K, int N, int p0, u64 msk, int ksplit, int kchunk) {
-  constexpr int TX = BN / 4, TY = BM / 4, NT = TX * TY;
+  constexpr int TX = BN / TN, TY = BM / 4, NT = TX * TY;
   __shared__ u64 Ds[BG_BK][BM + 1];
   __shared__ u64 As[BG_BK][BM + 1];
   __shared__ u64 Bs[BG_BK][BN];
@@ -31,16 +61,14 @@ __global__ void __launch_bounds__((BM / 4) * (BN / 4))
   const bool addE = (l == p0);
   const int row0 = blockIdx.y * BM, col0 = blockIdx.x * BN;
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
-  u64 acc[4][4];
+  u64 acc[4][TN];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0;
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0;
 
   for (int k0 = kbeg; k0 < kend; k0 += BG_BK) {
-#pragma unroll
-    for (int q = 0; q < (BM * BG_BK) / NT; ++q) {
-      const int idx = threadIdx.x + q * NT;
+    for (int idx = threadIdx.x; idx < BM * BG_BK; idx += NT) {
       const int r = idx / BG_BK, kk = idx % BG_BK;
       const int gr = row0 + r, gk = k0 + kk;
       const bool ok = gr < M && gk < kend;
@@ -48,9 +76,7 @@ __global__ void __launch_bounds__((BM / 4) * (BN / 4))
       Ds[kk][r] = ok ? D[o] : 0ull;
       As[kk][r] = ok ? Al[o] : 0ull;
     }
-#pragma unroll
-    for (int q = 0; q < (BN * BG_BK) / NT; ++q) {
-      const int idx = threadIdx.x + q * NT;
+    for (int idx = threadIdx.x; idx < BN * BG_BK; idx += NT) {
       const int kk = idx / BN, c = idx % BN;
       const int gk = k0 + kk, gc = col0 + c;
       const bool ok = gk < kend && gc < N;
@@ -60,24 +86,11 @@ __global__ void __launch_bounds__((BM / 4) * (BN / 4))
       Bs[kk][c] = ok ? (Bl[o] + (addE ? e : 0ull)) : 0ull;
     }
     __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < BG_BK; ++kk) {
-      u64 d[4], a[4], b[4], e[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        d[i] = Ds[kk][ty + TY * i];
-        a[i] = As[kk][ty + TY * i];
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        b[j] = Bs[kk][tx + TX * j];
-        e[j] = Es[kk][tx + TX * j];
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] += d[i] * b[j] + a[i] * e[j];
-    }
+    const int kn = kend - k0;
+    if (kn >= BG_BK)
+      bg_tile_math<BM, BN, TN, true>(acc, Ds, As, Bs, Es, tx, ty, kn);
+    else
+      bg_tile_math<BM, BN, TN, false>(acc, Ds, As, Bs, Es, tx, ty, kn);
     __syncthreads();
   }
   u64* Zl = Z + (i64)l * sZ;
@@ -87,7 +100,7 @@ __global__ void __launch_bounds__((BM / 4) * (BN / 4))
     const int gr = row0 + ty + TY * i;
     if (gr >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < TN; ++j) {
       const int gc = col0 + tx + TX * j;
       if (gc >= N) continue;
       const i64 o = (i64)gr * N + gc;
@@ -101,16 +114,20 @@ __global__ void __launch_bounds__((BM / 4) * (BN / 4))
 
 namespace {
 struct Cfg {
-  int bm, bn;
+  int bm, bn, tn;
 };
-const Cfg kCfgs[] = {{64, 64}, {128, 32}, {128, 16}, {32, 32}};
+// (BM, BN, TN): square-ish tiles for wide outputs, thin ones sized to common
+// layer widths (20 / 10 output channels), small-M tiles for weight gradients
+const Cfg kCfgs[] = {{64, 64, 4}, {128, 32, 4}, {128, 16, 4}, {32, 32, 4},
+                     {128, 20, 5}, {128, 10, 5}, {32, 20, 5}, {32, 10, 5}};
+constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 
-template <int BM, int BN>
+template <int BM, int BN, int TN>
 void launch(dim3 grid, cudaStream_t s, uint64_t* Z, int64_t sZ, const uint64_t* C, int64_t sC, const uint64_t* D,
             const uint64_t* E, const uint64_t* A, int64_t sA, const uint64_t* B, int64_t sB, int M, int K, int N,
             int p0, u64 msk, int ksplit, int kchunk) {
-  k_beaver_gemm<BM, BN><<<grid, (BM / 4) * (BN / 4), 0, s>>>(Z, sZ, C, sC, D, E, A, sA, B, sB, M, K, N, p0, msk,
-                                                              ksplit, kchunk);
+  k_beaver_gemm<BM, BN, TN><<<grid, (BM / 4) * (BN / TN), 0, s>>>(Z, sZ, C, sC, D, E, A, sA, B, sB, M, K, N, p0,
+                                                                    msk, ksplit, kchunk);
 }
 }  // namespace
 
@@ -122,20 +139,25 @@ extern "C" int mpx_beaver_gemm(uint64_t* Z, int64_t sZ, const uint64_t* C, int64
   CHECK_ARG(p0 < L);
   // tile shape: least padded output area, ties to the larger tile
   int best = 0;
-  i64 best_cost = -1;
-  for (int c = 0; c < 4; ++c) {
+  i64 best_cost = -1, best_area = 0;
+  for (int c = 0; c < kNumCfgs; ++c) {
     const i64 bm = kCfgs[c].bm, bn = kCfgs[c].bn;
     const i64 cost = ((M + bm - 1) / bm) * bm * ((N + bn - 1) / bn) * bn;
-    if (best_cost < 0 || cost < best_cost) {
+    if (best_cost < 0 || cost < best_cost || (cost == best_cost && bm * bn > best_area)) {
       best = c;
       best_cost = cost;
+      best_area = bm * bn;
     }
   }
   const int bm = kCfgs[best].bm, bn = kCfgs[best].bn;
+  const int nt = (bm / 4) * (bn / kCfgs[best].tn);
   const i64 tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn) * L;
+  // resident CTAs per SM at <= 128 registers per thread
+  const i64 per_sm = min((i64)32, (i64)(65536 / (max(nt, 32) * 128)));
+  const i64 target = 148 * per_sm;
   int ksplit = 1;
-  if (width == 64 && tiles < 2 * 148 && K >= 4 * BG_BK) {
-    ksplit = (int)min((i64)((2 * 148 + tiles - 1) / tiles), (K + 4 * BG_BK - 1) / (4 * BG_BK));
+  if (width == 64 && tiles < target && K >= 4 * BG_BK) {
+    ksplit = (int)min((target + tiles - 1) / tiles, (K + BG_BK - 1) / BG_BK);
     if (ksplit < 1) ksplit = 1;
   }
   const i64 kchunk = ((K + ksplit - 1) / ksplit + BG_BK - 1) / BG_BK * BG_BK;
@@ -150,11 +172,21 @@ extern "C" int mpx_beaver_gemm(uint64_t* Z, int64_t sZ, const uint64_t* C, int64
   }
   dim3 grid((unsigned)((N + bn - 1) / bn), (unsigned)((M + bm - 1) / bm), (unsigned)(L * ksplit));
   const u64 msk = ring_mask(width);
+#define BG_CASE(I, BM_, BN_, TN_)                                                                             \
+  case I:                                                                                                    \
+    launch<BM_, BN_, TN_>(grid, s, Z, sZ, C, sC, D, E, A, sA, B, sB, (int)M, (int)K, (int)N, p0, msk, ksplit, \
+                          (int)kchunk);                                                                      \
+    break;
   switch (best) {
-    case 0: launch<64, 64>(grid, s, Z, sZ, C, sC, D, E, A, sA, B, sB, (int)M, (int)K, (int)N, p0, msk, ksplit, (int)kchunk); break;
-    case 1: launch<128, 32>(grid, s, Z, sZ, C, sC, D, E, A, sA, B, sB, (int)M, (int)K, (int)N, p0, msk, ksplit, (int)kchunk); break;
-    case 2: launch<128, 16>(grid, s, Z, sZ, C, sC, D, E, A, sA, B, sB, (int)M, (int)K, (int)N, p0, msk, ksplit, (int)kchunk); break;
-    default: launch<32, 32>(grid, s, Z, sZ, C, sC, D, E, A, sA, B, sB, (int)M, (int)K, (int)N, p0, msk, ksplit, (int)kchunk); break;
+    BG_CASE(0, 64, 64, 4)
+    BG_CASE(1, 128, 32, 4)
+    BG_CASE(2, 128, 16, 4)
+    BG_CASE(3, 32, 32, 4)
+    BG_CASE(4, 128, 20, 5)
+    BG_CASE(5, 128, 10, 5)
+    BG_CASE(6, 32, 20, 5)
+    default: BG_CASE(7, 32, 10, 5)
   }
+#undef BG_CASE
   return launch_status();
 }

@@ -363,7 +363,7 @@ def gemm_tc(C, A, B, batch, M, K, N, sA, sB, sC, accumulate, width):
     if _dry(C):
         return C
     dev = C.device
-    Mpad, Npad = _rup(M, 128), _rup(N, 64)
+    Mpad, Npad = _rup(M, 128), _rup(N, 32)
     a_ptr = A if isinstance(A, int) else ptr(A)
     b_ptr = B if isinstance(B, int) else ptr(B)
     step = K if width == 64 else TC_MAX_K

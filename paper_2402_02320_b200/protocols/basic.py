@@ -90,16 +90,16 @@ def batch_matmul(session, pairs) -> list[AShare]:
 def _use_tc(m, k, r, w=64) -> bool:
     """tcgen05 limb GEMM when the output fills its 128 x 64 tiles (padding
     waste <= 1/3 on each side); thin or tiny products go to the SIMT kernel."""
-    if m < 96 or r < 48:
+    if m < 96 or r < 24:
         return False
-    waste = (K._rup(m, 128) / m) * (K._rup(r, 64) / r)
+    waste = (K._rup(m, 128) / m) * (K._rup(r, 32) / r)
     return waste <= 1.5 and K.tc_eligible(m, 2 * k, r, w) and (w == 64 or 2 * k <= K.TC_MAX_K)
 
 
 def _beaver_matmul_tc(session, Z, D, E, A, B, C, L, m, k, r, w):
     """Z_l += [D | A_l] @ [B_l + [l==p0] E ; E] as ONE tcgen05 limb GEMM per party
     (K doubled), so D@E at party 0 folds into its B operand (basic.py:72-75)."""
-    Mp, Np, Kp = K._rup(m, 128), K._rup(r, 64), K._rup(2 * k, 128)
+    Mp, Np, Kp = K._rup(m, 128), K._rup(r, 32), K._rup(2 * k, 128)
     A8 = torch.empty((L, 8, Mp, Kp), dtype=torch.uint8, device=Z.device)
     B8 = torch.empty((L, 8, Np, Kp), dtype=torch.uint8, device=Z.device)
     if Mp > m:

@@ -54,6 +54,9 @@ def _mm(a, b):
     (1, 77, 33, 9, 0, 64),
     (4, 50, 40, 16, 2, 32),       # narrow ring: no split
     (2, 3, 300, 5, 0, 64),
+    (3, 1000, 30, 10, 0, 64),     # 128x10 tiles, partial k-tile
+    (3, 2000, 25, 20, 1, 64),     # 128x20 tiles
+    (2, 20, 3000, 10, 0, 64),     # 32x10 tiles, split-K
 ])
 def test_beaver_gemm_matches_numpy(K, L, M, Kd, N, p0, w):
     rng = np.random.default_rng(M * 7 + N)

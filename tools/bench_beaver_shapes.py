@@ -1,0 +1,58 @@
+"""Time the Beaver matrix-product reconstruction per shape on both kernels:
+SIMT one-launch (mpx_beaver_gemm) vs tcgen05 limbs (beaver_limbs + gemm_limbs).
+
+    python tools/bench_beaver_shapes.py [--parties 3]
+Shapes default to the LeNet batch-128 training step's products (m, k, r).
+"""
+import argparse, json, os, sys
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2402_02320_b200 import kernels as K  # noqa: E402
+
+LENET = [(73728, 25, 20), (25, 73728, 20), (8192, 500, 50), (500, 8192, 50), (8192, 50, 500),
+         (128, 800, 500), (800, 128, 500), (128, 500, 800), (128, 500, 10), (500, 128, 10), (128, 10, 500)]
+
+
+def timeit(fn, reps=20):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps * 1e3
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--parties", type=int, default=3)
+    a = ap.parse_args()
+    L = a.parties
+    out = []
+    for m, k, r in LENET:
+        g = torch.Generator(device="cuda").manual_seed(1)
+        rnd = lambda *s: torch.randint(-2**62, 2**62, s, device="cuda", generator=g)  # noqa: E731
+        D, E = rnd(m, k), rnd(k, r)
+        A, B, C = rnd(L, m, k), rnd(L, k, r), rnd(L, m, r)
+        Z = torch.empty((L, m, r), dtype=torch.int64, device="cuda")
+        simt = timeit(lambda: K.beaver_gemm(Z, m * r, C.data_ptr(), m * r, D, E, A.data_ptr(), m * k, B.data_ptr(),
+                                            k * r, L, m, k, r, 0, 64))
+        Zs = Z.clone()
+        Mp, Np, Kp = K._rup(m, 128), K._rup(r, 32), K._rup(2 * k, 128)
+        A8 = torch.zeros((L, 8, Mp, Kp), dtype=torch.uint8, device="cuda")
+        B8 = torch.empty((L, 8, Np, Kp), dtype=torch.uint8, device="cuda")
+
+        def tc():
+            K.beaver_limbs(A8, B8, D, E, A.data_ptr(), m * k, B.data_ptr(), k * r, L, m, k, r, Mp, Np, Kp, 0)
+            K.gemm_limbs(Z, A8, B8, L, m, r, Mp, Np, Kp, r, m * r, False, 64, cin=C, s_cin=m * r)
+        t = timeit(tc)
+        same = bool(torch.equal(Z, Zs))
+        out.append({"m": m, "k": k, "r": r, "simt_us": round(simt, 1), "tc_us": round(t, 1), "equal": same})
+        print(json.dumps(out[-1]), flush=True)
+
+
+if __name__ == "__main__":
+    main()
