@@ -157,16 +157,58 @@ def cpu_lenet_reference(n_parties: int, cores: int | None = None):
 
 
 class ClockSampler:
+    """SM clock + throttle reasons polled every 5 ms from NVML on a host
+    thread, so even a ~50 ms timed region holds several samples; falls back
+    to `nvidia-smi -lms 50` when NVML is unavailable."""
+
     FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4))
 
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.proc = None
+        self.thread = None
+        self.rows = []
         self.path = tempfile.mktemp(suffix=".csv")
 
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        want = str(getattr(torch.cuda.get_device_properties(self.gpu), "uuid", "")).lower()
+        for i in range(pynvml.nvmlDeviceGetCount()):
+            h = pynvml.nvmlDeviceGetHandleByIndex(i)
+            u = pynvml.nvmlDeviceGetUUID(h)
+            u = (u.decode() if isinstance(u, bytes) else str(u)).lower()
+            if want and want in u:
+                return pynvml, h
+        return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+
     def start(self):
+        import threading
+        try:
+            nv, h = self._nvml_handle()
+            self.stop_evt = threading.Event()
+            getr = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+
+            def poll():
+                while not self.stop_evt.is_set():
+                    try:
+                        self.rows.append((time.time(), float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                          float(smax), int(getr(h))))
+                    except Exception:
+                        pass
+                    self.stop_evt.wait(0.005)
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.thread = None
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
@@ -175,37 +217,42 @@ class ClockSampler:
         except OSError:
             self.proc = None
 
-    def stop(self, window=None) -> dict:
-        """Median SM clock and active throttle reasons over the samples taken
-        inside ``window`` (host epoch seconds of the timed region)."""
+    def _smi_rows(self):
         import datetime
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
         self.proc.wait()
         self.fh.close()
         rows = []
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 10:
                 continue
             try:
                 ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
-                rows.append((ts, float(parts[2]), float(parts[3]), parts[6:10]))
+                mask = sum(bit for (_, bit), v in zip(self.REASONS, parts[6:10]) if v.lower().startswith("active"))
+                rows.append((ts, float(parts[2]), float(parts[3]), mask))
             except ValueError:
                 continue
         os.unlink(self.path)
-        inside = [r for r in rows if window and window[0] - 0.05 <= r[0] <= window[1] + 0.05]
+        return rows
+
+    def stop(self, window=None) -> dict:
+        """Median SM clock and active throttle reasons over the samples taken
+        inside ``window`` (host epoch seconds of the timed region)."""
+        if self.thread is not None:
+            self.stop_evt.set()
+            self.thread.join()
+            rows, src = self.rows, "nvml 5 ms"
+        elif self.proc is not None:
+            rows, src = self._smi_rows(), "nvidia-smi 50 ms"
+        else:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml / nvidia-smi unavailable"]}
+        inside = [r for r in rows if window and window[0] <= r[0] <= window[1]]
         use = inside or rows
-        reasons = set()
-        for r in use:
-            for nm, v in zip(names, r[3]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
+        reasons = sorted({nm for r in use for nm, bit in self.REASONS if r[3] & bit})
         return {"sm_mhz": float(np.median([r[1] for r in use])) if use else None,
                 "sm_max_mhz": max(r[2] for r in use) if use else None,
-                "reasons": sorted(reasons), "samples": len(use),
+                "reasons": reasons, "samples": len(use), "source": src,
                 "window": "timed region" if inside else "whole run (no sample fell inside the timed region)"}
 
 
@@ -752,7 +799,7 @@ def run_b200(args, group=None):
             "clocks": clk,
             "roofline": roofline,
             "rounds_per_step": sd.metrics.total.rounds,
-            "dealer_ms_per_step": float(np.mean(deal_ms)),
+            "dealer_ms_per_step": float(np.median(deal_ms[args.warmup:])),
             "loss_first_last": losses,
             "kernels": _kernel_table(per),
             "cpu_baseline": cpu,

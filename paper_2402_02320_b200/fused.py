@@ -15,6 +15,7 @@ tests/test_fused_ops.py.
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 
 import torch
@@ -43,7 +44,7 @@ class FusedParams(ctypes.Structure):
                 ("c", ctypes.c_int), ("L", ctypes.c_int), ("p0", ctypes.c_int),
                 ("log2e_p", ctypes.c_uint64), ("bias_2p", ctypes.c_uint64), ("one_p", ctypes.c_uint64),
                 ("m1_p", ctypes.c_uint64), ("ln2_p", ctypes.c_uint64), ("coef_p", ctypes.c_uint64 * 5),
-                ("coef0_2p", ctypes.c_uint64), ("coef_nz", ctypes.c_int * 5)]
+                ("coef0_2p", ctypes.c_uint64), ("coef_nz", ctypes.c_int * 5), ("pf", ctypes.c_int)]
 
 
 def _take_ref(store, method: str, args: tuple, n: int) -> tuple:
@@ -272,9 +273,15 @@ def run_fused(kind: str, session, x: AShare, params, protocol) -> AShare:
     return AShare(y, out_w, out_f, session.parties)
 
 
+# 1: the ReLU / max-level kernels pull each element's whole take list towards
+# L2 before the first round (latency-bound carry chains); env MPX_PF_CMP=0 off.
+PREFETCH_CMP = int(os.environ.get("MPX_PF_CMP", "1"))
+
+
 def _basic_params(session, x: AShare) -> FusedParams:
     P = FusedParams()
     P.w, P.p, P.L, P.p0 = x.width, x.frac, session.L, session.p0
+    P.pf = PREFETCH_CMP
     return P
 
 
