@@ -305,10 +305,28 @@ def alg_bytes(name, a):
             return 16 * a[4]
         if name == "mpx_gemm_limbs":     # int8 ops, not bytes: see roofline_for
             return None
-        if name in ("mpx_reciprocal_fused", "mpx_exp_fused", "mpx_log_fused"):
+        if name in ("mpx_reciprocal_fused", "mpx_exp_fused", "mpx_log_fused", "mpx_relu_fused",
+                    "mpx_maxlevel_fused"):
             from paper_2402_02320_b200.fused import material_bytes
-            kind, n, L, calls = a
-            return material_bytes(calls, L) + 2 * 8 * L * n   # material + x in + y out
+            kind, n, L, calls, io = a
+            return material_bytes(calls, L) + io * 8 * L * n   # material + share words in / out
+        if name == "mpx_ring_colsum":
+            L, rows, cols = a[2], a[3], a[4]
+            return 8 * L * rows * cols + 8 * L * cols
+        if name == "mpx_ring_pool_sum":
+            planes, H, W, k = a[2], a[3], a[4], a[5]
+            return 8 * planes * H * W + 8 * planes * (H // k) * (W // k)
+        if name == "mpx_ring_add_rowvec":
+            L, rows, cols = a[2], a[3], a[4]
+            return 16 * L * rows * cols + 8 * L * cols
+        if name == "mpx_im2col":
+            L, B, C, H, W, K, st, pd = a[2:10]
+            OH, OW = (H + 2 * pd - K) // st + 1, (W + 2 * pd - K) // st + 1
+            return 8 * L * B * C * H * W + 8 * L * B * OH * OW * C * K * K
+        if name == "mpx_col2im":
+            L, B, C, H, W, K, st, pd = a[2:10]
+            OH, OW = (H + 2 * pd - K) // st + 1, (W + 2 * pd - K) // st + 1
+            return 8 * L * B * C * H * W + 8 * L * B * OH * OW * C * K * K
     except (IndexError, TypeError):
         return None
     return None

@@ -96,6 +96,10 @@ int mpx_open_xor(uint64_t* out, const uint64_t* x, int L, int64_t n, void* strea
  * mul/matmul (basic.py:36, :66) and decompose (basic.py:211). */
 int mpx_mask_sub(uint64_t* out, const uint64_t* x, const uint64_t* a, int64_t a_ps, int L, int64_t n,
                  int width, void* stream);
+/* Same for a transposed operand stored cols x rows (party stride x_ps):
+ * out[r][c] = sum_l (x_l[c][r] - a_l[r][c]) (Beaver masks of X^T, W^T). */
+int mpx_mask_sub_t(uint64_t* out, const uint64_t* x, int64_t x_ps, const uint64_t* a, int64_t a_ps, int L,
+                   int64_t rows, int64_t cols, int width, void* stream);
 
 /* ---- Beaver multiplication (basic.py:27-42) ----
  * z_l = c_l + d*b_l + e*a_l + [l==p0] d*e. */
@@ -119,6 +123,11 @@ int mpx_trunc_finish(uint64_t* z, const uint64_t* c, const uint64_t* r_hi, int64
 int mpx_trunc_fused(uint64_t* z, const uint64_t* x, const uint64_t* r_lo, int64_t lo_ps,
                     const uint64_t* r_hi, int64_t hi_ps, int L, int64_t n, int width, int f,
                     uint64_t bias, uint64_t unbias, int p0, void* stream);
+/* Up to 16 independent sim-mode truncations in one launch; each job is
+ * z = trunc(x) or, with a base, z = base - trunc(x) (SGD updates). jobs_host
+ * points to a host TruncJobs {TruncJob j[16]; int64_t start[17]; int n, pad}
+ * with TruncJob {z, base, x, r_lo, r_hi, lo_ps, hi_ps, n, bias, unbias, f, pad}. */
+int mpx_trunc_sub_multi(const void* jobs_host, int L, int width, int p0, void* stream);
 
 /* ---- binary Beaver AND on row-packed bits (basic.py:82-95) ----
  * triple for (row r, bit j) = bit (t_bit + r*m + j) of the bintriple stream. */

@@ -188,6 +188,79 @@ extern "C" int mpx_trunc_fused(uint64_t* z, const uint64_t* x, const uint64_t* r
   return launch_status();
 }
 
+// Several independent sim-mode truncations in ONE launch, each optionally
+// subtracted from a base: z = base - trunc(x) (the SGD update W -= trunc(dW)
+// of every layer; derived.py:20-70 per job, material in job order).
+#define TRUNC_JOBS_MAX 16
+struct TruncJob {
+  u64* z;
+  const u64* base;  // may be null: z = trunc(x)
+  const u64* x;
+  const u64* r_lo;
+  const u64* r_hi;  // may be null (f = w - 1)
+  i64 lo_ps, hi_ps, n;
+  u64 bias, unbias;
+  int f, pad;
+};
+struct TruncJobs {
+  TruncJob j[TRUNC_JOBS_MAX];
+  i64 start[TRUNC_JOBS_MAX + 1];  // first block of each job
+  int n, pad;
+};
+
+template <int LMAX>
+__global__ void __launch_bounds__(256) k_trunc_sub_multi(const __grid_constant__ TruncJobs jobs, int L, u64 msk,
+                                                         int p0) {
+  int k = 0;
+  while (k + 1 < jobs.n && (i64)blockIdx.x >= jobs.start[k + 1]) ++k;
+  const TruncJob& J = jobs.j[k];
+  const i64 i = ((i64)blockIdx.x - jobs.start[k]) * blockDim.x + threadIdx.x;
+  if (i >= J.n) return;
+  u64 hv[LMAX];
+  u64 s = 0;
+#pragma unroll
+  for (int l = 0; l < LMAX; ++l) {
+    if (l < L) {
+      hv[l] = J.r_hi ? J.r_hi[l * J.hi_ps + i] : 0ull;
+      u64 v = J.x[l * J.n + i] + J.r_lo[l * J.lo_ps + i] + (hv[l] << J.f);
+      if (l == p0) v += J.bias;
+      s += v;
+    }
+  }
+  const u64 chi = (s & msk) >> J.f;
+#pragma unroll
+  for (int l = 0; l < LMAX; ++l) {
+    if (l < L) {
+      u64 v = 0ull - hv[l];
+      if (l == p0) v += chi - J.unbias;
+      if (J.base) v = J.base[l * J.n + i] - v;
+      J.z[l * J.n + i] = v & msk;
+    }
+  }
+}
+
+extern "C" int mpx_trunc_sub_multi(const void* jobs_host, int L, int width, int p0, void* stream) {
+  CHECK_ARG(jobs_host && L >= 1 && L <= 16 && width >= 2 && width <= 64);
+  TruncJobs J = *(const TruncJobs*)jobs_host;
+  CHECK_ARG(J.n >= 1 && J.n <= TRUNC_JOBS_MAX);
+  i64 b = 0;
+  for (int k = 0; k < J.n; ++k) {
+    CHECK_ARG(J.j[k].z && J.j[k].x && J.j[k].r_lo && J.j[k].n >= 0 && J.j[k].f >= 1 && J.j[k].f < width);
+    J.start[k] = b;
+    b += (J.j[k].n + 255) / 256;
+  }
+  J.start[J.n] = b;
+  if (b == 0) return MPX_OK;
+  CHECK_ARG(b < (1ll << 31));
+  const u64 msk = ring_mask(width);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (L <= 4)
+    k_trunc_sub_multi<4><<<(unsigned)b, 256, 0, s>>>(J, L, msk, p0);
+  else
+    k_trunc_sub_multi<16><<<(unsigned)b, 256, 0, s>>>(J, L, msk, p0);
+  return launch_status();
+}
+
 // ==========================================================================
 // Binary Beaver AND on row-packed bits (basic.py:82-95)
 

@@ -300,6 +300,46 @@ extern "C" int mpx_mask_sub(uint64_t* out, const uint64_t* x, const uint64_t* a,
   return launch_status();
 }
 
+// Beaver mask of a transposed operand without materialising the transpose:
+// out[r][c] = sum_l (x_l[c][r] - a_l[r][c]) mod 2^w, x_l stored cols x rows
+// (party stride x_ps). 32 x 32 tiles through shared memory: x is read along
+// its rows, a and out along theirs.
+__global__ void k_mask_sub_t(u64* __restrict__ out, const u64* __restrict__ x, i64 x_ps, const u64* __restrict__ a,
+                             i64 a_ps, int L, i64 rows, i64 cols, u64 msk) {
+  __shared__ u64 tile[32][33];
+  const i64 r0 = (i64)blockIdx.y * 32, c0 = (i64)blockIdx.x * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+#pragma unroll
+  for (int j = 0; j < 32; j += 8) {
+    const i64 c = c0 + ty + j, r = r0 + tx;
+    u64 s = 0;
+    if (c < cols && r < rows)
+      for (int l = 0; l < L; ++l) s += x[(i64)l * x_ps + c * rows + r];
+    tile[ty + j][tx] = s;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 32; j += 8) {
+    const i64 r = r0 + ty + j, c = c0 + tx;
+    if (r < rows && c < cols) {
+      u64 s = tile[tx][ty + j];
+      for (int l = 0; l < L; ++l) s -= a[(i64)l * a_ps + r * cols + c];
+      out[r * cols + c] = s & msk;
+    }
+  }
+}
+
+extern "C" int mpx_mask_sub_t(uint64_t* out, const uint64_t* x, int64_t x_ps, const uint64_t* a, int64_t a_ps,
+                              int L, int64_t rows, int64_t cols, int width, void* stream) {
+  CHECK_ARG(out && x && a && L >= 1 && rows >= 0 && cols >= 0 && width >= 1 && width <= 64);
+  if (rows == 0 || cols == 0) return MPX_OK;
+  CHECK_ARG((rows + 31) / 32 <= 65535);
+  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  k_mask_sub_t<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(out, x, x_ps, a, a_ps, L, rows, cols,
+                                                                ring_mask(width));
+  return launch_status();
+}
+
 // --------------------------------------------------------------------------
 // Local bit ops on row-packed words.
 

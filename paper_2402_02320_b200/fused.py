@@ -269,7 +269,7 @@ def run_fused(kind: str, session, x: AShare, params, protocol) -> AShare:
     y = session.alloc(x.values.shape)
     xv = x.values.contiguous()
     _launch(lib, _ENTRY[kind], (y.data_ptr(), xv.data_ptr(), x.size, ctypes.addressof(tape), ctypes.addressof(P)),
-            (kind, x.size, session.L, calls))
+            (kind, x.size, session.L, calls, 2))
     return AShare(y, out_w, out_f, session.parties)
 
 
@@ -295,7 +295,7 @@ def relu_fused(session, x: AShare, protocol, want_sign: bool):
     sg = session.alloc(x.values.shape) if want_sign else None
     _launch(lib, "mpx_relu_fused", (y.data_ptr(), sg.data_ptr() if sg is not None else None,
                                     x.values.contiguous().data_ptr(), x.size, ctypes.addressof(tape),
-                                    ctypes.addressof(P)), ("relu", x.size, session.L, calls))
+                                    ctypes.addressof(P)), ("relu", x.size, session.L, calls, 3 if want_sign else 2))
     out = AShare(y, out_w, out_f, session.parties)
     return out, (AShare(sg, x.width, 0, session.parties) if sg is not None else None)
 
@@ -309,5 +309,5 @@ def maxlevel_fused(session, u: AShare, v: AShare, protocol) -> AShare:
     y = session.alloc(u.values.shape)
     _launch(lib, "mpx_maxlevel_fused", (y.data_ptr(), u.values.contiguous().data_ptr(),
                                         v.values.contiguous().data_ptr(), u.size, ctypes.addressof(tape),
-                                        ctypes.addressof(P)), ("maxlevel", u.size, session.L, calls))
+                                        ctypes.addressof(P)), ("maxlevel", u.size, session.L, calls, 3))
     return AShare(y, out_w, out_f, session.parties)

@@ -86,6 +86,55 @@ def mask_sub(out, x, a_ptr, a_ps, L, n, width):
     return out
 
 
+class TruncJob(ctypes.Structure):
+    _fields_ = [("z", ctypes.c_void_p), ("base", ctypes.c_void_p), ("x", ctypes.c_void_p),
+                ("r_lo", ctypes.c_void_p), ("r_hi", ctypes.c_void_p), ("lo_ps", ctypes.c_int64),
+                ("hi_ps", ctypes.c_int64), ("n", ctypes.c_int64), ("bias", ctypes.c_uint64),
+                ("unbias", ctypes.c_uint64), ("f", ctypes.c_int), ("pad", ctypes.c_int)]
+
+
+TRUNC_JOBS_MAX = 16
+
+
+class TruncJobs(ctypes.Structure):
+    _fields_ = [("j", TruncJob * TRUNC_JOBS_MAX), ("start", ctypes.c_int64 * (TRUNC_JOBS_MAX + 1)),
+                ("n", ctypes.c_int), ("pad", ctypes.c_int)]
+
+
+def trunc_sub_multi(jobs, L, width, p0):
+    """jobs: list of dicts z, base (or None), x, r_lo, lo_ps, r_hi (or None), hi_ps, n, f, bias, unbias."""
+    if not jobs or _dry(jobs[0]["z"]):
+        return
+    J = TruncJobs()
+    J.n = len(jobs)
+    for i, jb in enumerate(jobs):
+        t = J.j[i]
+        t.z, t.x = ptr(jb["z"]), ptr(jb["x"])
+        t.base = ptr(jb["base"]) if jb["base"] is not None else None
+        t.r_lo, t.r_hi = jb["r_lo"], jb["r_hi"]
+        t.lo_ps, t.hi_ps, t.n = jb["lo_ps"], jb["hi_ps"], jb["n"]
+        t.bias, t.unbias, t.f = jb["bias"], jb["unbias"], jb["f"]
+    call("mpx_trunc_sub_multi", ctypes.addressof(J), L, width, p0)
+
+
+def mask_sub_t(out, x_ptr, x_ps, a_ptr, a_ps, L, rows, cols, width):
+    if _dry(out):
+        return out
+    call("mpx_mask_sub_t", ptr(out), x_ptr, x_ps, a_ptr, a_ps, L, rows, cols, width)
+    return out
+
+
+def transposed_base(v):
+    """(base tensor, party stride) when ``v`` [L, r, c] is the last-two-axes
+    transpose of a contiguous [L, c, r] tensor, else None."""
+    if v.dim() != 3 or v.is_contiguous():
+        return None
+    L, r, c = v.shape
+    if v.stride() == (c * r, 1, r):
+        return v.stride(0)
+    return None
+
+
 # ---- Beaver arithmetic ----------------------------------------------------
 
 def mul_finish(z, d, e, a, b, c, t_ps, L, n, width, p0):

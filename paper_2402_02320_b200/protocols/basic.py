@@ -64,8 +64,8 @@ def batch_matmul(session, pairs) -> list[AShare]:
         r = y.shape[1]
         A, B, C = session.store.take_matrix_triple(w, m, k, r)
         D, E = session.alloc((m * k,)), session.alloc((k * r,))
-        K.mask_sub(D, x.values, A.data_ptr(), A.stride(0), L, m * k, w)
-        K.mask_sub(E, y.values, B.data_ptr(), B.stride(0), L, k * r, w)
+        _mask(D, x.values, A, L, m, k, w)
+        _mask(E, y.values, B, L, k, r, w)
         trip.append((A, B, C))
         masked += [(D, w), (E, w)]
     opened = session.exchange(arith=masked)
@@ -85,6 +85,20 @@ def batch_matmul(session, pairs) -> list[AShare]:
         session.metrics.count(matmul_count=1, matmul_macs=m * k * r)
         out.append(AShare(Z, w, x.frac + y.frac, session.parties))
     return out
+
+
+def _mask(out, v, T, L, rows, cols, w):
+    """out = open(v - T) (sim) / v - T (party); a transposed view of a
+    contiguous tensor (X^T, W^T in backward) is read in place."""
+    tps = K.transposed_base(v) if not session_dry(v) else None
+    if tps is not None:
+        K.mask_sub_t(out, v.data_ptr(), tps, T.data_ptr(), T.stride(0), L, rows, cols, w)
+    else:
+        K.mask_sub(out, v.contiguous(), T.data_ptr(), T.stride(0), L, rows * cols, w)
+
+
+def session_dry(v) -> bool:
+    return v.is_meta
 
 
 def _use_tc(m, k, r, w=64) -> bool:

@@ -36,7 +36,8 @@ from .sharing import AShare, public_ashare
 
 
 def _transpose(x: AShare) -> AShare:
-    return AShare(x.values.transpose(-1, -2).contiguous(), x.width, x.frac, x.parties)
+    """Transposed VIEW (no copy): batch_matmul masks it with mpx_mask_sub_t."""
+    return AShare(x.values.transpose(-1, -2), x.width, x.frac, x.parties)
 
 
 def _colsum(session, z: AShare) -> AShare:
@@ -232,9 +233,39 @@ class Model:
             for i in range(len(self.layers) - 1, -1, -1):
                 g = self.layers[i].backward(s, g, need_dx=i > 0)
         with s.scope("sgd"):
-            for layer in self.layers:
-                layer.step(s, lr_shift + bshift)
+            _sgd(s, self.layers, lr_shift + bshift)
         return logits
+
+
+def _sgd(s, layers, shift: int) -> None:
+    """W -= trunc(dW_2p, p + shift), b -= trunc(db, shift) for every layer.
+    Sim mode: all truncations in ONE launch (mpx_trunc_sub_multi), same
+    material order, rounds and ledger as the per-layer path (derived.py:20-70)."""
+    jobs = [(layer, nm, g, f) for layer in layers if hasattr(layer, "W")
+            for nm, g, f in (("W", layer.gW, layer.p + shift), ("b", layer.gb, shift))]
+    if not (s.fused and getattr(s, "fuse_ops", True) and jobs and len(jobs) <= K.TRUNC_JOBS_MAX and s.L <= 16
+            and all(g.width == 64 for _, _, g, _ in jobs)):
+        for layer in layers:
+            layer.step(s, shift)
+        return
+    from .session import arith_payload
+    w = 64
+    kj = []
+    for layer, nm, g, f in jobs:
+        n = g.size
+        r_lo, _ = s.store.take_edabits(w, f, n, need_bits=False)
+        hw = w - 1 - f
+        r_hi = s.store.take_edabits(w, hw, n, need_bits=False)[0] if hw > 0 else None
+        base = getattr(layer, nm)
+        z = s.alloc((s.L,) + g.shape)
+        kj.append({"z": z, "base": base.values.contiguous(), "x": g.values.contiguous(), "r_lo": r_lo.ptr,
+                   "lo_ps": r_lo.ps, "r_hi": r_hi.ptr if r_hi is not None else None,
+                   "hi_ps": r_hi.ps if r_hi is not None else 0, "n": n, "f": f,
+                   "bias": 1 << (w - 2), "unbias": 1 << (w - 2 - f)})
+        s.exchange(payload=arith_payload(w, n))
+        s.metrics.count(trunc_count=1)
+        setattr(layer, nm, AShare(z, w, base.frac, s.parties))
+    K.trunc_sub_multi(kj, s.L, w, s.p0)
 
 
 def lenet(session, spec: InitSpec = InitSpec()) -> Model:
