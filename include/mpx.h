@@ -128,6 +128,20 @@ int mpx_trunc_fused(uint64_t* z, const uint64_t* x, const uint64_t* r_lo, int64_
  * points to a host TruncJobs {TruncJob j[16]; int64_t start[17]; int n, pad}
  * with TruncJob {z, base, x, r_lo, r_hi, lo_ps, hi_ps, n, bias, unbias, f, pad}. */
 int mpx_trunc_sub_multi(const void* jobs_host, int L, int width, int p0, void* stream);
+/* Sim-mode truncation of x[l][b*S+s][c] + (brow[l][c] << bshift) (a layer's
+ * product plus its lifted bias row, brow may be null), material in that row
+ * order; nchw = 1 stores z[l][b][c][s] (conv output), 0 stores rows. L <= 4. */
+int mpx_trunc_rows_bias(uint64_t* z, const uint64_t* x, const uint64_t* brow, int bshift, const uint64_t* r_lo,
+                        int64_t lo_ps, const uint64_t* r_hi, int64_t hi_ps, int L, int64_t B, int64_t S,
+                        int64_t C, int nchw, int width, int f, uint64_t bias, uint64_t unbias, int p0,
+                        void* stream);
+/* Sim-mode truncation of an NCHW tensor x[l][b][c][hs][ws], each value
+ * broadcast to its k x k window in conv row order z[l][(b*H+h)*W+w][c]
+ * (average-pool backward feeding a conv backward). L <= 4. */
+int mpx_trunc_expand_rows(uint64_t* z, const uint64_t* x, const uint64_t* r_lo, int64_t lo_ps,
+                          const uint64_t* r_hi, int64_t hi_ps, int L, int64_t B, int64_t C, int64_t Hs,
+                          int64_t Ws, int64_t k, int width, int f, uint64_t bias, uint64_t unbias, int p0,
+                          void* stream);
 
 /* ---- binary Beaver AND on row-packed bits (basic.py:82-95) ----
  * triple for (row r, bit j) = bit (t_bit + r*m + j) of the bintriple stream. */

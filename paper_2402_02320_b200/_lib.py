@@ -35,6 +35,8 @@ _SIGS = {
     "mpx_open_xor": [_P, _P, _I, _L, _P],
     "mpx_mask_sub": [_P, _P, _P, _L, _I, _L, _I, _P],
     "mpx_trunc_sub_multi": [_P, _I, _I, _I, _P],
+    "mpx_trunc_rows_bias": [_P, _P, _P, _I, _P, _L, _P, _L, _I, _L, _L, _L, _I, _I, _I, _U, _U, _I, _P],
+    "mpx_trunc_expand_rows": [_P, _P, _P, _L, _P, _L, _I, _L, _L, _L, _L, _L, _I, _I, _U, _U, _I, _P],
     "mpx_mask_sub_t": [_P, _P, _L, _P, _L, _I, _L, _L, _I, _P],
     "mpx_mul_finish": [_P, _P, _P, _P, _P, _P, _L, _I, _L, _I, _I, _P],
     "mpx_mul_fused": [_P, _P, _P, _P, _P, _P, _L, _I, _L, _I, _I, _P],

@@ -261,6 +261,159 @@ extern "C" int mpx_trunc_sub_multi(const void* jobs_host, int L, int width, int 
   return launch_status();
 }
 
+// Truncation fused with the layer plumbing around it (sim mode). The
+// truncated tensor and its material order are the reference's; only where the
+// result lands changes (derived.py:55-70 per element).
+template <int LMAX>
+__device__ __forceinline__ void trunc_elem(u64 (&out)[LMAX], const u64 (&xv)[LMAX], const u64* r_lo, i64 lo_ps,
+                                           const u64* r_hi, i64 hi_ps, int L, i64 i, u64 msk, int f, u64 bias,
+                                           u64 unbias, int p0) {
+  u64 hv[LMAX];
+  u64 s = 0;
+#pragma unroll
+  for (int l = 0; l < LMAX; ++l) {
+    hv[l] = 0;
+    if (l < L) {
+      hv[l] = r_hi ? r_hi[l * hi_ps + i] : 0ull;
+      u64 v = xv[l] + r_lo[l * lo_ps + i] + (hv[l] << f);
+      if (l == p0) v += bias;
+      s += v;
+    }
+  }
+  const u64 chi = (s & msk) >> f;
+#pragma unroll
+  for (int l = 0; l < LMAX; ++l) {
+    u64 v = 0ull - hv[l];
+    if (l == p0) v += chi - unbias;
+    out[l] = v & msk;
+  }
+}
+
+// Conv output: z_nchw[l][b][c][s] = trunc(x[l][b*S+s][c] + (brow[l][c] << bshift)),
+// 32 x 32 (s, c) tiles transposed through shared memory. nchw = 0 (linear
+// layers): plain row order.
+template <int LMAX>
+__global__ void __launch_bounds__(256) k_trunc_rows_bias_nchw(u64* __restrict__ z, const u64* __restrict__ x,
+                                                              const u64* __restrict__ brow, int bshift,
+                                                              const u64* __restrict__ r_lo, i64 lo_ps,
+                                                              const u64* __restrict__ r_hi, i64 hi_ps, int L,
+                                                              i64 R, int S, int C, u64 msk, int f, u64 bias,
+                                                              u64 unbias, int p0) {
+  __shared__ u64 tile[LMAX][32][33];
+  const i64 b = blockIdx.z;
+  const int c0 = blockIdx.x * 32, s0 = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const i64 n = R * C;
+#pragma unroll
+  for (int j = 0; j < 32; j += 8) {
+    const int sl = ty + j, c = c0 + tx, sg = s0 + sl;
+    if (c < C && sg < S) {
+      const i64 i = (b * S + sg) * C + c;
+      u64 xv[LMAX], o[LMAX];
+#pragma unroll
+      for (int l = 0; l < LMAX; ++l)
+        xv[l] = l < L ? x[l * n + i] + (brow ? brow[l * C + c] << bshift : 0ull) : 0ull;
+      trunc_elem<LMAX>(o, xv, r_lo, lo_ps, r_hi, hi_ps, L, i, msk, f, bias, unbias, p0);
+#pragma unroll
+      for (int l = 0; l < LMAX; ++l) tile[l][sl][tx] = o[l];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 32; j += 8) {
+    const int cl = ty + j, c = c0 + cl, sg = s0 + tx;
+    if (c < C && sg < S)
+#pragma unroll
+      for (int l = 0; l < LMAX; ++l)
+        if (l < L) z[l * n + (b * C + c) * S + sg] = tile[l][tx][cl];
+  }
+}
+
+template <int LMAX>
+__global__ void k_trunc_rows_bias(u64* __restrict__ z, const u64* __restrict__ x, const u64* __restrict__ brow,
+                                  int bshift, const u64* __restrict__ r_lo, i64 lo_ps, const u64* __restrict__ r_hi,
+                                  i64 hi_ps, int L, i64 R, int C, u64 msk, int f, u64 bias, u64 unbias, int p0) {
+  const i64 n = R * C;
+  GRID_STRIDE(i, n) {
+    const int c = (int)(i % C);
+    u64 xv[LMAX], o[LMAX];
+#pragma unroll
+    for (int l = 0; l < LMAX; ++l)
+      xv[l] = l < L ? x[l * n + i] + (brow ? brow[l * C + c] << bshift : 0ull) : 0ull;
+    trunc_elem<LMAX>(o, xv, r_lo, lo_ps, r_hi, hi_ps, L, i, msk, f, bias, unbias, p0);
+#pragma unroll
+    for (int l = 0; l < LMAX; ++l)
+      if (l < L) z[l * n + i] = o[l];
+  }
+}
+
+extern "C" int mpx_trunc_rows_bias(uint64_t* z, const uint64_t* x, const uint64_t* brow, int bshift,
+                                   const uint64_t* r_lo, int64_t lo_ps, const uint64_t* r_hi, int64_t hi_ps, int L,
+                                   int64_t B, int64_t S, int64_t C, int nchw, int width, int f, uint64_t bias,
+                                   uint64_t unbias, int p0, void* stream) {
+  CHECK_ARG(z && x && r_lo && L >= 1 && L <= 4 && B >= 0 && S >= 1 && C >= 1 && width >= 2 && width <= 64 &&
+            f >= 1 && f < width && bshift >= 0 && bshift < 64);
+  const i64 R = B * S;
+  if (R == 0) return MPX_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const u64 msk = ring_mask(width);
+  if (nchw) {
+    CHECK_ARG(B <= 65535 && S < (1 << 30) && C < (1 << 30));
+    dim3 grid((unsigned)((C + 31) / 32), (unsigned)((S + 31) / 32), (unsigned)B);
+    k_trunc_rows_bias_nchw<4><<<grid, dim3(32, 8), 0, s>>>(z, x, brow, bshift, r_lo, lo_ps, r_hi, hi_ps, L, R,
+                                                           (int)S, (int)C, msk, f, bias, unbias, p0);
+  } else {
+    CHECK_ARG(C < (1 << 30));
+    k_trunc_rows_bias<4><<<grid_for(R * C), MPX_THREADS, 0, s>>>(z, x, brow, bshift, r_lo, lo_ps, r_hi, hi_ps,
+                                                                 L, R, (int)C, msk, f, bias, unbias, p0);
+  }
+  return launch_status();
+}
+
+// Average-pool backward: d = trunc(dy) over dy's NCHW order, each value
+// broadcast to its k x k window and stored in conv "rows" order
+// z[l][(b*H + h)*W + w][c] (the layout the conv backward multiplies).
+template <int LMAX>
+__global__ void k_trunc_expand_rows(u64* __restrict__ z, const u64* __restrict__ x, const u64* __restrict__ r_lo,
+                                    i64 lo_ps, const u64* __restrict__ r_hi, i64 hi_ps, int L, i64 B, int C, int Hs,
+                                    int Ws, int k, u64 msk, int f, u64 bias, u64 unbias, int p0) {
+  const i64 n = B * C * Hs * Ws;
+  const i64 H = (i64)Hs * k, W = (i64)Ws * k;
+  GRID_STRIDE(i, n) {
+    const int ws = (int)(i % Ws);
+    const i64 t1 = i / Ws;
+    const int hs = (int)(t1 % Hs);
+    const i64 t2 = t1 / Hs;
+    const int c = (int)(t2 % C);
+    const i64 b = t2 / C;
+    u64 xv[LMAX], o[LMAX];
+#pragma unroll
+    for (int l = 0; l < LMAX; ++l) xv[l] = l < L ? x[l * n + i] : 0ull;
+    trunc_elem<LMAX>(o, xv, r_lo, lo_ps, r_hi, hi_ps, L, i, msk, f, bias, unbias, p0);
+    for (int a = 0; a < k; ++a)
+      for (int bb = 0; bb < k; ++bb) {
+        const i64 row = (b * H + (i64)hs * k + a) * W + (i64)ws * k + bb;
+#pragma unroll
+        for (int l = 0; l < LMAX; ++l)
+          if (l < L) z[(i64)l * n * k * k + row * C + c] = o[l];
+      }
+  }
+}
+
+extern "C" int mpx_trunc_expand_rows(uint64_t* z, const uint64_t* x, const uint64_t* r_lo, int64_t lo_ps,
+                                     const uint64_t* r_hi, int64_t hi_ps, int L, int64_t B, int64_t C, int64_t Hs,
+                                     int64_t Ws, int64_t k, int width, int f, uint64_t bias, uint64_t unbias, int p0,
+                                     void* stream) {
+  CHECK_ARG(z && x && r_lo && L >= 1 && L <= 4 && B >= 0 && C >= 1 && Hs >= 1 && Ws >= 1 && k >= 1 &&
+            C < (1 << 30) && Hs * k < (1 << 30) && Ws * k < (1 << 30) && width >= 2 && width <= 64 && f >= 1 &&
+            f < width);
+  const i64 n = B * C * Hs * Ws;
+  if (n == 0) return MPX_OK;
+  k_trunc_expand_rows<4><<<grid_for(n), MPX_THREADS, 0, (cudaStream_t)stream>>>(
+      z, x, r_lo, lo_ps, r_hi, hi_ps, L, B, (int)C, (int)Hs, (int)Ws, (int)k, ring_mask(width), f, bias, unbias, p0);
+  return launch_status();
+}
+
 // ==========================================================================
 // Binary Beaver AND on row-packed bits (basic.py:82-95)
 

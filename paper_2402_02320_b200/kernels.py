@@ -117,6 +117,22 @@ def trunc_sub_multi(jobs, L, width, p0):
     call("mpx_trunc_sub_multi", ctypes.addressof(J), L, width, p0)
 
 
+def trunc_rows_bias(z, x, brow, bshift, r_lo, lo_ps, r_hi, hi_ps, L, B, S, C, nchw, width, f, bias, unbias, p0):
+    if _dry(z):
+        return z
+    call("mpx_trunc_rows_bias", ptr(z), ptr(x), ptr(brow) if brow is not None else None, bshift, r_lo, lo_ps,
+         r_hi, hi_ps, L, B, S, C, int(nchw), width, f, bias, unbias, p0)
+    return z
+
+
+def trunc_expand_rows(z, x, r_lo, lo_ps, r_hi, hi_ps, L, B, C, Hs, Ws, k, width, f, bias, unbias, p0):
+    if _dry(z):
+        return z
+    call("mpx_trunc_expand_rows", ptr(z), ptr(x), r_lo, lo_ps, r_hi, hi_ps, L, B, C, Hs, Ws, k, width, f, bias,
+         unbias, p0)
+    return z
+
+
 def mask_sub_t(out, x_ptr, x_ps, a_ptr, a_ps, L, rows, cols, width):
     if _dry(out):
         return out

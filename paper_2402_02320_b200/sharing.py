@@ -51,6 +51,14 @@ class AShare:
         if len(self.parties) != values.shape[0]:
             raise ValueError("party axis does not match `parties`")
 
+    @classmethod
+    def strided(cls, values: torch.Tensor, width: int, frac: int, parties) -> "AShare":
+        """Non-contiguous view (e.g. a transpose) kept as is: only for operands
+        that are read once by a stride-aware kernel (batch_matmul masks)."""
+        out = cls.__new__(cls)
+        out.values, out.width, out.frac, out.parties = values, int(width), int(frac), tuple(parties)
+        return out
+
     # -- shape ---------------------------------------------------------------
     @property
     def shape(self):

@@ -37,7 +37,7 @@ from .sharing import AShare, public_ashare
 
 def _transpose(x: AShare) -> AShare:
     """Transposed VIEW (no copy): batch_matmul masks it with mpx_mask_sub_t."""
-    return AShare(x.values.transpose(-1, -2), x.width, x.frac, x.parties)
+    return AShare.strided(x.values.transpose(-1, -2), x.width, x.frac, x.parties)
 
 
 def _colsum(session, z: AShare) -> AShare:
@@ -46,6 +46,33 @@ def _colsum(session, z: AShare) -> AShare:
     out = session.alloc((session.L, c))
     K.ring_colsum(out, z.values.contiguous(), session.L, r, c, z.width)
     return AShare(out, z.width, z.frac, session.parties)
+
+
+def _fused_layer(s) -> bool:
+    """Sim mode with the layer-plumbing kernels (all parties local, L <= 4)."""
+    return s.fused and getattr(s, "fuse_ops", True) and s.L <= 4
+
+
+def _trunc_takes(s, n: int, f: int, w: int):
+    """Material + ledger of one signed truncation, in _truncate_core's order
+    (derived.py:20-70): edaBit(w, f) arithmetic, edaBit(w, w-1-f), one round."""
+    from .session import arith_payload
+    r_lo, _ = s.store.take_edabits(w, f, n, need_bits=False)
+    hw = w - 1 - f
+    r_hi = s.store.take_edabits(w, hw, n, need_bits=False)[0] if hw > 0 else None
+    s.exchange(payload=arith_payload(w, n))
+    s.metrics.count(trunc_count=1)
+    return (r_lo.ptr, r_lo.ps), ((r_hi.ptr, r_hi.ps) if r_hi is not None else (None, 0))
+
+
+def _trunc_bias_out(s, z: AShare, b: AShare, p: int, B: int, S: int, nchw: bool, out_shape) -> AShare:
+    """trunc(z + lift(b), p) in one kernel; nchw stores the conv output layout."""
+    w = z.width
+    out = s.alloc((s.L,) + tuple(out_shape))
+    (lo, lo_ps), (hi, hi_ps) = _trunc_takes(s, z.size, p, w)
+    K.trunc_rows_bias(out, z.values, b.values.contiguous(), p, lo, lo_ps, hi, hi_ps, s.L, B, S, z.shape[-1], nchw,
+                      w, p, 1 << (w - 2), 1 << (w - 2 - p), s.p0)
+    return AShare(out, w, z.frac - p, s.parties)
 
 
 def _add_bias(session, z: AShare, b: AShare, p: int) -> AShare:
@@ -94,8 +121,10 @@ class Conv2d(Layer):
         self.cols = AShare(cv, x.width, x.frac, s.parties)
         self.in_shape = (B, C, H, W)
         z = batch_matmul(s, [(self.cols, self.W)])[0]
-        z = truncate(s, _add_bias(s, z, self.b, self.p), self.p)
         self.out_hw = (OH, OW)
+        if _fused_layer(s):
+            return _trunc_bias_out(s, z, self.b, self.p, B, OH * OW, True, (B, self.cout, OH, OW))
+        z = truncate(s, _add_bias(s, z, self.b, self.p), self.p)
         v = z.values.view(s.L, B, OH, OW, self.cout).permute(0, 1, 4, 2, 3).contiguous()
         return AShare(v, z.width, z.frac, s.parties)
 
@@ -138,9 +167,20 @@ class AvgPool2d(Layer):
         self.in_shape = (B, C, H, W)
         return truncate(s, AShare(out, x.width, x.frac, s.parties), self.shift, out_frac=x.frac)
 
+    rows_out = False   # set by Model when a Conv2d precedes: emit the conv's row layout
+
     def backward(self, s, dy: AShare, need_dx: bool = True) -> AShare:
         B, C, H, W = self.in_shape
         k = self.k
+        if self.rows_out and _fused_layer(s):
+            z = s.alloc((s.L, B * H * W, C))
+            (lo, lo_ps), (hi, hi_ps) = _trunc_takes(s, dy.size, self.shift, dy.width)
+            w = dy.width
+            K.trunc_expand_rows(z, dy.values.contiguous(), lo, lo_ps, hi, hi_ps, s.L, B, C, H // k, W // k, k, w,
+                                self.shift, 1 << (w - 2), 1 << (w - 2 - self.shift), s.p0)
+            # logical NCHW view of the row-layout buffer: the conv backward's
+            # permute back to rows is then free
+            return AShare.strided(z.view(s.L, B, H, W, C).permute(0, 1, 4, 2, 3), w, dy.frac, s.parties)
         d = truncate(s, dy, self.shift, out_frac=dy.frac)
         v = d.values.view(s.L, B, C, H // k, 1, W // k, 1).expand(s.L, B, C, H // k, k, W // k, k)
         return AShare(v.reshape(s.L, B, C, H, W).contiguous(), d.width, d.frac, s.parties)
@@ -185,6 +225,8 @@ class Linear(Layer):
     def forward(self, s, x: AShare) -> AShare:
         self.x = x
         z = batch_matmul(s, [(x, self.W)])[0]
+        if _fused_layer(s):
+            return _trunc_bias_out(s, z, self.b, self.p, z.shape[0], 1, False, z.shape)
         return truncate(s, _add_bias(s, z, self.b, self.p), self.p)
 
     def backward(self, s, dy: AShare, need_dx: bool = True) -> AShare | None:
@@ -211,6 +253,9 @@ class Model:
 
     def __init__(self, layers):
         self.layers = list(layers)
+        for prev, layer in zip(self.layers, self.layers[1:]):
+            if isinstance(layer, AvgPool2d) and isinstance(prev, Conv2d):
+                layer.rows_out = True
 
     def forward(self, s, x: AShare) -> AShare:
         for layer in self.layers:
@@ -257,14 +302,16 @@ def _sgd(s, layers, shift: int) -> None:
         hw = w - 1 - f
         r_hi = s.store.take_edabits(w, hw, n, need_bits=False)[0] if hw > 0 else None
         base = getattr(layer, nm)
-        z = s.alloc((s.L,) + g.shape)
+        # in place: each element is read and written by the same thread
+        z = base.values if base.values.is_contiguous() else s.alloc((s.L,) + g.shape)
         kj.append({"z": z, "base": base.values.contiguous(), "x": g.values.contiguous(), "r_lo": r_lo.ptr,
                    "lo_ps": r_lo.ps, "r_hi": r_hi.ptr if r_hi is not None else None,
                    "hi_ps": r_hi.ps if r_hi is not None else 0, "n": n, "f": f,
                    "bias": 1 << (w - 2), "unbias": 1 << (w - 2 - f)})
         s.exchange(payload=arith_payload(w, n))
         s.metrics.count(trunc_count=1)
-        setattr(layer, nm, AShare(z, w, base.frac, s.parties))
+        if z is not base.values:
+            setattr(layer, nm, AShare(z, w, base.frac, s.parties))
     K.trunc_sub_multi(kj, s.L, w, s.p0)
 
 
