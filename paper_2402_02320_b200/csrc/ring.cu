@@ -591,7 +591,7 @@ __global__ void k_im2col(u64* __restrict__ out, const u64* __restrict__ x, IT B,
   }
 }
 
-template <typename IT>
+template <typename IT, bool S1>
 __global__ void k_col2im(u64* __restrict__ dx, const u64* __restrict__ colsb, IT B, IT C, IT H, IT W, IT K,
                          IT S, IT P, IT OH, IT OW, IT total, u64 msk) {
   const IT cols = C * K * K;
@@ -607,19 +607,62 @@ __global__ void k_col2im(u64* __restrict__ dx, const u64* __restrict__ colsb, IT
     u64 acc = 0;
     for (IT kh = 0; kh < K; ++kh) {
       const long long hh = (long long)(h + P) - (long long)kh;
-      if (hh < 0 || hh % S) continue;
-      const IT oh = (IT)(hh / S);
+      if (hh < 0 || (!S1 && hh % S)) continue;
+      const IT oh = S1 ? (IT)hh : (IT)(hh / S);
       if (oh >= OH) continue;
       for (IT kw = 0; kw < K; ++kw) {
         const long long ww = (long long)(w + P) - (long long)kw;
-        if (ww < 0 || ww % S) continue;
-        const IT ow = (IT)(ww / S);
+        if (ww < 0 || (!S1 && ww % S)) continue;
+        const IT ow = S1 ? (IT)ww : (IT)(ww / S);
         if (ow >= OW) continue;
         const i64 row = ((i64)b * OH + oh) * OW + ow;
         acc += colsb[((i64)l * rows + row) * cols + ((i64)c * K + kh) * K + kw];
       }
     }
     dx[t] = acc & msk;
+  }
+}
+
+// Row-per-warp im2col: the (c, kh, kw) -> input-offset table of a column is
+// built once per block in shared memory, each warp decodes its output row
+// (b, oh, ow) once and its lanes copy the row's columns with coalesced
+// stores; no per-element integer division.
+__global__ void __launch_bounds__(256) k_im2col_tab(u64* __restrict__ out, const u64* __restrict__ x, int L,
+                                                    int B, int C, int H, int W, int K, int S, int P, int OH, int OW) {
+  extern __shared__ int tab[];  // [cols] input offset, [cols] kh << 16 | kw
+  const int cols = C * K * K;
+  for (int col = threadIdx.x; col < cols; col += blockDim.x) {
+    const int c = col / (K * K), r = col - c * K * K, kh = r / K, kw = r - kh * K;
+    tab[col] = (c * H + kh) * W + kw;
+    tab[cols + col] = (kh << 16) | kw;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const i64 rows = (i64)B * OH * OW;
+  const i64 nrow = (i64)L * rows;
+  const i64 warp = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 lr = warp; lr < nrow; lr += nwarps) {
+    const i64 l = lr / rows, row = lr - l * rows;
+    const int ow = (int)(row % OW);
+    const i64 t = row / OW;
+    const int oh = (int)(t % OH);
+    const i64 b = t / OH;
+    const int h0 = oh * S - P, w0 = ow * S - P;
+    const bool inside = h0 >= 0 && w0 >= 0 && h0 + K <= H && w0 + K <= W;
+    const u64* xb = x + (l * B + b) * (i64)C * H * W;
+    const i64 base = (i64)h0 * W + w0;
+    u64* o = out + lr * cols;
+    for (int col = lane; col < cols; col += 32) {
+      u64 v;
+      if (inside) {
+        v = xb[base + tab[col]];
+      } else {
+        const int kk = tab[cols + col], h = h0 + (kk >> 16), w = w0 + (kk & 0xFFFF);
+        v = (h >= 0 && h < H && w >= 0 && w < W) ? xb[base + tab[col]] : 0ull;
+      }
+      o[col] = v;
+    }
   }
 }
 
@@ -630,6 +673,15 @@ extern "C" int mpx_im2col(uint64_t* out, const uint64_t* x, int L, int64_t B, in
   CHECK_ARG(OH >= 1 && OW >= 1);
   const i64 total = (i64)L * B * OH * OW * C * K * K;
   if (total == 0) return MPX_OK;
+  const i64 cols = (i64)C * K * K;
+  // narrow rows (< 64 columns) leave most lanes idle: element-per-thread path
+  if (cols >= 64 && cols <= 8192 && (i64)C * H * W < (1ll << 31)) {
+    const i64 nrow = (i64)L * B * OH * OW;
+    const i64 blocks = min((nrow + 7) / 8, (i64)148 * 16);
+    k_im2col_tab<<<(unsigned)blocks, 256, (size_t)cols * 8, (cudaStream_t)stream>>>(out, x, L, (int)B, C, H, W, K,
+                                                                                   stride, pad, OH, OW);
+    return launch_status();
+  }
   if (total < (1ll << 31))
     k_im2col<uint32_t><<<grid_for(total), MPX_THREADS, 0, (cudaStream_t)stream>>>(
         out, x, (uint32_t)B, C, H, W, K, stride, pad, OH, OW, (uint32_t)total);
@@ -648,10 +700,14 @@ extern "C" int mpx_col2im(uint64_t* dx, const uint64_t* cols, int L, int64_t B, 
   const i64 total = (i64)L * B * C * H * W;
   if (total == 0) return MPX_OK;
   if (total < (1ll << 31) && (i64)L * B * OH * OW * C * K * K < (1ll << 32))
-    k_col2im<uint32_t><<<grid_for(total), MPX_THREADS, 0, (cudaStream_t)stream>>>(
-        dx, cols, (uint32_t)B, C, H, W, K, stride, pad, OH, OW, (uint32_t)total, ring_mask(width));
+    if (stride == 1)
+      k_col2im<uint32_t, true><<<grid_for(total), MPX_THREADS, 0, (cudaStream_t)stream>>>(
+          dx, cols, (uint32_t)B, C, H, W, K, stride, pad, OH, OW, (uint32_t)total, ring_mask(width));
+    else
+      k_col2im<uint32_t, false><<<grid_for(total), MPX_THREADS, 0, (cudaStream_t)stream>>>(
+          dx, cols, (uint32_t)B, C, H, W, K, stride, pad, OH, OW, (uint32_t)total, ring_mask(width));
   else
-    k_col2im<uint64_t><<<grid_for(total), MPX_THREADS, 0, (cudaStream_t)stream>>>(
+    k_col2im<uint64_t, false><<<grid_for(total), MPX_THREADS, 0, (cudaStream_t)stream>>>(
         dx, cols, (uint64_t)B, C, H, W, K, stride, pad, OH, OW, (uint64_t)total, ring_mask(width));
   return launch_status();
 }
