@@ -182,43 +182,57 @@ __device__ __forceinline__ Sh<L> d_trunc(const Sh<L>& x, const MatRef& lo, const
 
 // Kogge-Stone carries over m-bit words (basic.py:98-136), consuming one tape
 // entry per level; returns the sum bits P0 ^ (G << 1).
+// One Kogge-Stone level (basic.py:98-129): bintriple fields for this level's
+// G (and P, unless last) AND gates, opened across the L local parties.
+template <int L>
+__device__ __forceinline__ void d_carry_level(u64 (&G)[L], u64 (&P)[L], int m, int s, const MatRef& t, i64 e,
+                                              int p0) {
+  const bool last = 2 * s >= m;
+  const int W = m - s;
+  const int RW = last ? W : 2 * W;
+  const u64 hi = low_bits(m) & ~low_bits(s);
+  const i64 bit = t.off + e * (i64)RW;
+  u64 ag[L], bg[L], ap[L], bp[L];
+  u64 dg = 0, eg = 0, dp = 0, ep = 0;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    ag[l] = load_bits(t.p0 + l * t.ps0, bit, W) << s;
+    bg[l] = load_bits(t.p1 + l * t.ps1, bit, W) << s;
+    const u64 left = P[l] & hi;
+    dg ^= left ^ ag[l];
+    eg ^= ((G[l] << s) & hi) ^ bg[l];
+    if (!last) {
+      ap[l] = load_bits(t.p0 + l * t.ps0, bit + W, W) << s;
+      bp[l] = load_bits(t.p1 + l * t.ps1, bit + W, W) << s;
+      dp ^= left ^ ap[l];
+      ep ^= ((P[l] << s) & hi) ^ bp[l];
+    }
+  }
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    u64 zg = (load_bits(t.p2 + l * t.ps2, bit, W) << s) ^ (dg & bg[l]) ^ (eg & ag[l]);
+    if (l == p0) zg ^= dg & eg;
+    G[l] ^= zg;
+    if (!last) {
+      u64 zp = (load_bits(t.p2 + l * t.ps2, bit + W, W) << s) ^ (dp & bp[l]) ^ (ep & ap[l]);
+      if (l == p0) zp ^= dp & ep;
+      P[l] = (P[l] & low_bits(s)) | zp;
+    }
+  }
+}
+
+// Kogge-Stone carries over m-bit words (basic.py:98-136), consuming one tape
+// entry per level; returns the sum bits P0 ^ (G << 1). m = 64 (the common
+// ring) runs a fully unrolled level sequence so independent loads of the
+// next level can be scheduled early.
 template <int L>
 __device__ __forceinline__ void d_carry_sum(u64 (&G)[L], u64 (&P)[L], const u64 (&P0)[L], int m, const Tape& tape,
                                             int& ti, i64 e, int p0, Sh<L>& out) {
-  for (int s = 1; s < m; s *= 2) {
-    const MatRef& t = next_take<L>(tape, ti, e);
-    const bool last = 2 * s >= m;
-    const int W = m - s;
-    const int RW = last ? W : 2 * W;
-    const u64 hi = low_bits(m) & ~low_bits(s);
-    const i64 bit = t.off + e * (i64)RW;
-    u64 ag[L], bg[L], ap[L], bp[L];
-    u64 dg = 0, eg = 0, dp = 0, ep = 0;
+  if (m == 64) {
 #pragma unroll
-    for (int l = 0; l < L; ++l) {
-      ag[l] = load_bits(t.p0 + l * t.ps0, bit, W) << s;
-      bg[l] = load_bits(t.p1 + l * t.ps1, bit, W) << s;
-      const u64 left = P[l] & hi;
-      dg ^= left ^ ag[l];
-      eg ^= ((G[l] << s) & hi) ^ bg[l];
-      if (!last) {
-        ap[l] = load_bits(t.p0 + l * t.ps0, bit + W, W) << s;
-        bp[l] = load_bits(t.p1 + l * t.ps1, bit + W, W) << s;
-        dp ^= left ^ ap[l];
-        ep ^= ((P[l] << s) & hi) ^ bp[l];
-      }
-    }
-#pragma unroll
-    for (int l = 0; l < L; ++l) {
-      u64 zg = (load_bits(t.p2 + l * t.ps2, bit, W) << s) ^ (dg & bg[l]) ^ (eg & ag[l]);
-      if (l == p0) zg ^= dg & eg;
-      G[l] ^= zg;
-      if (!last) {
-        u64 zp = (load_bits(t.p2 + l * t.ps2, bit + W, W) << s) ^ (dp & bp[l]) ^ (ep & ap[l]);
-        if (l == p0) zp ^= dp & ep;
-        P[l] = (P[l] & low_bits(s)) | zp;
-      }
-    }
+    for (int s = 1; s < 64; s *= 2) d_carry_level<L>(G, P, 64, s, next_take<L>(tape, ti, e), e, p0);
+  } else {
+    for (int s = 1; s < m; s *= 2) d_carry_level<L>(G, P, m, s, next_take<L>(tape, ti, e), e, p0);
   }
 #pragma unroll
   for (int l = 0; l < L; ++l) out.v[l] = (P0[l] ^ (G[l] << 1)) & low_bits(m);
