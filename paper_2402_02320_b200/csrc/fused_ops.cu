@@ -263,33 +263,41 @@ __device__ __forceinline__ Sh<L> d_decompose(const Sh<L>& x, int w, const Tape& 
   return out;
 }
 
-// leftmost one (derived.py:131-149)
+// one leftmost-one level: suffix OR via a ^ b ^ ab
+template <int L>
+__device__ __forceinline__ void d_lmo_level(u64 (&Y)[L], int m, int s, const MatRef& t, i64 e, int p0) {
+  const int W = m - s;
+  const u64 mw = low_bits(W);
+  const i64 bit = t.off + e * (i64)W;
+  u64 a[L], b[L];
+  u64 d = 0, f = 0;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    a[l] = load_bits(t.p0 + l * t.ps0, bit, W);
+    b[l] = load_bits(t.p1 + l * t.ps1, bit, W);
+    d ^= (Y[l] & mw) ^ a[l];
+    f ^= ((Y[l] >> s) & mw) ^ b[l];
+  }
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    u64 z = load_bits(t.p2 + l * t.ps2, bit, W) ^ (d & b[l]) ^ (f & a[l]);
+    if (l == p0) z ^= d & f;
+    const u64 lo = Y[l] & mw, hi = (Y[l] >> s) & mw;
+    Y[l] = (Y[l] & ~mw) | ((lo ^ hi ^ z) & mw);
+  }
+}
+
+// leftmost one (derived.py:131-149); m = 63 (the 64-bit ring) unrolled
 template <int L>
 __device__ __forceinline__ Sh<L> d_lmo(const Sh<L>& bits, int m, const Tape& tape, int& ti, i64 e, int p0) {
   u64 Y[L];
 #pragma unroll
   for (int l = 0; l < L; ++l) Y[l] = bits.v[l];
-  for (int s = 1; s < m; s *= 2) {
-    const MatRef& t = next_take<L>(tape, ti, e);
-    const int W = m - s;
-    const u64 mw = low_bits(W);
-    const i64 bit = t.off + e * (i64)W;
-    u64 a[L], b[L];
-    u64 d = 0, f = 0;
+  if (m == 63) {
 #pragma unroll
-    for (int l = 0; l < L; ++l) {
-      a[l] = load_bits(t.p0 + l * t.ps0, bit, W);
-      b[l] = load_bits(t.p1 + l * t.ps1, bit, W);
-      d ^= (Y[l] & mw) ^ a[l];
-      f ^= ((Y[l] >> s) & mw) ^ b[l];
-    }
-#pragma unroll
-    for (int l = 0; l < L; ++l) {
-      u64 z = load_bits(t.p2 + l * t.ps2, bit, W) ^ (d & b[l]) ^ (f & a[l]);
-      if (l == p0) z ^= d & f;
-      const u64 lo = Y[l] & mw, hi = (Y[l] >> s) & mw;
-      Y[l] = (Y[l] & ~mw) | ((lo ^ hi ^ z) & mw);
-    }
+    for (int s = 1; s < 63; s *= 2) d_lmo_level<L>(Y, 63, s, next_take<L>(tape, ti, e), e, p0);
+  } else {
+    for (int s = 1; s < m; s *= 2) d_lmo_level<L>(Y, m, s, next_take<L>(tape, ti, e), e, p0);
   }
   Sh<L> o;
 #pragma unroll
