@@ -412,13 +412,17 @@ def sweep_entry(torch, G, make_session, parties, n_parties, dev, name, steps=2, 
         e1.record()
         torch.cuda.synchronize()
         if _lib.profiling() is not None:
-            for nm, _a, p0, p1 in _lib.profile_end():
+            prof = _lib.profile_end()
+            for nm, _a, p0, p1 in prof:
                 prof_ms[nm] = prof_ms.get(nm, 0.0) + p0.elapsed_time(p1)
+            per = _profile_kernels(prof)
         if step >= warmup:
             times.append(e0.elapsed_time(e1))
     del store
     ms = float(np.mean(times))
     out = {"ms_per_op": ms, "steps": steps}
+    if name != "matmul":
+        out["roofline"] = roofline_for(per)
     if name == "matmul":
         macs = len(parties) * D * (2 * D) * D          # [D|A_l] @ [B_l';E] per local party
         tc_ms = prof_ms.get("mpx_gemm_limbs", 0.0)

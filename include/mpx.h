@@ -275,6 +275,9 @@ int mpx_exp_fused(uint64_t* y, const uint64_t* x, int64_t n, const void* tape_ho
                   const void* params_host, void* stream);
 int mpx_log_fused(uint64_t* y, const uint64_t* x, int64_t n, const void* tape_host,
                   const void* params_host, void* stream);
+/* attention_exp (nonlinear.py:315-356): 32-bit ring input, 64-bit ring output. */
+int mpx_attexp_fused(uint64_t* y, const uint64_t* x, int64_t n, const void* tape_host,
+                     const void* params_host, void* stream);
 /* ReLU (nn.py:92-97) in one kernel: y = bit2a(gt(x, 0)) * x; when s_out is
  * non-null the converted sign is stored too (training backward). */
 int mpx_relu_fused(uint64_t* y, uint64_t* s_out, const uint64_t* x, int64_t n, const void* tape_host,

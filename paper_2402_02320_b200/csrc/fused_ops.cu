@@ -223,17 +223,15 @@ __device__ __forceinline__ void d_carry_level(u64 (&G)[L], u64 (&P)[L], int m, i
 
 // Kogge-Stone carries over m-bit words (basic.py:98-136), consuming one tape
 // entry per level; returns the sum bits P0 ^ (G << 1). m = 64 (the common
-// ring) runs a fully unrolled level sequence so independent loads of the
+// ring) runs as a fully unrolled level sequence so independent loads of the
 // next level can be scheduled early.
 template <int L>
 __device__ __forceinline__ void d_carry_sum(u64 (&G)[L], u64 (&P)[L], const u64 (&P0)[L], int m, const Tape& tape,
                                             int& ti, i64 e, int p0, Sh<L>& out) {
-  if (m == 64) {
+  // levels s = 1, 2, 4, ... < m, unrolled (m <= 64; the guard is uniform)
 #pragma unroll
-    for (int s = 1; s < 64; s *= 2) d_carry_level<L>(G, P, 64, s, next_take<L>(tape, ti, e), e, p0);
-  } else {
-    for (int s = 1; s < m; s *= 2) d_carry_level<L>(G, P, m, s, next_take<L>(tape, ti, e), e, p0);
-  }
+  for (int s = 1; s < 64; s *= 2)
+    if (s < m) d_carry_level<L>(G, P, m, s, next_take<L>(tape, ti, e), e, p0);
 #pragma unroll
   for (int l = 0; l < L; ++l) out.v[l] = (P0[l] ^ (G[l] << 1)) & low_bits(m);
 }
@@ -287,18 +285,15 @@ __device__ __forceinline__ void d_lmo_level(u64 (&Y)[L], int m, int s, const Mat
   }
 }
 
-// leftmost one (derived.py:131-149); m = 63 (the 64-bit ring) unrolled
+// leftmost one (derived.py:131-149); levels unrolled like the carries
 template <int L>
 __device__ __forceinline__ Sh<L> d_lmo(const Sh<L>& bits, int m, const Tape& tape, int& ti, i64 e, int p0) {
   u64 Y[L];
 #pragma unroll
   for (int l = 0; l < L; ++l) Y[l] = bits.v[l];
-  if (m == 63) {
 #pragma unroll
-    for (int s = 1; s < 63; s *= 2) d_lmo_level<L>(Y, 63, s, next_take<L>(tape, ti, e), e, p0);
-  } else {
-    for (int s = 1; s < m; s *= 2) d_lmo_level<L>(Y, m, s, next_take<L>(tape, ti, e), e, p0);
-  }
+  for (int s = 1; s < 64; s *= 2)
+    if (s < m) d_lmo_level<L>(Y, m, s, next_take<L>(tape, ti, e), e, p0);
   Sh<L> o;
 #pragma unroll
   for (int l = 0; l < L; ++l) o.v[l] = Y[l] ^ (Y[l] >> 1);
@@ -578,6 +573,67 @@ __global__ void __launch_bounds__(128) k_exp_fused(u64* __restrict__ y, const u6
 }
 
 // ---------------------------------------------------------------------------
+// Attention exponential 2^x (App. E; nonlinear.py:315-356): narrow w_in = 32
+// input decomposed in its own ring, bits converted into the 64-bit ring, the
+// fraction evaluated by the square-completed polynomial (nonlinear.py:59-86).
+// P.coef_p[0] = enc(p + delta, 32, p), coef_p[1..3] = enc(t3 | t2 | lead*t1,
+// 64, p), coef0_2p = enc(lead*t0, 64, 2p), P.bias = lead_shift, P.c = c.
+
+template <int L>
+__global__ void __launch_bounds__(128) k_attexp_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
+                                                      const __grid_constant__ Tape tape, FusedParams P) {
+  const int win = P.w, p = P.p, p0 = P.p0, c = P.c;
+  const u64 msk_in = ring_mask(win), msk = ring_mask(64);
+  GRID_STRIDE(e, n) {
+    int ti = 0;
+    const Sh<L> x = load_sh<L>(xin, n, e);
+    const Sh<L> xb = sh_scale<L>(x, 1ull, P.coef_p[0], p0, msk_in);
+    const Sh<L> bits = d_decompose<L>(xb, win, tape, ti, e, p0);
+    const int k = p + c + 1;
+    Sh<L> seg;
+#pragma unroll
+    for (int l = 0; l < L; ++l)
+      seg.v[l] = (bits.v[l] & low_bits(p + c)) | (((bits.v[l] >> (win - 1)) & 1ull) << (p + c));
+    const MatRef& tc = next_take<L>(tape, ti, e);
+    const u64 cw = d_bit2a_open<L>(seg, k, tc, e);
+    Sh<L> t;
+#pragma unroll
+    for (int l = 0; l < L; ++l) t.v[l] = 0;
+    d_bit2a_row<L>(cw, p, k, tc, e, p0, msk, [&](int l, int j, u64 z) { t.v[l] += z << j; });
+    // 2^int as a product of (2^(2^i) b_i - b_i + 1) (nonlinear.py:125-131)
+    Sh<L> pw = sh_scale<L>(d_bit2a_get<L>(cw, p, k, tc, e, p0, msk), 1ull, 1ull, p0, msk);
+    for (int i = 1; i < c; ++i) {
+      const Sh<L> bi = d_bit2a_get<L>(cw, p + i, k, tc, e, p0, msk);
+      const u64 kf = (1ull << (1 << i)) - 1ull;
+      pw = d_mul<L>(pw, sh_scale<L>(bi, kf, 1ull, p0, msk), next_take<L>(tape, ti, e), e, p0, msk);
+    }
+    const Sh<L> sgn = d_bit2a_get<L>(cw, p + c, k, tc, e, p0, msk);
+    // evaluate_square_completed (derived.py:111-128)
+    const Sh<L> u = sh_scale<L>(t, 1ull, P.coef_p[1], p0, msk);
+    const Sh<L> u2 = d_mul_trunc<L>(u, u, tape, ti, e, p, 64, p0, msk);
+    const Sh<L> v = sh_scale<L>(u2, 1ull, P.coef_p[2], p0, msk);
+    const Sh<L> sq = d_mul<L>(v, v, next_take<L>(tape, ti, e), e, p0, msk);
+    Sh<L> lead = sq;  // truncate(sq, 0) is a copy (derived.py:55-57)
+    if (P.bias > 0) {
+      const MatRef& lo = next_take<L>(tape, ti, e);
+      const MatRef* hi = (64 - 1 - P.bias > 0) ? &next_take<L>(tape, ti, e) : nullptr;
+      lead = d_trunc<L>(sq, lo, hi, e, P.bias, true, 64, p0, msk);
+    }
+    Sh<L> acc = sh_lin<L>(lead, 1ull, t, P.coef_p[3], P.coef0_2p, p0, msk);
+    Sh<L> ev;
+    {
+      const MatRef& lo = next_take<L>(tape, ti, e);
+      const MatRef& hi = next_take<L>(tape, ti, e);
+      ev = d_trunc<L>(acc, lo, &hi, e, p, true, 64, p0, msk);
+    }
+    const Sh<L> yv = d_mul<L>(pw, ev, next_take<L>(tape, ti, e), e, p0, msk);
+    const Sh<L> s1 = sh_scale<L>(sgn, 0ull - 1ull, 1ull, p0, msk);
+    const Sh<L> out = d_mul_trunc<L>(s1, yv, tape, ti, e, p, 64, p0, msk);
+    store_sh<L>(y, n, e, out);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Logarithm, paper Alg. 3 without the big-input pre-shift (nonlinear.py:216-267)
 
 template <int L>
@@ -767,6 +823,7 @@ DEFINE_LAUNCH2(mpx_relu_fused, k_relu_fused, uint64_t*, const uint64_t*)
 DEFINE_LAUNCH2(mpx_maxlevel_fused, k_maxlevel_fused, const uint64_t*, const uint64_t*)
 DEFINE_LAUNCH(mpx_exp_fused, k_exp_fused)
 DEFINE_LAUNCH(mpx_log_fused, k_log_fused)
+DEFINE_LAUNCH(mpx_attexp_fused, k_attexp_fused)
 
 extern "C" int mpx_fused_abi_sizes(int64_t* matref, int64_t* tape, int64_t* params, int64_t* tape_max) {
   *matref = sizeof(MatRef);

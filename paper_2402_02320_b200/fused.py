@@ -134,7 +134,8 @@ def _merge_metrics(dst, src) -> None:
 _SCHEDULES: dict = {}
 
 
-_ENTRY = {"reciprocal": "mpx_reciprocal_fused", "exp": "mpx_exp_fused", "log": "mpx_log_fused"}
+_ENTRY = {"reciprocal": "mpx_reciprocal_fused", "exp": "mpx_exp_fused", "log": "mpx_log_fused",
+          "attexp": "mpx_attexp_fused"}
 _SIG_SET = False
 
 
@@ -182,6 +183,15 @@ def fusable(session, x: AShare) -> bool:
             and x.width == 64 and 1 <= session.L <= 4 and 2 * x.frac <= 62 and x.size > 0)
 
 
+def fusable_attexp(session, x: AShare) -> bool:
+    """attention_exp kernel: w32 input -> w64 output; the converted segment
+    (p + clog2(p) + 1 bits) fits the narrow word and 2p <= 62."""
+    p = x.frac
+    return (getattr(session, "fused", False) and getattr(session, "fuse_ops", True)
+            and x.width == 32 and 1 <= session.L <= 4 and x.size > 0 and 1 <= p <= 31
+            and p + max(1, (p - 1).bit_length()) + 1 <= 32)
+
+
 def fusable_cmp(session, x: AShare) -> bool:
     """ReLU / max-level kernels: any ring width >= 8."""
     return (getattr(session, "fused", False) and getattr(session, "fuse_ops", True)
@@ -200,6 +210,17 @@ def params_for(kind: str, session, x: AShare, params) -> FusedParams:
         P.log2e_p = encode_scalar(math.log2(math.e), w, p)
         P.bias_2p = encode_scalar(float(P.bias), w, 2 * p)
         coeffs = params.exp_coeffs
+    elif kind == "attexp":
+        sq = params.exp_square
+        delta = math.log2(params.exp_coeffs[4]) + sq.lead_shift
+        P.c = max(1, (p - 1).bit_length())
+        P.bias = sq.lead_shift
+        P.coef_p[0] = encode_scalar(float(p) + delta, w, p)
+        P.coef_p[1] = encode_scalar(sq.t3, 64, p)
+        P.coef_p[2] = encode_scalar(sq.t2, 64, p)
+        P.coef_p[3] = encode_scalar(sq.lead * sq.t1, 64, p)
+        P.coef0_2p = encode_scalar(sq.lead * sq.t0, 64, 2 * p)
+        return P
     elif kind == "log":
         P.m1_p = encode_scalar(-1.0, w, p)
         P.ln2_p = encode_scalar(math.log(2.0), w, p)

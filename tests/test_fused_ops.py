@@ -82,8 +82,30 @@ def _maxcut_softmax(M, s):
     return {"mc": M.maxcut(s, x), "sm": M.softmax(s, x)}
 
 
-@pytest.mark.parametrize("fn", [_relu, _relu32, _max_odd, _maxcut_softmax],
-                         ids=["relu", "relu_w32", "max_odd", "maxcut_softmax"])
+def _attexp(M, s):
+    rng = np.random.default_rng(30)
+    x = M.deal_fixed(s, -np.abs(rng.normal(0, 6, 3000)) - 2 ** -23, 32, 23, tag=0)
+    return {"y": M.attention_exp(s, x)}
+
+
+def _attexp14(M, s):
+    rng = np.random.default_rng(31)
+    x = M.deal_fixed(s, -np.abs(rng.normal(0, 4, (16, 40))), 32, 14, tag=0)
+    return {"y": M.attention_exp(s, x)}
+
+
+def _attention(M, s):
+    rng = np.random.default_rng(32)
+    heads = []
+    for h in range(2):
+        q, k, v = (M.deal_fixed(s, rng.normal(0, 1, (24, 16)), 64, 14, tag=3 * h + i) for i in range(3))
+        heads.append((q, k, v))
+    return {"a": M.attention_block(s, heads, optimized=True)}
+
+
+@pytest.mark.parametrize("fn", [_relu, _relu32, _max_odd, _maxcut_softmax, _attexp, _attexp14, _attention],
+                         ids=["relu", "relu_w32", "max_odd", "maxcut_softmax", "attexp", "attexp_p14",
+                              "attention"])
 @pytest.mark.parametrize("n", [2, 3, 4])
 def test_fused_cmp_equals_per_round_and_oracle(engines, fn, n):
     g, o = engines
