@@ -96,10 +96,16 @@ int mpx_open_xor(uint64_t* out, const uint64_t* x, int L, int64_t n, void* strea
  * mul/matmul (basic.py:36, :66) and decompose (basic.py:211). */
 int mpx_mask_sub(uint64_t* out, const uint64_t* x, const uint64_t* a, int64_t a_ps, int L, int64_t n,
                  int width, void* stream);
-/* Same for a transposed operand stored cols x rows (party stride x_ps):
- * out[r][c] = sum_l (x_l[c][r] - a_l[r][c]) (Beaver masks of X^T, W^T). */
-int mpx_mask_sub_t(uint64_t* out, const uint64_t* x, int64_t x_ps, const uint64_t* a, int64_t a_ps, int L,
-                   int64_t rows, int64_t cols, int width, void* stream);
+/* Batched, strided masks (every equal-shape product of a batch_matmul round):
+ * out[b][j] = sum_l (x_l[b][j] - a_l[b][j]); x at party / batch strides
+ * x_ps / x_bs, a at a_ps / a_bs; out contiguous [batch][n]. */
+int mpx_mask_sub_bs(uint64_t* out, const uint64_t* x, int64_t x_ps, int64_t x_bs, const uint64_t* a,
+                    int64_t a_ps, int64_t a_bs, int L, int64_t batch, int64_t n, int width, void* stream);
+/* Transposed operands read in place: out[b][r][c] = sum_l (x_l[b][c][r] - a_l[b][r][c])
+ * (Beaver masks of X^T, W^T, K^T). */
+int mpx_mask_sub_t(uint64_t* out, const uint64_t* x, int64_t x_ps, int64_t x_bs, const uint64_t* a,
+                   int64_t a_ps, int64_t a_bs, int L, int64_t batch, int64_t rows, int64_t cols, int width,
+                   void* stream);
 
 /* ---- Beaver multiplication (basic.py:27-42) ----
  * z_l = c_l + d*b_l + e*a_l + [l==p0] d*e. */
@@ -262,6 +268,12 @@ int mpx_gemm_limbs(uint64_t* C, const uint8_t* A8, const uint8_t* B8, int64_t ba
 int mpx_beaver_gemm(uint64_t* Z, int64_t sZ, const uint64_t* C, int64_t sC, const uint64_t* D,
                     const uint64_t* E, const uint64_t* A, int64_t sA, const uint64_t* B, int64_t sB,
                     int L, int64_t M, int64_t K, int64_t N, int p0, int width, void* stream);
+/* `batch` independent equal-shape reconstructions in one launch; product b
+ * uses Z + b*bZ, C + b*bC, D + b*M*K, E + b*K*N, A + b*bA, B + b*bB. */
+int mpx_beaver_gemm_batched(uint64_t* Z, int64_t sZ, int64_t bZ, const uint64_t* C, int64_t sC, int64_t bC,
+                            const uint64_t* D, const uint64_t* E, const uint64_t* A, int64_t sA, int64_t bA,
+                            const uint64_t* B, int64_t sB, int64_t bB, int L, int64_t batch, int64_t M,
+                            int64_t K, int64_t N, int p0, int width, void* stream);
 
 /* ---- sim-mode whole-op fused kernels (fused_ops.cu) ----
  * All L parties on this GPU: the whole Reciprocal / Exp / Log protocol

@@ -37,7 +37,8 @@ _SIGS = {
     "mpx_trunc_sub_multi": [_P, _I, _I, _I, _P],
     "mpx_trunc_rows_bias": [_P, _P, _P, _I, _P, _L, _P, _L, _I, _L, _L, _L, _I, _I, _I, _U, _U, _I, _P],
     "mpx_trunc_expand_rows": [_P, _P, _P, _L, _P, _L, _I, _L, _L, _L, _L, _L, _I, _I, _U, _U, _I, _P],
-    "mpx_mask_sub_t": [_P, _P, _L, _P, _L, _I, _L, _L, _I, _P],
+    "mpx_mask_sub_t": [_P, _P, _L, _L, _P, _L, _L, _I, _L, _L, _L, _I, _P],
+    "mpx_mask_sub_bs": [_P, _P, _L, _L, _P, _L, _L, _I, _L, _L, _I, _P],
     "mpx_mul_finish": [_P, _P, _P, _P, _P, _P, _L, _I, _L, _I, _I, _P],
     "mpx_mul_fused": [_P, _P, _P, _P, _P, _P, _L, _I, _L, _I, _I, _P],
     "mpx_trunc_mask": [_P, _P, _P, _L, _P, _L, _I, _L, _I, _I, _U, _I, _P],
@@ -68,6 +69,8 @@ _SIGS = {
     "mpx_limb_split": [_P, _P, _L, _L, _L, _L, _L, _L, _I, _P],
     "mpx_beaver_limbs": [_P, _P, _P, _P, _P, _L, _P, _L, _I, _L, _L, _L, _L, _L, _L, _I, _P],
     "mpx_beaver_gemm": [_P, _L, _P, _L, _P, _P, _P, _L, _P, _L, _I, _L, _L, _L, _I, _I, _P],
+    "mpx_beaver_gemm_batched": [_P, _L, _L, _P, _L, _L, _P, _P, _P, _L, _L, _P, _L, _L, _I, _L, _L, _L, _L, _I, _I,
+                                _P],
     "mpx_ring_colsum": [_P, _P, _I, _L, _L, _I, _P],
     "mpx_ring_pool_sum": [_P, _P, _L, _L, _L, _L, _I, _P],
     "mpx_ring_add_rowvec": [_P, _P, _I, _L, _L, _I, _I, _P],

@@ -47,14 +47,22 @@ template <int BM, int BN, int TN>
 __global__ void __launch_bounds__((BM / 4) * (BN / TN), bg_min_blocks((BM / 4) * (BN / TN)))
     k_beaver_gemm(u64* __restrict__ Z, i64 sZ, const u64* __restrict__ C, i64 sC, const u64* __restrict__ D,
                   const u64* __restrict__ E, const u64* __restrict__ A, i64 sA, const u64* __restrict__ B,
-                  i64 sB, int M, int K, int N, int p0, u64 msk, int ksplit, int kchunk) {
+                  i64 sB, int M, int K, int N, int p0, u64 msk, int ksplit, int kchunk, int L, i64 bZ, i64 bC,
+                  i64 bA, i64 bB) {
   constexpr int TX = BN / TN, TY = BM / 4, NT = TX * TY;
   __shared__ u64 Ds[BG_BK][BM + 1];
   __shared__ u64 As[BG_BK][BM + 1];
   __shared__ u64 Bs[BG_BK][BN];
   __shared__ u64 Es[BG_BK][BN];
-  const int l = blockIdx.z / ksplit;
+  const int zl = blockIdx.z / ksplit;  // (product, party)
   const int ks = blockIdx.z % ksplit;
+  const int bt = zl / L, l = zl - bt * L;
+  Z += bt * bZ;
+  C += bt * bC;
+  A += bt * bA;
+  B += bt * bB;
+  D += (i64)bt * M * K;
+  E += (i64)bt * K * N;
   const int kbeg = ks * kchunk, kend = min(K, kbeg + kchunk);
   const u64* Al = A + (i64)l * sA;
   const u64* Bl = B + (i64)l * sB;
@@ -122,19 +130,29 @@ const Cfg kCfgs[] = {{64, 64, 4}, {128, 32, 4}, {128, 16, 4}, {32, 32, 4},
                      {128, 20, 5}, {128, 10, 5}, {32, 20, 5}, {32, 10, 5}};
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 
+struct Batch {
+  int L;
+  i64 bZ, bC, bA, bB;
+};
+
 template <int BM, int BN, int TN>
 void launch(dim3 grid, cudaStream_t s, uint64_t* Z, int64_t sZ, const uint64_t* C, int64_t sC, const uint64_t* D,
             const uint64_t* E, const uint64_t* A, int64_t sA, const uint64_t* B, int64_t sB, int M, int K, int N,
-            int p0, u64 msk, int ksplit, int kchunk) {
+            int p0, u64 msk, int ksplit, int kchunk, const Batch& bt) {
   k_beaver_gemm<BM, BN, TN><<<grid, (BM / 4) * (BN / TN), 0, s>>>(Z, sZ, C, sC, D, E, A, sA, B, sB, M, K, N, p0,
-                                                                    msk, ksplit, kchunk);
+                                                                    msk, ksplit, kchunk, bt.L, bt.bZ, bt.bC, bt.bA,
+                                                                    bt.bB);
 }
 }  // namespace
 
-extern "C" int mpx_beaver_gemm(uint64_t* Z, int64_t sZ, const uint64_t* C, int64_t sC, const uint64_t* D,
-                               const uint64_t* E, const uint64_t* A, int64_t sA, const uint64_t* B, int64_t sB,
-                               int L, int64_t M, int64_t K, int64_t N, int p0, int width, void* stream) {
+extern "C" int mpx_beaver_gemm_batched(uint64_t* Z, int64_t sZ, int64_t bZ, const uint64_t* C, int64_t sC,
+                                       int64_t bC, const uint64_t* D, const uint64_t* E, const uint64_t* A,
+                                       int64_t sA, int64_t bA, const uint64_t* B, int64_t sB, int64_t bB, int L,
+                                       int64_t batch, int64_t M, int64_t K, int64_t N, int p0, int width,
+                                       void* stream) {
   CHECK_ARG(Z && C && D && E && A && B && L >= 1 && M >= 1 && K >= 1 && N >= 1 && width >= 1 && width <= 64);
+  CHECK_ARG(batch >= 1 && batch * L <= 65535);
+  const Batch bt{L, bZ, bC, bA, bB};
   CHECK_ARG(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31) && M * K < (1ll << 40));
   CHECK_ARG(p0 < L);
   // tile shape: least padded output area, ties to the larger tile
@@ -151,7 +169,7 @@ extern "C" int mpx_beaver_gemm(uint64_t* Z, int64_t sZ, const uint64_t* C, int64
   }
   const int bm = kCfgs[best].bm, bn = kCfgs[best].bn;
   const int nt = (bm / 4) * (bn / kCfgs[best].tn);
-  const i64 tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn) * L;
+  const i64 tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn) * L * batch;
   // resident CTAs per SM at <= 128 registers per thread
   const i64 per_sm = min((i64)32, (i64)(65536 / (max(nt, 32) * 128)));
   const i64 target = 148 * per_sm;
@@ -162,20 +180,21 @@ extern "C" int mpx_beaver_gemm(uint64_t* Z, int64_t sZ, const uint64_t* C, int64
   }
   const i64 kchunk = ((K + ksplit - 1) / ksplit + BG_BK - 1) / BG_BK * BG_BK;
   ksplit = (int)((K + kchunk - 1) / kchunk);
-  CHECK_ARG((i64)L * ksplit <= 65535 && (M + bm - 1) / bm <= 65535);
+  CHECK_ARG((i64)L * batch * ksplit <= 65535 && (M + bm - 1) / bm <= 65535);
   cudaStream_t s = (cudaStream_t)stream;
   if (ksplit > 1) {
     // every party's partial products land on a copy of its C
-    if (cudaMemcpy2DAsync(Z, (size_t)sZ * 8, C, (size_t)sC * 8, (size_t)(M * N * 8), (size_t)L,
-                          cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-      return MPX_ERR_CUDA;
+    for (i64 b = 0; b < batch; ++b)
+      if (cudaMemcpy2DAsync(Z + b * bZ, (size_t)sZ * 8, C + b * bC, (size_t)sC * 8, (size_t)(M * N * 8), (size_t)L,
+                            cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        return MPX_ERR_CUDA;
   }
-  dim3 grid((unsigned)((N + bn - 1) / bn), (unsigned)((M + bm - 1) / bm), (unsigned)(L * ksplit));
+  dim3 grid((unsigned)((N + bn - 1) / bn), (unsigned)((M + bm - 1) / bm), (unsigned)(L * batch * ksplit));
   const u64 msk = ring_mask(width);
 #define BG_CASE(I, BM_, BN_, TN_)                                                                             \
   case I:                                                                                                    \
     launch<BM_, BN_, TN_>(grid, s, Z, sZ, C, sC, D, E, A, sA, B, sB, (int)M, (int)K, (int)N, p0, msk, ksplit, \
-                          (int)kchunk);                                                                      \
+                          (int)kchunk, bt);                                                                  \
     break;
   switch (best) {
     BG_CASE(0, 64, 64, 4)
@@ -189,4 +208,10 @@ extern "C" int mpx_beaver_gemm(uint64_t* Z, int64_t sZ, const uint64_t* C, int64
   }
 #undef BG_CASE
   return launch_status();
+}
+
+extern "C" int mpx_beaver_gemm(uint64_t* Z, int64_t sZ, const uint64_t* C, int64_t sC, const uint64_t* D,
+                               const uint64_t* E, const uint64_t* A, int64_t sA, const uint64_t* B, int64_t sB,
+                               int L, int64_t M, int64_t K, int64_t N, int p0, int width, void* stream) {
+  return mpx_beaver_gemm_batched(Z, sZ, 0, C, sC, 0, D, E, A, sA, 0, B, sB, 0, L, 1, M, K, N, p0, width, stream);
 }

@@ -300,13 +300,42 @@ extern "C" int mpx_mask_sub(uint64_t* out, const uint64_t* x, const uint64_t* a,
   return launch_status();
 }
 
-// Beaver mask of a transposed operand without materialising the transpose:
-// out[r][c] = sum_l (x_l[c][r] - a_l[r][c]) mod 2^w, x_l stored cols x rows
-// (party stride x_ps). 32 x 32 tiles through shared memory: x is read along
-// its rows, a and out along theirs.
-__global__ void k_mask_sub_t(u64* __restrict__ out, const u64* __restrict__ x, i64 x_ps, const u64* __restrict__ a,
-                             i64 a_ps, int L, i64 rows, i64 cols, u64 msk) {
+// Beaver masks of a batch of operands read in place (one launch for all the
+// equal-shape products of a batch_matmul round):
+//   out[b][j] = sum_l (x_l[b][j] - a_l[b][j]) mod 2^w,
+// x at party stride x_ps and batch stride x_bs, a at a_ps / a_bs.
+__global__ void k_mask_sub_bs(u64* __restrict__ out, const u64* __restrict__ x, i64 x_ps, i64 x_bs,
+                              const u64* __restrict__ a, i64 a_ps, i64 a_bs, int L, i64 batch, i64 n, u64 msk) {
+  const i64 total = batch * n;
+  GRID_STRIDE(t, total) {
+    const i64 b = t / n, j = t - b * n;
+    u64 s = 0;
+    for (int l = 0; l < L; ++l) s += x[(i64)l * x_ps + b * x_bs + j] - a[(i64)l * a_ps + b * a_bs + j];
+    out[t] = s & msk;
+  }
+}
+
+extern "C" int mpx_mask_sub_bs(uint64_t* out, const uint64_t* x, int64_t x_ps, int64_t x_bs, const uint64_t* a,
+                               int64_t a_ps, int64_t a_bs, int L, int64_t batch, int64_t n, int width,
+                               void* stream) {
+  CHECK_ARG(out && x && a && L >= 1 && batch >= 0 && n >= 0 && width >= 1 && width <= 64);
+  if (batch == 0 || n == 0) return MPX_OK;
+  k_mask_sub_bs<<<grid_for(batch * n), MPX_THREADS, 0, (cudaStream_t)stream>>>(out, x, x_ps, x_bs, a, a_ps, a_bs,
+                                                                              L, batch, n, ring_mask(width));
+  return launch_status();
+}
+
+// Same for transposed operands without materialising the transpose:
+// out[b][r][c] = sum_l (x_l[b][c][r] - a_l[b][r][c]) mod 2^w, x_l[b] stored
+// cols x rows. 32 x 32 tiles through shared memory: x is read along its rows,
+// a and out along theirs.
+__global__ void k_mask_sub_t(u64* __restrict__ out, const u64* __restrict__ x, i64 x_ps, i64 x_bs,
+                             const u64* __restrict__ a, i64 a_ps, i64 a_bs, int L, i64 rows, i64 cols, u64 msk) {
   __shared__ u64 tile[32][33];
+  const i64 bt = blockIdx.z;
+  x += bt * x_bs;
+  a += bt * a_bs;
+  out += bt * rows * cols;
   const i64 r0 = (i64)blockIdx.y * 32, c0 = (i64)blockIdx.x * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
 #pragma unroll
@@ -329,13 +358,14 @@ __global__ void k_mask_sub_t(u64* __restrict__ out, const u64* __restrict__ x, i
   }
 }
 
-extern "C" int mpx_mask_sub_t(uint64_t* out, const uint64_t* x, int64_t x_ps, const uint64_t* a, int64_t a_ps,
-                              int L, int64_t rows, int64_t cols, int width, void* stream) {
-  CHECK_ARG(out && x && a && L >= 1 && rows >= 0 && cols >= 0 && width >= 1 && width <= 64);
-  if (rows == 0 || cols == 0) return MPX_OK;
-  CHECK_ARG((rows + 31) / 32 <= 65535);
-  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
-  k_mask_sub_t<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(out, x, x_ps, a, a_ps, L, rows, cols,
+extern "C" int mpx_mask_sub_t(uint64_t* out, const uint64_t* x, int64_t x_ps, int64_t x_bs, const uint64_t* a,
+                              int64_t a_ps, int64_t a_bs, int L, int64_t batch, int64_t rows, int64_t cols,
+                              int width, void* stream) {
+  CHECK_ARG(out && x && a && L >= 1 && batch >= 0 && rows >= 0 && cols >= 0 && width >= 1 && width <= 64);
+  if (batch == 0 || rows == 0 || cols == 0) return MPX_OK;
+  CHECK_ARG((rows + 31) / 32 <= 65535 && batch <= 65535);
+  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32), (unsigned)batch);
+  k_mask_sub_t<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(out, x, x_ps, x_bs, a, a_ps, a_bs, L, rows, cols,
                                                                 ring_mask(width));
   return launch_status();
 }

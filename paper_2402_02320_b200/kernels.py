@@ -134,20 +134,39 @@ def trunc_expand_rows(z, x, r_lo, lo_ps, r_hi, hi_ps, L, B, C, Hs, Ws, k, width,
     return z
 
 
-def mask_sub_t(out, x_ptr, x_ps, a_ptr, a_ps, L, rows, cols, width):
+def mask_sub_t(out, x_ptr, x_ps, a_ptr, a_ps, L, rows, cols, width, batch=1, x_bs=0, a_bs=0):
     if _dry(out):
         return out
-    call("mpx_mask_sub_t", ptr(out), x_ptr, x_ps, a_ptr, a_ps, L, rows, cols, width)
+    call("mpx_mask_sub_t", ptr(out), x_ptr, x_ps, x_bs, a_ptr, a_ps, a_bs, L, batch, rows, cols, width)
+    return out
+
+
+def mask_sub_bs(out, x_ptr, x_ps, x_bs, a_ptr, a_ps, a_bs, L, batch, n, width):
+    if _dry(out):
+        return out
+    call("mpx_mask_sub_bs", ptr(out), x_ptr, x_ps, x_bs, a_ptr, a_ps, a_bs, L, batch, n, width)
     return out
 
 
 def transposed_base(v):
-    """(base tensor, party stride) when ``v`` [L, r, c] is the last-two-axes
-    transpose of a contiguous [L, c, r] tensor, else None."""
+    """Party stride when ``v`` [L, r, c] is the last-two-axes transpose of a
+    [c, r]-contiguous matrix per party (any party stride), else None."""
     if v.dim() != 3 or v.is_contiguous():
         return None
     L, r, c = v.shape
-    if v.stride() == (c * r, 1, r):
+    if v.stride(1) == 1 and v.stride(2) == r and (L == 1 or v.stride(0) >= r * c):
+        return v.stride(0)
+    return None
+
+
+def rows_base(v):
+    """Party stride when ``v`` [L, ...] is row-major contiguous within each
+    party (any party stride), else None."""
+    if v.dim() < 2:
+        return None
+    inner = v[0] if v.shape[0] > 0 else v
+    n = inner.numel()
+    if inner.is_contiguous() and (v.shape[0] == 1 or v.stride(0) >= n):
         return v.stride(0)
     return None
 
@@ -394,6 +413,16 @@ def ring_add_rowvec(z, b, L, rows, cols, shift, width):
         return z
     call("mpx_ring_add_rowvec", ptr(z), ptr(b), L, rows, cols, shift, width)
     return z
+
+
+def beaver_gemm_batched(Z, sZ, bZ, C_ptr, sC, bC, D, E, A_ptr, sA, bA, B_ptr, sB, bB, L, batch, M, K, N, p0,
+                        width):
+    """``batch`` equal-shape Beaver reconstructions (one launch, all local parties)."""
+    if _dry(Z):
+        return Z
+    call("mpx_beaver_gemm_batched", ptr(Z), sZ, bZ, C_ptr, sC, bC, ptr(D), ptr(E), A_ptr, sA, bA, B_ptr, sB, bB, L,
+         batch, M, K, N, p0, width)
+    return Z
 
 
 def beaver_gemm(Z, sZ, C_ptr, sC, D, E, A_ptr, sA, B_ptr, sB, L, M, K, N, p0, width):

@@ -52,49 +52,132 @@ def matmul(session, x: AShare, y: AShare) -> AShare:
 def batch_matmul(session, pairs) -> list[AShare]:
     """Independent matrix products in one round, one matrix triple each (basic.py:45-79).
 
-    Z_l = C_l + D @ B_l + A_l @ E + [l==p0] D @ E, on the Z_2^64 GEMM kernel.
+    Z_l = C_l + D @ B_l + A_l @ E + [l==p0] D @ E, on the Z_2^64 GEMM kernels.
+    Runs of equal-shape pairs whose operands sit at uniform strides (attention
+    heads, Q/K/V on one input) are masked and reconstructed with one launch
+    each; material order, the round and the ledger are per pair as in the
+    reference.
     """
     L = session.L
-    trip, masked = [], []
     for x, y in pairs:
         if len(x.shape) != 2 or len(y.shape) != 2 or x.shape[1] != y.shape[0]:
             raise ValueError(f"bad matmul shapes {x.shape} @ {y.shape}")
-        w = x.width
+    trip = []
+    for x, y in pairs:
         m, k = x.shape
-        r = y.shape[1]
-        A, B, C = session.store.take_matrix_triple(w, m, k, r)
-        D, E = session.alloc((m * k,)), session.alloc((k * r,))
-        _mask(D, x.values, A, L, m, k, w)
-        _mask(E, y.values, B, L, k, r, w)
-        trip.append((A, B, C))
-        masked += [(D, w), (E, w)]
+        trip.append(session.store.take_matrix_triple(x.width, m, k, y.shape[1]))
+    groups = _groups(session, pairs, trip)
+    masked = []
+    for g in groups:
+        x0, y0 = pairs[g[0]]
+        w, (m, k), r = x0.width, x0.shape, y0.shape[1]
+        D = session.alloc((len(g), m * k))
+        E = session.alloc((len(g), k * r))
+        _mask_group(D, [pairs[i][0].values for i in g], [trip[i][0] for i in g], L, m, k, w)
+        _mask_group(E, [pairs[i][1].values for i in g], [trip[i][1] for i in g], L, k, r, w)
+        for j in range(len(g)):
+            masked += [(D[j], w), (E[j], w)]
     opened = session.exchange(arith=masked)
-    out = []
-    for i, (x, y) in enumerate(pairs):
-        w = x.width
-        m, k = x.shape
-        r = y.shape[1]
-        A, B, C = trip[i]
-        D, E = opened[2 * i], opened[2 * i + 1]
-        Z = session.alloc((L, m, r))
+    out = [None] * len(pairs)
+    pos = 0
+    for g in groups:
+        x0, y0 = pairs[g[0]]
+        w, (m, k), r = x0.width, x0.shape, y0.shape[1]
+        Ds = opened[pos:pos + 2 * len(g):2]
+        Es = opened[pos + 1:pos + 2 * len(g):2]
+        pos += 2 * len(g)
+        Zg = session.alloc((len(g), L, m, r))
         if not session.dry and _use_tc(m, k, r, w):
-            _beaver_matmul_tc(session, Z, D, E, A, B, C, L, m, k, r, w)
+            for j, i in enumerate(g):
+                A, B, C = trip[i]
+                _beaver_matmul_tc(session, Zg[j], Ds[j], Es[j], A, B, C, L, m, k, r, w)
         else:
-            K.beaver_gemm(Z, m * r, C.data_ptr(), C.stride(0), D, E, A.data_ptr(), A.stride(0), B.data_ptr(),
-                          B.stride(0), L, m, k, r, session.p0, w)
-        session.metrics.count(matmul_count=1, matmul_macs=m * k * r)
-        out.append(AShare(Z, w, x.frac + y.frac, session.parties))
+            A0, B0, C0 = trip[g[0]]
+            Dg, Eg = _stacked(Ds, m * k), _stacked(Es, k * r)
+            K.beaver_gemm_batched(Zg, m * r, L * m * r, C0.data_ptr(), C0.stride(0), _bstride(trip, g, 2),
+                                  Dg, Eg, A0.data_ptr(), A0.stride(0), _bstride(trip, g, 0),
+                                  B0.data_ptr(), B0.stride(0), _bstride(trip, g, 1), L, len(g), m, k, r,
+                                  session.p0, w)
+        for j, i in enumerate(g):
+            x, y = pairs[i]
+            session.metrics.count(matmul_count=1, matmul_macs=m * k * r)
+            out[i] = AShare(Zg[j], w, x.frac + y.frac, session.parties)
     return out
 
 
-def _mask(out, v, T, L, rows, cols, w):
-    """out = open(v - T) (sim) / v - T (party); a transposed view of a
-    contiguous tensor (X^T, W^T in backward) is read in place."""
-    tps = K.transposed_base(v) if not session_dry(v) else None
+def _ptr(t) -> int:
+    return 0 if t.is_meta else t.data_ptr()
+
+
+def _uniform(ptrs) -> int | None:
+    """Common byte step of a pointer sequence (0 allowed), else None."""
+    if len(ptrs) < 2:
+        return 0
+    d = ptrs[1] - ptrs[0]
+    return d if all(ptrs[i + 1] - ptrs[i] == d for i in range(len(ptrs) - 1)) else None
+
+
+def _layout(v):
+    """('t' | 'r', party stride) of an operand the mask kernels read in place."""
+    tps = K.transposed_base(v)
     if tps is not None:
-        K.mask_sub_t(out, v.data_ptr(), tps, T.data_ptr(), T.stride(0), L, rows, cols, w)
+        return "t", tps
+    rps = K.rows_base(v)
+    return ("r", rps) if rps is not None else (None, None)
+
+
+def _groups(session, pairs, trip) -> list[list[int]]:
+    """Consecutive equal-shape pairs whose x, y operands and triple parts sit
+    at uniform strides (one launch per group); singletons otherwise."""
+    groups: list[list[int]] = []
+    for i, (x, y) in enumerate(pairs):
+        if groups and not session.dry:
+            g = groups[-1]
+            x0, y0 = pairs[g[0]]
+            same = (x.shape == x0.shape and y.shape == y0.shape and x.width == x0.width
+                    and _layout(x.values) == _layout(x0.values) and _layout(y.values) == _layout(y0.values)
+                    and _layout(x.values)[0] is not None and _layout(y.values)[0] is not None)
+            if same:
+                cand = g + [i]
+                ok = all(_uniform([_ptr(pairs[j][s].values) for j in cand]) is not None for s in (0, 1)) and \
+                    all(_uniform([_ptr(trip[j][s]) for j in cand]) is not None and
+                        trip[cand[-1]][s].stride(0) == trip[g[0]][s].stride(0) for s in (0, 1, 2))
+                if ok:
+                    g.append(i)
+                    continue
+        groups.append([i])
+    return groups
+
+
+def _bstride(trip, g, s) -> int:
+    return (_uniform([_ptr(trip[i][s]) for i in g]) or 0) // 8
+
+
+def _stacked(ts, n):
+    """[len(ts), n] view when the tensors are consecutive rows of one buffer."""
+    if len(ts) == 1:
+        return ts[0].reshape(1, n)
+    base = ts[0]
+    if all(_ptr(t) == _ptr(base) + 8 * n * j for j, t in enumerate(ts)) and not base.is_meta:
+        return base.as_strided((len(ts), n), (n, 1))
+    return torch.stack([t.reshape(n) for t in ts])
+
+
+def _mask_group(out, vs, Ts, L, rows, cols, w):
+    """out[j] = open(vs[j] - Ts[j]) (sim) / vs[j] - Ts[j] (party) for a group,
+    one launch; transposed views (X^T, W^T, K^T) are read in place."""
+    v0, T0 = vs[0], Ts[0]
+    xbs = (_uniform([_ptr(v) for v in vs]) or 0) // 8
+    abs_ = (_uniform([_ptr(T) for T in Ts]) or 0) // 8
+    kind, ps = _layout(v0) if not v0.is_meta else ("r", rows * cols)
+    if kind == "t":
+        K.mask_sub_t(out, _ptr(v0), ps, _ptr(T0), T0.stride(0), L, rows, cols, w, batch=len(vs), x_bs=xbs,
+                     a_bs=abs_)
+    elif kind == "r":
+        K.mask_sub_bs(out, _ptr(v0), ps, xbs, _ptr(T0), T0.stride(0), abs_, L, len(vs), rows * cols, w)
     else:
-        K.mask_sub(out, v.contiguous(), T.data_ptr(), T.stride(0), L, rows * cols, w)
+        for j, (v, T) in enumerate(zip(vs, Ts)):
+            K.mask_sub(out[j], v.contiguous(), _ptr(T), T.stride(0), L, rows * cols, w)
 
 
 def session_dry(v) -> bool:

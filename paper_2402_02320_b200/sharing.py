@@ -111,6 +111,12 @@ class AShare:
         idx = idx if isinstance(idx, tuple) else (idx,)
         return self._new(self.values[(slice(None),) + idx].contiguous())
 
+    def view_at(self, idx) -> "AShare":
+        """Like ``self[idx]`` but a strided view (no copy): for operands read
+        once by stride-aware kernels (batch_matmul masks)."""
+        idx = idx if isinstance(idx, tuple) else (idx,)
+        return AShare.strided(self.values[(slice(None),) + idx], self.width, self.frac, self.parties)
+
     def reshape(self, shape) -> "AShare":
         return self._new(self.values.reshape((self.L,) + tuple(shape)))
 

@@ -62,7 +62,8 @@ class Transformer:
         S = t.shape[0]
         dh = self.d // self.heads
         v = t.values.view(t.L, S, self.heads, dh).permute(0, 2, 1, 3).contiguous()
-        return [AShare(v[:, h].contiguous(), t.width, t.frac, t.parties) for h in range(self.heads)]
+        # strided per-head views of one buffer: the head products batch into single launches
+        return [AShare.strided(v[:, h], t.width, t.frac, t.parties) for h in range(self.heads)]
 
     def layer(self, s, i: int, x: AShare) -> AShare:
         W, p = self.W[i], self.p
