@@ -313,9 +313,9 @@ def alg_bytes(name, a):
         if name == "mpx_ring_colsum":
             L, rows, cols = a[2], a[3], a[4]
             return 8 * L * rows * cols + 8 * L * cols
-        if name == "mpx_ring_pool_sum":
-            planes, H, W, k = a[2], a[3], a[4], a[5]
-            return 8 * planes * H * W + 8 * planes * (H // k) * (W // k)
+        if name in ("mpx_ring_pool_sum", "mpx_ring_pool_scatter"):
+            planes, H, W, k, st = a[2], a[3], a[4], a[5], a[6]
+            return 8 * planes * H * W + 8 * planes * ((H - k) // st + 1) * ((W - k) // st + 1)
         if name == "mpx_ring_add_rowvec":
             L, rows, cols = a[2], a[3], a[4]
             return 16 * L * rows * cols + 8 * L * cols

@@ -76,9 +76,13 @@ int mpx_ring_rowdot(uint64_t* out, const uint64_t* x, const uint64_t* wts, int L
 /* out[l][c] = sum_r x[l][r][c] mod 2^width, x: [L][rows][cols] (bias gradients). */
 int mpx_ring_colsum(uint64_t* out, const uint64_t* x, int L, int64_t rows, int64_t cols, int width,
                     void* stream);
-/* k x k, stride-k window sums over [planes][H][W] -> [planes][H/k][W/k] (average pooling). */
+/* k x k window sums, stride st, over [planes][H][W] -> [planes][OH][OW] with
+ * OH = (H - k) / st + 1 (average pooling before its 1/k^2 scaling). */
 int mpx_ring_pool_sum(uint64_t* out, const uint64_t* x, int64_t planes, int64_t H, int64_t W, int64_t k,
-                      int width, void* stream);
+                      int64_t stride, int width, void* stream);
+/* Adjoint: dx[p][h][w] = sum of d[p][oi][oj] over the windows covering (h, w). */
+int mpx_ring_pool_scatter(uint64_t* dx, const uint64_t* d, int64_t planes, int64_t H, int64_t W, int64_t k,
+                          int64_t stride, int width, void* stream);
 /* z[l][r][c] = z[l][r][c] + (b[l][c] << shift) mod 2^width, in place (bias rows). */
 int mpx_ring_add_rowvec(uint64_t* z, const uint64_t* b, int L, int64_t rows, int64_t cols, int shift,
                         int width, void* stream);

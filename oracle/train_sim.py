@@ -77,12 +77,13 @@ def _colsum(z: O.AShare) -> O.AShare:
 
 
 class Conv2d:
-    def __init__(self, s, cin, cout, k, stride=1, pad=0, *, rng, name, seed, frac, width=64):
+    def __init__(self, s, cin, cout, k, stride=1, pad=0, *, rng, name, seed, frac, width=64, bias=True):
         self.cin, self.cout, self.k, self.stride, self.pad, self.p = cin, cout, k, stride, pad, frac
         fan_in = cin * k * k
         self.W = share_fixed(s, rng.normal(0.0, math.sqrt(2.0 / fan_in), (fan_in, cout)), width, frac,
                              _key(seed, name + ".W"))
-        self.b = share_fixed(s, np.zeros(cout), width, frac, _key(seed, name + ".b"))
+        if bias:
+            self.b = share_fixed(s, np.zeros(cout), width, frac, _key(seed, name + ".b"))
 
     def forward(self, s, x):
         n, B, C, H, W = x.values.shape
@@ -91,7 +92,9 @@ class Conv2d:
         OH, OW = (H + 2 * self.pad - self.k) // self.stride + 1, (W + 2 * self.pad - self.k) // self.stride + 1
         self.out_hw = (OH, OW)
         z = O.batch_matmul(s, [(self.cols, self.W)])[0]
-        z = O.truncate(s, z + _bcast_rows(_lift(self.b, self.p), B * OH * OW), self.p)
+        if hasattr(self, "b"):
+            z = z + _bcast_rows(_lift(self.b, self.p), B * OH * OW)
+        z = O.truncate(s, z, self.p)
         v = z.values.reshape(n, B, OH, OW, self.cout).transpose(0, 1, 4, 2, 3)
         return O.AShare(np.ascontiguousarray(v), z.width, z.frac)
 
@@ -104,7 +107,9 @@ class Conv2d:
         if need_dx:
             pairs.append((dz, _T(self.W)))
         outs = O.batch_matmul(s, pairs)
-        self.gW, self.gb = outs[0], _colsum(dz)
+        self.gW = outs[0]
+        if hasattr(self, "b"):
+            self.gb = _colsum(dz)
         if not need_dx:
             return None
         dcols = O.truncate(s, outs[1], self.p)
@@ -113,28 +118,53 @@ class Conv2d:
 
     def step(self, s, shift):
         self.W = self.W - O.truncate(s, self.gW, self.p + shift, out_frac=self.p)
-        self.b = self.b - O.truncate(s, self.gb, shift, out_frac=self.p)
+        if hasattr(self, "b"):
+            self.b = self.b - O.truncate(s, self.gb, shift, out_frac=self.p)
 
 
 class AvgPool2d:
-    def __init__(self, k=2):
+    """k x k average pool, stride st (default k): window sum, then / k^2 as a
+    truncation by log2(k^2) for power-of-two windows, else scale by the
+    public fixed-point 1/k^2 and truncate by p. Backward: the same scaling of
+    dy, scattered back over the windows (the sum's adjoint)."""
+
+    def __init__(self, k=2, stride=None):
         self.k = k
-        self.shift = int(round(math.log2(k * k)))
+        self.st = k if stride is None else stride
+        area = k * k
+        self.shift = area.bit_length() - 1 if area & (area - 1) == 0 else None
+
+    def _scale(self, s, v: O.AShare) -> O.AShare:
+        if self.shift is not None:
+            return O.truncate(s, v, self.shift, out_frac=v.frac)
+        return O.truncate(s, O.scale_fixed(s, v, 1.0 / (self.k * self.k)), v.frac)
+
+    def _out_hw(self, H, W):
+        return (H - self.k) // self.st + 1, (W - self.k) // self.st + 1
 
     def forward(self, s, x):
         n, B, C, H, W = x.values.shape
-        k = self.k
+        k, st = self.k, self.st
+        OH, OW = self._out_hw(H, W)
         self.in_shape = x.values.shape
-        v = x.values.reshape(n, B, C, H // k, k, W // k, k).transpose(0, 1, 2, 3, 5, 4, 6)
-        summed = O.rsum(v.reshape(n, B, C, H // k, W // k, k * k), x.width)
-        return O.truncate(s, O.AShare(summed, x.width, x.frac), self.shift, out_frac=x.frac)
+        acc = np.zeros((n, B, C, OH, OW), U64)
+        with np.errstate(over="ignore"):
+            for a in range(k):
+                for b in range(k):
+                    acc += x.values[:, :, :, a:a + st * (OH - 1) + 1:st, b:b + st * (OW - 1) + 1:st]
+        return self._scale(s, O.AShare(O.wrap(acc, x.width), x.width, x.frac))
 
     def backward(self, s, dy, need_dx=True):
         n, B, C, H, W = self.in_shape
-        k = self.k
-        d = O.truncate(s, dy, self.shift, out_frac=dy.frac)
-        v = np.broadcast_to(d.values.reshape(n, B, C, H // k, 1, W // k, 1), (n, B, C, H // k, k, W // k, k))
-        return O.AShare(np.ascontiguousarray(v).reshape(n, B, C, H, W), d.width, d.frac)
+        k, st = self.k, self.st
+        OH, OW = self._out_hw(H, W)
+        d = self._scale(s, dy)
+        dx = np.zeros((n, B, C, H, W), U64)
+        with np.errstate(over="ignore"):
+            for a in range(k):
+                for b in range(k):
+                    dx[:, :, :, a:a + st * (OH - 1) + 1:st, b:b + st * (OW - 1) + 1:st] += d.values
+        return O.AShare(O.wrap(dx, d.width), d.width, d.frac)
 
 
 class ReLU:
@@ -166,28 +196,34 @@ AvgPool2d.step = lambda self, s, shift: None
 
 
 class Linear:
-    def __init__(self, s, fin, fout, *, rng, name, seed, frac, width=64):
+    def __init__(self, s, fin, fout, *, rng, name, seed, frac, width=64, bias=True):
         self.p = frac
         self.W = share_fixed(s, rng.normal(0.0, math.sqrt(2.0 / fin), (fin, fout)), width, frac,
                              _key(seed, name + ".W"))
-        self.b = share_fixed(s, np.zeros(fout), width, frac, _key(seed, name + ".b"))
+        if bias:
+            self.b = share_fixed(s, np.zeros(fout), width, frac, _key(seed, name + ".b"))
 
     def forward(self, s, x):
         self.x = x
         z = O.batch_matmul(s, [(x, self.W)])[0]
-        return O.truncate(s, z + _bcast_rows(_lift(self.b, self.p), x.shape[0]), self.p)
+        if hasattr(self, "b"):
+            z = z + _bcast_rows(_lift(self.b, self.p), x.shape[0])
+        return O.truncate(s, z, self.p)
 
     def backward(self, s, dy, need_dx=True):
         pairs = [(_T(self.x), dy)]
         if need_dx:
             pairs.append((dy, _T(self.W)))
         outs = O.batch_matmul(s, pairs)
-        self.gW, self.gb = outs[0], _colsum(dy)
+        self.gW = outs[0]
+        if hasattr(self, "b"):
+            self.gb = _colsum(dy)
         return O.truncate(s, outs[1], self.p) if need_dx else None
 
     def step(self, s, shift):
         self.W = self.W - O.truncate(s, self.gW, self.p + shift, out_frac=self.p)
-        self.b = self.b - O.truncate(s, self.gb, shift, out_frac=self.p)
+        if hasattr(self, "b"):
+            self.b = self.b - O.truncate(s, self.gb, shift, out_frac=self.p)
 
 
 class Model:
@@ -217,12 +253,47 @@ class Model:
 
 
 def lenet(s, seed=7, frac=23):
+    """Paper Table 'LeNet': 430,500 weights, no biases."""
     rng = np.random.default_rng(seed)
-    kw = dict(seed=seed, frac=frac)
+    kw = dict(seed=seed, frac=frac, bias=False)
     return Model([Conv2d(s, 1, 20, 5, rng=rng, name="conv1", **kw), AvgPool2d(2), ReLU(),
                   Conv2d(s, 20, 50, 5, rng=rng, name="conv2", **kw), AvgPool2d(2), ReLU(), Flatten(),
                   Linear(s, 800, 500, rng=rng, name="fc1", **kw), ReLU(),
                   Linear(s, 500, 10, rng=rng, name="fc2", **kw)])
+
+
+def alexnet(s, seed=7, frac=23):
+    """Paper Table 'AlexNet', CIFAR-10 3x32x32: 2,552,874
+    parameters = bias-free convolutions + fully-connected layers with bias."""
+    rng = np.random.default_rng(seed)
+    kw = dict(seed=seed, frac=frac)
+    return Model([Conv2d(s, 3, 96, 11, 4, 9, rng=rng, name="conv1", bias=False, **kw), AvgPool2d(3, 2), ReLU(),
+                  Conv2d(s, 96, 256, 5, 1, 1, rng=rng, name="conv2", bias=False, **kw), AvgPool2d(2, 1), ReLU(),
+                  Conv2d(s, 256, 384, 3, 1, 1, rng=rng, name="conv3", bias=False, **kw), ReLU(),
+                  Conv2d(s, 384, 256, 3, 1, 1, rng=rng, name="conv4", bias=False, **kw), ReLU(), Flatten(),
+                  Linear(s, 256, 256, rng=rng, name="fc1", **kw), ReLU(),
+                  Linear(s, 256, 256, rng=rng, name="fc2", **kw), ReLU(),
+                  Linear(s, 256, 10, rng=rng, name="fc3", **kw)])
+
+
+def vgg16m(s, seed=7, frac=26):
+    """Paper Table 'VGG16m', CIFAR-10 3x32x32, p = 26:
+    bias-free 3x3 convolutions, fully-connected layers with bias."""
+    rng = np.random.default_rng(seed)
+    kw = dict(seed=seed, frac=frac)
+    layers = []
+    cin = 3
+    for i, (cout, pool) in enumerate([(64, False), (64, True), (128, False), (128, True), (256, False),
+                                      (256, True), (512, False), (512, True), (512, True)]):
+        layers.append(Conv2d(s, cin, cout, 3, 1, 1, rng=rng, name=f"conv{i + 1}", bias=False, **kw))
+        if pool:
+            layers.append(AvgPool2d(2))
+        layers.append(ReLU())
+        cin = cout
+    layers += [Flatten(), Linear(s, 512, 256, rng=rng, name="fc1", **kw), ReLU(),
+               Linear(s, 256, 256, rng=rng, name="fc2", **kw), ReLU(),
+               Linear(s, 256, 10, rng=rng, name="fc3", **kw)]
+    return Model(layers)
 
 
 def simple_mlp(s, seed=7, frac=23):

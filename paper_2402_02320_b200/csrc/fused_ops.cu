@@ -36,6 +36,10 @@ struct Tape {
 #define MPX_CMP_MINB 6  // 80 regs: 1.46 vs 1.63 ms (3 parties, 2^22 ReLU)
 #endif
 
+#ifndef MPX_LOG_MINB
+#define MPX_LOG_MINB 6  // 80 regs, 6 blocks: 8.95 vs 9.34 ms at 2^24
+#endif
+
 #ifndef MPX_PREFETCH_DIST
 #define MPX_PREFETCH_DIST 0
 #endif
@@ -637,7 +641,7 @@ __global__ void __launch_bounds__(128) k_attexp_fused(u64* __restrict__ y, const
 // Logarithm, paper Alg. 3 without the big-input pre-shift (nonlinear.py:216-267)
 
 template <int L>
-__global__ void __launch_bounds__(128) k_log_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
+__global__ void __launch_bounds__(128, MPX_LOG_MINB) k_log_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
                                                    const __grid_constant__ Tape tape, FusedParams P) {
   const int w = P.w, p = P.p, p0 = P.p0;
   const u64 msk = ring_mask(w);

@@ -174,18 +174,17 @@ extern "C" int mpx_ring_add_rowvec(uint64_t* z, const uint64_t* b, int L, int64_
   return launch_status();
 }
 
-// k x k window sums with stride k over [planes][H][W] -> [planes][H/k][W/k]
-// (average pooling before its power-of-two truncation).
+// k x k window sums with stride st over [planes][H][W] -> [planes][OH][OW],
+// OH = (H - k) / st + 1 (average pooling before its scaling).
 __global__ void k_ring_pool_sum(u64* __restrict__ out, const u64* __restrict__ x, i64 planes, int H, int W,
-                                int k, u64 msk) {
-  const int OH = H / k, OW = W / k;
+                                int k, int st, int OH, int OW, u64 msk) {
   const i64 n = planes * OH * OW;
   GRID_STRIDE(i, n) {
     const int oj = (int)(i % OW);
     const i64 t = i / OW;
     const int oi = (int)(t % OH);
     const i64 p = t / OH;
-    const u64* src = x + (p * H + (i64)oi * k) * W + (i64)oj * k;
+    const u64* src = x + (p * H + (i64)oi * st) * W + (i64)oj * st;
     u64 acc = 0;
     for (int a = 0; a < k; ++a)
       for (int b = 0; b < k; ++b) acc += src[(i64)a * W + b];
@@ -194,13 +193,51 @@ __global__ void k_ring_pool_sum(u64* __restrict__ out, const u64* __restrict__ x
 }
 
 extern "C" int mpx_ring_pool_sum(uint64_t* out, const uint64_t* x, int64_t planes, int64_t H, int64_t W,
-                                 int64_t k, int width, void* stream) {
-  CHECK_ARG(out && x && planes >= 0 && k >= 1 && H % k == 0 && W % k == 0 && H < (1 << 20) && W < (1 << 20) &&
-            width >= 1 && width <= 64);
-  const i64 n = planes * (H / k) * (W / k);
+                                 int64_t k, int64_t stride, int width, void* stream) {
+  CHECK_ARG(out && x && planes >= 0 && k >= 1 && stride >= 1 && H >= k && W >= k && H < (1 << 20) &&
+            W < (1 << 20) && width >= 1 && width <= 64);
+  const int OH = (int)((H - k) / stride + 1), OW = (int)((W - k) / stride + 1);
+  const i64 n = planes * OH * OW;
   if (n == 0) return MPX_OK;
   k_ring_pool_sum<<<grid_for(n), MPX_THREADS, 0, (cudaStream_t)stream>>>(out, x, planes, (int)H, (int)W, (int)k,
-                                                                          ring_mask(width));
+                                                                          (int)stride, OH, OW, ring_mask(width));
+  return launch_status();
+}
+
+// Adjoint of the window sum: dx[p][h][w] = sum of d over the windows that
+// cover (h, w) (average-pool backward, overlapping windows allowed).
+__global__ void k_ring_pool_scatter(u64* __restrict__ dx, const u64* __restrict__ d, i64 planes, int H, int W,
+                                    int k, int st, int OH, int OW, u64 msk) {
+  const i64 n = planes * H * W;
+  GRID_STRIDE(i, n) {
+    const int w = (int)(i % W);
+    const i64 t = i / W;
+    const int h = (int)(t % H);
+    const i64 p = t / H;
+    // windows oi with oi*st <= h < oi*st + k
+    const int oi_hi = min(OH - 1, h / st), oj_hi = min(OW - 1, w / st);
+    const int oi_lo = max(0, (h - k + st) / st), oj_lo = max(0, (w - k + st) / st);
+    u64 acc = 0;
+    for (int oi = oi_lo; oi <= oi_hi; ++oi) {
+      if (h >= oi * st + k) continue;
+      for (int oj = oj_lo; oj <= oj_hi; ++oj) {
+        if (w >= oj * st + k) continue;
+        acc += d[(p * OH + oi) * OW + oj];
+      }
+    }
+    dx[i] = acc & msk;
+  }
+}
+
+extern "C" int mpx_ring_pool_scatter(uint64_t* dx, const uint64_t* d, int64_t planes, int64_t H, int64_t W,
+                                     int64_t k, int64_t stride, int width, void* stream) {
+  CHECK_ARG(dx && d && planes >= 0 && k >= 1 && stride >= 1 && H >= k && W >= k && H < (1 << 20) &&
+            W < (1 << 20) && width >= 1 && width <= 64);
+  const int OH = (int)((H - k) / stride + 1), OW = (int)((W - k) / stride + 1);
+  const i64 n = planes * H * W;
+  if (n == 0) return MPX_OK;
+  k_ring_pool_scatter<<<grid_for(n), MPX_THREADS, 0, (cudaStream_t)stream>>>(dx, d, planes, (int)H, (int)W, (int)k,
+                                                                              (int)stride, OH, OW, ring_mask(width));
   return launch_status();
 }
 

@@ -401,11 +401,18 @@ def ring_colsum(out, x, L, rows, cols, width):
     return out
 
 
-def ring_pool_sum(out, x, planes, H, W, k, width):
+def ring_pool_sum(out, x, planes, H, W, k, width, stride=None):
     if _dry(out):
         return out
-    call("mpx_ring_pool_sum", ptr(out), ptr(x), planes, H, W, k, width)
+    call("mpx_ring_pool_sum", ptr(out), ptr(x), planes, H, W, k, k if stride is None else stride, width)
     return out
+
+
+def ring_pool_scatter(dx, d, planes, H, W, k, stride, width):
+    if _dry(dx):
+        return dx
+    call("mpx_ring_pool_scatter", ptr(dx), ptr(d), planes, H, W, k, stride, width)
+    return dx
 
 
 def ring_add_rowvec(z, b, L, rows, cols, shift, width):

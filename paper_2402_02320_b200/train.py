@@ -31,7 +31,7 @@ import torch
 
 from . import kernels as K
 from .nn import softmax
-from .protocols import batch_matmul, bit2a, gt, mul, truncate
+from .protocols import batch_matmul, bit2a, gt, mul, scale_fixed, truncate
 from .sharing import AShare, public_ashare
 
 
@@ -70,8 +70,8 @@ def _trunc_bias_out(s, z: AShare, b: AShare, p: int, B: int, S: int, nchw: bool,
     w = z.width
     out = s.alloc((s.L,) + tuple(out_shape))
     (lo, lo_ps), (hi, hi_ps) = _trunc_takes(s, z.size, p, w)
-    K.trunc_rows_bias(out, z.values, b.values.contiguous(), p, lo, lo_ps, hi, hi_ps, s.L, B, S, z.shape[-1], nchw,
-                      w, p, 1 << (w - 2), 1 << (w - 2 - p), s.p0)
+    K.trunc_rows_bias(out, z.values, b.values.contiguous() if b is not None else None, p, lo, lo_ps, hi, hi_ps, s.L,
+                      B, S, z.shape[-1], nchw, w, p, 1 << (w - 2), 1 << (w - 2 - p), s.p0)
     return AShare(out, w, z.frac - p, s.parties)
 
 
@@ -103,13 +103,14 @@ class Layer:
 class Conv2d(Layer):
     """(C_in -> C_out, K x K, stride, pad); weight matrix (C_in*K*K, C_out)."""
 
-    def __init__(self, session, cin, cout, k, stride=1, pad=0, *, rng, name, spec: InitSpec):
+    def __init__(self, session, cin, cout, k, stride=1, pad=0, *, rng, name, spec: InitSpec, bias: bool = True):
         self.cin, self.cout, self.k, self.stride, self.pad = cin, cout, k, stride, pad
         self.p = spec.frac
         fan_in = cin * k * k
         self.W = session.share_fixed(_kaiming(rng, fan_in, (fan_in, cout)), spec.width, spec.frac,
                                      _key(spec, name + ".W"))
-        self.b = session.share_fixed(np.zeros(cout), spec.width, spec.frac, _key(spec, name + ".b"))
+        if bias:
+            self.b = session.share_fixed(np.zeros(cout), spec.width, spec.frac, _key(spec, name + ".b"))
 
     def forward(self, s, x: AShare) -> AShare:
         B, C, H, W = x.shape
@@ -122,9 +123,10 @@ class Conv2d(Layer):
         self.in_shape = (B, C, H, W)
         z = batch_matmul(s, [(self.cols, self.W)])[0]
         self.out_hw = (OH, OW)
+        b = getattr(self, "b", None)
         if _fused_layer(s):
-            return _trunc_bias_out(s, z, self.b, self.p, B, OH * OW, True, (B, self.cout, OH, OW))
-        z = truncate(s, _add_bias(s, z, self.b, self.p), self.p)
+            return _trunc_bias_out(s, z, b, self.p, B, OH * OW, True, (B, self.cout, OH, OW))
+        z = truncate(s, _add_bias(s, z, b, self.p) if b is not None else z, self.p)
         v = z.values.view(s.L, B, OH, OW, self.cout).permute(0, 1, 4, 2, 3).contiguous()
         return AShare(v, z.width, z.frac, s.parties)
 
@@ -137,7 +139,9 @@ class Conv2d(Layer):
         if need_dx:
             pairs.append((dz, _transpose(self.W)))
         outs = batch_matmul(s, pairs)
-        self.gW, self.gb = outs[0], _colsum(s, dz)
+        self.gW = outs[0]
+        if hasattr(self, "b"):
+            self.gb = _colsum(s, dz)
         if not need_dx:
             return None
         dcols = truncate(s, outs[1], self.p)
@@ -147,32 +151,45 @@ class Conv2d(Layer):
 
     def step(self, s, shift: int) -> None:
         self.W = self.W - truncate(s, self.gW, self.p + shift, out_frac=self.p)
-        self.b = self.b - truncate(s, self.gb, shift, out_frac=self.p)
+        if hasattr(self, "b"):
+            self.b = self.b - truncate(s, self.gb, shift, out_frac=self.p)
 
 
 class AvgPool2d(Layer):
-    """Average pool with a power-of-two window (k x k, stride k)."""
+    """k x k average pool, stride st (default k; PAPER.md:1348-1458 uses 3x3/2
+    and 2x2/1 too): window sum, then / k^2 as a truncation by log2(k^2) for
+    power-of-two windows, else a public fixed-point 1/k^2 scale + truncation
+    by p. Backward: the same scaling of dy, scattered over the windows."""
 
-    def __init__(self, k: int = 2):
+    def __init__(self, k: int = 2, stride: int | None = None):
         self.k = k
-        self.shift = int(round(math.log2(k * k)))
-        if (1 << self.shift) != k * k:
-            raise ValueError("AvgPool2d needs a power-of-two window area")
+        self.st = k if stride is None else stride
+        area = k * k
+        self.shift = area.bit_length() - 1 if area & (area - 1) == 0 else None
+
+    def _scale(self, s, v: AShare) -> AShare:
+        if self.shift is not None:
+            return truncate(s, v, self.shift, out_frac=v.frac)
+        return truncate(s, scale_fixed(s, v, 1.0 / (self.k * self.k)), v.frac)
+
+    def _out_hw(self, H, W):
+        return (H - self.k) // self.st + 1, (W - self.k) // self.st + 1
 
     def forward(self, s, x: AShare) -> AShare:
         B, C, H, W = x.shape
-        k = self.k
-        out = s.alloc((s.L, B, C, H // k, W // k))
-        K.ring_pool_sum(out, x.values.contiguous(), s.L * B * C, H, W, k, x.width)
+        OH, OW = self._out_hw(H, W)
+        out = s.alloc((s.L, B, C, OH, OW))
+        K.ring_pool_sum(out, x.values.contiguous(), s.L * B * C, H, W, self.k, x.width, stride=self.st)
         self.in_shape = (B, C, H, W)
-        return truncate(s, AShare(out, x.width, x.frac, s.parties), self.shift, out_frac=x.frac)
+        return self._scale(s, AShare(out, x.width, x.frac, s.parties))
 
     rows_out = False   # set by Model when a Conv2d precedes: emit the conv's row layout
 
     def backward(self, s, dy: AShare, need_dx: bool = True) -> AShare:
         B, C, H, W = self.in_shape
         k = self.k
-        if self.rows_out and _fused_layer(s):
+        if self.rows_out and _fused_layer(s) and self.shift is not None and self.st == k \
+                and H % k == 0 and W % k == 0:
             z = s.alloc((s.L, B * H * W, C))
             (lo, lo_ps), (hi, hi_ps) = _trunc_takes(s, dy.size, self.shift, dy.width)
             w = dy.width
@@ -181,9 +198,10 @@ class AvgPool2d(Layer):
             # logical NCHW view of the row-layout buffer: the conv backward's
             # permute back to rows is then free
             return AShare.strided(z.view(s.L, B, H, W, C).permute(0, 1, 4, 2, 3), w, dy.frac, s.parties)
-        d = truncate(s, dy, self.shift, out_frac=dy.frac)
-        v = d.values.view(s.L, B, C, H // k, 1, W // k, 1).expand(s.L, B, C, H // k, k, W // k, k)
-        return AShare(v.reshape(s.L, B, C, H, W).contiguous(), d.width, d.frac, s.parties)
+        d = self._scale(s, dy)
+        dx = s.alloc((s.L, B, C, H, W))
+        K.ring_pool_scatter(dx, d.values.contiguous(), s.L * B * C, H, W, k, self.st, d.width)
+        return AShare(dx, d.width, d.frac, s.parties)
 
 
 class ReLU(Layer):
@@ -216,30 +234,35 @@ class Flatten(Layer):
 
 
 class Linear(Layer):
-    def __init__(self, session, fin, fout, *, rng, name, spec: InitSpec):
+    def __init__(self, session, fin, fout, *, rng, name, spec: InitSpec, bias: bool = True):
         self.p = spec.frac
         self.W = session.share_fixed(_kaiming(rng, fin, (fin, fout)), spec.width, spec.frac,
                                      _key(spec, name + ".W"))
-        self.b = session.share_fixed(np.zeros(fout), spec.width, spec.frac, _key(spec, name + ".b"))
+        if bias:
+            self.b = session.share_fixed(np.zeros(fout), spec.width, spec.frac, _key(spec, name + ".b"))
 
     def forward(self, s, x: AShare) -> AShare:
         self.x = x
         z = batch_matmul(s, [(x, self.W)])[0]
+        b = getattr(self, "b", None)
         if _fused_layer(s):
-            return _trunc_bias_out(s, z, self.b, self.p, z.shape[0], 1, False, z.shape)
-        return truncate(s, _add_bias(s, z, self.b, self.p), self.p)
+            return _trunc_bias_out(s, z, b, self.p, z.shape[0], 1, False, z.shape)
+        return truncate(s, _add_bias(s, z, b, self.p) if b is not None else z, self.p)
 
     def backward(self, s, dy: AShare, need_dx: bool = True) -> AShare | None:
         pairs = [(_transpose(self.x), dy)]
         if need_dx:
             pairs.append((dy, _transpose(self.W)))
         outs = batch_matmul(s, pairs)
-        self.gW, self.gb = outs[0], _colsum(s, dy)
+        self.gW = outs[0]
+        if hasattr(self, "b"):
+            self.gb = _colsum(s, dy)
         return truncate(s, outs[1], self.p) if need_dx else None
 
     def step(self, s, shift: int) -> None:
         self.W = self.W - truncate(s, self.gW, self.p + shift, out_frac=self.p)
-        self.b = self.b - truncate(s, self.gb, shift, out_frac=self.p)
+        if hasattr(self, "b"):
+            self.b = self.b - truncate(s, self.gb, shift, out_frac=self.p)
 
 
 def _key(spec: InitSpec, label: str):
@@ -250,6 +273,10 @@ def _key(spec: InitSpec, label: str):
 
 class Model:
     """Sequential secure model with a softmax-cross-entropy head."""
+
+    @property
+    def n_params(self) -> int:
+        return sum(getattr(layer, nm).size for layer in self.layers for nm in ("W", "b") if hasattr(layer, nm))
 
     def __init__(self, layers):
         self.layers = list(layers)
@@ -286,8 +313,8 @@ def _sgd(s, layers, shift: int) -> None:
     """W -= trunc(dW_2p, p + shift), b -= trunc(db, shift) for every layer.
     Sim mode: all truncations in ONE launch (mpx_trunc_sub_multi), same
     material order, rounds and ledger as the per-layer path (derived.py:20-70)."""
-    jobs = [(layer, nm, g, f) for layer in layers if hasattr(layer, "W")
-            for nm, g, f in (("W", layer.gW, layer.p + shift), ("b", layer.gb, shift))]
+    jobs = [(layer, nm, getattr(layer, g), f) for layer in layers if hasattr(layer, "W")
+            for nm, g, f in (("W", "gW", layer.p + shift), ("b", "gb", shift)) if hasattr(layer, nm)]
     if not (s.fused and getattr(s, "fuse_ops", True) and jobs and len(jobs) <= K.TRUNC_JOBS_MAX and s.L <= 16
             and all(g.width == 64 for _, _, g, _ in jobs)):
         for layer in layers:
@@ -316,12 +343,50 @@ def _sgd(s, layers, shift: int) -> None:
 
 
 def lenet(session, spec: InitSpec = InitSpec()) -> Model:
-    """Paper Table 'LeNet': conv(20,5x5) pool ReLU conv(50,5x5) pool ReLU FC800x500 ReLU FC500x10."""
+    """Paper Table 'LeNet': conv(20,5x5) pool ReLU conv(50,5x5) pool ReLU FC800x500 ReLU
+    FC500x10 — 430,500 weights, no biases (the table's count)."""
     rng = np.random.default_rng(spec.seed)
-    return Model([Conv2d(session, 1, 20, 5, rng=rng, name="conv1", spec=spec), AvgPool2d(2), ReLU(),
-                  Conv2d(session, 20, 50, 5, rng=rng, name="conv2", spec=spec), AvgPool2d(2), ReLU(), Flatten(),
-                  Linear(session, 800, 500, rng=rng, name="fc1", spec=spec), ReLU(),
-                  Linear(session, 500, 10, rng=rng, name="fc2", spec=spec)])
+    kw = dict(rng=rng, spec=spec, bias=False)
+    return Model([Conv2d(session, 1, 20, 5, name="conv1", **kw), AvgPool2d(2), ReLU(),
+                  Conv2d(session, 20, 50, 5, name="conv2", **kw), AvgPool2d(2), ReLU(), Flatten(),
+                  Linear(session, 800, 500, name="fc1", **kw), ReLU(),
+                  Linear(session, 500, 10, name="fc2", **kw)])
+
+
+def alexnet(session, spec: InitSpec = InitSpec()) -> Model:
+    """Paper Table 'AlexNet' on CIFAR-10 3x32x32: 2,552,874
+    parameters = bias-free convolutions + fully-connected layers with bias."""
+    rng = np.random.default_rng(spec.seed)
+    kw = dict(rng=rng, spec=spec)
+    return Model([Conv2d(session, 3, 96, 11, 4, 9, name="conv1", bias=False, **kw), AvgPool2d(3, 2), ReLU(),
+                  Conv2d(session, 96, 256, 5, 1, 1, name="conv2", bias=False, **kw), AvgPool2d(2, 1), ReLU(),
+                  Conv2d(session, 256, 384, 3, 1, 1, name="conv3", bias=False, **kw), ReLU(),
+                  Conv2d(session, 384, 256, 3, 1, 1, name="conv4", bias=False, **kw), ReLU(), Flatten(),
+                  Linear(session, 256, 256, name="fc1", **kw), ReLU(),
+                  Linear(session, 256, 256, name="fc2", **kw), ReLU(),
+                  Linear(session, 256, 10, name="fc3", **kw)])
+
+
+def vgg16m(session, spec: InitSpec = InitSpec(frac=26)) -> Model:
+    """Paper Table 'VGG16m' on CIFAR-10 3x32x32, p = 26:
+    nine bias-free 3x3 convolutions with five 2x2 average pools, three
+    fully-connected layers with bias — 7,242,442 parameters as the table's
+    layer list gives them (its caption says 7,439,306; the listed layers do
+    not reach that count with or without biases)."""
+    rng = np.random.default_rng(spec.seed)
+    kw = dict(rng=rng, spec=spec)
+    layers, cin = [], 3
+    for i, (cout, pool) in enumerate([(64, False), (64, True), (128, False), (128, True), (256, False),
+                                      (256, True), (512, False), (512, True), (512, True)]):
+        layers.append(Conv2d(session, cin, cout, 3, 1, 1, name=f"conv{i + 1}", bias=False, **kw))
+        if pool:
+            layers.append(AvgPool2d(2))
+        layers.append(ReLU())
+        cin = cout
+    layers += [Flatten(), Linear(session, 512, 256, name="fc1", **kw), ReLU(),
+               Linear(session, 256, 256, name="fc2", **kw), ReLU(),
+               Linear(session, 256, 10, name="fc3", **kw)]
+    return Model(layers)
 
 
 def simple_mlp(session, spec: InitSpec = InitSpec()) -> Model:

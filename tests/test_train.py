@@ -31,19 +31,21 @@ def _data(B, shape, seed=3):
     return x, y
 
 
-def _gpu_lenet_step(s, x, y, B, lr_shift=5):
+def _gpu_lenet_step(s, x, y, B, lr_shift=5, arch="lenet"):
     from paper_2402_02320_b200 import train
-    model = train.lenet(s)
-    xs = s.share_fixed(x, 64, 23, _key("x"))
-    ys = s.share_fixed(y, 64, 23, _key("y"))
+    model = getattr(train, arch)(s)
+    p = model.layers[0].p
+    xs = s.share_fixed(x, 64, p, _key("x"))
+    ys = s.share_fixed(y, 64, p, _key("y"))
     logits = model.train_step(s, xs, ys, lr_shift)
     return model, logits
 
 
-def _oracle_lenet_step(s, x, y, B, lr_shift=5):
-    model = OT.lenet(s)
-    xs = OT.share_fixed(s, x, 64, 23, _key("x"))
-    ys = OT.share_fixed(s, y, 64, 23, _key("y"))
+def _oracle_lenet_step(s, x, y, B, lr_shift=5, arch="lenet"):
+    model = getattr(OT, arch)(s)
+    p = model.layers[0].p
+    xs = OT.share_fixed(s, x, 64, p, _key("x"))
+    ys = OT.share_fixed(s, y, 64, p, _key("y"))
     logits = model.train_step(s, xs, ys, lr_shift)
     return model, logits
 
@@ -79,6 +81,47 @@ def test_lenet_step_bit_exact_vs_oracle(n):
     gm, gl = _gpu_lenet_step(s, x, y, B)
     torch.cuda.synchronize()
     (om, ol), _ = O.simulate(lambda so: _oracle_lenet_step(so, x, y, B), n, 11)
+    assert np.array_equal(gl.values.cpu().numpy().view(np.uint64), ol.values)
+    for gl_, ol_ in zip(gm.layers, om.layers):
+        for attr in ("W", "b"):
+            if hasattr(ol_, attr):
+                assert np.array_equal(getattr(gl_, attr).values.cpu().numpy().view(np.uint64),
+                                      getattr(ol_, attr).values), (type(ol_).__name__, attr)
+
+
+@pytest.mark.parametrize("arch", ["alexnet", "vgg16m"])
+def test_cifar_nets_dry_run_match_oracle_ledger(arch):
+    """configs[2] networks: exact material demand and ledger of one step."""
+    from paper_2402_02320_b200.preprocessing import DemandCounter
+    from paper_2402_02320_b200.session import SimSession, demands_by_name
+    B, n = 2, 2
+    x, y = _data(B, (3, 32, 32))
+    c = DemandCounter(tuple(range(n)), n)
+    s = SimSession(n, c)
+    _gpu_lenet_step(s, x, y, B, arch=arch)
+    od = O.Sim(n, O.Demand(n))
+    _oracle_lenet_step(od, x, y, B, arch=arch)
+    assert demands_by_name(c) == dict(sorted(od.store.demands.items()))
+    assert s.metrics.total.as_dict() == od.ledger.total.as_dict()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("arch", ["alexnet", "vgg16m"])
+def test_cifar_net_step_bit_exact_vs_oracle(arch):
+    """configs[2] AlexNet / VGG16m training step (overlapping 3x3/2 and 2x2/1
+    average pools, padded strided convolutions) bit-exact vs the oracle."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2402_02320_b200.preprocessing import DemandCounter, device_store
+    from paper_2402_02320_b200.session import SimSession
+    B, n = 2, 2
+    x, y = _data(B, (3, 32, 32))
+    c = DemandCounter(tuple(range(n)), n)
+    _gpu_lenet_step(SimSession(n, c), x, y, B, arch=arch)
+    s = SimSession(n, device_store(11, n, c.demands, needs_bits=c.needs_bits))
+    gm, gl = _gpu_lenet_step(s, x, y, B, arch=arch)
+    torch.cuda.synchronize()
+    (om, ol), _ = O.simulate(lambda so: _oracle_lenet_step(so, x, y, B, arch=arch), n, 11)
     assert np.array_equal(gl.values.cpu().numpy().view(np.uint64), ol.values)
     for gl_, ol_ in zip(gm.layers, om.layers):
         for attr in ("W", "b"):
