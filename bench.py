@@ -593,6 +593,45 @@ def mlp_entry(torch, dev, steps, warmup):
             "steps_per_s": 1e3 / ms, "cuda_graph": True}
 
 
+def cifar_entry(torch, dev, arch, steps, warmup, n=2):
+    """configs[2]: AlexNet / VGG16m training step (paper tables) on a synthetic
+    CIFAR-10-shape batch of 128, n parties simulated on one GPU, CUDA graph."""
+    from paper_2402_02320_b200 import train
+    from paper_2402_02320_b200.preprocessing import DemandCounter, device_store
+    from paper_2402_02320_b200.session import SimSession
+    rng = np.random.default_rng(6)
+    x, y = rng.uniform(0, 1, (BATCH, 3, 32, 32)), np.eye(10)[rng.integers(0, 10, BATCH)]
+    build = getattr(train, arch)
+    c = DemandCounter(tuple(range(n)), n)
+    sd = SimSession(n, c, device=dev)
+    md = build(sd)
+    p = md.layers[0].p
+    md.train_step(sd, sd.share_fixed(x, WIDTH, p, [2, 1]), sd.share_fixed(y, WIDTH, p, [2, 2]), LR_SHIFT)
+    s = SimSession(n, None, device=dev)
+    m = build(s)
+    g = train.GraphedStep(s, m, s.share_fixed(x, WIDTH, p, [2, 1]), s.share_fixed(y, WIDTH, p, [2, 2]),
+                          LR_SHIFT, c.demands, c.needs_bits, seed0=80)
+    times, deal = [], []
+    for t in range(warmup + steps):
+        t0 = time.perf_counter()
+        device_store(81 + t, n, c.demands, device=dev, needs_bits=c.needs_bits, into=s.store)
+        torch.cuda.synchronize()
+        deal.append(1e3 * (time.perf_counter() - t0))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        if t >= warmup:
+            times.append(e0.elapsed_time(e1))
+    ms = float(np.mean(times))
+    mat = sum(t.numel() * t.element_size() for d in s.store._arrays.values() for t in d.values())
+    return {"model": arch, "params": m.n_params, "parties": n, "batch": BATCH, "frac": p, "ms_per_step": ms,
+            "steps_per_s": 1e3 / ms, "rounds_per_step": sd.metrics.total.rounds,
+            "material_GB_per_step": mat / 1e9, "dealer_ms_per_step": float(np.median(deal[warmup:])),
+            "cuda_graph": True}
+
+
 def transformer_entry(torch, dev, steps, warmup):
     """configs[3]: 18.9M-parameter Transformer secure inference, seq 128, p = 14,
     2 parties on one GPU, forward captured in one CUDA graph. Latency per
@@ -794,6 +833,8 @@ def run_b200(args, group=None):
         if world == 1:
             sweep["mlp_train"] = mlp_entry(torch, dev, 5, 3)
             sweep["transformer"] = transformer_entry(torch, dev, 3, 2)
+            for arch in ("alexnet", "vgg16m"):
+                sweep[f"{arch}_train"] = cifar_entry(torch, dev, arch, 3, 2)
 
     line = None
     if rank == 0:

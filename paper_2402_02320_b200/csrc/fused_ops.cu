@@ -232,10 +232,16 @@ __device__ __forceinline__ void d_carry_level(u64 (&G)[L], u64 (&P)[L], int m, i
 template <int L>
 __device__ __forceinline__ void d_carry_sum(u64 (&G)[L], u64 (&P)[L], const u64 (&P0)[L], int m, const Tape& tape,
                                             int& ti, i64 e, int p0, Sh<L>& out) {
-  // levels s = 1, 2, 4, ... < m, unrolled (m <= 64; the guard is uniform)
+  // levels s = 1, 2, 4, ... < m, unrolled; the 64-bit ring gets its own
+  // constant-m copy (measured 7.7 vs 8.9 ms for the 2^24 Reciprocal)
+  if (m == 64) {
 #pragma unroll
-  for (int s = 1; s < 64; s *= 2)
-    if (s < m) d_carry_level<L>(G, P, m, s, next_take<L>(tape, ti, e), e, p0);
+    for (int s = 1; s < 64; s *= 2) d_carry_level<L>(G, P, 64, s, next_take<L>(tape, ti, e), e, p0);
+  } else {
+#pragma unroll
+    for (int s = 1; s < 64; s *= 2)
+      if (s < m) d_carry_level<L>(G, P, m, s, next_take<L>(tape, ti, e), e, p0);
+  }
 #pragma unroll
   for (int l = 0; l < L; ++l) out.v[l] = (P0[l] ^ (G[l] << 1)) & low_bits(m);
 }
@@ -295,9 +301,14 @@ __device__ __forceinline__ Sh<L> d_lmo(const Sh<L>& bits, int m, const Tape& tap
   u64 Y[L];
 #pragma unroll
   for (int l = 0; l < L; ++l) Y[l] = bits.v[l];
+  if (m == 63) {
 #pragma unroll
-  for (int s = 1; s < 64; s *= 2)
-    if (s < m) d_lmo_level<L>(Y, m, s, next_take<L>(tape, ti, e), e, p0);
+    for (int s = 1; s < 63; s *= 2) d_lmo_level<L>(Y, 63, s, next_take<L>(tape, ti, e), e, p0);
+  } else {
+#pragma unroll
+    for (int s = 1; s < 64; s *= 2)
+      if (s < m) d_lmo_level<L>(Y, m, s, next_take<L>(tape, ti, e), e, p0);
+  }
   Sh<L> o;
 #pragma unroll
   for (int l = 0; l < L; ++l) o.v[l] = Y[l] ^ (Y[l] >> 1);

@@ -21,8 +21,8 @@ def main():
     ap.add_argument("--graph", action="store_true")
     a = ap.parse_args()
     n, B = a.parties, a.batch
-    shape = (1, 28, 28) if a.model == "lenet" else (784,)
-    build = train.lenet if a.model == "lenet" else train.simple_mlp
+    shape = {"lenet": (1, 28, 28), "mlp": (784,), "alexnet": (3, 32, 32), "vgg16m": (3, 32, 32)}[a.model]
+    build = {"lenet": train.lenet, "mlp": train.simple_mlp, "alexnet": train.alexnet, "vgg16m": train.vgg16m}[a.model]
     rng = np.random.default_rng(0)
     x = rng.uniform(0, 1, (B,) + shape)
     y = np.eye(10)[rng.integers(0, 10, B)]
@@ -30,11 +30,12 @@ def main():
     sd = SimSession(n, c)
     m = build(sd)
     t0 = time.perf_counter()
-    m.train_step(sd, sd.share_fixed(x, 64, 23, [1, 2]), sd.share_fixed(y, 64, 23, [3, 4]), 5)
+    p = m.layers[0].p
+    m.train_step(sd, sd.share_fixed(x, 64, p, [1, 2]), sd.share_fixed(y, 64, p, [3, 4]), 5)
     dry_s = time.perf_counter() - t0
     s = SimSession(n, None)
     model = build(s)
-    xs, ys = s.share_fixed(x, 64, 23, [1, 2]), s.share_fixed(y, 64, 23, [3, 4])
+    xs, ys = s.share_fixed(x, 64, p, [1, 2]), s.share_fixed(y, 64, p, [3, 4])
     times, deal, host = [], [], []
     if a.graph:
         g = train.GraphedStep(s, model, xs, ys, 5, c.demands, c.needs_bits, seed0=50)
@@ -74,7 +75,8 @@ def main():
         if t:
             times.append(e0.elapsed_time(e1))
             host.append((h1 - h0) * 1e3)
-    out = {"graph": a.graph, "model": a.model, "parties": n, "batch": B, "ms_per_step": float(np.mean(times)),
+    mat = sum(t.numel() * t.element_size() for d in s.store._arrays.values() for t in d.values())
+    out = {"material_GB": mat / 1e9, "params": model.n_params, "graph": a.graph, "model": a.model, "parties": n, "batch": B, "ms_per_step": float(np.mean(times)),
            "steps_per_s": 1e3 / float(np.mean(times)), "host_issue_ms": float(np.mean(host)),
            "dealer_ms": 1e3 * float(np.mean(deal[1:])), "dry_run_s": dry_s,
            "rounds_per_step": s.metrics.total.rounds // max(1, a.steps + 1),
