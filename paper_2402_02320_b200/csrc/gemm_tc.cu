@@ -18,6 +18,7 @@
 // Operand tiles are TMA-loaded with 128-byte swizzle; UMMA smem descriptors
 // are K-major SWIZZLE_128B.
 #include <cuda.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -335,6 +336,222 @@ __global__ void __launch_bounds__(192, BN == 32 ? 2 : 1)
 }
 
 // --------------------------------------------------------------------------
+// Persistent variant for short reductions with large outputs (conv backward
+// dX: K of one or two k-blocks, M x N in the 10^7-10^8 range). One CTA per SM
+// walks 128 x 64 output tiles blockIdx.x, +gridDim.x, ... The 8 diagonal
+// accumulators take all 512 TMEM columns, so instead of double-buffering TMEM
+// the epilogue drains them into shared memory right away and hands TMEM back
+// (tmem_empty) before its slow part — the C-addend loads and the coalesced
+// global stores — which then overlaps the next tile's TMA loads and MMAs.
+#define TCP_BN 64
+#define TCP_AST 4
+#define TCP_BST 1
+#define TCP_STAGE_BYTES (4 * 2 * 32 * 33 * 8)
+constexpr int tcp_smem_bytes() {
+  return TCP_AST * TC_A_TILE + TCP_BST * 8 * TCP_BN * TC_BK + TCP_STAGE_BYTES + 1024 + 256;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(192, 1)
+    k_gemm_limbs_tc_pers(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                         TcArgs args, int batch) {
+  constexpr int BN = TCP_BN, AST = TCP_AST, BST = TCP_BST;
+  constexpr int B_TILE = BN * TC_BK;
+  constexpr int B_STAGE = 8 * B_TILE;
+  constexpr uint32_t ACC_COLS = 8 * BN;  // 8 diagonals = all 512 columns
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + AST * TC_A_TILE;
+  u64* stage_all = reinterpret_cast<u64*>(sB + BST * B_STAGE);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stage_all) + TCP_STAGE_BYTES);
+  uint64_t* fullA = bars;
+  uint64_t* emptyA = bars + AST;
+  uint64_t* fullB = bars + 2 * AST;
+  uint64_t* emptyB = bars + 2 * AST + BST;
+  uint64_t* tfull = bars + 2 * AST + 2 * BST;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_holder = (uint32_t*)(tempty + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int tiles_m = args.Mpad / TC_BM, tiles_n = args.Npad / BN;
+  const int per_batch = tiles_m * tiles_n;
+  const int total = per_batch * batch;
+  const int nk = args.nk_total;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < AST; ++s) {
+      mbar_init(&fullA[s], 1);
+      mbar_init(&emptyA[s], 1);
+    }
+    for (int s = 0; s < BST; ++s) {
+      mbar_init(&fullB[s], 1);
+      mbar_init(&emptyB[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);  // one arrival per epilogue warp
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "r"(ACC_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_holder;
+
+  auto tile_coords = [&](int t, int& z, int& m0, int& n0) {
+    z = t / per_batch;
+    const int lin = t - z * per_batch;
+    const int per_group = TC_GROUP_M * tiles_n;
+    const int g = lin / per_group;
+    const int first_m = g * TC_GROUP_M;
+    const int gm = min(TC_GROUP_M, tiles_m - first_m);
+    const int in_g = lin - g * per_group;
+    m0 = (first_m + in_g % gm) * TC_BM;
+    n0 = (in_g / gm) * BN;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      int as = 0, gkb = 0;
+      uint32_t aph = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        int z, m0, n0;
+        tile_coords(t, z, m0, n0);
+        for (int kb = 0; kb < nk; ++kb, ++gkb) {
+          const int bs = gkb % BST;
+          const uint32_t bph = (uint32_t)((gkb / BST) & 1);
+          mbar_wait(&emptyB[bs], bph ^ 1);
+          mbar_expect_tx(&fullB[bs], B_STAGE);
+          for (int j = 0; j < 8; ++j)
+            tma_load_2d(sB + bs * B_STAGE + j * B_TILE, &mapB, &fullB[bs], kb * TC_BK, (z * 8 + j) * args.Npad + n0);
+          for (int i = 0; i < 8; ++i) {
+            mbar_wait(&emptyA[as], aph ^ 1);
+            mbar_expect_tx(&fullA[as], TC_A_TILE);
+            tma_load_2d(sA + as * TC_A_TILE, &mapA, &fullA[as], kb * TC_BK, (z * 8 + i) * args.Mpad + m0);
+            if (++as == AST) {
+              as = 0;
+              aph ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      const uint32_t idesc = (2u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+      const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA));
+      const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sB));
+      int as = 0, gkb = 0, it = 0;
+      uint32_t aph = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+        mbar_wait(tempty, (uint32_t)((it & 1) ^ 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int kb = 0; kb < nk; ++kb, ++gkb) {
+          const int bs = gkb % BST;
+          const uint32_t bph = (uint32_t)((gkb / BST) & 1);
+          mbar_wait(&fullB[bs], bph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t bd0 = b_desc0 + (uint64_t)((bs * B_STAGE) >> 4);
+          const uint32_t first = kb == 0 ? 0u : 1u;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            mbar_wait(&fullA[as], aph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint64_t ad = a_desc0 + (uint64_t)((as * TC_A_TILE) >> 4);
+#pragma unroll
+            for (int j = 0; j <= 7 - i; ++j) {
+              const uint32_t d_tmem = tmem_base + (uint32_t)((i + j) * BN);
+              const uint64_t bd = bd0 + (uint64_t)((j * B_TILE) >> 4);
+#pragma unroll
+              for (int kk = 0; kk < TC_BK / 32; ++kk)
+                mma_i8(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, (i > 0 || kk > 0) ? 1u : first);
+            }
+            umma_commit(&emptyA[as]);
+            if (++as == AST) {
+              as = 0;
+              aph ^= 1;
+            }
+          }
+          umma_commit(&emptyB[bs]);
+        }
+        umma_commit(tfull);
+      }
+    }
+  } else {
+    // ---------------- epilogue: warps 2..5 ----------------
+    const int sp = warp & 3;
+    u64* stage = stage_all + sp * (2 * 32 * 33);
+    int it = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+      int z, m0, n0;
+      tile_coords(t, z, m0, n0);
+      mbar_wait(tfull, (uint32_t)(it & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        u64 res[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) res[q] = 0;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+          uint32_t v[32];
+          const uint32_t taddr = tmem_base + ((uint32_t)(sp * 32) << 16) + (uint32_t)(d * BN + c * 32);
+          TMEM_LD32(taddr, v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int q = 0; q < 32; ++q) res[q] += (u64)v[q] << (8 * d);
+        }
+#pragma unroll
+        for (int q = 0; q < 32; ++q) stage[c * 32 * 33 + lane * 33 + q] = res[q];
+      }
+      // accumulators drained: the MMA warp may start the next tile
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
+      const i64 rbase = (i64)m0 + sp * 32;
+      const i64 rows = min((i64)32, (i64)args.M - rbase);
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        const int col = n0 + c * 32 + lane;
+        const int rmax = (col < args.N) ? (int)rows : 0;
+        u64* dst = args.C + (i64)z * args.sC + rbase * args.ldc + col;
+        const u64* src = args.Cin ? args.Cin + (i64)z * args.sCin + rbase * args.ldc + col
+                                  : (args.accumulate ? dst : nullptr);
+        const u64* st = stage + c * 32 * 33;
+        for (int h = 0; h < 32; h += 16) {
+          u64 add[16];
+#pragma unroll
+          for (int r = 0; r < 16; ++r) add[r] = (src && h + r < rmax) ? src[(i64)(h + r) * args.ldc] : 0ull;
+#pragma unroll
+          for (int r = 0; r < 16; ++r)
+            if (h + r < rmax) dst[(i64)(h + r) * args.ldc] = (st[(h + r) * 33 + lane] + add[r]) & args.msk;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ACC_COLS));
+  }
+}
+
+// --------------------------------------------------------------------------
 // Limb split: u64 matrix -> 8 u8 planes. `trans` = 0: plane[i][r][coff + c];
 // trans = 1: plane[i][c][coff + r] (K-major operand from a row-major KxN).
 
@@ -583,8 +800,15 @@ extern "C" int mpx_gemm_limbs(uint64_t* C, const uint8_t* A8, const uint8_t* B8,
   CHECK_ARG(batch * 8 * Mpad < (1ll << 31) && batch * 8 * Npad < (1ll << 31));
   CUtensorMap mapA, mapB;
   if (make_map(&mapA, A8, batch * 8 * Mpad, Kpad, TC_BM) != MPX_OK) return MPX_ERR_CUDA;
-  // narrow tiles when N is not a multiple of 64 or the reduction is short
-  const bool narrow = (Npad % 64 != 0) || nk_per <= 2;
+  // persistent 128x64 tiles (epilogue overlapped with the next tile) for
+  // short unsplit reductions over many output tiles; else narrow tiles when N
+  // is not a multiple of 64 or the reduction is short, wide tiles otherwise
+  const i64 ntiles64 = (Npad / 64) * (Mpad / TC_BM) * batch;
+  // (one k-block per tile leaves too little MMA work to hide the epilogue:
+  // measured slower there, faster at 2-4)
+  const bool pers = Npad % 64 == 0 && ksplit == 1 && nk_total >= 2 && nk_total <= 4 && ntiles64 >= 4 * 148 &&
+                    getenv("MPX_TC_NO_PERSIST") == nullptr;
+  const bool narrow = !pers && ((Npad % 64 != 0) || nk_per <= 2);
   const int bn = narrow ? 32 : 64;
   if (make_map(&mapB, B8, batch * 8 * Npad, Kpad, bn) != MPX_OK) return MPX_ERR_CUDA;
   static bool attr_set = false;
@@ -592,7 +816,9 @@ extern "C" int mpx_gemm_limbs(uint64_t* C, const uint8_t* A8, const uint8_t* B8,
     if (cudaFuncSetAttribute(k_gemm_limbs_tc<TC_WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              tc_smem_bytes(TC_WIDE)) != cudaSuccess ||
         cudaFuncSetAttribute(k_gemm_limbs_tc<TC_NARROW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             tc_smem_bytes(TC_NARROW)) != cudaSuccess)
+                             tc_smem_bytes(TC_NARROW)) != cudaSuccess ||
+        cudaFuncSetAttribute(k_gemm_limbs_tc_pers, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             tcp_smem_bytes()) != cudaSuccess)
       return MPX_ERR_CUDA;
     attr_set = true;
   }
@@ -611,6 +837,11 @@ extern "C" int mpx_gemm_limbs(uint64_t* C, const uint8_t* A8, const uint8_t* B8,
   a.ksplit = ksplit;
   a.accumulate = accumulate;
   a.msk = ring_mask(width);
+  if (pers) {
+    const unsigned g = (unsigned)min(ntiles64, (i64)148);
+    k_gemm_limbs_tc_pers<<<g, 192, tcp_smem_bytes(), (cudaStream_t)stream>>>(mapA, mapB, a, (int)batch);
+    return launch_status();
+  }
   dim3 grid((unsigned)((Npad / bn) * (Mpad / TC_BM) * ksplit), 1, (unsigned)batch);
   if (narrow)
     k_gemm_limbs_tc<TC_NARROW><<<grid, 192, tc_smem_bytes(TC_NARROW), (cudaStream_t)stream>>>(mapA, mapB, a);

@@ -137,3 +137,27 @@ def test_im2col_col2im(K, Bn, C, H, k, st, pd):
     dx = torch.empty((L, Bn, C, H, H), dtype=torch.int64, device="cuda")
     K.col2im(dx, _dev(g), L, Bn, C, H, H, k, st, pd, 64)
     assert np.array_equal(_host(dx), OT.col2im(g, (L, Bn, C, H, H), k, st, pd, 64))
+
+
+@pytest.mark.parametrize("M,Kd,N,b,mode", [(4000, 100, 640, 1, "cin"), (2048, 256, 300, 2, "acc"),
+                                          (1500, 64, 1000, 1, "plain")])
+def test_gemm_limbs_persistent_short_k(K, M, Kd, N, b, mode):
+    """Short-K, many-tile products run on the persistent double-buffered
+    tcgen05 kernel; exact vs numpy with each addend mode."""
+    rng = np.random.default_rng(M + N)
+    A, B, C = _rand(rng, (b, M, Kd), 64), _rand(rng, (b, Kd, N), 64), _rand(rng, (b, M, N), 64)
+    Mp, Np, Kp = K._rup(M, 128), K._rup(N, 32), K._rup(Kd, 128)
+    Ad, Bd, Cd = _dev(A), _dev(B), _dev(C)
+    A8 = torch.zeros((b, 8, Mp, Kp), dtype=torch.uint8, device="cuda")
+    B8 = torch.zeros((b, 8, Np, Kp), dtype=torch.uint8, device="cuda")
+    for z in range(b):
+        K.limb_split(A8[z], Ad.data_ptr() + 8 * z * M * Kd, M, Kd, Kd, Mp * Kp, Kp, 0, False)
+        K.limb_split(B8[z], Bd.data_ptr() + 8 * z * Kd * N, Kd, N, N, Np * Kp, Kp, 0, True)
+    Z = Cd.clone() if mode == "acc" else torch.full((b, M, N), 3, dtype=torch.int64, device="cuda")
+    K.gemm_limbs(Z, A8, B8, b, M, N, Mp, Np, Kp, N, M * N, mode == "acc", 64, ksplit=1,
+                 cin=Cd if mode == "cin" else None, s_cin=M * N)
+    got = _host(Z)
+    with np.errstate(over="ignore"):
+        for z in range(b):
+            want = _mm(A[z], B[z]) + (C[z] if mode in ("cin", "acc") else np.uint64(0))
+            assert np.array_equal(got[z], want), z

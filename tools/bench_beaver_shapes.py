@@ -13,7 +13,21 @@ LENET = [(73728, 25, 20), (25, 73728, 20), (8192, 500, 50), (500, 8192, 50), (81
          (128, 800, 500), (800, 128, 500), (128, 500, 800), (128, 500, 10), (500, 128, 10), (128, 10, 500)]
 
 
-def timeit(fn, reps=20):
+def _vgg():
+    convs = [(3, 64, 32), (64, 64, 32), (64, 128, 16), (128, 128, 16), (128, 256, 8), (256, 256, 8),
+             (256, 512, 4), (512, 512, 4), (512, 512, 2)]
+    out = []
+    for cin, cout, hw in convs:
+        m, k = 128 * hw * hw, 9 * cin
+        out += [(m, k, cout), (k, m, cout), (m, cout, k)]      # forward, dW, dX
+    return out
+
+
+REPS = [20]
+
+
+def timeit(fn, reps=None):
+    reps = reps or REPS[0]
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
@@ -29,17 +43,26 @@ def timeit(fn, reps=20):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--parties", type=int, default=3)
+    ap.add_argument("--shapes", default="lenet")
+    ap.add_argument("--no-simt", action="store_true")
+    ap.add_argument("--only", default=None, help="m,k,r")
+    ap.add_argument("--reps", type=int, default=20)
     a = ap.parse_args()
     L = a.parties
+    REPS[0] = a.reps
     out = []
-    for m, k, r in LENET:
+    shapes = _vgg() if a.shapes == "vgg" else LENET
+    if a.only:
+        shapes = [tuple(int(v) for v in a.only.split(","))]
+    for m, k, r in shapes:
         g = torch.Generator(device="cuda").manual_seed(1)
         rnd = lambda *s: torch.randint(-2**62, 2**62, s, device="cuda", generator=g)  # noqa: E731
         D, E = rnd(m, k), rnd(k, r)
         A, B, C = rnd(L, m, k), rnd(L, k, r), rnd(L, m, r)
         Z = torch.empty((L, m, r), dtype=torch.int64, device="cuda")
-        simt = timeit(lambda: K.beaver_gemm(Z, m * r, C.data_ptr(), m * r, D, E, A.data_ptr(), m * k, B.data_ptr(),
-                                            k * r, L, m, k, r, 0, 64))
+        simt = None if a.no_simt else timeit(
+            lambda: K.beaver_gemm(Z, m * r, C.data_ptr(), m * r, D, E, A.data_ptr(), m * k, B.data_ptr(),
+                                  k * r, L, m, k, r, 0, 64))
         Zs = Z.clone()
         Mp, Np, Kp = K._rup(m, 128), K._rup(r, 32), K._rup(2 * k, 128)
         A8 = torch.zeros((L, 8, Mp, Kp), dtype=torch.uint8, device="cuda")
@@ -49,8 +72,12 @@ def main():
             K.beaver_limbs(A8, B8, D, E, A.data_ptr(), m * k, B.data_ptr(), k * r, L, m, k, r, Mp, Np, Kp, 0)
             K.gemm_limbs(Z, A8, B8, L, m, r, Mp, Np, Kp, r, m * r, False, 64, cin=C, s_cin=m * r)
         t = timeit(tc)
-        same = bool(torch.equal(Z, Zs))
-        out.append({"m": m, "k": k, "r": r, "simt_us": round(simt, 1), "tc_us": round(t, 1), "equal": same})
+        same = None if simt is None else bool(torch.equal(Z, Zs))
+        lim = timeit(lambda: K.beaver_limbs(A8, B8, D, E, A.data_ptr(), m * k, B.data_ptr(), k * r, L, m, k, r, Mp,
+                                            Np, Kp, 0))
+        ops = 2 * 36 * L * Mp * Np * Kp
+        out.append({"m": m, "k": k, "r": r, "simt_us": None if simt is None else round(simt, 1), "tc_us": round(t, 1),
+                    "limbs_us": round(lim, 1), "gemm_TOPS": round(ops / ((t - lim) * 1e-6) / 1e12, 1), "equal": same})
         print(json.dumps(out[-1]), flush=True)
 
 
