@@ -303,8 +303,21 @@ def alg_bytes(name, a):
             return L * rows * cols * 8 + L * rows * 8
         if name == "mpx_bits_gather":
             return 16 * a[4]
-        if name == "mpx_gemm_limbs":     # int8 ops, not bytes: see roofline_for
+        if name in ("mpx_gemm_limbs", "mpx_gemm_limbs_split"):  # int8 ops, not bytes: see roofline_for
             return None
+        if name == "mpx_mask_limbs":
+            # X_l, T_l read once; shared S limbs + per-party T limbs written
+            L, R, Kd, Rpad, Kp = a[10], a[11], a[12], a[13], a[14]
+            return 2 * L * R * Kd * 8 + (1 + L) * 8 * Rpad * Kp
+        if name == "mpx_mask_sub_bs":
+            L, batch, n = a[7], a[8], a[9]
+            return batch * n * 8 * (2 * L + 1)
+        if name == "mpx_mask_sub_t":
+            L, batch, rows, cols = a[7], a[8], a[9], a[10]
+            return batch * rows * cols * 8 * (2 * L + 1)
+        if name == "mpx_beaver_limbs":
+            L, M, Kd, N, Mpad, Npad, Kpad = a[8], a[9], a[10], a[11], a[12], a[13], a[14]
+            return (1 + L) * 8 * (M * Kd + Kd * N) + L * 8 * (Mpad + Npad) * Kpad
         if name in ("mpx_reciprocal_fused", "mpx_exp_fused", "mpx_log_fused", "mpx_relu_fused",
                     "mpx_maxlevel_fused"):
             from paper_2402_02320_b200.fused import material_bytes
@@ -425,7 +438,7 @@ def sweep_entry(torch, G, make_session, parties, n_parties, dev, name, steps=2, 
         out["roofline"] = roofline_for(per)
     if name == "matmul":
         macs = len(parties) * D * (2 * D) * D          # [D|A_l] @ [B_l';E] per local party
-        tc_ms = prof_ms.get("mpx_gemm_limbs", 0.0)
+        tc_ms = prof_ms.get("mpx_gemm_limbs", 0.0) + prof_ms.get("mpx_gemm_limbs_split", 0.0)
         out.update({"shape": [D, D, D], "ring_GMAC_per_s": macs / (ms / 1e3) / 1e9,
                     "gemm_kernel_ms": tc_ms,
                     "gemm_int8_TOPS": 36 * 2 * macs / (tc_ms / 1e3) / 1e12 if tc_ms else None})
@@ -479,6 +492,9 @@ def _profile_kernels(prof):
         if name == "mpx_gemm_limbs":
             # (C, A8, B8, batch, M, N, Mpad, Npad, Kpad, ...): 36 limb MACs per ring MAC
             d["ops"] += 2 * 36 * a[3] * a[4] * a[5] * a[8]
+        elif name == "mpx_gemm_limbs_split":
+            # (C, PA8, SA8, PB8, SB8, batch, M, N, Mpad, Npad, Kh, ...): reduction length 2 Kh
+            d["ops"] += 2 * 36 * a[5] * a[6] * a[7] * 2 * a[10]
         b = alg_bytes(name, a)
         if b is None:
             d["bytes_known"] = False
@@ -494,7 +510,7 @@ def roofline_for(per, int8_peak=None):
     dom = per[dom_name]
     common = {"kernel": dom_name, "launches": dom["n"], "avg_launch_us": 1e3 * dom["ms"] / dom["n"],
               "share_of_step": dom["ms"] / step_ms}
-    if dom_name == "mpx_gemm_limbs":
+    if dom_name in ("mpx_gemm_limbs", "mpx_gemm_limbs_split"):
         ach = dom["ops"] / (dom["ms"] / 1e3) / 1e12
         return dict(common, bound="tensor", achieved=ach, peak=int8_peak, unit="TOPS int8",
                     peak_kind="measured in-run: torch._int_mm int8 8192^3 (cuBLASLt), burst",

@@ -42,6 +42,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src in srcs:
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        objs.append(obj)
+        hdrs = [os.path.join(HERE, "common.cuh"), os.path.join(REPO, "include", "mpx.h")]
+        if not force and os.path.exists(obj) and \
+                os.path.getmtime(obj) >= max(os.path.getmtime(p) for p in [src] + hdrs):
+            continue  # object up to date
         cmd = [nvcc(), "-c", src, "-o", obj] + flags()
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
@@ -50,7 +55,6 @@ def build(force: bool = False, verbose: bool = False) -> str:
             print(res.stderr, file=sys.stderr)
         with open(obj + ".ptxas.txt", "w") as fh:
             fh.write(res.stderr)
-        objs.append(obj)
     tmp = OUT + ".tmp"
     cmd = [nvcc(), "-shared", "-o", tmp] + objs + ["-gencode", "arch=compute_100a,code=sm_100a",
                                                    "-lcuda"]

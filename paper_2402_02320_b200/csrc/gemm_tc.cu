@@ -121,6 +121,9 @@ struct TcArgs {
   int ksplit;    // CTAs per output tile along K; > 1 => wrapping atomic adds
   int accumulate;
   u64 msk;
+  int kb_half;  // > 0: split operands (persistent kernel only): k-blocks
+                // [0, kb_half) pair shared A (mapA2) with party B (mapB),
+                // the rest party A (mapA) with shared B (mapB2)
 };
 
 template <int BN, int AST, int BST>
@@ -336,27 +339,57 @@ __global__ void __launch_bounds__(192, BN == 32 ? 2 : 1)
 }
 
 // --------------------------------------------------------------------------
-// Persistent variant for short reductions with large outputs (conv backward
-// dX: K of one or two k-blocks, M x N in the 10^7-10^8 range). One CTA per SM
-// walks 128 x 64 output tiles blockIdx.x, +gridDim.x, ... The 8 diagonal
-// accumulators take all 512 TMEM columns, so instead of double-buffering TMEM
-// the epilogue drains them into shared memory right away and hands TMEM back
-// (tmem_empty) before its slow part — the C-addend loads and the coalesced
-// global stores — which then overlaps the next tile's TMA loads and MMAs.
+// Persistent kernel: one CTA per SM walks work units u = blockIdx.x,
+// +gridDim.x, ...; a unit is one 128 x 64 output tile and one slice of its
+// k-blocks (split-K slices add their partials with wrapping 64-bit atomics,
+// exact mod 2^64). The 8 diagonal accumulators take all 512 TMEM columns, so
+// instead of double-buffering TMEM the epilogue drains them into registers
+// (a thread owns one row: 64 u64) and hands TMEM back (tempty) before its
+// global stores, which then overlap the next unit's TMA loads and MMAs.
+// A ring of 4 single-limb stages + double-buffered B stages (8 limbs each)
+// keep the tensor pipe fed across unit boundaries. N tiles of 64 also cover
+// Npad % 64 == 32: the extra 32 B rows belong to the next plane (or are
+// TMA zero-fill past the end) and only feed columns >= Npad, never stored.
 #define TCP_BN 64
 #define TCP_AST 4
-#define TCP_BST 1
-#define TCP_STAGE_BYTES (4 * 2 * 32 * 33 * 8)
-constexpr int tcp_smem_bytes() {
-  return TCP_AST * TC_A_TILE + TCP_BST * 8 * TCP_BN * TC_BK + TCP_STAGE_BYTES + 1024 + 256;
+#define TCP_BST 2
+#define TCP_STAGE_BYTES (4 * 32 * 33 * 8)
+#define TCP_STAGED_MAX_KB 4  // one 32 x 32 u64 transpose tile per epilogue warp
+constexpr int tcp_smem_bytes(bool staged) {
+  return TCP_AST * TC_A_TILE + TCP_BST * 8 * TCP_BN * TC_BK + (staged ? TCP_STAGE_BYTES : 0) + 1024 + 256;
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+struct TcpUnit {
+  int z, m0, n0, kb0, nk, ks;
+};
+
+__device__ __forceinline__ TcpUnit tcp_unit(int u, const TcArgs& a, int tiles_m, int tiles_n) {
+  TcpUnit t;
+  t.ks = u % a.ksplit;
+  const int lin_all = u / a.ksplit;
+  const int per_batch = tiles_m * tiles_n;
+  t.z = lin_all / per_batch;
+  const int lin = lin_all - t.z * per_batch;
+  const int per_group = TC_GROUP_M * tiles_n;
+  const int g = lin / per_group;
+  const int first_m = g * TC_GROUP_M;
+  const int gm = min(TC_GROUP_M, tiles_m - first_m);
+  const int in_g = lin - g * per_group;
+  t.m0 = (first_m + in_g % gm) * TC_BM;
+  t.n0 = (in_g / gm) * TCP_BN;
+  t.kb0 = t.ks * a.nk;
+  t.nk = min(a.nk, a.nk_total - t.kb0);
+  return t;
+}
+
+template <bool STAGED>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_limbs_tc_pers(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                         const __grid_constant__ CUtensorMap mapA2, const __grid_constant__ CUtensorMap mapB2,
                          TcArgs args, int batch) {
   constexpr int BN = TCP_BN, AST = TCP_AST, BST = TCP_BST;
   constexpr int B_TILE = BN * TC_BK;
@@ -367,7 +400,8 @@ __global__ void __launch_bounds__(192, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + AST * TC_A_TILE;
   u64* stage_all = reinterpret_cast<u64*>(sB + BST * B_STAGE);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stage_all) + TCP_STAGE_BYTES);
+  uint64_t* bars =
+      reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stage_all) + (STAGED ? TCP_STAGE_BYTES : 0));
   uint64_t* fullA = bars;
   uint64_t* emptyA = bars + AST;
   uint64_t* fullB = bars + 2 * AST;
@@ -378,10 +412,8 @@ __global__ void __launch_bounds__(192, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int tiles_m = args.Mpad / TC_BM, tiles_n = args.Npad / BN;
-  const int per_batch = tiles_m * tiles_n;
-  const int total = per_batch * batch;
-  const int nk = args.nk_total;
+  const int tiles_m = args.Mpad / TC_BM, tiles_n = (args.Npad + BN - 1) / BN;
+  const int units = tiles_m * tiles_n * batch * args.ksplit;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < AST; ++s) {
@@ -397,6 +429,10 @@ __global__ void __launch_bounds__(192, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
+    if (args.kb_half > 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA2) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB2) : "memory");
+    }
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -409,37 +445,33 @@ __global__ void __launch_bounds__(192, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_holder;
 
-  auto tile_coords = [&](int t, int& z, int& m0, int& n0) {
-    z = t / per_batch;
-    const int lin = t - z * per_batch;
-    const int per_group = TC_GROUP_M * tiles_n;
-    const int g = lin / per_group;
-    const int first_m = g * TC_GROUP_M;
-    const int gm = min(TC_GROUP_M, tiles_m - first_m);
-    const int in_g = lin - g * per_group;
-    m0 = (first_m + in_g % gm) * TC_BM;
-    n0 = (in_g / gm) * BN;
-  };
-
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
       int as = 0, gkb = 0;
       uint32_t aph = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        int z, m0, n0;
-        tile_coords(t, z, m0, n0);
-        for (int kb = 0; kb < nk; ++kb, ++gkb) {
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const TcpUnit t = tcp_unit(u, args, tiles_m, tiles_n);
+        for (int kb = 0; kb < t.nk; ++kb, ++gkb) {
           const int bs = gkb % BST;
           const uint32_t bph = (uint32_t)((gkb / BST) & 1);
+          const int kg = t.kb0 + kb;
+          // split operands: first half = shared A x party B, second half =
+          // party A x shared B (each half indexed from its own k origin)
+          const bool lo = args.kb_half > 0 && kg < args.kb_half;
+          const bool hi = args.kb_half > 0 && kg >= args.kb_half;
+          const int kx = (hi ? kg - args.kb_half : kg) * TC_BK;
+          const CUtensorMap* mA = lo ? &mapA2 : &mapA;
+          const CUtensorMap* mB = hi ? &mapB2 : &mapB;
+          const int zA = lo ? 0 : t.z, zB = hi ? 0 : t.z;
           mbar_wait(&emptyB[bs], bph ^ 1);
           mbar_expect_tx(&fullB[bs], B_STAGE);
           for (int j = 0; j < 8; ++j)
-            tma_load_2d(sB + bs * B_STAGE + j * B_TILE, &mapB, &fullB[bs], kb * TC_BK, (z * 8 + j) * args.Npad + n0);
+            tma_load_2d(sB + bs * B_STAGE + j * B_TILE, mB, &fullB[bs], kx, (zB * 8 + j) * args.Npad + t.n0);
           for (int i = 0; i < 8; ++i) {
             mbar_wait(&emptyA[as], aph ^ 1);
             mbar_expect_tx(&fullA[as], TC_A_TILE);
-            tma_load_2d(sA + as * TC_A_TILE, &mapA, &fullA[as], kb * TC_BK, (z * 8 + i) * args.Mpad + m0);
+            tma_load_2d(sA + as * TC_A_TILE, mA, &fullA[as], kx, (zA * 8 + i) * args.Mpad + t.m0);
             if (++as == AST) {
               as = 0;
               aph ^= 1;
@@ -456,10 +488,11 @@ __global__ void __launch_bounds__(192, 1)
       const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sB));
       int as = 0, gkb = 0, it = 0;
       uint32_t aph = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+        const TcpUnit t = tcp_unit(u, args, tiles_m, tiles_n);
         mbar_wait(tempty, (uint32_t)((it & 1) ^ 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        for (int kb = 0; kb < nk; ++kb, ++gkb) {
+        for (int kb = 0; kb < t.nk; ++kb, ++gkb) {
           const int bs = gkb % BST;
           const uint32_t bph = (uint32_t)((gkb / BST) & 1);
           mbar_wait(&fullB[bs], bph);
@@ -492,19 +525,17 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     // ---------------- epilogue: warps 2..5 ----------------
+    // TMEM lane = tile row: a thread owns one output row of the tile.
     const int sp = warp & 3;
-    u64* stage = stage_all + sp * (2 * 32 * 33);
     int it = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
-      int z, m0, n0;
-      tile_coords(t, z, m0, n0);
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+      const TcpUnit t = tcp_unit(u, args, tiles_m, tiles_n);
       mbar_wait(tfull, (uint32_t)(it & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll 1
-      for (int c = 0; c < 2; ++c) {
-        u64 res[32];
+      // columns [32c, 32c + 32) of this warp's 32 rows, limb-recombined
+      auto drain = [&](int c, u64 (&acc)[32]) {
 #pragma unroll
-        for (int q = 0; q < 32; ++q) res[q] = 0;
+        for (int q = 0; q < 32; ++q) acc[q] = 0;
 #pragma unroll
         for (int d = 0; d < 8; ++d) {
           uint32_t v[32];
@@ -512,35 +543,86 @@ __global__ void __launch_bounds__(192, 1)
           TMEM_LD32(taddr, v);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-          for (int q = 0; q < 32; ++q) res[q] += (u64)v[q] << (8 * d);
+          for (int q = 0; q < 32; ++q) acc[q] += (u64)v[q] << (8 * d);
         }
+      };
+      auto release = [&]() {  // accumulators drained: the MMA warp may start the next unit
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty);
+      };
+      const bool atom = args.ksplit > 1;
+      if constexpr (!STAGED) {
+        // long reductions: the epilogue is a small share of a unit; per-row
+        // direct stores (a thread writes its own row)
+        u64 r0v[32], r1v[32];
+        drain(0, r0v);
+        drain(1, r1v);
+        release();
+        const i64 row = (i64)t.m0 + sp * 32 + lane;
+        if (row < args.M) {
+          u64* Crow = args.C + (i64)t.z * args.sC + row * args.ldc;
+          const u64* Cin = args.Cin ? args.Cin + (i64)t.z * args.sCin + row * args.ldc : nullptr;
+          const u64* src = atom ? (t.ks == 0 ? Cin : nullptr) : (Cin ? Cin : (args.accumulate ? Crow : nullptr));
 #pragma unroll
-        for (int q = 0; q < 32; ++q) stage[c * 32 * 33 + lane * 33 + q] = res[q];
+          for (int q = 0; q < 64; ++q) {
+            const int col = t.n0 + q;
+            if (col < args.N) {
+              const u64 v = (q < 32 ? r0v[q] : r1v[q - 32]) + (src ? src[col] : 0ull);
+              if (atom)
+                atomicAdd(reinterpret_cast<unsigned long long*>(Crow + col), (unsigned long long)v);
+              else
+                Crow[col] = v & args.msk;
+            }
+          }
+        }
+        continue;
       }
-      // accumulators drained: the MMA warp may start the next tile
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(tempty);
-      const i64 rbase = (i64)m0 + sp * 32;
-      const i64 rows = min((i64)32, (i64)args.M - rbase);
-#pragma unroll 1
+      // coalesced stores: each 32 x 32 block goes through this warp's smem
+      // tile (row-owned -> column-owned), so a warp instruction writes 32
+      // consecutive u64 of one output row. Chunk 0 is parked in shared memory
+      // and chunk 1 in registers, so TMEM is released before any global
+      // traffic.
+      u64* stage = stage_all + sp * (32 * 33);
+      u64 hold[32];
+      drain(0, hold);
+#pragma unroll
+      for (int q = 0; q < 32; ++q) stage[lane * 33 + q] = hold[q];
+      drain(1, hold);
+      release();
+      const i64 rbase = (i64)t.m0 + sp * 32;
+      const int rmax = (int)max((i64)0, min((i64)32, (i64)args.M - rbase));
+      u64* Cz = args.C + (i64)t.z * args.sC + rbase * args.ldc;
+      const u64* Cin = args.Cin ? args.Cin + (i64)t.z * args.sCin + rbase * args.ldc : nullptr;
+      // split slices meet in C through atomics (zeroed, or holding the
+      // accumulate operand); slice 0 carries the Cin addend
+      const u64* src = atom ? (t.ks == 0 ? Cin : nullptr) : (Cin ? Cin : (args.accumulate ? Cz : nullptr));
+#pragma unroll
       for (int c = 0; c < 2; ++c) {
-        const int col = n0 + c * 32 + lane;
-        const int rmax = (col < args.N) ? (int)rows : 0;
-        u64* dst = args.C + (i64)z * args.sC + rbase * args.ldc + col;
-        const u64* src = args.Cin ? args.Cin + (i64)z * args.sCin + rbase * args.ldc + col
-                                  : (args.accumulate ? dst : nullptr);
-        const u64* st = stage + c * 32 * 33;
-        for (int h = 0; h < 32; h += 16) {
-          u64 add[16];
+        if (c == 1) {
 #pragma unroll
-          for (int r = 0; r < 16; ++r) add[r] = (src && h + r < rmax) ? src[(i64)(h + r) * args.ldc] : 0ull;
-#pragma unroll
-          for (int r = 0; r < 16; ++r)
-            if (h + r < rmax) dst[(i64)(h + r) * args.ldc] = (st[(h + r) * 33 + lane] + add[r]) & args.msk;
+          for (int q = 0; q < 32; ++q) stage[lane * 33 + q] = hold[q];
         }
+        __syncwarp();
+        const int col = t.n0 + c * 32 + lane;
+        const int rows = col < args.N ? rmax : 0;
+        // all 32 addend loads in flight before the stores that use them
+        u64 add[32];
+#pragma unroll
+        for (int r = 0; r < 32; ++r) add[r] = (src && r < rows) ? src[(i64)r * args.ldc + col] : 0ull;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+          if (r < rows) {
+            const u64 v = stage[r * 33 + lane] + add[r];
+            u64* dst = Cz + (i64)r * args.ldc + col;
+            if (atom)
+              atomicAdd(reinterpret_cast<unsigned long long*>(dst), (unsigned long long)v);
+            else
+              *dst = v & args.msk;
+          }
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -732,6 +814,145 @@ extern "C" int mpx_beaver_limbs(uint8_t* A8, uint8_t* B8, const uint64_t* D, con
 }
 
 // --------------------------------------------------------------------------
+// Fused Beaver mask + limb split for the all-parties-local (sim) session,
+// where opening D = sum_l (X_l - T_l) (basic.py:66-70) is a local reduction:
+//   S8[i][rho][kappa]    = limb i of S = (sum_l X_l - T_l) mod 2^w   (shared)
+//   P8[l][i][rho][kappa] = limb i of T_l (+ S at party p0 when add_p0)
+// X_l and T_l are logical R x K matrices at arbitrary (row, col) strides
+// (transposed operands are read in place, each with its own coalesced
+// mapping); output planes are K-major [Rpad][Kp], zero padded. This replaces
+// mask kernel -> D in HBM -> limb kernel re-reading D once per party: S is
+// written once as limbs and shared by every party's GEMM (split tensor maps
+// in k_gemm_limbs_tc_pers).
+struct MaskLimbArgs {
+  const u64* X;
+  i64 x_ps, x_sr, x_sc;
+  const u64* T;
+  i64 t_ps, t_sr, t_sc;
+  uint8_t* S8;
+  uint8_t* P8;
+  i64 R, K, Rpad, Kp;
+  u64 msk;
+  int L, p0, add_p0, pad;
+};
+
+// A thread owns (row rr, 8-column group g) of a 32 (rows) x 64 (k) tile and
+// gets its 8 consecutive-k values of a source either straight from global
+// (k-fastest source: 64 contiguous bytes) or through a shared-memory
+// transpose (any other strides: the tile is read along rows, coalesced).
+template <bool KFAST>
+__device__ __forceinline__ void ml_load8(u64 (&v)[8], const u64* __restrict__ src, i64 sr, i64 sc, i64 r0, i64 k0,
+                                         i64 R, i64 K, u64 (*tile)[33], int t) {
+  const int rr = t >> 3, g = t & 7;
+  if constexpr (KFAST) {
+    const i64 r = r0 + rr;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const i64 k = k0 + g * 8 + c;
+      v[c] = (r < R && k < K) ? src[r * sr + k] : 0ull;
+    }
+  } else {
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      const int r2 = t & 31, k2 = (t >> 5) + 8 * p;
+      const i64 r = r0 + r2, k = k0 + k2;
+      tile[k2][r2] = (r < R && k < K) ? src[r * sr + k * sc] : 0ull;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[c] = tile[g * 8 + c][rr];
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ void ml_emit(uint8_t* base, i64 plane, const u64 (&w)[8], i64 r0, i64 k0, i64 Kp,
+                                        int t) {
+  const int rr = t >> 3, g = t & 7;
+  u64 pl[8];
+  bytes_transpose8(w, pl);
+  uint8_t* dst = base + (r0 + rr) * Kp + k0 + g * 8;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) *reinterpret_cast<u64*>(dst + i * plane) = pl[i];
+}
+
+// Every source is read exactly once: party limbs are emitted as soon as the
+// party's material is loaded, except party p0's when S must be added (kept
+// in registers until S is complete).
+template <bool XK, bool TK>
+__global__ void __launch_bounds__(256, 2) k_mask_limbs(MaskLimbArgs a) {
+  __shared__ u64 tile[64][33];
+  const i64 r0 = (i64)blockIdx.x * 32, k0 = (i64)blockIdx.y * 64;
+  const int t = threadIdx.x;
+  const i64 plane = a.Rpad * a.Kp;
+  u64 s[8], keep[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s[c] = keep[c] = 0;
+  for (int l = 0; l < a.L; ++l) {
+    u64 v[8];
+    ml_load8<XK>(v, a.X + (i64)l * a.x_ps, a.x_sr, a.x_sc, r0, k0, a.R, a.K, tile, t);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) s[c] += v[c];
+    ml_load8<TK>(v, a.T + (i64)l * a.t_ps, a.t_sr, a.t_sc, r0, k0, a.R, a.K, tile, t);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) s[c] -= v[c];
+    if (a.add_p0 && l == a.p0) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) keep[c] = v[c];
+    } else {
+      ml_emit(a.P8 + (i64)l * 8 * plane, plane, v, r0, k0, a.Kp, t);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s[c] &= a.msk;
+  ml_emit(a.S8, plane, s, r0, k0, a.Kp, t);
+  if (a.add_p0 && a.p0 >= 0) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) keep[c] = (keep[c] + s[c]) & a.msk;
+    ml_emit(a.P8 + (i64)a.p0 * 8 * plane, plane, keep, r0, k0, a.Kp, t);
+  }
+}
+
+extern "C" int mpx_mask_limbs(uint8_t* S8, uint8_t* P8, const uint64_t* X, int64_t x_ps, int64_t x_sr, int64_t x_sc,
+                              const uint64_t* T, int64_t t_ps, int64_t t_sr, int64_t t_sc, int L, int64_t R,
+                              int64_t K, int64_t Rpad, int64_t Kp, int p0, int add_p0, int width, void* stream) {
+  CHECK_ARG(S8 && P8 && X && T && L >= 1 && R >= 1 && K >= 1 && width >= 1 && width <= 64);
+  CHECK_ARG(Rpad >= R && Rpad % 32 == 0 && Kp >= K && Kp % 64 == 0);
+  CHECK_ARG(Rpad / 32 <= 0x7FFFFFFF && Kp / 64 <= 65535);
+  MaskLimbArgs a;
+  a.X = X;
+  a.x_ps = x_ps;
+  a.x_sr = x_sr;
+  a.x_sc = x_sc;
+  a.T = T;
+  a.t_ps = t_ps;
+  a.t_sr = t_sr;
+  a.t_sc = t_sc;
+  a.S8 = S8;
+  a.P8 = P8;
+  a.R = R;
+  a.K = K;
+  a.Rpad = Rpad;
+  a.Kp = Kp;
+  a.msk = ring_mask(width);
+  a.L = L;
+  a.p0 = p0;
+  a.add_p0 = add_p0;
+  a.pad = 0;
+  dim3 grid((unsigned)(Rpad / 32), (unsigned)(Kp / 64));
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool xk = x_sc == 1, tk = t_sc == 1;
+  if (xk && tk)
+    k_mask_limbs<true, true><<<grid, 256, 0, s>>>(a);
+  else if (xk)
+    k_mask_limbs<true, false><<<grid, 256, 0, s>>>(a);
+  else if (tk)
+    k_mask_limbs<false, true><<<grid, 256, 0, s>>>(a);
+  else
+    k_mask_limbs<false, false><<<grid, 256, 0, s>>>(a);
+  return launch_status();
+}
+
+// --------------------------------------------------------------------------
 // Host: tensor maps + launch
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -767,14 +988,73 @@ static int make_map(CUtensorMap* map, const uint8_t* base, i64 rows, i64 kbytes,
 // C[z] (+)= sum_{i+j<=7} 2^(8(i+j)) A8[z][i] @ B8[z][j]^T  (mod 2^width)
 // A8: [batch][8][Mpad][Kpad] u8, B8: [batch][8][Npad][Kpad] u8, zero padded;
 // Mpad % 128 == 0, Npad % 64 == 0, Kpad % 128 == 0, Kpad <= 16384.
-extern "C" int mpx_gemm_limbs(uint64_t* C, const uint8_t* A8, const uint8_t* B8, int64_t batch, int64_t M,
-                              int64_t N, int64_t Mpad, int64_t Npad, int64_t Kpad, int64_t ldc, int64_t sC,
-                              int accumulate, int width, int ksplit, const uint64_t* Cin, int64_t sCin,
-                              void* stream) {
+// Split-K for the persistent kernel: minimise waves x (k-blocks per unit +
+// per-unit epilogue cost) over the slice counts that keep every slice within
+// the exactness bound (<= 16384 of K per accumulator).
+static int tcp_auto_split(i64 tiles, int nk_total, int sms) {
+  const int need = (nk_total * TC_BK + 16383) / 16384;
+  int best = need;
+  double best_cost = 1e30;
+  for (int s = need; s <= nk_total && s <= 64; ++s) {
+    const int per = (nk_total + s - 1) / s;
+    const int se = (nk_total + per - 1) / per;
+    if (se != s) continue;
+    const i64 units = tiles * se;
+    const i64 waves = (units + sms - 1) / sms;
+    const double epi = se > 1 ? 1.0 : 0.5;  // atomics cost more than plain stores
+    const double cost = (double)waves * (per + epi);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = s;
+    }
+  }
+  return best;
+}
+
+static int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+// C[z] (+)= sum_{i+j<=7} 2^(8(i+j)) A8[z][i] @ B8[z][j]^T  (mod 2^width)
+// A8: [batch][8][Mpad][Kpad] u8, B8: [batch][8][Npad][Kpad] u8, zero padded;
+// Mpad % 128 == 0, Npad % 32 == 0, Kpad % 128 == 0. ksplit 0 = automatic
+// (width 64 only), >= 1 = forced slice count.
+static int gemm_limbs_impl(uint64_t* C, const uint8_t* A8, const uint8_t* B8, const uint8_t* A8s,
+                           const uint8_t* B8s, int64_t batch, int64_t M, int64_t N, int64_t Mpad, int64_t Npad,
+                           int64_t Kpad, int64_t ldc, int64_t sC, int accumulate, int width, int ksplit,
+                           const uint64_t* Cin, int64_t sCin, void* stream) {
   CHECK_ARG(C && A8 && B8 && batch >= 1 && batch <= 65535 && M >= 1 && N >= 1 && width >= 1 && width <= 64);
+  const bool split_ops = A8s != nullptr;
+  CHECK_ARG(!split_ops || (B8s && Kpad % (2 * TC_BK) == 0));
   CHECK_ARG(Mpad % TC_BM == 0 && Npad % 32 == 0 && Kpad % TC_BK == 0 && Kpad >= TC_BK);
+  CHECK_ARG(M <= Mpad && N <= Npad && ldc >= N);
+  CHECK_ARG(batch * 8 * Mpad < (1ll << 31) && batch * 8 * Npad < (1ll << 31));
+  CHECK_ARG(!(Cin && accumulate));
+  cudaStream_t s = (cudaStream_t)stream;
   const int nk_total = (int)(Kpad / TC_BK);
-  if (ksplit < 1) ksplit = 1;
+  const bool legacy = getenv("MPX_TC_LEGACY") != nullptr && !split_ops;
+  const i64 ptiles = (Mpad / TC_BM) * ((Npad + TCP_BN - 1) / TCP_BN) * batch;
+  if (ksplit < 1) {
+    CHECK_ARG(width == 64 || nk_total * TC_BK <= 16384);
+    if (width != 64) {
+      ksplit = 1;
+    } else if (legacy) {  // two waves of one-tile CTAs, every slice <= 16384 of K
+      const i64 t64 = (Mpad / TC_BM) * (Npad / 64) * batch;
+      const int need = (nk_total * TC_BK + 16383) / 16384;
+      const int want = (int)max((i64)1, (2 * (i64)num_sms()) / max((i64)1, t64));
+      ksplit = max(need, min(want, max(1, nk_total / 2)));
+    } else {
+      const char* force = getenv("MPX_TC_KSPLIT");  // sweeps / A-B timing
+      ksplit = force ? max(1, atoi(force)) : tcp_auto_split(ptiles, nk_total, num_sms());
+      ksplit = max(ksplit, (nk_total * TC_BK + 16383) / 16384);
+    }
+  }
   if (ksplit > nk_total) ksplit = nk_total;
   int nk_per = (nk_total + ksplit - 1) / ksplit;
   ksplit = (nk_total + nk_per - 1) / nk_per;
@@ -782,43 +1062,20 @@ extern "C" int mpx_gemm_limbs(uint64_t* C, const uint8_t* A8, const uint8_t* B8,
   CHECK_ARG((i64)nk_per * TC_BK <= 16384);
   // split-K adds partials with wrapping 64-bit atomics: exact mod 2^64 only
   CHECK_ARG(ksplit == 1 || width == 64);
-  CHECK_ARG(!(Cin && accumulate));
-  if (ksplit > 1 && Cin) {
-    // partial sums land on a copy of the addend
-    for (i64 z = 0; z < batch; ++z)
-      if (cudaMemcpy2DAsync(C + z * sC, (size_t)ldc * 8, Cin + z * sCin, (size_t)ldc * 8, (size_t)N * 8,
-                            (size_t)M, cudaMemcpyDeviceToDevice, (cudaStream_t)stream) != cudaSuccess)
-        return MPX_ERR_CUDA;
-    Cin = nullptr;
-  } else if (ksplit > 1 && !accumulate) {
-    for (i64 z = 0; z < batch; ++z)
-      if (cudaMemset2DAsync(C + z * sC, (size_t)ldc * 8, 0, (size_t)N * 8, (size_t)M, (cudaStream_t)stream) !=
-          cudaSuccess)
-        return MPX_ERR_CUDA;
-  }
-  CHECK_ARG(M <= Mpad && N <= Npad && ldc >= N);
-  CHECK_ARG(batch * 8 * Mpad < (1ll << 31) && batch * 8 * Npad < (1ll << 31));
-  CUtensorMap mapA, mapB;
-  if (make_map(&mapA, A8, batch * 8 * Mpad, Kpad, TC_BM) != MPX_OK) return MPX_ERR_CUDA;
-  // persistent 128x64 tiles (epilogue overlapped with the next tile) for
-  // short unsplit reductions over many output tiles; else narrow tiles when N
-  // is not a multiple of 64 or the reduction is short, wide tiles otherwise
-  const i64 ntiles64 = (Npad / 64) * (Mpad / TC_BM) * batch;
-  // (one k-block per tile leaves too little MMA work to hide the epilogue:
-  // measured slower there, faster at 2-4)
-  const bool pers = Npad % 64 == 0 && ksplit == 1 && nk_total >= 2 && nk_total <= 4 && ntiles64 >= 4 * 148 &&
-                    getenv("MPX_TC_NO_PERSIST") == nullptr;
-  const bool narrow = !pers && ((Npad % 64 != 0) || nk_per <= 2);
-  const int bn = narrow ? 32 : 64;
-  if (make_map(&mapB, B8, batch * 8 * Npad, Kpad, bn) != MPX_OK) return MPX_ERR_CUDA;
+  CUtensorMap mapA, mapB, mapA2, mapB2;
+  // split operands: each half is its own [.][8][rows][Kpad/2] plane set
+  const i64 kcols = split_ops ? Kpad / 2 : Kpad;
+  if (make_map(&mapA, A8, batch * 8 * Mpad, kcols, TC_BM) != MPX_OK) return MPX_ERR_CUDA;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(k_gemm_limbs_tc<TC_WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              tc_smem_bytes(TC_WIDE)) != cudaSuccess ||
         cudaFuncSetAttribute(k_gemm_limbs_tc<TC_NARROW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              tc_smem_bytes(TC_NARROW)) != cudaSuccess ||
-        cudaFuncSetAttribute(k_gemm_limbs_tc_pers, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             tcp_smem_bytes()) != cudaSuccess)
+        cudaFuncSetAttribute(k_gemm_limbs_tc_pers<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             tcp_smem_bytes(true)) != cudaSuccess ||
+        cudaFuncSetAttribute(k_gemm_limbs_tc_pers<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             tcp_smem_bytes(false)) != cudaSuccess)
       return MPX_ERR_CUDA;
     attr_set = true;
   }
@@ -837,17 +1094,76 @@ extern "C" int mpx_gemm_limbs(uint64_t* C, const uint8_t* A8, const uint8_t* B8,
   a.ksplit = ksplit;
   a.accumulate = accumulate;
   a.msk = ring_mask(width);
-  if (pers) {
-    const unsigned g = (unsigned)min(ntiles64, (i64)148);
-    k_gemm_limbs_tc_pers<<<g, 192, tcp_smem_bytes(), (cudaStream_t)stream>>>(mapA, mapB, a, (int)batch);
+  a.kb_half = split_ops ? (int)(kcols / TC_BK) : 0;
+  if (!legacy) {
+    // split slices meet in C through atomics: start from zero unless C is
+    // the accumulate operand (the addend rides on slice 0)
+    if (ksplit > 1 && !accumulate)
+      for (i64 z = 0; z < batch; ++z)
+        if (cudaMemset2DAsync(C + z * sC, (size_t)ldc * 8, 0, (size_t)N * 8, (size_t)M, s) != cudaSuccess)
+          return MPX_ERR_CUDA;
+    if (make_map(&mapB, B8, batch * 8 * Npad, kcols, TCP_BN) != MPX_OK) return MPX_ERR_CUDA;
+    if (split_ops) {
+      if (make_map(&mapA2, A8s, 8 * Mpad, kcols, TC_BM) != MPX_OK ||
+          make_map(&mapB2, B8s, 8 * Npad, kcols, TCP_BN) != MPX_OK)
+        return MPX_ERR_CUDA;
+    } else {
+      mapA2 = mapA;
+      mapB2 = mapB;
+    }
+    const i64 units = ptiles * ksplit;
+    const unsigned g = (unsigned)min(units, (i64)num_sms());
+    // coalesced (smem-staged) stores when the epilogue is a large share of a
+    // unit; direct per-row stores for long reductions
+    const char* st = getenv("MPX_TC_STAGED");
+    const bool staged = st ? atoi(st) != 0 : nk_per <= TCP_STAGED_MAX_KB;
+    if (staged)
+      k_gemm_limbs_tc_pers<true><<<g, 192, tcp_smem_bytes(true), s>>>(mapA, mapB, mapA2, mapB2, a, (int)batch);
+    else
+      k_gemm_limbs_tc_pers<false><<<g, 192, tcp_smem_bytes(false), s>>>(mapA, mapB, mapA2, mapB2, a, (int)batch);
     return launch_status();
   }
+  // legacy one-tile-per-CTA kernels (MPX_TC_LEGACY=1, for A/B timing)
+  if (ksplit > 1 && Cin) {
+    for (i64 z = 0; z < batch; ++z)
+      if (cudaMemcpy2DAsync(C + z * sC, (size_t)ldc * 8, Cin + z * sCin, (size_t)ldc * 8, (size_t)N * 8,
+                            (size_t)M, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        return MPX_ERR_CUDA;
+    a.Cin = nullptr;
+  } else if (ksplit > 1 && !accumulate) {
+    for (i64 z = 0; z < batch; ++z)
+      if (cudaMemset2DAsync(C + z * sC, (size_t)ldc * 8, 0, (size_t)N * 8, (size_t)M, s) != cudaSuccess)
+        return MPX_ERR_CUDA;
+  }
+  const bool narrow = (Npad % 64 != 0) || nk_per <= 2;
+  const int bn = narrow ? 32 : 64;
+  if (make_map(&mapB, B8, batch * 8 * Npad, Kpad, bn) != MPX_OK) return MPX_ERR_CUDA;
   dim3 grid((unsigned)((Npad / bn) * (Mpad / TC_BM) * ksplit), 1, (unsigned)batch);
   if (narrow)
-    k_gemm_limbs_tc<TC_NARROW><<<grid, 192, tc_smem_bytes(TC_NARROW), (cudaStream_t)stream>>>(mapA, mapB, a);
+    k_gemm_limbs_tc<TC_NARROW><<<grid, 192, tc_smem_bytes(TC_NARROW), s>>>(mapA, mapB, a);
   else
-    k_gemm_limbs_tc<TC_WIDE><<<grid, 192, tc_smem_bytes(TC_WIDE), (cudaStream_t)stream>>>(mapA, mapB, a);
+    k_gemm_limbs_tc<TC_WIDE><<<grid, 192, tc_smem_bytes(TC_WIDE), s>>>(mapA, mapB, a);
   return launch_status();
+}
+
+extern "C" int mpx_gemm_limbs(uint64_t* C, const uint8_t* A8, const uint8_t* B8, int64_t batch, int64_t M,
+                              int64_t N, int64_t Mpad, int64_t Npad, int64_t Kpad, int64_t ldc, int64_t sC,
+                              int accumulate, int width, int ksplit, const uint64_t* Cin, int64_t sCin,
+                              void* stream) {
+  return gemm_limbs_impl(C, A8, B8, nullptr, nullptr, batch, M, N, Mpad, Npad, Kpad, ldc, sC, accumulate, width,
+                         ksplit, Cin, sCin, stream);
+}
+
+// Beaver reconstruction from split limb operands (k_mask_limbs output):
+// C[z] = Cin[z] + [S_A | P_A[z]] @ [P_B[z] ; S_B] with S_* shared by all z
+// ([8][rows][Kh] planes) and P_* per party ([batch][8][rows][Kh]).
+extern "C" int mpx_gemm_limbs_split(uint64_t* C, const uint8_t* PA8, const uint8_t* SA8, const uint8_t* PB8,
+                                    const uint8_t* SB8, int64_t batch, int64_t M, int64_t N, int64_t Mpad,
+                                    int64_t Npad, int64_t Kh, int64_t ldc, int64_t sC, int width, int ksplit,
+                                    const uint64_t* Cin, int64_t sCin, void* stream) {
+  CHECK_ARG(SA8 && SB8 && Kh % TC_BK == 0);
+  return gemm_limbs_impl(C, PA8, PB8, SA8, SB8, batch, M, N, Mpad, Npad, 2 * Kh, ldc, sC, 0, width, ksplit, Cin,
+                         sCin, stream);
 }
 
 int mpx_gemm_tc(uint64_t*, const uint64_t*, const uint64_t*, int64_t, int64_t, int64_t, int64_t, int64_t,

@@ -383,17 +383,6 @@ def limb_split(out, A, rows, cols, lda, plane, pitch, coff, trans):
     return out
 
 
-def auto_ksplit(tiles: int, batch: int, Kpad: int) -> int:
-    """Split K so small-output GEMMs still fill the SMs; every slice <= TC_MAX_K."""
-    nk = Kpad // 128
-    need = -(-Kpad // TC_MAX_K)
-    want = max(1, (KSPLIT_WAVES * NUM_SMS) // max(1, tiles * batch))
-    return max(need, min(want, max(1, nk // 2)))
-
-
-KSPLIT_WAVES = int(os.environ.get("MPX_KSPLIT_WAVES", "2"))  # 2 measured best (LeNet 2.14 vs 2.19 ms at 4, 2.24 at 8)
-
-
 def ring_colsum(out, x, L, rows, cols, width):
     if _dry(out):
         return out
@@ -454,11 +443,30 @@ def gemm_limbs(C, A8, B8, batch, M, N, Mpad, Npad, Kpad, ldc, sC, accumulate, wi
     if _dry(C):
         return C
     if ksplit is None:
-        ksplit = auto_ksplit((Mpad // 128) * (Npad // 64), batch, Kpad) if width == 64 else 1
+        ksplit = 0          # libmpx picks the split (persistent kernel: fewest waves)
     cin_ptr = None if cin is None else (cin if isinstance(cin, int) else ptr(cin))
     call("mpx_gemm_limbs", ptr(C), ptr(A8), ptr(B8), batch, M, N, Mpad, Npad, Kpad, ldc, sC,
          int(accumulate), width, int(ksplit), cin_ptr, s_cin)
     return C
+
+
+def gemm_limbs_split(C, PA8, SA8, PB8, SB8, batch, M, N, Mpad, Npad, Kh, ldc, sC, width, cin, s_cin, ksplit=0):
+    """C[z] = Cin[z] + [SA | PA[z]] @ [PB[z] ; SB] on the persistent tcgen05 kernel."""
+    if _dry(C):
+        return C
+    cin_ptr = cin if isinstance(cin, int) else ptr(cin)
+    call("mpx_gemm_limbs_split", ptr(C), ptr(PA8), ptr(SA8), ptr(PB8), ptr(SB8), batch, M, N, Mpad, Npad, Kh, ldc,
+         sC, width, int(ksplit), cin_ptr, s_cin)
+    return C
+
+
+def mask_limbs(S8, P8, x_ptr, x_ps, x_sr, x_sc, t_ptr, t_ps, t_sr, t_sc, L, R, Kd, Rpad, Kp, p0, add_p0, width):
+    """Fused sim-mode Beaver mask + limb split (shared S limbs, per-party T limbs)."""
+    if _dry(S8):
+        return S8
+    call("mpx_mask_limbs", ptr(S8), ptr(P8), x_ptr, x_ps, x_sr, x_sc, t_ptr, t_ps, t_sr, t_sc, L, R, Kd, Rpad, Kp,
+         p0, int(add_p0), width)
+    return S8
 
 
 def gemm_tc(C, A, B, batch, M, K, N, sA, sB, sC, accumulate, width):

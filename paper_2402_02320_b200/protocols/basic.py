@@ -68,21 +68,37 @@ def batch_matmul(session, pairs) -> list[AShare]:
         trip.append(session.store.take_matrix_triple(x.width, m, k, y.shape[1]))
     groups = _groups(session, pairs, trip)
     masked = []
+    fused_payload = 0
     for g in groups:
         x0, y0 = pairs[g[0]]
         w, (m, k), r = x0.width, x0.shape, y0.shape[1]
+        if _fused_tc(session, m, k, r, w):
+            # sim mode: mask + open + limb split fused below (one round, same
+            # logical payload as the reference's D, E openings)
+            fused_payload += len(g) * (arith_payload(w, m * k) + arith_payload(w, k * r))
+            continue
         D = session.alloc((len(g), m * k))
         E = session.alloc((len(g), k * r))
         _mask_group(D, [pairs[i][0].values for i in g], [trip[i][0] for i in g], L, m, k, w)
         _mask_group(E, [pairs[i][1].values for i in g], [trip[i][1] for i in g], L, k, r, w)
         for j in range(len(g)):
             masked += [(D[j], w), (E[j], w)]
-    opened = session.exchange(arith=masked)
+    payload = sum(arith_payload(w, t.numel()) for t, w in masked) + fused_payload
+    opened = session.exchange(arith=masked, payload=payload)
     out = [None] * len(pairs)
     pos = 0
     for g in groups:
         x0, y0 = pairs[g[0]]
         w, (m, k), r = x0.width, x0.shape, y0.shape[1]
+        if _fused_tc(session, m, k, r, w):
+            Zg = session.alloc((len(g), L, m, r))
+            for j, i in enumerate(g):
+                x, y = pairs[i]
+                A, B, C = trip[i]
+                _beaver_matmul_fused_tc(session, Zg[j], x.values, y.values, A, B, C, L, m, k, r, w)
+                session.metrics.count(matmul_count=1, matmul_macs=m * k * r)
+                out[i] = AShare(Zg[j], w, x.frac + y.frac, session.parties)
+            continue
         Ds = opened[pos:pos + 2 * len(g):2]
         Es = opened[pos + 1:pos + 2 * len(g):2]
         pos += 2 * len(g)
@@ -191,6 +207,43 @@ def _use_tc(m, k, r, w=64) -> bool:
         return False
     waste = (K._rup(m, 128) / m) * (K._rup(r, 32) / r)
     return waste <= 1.5 and K.tc_eligible(m, 2 * k, r, w) and (w == 64 or 2 * k <= K.TC_MAX_K)
+
+
+def _fused_tc(session, m, k, r, w) -> bool:
+    """Sim sessions run tcgen05-sized products as fused mask+limb split +
+    split-operand GEMM; below K = 64 the per-half padding would double the
+    MMA work, so those keep the concatenated-limb path."""
+    return session.fused and k > 64 and _use_tc(m, k, r, w)
+
+
+def _strides3(v):
+    """(party, row, col) element strides of an [L, rows, cols] view."""
+    if v.dim() != 3:
+        raise ValueError("expected an [L, rows, cols] share view")
+    return v.stride(0), v.stride(1), v.stride(2)
+
+
+def _beaver_matmul_fused_tc(session, Z, X, Y, A, B, C, L, m, k, r, w):
+    """All parties local: D = sum_l X_l - A_l and E = sum_l Y_l - B_l are
+    never materialised as u64; one kernel per side writes their limb planes
+    once (shared by every party's GEMM) next to the per-party material limbs
+    (A_l; B_l + [l==p0] E), and the split-operand GEMM computes
+    Z_l = C_l + [D | A_l] @ [B_l + [l==p0] E ; E] (basic.py:66-75)."""
+    Mp, Np, Kh = K._rup(m, 128), K._rup(r, 32), K._rup(k, 128)
+    dev = Z.device
+    SA = torch.empty((8, Mp, Kh), dtype=torch.uint8, device=dev)
+    PA = torch.empty((L, 8, Mp, Kh), dtype=torch.uint8, device=dev)
+    SB = torch.empty((8, Np, Kh), dtype=torch.uint8, device=dev)
+    PB = torch.empty((L, 8, Np, Kh), dtype=torch.uint8, device=dev)
+    xps, xsr, xsc = _strides3(X)
+    yps, ysk, ysn = _strides3(Y)
+    # A side: logical (m, k); material A_l row-major m x k
+    K.mask_limbs(SA, PA, _ptr(X), xps, xsr, xsc, A.data_ptr(), A.stride(0), k, 1, L, m, k, Mp, Kh, session.p0,
+                 False, w)
+    # B side: logical (r, k) = Y^T; material B_l row-major k x r
+    K.mask_limbs(SB, PB, _ptr(Y), yps, ysn, ysk, B.data_ptr(), B.stride(0), 1, r, L, r, k, Np, Kh, session.p0,
+                 True, w)
+    K.gemm_limbs_split(Z, PA, SA, PB, SB, L, m, r, Mp, Np, Kh, r, m * r, w, C.data_ptr(), C.stride(0))
 
 
 def _beaver_matmul_tc(session, Z, D, E, A, B, C, L, m, k, r, w):

@@ -161,3 +161,29 @@ def test_gemm_limbs_persistent_short_k(K, M, Kd, N, b, mode):
         for z in range(b):
             want = _mm(A[z], B[z]) + (C[z] if mode in ("cin", "acc") else np.uint64(0))
             assert np.array_equal(got[z], want), z
+
+
+@pytest.mark.parametrize("mode", ["cin", "acc", "plain"])
+@pytest.mark.parametrize("ks", [1, 2, 3, None])
+def test_gemm_limbs_persistent_splits(K, mode, ks):
+    """Persistent tcgen05 kernel: every split-K slice count (wrapping atomics
+    with the addend on slice 0, or onto the accumulate operand), an N tile
+    that straddles Npad % 64 == 32, several units per CTA; exact vs numpy."""
+    rng = np.random.default_rng(11 + (ks or 0))
+    b, M, Kd, N = 2, 700, 300, 96
+    A, B, C = _rand(rng, (b, M, Kd), 64), _rand(rng, (b, Kd, N), 64), _rand(rng, (b, M, N), 64)
+    Mp, Np, Kp = K._rup(M, 128), K._rup(N, 32), K._rup(Kd, 128)
+    Ad, Bd, Cd = _dev(A), _dev(B), _dev(C)
+    A8 = torch.zeros((b, 8, Mp, Kp), dtype=torch.uint8, device="cuda")
+    B8 = torch.zeros((b, 8, Np, Kp), dtype=torch.uint8, device="cuda")
+    for z in range(b):
+        K.limb_split(A8[z], Ad.data_ptr() + 8 * z * M * Kd, M, Kd, Kd, Mp * Kp, Kp, 0, False)
+        K.limb_split(B8[z], Bd.data_ptr() + 8 * z * Kd * N, Kd, N, N, Np * Kp, Kp, 0, True)
+    Z = Cd.clone() if mode == "acc" else torch.full((b, M, N), 5, dtype=torch.int64, device="cuda")
+    K.gemm_limbs(Z, A8, B8, b, M, N, Mp, Np, Kp, N, M * N, mode == "acc", 64, ksplit=ks,
+                 cin=Cd if mode == "cin" else None, s_cin=M * N)
+    got = _host(Z)
+    with np.errstate(over="ignore"):
+        for z in range(b):
+            want = _mm(A[z], B[z]) + (C[z] if mode in ("cin", "acc") else np.uint64(0))
+            assert np.array_equal(got[z], want), z

@@ -40,6 +40,20 @@ def timeit(fn, reps=None):
     return e0.elapsed_time(e1) / reps * 1e3
 
 
+def _tc_time(m, k, r, L):
+    """GEMM-only time (limb planes prepared once) of the Beaver product."""
+    g = torch.Generator(device="cuda").manual_seed(1)
+    rnd = lambda *s: torch.randint(-2**62, 2**62, s, device="cuda", generator=g)  # noqa: E731
+    D, E = rnd(m, k), rnd(k, r)
+    A, B, C = rnd(L, m, k), rnd(L, k, r), rnd(L, m, r)
+    Z = torch.empty((L, m, r), dtype=torch.int64, device="cuda")
+    Mp, Np, Kp = K._rup(m, 128), K._rup(r, 32), K._rup(2 * k, 128)
+    A8 = torch.zeros((L, 8, Mp, Kp), dtype=torch.uint8, device="cuda")
+    B8 = torch.empty((L, 8, Np, Kp), dtype=torch.uint8, device="cuda")
+    K.beaver_limbs(A8, B8, D, E, A.data_ptr(), m * k, B.data_ptr(), k * r, L, m, k, r, Mp, Np, Kp, 0)
+    return timeit(lambda: K.gemm_limbs(Z, A8, B8, L, m, r, Mp, Np, Kp, r, m * r, False, 64, cin=C, s_cin=m * r))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--parties", type=int, default=3)
@@ -47,6 +61,7 @@ def main():
     ap.add_argument("--no-simt", action="store_true")
     ap.add_argument("--only", default=None, help="m,k,r")
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--splits", default=None, help="comma list of forced split-K counts")
     a = ap.parse_args()
     L = a.parties
     REPS[0] = a.reps
@@ -54,6 +69,16 @@ def main():
     shapes = _vgg() if a.shapes == "vgg" else LENET
     if a.only:
         shapes = [tuple(int(v) for v in a.only.split(","))]
+    if a.splits:
+        for m, k, r in shapes:
+            res = {}
+            for sp in a.splits.split(","):
+                os.environ["MPX_TC_KSPLIT"] = sp
+                res[sp] = round(_tc_time(m, k, r, L), 1)
+            os.environ.pop("MPX_TC_KSPLIT", None)
+            res["auto"] = round(_tc_time(m, k, r, L), 1)
+            print(json.dumps({"m": m, "k": k, "r": r, "gemm_us_by_split": res}), flush=True)
+        return
     for m, k, r in shapes:
         g = torch.Generator(device="cuda").manual_seed(1)
         rnd = lambda *s: torch.randint(-2**62, 2**62, s, device="cuda", generator=g)  # noqa: E731

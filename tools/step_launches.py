@@ -60,6 +60,8 @@ def main():
             ops = None
             if name == "mpx_gemm_limbs":
                 ops = 2 * 36 * args[3] * args[4] * args[5] * args[8]
+            elif name == "mpx_gemm_limbs_split":
+                ops = 2 * 36 * args[5] * args[6] * args[7] * 2 * args[10]
             short = [v for v in args if isinstance(v, int) and abs(v) < 1 << 40][:12]
             cur.append([name, short, us, b, ops])
         if rows is None:
