@@ -379,11 +379,11 @@ def int8_peak_tops(torch, n=8192, iters=10):
     return 2 * n ** 3 / (best / 1e3) / 1e12
 
 
-def sweep_entry(torch, G, make_session, parties, n_parties, dev, name, steps=2, warmup=1):
+def sweep_entry(torch, G, make_session, parties, n_parties, dev, name, steps=2, warmup=1, elems=1 << 24):
     from paper_2402_02320_b200 import _lib
     from paper_2402_02320_b200.preprocessing import DemandCounter, device_store
     from paper_2402_02320_b200.protocols import batch_matmul
-    N = 1 << 24
+    N = elems
     rng = np.random.default_rng(7)
     if name == "matmul":
         D = 4096
@@ -536,11 +536,11 @@ def _kernel_table(per):
             for k, v in sorted(per.items(), key=lambda kv: -kv[1]["ms"])}
 
 
-def reciprocal_entry(torch, G, make_session, parties, n_parties, dev, group, steps, warmup):
+def reciprocal_entry(torch, G, make_session, parties, n_parties, dev, group, steps, warmup, elems=1 << 24):
     """cfg 5: secure Reciprocal on 2^24 elements (one fused kernel in sim mode)."""
     from paper_2402_02320_b200 import _lib
     from paper_2402_02320_b200.preprocessing import DemandCounter, device_store
-    N = 1 << 24
+    N = elems
     xs = workload_inputs(N)
     enc = encode_np(xs)
     key = label_key("share:x")
@@ -616,7 +616,8 @@ def cifar_entry(torch, dev, arch, steps, warmup, n=2):
     from paper_2402_02320_b200.preprocessing import DemandCounter, device_store
     from paper_2402_02320_b200.session import SimSession
     rng = np.random.default_rng(6)
-    x, y = rng.uniform(0, 1, (BATCH, 3, 32, 32)), np.eye(10)[rng.integers(0, 10, BATCH)]
+    shape = (BATCH, 1, 28, 28) if arch == "lenet" else (BATCH, 3, 32, 32)
+    x, y = rng.uniform(0, 1, shape), np.eye(10)[rng.integers(0, 10, BATCH)]
     build = getattr(train, arch)
     c = DemandCounter(tuple(range(n)), n)
     sd = SimSession(n, c, device=dev)
@@ -648,16 +649,16 @@ def cifar_entry(torch, dev, arch, steps, warmup, n=2):
             "cuda_graph": True}
 
 
-def transformer_entry(torch, dev, steps, warmup):
+def transformer_entry(torch, dev, steps, warmup, n=2):
     """configs[3]: 18.9M-parameter Transformer secure inference, seq 128, p = 14,
     2 parties on one GPU, forward captured in one CUDA graph. Latency per
     forward (lower is better)."""
     from paper_2402_02320_b200.preprocessing import DemandCounter, device_store
     from paper_2402_02320_b200.session import SimSession
     from paper_2402_02320_b200.transformer import GraphedInference, Transformer
-    n, S = 2, 128
+    S = 128
     x = np.random.default_rng(3).normal(0, 1, (S, 512))
-    c = DemandCounter((0, 1), n)
+    c = DemandCounter(tuple(range(n)), n)
     sd = SimSession(n, c, device=dev)
     Transformer(sd).forward(sd, sd.share_fixed(x, WIDTH, 14, [5, 5]))
     s = SimSession(n, None, device=dev)
@@ -680,6 +681,33 @@ def transformer_entry(torch, dev, steps, warmup):
             "frac": 14, "latency_ms": float(np.mean(times)), "higher_is_better": False,
             "rounds": sd.metrics.total.rounds, "cuda_graph": True,
             "max_abs_err_vs_float64": float(np.abs(y - m.plaintext(xq)).max())}
+
+
+def party_scaling(torch, G, dev, group, ns=(2, 4, 8)):
+    """North-star party sweep, all n parties simulated on one GPU (one-GPU-
+    per-party runs need an n-GPU box: bench.py --gpus n under torchrun):
+    LeNet training step, 18.9M Transformer inference, Beaver matmul 4096^2,
+    and Reciprocal / Exp / Log on 2^22 elements (2^24 x 8 parties of
+    single-use material would exceed HBM)."""
+    from paper_2402_02320_b200.session import SimSession
+    out = {}
+    for n in ns:
+        def mk(store, n=n):
+            return SimSession(n, store, device=dev)
+        parties = tuple(range(n))
+        e = {"lenet_train_ms": cifar_entry(torch, dev, "lenet", 3, 2, n=n)["ms_per_step"],
+             "transformer_infer_ms": transformer_entry(torch, dev, 3, 2, n=n)["latency_ms"]}
+        mm = sweep_entry(torch, G, mk, parties, n, dev, "matmul")
+        e["matmul_4096_ms"] = mm["ms_per_op"]
+        r = reciprocal_entry(torch, G, mk, parties, n, dev, group, 2, 1, elems=1 << 22)
+        e["reciprocal_2^22_ms"] = r["ms_per_op"]
+        e["reciprocal_hbm_frac"] = r["roofline"]["frac"]
+        for nm in ("exp", "log"):
+            s = sweep_entry(torch, G, mk, parties, n, dev, nm, elems=1 << 22)
+            e[f"{nm}_2^22_ms"] = s["ms_per_op"]
+            e[f"{nm}_hbm_frac"] = s["roofline"]["frac"]
+        out[str(n)] = e
+    return out
 
 
 def run_b200(args, group=None):
@@ -851,6 +879,8 @@ def run_b200(args, group=None):
             sweep["transformer"] = transformer_entry(torch, dev, 3, 2)
             for arch in ("alexnet", "vgg16m"):
                 sweep[f"{arch}_train"] = cifar_entry(torch, dev, arch, 3, 2)
+            if not getattr(args, "no_party_sweep", False):
+                sweep["party_scaling_sim"] = party_scaling(torch, G, dev, group)
 
     line = None
     if rank == 0:
@@ -924,6 +954,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=1 << 20)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-party-sweep", action="store_true")
     ap.add_argument("--chunks", type=int, default=8)
     args = ap.parse_args()
     if args.impl == "reference":

@@ -350,13 +350,29 @@ __global__ void __launch_bounds__(192, BN == 32 ? 2 : 1)
 // keep the tensor pipe fed across unit boundaries. N tiles of 64 also cover
 // Npad % 64 == 32: the extra 32 B rows belong to the next plane (or are
 // TMA zero-fill past the end) and only feed columns >= Npad, never stored.
-#define TCP_BN 64
-#define TCP_AST 4
+// Template: BK = k-block bytes (128 / 64 / 32 with the matching 128B / 64B /
+// 32B swizzle, so short reductions pad K to 32 or 64 instead of 128), BN =
+// N tile (64, or 32 for outputs at most 32 wide: 256 TMEM columns).
 #define TCP_BST 2
-#define TCP_STAGE_BYTES (4 * 32 * 33 * 8)
-#define TCP_STAGED_MAX_KB 4  // one 32 x 32 u64 transpose tile per epilogue warp
-constexpr int tcp_smem_bytes(bool staged) {
-  return TCP_AST * TC_A_TILE + TCP_BST * 8 * TCP_BN * TC_BK + (staged ? TCP_STAGE_BYTES : 0) + 1024 + 256;
+#define TCP_STAGE_BYTES (4 * 32 * 33 * 8)  // one 32 x 32 u64 transpose tile per epilogue warp
+#define TCP_STAGED_MAX_KB 4
+constexpr int tcp_ast(int bk) { return 65536 / (TC_BM * bk); }  // 64 KB A ring
+constexpr int tcp_smem_bytes(int bk, int bn, bool staged) {
+  return tcp_ast(bk) * TC_BM * bk + TCP_BST * 8 * bn * bk + (staged ? TCP_STAGE_BYTES : 0) + 1024 + 512;
+}
+
+// K-major UMMA shared-memory descriptor for a BK-byte-row swizzled tile
+// (version 1 = sm100): SBO = 8 rows, layout 2 / 4 / 6 = 128B / 64B / 32B.
+template <int BK>
+__device__ __forceinline__ uint64_t umma_desc_sw(uint32_t saddr) {
+  constexpr uint64_t layout = BK == 128 ? 2 : (BK == 64 ? 4 : 6);
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)((8 * BK) >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= layout << 61;
+  return d;
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -367,7 +383,7 @@ struct TcpUnit {
   int z, m0, n0, kb0, nk, ks;
 };
 
-__device__ __forceinline__ TcpUnit tcp_unit(int u, const TcArgs& a, int tiles_m, int tiles_n) {
+__device__ __forceinline__ TcpUnit tcp_unit(int u, const TcArgs& a, int tiles_m, int tiles_n, int bn) {
   TcpUnit t;
   t.ks = u % a.ksplit;
   const int lin_all = u / a.ksplit;
@@ -380,25 +396,27 @@ __device__ __forceinline__ TcpUnit tcp_unit(int u, const TcArgs& a, int tiles_m,
   const int gm = min(TC_GROUP_M, tiles_m - first_m);
   const int in_g = lin - g * per_group;
   t.m0 = (first_m + in_g % gm) * TC_BM;
-  t.n0 = (in_g / gm) * TCP_BN;
+  t.n0 = (in_g / gm) * bn;
   t.kb0 = t.ks * a.nk;
   t.nk = min(a.nk, a.nk_total - t.kb0);
   return t;
 }
 
-template <bool STAGED>
+template <int BK, int BN, bool STAGED>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_limbs_tc_pers(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                          const __grid_constant__ CUtensorMap mapA2, const __grid_constant__ CUtensorMap mapB2,
                          TcArgs args, int batch) {
-  constexpr int BN = TCP_BN, AST = TCP_AST, BST = TCP_BST;
-  constexpr int B_TILE = BN * TC_BK;
+  constexpr int AST = tcp_ast(BK), BST = TCP_BST;
+  constexpr int A_TILE = TC_BM * BK;
+  constexpr int B_TILE = BN * BK;
   constexpr int B_STAGE = 8 * B_TILE;
-  constexpr uint32_t ACC_COLS = 8 * BN;  // 8 diagonals = all 512 columns
+  constexpr int NC = BN / 32;             // 32-column epilogue chunks
+  constexpr uint32_t ACC_COLS = 8 * BN;  // 8 diagonals (512 or 256 columns)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
-  uint8_t* sB = smem + AST * TC_A_TILE;
+  uint8_t* sB = smem + AST * A_TILE;
   u64* stage_all = reinterpret_cast<u64*>(sB + BST * B_STAGE);
   uint64_t* bars =
       reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stage_all) + (STAGED ? TCP_STAGE_BYTES : 0));
@@ -451,7 +469,7 @@ __global__ void __launch_bounds__(192, 1)
       int as = 0, gkb = 0;
       uint32_t aph = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const TcpUnit t = tcp_unit(u, args, tiles_m, tiles_n);
+        const TcpUnit t = tcp_unit(u, args, tiles_m, tiles_n, BN);
         for (int kb = 0; kb < t.nk; ++kb, ++gkb) {
           const int bs = gkb % BST;
           const uint32_t bph = (uint32_t)((gkb / BST) & 1);
@@ -460,7 +478,7 @@ __global__ void __launch_bounds__(192, 1)
           // party A x shared B (each half indexed from its own k origin)
           const bool lo = args.kb_half > 0 && kg < args.kb_half;
           const bool hi = args.kb_half > 0 && kg >= args.kb_half;
-          const int kx = (hi ? kg - args.kb_half : kg) * TC_BK;
+          const int kx = (hi ? kg - args.kb_half : kg) * BK;
           const CUtensorMap* mA = lo ? &mapA2 : &mapA;
           const CUtensorMap* mB = hi ? &mapB2 : &mapB;
           const int zA = lo ? 0 : t.z, zB = hi ? 0 : t.z;
@@ -470,8 +488,8 @@ __global__ void __launch_bounds__(192, 1)
             tma_load_2d(sB + bs * B_STAGE + j * B_TILE, mB, &fullB[bs], kx, (zB * 8 + j) * args.Npad + t.n0);
           for (int i = 0; i < 8; ++i) {
             mbar_wait(&emptyA[as], aph ^ 1);
-            mbar_expect_tx(&fullA[as], TC_A_TILE);
-            tma_load_2d(sA + as * TC_A_TILE, mA, &fullA[as], kx, (zA * 8 + i) * args.Mpad + t.m0);
+            mbar_expect_tx(&fullA[as], A_TILE);
+            tma_load_2d(sA + as * A_TILE, mA, &fullA[as], kx, (zA * 8 + i) * args.Mpad + t.m0);
             if (++as == AST) {
               as = 0;
               aph ^= 1;
@@ -484,12 +502,12 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
       const uint32_t idesc = (2u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
-      const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA));
-      const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sB));
+      const uint64_t a_desc0 = umma_desc_sw<BK>(smem_u32(sA));
+      const uint64_t b_desc0 = umma_desc_sw<BK>(smem_u32(sB));
       int as = 0, gkb = 0, it = 0;
       uint32_t aph = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
-        const TcpUnit t = tcp_unit(u, args, tiles_m, tiles_n);
+        const TcpUnit t = tcp_unit(u, args, tiles_m, tiles_n, BN);
         mbar_wait(tempty, (uint32_t)((it & 1) ^ 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         for (int kb = 0; kb < t.nk; ++kb, ++gkb) {
@@ -503,13 +521,13 @@ __global__ void __launch_bounds__(192, 1)
           for (int i = 0; i < 8; ++i) {
             mbar_wait(&fullA[as], aph);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint64_t ad = a_desc0 + (uint64_t)((as * TC_A_TILE) >> 4);
+            const uint64_t ad = a_desc0 + (uint64_t)((as * A_TILE) >> 4);
 #pragma unroll
             for (int j = 0; j <= 7 - i; ++j) {
               const uint32_t d_tmem = tmem_base + (uint32_t)((i + j) * BN);
               const uint64_t bd = bd0 + (uint64_t)((j * B_TILE) >> 4);
 #pragma unroll
-              for (int kk = 0; kk < TC_BK / 32; ++kk)
+              for (int kk = 0; kk < BK / 32; ++kk)
                 mma_i8(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, (i > 0 || kk > 0) ? 1u : first);
             }
             umma_commit(&emptyA[as]);
@@ -529,7 +547,31 @@ __global__ void __launch_bounds__(192, 1)
     const int sp = warp & 3;
     int it = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
-      const TcpUnit t = tcp_unit(u, args, tiles_m, tiles_n);
+      const TcpUnit t = tcp_unit(u, args, tiles_m, tiles_n, BN);
+      const bool atom = args.ksplit > 1;
+      const i64 rbase = (i64)t.m0 + sp * 32;
+      const int rmax = (int)max((i64)0, min((i64)32, (i64)args.M - rbase));
+      u64* Cz = args.C + (i64)t.z * args.sC + rbase * args.ldc;
+      const u64* Cin = args.Cin ? args.Cin + (i64)t.z * args.sCin + rbase * args.ldc : nullptr;
+      // split slices meet in C through atomics (zeroed, or holding the
+      // accumulate operand); slice 0 carries the Cin addend
+      const u64* src = atom ? (t.ks == 0 ? Cin : nullptr) : (Cin ? Cin : (args.accumulate ? Cz : nullptr));
+      u64* stage = stage_all + sp * (32 * 33);
+      if constexpr (STAGED) {
+        // chunk 0's addend block lands in the transpose tile (cp.async,
+        // coalesced along the row) while the MMAs are still running
+        const int col = t.n0 + lane;
+        const int rows = col < args.N ? rmax : 0;
+#pragma unroll 8
+        for (int r = 0; r < 32; ++r) {
+          const u64* g = src + (i64)r * args.ldc + col;
+          const uint32_t sz = (src && r < rows) ? 8u : 0u;  // 0: zero-fill
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(stage + r * 33 + lane)),
+                       "l"(sz ? g : args.C), "r"(sz)
+                       : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
       mbar_wait(tfull, (uint32_t)(it & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       // columns [32c, 32c + 32) of this warp's 32 rows, limb-recombined
@@ -551,13 +593,12 @@ __global__ void __launch_bounds__(192, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty);
       };
-      const bool atom = args.ksplit > 1;
       if constexpr (!STAGED) {
         // long reductions: the epilogue is a small share of a unit; per-row
         // direct stores (a thread writes its own row)
         u64 r0v[32], r1v[32];
         drain(0, r0v);
-        drain(1, r1v);
+        if constexpr (NC > 1) drain(1, r1v);
         release();
         const i64 row = (i64)t.m0 + sp * 32 + lane;
         if (row < args.M) {
@@ -565,7 +606,7 @@ __global__ void __launch_bounds__(192, 1)
           const u64* Cin = args.Cin ? args.Cin + (i64)t.z * args.sCin + row * args.ldc : nullptr;
           const u64* src = atom ? (t.ks == 0 ? Cin : nullptr) : (Cin ? Cin : (args.accumulate ? Crow : nullptr));
 #pragma unroll
-          for (int q = 0; q < 64; ++q) {
+          for (int q = 0; q < BN; ++q) {
             const int col = t.n0 + q;
             if (col < args.N) {
               const u64 v = (q < 32 ? r0v[q] : r1v[q - 32]) + (src ? src[col] : 0ull);
@@ -583,23 +624,18 @@ __global__ void __launch_bounds__(192, 1)
       // consecutive u64 of one output row. Chunk 0 is parked in shared memory
       // and chunk 1 in registers, so TMEM is released before any global
       // traffic.
-      u64* stage = stage_all + sp * (32 * 33);
       u64 hold[32];
       drain(0, hold);
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncwarp();
 #pragma unroll
-      for (int q = 0; q < 32; ++q) stage[lane * 33 + q] = hold[q];
-      drain(1, hold);
+      for (int q = 0; q < 32; ++q) stage[lane * 33 + q] += hold[q];  // thread = row, q = column
+      if constexpr (NC > 1) drain(1, hold);
       release();
-      const i64 rbase = (i64)t.m0 + sp * 32;
-      const int rmax = (int)max((i64)0, min((i64)32, (i64)args.M - rbase));
-      u64* Cz = args.C + (i64)t.z * args.sC + rbase * args.ldc;
-      const u64* Cin = args.Cin ? args.Cin + (i64)t.z * args.sCin + rbase * args.ldc : nullptr;
-      // split slices meet in C through atomics (zeroed, or holding the
-      // accumulate operand); slice 0 carries the Cin addend
-      const u64* src = atom ? (t.ks == 0 ? Cin : nullptr) : (Cin ? Cin : (args.accumulate ? Cz : nullptr));
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        if (c == 1) {
+      for (int c = 0; c < NC; ++c) {
+        if (c == 1) {  // chunk 1 waited in registers; its addend is read now
+          __syncwarp();
 #pragma unroll
           for (int q = 0; q < 32; ++q) stage[lane * 33 + q] = hold[q];
         }
@@ -609,7 +645,7 @@ __global__ void __launch_bounds__(192, 1)
         // all 32 addend loads in flight before the stores that use them
         u64 add[32];
 #pragma unroll
-        for (int r = 0; r < 32; ++r) add[r] = (src && r < rows) ? src[(i64)r * args.ldc + col] : 0ull;
+        for (int r = 0; r < 32; ++r) add[r] = (c == 1 && src && r < rows) ? src[(i64)r * args.ldc + col] : 0ull;
 #pragma unroll
         for (int r = 0; r < 32; ++r) {
           if (r < rows) {
@@ -802,12 +838,12 @@ extern "C" int mpx_beaver_limbs(uint8_t* A8, uint8_t* B8, const uint64_t* D, con
                                 int64_t a_ps, const uint64_t* B, int64_t b_ps, int L, int64_t M, int64_t K,
                                 int64_t N, int64_t Mpad, int64_t Npad, int64_t Kpad, int p0, void* stream) {
   CHECK_ARG(A8 && B8 && D && E && A && B && L >= 1 && L <= 65535 && M >= 1 && K >= 1 && N >= 1);
-  CHECK_ARG(Mpad >= M && Npad >= N && Kpad >= 2 * K && Kpad % 64 == 0 && Kpad % 8 == 0);
+  CHECK_ARG(Mpad >= M && Npad >= N && Kpad >= 2 * K && Kpad % 32 == 0);
   cudaStream_t s = (cudaStream_t)stream;
   const i64 ta = (i64)L * M * ((Kpad + 7) / 8);
   // A side also zero-fills the K padding columns (groups beyond 2K read as 0)
   k_beaver_limbs_a<<<grid_for(ta), MPX_THREADS, 0, s>>>(A8, D, A, a_ps, L, M, K, Mpad, Kpad);
-  dim3 grid((unsigned)((Npad + 31) / 32), (unsigned)(Kpad / 64), (unsigned)L);
+  dim3 grid((unsigned)((Npad + 31) / 32), (unsigned)((Kpad + 63) / 64), (unsigned)L);
   CHECK_ARG(grid.y <= 65535);
   k_beaver_limbs_b<<<grid, 256, 0, s>>>(B8, B, b_ps, E, p0, K, N, Npad, Kpad);
   return launch_status();
@@ -870,6 +906,7 @@ __device__ __forceinline__ void ml_emit(uint8_t* base, i64 plane, const u64 (&w)
   const int rr = t >> 3, g = t & 7;
   u64 pl[8];
   bytes_transpose8(w, pl);
+  if (k0 + g * 8 >= Kp) return;  // Kp % 64 == 32: the last tile's upper half
   uint8_t* dst = base + (r0 + rr) * Kp + k0 + g * 8;
 #pragma unroll
   for (int i = 0; i < 8; ++i) *reinterpret_cast<u64*>(dst + i * plane) = pl[i];
@@ -916,8 +953,8 @@ extern "C" int mpx_mask_limbs(uint8_t* S8, uint8_t* P8, const uint64_t* X, int64
                               const uint64_t* T, int64_t t_ps, int64_t t_sr, int64_t t_sc, int L, int64_t R,
                               int64_t K, int64_t Rpad, int64_t Kp, int p0, int add_p0, int width, void* stream) {
   CHECK_ARG(S8 && P8 && X && T && L >= 1 && R >= 1 && K >= 1 && width >= 1 && width <= 64);
-  CHECK_ARG(Rpad >= R && Rpad % 32 == 0 && Kp >= K && Kp % 64 == 0);
-  CHECK_ARG(Rpad / 32 <= 0x7FFFFFFF && Kp / 64 <= 65535);
+  CHECK_ARG(Rpad >= R && Rpad % 32 == 0 && Kp >= K && Kp % 32 == 0);
+  CHECK_ARG(Rpad / 32 <= 0x7FFFFFFF && (Kp + 63) / 64 <= 65535);
   MaskLimbArgs a;
   a.X = X;
   a.x_ps = x_ps;
@@ -938,7 +975,7 @@ extern "C" int mpx_mask_limbs(uint8_t* S8, uint8_t* P8, const uint64_t* X, int64
   a.p0 = p0;
   a.add_p0 = add_p0;
   a.pad = 0;
-  dim3 grid((unsigned)(Rpad / 32), (unsigned)(Kp / 64));
+  dim3 grid((unsigned)(Rpad / 32), (unsigned)((Kp + 63) / 64));
   cudaStream_t s = (cudaStream_t)stream;
   const bool xk = x_sc == 1, tk = t_sc == 1;
   if (xk && tk)
@@ -972,15 +1009,17 @@ static PFN_encodeTiled get_encode() {
   return fn;
 }
 
-static int make_map(CUtensorMap* map, const uint8_t* base, i64 rows, i64 kbytes, int box_rows) {
+static int make_map(CUtensorMap* map, const uint8_t* base, i64 rows, i64 kbytes, int box_rows, int bk = TC_BK) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return MPX_ERR_CUDA;
   cuuint64_t dims[2] = {(cuuint64_t)kbytes, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)kbytes};
-  cuuint32_t box[2] = {TC_BK, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)bk, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapSwizzle sw = bk == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                          : (bk == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)base, dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? MPX_OK : MPX_ERR_CUDA;
 }
@@ -991,8 +1030,8 @@ static int make_map(CUtensorMap* map, const uint8_t* base, i64 rows, i64 kbytes,
 // Split-K for the persistent kernel: minimise waves x (k-blocks per unit +
 // per-unit epilogue cost) over the slice counts that keep every slice within
 // the exactness bound (<= 16384 of K per accumulator).
-static int tcp_auto_split(i64 tiles, int nk_total, int sms) {
-  const int need = (nk_total * TC_BK + 16383) / 16384;
+static int tcp_auto_split(i64 tiles, int nk_total, int sms, int bk = TC_BK) {
+  const int need = (nk_total * bk + 16383) / 16384;
   int best = need;
   double best_cost = 1e30;
   for (int s = need; s <= nk_total && s <= 64; ++s) {
@@ -1025,23 +1064,45 @@ static int num_sms() {
 // A8: [batch][8][Mpad][Kpad] u8, B8: [batch][8][Npad][Kpad] u8, zero padded;
 // Mpad % 128 == 0, Npad % 32 == 0, Kpad % 128 == 0. ksplit 0 = automatic
 // (width 64 only), >= 1 = forced slice count.
+template <int BK, int BN, bool ST>
+static int tcp_launch(unsigned g, cudaStream_t s, const CUtensorMap& mA, const CUtensorMap& mB,
+                      const CUtensorMap& mA2, const CUtensorMap& mB2, const TcArgs& a, int batch) {
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_gemm_limbs_tc_pers<BK, BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             tcp_smem_bytes(BK, BN, ST)) != cudaSuccess)
+      return MPX_ERR_CUDA;
+    attr = true;
+  }
+  k_gemm_limbs_tc_pers<BK, BN, ST><<<g, 192, tcp_smem_bytes(BK, BN, ST), s>>>(mA, mB, mA2, mB2, a, batch);
+  return launch_status();
+}
+
+// C[z] (+)= sum_{i+j<=7} 2^(8(i+j)) A8[z][i] @ B8[z][j]^T  (mod 2^width)
+// A8: [batch][8][Mpad][Kpad] u8, B8: [batch][8][Npad][Kpad] u8, zero padded;
+// Mpad % 128 == 0, Npad % 32 == 0, Kpad % 32 == 0 (k-block = the largest of
+// 128 / 64 / 32 bytes dividing Kpad). ksplit 0 = automatic (width 64 only),
+// >= 1 = forced slice count.
 static int gemm_limbs_impl(uint64_t* C, const uint8_t* A8, const uint8_t* B8, const uint8_t* A8s,
                            const uint8_t* B8s, int64_t batch, int64_t M, int64_t N, int64_t Mpad, int64_t Npad,
                            int64_t Kpad, int64_t ldc, int64_t sC, int accumulate, int width, int ksplit,
                            const uint64_t* Cin, int64_t sCin, void* stream) {
   CHECK_ARG(C && A8 && B8 && batch >= 1 && batch <= 65535 && M >= 1 && N >= 1 && width >= 1 && width <= 64);
   const bool split_ops = A8s != nullptr;
-  CHECK_ARG(!split_ops || (B8s && Kpad % (2 * TC_BK) == 0));
-  CHECK_ARG(Mpad % TC_BM == 0 && Npad % 32 == 0 && Kpad % TC_BK == 0 && Kpad >= TC_BK);
+  CHECK_ARG(Mpad % TC_BM == 0 && Npad % 32 == 0 && Kpad % 32 == 0 && Kpad >= 32);
+  const i64 kcols = split_ops ? Kpad / 2 : Kpad;  // split operands: each half its own plane set
+  const int bk = kcols % 128 == 0 ? 128 : (kcols % 64 == 0 ? 64 : 32);
+  CHECK_ARG(!split_ops || (B8s && Kpad % 2 == 0 && kcols % 32 == 0));
   CHECK_ARG(M <= Mpad && N <= Npad && ldc >= N);
   CHECK_ARG(batch * 8 * Mpad < (1ll << 31) && batch * 8 * Npad < (1ll << 31));
   CHECK_ARG(!(Cin && accumulate));
   cudaStream_t s = (cudaStream_t)stream;
-  const int nk_total = (int)(Kpad / TC_BK);
-  const bool legacy = getenv("MPX_TC_LEGACY") != nullptr && !split_ops;
-  const i64 ptiles = (Mpad / TC_BM) * ((Npad + TCP_BN - 1) / TCP_BN) * batch;
+  const int nk_total = (int)(Kpad / bk);
+  const bool legacy = getenv("MPX_TC_LEGACY") != nullptr && !split_ops && bk == TC_BK;
+  const int bn = Npad <= 32 ? 32 : 64;
+  const i64 ptiles = (Mpad / TC_BM) * ((Npad + bn - 1) / bn) * batch;
   if (ksplit < 1) {
-    CHECK_ARG(width == 64 || nk_total * TC_BK <= 16384);
+    CHECK_ARG(width == 64 || nk_total * bk <= 16384);
     if (width != 64) {
       ksplit = 1;
     } else if (legacy) {  // two waves of one-tile CTAs, every slice <= 16384 of K
@@ -1051,34 +1112,17 @@ static int gemm_limbs_impl(uint64_t* C, const uint8_t* A8, const uint8_t* B8, co
       ksplit = max(need, min(want, max(1, nk_total / 2)));
     } else {
       const char* force = getenv("MPX_TC_KSPLIT");  // sweeps / A-B timing
-      ksplit = force ? max(1, atoi(force)) : tcp_auto_split(ptiles, nk_total, num_sms());
-      ksplit = max(ksplit, (nk_total * TC_BK + 16383) / 16384);
+      ksplit = force ? max(1, atoi(force)) : tcp_auto_split(ptiles, nk_total, num_sms(), bk);
+      ksplit = max(ksplit, (nk_total * bk + 16383) / 16384);
     }
   }
   if (ksplit > nk_total) ksplit = nk_total;
   int nk_per = (nk_total + ksplit - 1) / ksplit;
   ksplit = (nk_total + nk_per - 1) / nk_per;
   // exactness: each CTA's s32 diagonal accumulators see at most 16384 of K
-  CHECK_ARG((i64)nk_per * TC_BK <= 16384);
+  CHECK_ARG((i64)nk_per * bk <= 16384);
   // split-K adds partials with wrapping 64-bit atomics: exact mod 2^64 only
   CHECK_ARG(ksplit == 1 || width == 64);
-  CUtensorMap mapA, mapB, mapA2, mapB2;
-  // split operands: each half is its own [.][8][rows][Kpad/2] plane set
-  const i64 kcols = split_ops ? Kpad / 2 : Kpad;
-  if (make_map(&mapA, A8, batch * 8 * Mpad, kcols, TC_BM) != MPX_OK) return MPX_ERR_CUDA;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(k_gemm_limbs_tc<TC_WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             tc_smem_bytes(TC_WIDE)) != cudaSuccess ||
-        cudaFuncSetAttribute(k_gemm_limbs_tc<TC_NARROW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             tc_smem_bytes(TC_NARROW)) != cudaSuccess ||
-        cudaFuncSetAttribute(k_gemm_limbs_tc_pers<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             tcp_smem_bytes(true)) != cudaSuccess ||
-        cudaFuncSetAttribute(k_gemm_limbs_tc_pers<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             tcp_smem_bytes(false)) != cudaSuccess)
-      return MPX_ERR_CUDA;
-    attr_set = true;
-  }
   TcArgs a;
   a.C = C;
   a.Cin = Cin;
@@ -1094,7 +1138,8 @@ static int gemm_limbs_impl(uint64_t* C, const uint8_t* A8, const uint8_t* B8, co
   a.ksplit = ksplit;
   a.accumulate = accumulate;
   a.msk = ring_mask(width);
-  a.kb_half = split_ops ? (int)(kcols / TC_BK) : 0;
+  a.kb_half = split_ops ? (int)(kcols / bk) : 0;
+  CUtensorMap mapA, mapB, mapA2, mapB2;
   if (!legacy) {
     // split slices meet in C through atomics: start from zero unless C is
     // the accumulate operand (the addend rides on slice 0)
@@ -1102,10 +1147,12 @@ static int gemm_limbs_impl(uint64_t* C, const uint8_t* A8, const uint8_t* B8, co
       for (i64 z = 0; z < batch; ++z)
         if (cudaMemset2DAsync(C + z * sC, (size_t)ldc * 8, 0, (size_t)N * 8, (size_t)M, s) != cudaSuccess)
           return MPX_ERR_CUDA;
-    if (make_map(&mapB, B8, batch * 8 * Npad, kcols, TCP_BN) != MPX_OK) return MPX_ERR_CUDA;
+    if (make_map(&mapA, A8, batch * 8 * Mpad, kcols, TC_BM, bk) != MPX_OK ||
+        make_map(&mapB, B8, batch * 8 * Npad, kcols, bn, bk) != MPX_OK)
+      return MPX_ERR_CUDA;
     if (split_ops) {
-      if (make_map(&mapA2, A8s, 8 * Mpad, kcols, TC_BM) != MPX_OK ||
-          make_map(&mapB2, B8s, 8 * Npad, kcols, TCP_BN) != MPX_OK)
+      if (make_map(&mapA2, A8s, 8 * Mpad, kcols, TC_BM, bk) != MPX_OK ||
+          make_map(&mapB2, B8s, 8 * Npad, kcols, bn, bk) != MPX_OK)
         return MPX_ERR_CUDA;
     } else {
       mapA2 = mapA;
@@ -1116,14 +1163,29 @@ static int gemm_limbs_impl(uint64_t* C, const uint8_t* A8, const uint8_t* B8, co
     // coalesced (smem-staged) stores when the epilogue is a large share of a
     // unit; direct per-row stores for long reductions
     const char* st = getenv("MPX_TC_STAGED");
-    const bool staged = st ? atoi(st) != 0 : nk_per <= TCP_STAGED_MAX_KB;
-    if (staged)
-      k_gemm_limbs_tc_pers<true><<<g, 192, tcp_smem_bytes(true), s>>>(mapA, mapB, mapA2, mapB2, a, (int)batch);
-    else
-      k_gemm_limbs_tc_pers<false><<<g, 192, tcp_smem_bytes(false), s>>>(mapA, mapB, mapA2, mapB2, a, (int)batch);
-    return launch_status();
+    const bool staged = st ? atoi(st) != 0 : (i64)nk_per * bk <= TCP_STAGED_MAX_KB * 128;
+    const int b = (int)batch;
+    if (bk == 128 && bn == 64)
+      return staged ? tcp_launch<128, 64, true>(g, s, mapA, mapB, mapA2, mapB2, a, b)
+                    : tcp_launch<128, 64, false>(g, s, mapA, mapB, mapA2, mapB2, a, b);
+    if (bk == 128) return tcp_launch<128, 32, true>(g, s, mapA, mapB, mapA2, mapB2, a, b);
+    if (bk == 64)
+      return bn == 64 ? tcp_launch<64, 64, true>(g, s, mapA, mapB, mapA2, mapB2, a, b)
+                      : tcp_launch<64, 32, true>(g, s, mapA, mapB, mapA2, mapB2, a, b);
+    return bn == 64 ? tcp_launch<32, 64, true>(g, s, mapA, mapB, mapA2, mapB2, a, b)
+                    : tcp_launch<32, 32, true>(g, s, mapA, mapB, mapA2, mapB2, a, b);
   }
   // legacy one-tile-per-CTA kernels (MPX_TC_LEGACY=1, for A/B timing)
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(k_gemm_limbs_tc<TC_WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             tc_smem_bytes(TC_WIDE)) != cudaSuccess ||
+        cudaFuncSetAttribute(k_gemm_limbs_tc<TC_NARROW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             tc_smem_bytes(TC_NARROW)) != cudaSuccess)
+      return MPX_ERR_CUDA;
+    attr_set = true;
+  }
+  if (make_map(&mapA, A8, batch * 8 * Mpad, Kpad, TC_BM) != MPX_OK) return MPX_ERR_CUDA;
   if (ksplit > 1 && Cin) {
     for (i64 z = 0; z < batch; ++z)
       if (cudaMemcpy2DAsync(C + z * sC, (size_t)ldc * 8, Cin + z * sCin, (size_t)ldc * 8, (size_t)N * 8,
@@ -1136,9 +1198,9 @@ static int gemm_limbs_impl(uint64_t* C, const uint8_t* A8, const uint8_t* B8, co
         return MPX_ERR_CUDA;
   }
   const bool narrow = (Npad % 64 != 0) || nk_per <= 2;
-  const int bn = narrow ? 32 : 64;
-  if (make_map(&mapB, B8, batch * 8 * Npad, Kpad, bn) != MPX_OK) return MPX_ERR_CUDA;
-  dim3 grid((unsigned)((Npad / bn) * (Mpad / TC_BM) * ksplit), 1, (unsigned)batch);
+  const int lbn = narrow ? 32 : 64;
+  if (make_map(&mapB, B8, batch * 8 * Npad, Kpad, lbn) != MPX_OK) return MPX_ERR_CUDA;
+  dim3 grid((unsigned)((Npad / lbn) * (Mpad / TC_BM) * ksplit), 1, (unsigned)batch);
   if (narrow)
     k_gemm_limbs_tc<TC_NARROW><<<grid, 192, tc_smem_bytes(TC_NARROW), s>>>(mapA, mapB, a);
   else
@@ -1161,7 +1223,7 @@ extern "C" int mpx_gemm_limbs_split(uint64_t* C, const uint8_t* PA8, const uint8
                                     const uint8_t* SB8, int64_t batch, int64_t M, int64_t N, int64_t Mpad,
                                     int64_t Npad, int64_t Kh, int64_t ldc, int64_t sC, int width, int ksplit,
                                     const uint64_t* Cin, int64_t sCin, void* stream) {
-  CHECK_ARG(SA8 && SB8 && Kh % TC_BK == 0);
+  CHECK_ARG(SA8 && SB8 && Kh % 32 == 0);
   return gemm_limbs_impl(C, PA8, PB8, SA8, SB8, batch, M, N, Mpad, Npad, 2 * Kh, ldc, sC, 0, width, ksplit, Cin,
                          sCin, stream);
 }

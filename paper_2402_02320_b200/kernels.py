@@ -375,6 +375,22 @@ def _rup(x, m):
     return (x + m - 1) // m * m
 
 
+def kpad(kbytes: int) -> int:
+    """Padded reduction length of a limb GEMM: the k-block is 32, 64 or 128
+    bytes (32B / 64B / 128B swizzle), so short reductions are not padded to 128."""
+    if kbytes <= 32:
+        return 32
+    if kbytes <= 64:
+        return 64
+    return _rup(kbytes, 128)
+
+
+def npad_tiles(n: int) -> int:
+    """Output columns the persistent kernel's N tiles cover (32-wide tile for
+    outputs up to 32 wide, 64-wide tiles otherwise)."""
+    return 32 if n <= 32 else _rup(n, 64)
+
+
 def limb_split(out, A, rows, cols, lda, plane, pitch, coff, trans):
     if _dry(out):
         return out

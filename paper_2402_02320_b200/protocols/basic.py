@@ -200,20 +200,25 @@ def session_dry(v) -> bool:
     return v.is_meta
 
 
+TC_MAX_WASTE = 2.2     # padded / useful MACs above which the SIMT kernel wins (conv1 fwd: 2.05 on TC)
+
+
 def _use_tc(m, k, r, w=64) -> bool:
-    """tcgen05 limb GEMM when the output fills its 128 x 64 tiles (padding
-    waste <= 1/3 on each side); thin or tiny products go to the SIMT kernel."""
-    if m < 96 or r < 24:
+    """tcgen05 limb GEMM when the padded work (128-row M tiles, 32/64-wide N
+    tiles, 32/64/128-byte k-blocks) stays within TC_MAX_WASTE of the useful
+    MACs; thin or tiny products go to the SIMT kernel."""
+    if m < 96 or r < 16 or m * 2 * k * r < K.TC_MIN_MACS or (w != 64 and 2 * k > K.TC_MAX_K):
         return False
-    waste = (K._rup(m, 128) / m) * (K._rup(r, 32) / r)
-    return waste <= 1.5 and K.tc_eligible(m, 2 * k, r, w) and (w == 64 or 2 * k <= K.TC_MAX_K)
+    waste = (K._rup(m, 128) / m) * (K.npad_tiles(r) / r) * (K.kpad(2 * k) / (2 * k))
+    return waste <= TC_MAX_WASTE
 
 
 def _fused_tc(session, m, k, r, w) -> bool:
     """Sim sessions run tcgen05-sized products as fused mask+limb split +
-    split-operand GEMM; below K = 64 the per-half padding would double the
-    MMA work, so those keep the concatenated-limb path."""
-    return session.fused and k > 64 and _use_tc(m, k, r, w)
+    split-operand GEMM, unless padding each K half separately (32 / 64 /
+    128-byte k-blocks) costs noticeably more MMA work than padding the
+    concatenated 2K (e.g. K = 10: 2 x 32 vs 32)."""
+    return session.fused and 2 * K.kpad(k) <= 1.1 * K.kpad(2 * k) and _use_tc(m, k, r, w)
 
 
 def _strides3(v):
@@ -229,7 +234,7 @@ def _beaver_matmul_fused_tc(session, Z, X, Y, A, B, C, L, m, k, r, w):
     once (shared by every party's GEMM) next to the per-party material limbs
     (A_l; B_l + [l==p0] E), and the split-operand GEMM computes
     Z_l = C_l + [D | A_l] @ [B_l + [l==p0] E ; E] (basic.py:66-75)."""
-    Mp, Np, Kh = K._rup(m, 128), K._rup(r, 32), K._rup(k, 128)
+    Mp, Np, Kh = K._rup(m, 128), K._rup(r, 32), K.kpad(k)
     dev = Z.device
     SA = torch.empty((8, Mp, Kh), dtype=torch.uint8, device=dev)
     PA = torch.empty((L, 8, Mp, Kh), dtype=torch.uint8, device=dev)
@@ -249,7 +254,7 @@ def _beaver_matmul_fused_tc(session, Z, X, Y, A, B, C, L, m, k, r, w):
 def _beaver_matmul_tc(session, Z, D, E, A, B, C, L, m, k, r, w):
     """Z_l += [D | A_l] @ [B_l + [l==p0] E ; E] as ONE tcgen05 limb GEMM per party
     (K doubled), so D@E at party 0 folds into its B operand (basic.py:72-75)."""
-    Mp, Np, Kp = K._rup(m, 128), K._rup(r, 32), K._rup(2 * k, 128)
+    Mp, Np, Kp = K._rup(m, 128), K._rup(r, 32), K.kpad(2 * k)
     A8 = torch.empty((L, 8, Mp, Kp), dtype=torch.uint8, device=Z.device)
     B8 = torch.empty((L, 8, Np, Kp), dtype=torch.uint8, device=Z.device)
     if Mp > m:

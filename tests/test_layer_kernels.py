@@ -187,3 +187,25 @@ def test_gemm_limbs_persistent_splits(K, mode, ks):
         for z in range(b):
             want = _mm(A[z], B[z]) + (C[z] if mode in ("cin", "acc") else np.uint64(0))
             assert np.array_equal(got[z], want), z
+
+
+@pytest.mark.parametrize("M,Kd,N,b", [(300, 20, 20, 3), (1000, 50, 30, 2), (700, 60, 100, 1), (256, 32, 64, 2),
+                                      (130, 100, 20, 1)])
+def test_gemm_limbs_short_k_blocks(K, M, Kd, N, b):
+    """32- and 64-byte k-blocks (32B / 64B swizzle) and the 32-wide N tile of
+    the persistent kernel; exact vs numpy with the C addend."""
+    rng = np.random.default_rng(M + Kd + N)
+    A, B, C = _rand(rng, (b, M, Kd), 64), _rand(rng, (b, Kd, N), 64), _rand(rng, (b, M, N), 64)
+    Mp, Np, Kp = K._rup(M, 128), K._rup(N, 32), K.kpad(Kd)
+    Ad, Bd, Cd = _dev(A), _dev(B), _dev(C)
+    A8 = torch.zeros((b, 8, Mp, Kp), dtype=torch.uint8, device="cuda")
+    B8 = torch.zeros((b, 8, Np, Kp), dtype=torch.uint8, device="cuda")
+    for z in range(b):
+        K.limb_split(A8[z], Ad.data_ptr() + 8 * z * M * Kd, M, Kd, Kd, Mp * Kp, Kp, 0, False)
+        K.limb_split(B8[z], Bd.data_ptr() + 8 * z * Kd * N, Kd, N, N, Np * Kp, Kp, 0, True)
+    Z = torch.full((b, M, N), 9, dtype=torch.int64, device="cuda")
+    K.gemm_limbs(Z, A8, B8, b, M, N, Mp, Np, Kp, N, M * N, False, 64, cin=Cd, s_cin=M * N)
+    got = _host(Z)
+    with np.errstate(over="ignore"):
+        for z in range(b):
+            assert np.array_equal(got[z], C[z] + _mm(A[z], B[z])), z

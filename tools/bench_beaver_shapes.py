@@ -47,7 +47,7 @@ def _tc_time(m, k, r, L):
     D, E = rnd(m, k), rnd(k, r)
     A, B, C = rnd(L, m, k), rnd(L, k, r), rnd(L, m, r)
     Z = torch.empty((L, m, r), dtype=torch.int64, device="cuda")
-    Mp, Np, Kp = K._rup(m, 128), K._rup(r, 32), K._rup(2 * k, 128)
+    Mp, Np, Kp = K._rup(m, 128), K._rup(r, 32), K.kpad(2 * k)
     A8 = torch.zeros((L, 8, Mp, Kp), dtype=torch.uint8, device="cuda")
     B8 = torch.empty((L, 8, Np, Kp), dtype=torch.uint8, device="cuda")
     K.beaver_limbs(A8, B8, D, E, A.data_ptr(), m * k, B.data_ptr(), k * r, L, m, k, r, Mp, Np, Kp, 0)
@@ -89,7 +89,7 @@ def main():
             lambda: K.beaver_gemm(Z, m * r, C.data_ptr(), m * r, D, E, A.data_ptr(), m * k, B.data_ptr(),
                                   k * r, L, m, k, r, 0, 64))
         Zs = Z.clone()
-        Mp, Np, Kp = K._rup(m, 128), K._rup(r, 32), K._rup(2 * k, 128)
+        Mp, Np, Kp = K._rup(m, 128), K._rup(r, 32), K.kpad(2 * k)
         A8 = torch.zeros((L, 8, Mp, Kp), dtype=torch.uint8, device="cuda")
         B8 = torch.empty((L, 8, Np, Kp), dtype=torch.uint8, device="cuda")
 
