@@ -121,6 +121,7 @@ struct TcArgs {
   int ksplit;    // CTAs per output tile along K; > 1 => wrapping atomic adds
   int accumulate;
   u64 msk;
+  int dbg;      // timing experiments (MPX_TC_DBG bits): 1 one diagonal, 2 no stores, 4 no MMA, 8 no addend, 16 no drain
   int kb_half;  // > 0: split operands (persistent kernel only): k-blocks
                 // [0, kb_half) pair shared A (mapA2) with party B (mapB),
                 // the rest party A (mapA) with shared B (mapB2)
@@ -354,11 +355,11 @@ __global__ void __launch_bounds__(192, BN == 32 ? 2 : 1)
 // 32B swizzle, so short reductions pad K to 32 or 64 instead of 128), BN =
 // N tile (64, or 32 for outputs at most 32 wide: 256 TMEM columns).
 #define TCP_BST 2
-#define TCP_STAGE_BYTES (4 * 32 * 33 * 8)  // one 32 x 32 u64 transpose tile per epilogue warp
+#define TCP_STAGE_TILE (32 * 33 * 8)  // one 32 x 32 u64 transpose tile per epilogue warp
 #define TCP_STAGED_MAX_KB 4
 constexpr int tcp_ast(int bk) { return 65536 / (TC_BM * bk); }  // 64 KB A ring
-constexpr int tcp_smem_bytes(int bk, int bn, bool staged) {
-  return tcp_ast(bk) * TC_BM * bk + TCP_BST * 8 * bn * bk + (staged ? TCP_STAGE_BYTES : 0) + 1024 + 512;
+constexpr int tcp_smem_bytes(int bk, int bn, bool staged, int ew) {
+  return tcp_ast(bk) * TC_BM * bk + TCP_BST * 8 * bn * bk + (staged ? ew * TCP_STAGE_TILE : 0) + 1024 + 512;
 }
 
 // K-major UMMA shared-memory descriptor for a BK-byte-row swizzled tile
@@ -402,8 +403,11 @@ __device__ __forceinline__ TcpUnit tcp_unit(int u, const TcArgs& a, int tiles_m,
   return t;
 }
 
-template <int BK, int BN, bool STAGED>
-__global__ void __launch_bounds__(192, 1)
+// EW = epilogue warps: 4 (one per TMEM lane quarter, all column chunks) or
+// 8 (two per quarter, one 32-column chunk each: twice the TMEM drain and
+// store parallelism for short reductions, where the epilogue paces a unit).
+template <int BK, int BN, bool STAGED, int EW>
+__global__ void __launch_bounds__(64 + 32 * EW, 1)
     k_gemm_limbs_tc_pers(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                          const __grid_constant__ CUtensorMap mapA2, const __grid_constant__ CUtensorMap mapB2,
                          TcArgs args, int batch) {
@@ -419,7 +423,7 @@ __global__ void __launch_bounds__(192, 1)
   uint8_t* sB = smem + AST * A_TILE;
   u64* stage_all = reinterpret_cast<u64*>(sB + BST * B_STAGE);
   uint64_t* bars =
-      reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stage_all) + (STAGED ? TCP_STAGE_BYTES : 0));
+      reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stage_all) + (STAGED ? EW * TCP_STAGE_TILE : 0));
   uint64_t* fullA = bars;
   uint64_t* emptyA = bars + AST;
   uint64_t* fullB = bars + 2 * AST;
@@ -443,7 +447,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&emptyB[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 4);  // one arrival per epilogue warp
+    mbar_init(tempty, EW);  // one arrival per epilogue warp
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
@@ -528,7 +532,7 @@ __global__ void __launch_bounds__(192, 1)
               const uint64_t bd = bd0 + (uint64_t)((j * B_TILE) >> 4);
 #pragma unroll
               for (int kk = 0; kk < BK / 32; ++kk)
-                mma_i8(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, (i > 0 || kk > 0) ? 1u : first);
+                if (!(args.dbg & 4)) mma_i8(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, (i > 0 || kk > 0) ? 1u : first);
             }
             umma_commit(&emptyA[as]);
             if (++as == AST) {
@@ -542,9 +546,14 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    // ---------------- epilogue: warps 2..5 ----------------
-    // TMEM lane = tile row: a thread owns one output row of the tile.
+    // ---------------- epilogue: warps 2..(1 + EW) ----------------
+    // TMEM lane = tile row: a thread owns one output row of the tile; with
+    // 8 warps the second four take the second 32-column chunk.
+    static_assert(EW == 4 || (EW == 8 && BN == 64 && STAGED), "8 epilogue warps: staged 64-wide tiles");
     const int sp = warp & 3;
+    const int ew = warp - 2;
+    constexpr int NCW = EW == 8 ? 1 : NC;  // chunks per warp
+    const int c0 = EW == 8 ? (ew >> 2) : 0;
     int it = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
       const TcpUnit t = tcp_unit(u, args, tiles_m, tiles_n, BN);
@@ -556,16 +565,16 @@ __global__ void __launch_bounds__(192, 1)
       // split slices meet in C through atomics (zeroed, or holding the
       // accumulate operand); slice 0 carries the Cin addend
       const u64* src = atom ? (t.ks == 0 ? Cin : nullptr) : (Cin ? Cin : (args.accumulate ? Cz : nullptr));
-      u64* stage = stage_all + sp * (32 * 33);
+      u64* stage = stage_all + ew * (32 * 33);
       if constexpr (STAGED) {
-        // chunk 0's addend block lands in the transpose tile (cp.async,
-        // coalesced along the row) while the MMAs are still running
-        const int col = t.n0 + lane;
+        // the first chunk's addend block lands in the transpose tile
+        // (cp.async, coalesced along the row) while the MMAs still run
+        const int col = t.n0 + c0 * 32 + lane;
         const int rows = col < args.N ? rmax : 0;
 #pragma unroll 8
         for (int r = 0; r < 32; ++r) {
           const u64* g = src + (i64)r * args.ldc + col;
-          const uint32_t sz = (src && r < rows) ? 8u : 0u;  // 0: zero-fill
+          const uint32_t sz = (src && r < rows && !(args.dbg & 8)) ? 8u : 0u;  // 0: zero-fill
           asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(stage + r * 33 + lane)),
                        "l"(sz ? g : args.C), "r"(sz)
                        : "memory");
@@ -580,6 +589,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int q = 0; q < 32; ++q) acc[q] = 0;
 #pragma unroll
         for (int d = 0; d < 8; ++d) {
+          if (((args.dbg & 1) && d > 0) || (args.dbg & 16)) break;  // timing experiments only (wrong results)
           uint32_t v[32];
           const uint32_t taddr = tmem_base + ((uint32_t)(sp * 32) << 16) + (uint32_t)(d * BN + c * 32);
           TMEM_LD32(taddr, v);
@@ -625,16 +635,28 @@ __global__ void __launch_bounds__(192, 1)
       // and chunk 1 in registers, so TMEM is released before any global
       // traffic.
       u64 hold[32];
-      drain(0, hold);
-      asm volatile("cp.async.wait_all;" ::: "memory");
-      __syncwarp();
+      drain(c0, hold);
+      if constexpr (NCW > 1) {
+        u64 hold1[32];
+        drain(1, hold1);
+        release();  // TMEM free before waiting on any global traffic
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
 #pragma unroll
-      for (int q = 0; q < 32; ++q) stage[lane * 33 + q] += hold[q];  // thread = row, q = column
-      if constexpr (NC > 1) drain(1, hold);
-      release();
+        for (int q = 0; q < 32; ++q) stage[lane * 33 + q] += hold[q];  // thread = row, q = column
 #pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        if (c == 1) {  // chunk 1 waited in registers; its addend is read now
+        for (int q = 0; q < 32; ++q) hold[q] = hold1[q];
+      } else {
+        release();
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 32; ++q) stage[lane * 33 + q] += hold[q];
+      }
+#pragma unroll
+      for (int cc = 0; cc < NCW; ++cc) {
+        const int c = c0 + cc;
+        if (cc == 1) {  // chunk 1 waited in registers; its addend is read now
           __syncwarp();
 #pragma unroll
           for (int q = 0; q < 32; ++q) stage[lane * 33 + q] = hold[q];
@@ -645,10 +667,10 @@ __global__ void __launch_bounds__(192, 1)
         // all 32 addend loads in flight before the stores that use them
         u64 add[32];
 #pragma unroll
-        for (int r = 0; r < 32; ++r) add[r] = (c == 1 && src && r < rows) ? src[(i64)r * args.ldc + col] : 0ull;
+        for (int r = 0; r < 32; ++r) add[r] = (cc == 1 && src && r < rows) ? src[(i64)r * args.ldc + col] : 0ull;
 #pragma unroll
         for (int r = 0; r < 32; ++r) {
-          if (r < rows) {
+          if (r < rows && !(args.dbg & 2)) {
             const u64 v = stage[r * 33 + lane] + add[r];
             u64* dst = Cz + (i64)r * args.ldc + col;
             if (atom)
@@ -912,18 +934,20 @@ __device__ __forceinline__ void ml_emit(uint8_t* base, i64 plane, const u64 (&w)
   for (int i = 0; i < 8; ++i) *reinterpret_cast<u64*>(dst + i * plane) = pl[i];
 }
 
-// Every source is read exactly once: party limbs are emitted as soon as the
-// party's material is loaded, except party p0's when S must be added (kept
-// in registers until S is complete).
+// Party limbs are emitted as soon as the party's material is loaded; party
+// p0's, when S must be added, is emitted last from a second (L2-hot) read of
+// its material tile, which keeps the register footprint small enough for
+// three CTAs per SM.
 template <bool XK, bool TK>
-__global__ void __launch_bounds__(256, 2) k_mask_limbs(MaskLimbArgs a) {
+__global__ void __launch_bounds__(256, 3) k_mask_limbs(MaskLimbArgs a) {
   __shared__ u64 tile[64][33];
   const i64 r0 = (i64)blockIdx.x * 32, k0 = (i64)blockIdx.y * 64;
   const int t = threadIdx.x;
   const i64 plane = a.Rpad * a.Kp;
-  u64 s[8], keep[8];
+  const bool defer = a.add_p0 && a.p0 >= 0;
+  u64 s[8];
 #pragma unroll
-  for (int c = 0; c < 8; ++c) s[c] = keep[c] = 0;
+  for (int c = 0; c < 8; ++c) s[c] = 0;
   for (int l = 0; l < a.L; ++l) {
     u64 v[8];
     ml_load8<XK>(v, a.X + (i64)l * a.x_ps, a.x_sr, a.x_sc, r0, k0, a.R, a.K, tile, t);
@@ -932,20 +956,17 @@ __global__ void __launch_bounds__(256, 2) k_mask_limbs(MaskLimbArgs a) {
     ml_load8<TK>(v, a.T + (i64)l * a.t_ps, a.t_sr, a.t_sc, r0, k0, a.R, a.K, tile, t);
 #pragma unroll
     for (int c = 0; c < 8; ++c) s[c] -= v[c];
-    if (a.add_p0 && l == a.p0) {
-#pragma unroll
-      for (int c = 0; c < 8; ++c) keep[c] = v[c];
-    } else {
-      ml_emit(a.P8 + (i64)l * 8 * plane, plane, v, r0, k0, a.Kp, t);
-    }
+    if (!(defer && l == a.p0)) ml_emit(a.P8 + (i64)l * 8 * plane, plane, v, r0, k0, a.Kp, t);
   }
 #pragma unroll
   for (int c = 0; c < 8; ++c) s[c] &= a.msk;
   ml_emit(a.S8, plane, s, r0, k0, a.Kp, t);
-  if (a.add_p0 && a.p0 >= 0) {
+  if (defer) {
+    u64 v[8];
+    ml_load8<TK>(v, a.T + (i64)a.p0 * a.t_ps, a.t_sr, a.t_sc, r0, k0, a.R, a.K, tile, t);
 #pragma unroll
-    for (int c = 0; c < 8; ++c) keep[c] = (keep[c] + s[c]) & a.msk;
-    ml_emit(a.P8 + (i64)a.p0 * 8 * plane, plane, keep, r0, k0, a.Kp, t);
+    for (int c = 0; c < 8; ++c) v[c] = (v[c] + s[c]) & a.msk;
+    ml_emit(a.P8 + (i64)a.p0 * 8 * plane, plane, v, r0, k0, a.Kp, t);
   }
 }
 
@@ -1040,7 +1061,8 @@ static int tcp_auto_split(i64 tiles, int nk_total, int sms, int bk = TC_BK) {
     if (se != s) continue;
     const i64 units = tiles * se;
     const i64 waves = (units + sms - 1) / sms;
-    const double epi = se > 1 ? 1.0 : 0.5;  // atomics cost more than plain stores
+    // epilogue (TMEM drain + stores) in k-blocks; atomics cost more than stores
+    const double epi = (se > 1 ? 1.0 : 0.5) * (128.0 / bk);
     const double cost = (double)waves * (per + epi);
     if (cost < best_cost - 1e-9) {
       best_cost = cost;
@@ -1064,17 +1086,19 @@ static int num_sms() {
 // A8: [batch][8][Mpad][Kpad] u8, B8: [batch][8][Npad][Kpad] u8, zero padded;
 // Mpad % 128 == 0, Npad % 32 == 0, Kpad % 128 == 0. ksplit 0 = automatic
 // (width 64 only), >= 1 = forced slice count.
-template <int BK, int BN, bool ST>
+template <int BK, int BN, bool ST, int EW = 4>
 static int tcp_launch(unsigned g, cudaStream_t s, const CUtensorMap& mA, const CUtensorMap& mB,
                       const CUtensorMap& mA2, const CUtensorMap& mB2, const TcArgs& a, int batch) {
   static bool attr = false;
+  constexpr int smem = tcp_smem_bytes(BK, BN, ST, EW);
+  static_assert(smem <= 232448, "shared memory budget");
   if (!attr) {
-    if (cudaFuncSetAttribute(k_gemm_limbs_tc_pers<BK, BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             tcp_smem_bytes(BK, BN, ST)) != cudaSuccess)
+    if (cudaFuncSetAttribute(k_gemm_limbs_tc_pers<BK, BN, ST, EW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem) != cudaSuccess)
       return MPX_ERR_CUDA;
     attr = true;
   }
-  k_gemm_limbs_tc_pers<BK, BN, ST><<<g, 192, tcp_smem_bytes(BK, BN, ST), s>>>(mA, mB, mA2, mB2, a, batch);
+  k_gemm_limbs_tc_pers<BK, BN, ST, EW><<<g, 64 + 32 * EW, smem, s>>>(mA, mB, mA2, mB2, a, batch);
   return launch_status();
 }
 
@@ -1091,34 +1115,47 @@ static int gemm_limbs_impl(uint64_t* C, const uint8_t* A8, const uint8_t* B8, co
   const bool split_ops = A8s != nullptr;
   CHECK_ARG(Mpad % TC_BM == 0 && Npad % 32 == 0 && Kpad % 32 == 0 && Kpad >= 32);
   const i64 kcols = split_ops ? Kpad / 2 : Kpad;  // split operands: each half its own plane set
-  const int bk = kcols % 128 == 0 ? 128 : (kcols % 64 == 0 ? 64 : 32);
+  int bk = kcols % 128 == 0 ? 128 : (kcols % 64 == 0 ? 64 : 32);
   CHECK_ARG(!split_ops || (B8s && Kpad % 2 == 0 && kcols % 32 == 0));
   CHECK_ARG(M <= Mpad && N <= Npad && ldc >= N);
   CHECK_ARG(batch * 8 * Mpad < (1ll << 31) && batch * 8 * Npad < (1ll << 31));
   CHECK_ARG(!(Cin && accumulate));
   cudaStream_t s = (cudaStream_t)stream;
-  const int nk_total = (int)(Kpad / bk);
   const bool legacy = getenv("MPX_TC_LEGACY") != nullptr && !split_ops && bk == TC_BK;
   const int bn = Npad <= 32 ? 32 : 64;
   const i64 ptiles = (Mpad / TC_BM) * ((Npad + bn - 1) / bn) * batch;
-  if (ksplit < 1) {
-    CHECK_ARG(width == 64 || nk_total * bk <= 16384);
-    if (width != 64) {
-      ksplit = 1;
-    } else if (legacy) {  // two waves of one-tile CTAs, every slice <= 16384 of K
-      const i64 t64 = (Mpad / TC_BM) * (Npad / 64) * batch;
-      const int need = (nk_total * TC_BK + 16383) / 16384;
-      const int want = (int)max((i64)1, (2 * (i64)num_sms()) / max((i64)1, t64));
-      ksplit = max(need, min(want, max(1, nk_total / 2)));
-    } else {
-      const char* force = getenv("MPX_TC_KSPLIT");  // sweeps / A-B timing
-      ksplit = force ? max(1, atoi(force)) : tcp_auto_split(ptiles, nk_total, num_sms(), bk);
-      ksplit = max(ksplit, (nk_total * bk + 16383) / 16384);
+  const int ks_req = ksplit;
+  int nk_total = 0, nk_per = 0;
+  auto plan = [&](int kb) -> int {
+    nk_total = (int)(Kpad / kb);
+    ksplit = ks_req;
+    if (ksplit < 1) {
+      if (width != 64) {
+        ksplit = 1;
+      } else if (legacy) {  // two waves of one-tile CTAs, every slice <= 16384 of K
+        const i64 t64 = (Mpad / TC_BM) * (Npad / 64) * batch;
+        const int need = (nk_total * TC_BK + 16383) / 16384;
+        const int want = (int)max((i64)1, (2 * (i64)num_sms()) / max((i64)1, t64));
+        ksplit = max(need, min(want, max(1, nk_total / 2)));
+      } else {
+        const char* force = getenv("MPX_TC_KSPLIT");  // sweeps / A-B timing
+        ksplit = force ? max(1, atoi(force)) : tcp_auto_split(ptiles, nk_total, num_sms(), kb);
+        ksplit = max(ksplit, (nk_total * kb + 16383) / 16384);
+      }
     }
+    if (ksplit > nk_total) ksplit = nk_total;
+    nk_per = (nk_total + ksplit - 1) / ksplit;
+    ksplit = (nk_total + nk_per - 1) / nk_per;
+    return ksplit;
+  };
+  CHECK_ARG(ksplit >= 1 || width == 64 || Kpad <= 16384);
+  plan(bk);
+  const char* st = getenv("MPX_TC_STAGED");
+  bool staged = st ? atoi(st) != 0 : (i64)nk_per * bk <= TCP_STAGED_MAX_KB * 128;
+  if (!legacy && staged && bn == 64 && bk == 128) {
+    bk = 64;  // staged 64-wide tiles run 64-byte k-blocks (room for 8 epilogue warps)
+    plan(bk);
   }
-  if (ksplit > nk_total) ksplit = nk_total;
-  int nk_per = (nk_total + ksplit - 1) / ksplit;
-  ksplit = (nk_total + nk_per - 1) / nk_per;
   // exactness: each CTA's s32 diagonal accumulators see at most 16384 of K
   CHECK_ARG((i64)nk_per * bk <= 16384);
   // split-K adds partials with wrapping 64-bit atomics: exact mod 2^64 only
@@ -1139,6 +1176,7 @@ static int gemm_limbs_impl(uint64_t* C, const uint8_t* A8, const uint8_t* B8, co
   a.accumulate = accumulate;
   a.msk = ring_mask(width);
   a.kb_half = split_ops ? (int)(kcols / bk) : 0;
+  a.dbg = getenv("MPX_TC_DBG") ? atoi(getenv("MPX_TC_DBG")) : 0;
   CUtensorMap mapA, mapB, mapA2, mapB2;
   if (!legacy) {
     // split slices meet in C through atomics: start from zero unless C is
@@ -1162,18 +1200,18 @@ static int gemm_limbs_impl(uint64_t* C, const uint8_t* A8, const uint8_t* B8, co
     const unsigned g = (unsigned)min(units, (i64)num_sms());
     // coalesced (smem-staged) stores when the epilogue is a large share of a
     // unit; direct per-row stores for long reductions
-    const char* st = getenv("MPX_TC_STAGED");
-    const bool staged = st ? atoi(st) != 0 : (i64)nk_per * bk <= TCP_STAGED_MAX_KB * 128;
     const int b = (int)batch;
-    if (bk == 128 && bn == 64)
-      return staged ? tcp_launch<128, 64, true>(g, s, mapA, mapB, mapA2, mapB2, a, b)
-                    : tcp_launch<128, 64, false>(g, s, mapA, mapB, mapA2, mapB2, a, b);
-    if (bk == 128) return tcp_launch<128, 32, true>(g, s, mapA, mapB, mapA2, mapB2, a, b);
-    if (bk == 64)
-      return bn == 64 ? tcp_launch<64, 64, true>(g, s, mapA, mapB, mapA2, mapB2, a, b)
-                      : tcp_launch<64, 32, true>(g, s, mapA, mapB, mapA2, mapB2, a, b);
-    return bn == 64 ? tcp_launch<32, 64, true>(g, s, mapA, mapB, mapA2, mapB2, a, b)
-                    : tcp_launch<32, 32, true>(g, s, mapA, mapB, mapA2, mapB2, a, b);
+    if (bk == 128 && bn == 64 && !staged)
+      return tcp_launch<128, 64, false>(g, s, mapA, mapB, mapA2, mapB2, a, b);
+    if (bk == 128 && bn == 32) return tcp_launch<128, 32, true>(g, s, mapA, mapB, mapA2, mapB2, a, b);
+    if (bn == 64) {
+      // staged 64-wide tiles: 64-byte k-blocks leave room for 8 epilogue
+      // warps' transpose tiles (short reductions are epilogue-paced)
+      if (bk == 32) return tcp_launch<32, 64, true, 8>(g, s, mapA, mapB, mapA2, mapB2, a, b);
+      return tcp_launch<64, 64, true, 8>(g, s, mapA, mapB, mapA2, mapB2, a, b);
+    }
+    if (bk == 64) return tcp_launch<64, 32, true>(g, s, mapA, mapB, mapA2, mapB2, a, b);
+    return tcp_launch<32, 32, true>(g, s, mapA, mapB, mapA2, mapB2, a, b);
   }
   // legacy one-tile-per-CTA kernels (MPX_TC_LEGACY=1, for A/B timing)
   static bool attr_set = false;

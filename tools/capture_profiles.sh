@@ -15,8 +15,8 @@ python tools/bench_train.py --graph --steps 3 > $OUT/bench_train.json 2>&1 || ex
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/lenet_launches.csv \
     python tools/bench_train.py --graph --steps 1 > $OUT/ncu_launches.log 2>&1
 ncu --set full --clock-control none \
-    -k regex:"k_gemm_limbs_tc|k_relu_fused|k_beaver_gemm|k_mask_sub|k_trunc_fused|k_beaver_limbs_a" \
-    --launch-skip 6 --launch-count 30 -o $OUT/lenet_full python tools/bench_train.py --graph --steps 1 \
+    -k regex:"k_gemm_limbs_tc|k_mask_limbs|k_relu_fused|k_beaver_gemm|k_mask_sub|k_trunc_fused|k_beaver_limbs_a" \
+    --launch-skip 6 --launch-count 40 -o $OUT/lenet_full python tools/bench_train.py --graph --steps 1 \
     > $OUT/ncu_lenet_full.log 2>&1
 reduce lenet_full
 fi
