@@ -320,6 +320,13 @@ int mpx_relu_fused(uint64_t* y, uint64_t* s_out, const uint64_t* x, int64_t n, c
 /* One max tournament level (derived.py:152-170): win = v + bit2a(gt(u, v)) * (u - v). */
 int mpx_maxlevel_fused(uint64_t* win, const uint64_t* u, const uint64_t* v, int64_t n,
                        const void* tape_host, const void* params_host, void* stream);
+/* A whole max_vec tournament (derived.py:152-170) of `rows` rows of width d0
+ * (<= 512) in one launch: one CTA per row, level by level in shared memory;
+ * `levels_host` holds each level's first tape index (the per-level tapes
+ * concatenated, so material order equals the per-level kernels'). */
+int mpx_maxtour_fused(uint64_t* y, const uint64_t* x, int64_t rows, int d0, const void* tape_host,
+                      const void* levels_host, const void* params_host, void* stream);
+int mpx_fused_tour_size(int64_t* levels);
 int mpx_fused_abi_sizes(int64_t* matref, int64_t* tape, int64_t* params, int64_t* tape_max);
 
 /* ---- trusted dealer (preprocessing.py:121-174; ring.py:124-134) ----

@@ -13,7 +13,7 @@
 // [e*per, e*per + per) — the reference's flattened C order.
 #include "common.cuh"
 
-#define TAPE_MAX 64
+#define TAPE_MAX 160  // a whole max_vec tournament (<= 10 levels of ~9 takes) fits one tape
 
 struct MatRef {
   const u64* p0;  // triple a | bintriple a | dabit/edabit arithmetic part
@@ -755,6 +755,29 @@ __global__ void __launch_bounds__(128, MPX_CMP_MINB) k_relu_fused(u64* __restric
 // One max_vec tournament level (derived.py:152-170) on pairs (u, v):
 // b = gt(u, v) (sign of v - u), s = bit2a(b), winner = v + s * (u - v).
 template <int L>
+__device__ __forceinline__ Sh<L> d_maxpair(const Sh<L>& u, const Sh<L>& v, const Tape& tape, int& ti, i64 e, int w,
+                                           int p0, u64 msk) {
+  Sh<L> diff, uv;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    diff.v[l] = (v.v[l] - u.v[l]) & msk;
+    uv.v[l] = (u.v[l] - v.v[l]) & msk;
+  }
+  const Sh<L> bits = d_decompose<L>(diff, w, tape, ti, e, p0);
+  Sh<L> sign;
+#pragma unroll
+  for (int l = 0; l < L; ++l) sign.v[l] = (bits.v[l] >> (w - 1)) & 1ull;
+  const MatRef& tb = next_take<L>(tape, ti, e);
+  const u64 c = d_bit2a_open<L>(sign, 1, tb, e);
+  const Sh<L> sa = d_bit2a_get<L>(c, 0, 1, tb, e, p0, msk);
+  const Sh<L> m = d_mul<L>(sa, uv, next_take<L>(tape, ti, e), e, p0, msk);
+  Sh<L> out;
+#pragma unroll
+  for (int l = 0; l < L; ++l) out.v[l] = (v.v[l] + m.v[l]) & msk;
+  return out;
+}
+
+template <int L>
 __global__ void __launch_bounds__(128, MPX_CMP_MINB) k_maxlevel_fused(u64* __restrict__ win, const u64* __restrict__ uin,
                                                         const u64* __restrict__ vin, i64 n,
                                                         const __grid_constant__ Tape tape, FusedParams P) {
@@ -766,25 +789,93 @@ __global__ void __launch_bounds__(128, MPX_CMP_MINB) k_maxlevel_fused(u64* __res
       for (int i = 0; i < tape.n; ++i) prefetch_take<L>(tape.m[i], e);
     const Sh<L> u = load_sh<L>(uin, n, e);
     const Sh<L> v = load_sh<L>(vin, n, e);
-    Sh<L> diff, uv;
-#pragma unroll
-    for (int l = 0; l < L; ++l) {
-      diff.v[l] = (v.v[l] - u.v[l]) & msk;
-      uv.v[l] = (u.v[l] - v.v[l]) & msk;
-    }
-    const Sh<L> bits = d_decompose<L>(diff, w, tape, ti, e, p0);
-    Sh<L> sign;
-#pragma unroll
-    for (int l = 0; l < L; ++l) sign.v[l] = (bits.v[l] >> (w - 1)) & 1ull;
-    const MatRef& tb = next_take<L>(tape, ti, e);
-    const u64 c = d_bit2a_open<L>(sign, 1, tb, e);
-    const Sh<L> sa = d_bit2a_get<L>(c, 0, 1, tb, e, p0, msk);
-    const Sh<L> m = d_mul<L>(sa, uv, next_take<L>(tape, ti, e), e, p0, msk);
-    Sh<L> out;
-#pragma unroll
-    for (int l = 0; l < L; ++l) out.v[l] = (v.v[l] + m.v[l]) & msk;
-    store_sh<L>(win, n, e, out);
+    store_sh<L>(win, n, e, d_maxpair<L>(u, v, tape, ti, e, w, p0, msk));
   }
+}
+
+// The whole max_vec tournament of a row in one CTA (derived.py:152-170): the
+// row's values sit in shared memory; level by level, thread j < half plays
+// pair (j, half + j) with the level's takes at element e = row * half + j
+// (the per-level kernel's flat index, so material use is identical), and an
+// odd leftover moves down behind the winners. One launch per max_vec instead
+// of one per level (7 for the attention's 128-wide rows).
+struct TourLevels {
+  int start[17];  // tape index of each level's first take; start[nlev] = tape.n
+  int nlev;
+};
+
+template <int L>
+__global__ void __launch_bounds__(256) k_maxtour_fused(u64* __restrict__ out, const u64* __restrict__ in, i64 rows,
+                                                       int d0, const __grid_constant__ Tape tape,
+                                                       const __grid_constant__ TourLevels lv, FusedParams P) {
+  extern __shared__ u64 vals[];  // [L][d0]
+  const int w = P.w, p0 = P.p0;
+  const u64 msk = ring_mask(w);
+  for (i64 row = blockIdx.x; row < rows; row += gridDim.x) {
+    for (int c = threadIdx.x; c < d0; c += blockDim.x)
+#pragma unroll
+      for (int l = 0; l < L; ++l) vals[l * d0 + c] = in[((i64)l * rows + row) * d0 + c];
+    __syncthreads();
+    int d = d0;
+    for (int lev = 0; lev < lv.nlev; ++lev) {
+      const int half = d / 2;
+      const int rest = d - 2 * half;
+      // thread j plays pair j (blockDim >= d0 / 2)
+      const int j = threadIdx.x;
+      Sh<L> win;
+      if (j < half) {
+        int ti = lv.start[lev];
+        const i64 e = row * (i64)half + j;
+        if (P.pf)
+          for (int i = lv.start[lev]; i < lv.start[lev + 1]; ++i) prefetch_take<L>(tape.m[i], e);
+        Sh<L> u, v;
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+          u.v[l] = vals[l * d0 + j];
+          v.v[l] = vals[l * d0 + half + j];
+        }
+        win = d_maxpair<L>(u, v, tape, ti, e, w, p0, msk);
+      }
+      Sh<L> rv;
+      if (threadIdx.x == 0 && rest)
+#pragma unroll
+        for (int l = 0; l < L; ++l) rv.v[l] = vals[l * d0 + 2 * half];
+      __syncthreads();
+      if (j < half)
+#pragma unroll
+        for (int l = 0; l < L; ++l) vals[l * d0 + j] = win.v[l];
+      if (threadIdx.x == 0 && rest)
+#pragma unroll
+        for (int l = 0; l < L; ++l) vals[l * d0 + half] = rv.v[l];
+      __syncthreads();
+      d = half + rest;
+    }
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int l = 0; l < L; ++l) out[(i64)l * rows + row] = vals[l * d0];
+    __syncthreads();
+  }
+}
+
+extern "C" int mpx_maxtour_fused(uint64_t* y, const uint64_t* x, int64_t rows, int d0, const void* tape_host,
+                                 const void* levels_host, const void* params_host, void* stream) {
+  CHECK_ARG(y && x && rows >= 0 && d0 >= 2 && d0 <= 512 && tape_host && levels_host && params_host);
+  const Tape& tp = *(const Tape*)tape_host;
+  const TourLevels& lv = *(const TourLevels*)levels_host;
+  const FusedParams& P = *(const FusedParams*)params_host;
+  CHECK_ARG(tp.n >= 1 && tp.n <= TAPE_MAX && lv.nlev >= 1 && lv.nlev <= 16 && P.L >= 1 && P.L <= 4);
+  if (rows == 0) return MPX_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int threads = min(256, max(32, ((d0 / 2 + 31) / 32) * 32));
+  const unsigned g = (unsigned)min(rows, (i64)(148 * 16));
+  const size_t sm = (size_t)P.L * d0 * 8;
+  switch (P.L) {
+    case 1: k_maxtour_fused<1><<<g, threads, sm, s>>>(y, x, rows, d0, tp, lv, P); break;
+    case 2: k_maxtour_fused<2><<<g, threads, sm, s>>>(y, x, rows, d0, tp, lv, P); break;
+    case 3: k_maxtour_fused<3><<<g, threads, sm, s>>>(y, x, rows, d0, tp, lv, P); break;
+    default: k_maxtour_fused<4><<<g, threads, sm, s>>>(y, x, rows, d0, tp, lv, P); break;
+  }
+  return launch_status();
 }
 
 // ---------------------------------------------------------------------------
@@ -839,6 +930,11 @@ DEFINE_LAUNCH2(mpx_maxlevel_fused, k_maxlevel_fused, const uint64_t*, const uint
 DEFINE_LAUNCH(mpx_exp_fused, k_exp_fused)
 DEFINE_LAUNCH(mpx_log_fused, k_log_fused)
 DEFINE_LAUNCH(mpx_attexp_fused, k_attexp_fused)
+
+extern "C" int mpx_fused_tour_size(int64_t* levels) {
+  *levels = sizeof(TourLevels);
+  return MPX_OK;
+}
 
 extern "C" int mpx_fused_abi_sizes(int64_t* matref, int64_t* tape, int64_t* params, int64_t* tape_max) {
   *matref = sizeof(MatRef);

@@ -25,7 +25,7 @@ from .preprocessing import ArithMat, BitMat, BitTriples
 from .ring import encode_scalar
 from .sharing import AShare
 
-TAPE_MAX = 64
+TAPE_MAX = 160
 
 
 class MatRef(ctypes.Structure):
@@ -37,6 +37,10 @@ class MatRef(ctypes.Structure):
 
 class Tape(ctypes.Structure):
     _fields_ = [("m", MatRef * TAPE_MAX), ("n", ctypes.c_int)]
+
+
+class TourLevels(ctypes.Structure):
+    _fields_ = [("start", ctypes.c_int * 17), ("nlev", ctypes.c_int)]
 
 
 class FusedParams(ctypes.Structure):
@@ -153,6 +157,14 @@ def _bind():
             fn.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                            ctypes.c_void_p, ctypes.c_void_p]
             fn.restype = ctypes.c_int
+        lib.mpx_maxtour_fused.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        lib.mpx_maxtour_fused.restype = ctypes.c_int
+        lib.mpx_fused_tour_size.argtypes = [ctypes.POINTER(ctypes.c_int64)]
+        tsz = ctypes.c_int64()
+        lib.mpx_fused_tour_size(ctypes.byref(tsz))
+        if tsz.value != ctypes.sizeof(TourLevels):
+            raise _lib.MpxError(f"fused tournament ABI mismatch: C {tsz.value} vs ctypes {ctypes.sizeof(TourLevels)}")
         lib.mpx_fused_abi_sizes.argtypes = [ctypes.POINTER(ctypes.c_int64)] * 4
         sizes = [ctypes.c_int64() for _ in range(4)]
         lib.mpx_fused_abi_sizes(*[ctypes.byref(s) for s in sizes])
@@ -332,3 +344,48 @@ def maxlevel_fused(session, u: AShare, v: AShare, protocol) -> AShare:
                                         v.values.contiguous().data_ptr(), u.size, ctypes.addressof(tape),
                                         ctypes.addressof(P)), ("maxlevel", u.size, session.L, calls, 3))
     return AShare(y, out_w, out_f, session.parties)
+
+
+def tour_fusable(session, x: AShare) -> bool:
+    d = x.shape[-1] if x.shape else 0
+    return fusable_cmp(session, x) and 2 <= d <= 512
+
+
+def maxtour_fused(session, x: AShare, protocol) -> AShare:
+    """A whole max_vec tournament in one kernel (one CTA per row). Each level's
+    takes are scheduled exactly as the per-level path would (same keys, same
+    order), then concatenated into one tape."""
+    lib = _bind()
+    d0 = x.shape[-1]
+    rows = x.size // d0
+    lead = x.shape[:-1]
+    entries, lev_start = [], []
+    d = d0
+    mu = None
+    while d > 1:
+        half = d // 2
+        shp = lead + (half,)
+        mu = AShare(torch.empty((session.L,) + shp, dtype=torch.int64, device="meta"), x.width, x.frac,
+                    x.parties)
+        key = ("maxlevel", shp, x.width, x.frac, session.L, session.n_parties, session.p0)
+        tape, _ = _schedule("maxlevel", session, key, rows * half, protocol, (mu, mu))
+        lev_start.append(len(entries))
+        entries += [tape.m[i] for i in range(tape.n)]
+        d = half + (d - 2 * half)
+    if len(entries) > TAPE_MAX or len(lev_start) > 16:
+        raise _lib.MpxError(f"max tournament of width {d0}: {len(entries)} takes exceed the tape")
+    tape = Tape()
+    for i, m in enumerate(entries):
+        tape.m[i] = m
+    tape.n = len(entries)
+    lv = TourLevels()
+    for i, s in enumerate(lev_start):
+        lv.start[i] = s
+    lv.start[len(lev_start)] = len(entries)
+    lv.nlev = len(lev_start)
+    P = _basic_params(session, x)
+    y = session.alloc((session.L,) + lead)
+    _launch(lib, "mpx_maxtour_fused", (y.data_ptr(), x.values.contiguous().data_ptr(), rows, d0,
+                                       ctypes.addressof(tape), ctypes.addressof(lv), ctypes.addressof(P)),
+            ("maxtour", rows, session.L, None, 0))
+    return AShare(y, x.width, x.frac, session.parties)
