@@ -308,7 +308,8 @@ def alg_bytes(name, a):
         if name == "mpx_mask_limbs":
             # X_l, T_l read once; shared S limbs + per-party T limbs written
             L, R, Kd, Rpad, Kp = a[10], a[11], a[12], a[13], a[14]
-            return 2 * L * R * Kd * 8 + (1 + L) * 8 * Rpad * Kp
+            jobs = a[18] if len(a) > 18 else 1
+            return jobs * (2 * L * R * Kd * 8 + (1 + L) * 8 * Rpad * Kp)
         if name == "mpx_mask_sub_bs":
             L, batch, n = a[7], a[8], a[9]
             return batch * n * 8 * (2 * L + 1)

@@ -268,20 +268,25 @@ int mpx_gemm_limbs(uint64_t* C, const uint8_t* A8, const uint8_t* B8, int64_t ba
  * C[z] = Cin[z] + [SA | PA[z]] @ [PB[z] ; SB] mod 2^w, SA / SB shared
  * [8][rows][Kh] limb planes, PA / PB per party [batch][8][rows][Kh]; i.e.
  * basic.py:72-75 with D, E limbs stored once for all parties. Kh % 128 == 0,
- * ksplit 0 = automatic. */
+ * ksplit 0 = automatic. Several equal-shape products in one launch: batch =
+ * jobs x zl parties, unit z uses shared plane set z / zl and addend
+ * Cin + (z % zl) * sCin + (z / zl) * sCin_j. */
 int mpx_gemm_limbs_split(uint64_t* C, const uint8_t* PA8, const uint8_t* SA8, const uint8_t* PB8,
                          const uint8_t* SB8, int64_t batch, int64_t M, int64_t N, int64_t Mpad, int64_t Npad,
                          int64_t Kh, int64_t ldc, int64_t sC, int width, int ksplit, const uint64_t* Cin,
-                         int64_t sCin, void* stream);
+                         int64_t sCin, int zl, int64_t sCin_j, void* stream);
 /* Fused Beaver mask + limb split for an all-parties-local session (the
  * opening of basic.py:66-70 is a local reduction): S8 = limbs of
  * S = sum_l (X_l - T_l) mod 2^w, P8[l] = limbs of T_l (+ S at party p0 when
  * add_p0). X_l, T_l: logical R x K at (row, col) strides (transposed views
  * read in place), party strides x_ps / t_ps; planes K-major [Rpad][Kp],
- * zero padded (Rpad % 32 == 0, Kp % 64 == 0). */
+ * zero padded (Rpad % 32 == 0, Kp % 32 == 0). `jobs` equal-shape operand
+ * pairs at element strides x_js / t_js in one launch; job j writes plane
+ * sets S8 + j * 8 * Rpad * Kp and P8 + j * L * 8 * Rpad * Kp. */
 int mpx_mask_limbs(uint8_t* S8, uint8_t* P8, const uint64_t* X, int64_t x_ps, int64_t x_sr, int64_t x_sc,
                    const uint64_t* T, int64_t t_ps, int64_t t_sr, int64_t t_sc, int L, int64_t R, int64_t K,
-                   int64_t Rpad, int64_t Kp, int p0, int add_p0, int width, void* stream);
+                   int64_t Rpad, int64_t Kp, int p0, int add_p0, int width, int jobs, int64_t x_js,
+                   int64_t t_js, void* stream);
 
 /* Beaver matrix-product reconstruction in one launch (basic.py:72-75):
  * Z_l = C_l + D @ (B_l + [l==p0] E) + A_l @ E mod 2^width for the L local

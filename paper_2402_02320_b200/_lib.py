@@ -76,8 +76,8 @@ _SIGS = {
     "mpx_ring_pool_scatter": [_P, _P, _L, _L, _L, _L, _L, _I, _P],
     "mpx_ring_add_rowvec": [_P, _P, _I, _L, _L, _I, _I, _P],
     "mpx_gemm_limbs": [_P, _P, _P, _L, _L, _L, _L, _L, _L, _L, _L, _I, _I, _I, _P, _L, _P],
-    "mpx_gemm_limbs_split": [_P, _P, _P, _P, _P, _L, _L, _L, _L, _L, _L, _L, _L, _I, _I, _P, _L, _P],
-    "mpx_mask_limbs": [_P, _P, _P, _L, _L, _L, _P, _L, _L, _L, _I, _L, _L, _L, _L, _I, _I, _I, _P],
+    "mpx_gemm_limbs_split": [_P, _P, _P, _P, _P, _L, _L, _L, _L, _L, _L, _L, _L, _I, _I, _P, _L, _I, _L, _P],
+    "mpx_mask_limbs": [_P, _P, _P, _L, _L, _L, _P, _L, _L, _L, _I, _L, _L, _L, _L, _I, _I, _I, _I, _L, _L, _P],
     "mpx_philox_elems": [_P, _U, _U, _L, _L, _I, _P],
     "mpx_philox_bits": [_P, _U, _U, _L, _L, _P],
     "mpx_deal_share_arith": [_P, _L, _P, _U, _U, _L, _L, _I, _I, _I, _I, _P],

@@ -121,6 +121,8 @@ struct TcArgs {
   int ksplit;    // CTAs per output tile along K; > 1 => wrapping atomic adds
   int accumulate;
   u64 msk;
+  int zl;       // split operands: parties per job (shared plane set = z / zl)
+  i64 sCin_j;   // job stride of Cin (Cin of unit z at (z % zl) * sCin + (z / zl) * sCin_j)
   int dbg;      // timing experiments (MPX_TC_DBG bits): 1 one diagonal, 2 no stores, 4 no MMA, 8 no addend, 16 no drain
   int kb_half;  // > 0: split operands (persistent kernel only): k-blocks
                 // [0, kb_half) pair shared A (mapA2) with party B (mapB),
@@ -485,7 +487,8 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
           const int kx = (hi ? kg - args.kb_half : kg) * BK;
           const CUtensorMap* mA = lo ? &mapA2 : &mapA;
           const CUtensorMap* mB = hi ? &mapB2 : &mapB;
-          const int zA = lo ? 0 : t.z, zB = hi ? 0 : t.z;
+          const int zs = args.kb_half > 0 ? t.z / args.zl : 0;
+          const int zA = lo ? zs : t.z, zB = hi ? zs : t.z;
           mbar_wait(&emptyB[bs], bph ^ 1);
           mbar_expect_tx(&fullB[bs], B_STAGE);
           for (int j = 0; j < 8; ++j)
@@ -561,7 +564,9 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
       const i64 rbase = (i64)t.m0 + sp * 32;
       const int rmax = (int)max((i64)0, min((i64)32, (i64)args.M - rbase));
       u64* Cz = args.C + (i64)t.z * args.sC + rbase * args.ldc;
-      const u64* Cin = args.Cin ? args.Cin + (i64)t.z * args.sCin + rbase * args.ldc : nullptr;
+      const u64* Cin =
+          args.Cin ? args.Cin + (i64)(t.z % args.zl) * args.sCin + (i64)(t.z / args.zl) * args.sCin_j + rbase * args.ldc
+                   : nullptr;
       // split slices meet in C through atomics (zeroed, or holding the
       // accumulate operand); slice 0 carries the Cin addend
       const u64* src = atom ? (t.ks == 0 ? Cin : nullptr) : (Cin ? Cin : (args.accumulate ? Cz : nullptr));
@@ -613,7 +618,9 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
         const i64 row = (i64)t.m0 + sp * 32 + lane;
         if (row < args.M) {
           u64* Crow = args.C + (i64)t.z * args.sC + row * args.ldc;
-          const u64* Cin = args.Cin ? args.Cin + (i64)t.z * args.sCin + row * args.ldc : nullptr;
+          const u64* Cin = args.Cin ? args.Cin + (i64)(t.z % args.zl) * args.sCin +
+                                          (i64)(t.z / args.zl) * args.sCin_j + row * args.ldc
+                                    : nullptr;
           const u64* src = atom ? (t.ks == 0 ? Cin : nullptr) : (Cin ? Cin : (args.accumulate ? Crow : nullptr));
 #pragma unroll
           for (int q = 0; q < BN; ++q) {
@@ -892,6 +899,7 @@ struct MaskLimbArgs {
   i64 R, K, Rpad, Kp;
   u64 msk;
   int L, p0, add_p0, pad;
+  i64 x_js, t_js;  // job strides (blockIdx.z = job) of X and T; planes follow per job
 };
 
 // A thread owns (row rr, 8-column group g) of a 32 (rows) x 64 (k) tile and
@@ -945,6 +953,13 @@ __global__ void __launch_bounds__(256, 3) k_mask_limbs(MaskLimbArgs a) {
   const int t = threadIdx.x;
   const i64 plane = a.Rpad * a.Kp;
   const bool defer = a.add_p0 && a.p0 >= 0;
+  {  // job blockIdx.z: its operands and its shared + per-party plane sets
+    const i64 jb = blockIdx.z;
+    a.X += jb * a.x_js;
+    a.T += jb * a.t_js;
+    a.S8 += jb * 8 * plane;
+    a.P8 += jb * (i64)a.L * 8 * plane;
+  }
   u64 s[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) s[c] = 0;
@@ -972,8 +987,10 @@ __global__ void __launch_bounds__(256, 3) k_mask_limbs(MaskLimbArgs a) {
 
 extern "C" int mpx_mask_limbs(uint8_t* S8, uint8_t* P8, const uint64_t* X, int64_t x_ps, int64_t x_sr, int64_t x_sc,
                               const uint64_t* T, int64_t t_ps, int64_t t_sr, int64_t t_sc, int L, int64_t R,
-                              int64_t K, int64_t Rpad, int64_t Kp, int p0, int add_p0, int width, void* stream) {
+                              int64_t K, int64_t Rpad, int64_t Kp, int p0, int add_p0, int width, int jobs,
+                              int64_t x_js, int64_t t_js, void* stream) {
   CHECK_ARG(S8 && P8 && X && T && L >= 1 && R >= 1 && K >= 1 && width >= 1 && width <= 64);
+  CHECK_ARG(jobs >= 1 && jobs <= 65535);
   CHECK_ARG(Rpad >= R && Rpad % 32 == 0 && Kp >= K && Kp % 32 == 0);
   CHECK_ARG(Rpad / 32 <= 0x7FFFFFFF && (Kp + 63) / 64 <= 65535);
   MaskLimbArgs a;
@@ -996,7 +1013,9 @@ extern "C" int mpx_mask_limbs(uint8_t* S8, uint8_t* P8, const uint64_t* X, int64
   a.p0 = p0;
   a.add_p0 = add_p0;
   a.pad = 0;
-  dim3 grid((unsigned)(Rpad / 32), (unsigned)((Kp + 63) / 64));
+  a.x_js = x_js;
+  a.t_js = t_js;
+  dim3 grid((unsigned)(Rpad / 32), (unsigned)((Kp + 63) / 64), (unsigned)jobs);
   cudaStream_t s = (cudaStream_t)stream;
   const bool xk = x_sc == 1, tk = t_sc == 1;
   if (xk && tk)
@@ -1110,7 +1129,8 @@ static int tcp_launch(unsigned g, cudaStream_t s, const CUtensorMap& mA, const C
 static int gemm_limbs_impl(uint64_t* C, const uint8_t* A8, const uint8_t* B8, const uint8_t* A8s,
                            const uint8_t* B8s, int64_t batch, int64_t M, int64_t N, int64_t Mpad, int64_t Npad,
                            int64_t Kpad, int64_t ldc, int64_t sC, int accumulate, int width, int ksplit,
-                           const uint64_t* Cin, int64_t sCin, void* stream) {
+                           const uint64_t* Cin, int64_t sCin, void* stream, int zl = 0, int64_t sCin_j = 0) {
+  if (zl <= 0) zl = (int)batch;  // one job: every z shares plane set 0
   CHECK_ARG(C && A8 && B8 && batch >= 1 && batch <= 65535 && M >= 1 && N >= 1 && width >= 1 && width <= 64);
   const bool split_ops = A8s != nullptr;
   CHECK_ARG(Mpad % TC_BM == 0 && Npad % 32 == 0 && Kpad % 32 == 0 && Kpad >= 32);
@@ -1177,6 +1197,9 @@ static int gemm_limbs_impl(uint64_t* C, const uint8_t* A8, const uint8_t* B8, co
   a.msk = ring_mask(width);
   a.kb_half = split_ops ? (int)(kcols / bk) : 0;
   a.dbg = getenv("MPX_TC_DBG") ? atoi(getenv("MPX_TC_DBG")) : 0;
+  a.zl = zl;
+  a.sCin_j = sCin_j;
+  CHECK_ARG(batch % zl == 0);
   CUtensorMap mapA, mapB, mapA2, mapB2;
   if (!legacy) {
     // split slices meet in C through atomics: start from zero unless C is
@@ -1189,8 +1212,9 @@ static int gemm_limbs_impl(uint64_t* C, const uint8_t* A8, const uint8_t* B8, co
         make_map(&mapB, B8, batch * 8 * Npad, kcols, bn, bk) != MPX_OK)
       return MPX_ERR_CUDA;
     if (split_ops) {
-      if (make_map(&mapA2, A8s, 8 * Mpad, kcols, TC_BM, bk) != MPX_OK ||
-          make_map(&mapB2, B8s, 8 * Npad, kcols, bn, bk) != MPX_OK)
+      const i64 jobs = batch / zl;
+      if (make_map(&mapA2, A8s, jobs * 8 * Mpad, kcols, TC_BM, bk) != MPX_OK ||
+          make_map(&mapB2, B8s, jobs * 8 * Npad, kcols, bn, bk) != MPX_OK)
         return MPX_ERR_CUDA;
     } else {
       mapA2 = mapA;
@@ -1260,10 +1284,10 @@ extern "C" int mpx_gemm_limbs(uint64_t* C, const uint8_t* A8, const uint8_t* B8,
 extern "C" int mpx_gemm_limbs_split(uint64_t* C, const uint8_t* PA8, const uint8_t* SA8, const uint8_t* PB8,
                                     const uint8_t* SB8, int64_t batch, int64_t M, int64_t N, int64_t Mpad,
                                     int64_t Npad, int64_t Kh, int64_t ldc, int64_t sC, int width, int ksplit,
-                                    const uint64_t* Cin, int64_t sCin, void* stream) {
-  CHECK_ARG(SA8 && SB8 && Kh % 32 == 0);
+                                    const uint64_t* Cin, int64_t sCin, int zl, int64_t sCin_j, void* stream) {
+  CHECK_ARG(SA8 && SB8 && Kh % 32 == 0 && zl >= 1 && batch % zl == 0);
   return gemm_limbs_impl(C, PA8, PB8, SA8, SB8, batch, M, N, Mpad, Npad, 2 * Kh, ldc, sC, 0, width, ksplit, Cin,
-                         sCin, stream);
+                         sCin, stream, zl, sCin_j);
 }
 
 int mpx_gemm_tc(uint64_t*, const uint64_t*, const uint64_t*, int64_t, int64_t, int64_t, int64_t, int64_t,

@@ -466,22 +466,24 @@ def gemm_limbs(C, A8, B8, batch, M, N, Mpad, Npad, Kpad, ldc, sC, accumulate, wi
     return C
 
 
-def gemm_limbs_split(C, PA8, SA8, PB8, SB8, batch, M, N, Mpad, Npad, Kh, ldc, sC, width, cin, s_cin, ksplit=0):
-    """C[z] = Cin[z] + [SA | PA[z]] @ [PB[z] ; SB] on the persistent tcgen05 kernel."""
+def gemm_limbs_split(C, PA8, SA8, PB8, SB8, batch, M, N, Mpad, Npad, Kh, ldc, sC, width, cin, s_cin, ksplit=0,
+                     zl=0, s_cin_j=0):
+    """C[z] = Cin[z] + [SA[z / zl] | PA[z]] @ [PB[z] ; SB[z / zl]] on the persistent tcgen05 kernel."""
     if _dry(C):
         return C
     cin_ptr = cin if isinstance(cin, int) else ptr(cin)
     call("mpx_gemm_limbs_split", ptr(C), ptr(PA8), ptr(SA8), ptr(PB8), ptr(SB8), batch, M, N, Mpad, Npad, Kh, ldc,
-         sC, width, int(ksplit), cin_ptr, s_cin)
+         sC, width, int(ksplit), cin_ptr, s_cin, zl or batch, s_cin_j)
     return C
 
 
-def mask_limbs(S8, P8, x_ptr, x_ps, x_sr, x_sc, t_ptr, t_ps, t_sr, t_sc, L, R, Kd, Rpad, Kp, p0, add_p0, width):
+def mask_limbs(S8, P8, x_ptr, x_ps, x_sr, x_sc, t_ptr, t_ps, t_sr, t_sc, L, R, Kd, Rpad, Kp, p0, add_p0, width,
+               jobs=1, x_js=0, t_js=0):
     """Fused sim-mode Beaver mask + limb split (shared S limbs, per-party T limbs)."""
     if _dry(S8):
         return S8
     call("mpx_mask_limbs", ptr(S8), ptr(P8), x_ptr, x_ps, x_sr, x_sc, t_ptr, t_ps, t_sr, t_sc, L, R, Kd, Rpad, Kp,
-         p0, int(add_p0), width)
+         p0, int(add_p0), width, jobs, x_js, t_js)
     return S8
 
 

@@ -92,10 +92,14 @@ def batch_matmul(session, pairs) -> list[AShare]:
         w, (m, k), r = x0.width, x0.shape, y0.shape[1]
         if _fused_tc(session, m, k, r, w):
             Zg = session.alloc((len(g), L, m, r))
+            if len(g) > 1:
+                _beaver_matmul_fused_tc_group(session, Zg, [pairs[i] for i in g], [trip[i] for i in g], L, m, k, r,
+                                              w)
             for j, i in enumerate(g):
                 x, y = pairs[i]
-                A, B, C = trip[i]
-                _beaver_matmul_fused_tc(session, Zg[j], x.values, y.values, A, B, C, L, m, k, r, w)
+                if len(g) == 1:
+                    A, B, C = trip[i]
+                    _beaver_matmul_fused_tc(session, Zg[j], x.values, y.values, A, B, C, L, m, k, r, w)
                 session.metrics.count(matmul_count=1, matmul_macs=m * k * r)
                 out[i] = AShare(Zg[j], w, x.frac + y.frac, session.parties)
             continue
@@ -249,6 +253,33 @@ def _beaver_matmul_fused_tc(session, Z, X, Y, A, B, C, L, m, k, r, w):
     K.mask_limbs(SB, PB, _ptr(Y), yps, ysn, ysk, B.data_ptr(), B.stride(0), 1, r, L, r, k, Np, Kh, session.p0,
                  True, w)
     K.gemm_limbs_split(Z, PA, SA, PB, SB, L, m, r, Mp, Np, Kh, r, m * r, w, C.data_ptr(), C.stride(0))
+
+
+def _beaver_matmul_fused_tc_group(session, Zg, pairs, trips, L, m, k, r, w):
+    """A group of equal-shape products whose operands and triples sit at
+    uniform strides (_groups): one mask+limb launch per side and one GEMM
+    launch for all of them (batch = products x parties); per product exactly
+    _beaver_matmul_fused_tc."""
+    J = len(pairs)
+    Mp, Np, Kh = K._rup(m, 128), K._rup(r, 32), K.kpad(k)
+    dev = Zg.device
+    SA = torch.empty((J, 8, Mp, Kh), dtype=torch.uint8, device=dev)
+    PA = torch.empty((J, L, 8, Mp, Kh), dtype=torch.uint8, device=dev)
+    SB = torch.empty((J, 8, Np, Kh), dtype=torch.uint8, device=dev)
+    PB = torch.empty((J, L, 8, Np, Kh), dtype=torch.uint8, device=dev)
+    X0, Y0 = pairs[0][0].values, pairs[0][1].values
+    A0, B0, C0 = trips[0]
+    step = lambda ts: (_uniform([_ptr(t) for t in ts]) or 0) // 8  # noqa: E731
+    x_js, y_js = step([p[0].values for p in pairs]), step([p[1].values for p in pairs])
+    a_js, b_js, c_js = step([t[0] for t in trips]), step([t[1] for t in trips]), step([t[2] for t in trips])
+    xps, xsr, xsc = _strides3(X0)
+    yps, ysk, ysn = _strides3(Y0)
+    K.mask_limbs(SA, PA, _ptr(X0), xps, xsr, xsc, A0.data_ptr(), A0.stride(0), k, 1, L, m, k, Mp, Kh, session.p0,
+                 False, w, jobs=J, x_js=x_js, t_js=a_js)
+    K.mask_limbs(SB, PB, _ptr(Y0), yps, ysn, ysk, B0.data_ptr(), B0.stride(0), 1, r, L, r, k, Np, Kh, session.p0,
+                 True, w, jobs=J, x_js=y_js, t_js=b_js)
+    K.gemm_limbs_split(Zg, PA, SA, PB, SB, J * L, m, r, Mp, Np, Kh, r, m * r, w, C0.data_ptr(), C0.stride(0),
+                       zl=L, s_cin_j=c_js)
 
 
 def _beaver_matmul_tc(session, Z, D, E, A, B, C, L, m, k, r, w):

@@ -25,6 +25,7 @@ import torch
 from .nn import attention_block, relu
 from .nonlinear import LOG2_E
 from .protocols import batch_matmul, truncate
+from .protocols.derived import truncate_many
 from .sharing import AShare
 
 
@@ -53,6 +54,12 @@ class Transformer:
         self.plain = init_weights(layers, d, ffn, heads, seed)
         self.W = [{nm: session.share_fixed(w, width, frac, _key(seed, f"{i}.{nm}")) for nm, w in lw.items()}
                   for i, lw in enumerate(self.plain)]
+        # Q, K, V weights of a layer in one buffer: uniform-stride views, so
+        # the three projections of x run as one batched Beaver product
+        for W in self.W:
+            buf = torch.stack([W[nm].values for nm in ("q", "k", "v")], dim=1)
+            for j, nm in enumerate(("q", "k", "v")):
+                W[nm] = AShare.strided(buf[:, j], W[nm].width, W[nm].frac, W[nm].parties)
 
     @property
     def n_params(self) -> int:
@@ -69,7 +76,7 @@ class Transformer:
         W, p = self.W[i], self.p
         with s.scope(f"layer{i}"):
             with s.scope("qkv"):
-                q, k, v = (truncate(s, z, p) for z in batch_matmul(s, [(x, W["q"]), (x, W["k"]), (x, W["v"])]))
+                q, k, v = truncate_many(s, batch_matmul(s, [(x, W["q"]), (x, W["k"]), (x, W["v"])]), p)
             with s.scope("attention"):
                 a = attention_block(s, list(zip(self._heads(q), self._heads(k), self._heads(v))), optimized=True)
             S = x.shape[0]
