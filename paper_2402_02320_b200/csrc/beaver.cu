@@ -351,7 +351,7 @@ extern "C" int mpx_trunc_rows_bias(uint64_t* z, const uint64_t* x, const uint64_
                                    const uint64_t* r_lo, int64_t lo_ps, const uint64_t* r_hi, int64_t hi_ps, int L,
                                    int64_t B, int64_t S, int64_t C, int nchw, int width, int f, uint64_t bias,
                                    uint64_t unbias, int p0, void* stream) {
-  CHECK_ARG(z && x && r_lo && L >= 1 && L <= 4 && B >= 0 && S >= 1 && C >= 1 && width >= 2 && width <= 64 &&
+  CHECK_ARG(z && x && r_lo && L >= 1 && L <= 8 && B >= 0 && S >= 1 && C >= 1 && width >= 2 && width <= 64 &&
             f >= 1 && f < width && bshift >= 0 && bshift < 64);
   const i64 R = B * S;
   if (R == 0) return MPX_OK;
@@ -360,12 +360,17 @@ extern "C" int mpx_trunc_rows_bias(uint64_t* z, const uint64_t* x, const uint64_
   if (nchw) {
     CHECK_ARG(B <= 65535 && S < (1 << 30) && C < (1 << 30));
     dim3 grid((unsigned)((C + 31) / 32), (unsigned)((S + 31) / 32), (unsigned)B);
+    CHECK_ARG(L <= 4);  // per-party 32 x 32 smem tiles
     k_trunc_rows_bias_nchw<4><<<grid, dim3(32, 8), 0, s>>>(z, x, brow, bshift, r_lo, lo_ps, r_hi, hi_ps, L, R,
                                                            (int)S, (int)C, msk, f, bias, unbias, p0);
   } else {
     CHECK_ARG(C < (1 << 30));
-    k_trunc_rows_bias<4><<<grid_for(R * C), MPX_THREADS, 0, s>>>(z, x, brow, bshift, r_lo, lo_ps, r_hi, hi_ps,
-                                                                 L, R, (int)C, msk, f, bias, unbias, p0);
+    if (L <= 4)
+      k_trunc_rows_bias<4><<<grid_for(R * C), MPX_THREADS, 0, s>>>(z, x, brow, bshift, r_lo, lo_ps, r_hi, hi_ps,
+                                                                   L, R, (int)C, msk, f, bias, unbias, p0);
+    else
+      k_trunc_rows_bias<8><<<grid_for(R * C), MPX_THREADS, 0, s>>>(z, x, brow, bshift, r_lo, lo_ps, r_hi, hi_ps,
+                                                                   L, R, (int)C, msk, f, bias, unbias, p0);
   }
   return launch_status();
 }
@@ -404,13 +409,17 @@ extern "C" int mpx_trunc_expand_rows(uint64_t* z, const uint64_t* x, const uint6
                                      const uint64_t* r_hi, int64_t hi_ps, int L, int64_t B, int64_t C, int64_t Hs,
                                      int64_t Ws, int64_t k, int width, int f, uint64_t bias, uint64_t unbias, int p0,
                                      void* stream) {
-  CHECK_ARG(z && x && r_lo && L >= 1 && L <= 4 && B >= 0 && C >= 1 && Hs >= 1 && Ws >= 1 && k >= 1 &&
+  CHECK_ARG(z && x && r_lo && L >= 1 && L <= 8 && B >= 0 && C >= 1 && Hs >= 1 && Ws >= 1 && k >= 1 &&
             C < (1 << 30) && Hs * k < (1 << 30) && Ws * k < (1 << 30) && width >= 2 && width <= 64 && f >= 1 &&
             f < width);
   const i64 n = B * C * Hs * Ws;
   if (n == 0) return MPX_OK;
-  k_trunc_expand_rows<4><<<grid_for(n), MPX_THREADS, 0, (cudaStream_t)stream>>>(
-      z, x, r_lo, lo_ps, r_hi, hi_ps, L, B, (int)C, (int)Hs, (int)Ws, (int)k, ring_mask(width), f, bias, unbias, p0);
+  if (L <= 4)
+    k_trunc_expand_rows<4><<<grid_for(n), MPX_THREADS, 0, (cudaStream_t)stream>>>(
+        z, x, r_lo, lo_ps, r_hi, hi_ps, L, B, (int)C, (int)Hs, (int)Ws, (int)k, ring_mask(width), f, bias, unbias, p0);
+  else
+    k_trunc_expand_rows<8><<<grid_for(n), MPX_THREADS, 0, (cudaStream_t)stream>>>(
+        z, x, r_lo, lo_ps, r_hi, hi_ps, L, B, (int)C, (int)Hs, (int)Ws, (int)k, ring_mask(width), f, bias, unbias, p0);
   return launch_status();
 }
 

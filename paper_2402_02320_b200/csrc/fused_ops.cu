@@ -13,6 +13,9 @@
 // [e*per, e*per + per) — the reference's flattened C order.
 #include "common.cuh"
 
+// local party counts with fused instantiations: every n <= 4, and n = 8
+#define FUSED_L_OK(L) (((L) >= 1 && (L) <= 4) || (L) == 8)
+
 #define TAPE_MAX 160  // a whole max_vec tournament (<= 10 levels of ~9 takes) fits one tape
 
 struct MatRef {
@@ -652,7 +655,7 @@ __global__ void __launch_bounds__(128) k_attexp_fused(u64* __restrict__ y, const
 // Logarithm, paper Alg. 3 without the big-input pre-shift (nonlinear.py:216-267)
 
 template <int L>
-__global__ void __launch_bounds__(128, MPX_LOG_MINB) k_log_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
+__global__ void __launch_bounds__(128, L <= 4 ? MPX_LOG_MINB : 1) k_log_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
                                                    const __grid_constant__ Tape tape, FusedParams P) {
   const int w = P.w, p = P.p, p0 = P.p0;
   const u64 msk = ring_mask(w);
@@ -726,7 +729,7 @@ __global__ void __launch_bounds__(128, MPX_LOG_MINB) k_log_fused(u64* __restrict
 // Also stores s (the converted sign) for the backward pass when s_out != 0.
 
 template <int L>
-__global__ void __launch_bounds__(128, MPX_CMP_MINB) k_relu_fused(u64* __restrict__ y, u64* __restrict__ s_out,
+__global__ void __launch_bounds__(128, L <= 4 ? MPX_CMP_MINB : 1) k_relu_fused(u64* __restrict__ y, u64* __restrict__ s_out,
                                                     const u64* __restrict__ xin, i64 n,
                                                     const __grid_constant__ Tape tape, FusedParams P) {
   const int w = P.w, p0 = P.p0;
@@ -778,7 +781,7 @@ __device__ __forceinline__ Sh<L> d_maxpair(const Sh<L>& u, const Sh<L>& v, const
 }
 
 template <int L>
-__global__ void __launch_bounds__(128, MPX_CMP_MINB) k_maxlevel_fused(u64* __restrict__ win, const u64* __restrict__ uin,
+__global__ void __launch_bounds__(128, L <= 4 ? MPX_CMP_MINB : 1) k_maxlevel_fused(u64* __restrict__ win, const u64* __restrict__ uin,
                                                         const u64* __restrict__ vin, i64 n,
                                                         const __grid_constant__ Tape tape, FusedParams P) {
   const int w = P.w, p0 = P.p0;
@@ -863,7 +866,7 @@ extern "C" int mpx_maxtour_fused(uint64_t* y, const uint64_t* x, int64_t rows, i
   const Tape& tp = *(const Tape*)tape_host;
   const TourLevels& lv = *(const TourLevels*)levels_host;
   const FusedParams& P = *(const FusedParams*)params_host;
-  CHECK_ARG(tp.n >= 1 && tp.n <= TAPE_MAX && lv.nlev >= 1 && lv.nlev <= 16 && P.L >= 1 && P.L <= 4);
+  CHECK_ARG(tp.n >= 1 && tp.n <= TAPE_MAX && lv.nlev >= 1 && lv.nlev <= 16 && FUSED_L_OK(P.L));
   if (rows == 0) return MPX_OK;
   cudaStream_t s = (cudaStream_t)stream;
   const int threads = min(256, max(32, ((d0 / 2 + 31) / 32) * 32));
@@ -873,7 +876,8 @@ extern "C" int mpx_maxtour_fused(uint64_t* y, const uint64_t* x, int64_t rows, i
     case 1: k_maxtour_fused<1><<<g, threads, sm, s>>>(y, x, rows, d0, tp, lv, P); break;
     case 2: k_maxtour_fused<2><<<g, threads, sm, s>>>(y, x, rows, d0, tp, lv, P); break;
     case 3: k_maxtour_fused<3><<<g, threads, sm, s>>>(y, x, rows, d0, tp, lv, P); break;
-    default: k_maxtour_fused<4><<<g, threads, sm, s>>>(y, x, rows, d0, tp, lv, P); break;
+    case 4: k_maxtour_fused<4><<<g, threads, sm, s>>>(y, x, rows, d0, tp, lv, P); break;
+    default: k_maxtour_fused<8><<<g, threads, sm, s>>>(y, x, rows, d0, tp, lv, P); break;
   }
   return launch_status();
 }
@@ -889,7 +893,7 @@ struct Dispatch;
     CHECK_ARG(y && x && n >= 0 && tape_host && params_host);                                               \
     const Tape& tp = *(const Tape*)tape_host;                                                              \
     const FusedParams& P = *(const FusedParams*)params_host;                                               \
-    CHECK_ARG(tp.n >= 1 && tp.n <= TAPE_MAX && P.w >= 8 && P.w <= 64 && P.L >= 1 && P.L <= 4);            \
+    CHECK_ARG(tp.n >= 1 && tp.n <= TAPE_MAX && P.w >= 8 && P.w <= 64 && FUSED_L_OK(P.L));                 \
     if (n == 0) return MPX_OK;                                                                             \
     cudaStream_t s = (cudaStream_t)stream;                                                                 \
     const unsigned g = grid_for(n, 128);                                                                   \
@@ -897,7 +901,8 @@ struct Dispatch;
       case 1: KFN<1><<<g, 128, 0, s>>>(y, x, n, tp, P); break;                                             \
       case 2: KFN<2><<<g, 128, 0, s>>>(y, x, n, tp, P); break;                                             \
       case 3: KFN<3><<<g, 128, 0, s>>>(y, x, n, tp, P); break;                                             \
-      default: KFN<4><<<g, 128, 0, s>>>(y, x, n, tp, P); break;                                            \
+      case 4: KFN<4><<<g, 128, 0, s>>>(y, x, n, tp, P); break;                                             \
+      default: KFN<8><<<g, 128, 0, s>>>(y, x, n, tp, P); break;                                            \
     }                                                                                                      \
     return launch_status();                                                                                \
   }
@@ -910,7 +915,7 @@ DEFINE_LAUNCH(mpx_reciprocal_fused, k_reciprocal_fused)
     CHECK_ARG(y && a2 && n >= 0 && tape_host && params_host);                                              \
     const Tape& tp = *(const Tape*)tape_host;                                                              \
     const FusedParams& P = *(const FusedParams*)params_host;                                               \
-    CHECK_ARG(tp.n >= 1 && tp.n <= TAPE_MAX && P.w >= 8 && P.w <= 64 && P.L >= 1 && P.L <= 4);            \
+    CHECK_ARG(tp.n >= 1 && tp.n <= TAPE_MAX && P.w >= 8 && P.w <= 64 && FUSED_L_OK(P.L));                 \
     if (n == 0) return MPX_OK;                                                                             \
     cudaStream_t s = (cudaStream_t)stream;                                                                 \
     const unsigned g = grid_for(n, 128);                                                                   \
@@ -918,7 +923,8 @@ DEFINE_LAUNCH(mpx_reciprocal_fused, k_reciprocal_fused)
       case 1: KFN<1><<<g, 128, 0, s>>>(y, a1, a2, n, tp, P); break;                                        \
       case 2: KFN<2><<<g, 128, 0, s>>>(y, a1, a2, n, tp, P); break;                                        \
       case 3: KFN<3><<<g, 128, 0, s>>>(y, a1, a2, n, tp, P); break;                                        \
-      default: KFN<4><<<g, 128, 0, s>>>(y, a1, a2, n, tp, P); break;                                       \
+      case 4: KFN<4><<<g, 128, 0, s>>>(y, a1, a2, n, tp, P); break;                                        \
+      default: KFN<8><<<g, 128, 0, s>>>(y, a1, a2, n, tp, P); break;                                       \
     }                                                                                                      \
     return launch_status();                                                                                \
   }

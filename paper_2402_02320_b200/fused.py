@@ -192,7 +192,7 @@ def material_bytes(calls, L: int) -> int:
 
 def fusable(session, x: AShare) -> bool:
     return (getattr(session, "fused", False) and getattr(session, "fuse_ops", True)
-            and x.width == 64 and 1 <= session.L <= 4 and 2 * x.frac <= 62 and x.size > 0)
+            and x.width == 64 and (1 <= session.L <= 4 or session.L == 8) and 2 * x.frac <= 62 and x.size > 0)
 
 
 def fusable_attexp(session, x: AShare) -> bool:
@@ -200,14 +200,14 @@ def fusable_attexp(session, x: AShare) -> bool:
     (p + clog2(p) + 1 bits) fits the narrow word and 2p <= 62."""
     p = x.frac
     return (getattr(session, "fused", False) and getattr(session, "fuse_ops", True)
-            and x.width == 32 and 1 <= session.L <= 4 and x.size > 0 and 1 <= p <= 31
+            and x.width == 32 and (1 <= session.L <= 4 or session.L == 8) and x.size > 0 and 1 <= p <= 31
             and p + max(1, (p - 1).bit_length()) + 1 <= 32)
 
 
 def fusable_cmp(session, x: AShare) -> bool:
     """ReLU / max-level kernels: any ring width >= 8."""
     return (getattr(session, "fused", False) and getattr(session, "fuse_ops", True)
-            and 8 <= x.width <= 64 and 1 <= session.L <= 4 and x.size > 0)
+            and 8 <= x.width <= 64 and (1 <= session.L <= 4 or session.L == 8) and x.size > 0)
 
 
 def params_for(kind: str, session, x: AShare, params) -> FusedParams:

@@ -49,8 +49,8 @@ def _colsum(session, z: AShare) -> AShare:
 
 
 def _fused_layer(s) -> bool:
-    """Sim mode with the layer-plumbing kernels (all parties local, L <= 4)."""
-    return s.fused and getattr(s, "fuse_ops", True) and s.L <= 4
+    """Sim mode with the layer-plumbing kernels (all parties local, L <= 8)."""
+    return s.fused and getattr(s, "fuse_ops", True) and s.L <= 8
 
 
 def _trunc_takes(s, n: int, f: int, w: int):
@@ -124,7 +124,7 @@ class Conv2d(Layer):
         z = batch_matmul(s, [(self.cols, self.W)])[0]
         self.out_hw = (OH, OW)
         b = getattr(self, "b", None)
-        if _fused_layer(s):
+        if _fused_layer(s) and s.L <= 4:   # the NCHW epilogue's smem tiles hold <= 4 parties
             return _trunc_bias_out(s, z, b, self.p, B, OH * OW, True, (B, self.cout, OH, OW))
         z = truncate(s, _add_bias(s, z, b, self.p) if b is not None else z, self.p)
         v = z.values.view(s.L, B, OH, OW, self.cout).permute(0, 1, 4, 2, 3).contiguous()

@@ -48,7 +48,7 @@ def _chain(M, s):
 
 
 @pytest.mark.parametrize("fn", [_recip, _exp, _exp14, _log, _chain], ids=["recip", "exp", "exp_p14", "log", "chain"])
-@pytest.mark.parametrize("n", [2, 3, 4])
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
 def test_fused_equals_per_round_and_oracle(engines, fn, n):
     g, o = engines
     fused, finfo, fs = g.run(fn, n, fuse=True)
@@ -106,7 +106,7 @@ def _attention(M, s):
 @pytest.mark.parametrize("fn", [_relu, _relu32, _max_odd, _maxcut_softmax, _attexp, _attexp14, _attention],
                          ids=["relu", "relu_w32", "max_odd", "maxcut_softmax", "attexp", "attexp_p14",
                               "attention"])
-@pytest.mark.parametrize("n", [2, 3, 4])
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
 def test_fused_cmp_equals_per_round_and_oracle(engines, fn, n):
     g, o = engines
     fused, finfo, fs = g.run(fn, n, fuse=True)
