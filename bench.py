@@ -511,14 +511,6 @@ def roofline_for(per, int8_peak=None):
     dom = per[dom_name]
     common = {"kernel": dom_name, "launches": dom["n"], "avg_launch_us": 1e3 * dom["ms"] / dom["n"],
               "share_of_step": dom["ms"] / step_ms}
-    if dom_name in ("mpx_gemm_limbs", "mpx_gemm_limbs_split"):
-        ach = dom["ops"] / (dom["ms"] / 1e3) / 1e12
-        return dict(common, bound="tensor", achieved=ach, peak=int8_peak, unit="TOPS int8",
-                    peak_kind="measured in-run: torch._int_mm int8 8192^3 (cuBLASLt), burst",
-                    frac=(ach / int8_peak) if int8_peak else None, traffic=None,
-                    alg_ops_per_launch=dom["ops"] // dom["n"])
-    peak, peak_kind = _read_peaks()
-    ach = dom["bytes"] / (dom["ms"] / 1e3) / 1e9 if dom["bytes_known"] else None
     traffic = None
     tpath = os.path.join(REPO, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -526,6 +518,14 @@ def roofline_for(per, int8_peak=None):
             traffic = json.load(open(tpath)).get(dom_name)
         except ValueError:
             traffic = None
+    if dom_name in ("mpx_gemm_limbs", "mpx_gemm_limbs_split"):
+        ach = dom["ops"] / (dom["ms"] / 1e3) / 1e12
+        return dict(common, bound="tensor", achieved=ach, peak=int8_peak, unit="TOPS int8",
+                    peak_kind="measured in-run: torch._int_mm int8 8192^3 (cuBLASLt), burst",
+                    frac=(ach / int8_peak) if int8_peak else None, traffic=traffic,
+                    traffic_unit="DRAM bytes per launch (ncu)", alg_ops_per_launch=dom["ops"] // dom["n"])
+    peak, peak_kind = _read_peaks()
+    ach = dom["bytes"] / (dom["ms"] / 1e3) / 1e9 if dom["bytes_known"] else None
     return dict(common, bound="hbm", achieved=ach, peak=peak, peak_kind=peak_kind, unit="GB/s",
                 frac=(ach / peak) if ach else None, traffic=traffic,
                 alg_bytes_per_launch=dom["bytes"] // dom["n"])
