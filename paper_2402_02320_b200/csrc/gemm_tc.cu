@@ -391,8 +391,19 @@ __device__ __forceinline__ TcpUnit tcp_unit(int u, const TcArgs& a, int tiles_m,
   t.ks = u % a.ksplit;
   const int lin_all = u / a.ksplit;
   const int per_batch = tiles_m * tiles_n;
-  t.z = lin_all / per_batch;
-  const int lin = lin_all - t.z * per_batch;
+  int lin;
+  if (a.kb_half > 0) {
+    // split operands: the parties of one job run the same tile back to back,
+    // so the shared D / E limb blocks come from L2 for all but the first
+    const int nz = a.zl;
+    const int zi = lin_all % nz, rest = lin_all / nz;
+    const int job = rest / per_batch;
+    lin = rest - job * per_batch;
+    t.z = job * nz + zi;
+  } else {
+    t.z = lin_all / per_batch;
+    lin = lin_all - t.z * per_batch;
+  }
   const int per_group = TC_GROUP_M * tiles_n;
   const int g = lin / per_group;
   const int first_m = g * TC_GROUP_M;

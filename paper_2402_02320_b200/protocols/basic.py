@@ -220,9 +220,10 @@ def _use_tc(m, k, r, w=64) -> bool:
 def _fused_tc(session, m, k, r, w) -> bool:
     """Sim sessions run tcgen05-sized products as fused mask+limb split +
     split-operand GEMM, unless padding each K half separately (32 / 64 /
-    128-byte k-blocks) costs noticeably more MMA work than padding the
-    concatenated 2K (e.g. K = 10: 2 x 32 vs 32)."""
-    return session.fused and 2 * K.kpad(k) <= 1.1 * K.kpad(2 * k) and _use_tc(m, k, r, w)
+    128-byte k-blocks) costs much more MMA work than padding the concatenated
+    2K (e.g. K = 10: 2 x 32 vs 32); up to 25% more MMA work is cheaper than
+    the separate mask and limb passes (VGG K = 576: 2 x 640 vs 1152)."""
+    return session.fused and 2 * K.kpad(k) <= 1.25 * K.kpad(2 * k) and _use_tc(m, k, r, w)
 
 
 def _strides3(v):

@@ -109,43 +109,16 @@ def main():
     s = SimSession(n, None, device=dev)
     m = build(s)
     xs, ys = s.share_fixed(x, 64, p, [2, 1]), s.share_fixed(y, 64, p, [2, 2])
-    rows = None
+    runs = []
     for rep in range(a.reps):
         s.store = device_store(50 + rep, n, c.demands, device=dev, needs_bits=c.needs_bits)
         torch.cuda.synchronize()
         _lib.profile_begin()
         m.train_step(s, xs, ys, bench.LR_SHIFT)
         torch.cuda.synchronize()
-        prof = _lib.profile_end()
-        cur = []
-        for name, args, e0, e1 in prof:
-            us = 1e3 * e0.elapsed_time(e1)
-            b = bench.alg_bytes(name, args)
-            ops = None
-            if name == "mpx_gemm_limbs":
-                ops = 2 * 36 * args[3] * args[4] * args[5] * args[8]
-            elif name == "mpx_gemm_limbs_split":
-                ops = 2 * 36 * args[5] * args[6] * args[7] * 2 * args[10]
-            short = [v for v in args if isinstance(v, int) and abs(v) < 1 << 40][:12]
-            cur.append([name, short, us, b, ops])
-        if rows is None:
-            rows = cur
-        else:
-            for r, c_ in zip(rows, cur):
-                r[2] = min(r[2], c_[2])
-    tot = sum(r[2] for r in rows)
-    for name, short, us, b, ops in rows:
-        extra = ""
-        if b:
-            extra = f"{b / 1e6:9.1f} MB {b / us / 1e3:7.0f} GB/s"
-        if ops:
-            extra = f"{ops / 1e9:9.1f} Gop {ops / us / 1e6:7.0f} TOPS"
-        print(f"{us:8.1f} us {100 * us / tot:5.1f}%  {name:28s} {extra:30s} {short}")
-    print(f"total {tot:.1f} us, {len(rows)} launches")
-    agg = {}
-    for name, _, us, _, _ in rows:
-        agg[name] = agg.get(name, 0) + us
-    print(json.dumps({k: round(v, 1) for k, v in sorted(agg.items(), key=lambda kv: -kv[1])}))
+        runs.append(_lib.profile_end())
+        del s.store
+    _print(_table(runs), full=not a.summary)
 
 
 if __name__ == "__main__":
