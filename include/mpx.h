@@ -242,13 +242,17 @@ int mpx_gemm_simt(uint64_t* C, const uint64_t* A, const uint64_t* B, int64_t bat
 
 /* ---- tcgen05 int8-limb Z_2^64 GEMM (gemm_tc.cu) ----
  * Limb split of a row-major u64 matrix into 8 u8 planes (plane stride
- * `plane`, row pitch `pitch`, column offset `coff` bytes): trans = 0 writes
- * plane[i][r][coff + c], trans = 1 writes plane[i][c][coff + r] (K-major B). */
+ * `plane`, padded K `pitch` bytes, `coff` must be 0): trans = 0 writes row r,
+ * K byte c; trans = 1 writes row c, K byte r (K-major B). Planes are K-block
+ * tiled: byte k of row r at ((k / tw) * Rpad + r) * tw + k % tw with
+ * tw = min(128, pitch), Rpad = plane / pitch, so each TMA box of the GEMM is
+ * one contiguous run of HBM. */
 int mpx_limb_split(uint8_t* out, const uint64_t* A, int64_t rows, int64_t cols, int64_t lda,
                    int64_t plane, int64_t pitch, int64_t coff, int trans, void* stream);
 /* Beaver matmul operands for all L parties in two launches: A8[l] = limbs
  * of [D | A_l] (M x 2K), B8[l] = limbs of [B_l + [l==p0] E ; E]^T (N x 2K);
- * A8 rows beyond M / B8 rows beyond N must be zero (caller zero-fills). */
+ * planes K-block tiled like mpx_limb_split's; padding rows and columns are
+ * written as zeros. */
 int mpx_beaver_limbs(uint8_t* A8, uint8_t* B8, const uint64_t* D, const uint64_t* E, const uint64_t* A,
                      int64_t a_ps, const uint64_t* B, int64_t b_ps, int L, int64_t M, int64_t K, int64_t N,
                      int64_t Mpad, int64_t Npad, int64_t Kpad, int p0, void* stream);

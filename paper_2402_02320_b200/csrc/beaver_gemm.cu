@@ -9,6 +9,8 @@
 // over K, the party-0 D @ E term folds into its B operand while the tile is
 // staged, and C is read in the epilogue (no separate copy). Tiny outputs
 // split K across CTAs and combine with wrapping 64-bit atomics on a copy of C.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 #define BG_BK 16
@@ -171,7 +173,8 @@ extern "C" int mpx_beaver_gemm_batched(uint64_t* Z, int64_t sZ, int64_t bZ, cons
   const int nt = (bm / 4) * (bn / kCfgs[best].tn);
   const i64 tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn) * L * batch;
   // resident CTAs per SM at <= 128 registers per thread
-  const i64 per_sm = min((i64)32, (i64)(65536 / (max(nt, 32) * 128)));
+  i64 per_sm = min((i64)32, (i64)(65536 / (max(nt, 32) * 128)));
+  if (const char* cap = getenv("MPX_BG_PER_SM")) per_sm = min(per_sm, (i64)max(1, atoi(cap)));  // sweeps
   const i64 target = 148 * per_sm;
   int ksplit = 1;
   if (width == 64 && tiles < target && K >= 4 * BG_BK) {

@@ -31,6 +31,17 @@
 // rings) fits 2 CTAs per SM so one CTA's epilogue overlaps the other's
 // mainloop - the shape of short-K / many-tile products (conv backward, thin
 // layers), where the epilogue is a large share of each tile.
+// K-block-tiled limb planes: byte k of row r of a [Rpad][Kp] plane sits at
+//   ((k / tw) * Rpad + r) * tw + (k % tw),   tw = min(128, Kp)
+// so one TMA box (tw-wide k-block x 128 rows) is one contiguous 16 KB run of
+// HBM instead of 128 row segments Kp bytes apart (measured: the TMA producer
+// alone of an 8192 x 1024-byte operand ran at half the HBM bandwidth with
+// row-major planes). Kp is 32, 64 or a multiple of 128 (kernels.kpad).
+__host__ __device__ __forceinline__ int limb_tw(i64 Kp) { return Kp >= 128 ? 128 : (int)Kp; }
+__host__ __device__ __forceinline__ i64 limb_off(i64 r, i64 k, i64 Rpad, int tw) {
+  return ((k / tw) * Rpad + r) * tw + (k % tw);
+}
+
 constexpr int tc_smem_bytes(int bn, int ast, int bst) { return ast * TC_A_TILE + bst * 8 * bn * TC_BK + 1024 + 256; }
 #define TC_WIDE 64, 6, 2
 #define TC_NARROW 32, 4, 1
@@ -121,6 +132,8 @@ struct TcArgs {
   int ksplit;    // CTAs per output tile along K; > 1 => wrapping atomic adds
   int accumulate;
   u64 msk;
+  int tw;       // limb-plane k-block tile width (bytes) and tiles per plane (per half if split)
+  int nkt;
   int zl;       // split operands: parties per job (shared plane set = z / zl)
   i64 sCin_j;   // job stride of Cin (Cin of unit z at (z % zl) * sCin + (z / zl) * sCin_j)
   int dbg;      // timing experiments (MPX_TC_DBG bits): 1 one diagonal, 2 no stores, 4 no MMA, 8 no addend, 16 no drain
@@ -202,12 +215,12 @@ __global__ void __launch_bounds__(192, BN == 32 ? 2 : 1)
         mbar_wait(&emptyB[bs], bph ^ 1);
         mbar_expect_tx(&fullB[bs], B_STAGE);
         for (int j = 0; j < 8; ++j)
-          tma_load_2d(sB + bs * B_STAGE + j * B_TILE, &mapB, &fullB[bs], (kb0 + kb) * TC_BK,
-                      (z * 8 + j) * args.Npad + n0);
+          tma_load_2d(sB + bs * B_STAGE + j * B_TILE, &mapB, &fullB[bs], 0,
+                      ((z * 8 + j) * args.nkt + kb0 + kb) * args.Npad + n0);
         for (int i = 0; i < 8; ++i) {
           mbar_wait(&emptyA[as], aph ^ 1);
           mbar_expect_tx(&fullA[as], TC_A_TILE);
-          tma_load_2d(sA + as * TC_A_TILE, &mapA, &fullA[as], (kb0 + kb) * TC_BK, (z * 8 + i) * args.Mpad + m0);
+          tma_load_2d(sA + as * TC_A_TILE, &mapA, &fullA[as], 0, ((z * 8 + i) * args.nkt + kb0 + kb) * args.Mpad + m0);
           if (++as == AST) {
             as = 0;
             aph ^= 1;
@@ -503,11 +516,13 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
           mbar_wait(&emptyB[bs], bph ^ 1);
           mbar_expect_tx(&fullB[bs], B_STAGE);
           for (int j = 0; j < 8; ++j)
-            tma_load_2d(sB + bs * B_STAGE + j * B_TILE, mB, &fullB[bs], kx, (zB * 8 + j) * args.Npad + t.n0);
+            tma_load_2d(sB + bs * B_STAGE + j * B_TILE, mB, &fullB[bs], kx % args.tw,
+                        ((zB * 8 + j) * args.nkt + kx / args.tw) * args.Npad + t.n0);
           for (int i = 0; i < 8; ++i) {
             mbar_wait(&emptyA[as], aph ^ 1);
             mbar_expect_tx(&fullA[as], A_TILE);
-            tma_load_2d(sA + as * A_TILE, mA, &fullA[as], kx, (zA * 8 + i) * args.Mpad + t.m0);
+            tma_load_2d(sA + as * A_TILE, mA, &fullA[as], kx % args.tw,
+                        ((zA * 8 + i) * args.nkt + kx / args.tw) * args.Mpad + t.m0);
             if (++as == AST) {
               as = 0;
               aph ^= 1;
@@ -725,7 +740,7 @@ __device__ __forceinline__ void bytes_transpose8(const u64 (&w)[8], u64 (&p)[8])
 
 // non-transposed: each thread takes 8 consecutive columns of one row
 __global__ void k_limb_split(uint8_t* __restrict__ out, const u64* __restrict__ A, i64 rows, i64 cols, i64 lda,
-                             i64 plane, i64 pitch, i64 coff) {
+                             i64 plane, i64 Rpad, int tw) {
   const i64 groups_per_row = (cols + 7) / 8;
   const i64 total = rows * groups_per_row;
   GRID_STRIDE(t, total) {
@@ -736,7 +751,7 @@ __global__ void k_limb_split(uint8_t* __restrict__ out, const u64* __restrict__ 
     for (int c = 0; c < 8; ++c) w[c] = (c0 + c < cols) ? A[r * lda + c0 + c] : 0ull;
     u64 p[8];
     bytes_transpose8(w, p);
-    uint8_t* dst = out + r * pitch + coff + c0;
+    uint8_t* dst = out + limb_off(r, c0, Rpad, tw);
     if (c0 + 8 <= cols && (((uintptr_t)dst) & 7) == 0) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) *reinterpret_cast<u64*>(dst + i * plane) = p[i];
@@ -749,8 +764,7 @@ __global__ void k_limb_split(uint8_t* __restrict__ out, const u64* __restrict__ 
 
 // transposed via a 64 (k) x 32 (n) smem tile
 __global__ void __launch_bounds__(256) k_limb_split_t(uint8_t* __restrict__ out, const u64* __restrict__ A,
-                                                      i64 rows, i64 cols, i64 lda, i64 plane, i64 pitch,
-                                                      i64 coff) {
+                                                      i64 rows, i64 cols, i64 lda, i64 plane, i64 Rpad, int tw) {
   __shared__ u64 tile[64][33];
   const i64 k0 = (i64)blockIdx.y * 64;
   const i64 n0 = (i64)blockIdx.x * 32;
@@ -772,7 +786,7 @@ __global__ void __launch_bounds__(256) k_limb_split_t(uint8_t* __restrict__ out,
     for (int c = 0; c < 8; ++c) w[c] = tile[g * 8 + c][n];
     u64 p[8];
     bytes_transpose8(w, p);
-    uint8_t* dst = out + gn * pitch + coff + gk;
+    uint8_t* dst = out + limb_off(gn, gk, Rpad, tw);
     if (gk + 8 <= rows && (((uintptr_t)dst) & 7) == 0) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) *reinterpret_cast<u64*>(dst + i * plane) = p[i];
@@ -786,15 +800,20 @@ __global__ void __launch_bounds__(256) k_limb_split_t(uint8_t* __restrict__ out,
 extern "C" int mpx_limb_split(uint8_t* out, const uint64_t* A, int64_t rows, int64_t cols, int64_t lda,
                               int64_t plane, int64_t pitch, int64_t coff, int trans, void* stream) {
   CHECK_ARG(out && A && rows >= 0 && cols >= 0 && lda >= cols);
+  // planes are K-block tiled (limb_off): `pitch` = padded K bytes, plane =
+  // Rpad * pitch; column offsets are not supported by the tiled layout
+  CHECK_ARG(coff == 0 && pitch > 0 && plane % pitch == 0 && (pitch % 128 == 0 || pitch == 32 || pitch == 64));
+  const i64 Rpad = plane / pitch;
+  const int tw = limb_tw(pitch);
   if (rows == 0 || cols == 0) return MPX_OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (!trans) {
-    k_limb_split<<<grid_for(rows * ((cols + 7) / 8)), MPX_THREADS, 0, s>>>(out, A, rows, cols, lda, plane,
-                                                                           pitch, coff);
+    k_limb_split<<<grid_for(rows * ((cols + 7) / 8)), MPX_THREADS, 0, s>>>(out, A, rows, cols, lda, plane, Rpad,
+                                                                           tw);
   } else {
     dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 63) / 64));
     CHECK_ARG(grid.y <= 65535);
-    k_limb_split_t<<<grid, 256, 0, s>>>(out, A, rows, cols, lda, plane, pitch, coff);
+    k_limb_split_t<<<grid, 256, 0, s>>>(out, A, rows, cols, lda, plane, Rpad, tw);
   }
   return launch_status();
 }
@@ -808,21 +827,21 @@ extern "C" int mpx_limb_split(uint8_t* out, const uint64_t* A, int64_t rows, int
 __global__ void k_beaver_limbs_a(uint8_t* __restrict__ A8, const u64* __restrict__ D, const u64* __restrict__ A,
                                  i64 a_ps, int L, i64 M, i64 Kd, i64 Mpad, i64 Kpad) {
   const i64 gpr = Kpad / 8;  // 8-column groups per row (columns >= 2K are zero padding)
-  const i64 total = (i64)L * M * gpr;
+  const i64 total = (i64)L * Mpad * gpr;  // rows >= M written as zeros (tiled planes)
   GRID_STRIDE(t, total) {
     const i64 g = t % gpr;
     const i64 rl = t / gpr;
-    const i64 r = rl % M, l = rl / M;
+    const i64 r = rl % Mpad, l = rl / Mpad;
     const i64 c0 = g * 8;
     u64 w[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const i64 cc = c0 + c;
-      w[c] = cc < Kd ? D[r * Kd + cc] : (cc < 2 * Kd ? A[l * a_ps + r * Kd + (cc - Kd)] : 0ull);
+      w[c] = r >= M ? 0ull : (cc < Kd ? D[r * Kd + cc] : (cc < 2 * Kd ? A[l * a_ps + r * Kd + (cc - Kd)] : 0ull));
     }
     u64 pl[8];
     bytes_transpose8(w, pl);
-    uint8_t* dst = A8 + (l * 8) * Mpad * Kpad + r * Kpad + c0;
+    uint8_t* dst = A8 + (l * 8) * Mpad * Kpad + limb_off(r, c0, Mpad, limb_tw(Kpad));
     const i64 plane = Mpad * Kpad;
     if (c0 + 8 <= Kpad && (((uintptr_t)dst) & 7) == 0) {
 #pragma unroll
@@ -867,7 +886,7 @@ __global__ void __launch_bounds__(256) k_beaver_limbs_b(uint8_t* __restrict__ B8
     for (int c = 0; c < 8; ++c) w[c] = tile[g * 8 + c][n];
     u64 pl[8];
     bytes_transpose8(w, pl);
-    uint8_t* dst = B8 + ((i64)l * 8) * Npad * Kpad + gn * Kpad + gk;
+    uint8_t* dst = B8 + ((i64)l * 8) * Npad * Kpad + limb_off(gn, gk, Npad, limb_tw(Kpad));
     const i64 plane = Npad * Kpad;
 #pragma unroll
     for (int i = 0; i < 8; ++i) *reinterpret_cast<u64*>(dst + i * plane) = pl[i];
@@ -880,7 +899,7 @@ extern "C" int mpx_beaver_limbs(uint8_t* A8, uint8_t* B8, const uint64_t* D, con
   CHECK_ARG(A8 && B8 && D && E && A && B && L >= 1 && L <= 65535 && M >= 1 && K >= 1 && N >= 1);
   CHECK_ARG(Mpad >= M && Npad >= N && Kpad >= 2 * K && Kpad % 32 == 0);
   cudaStream_t s = (cudaStream_t)stream;
-  const i64 ta = (i64)L * M * ((Kpad + 7) / 8);
+  const i64 ta = (i64)L * Mpad * ((Kpad + 7) / 8);
   // A side also zero-fills the K padding columns (groups beyond 2K read as 0)
   k_beaver_limbs_a<<<grid_for(ta), MPX_THREADS, 0, s>>>(A8, D, A, a_ps, L, M, K, Mpad, Kpad);
   dim3 grid((unsigned)((Npad + 31) / 32), (unsigned)((Kpad + 63) / 64), (unsigned)L);
@@ -948,7 +967,7 @@ __device__ __forceinline__ void ml_emit(uint8_t* base, i64 plane, const u64 (&w)
   u64 pl[8];
   bytes_transpose8(w, pl);
   if (k0 + g * 8 >= Kp) return;  // Kp % 64 == 32: the last tile's upper half
-  uint8_t* dst = base + (r0 + rr) * Kp + k0 + g * 8;
+  uint8_t* dst = base + limb_off(r0 + rr, k0 + g * 8, plane / Kp, limb_tw(Kp));
 #pragma unroll
   for (int i = 0; i < 8; ++i) *reinterpret_cast<u64*>(dst + i * plane) = pl[i];
 }
@@ -1060,11 +1079,18 @@ static PFN_encodeTiled get_encode() {
   return fn;
 }
 
-static int make_map(CUtensorMap* map, const uint8_t* base, i64 rows, i64 kbytes, int box_rows, int bk = TC_BK) {
+// `planes` K-block-tiled [Rpad][kbytes] limb planes (limb_off) as one 2D
+// tensor of (planes * kbytes / tw * Rpad) rows of tw bytes.
+static int make_map(CUtensorMap* map, const uint8_t* base, i64 planes, i64 Rpad, i64 kbytes, int box_rows,
+                    int bk = TC_BK) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return MPX_ERR_CUDA;
-  cuuint64_t dims[2] = {(cuuint64_t)kbytes, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)kbytes};
+  const int tw = limb_tw(kbytes);
+  if (kbytes % tw != 0 || tw % bk != 0) return MPX_ERR_ARG;
+  const i64 rows = planes * (kbytes / tw) * Rpad;
+  if (rows >= (1ll << 31)) return MPX_ERR_ARG;
+  cuuint64_t dims[2] = {(cuuint64_t)tw, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)tw};
   cuuint32_t box[2] = {(cuuint32_t)bk, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   const CUtensorMapSwizzle sw = bk == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
@@ -1207,6 +1233,8 @@ static int gemm_limbs_impl(uint64_t* C, const uint8_t* A8, const uint8_t* B8, co
   a.accumulate = accumulate;
   a.msk = ring_mask(width);
   a.kb_half = split_ops ? (int)(kcols / bk) : 0;
+  a.tw = limb_tw(kcols);
+  a.nkt = (int)(kcols / a.tw);
   a.dbg = getenv("MPX_TC_DBG") ? atoi(getenv("MPX_TC_DBG")) : 0;
   a.zl = zl;
   a.sCin_j = sCin_j;
@@ -1219,13 +1247,13 @@ static int gemm_limbs_impl(uint64_t* C, const uint8_t* A8, const uint8_t* B8, co
       for (i64 z = 0; z < batch; ++z)
         if (cudaMemset2DAsync(C + z * sC, (size_t)ldc * 8, 0, (size_t)N * 8, (size_t)M, s) != cudaSuccess)
           return MPX_ERR_CUDA;
-    if (make_map(&mapA, A8, batch * 8 * Mpad, kcols, TC_BM, bk) != MPX_OK ||
-        make_map(&mapB, B8, batch * 8 * Npad, kcols, bn, bk) != MPX_OK)
+    if (make_map(&mapA, A8, batch * 8, Mpad, kcols, TC_BM, bk) != MPX_OK ||
+        make_map(&mapB, B8, batch * 8, Npad, kcols, bn, bk) != MPX_OK)
       return MPX_ERR_CUDA;
     if (split_ops) {
       const i64 jobs = batch / zl;
-      if (make_map(&mapA2, A8s, jobs * 8 * Mpad, kcols, TC_BM, bk) != MPX_OK ||
-          make_map(&mapB2, B8s, jobs * 8 * Npad, kcols, bn, bk) != MPX_OK)
+      if (make_map(&mapA2, A8s, jobs * 8, Mpad, kcols, TC_BM, bk) != MPX_OK ||
+          make_map(&mapB2, B8s, jobs * 8, Npad, kcols, bn, bk) != MPX_OK)
         return MPX_ERR_CUDA;
     } else {
       mapA2 = mapA;
@@ -1258,7 +1286,7 @@ static int gemm_limbs_impl(uint64_t* C, const uint8_t* A8, const uint8_t* B8, co
       return MPX_ERR_CUDA;
     attr_set = true;
   }
-  if (make_map(&mapA, A8, batch * 8 * Mpad, Kpad, TC_BM) != MPX_OK) return MPX_ERR_CUDA;
+  if (make_map(&mapA, A8, batch * 8, Mpad, Kpad, TC_BM) != MPX_OK) return MPX_ERR_CUDA;
   if (ksplit > 1 && Cin) {
     for (i64 z = 0; z < batch; ++z)
       if (cudaMemcpy2DAsync(C + z * sC, (size_t)ldc * 8, Cin + z * sCin, (size_t)ldc * 8, (size_t)N * 8,
@@ -1272,7 +1300,7 @@ static int gemm_limbs_impl(uint64_t* C, const uint8_t* A8, const uint8_t* B8, co
   }
   const bool narrow = (Npad % 64 != 0) || nk_per <= 2;
   const int lbn = narrow ? 32 : 64;
-  if (make_map(&mapB, B8, batch * 8 * Npad, Kpad, lbn) != MPX_OK) return MPX_ERR_CUDA;
+  if (make_map(&mapB, B8, batch * 8, Npad, Kpad, lbn) != MPX_OK) return MPX_ERR_CUDA;
   dim3 grid((unsigned)((Npad / lbn) * (Mpad / TC_BM) * ksplit), 1, (unsigned)batch);
   if (narrow)
     k_gemm_limbs_tc<TC_NARROW><<<grid, 192, tc_smem_bytes(TC_NARROW), s>>>(mapA, mapB, a);

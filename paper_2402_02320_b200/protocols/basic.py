@@ -289,8 +289,6 @@ def _beaver_matmul_tc(session, Z, D, E, A, B, C, L, m, k, r, w):
     Mp, Np, Kp = K._rup(m, 128), K._rup(r, 32), K.kpad(2 * k)
     A8 = torch.empty((L, 8, Mp, Kp), dtype=torch.uint8, device=Z.device)
     B8 = torch.empty((L, 8, Np, Kp), dtype=torch.uint8, device=Z.device)
-    if Mp > m:
-        A8[:, :, m:, :].zero_()
     K.beaver_limbs(A8, B8, D, E, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), L, m, k, r, Mp, Np, Kp,
                    session.p0)
     K.gemm_limbs(Z, A8, B8, L, m, r, Mp, Np, Kp, r, m * r, False, w, cin=C.data_ptr(), s_cin=C.stride(0))
