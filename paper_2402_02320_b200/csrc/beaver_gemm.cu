@@ -20,7 +20,8 @@ constexpr int bg_min_blocks(int nt) { return 512 / (nt < 32 ? 32 : nt); }
 
 template <int BM, int BN, int TN, bool FULL>
 __device__ __forceinline__ void bg_tile_math(u64 (&acc)[4][TN], const u64 (*Ds)[BM + 1], const u64 (*As)[BM + 1],
-                                             const u64 (*Bs)[BN], const u64 (*Es)[BN], int tx, int ty, int kn) {
+                                             const u64 (*Bs)[BN], const u64 (*Es)[BN], int tx, int ty, int kn,
+                                             bool addE) {
   constexpr int TX = BN / TN, TY = BM / 4;
 #pragma unroll
   for (int kk = 0; kk < BG_BK; ++kk) {
@@ -33,8 +34,8 @@ __device__ __forceinline__ void bg_tile_math(u64 (&acc)[4][TN], const u64 (*Ds)[
     }
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
-      b[j] = Bs[kk][tx + TX * j];
       e[j] = Es[kk][tx + TX * j];
+      b[j] = Bs[kk][tx + TX * j] + (addE ? e[j] : 0ull);  // party 0's B' = B + E (basic.py:72-75)
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -43,8 +44,20 @@ __device__ __forceinline__ void bg_tile_math(u64 (&acc)[4][TN], const u64 (*Ds)[
   }
 }
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool ok) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(ok ? 8 : 0) : "memory");
+}
+
+template <int BM, int BN>
+constexpr int bg_stage_words() {
+  return 2 * BG_BK * (BM + 1) + 2 * BG_BK * BN;
+}
+
 // CTA tile BM x BN, each thread 4 rows x TN columns (strided by TY / TX so
-// shared-memory reads are conflict-free broadcasts / consecutive words).
+// shared-memory reads are conflict-free broadcasts / consecutive words). The
+// operand tiles stream through a two-stage cp.async pipeline (the next k-step
+// is in flight while this one multiplies).
 template <int BM, int BN, int TN>
 __global__ void __launch_bounds__((BM / 4) * (BN / TN), bg_min_blocks((BM / 4) * (BN / TN)))
     k_beaver_gemm(u64* __restrict__ Z, i64 sZ, const u64* __restrict__ C, i64 sC, const u64* __restrict__ D,
@@ -52,10 +65,14 @@ __global__ void __launch_bounds__((BM / 4) * (BN / TN), bg_min_blocks((BM / 4) *
                   i64 sB, int M, int K, int N, int p0, u64 msk, int ksplit, int kchunk, int L, i64 bZ, i64 bC,
                   i64 bA, i64 bB) {
   constexpr int TX = BN / TN, TY = BM / 4, NT = TX * TY;
-  __shared__ u64 Ds[BG_BK][BM + 1];
-  __shared__ u64 As[BG_BK][BM + 1];
-  __shared__ u64 Bs[BG_BK][BN];
-  __shared__ u64 Es[BG_BK][BN];
+  constexpr int STAGE = bg_stage_words<BM, BN>();
+  extern __shared__ u64 bg_sm[];
+  typedef u64 RowM[BM + 1];
+  typedef u64 RowN[BN];
+  auto Ds = [&](int s) { return reinterpret_cast<RowM*>(bg_sm + s * STAGE); };
+  auto As = [&](int s) { return reinterpret_cast<RowM*>(bg_sm + s * STAGE + BG_BK * (BM + 1)); };
+  auto Bs = [&](int s) { return reinterpret_cast<RowN*>(bg_sm + s * STAGE + 2 * BG_BK * (BM + 1)); };
+  auto Es = [&](int s) { return reinterpret_cast<RowN*>(bg_sm + s * STAGE + 2 * BG_BK * (BM + 1) + BG_BK * BN); };
   const int zl = blockIdx.z / ksplit;  // (product, party)
   const int ks = blockIdx.z % ksplit;
   const int bt = zl / L, l = zl - bt * L;
@@ -77,30 +94,46 @@ __global__ void __launch_bounds__((BM / 4) * (BN / TN), bg_min_blocks((BM / 4) *
 #pragma unroll
     for (int j = 0; j < TN; ++j) acc[i][j] = 0;
 
-  for (int k0 = kbeg; k0 < kend; k0 += BG_BK) {
+  auto issue = [&](int s, int k0) {
+    RowM* ds = Ds(s);
+    RowM* as = As(s);
+    RowN* bs = Bs(s);
+    RowN* es = Es(s);
     for (int idx = threadIdx.x; idx < BM * BG_BK; idx += NT) {
       const int r = idx / BG_BK, kk = idx % BG_BK;
       const int gr = row0 + r, gk = k0 + kk;
       const bool ok = gr < M && gk < kend;
-      const i64 o = (i64)gr * K + gk;
-      Ds[kk][r] = ok ? D[o] : 0ull;
-      As[kk][r] = ok ? Al[o] : 0ull;
+      const i64 o = ok ? (i64)gr * K + gk : 0;
+      cp_async8(&ds[kk][r], D + o, ok);
+      cp_async8(&as[kk][r], Al + o, ok);
     }
     for (int idx = threadIdx.x; idx < BN * BG_BK; idx += NT) {
       const int kk = idx / BN, c = idx % BN;
       const int gk = k0 + kk, gc = col0 + c;
       const bool ok = gk < kend && gc < N;
-      const i64 o = (i64)gk * N + gc;
-      const u64 e = ok ? E[o] : 0ull;
-      Es[kk][c] = e;
-      Bs[kk][c] = ok ? (Bl[o] + (addE ? e : 0ull)) : 0ull;
+      const i64 o = ok ? (i64)gk * N + gc : 0;
+      cp_async8(&es[kk][c], E + o, ok);
+      cp_async8(&bs[kk][c], Bl + o, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const int nsteps = kend > kbeg ? (kend - kbeg + BG_BK - 1) / BG_BK : 0;
+  if (nsteps > 0) issue(0, kbeg);
+  for (int step = 0; step < nsteps; ++step) {
+    const int k0 = kbeg + step * BG_BK;
+    if (step + 1 < nsteps) {
+      issue((step + 1) & 1, k0 + BG_BK);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
+    const int s = step & 1;
     const int kn = kend - k0;
     if (kn >= BG_BK)
-      bg_tile_math<BM, BN, TN, true>(acc, Ds, As, Bs, Es, tx, ty, kn);
+      bg_tile_math<BM, BN, TN, true>(acc, Ds(s), As(s), Bs(s), Es(s), tx, ty, kn, addE);
     else
-      bg_tile_math<BM, BN, TN, false>(acc, Ds, As, Bs, Es, tx, ty, kn);
+      bg_tile_math<BM, BN, TN, false>(acc, Ds(s), As(s), Bs(s), Es(s), tx, ty, kn, addE);
     __syncthreads();
   }
   u64* Zl = Z + (i64)l * sZ;
@@ -138,12 +171,21 @@ struct Batch {
 };
 
 template <int BM, int BN, int TN>
-void launch(dim3 grid, cudaStream_t s, uint64_t* Z, int64_t sZ, const uint64_t* C, int64_t sC, const uint64_t* D,
-            const uint64_t* E, const uint64_t* A, int64_t sA, const uint64_t* B, int64_t sB, int M, int K, int N,
-            int p0, u64 msk, int ksplit, int kchunk, const Batch& bt) {
-  k_beaver_gemm<BM, BN, TN><<<grid, (BM / 4) * (BN / TN), 0, s>>>(Z, sZ, C, sC, D, E, A, sA, B, sB, M, K, N, p0,
-                                                                    msk, ksplit, kchunk, bt.L, bt.bZ, bt.bC, bt.bA,
-                                                                    bt.bB);
+int launch(dim3 grid, cudaStream_t s, uint64_t* Z, int64_t sZ, const uint64_t* C, int64_t sC, const uint64_t* D,
+           const uint64_t* E, const uint64_t* A, int64_t sA, const uint64_t* B, int64_t sB, int M, int K, int N,
+           int p0, u64 msk, int ksplit, int kchunk, const Batch& bt) {
+  constexpr int smem = 2 * bg_stage_words<BM, BN>() * 8;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_beaver_gemm<BM, BN, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        cudaSuccess)
+      return MPX_ERR_CUDA;
+    attr = true;
+  }
+  k_beaver_gemm<BM, BN, TN><<<grid, (BM / 4) * (BN / TN), smem, s>>>(Z, sZ, C, sC, D, E, A, sA, B, sB, M, K, N, p0,
+                                                                       msk, ksplit, kchunk, bt.L, bt.bZ, bt.bC,
+                                                                       bt.bA, bt.bB);
+  return MPX_OK;
 }
 }  // namespace
 
@@ -196,8 +238,9 @@ extern "C" int mpx_beaver_gemm_batched(uint64_t* Z, int64_t sZ, int64_t bZ, cons
   const u64 msk = ring_mask(width);
 #define BG_CASE(I, BM_, BN_, TN_)                                                                             \
   case I:                                                                                                    \
-    launch<BM_, BN_, TN_>(grid, s, Z, sZ, C, sC, D, E, A, sA, B, sB, (int)M, (int)K, (int)N, p0, msk, ksplit, \
-                          (int)kchunk, bt);                                                                  \
+    if (launch<BM_, BN_, TN_>(grid, s, Z, sZ, C, sC, D, E, A, sA, B, sB, (int)M, (int)K, (int)N, p0, msk,     \
+                              ksplit, (int)kchunk, bt) != MPX_OK)                                            \
+      return MPX_ERR_CUDA;                                                                                   \
     break;
   switch (best) {
     BG_CASE(0, 64, 64, 4)

@@ -658,6 +658,36 @@ __global__ void k_im2col(u64* __restrict__ out, const u64* __restrict__ x, IT B,
   }
 }
 
+// Narrow rows (C*K*K < 64): a thread owns one output row, decomposes the row
+// index once and walks (c, kh, kw) with counters — the element-per-thread
+// kernel spent its time in six runtime integer divisions per element.
+__global__ void k_im2col_rows(u64* __restrict__ out, const u64* __restrict__ x, int L, int B, int C, int H, int W,
+                              int K, int S, int P, int OH, int OW) {
+  const int cols = C * K * K;
+  const i64 rows = (i64)B * OH * OW;
+  const i64 nrow = (i64)L * rows;
+  for (i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x; t < nrow; t += (i64)gridDim.x * blockDim.x) {
+    const i64 l = t / rows, row = t - l * rows;
+    const int ow = (int)(row % OW);
+    const i64 boh = row / OW;
+    const int oh = (int)(boh % OH), b = (int)(boh / OH);
+    const u64* img = x + ((i64)l * B + b) * C * H * W;
+    const int h0 = oh * S - P, w0 = ow * S - P;
+    u64* o = out + t * cols;
+    int col = 0;
+    for (int c = 0; c < C; ++c)
+      for (int kh = 0; kh < K; ++kh) {
+        const int h = h0 + kh;
+        const bool hin = h >= 0 && h < H;
+        const u64* rowp = img + ((i64)c * H + h) * W;
+        for (int kw = 0; kw < K; ++kw, ++col) {
+          const int w = w0 + kw;
+          o[col] = (hin && w >= 0 && w < W) ? rowp[w] : 0ull;
+        }
+      }
+  }
+}
+
 template <typename IT, bool S1>
 __global__ void k_col2im(u64* __restrict__ dx, const u64* __restrict__ colsb, IT B, IT C, IT H, IT W, IT K,
                          IT S, IT P, IT OH, IT OW, IT total, u64 msk) {
@@ -747,6 +777,11 @@ extern "C" int mpx_im2col(uint64_t* out, const uint64_t* x, int L, int64_t B, in
     const i64 blocks = min((nrow + 7) / 8, (i64)148 * 16);
     k_im2col_tab<<<(unsigned)blocks, 256, (size_t)cols * 8, (cudaStream_t)stream>>>(out, x, L, (int)B, C, H, W, K,
                                                                                    stride, pad, OH, OW);
+    return launch_status();
+  }
+  if (cols < 64 && (i64)L * B * C * H * W < (1ll << 40)) {
+    k_im2col_rows<<<grid_for((i64)L * B * OH * OW, 128), 128, 0, (cudaStream_t)stream>>>(
+        out, x, L, (int)B, C, H, W, K, stride, pad, OH, OW);
     return launch_status();
   }
   if (total < (1ll << 31))
