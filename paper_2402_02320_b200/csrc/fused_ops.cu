@@ -39,6 +39,15 @@ struct Tape {
 #define MPX_CMP_MINB 6  // 80 regs: 1.46 vs 1.63 ms (3 parties, 2^22 ReLU)
 #endif
 
+// min resident CTAs per SM (register cap) by local party count: L <= 2 / 3 / 4
+#ifndef MPX_MINB3
+#define MPX_MINB3 MPX_CMP_MINB
+#endif
+#ifndef MPX_MINB4
+#define MPX_MINB4 MPX_CMP_MINB
+#endif
+#define MPX_MINB_L(L, B2) ((L) <= 2 ? (B2) : (L) == 3 ? MPX_MINB3 : (L) == 4 ? MPX_MINB4 : 1)
+
 #ifndef MPX_LOG_MINB
 #define MPX_LOG_MINB 6  // 80 regs, 6 blocks: 8.95 vs 9.34 ms at 2^24
 #endif
@@ -655,7 +664,7 @@ __global__ void __launch_bounds__(128) k_attexp_fused(u64* __restrict__ y, const
 // Logarithm, paper Alg. 3 without the big-input pre-shift (nonlinear.py:216-267)
 
 template <int L>
-__global__ void __launch_bounds__(128, L <= 4 ? MPX_LOG_MINB : 1) k_log_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
+__global__ void __launch_bounds__(128, MPX_MINB_L(L, MPX_LOG_MINB)) k_log_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
                                                    const __grid_constant__ Tape tape, FusedParams P) {
   const int w = P.w, p = P.p, p0 = P.p0;
   const u64 msk = ring_mask(w);
@@ -729,7 +738,7 @@ __global__ void __launch_bounds__(128, L <= 4 ? MPX_LOG_MINB : 1) k_log_fused(u6
 // Also stores s (the converted sign) for the backward pass when s_out != 0.
 
 template <int L>
-__global__ void __launch_bounds__(128, L <= 4 ? MPX_CMP_MINB : 1) k_relu_fused(u64* __restrict__ y, u64* __restrict__ s_out,
+__global__ void __launch_bounds__(128, MPX_MINB_L(L, MPX_CMP_MINB)) k_relu_fused(u64* __restrict__ y, u64* __restrict__ s_out,
                                                     const u64* __restrict__ xin, i64 n,
                                                     const __grid_constant__ Tape tape, FusedParams P) {
   const int w = P.w, p0 = P.p0;
@@ -781,7 +790,7 @@ __device__ __forceinline__ Sh<L> d_maxpair(const Sh<L>& u, const Sh<L>& v, const
 }
 
 template <int L>
-__global__ void __launch_bounds__(128, L <= 4 ? MPX_CMP_MINB : 1) k_maxlevel_fused(u64* __restrict__ win, const u64* __restrict__ uin,
+__global__ void __launch_bounds__(128, MPX_MINB_L(L, MPX_CMP_MINB)) k_maxlevel_fused(u64* __restrict__ win, const u64* __restrict__ uin,
                                                         const u64* __restrict__ vin, i64 n,
                                                         const __grid_constant__ Tape tape, FusedParams P) {
   const int w = P.w, p0 = P.p0;

@@ -209,3 +209,45 @@ def test_gemm_limbs_short_k_blocks(K, M, Kd, N, b):
     with np.errstate(over="ignore"):
         for z in range(b):
             assert np.array_equal(got[z], C[z] + _mm(A[z], B[z])), z
+
+
+@pytest.mark.parametrize("L,p0,jobs,m,k,r,xt,yt", [
+    (3, 0, 1, 300, 130, 70, False, False),
+    (2, 1, 2, 128, 64, 96, False, True),     # batched jobs, transposed B-side operand
+    (3, 2, 1, 200, 25, 20, True, False),     # transposed A-side operand, 32-byte k-blocks, 32-wide N tile
+    (4, 0, 3, 96, 200, 40, False, False),
+])
+def test_mask_limbs_split_gemm_matches_numpy(K, L, p0, jobs, m, k, r, xt, yt):
+    """Fused sim-mode Beaver operands (mask + open + limb split, shared D/E
+    limbs) and the split-operand GEMM: Z_l = C_l + D @ (B_l + [l==p0] E) +
+    A_l @ E with D = sum_l X_l - A_l, E = sum_l Y_l - B_l (basic.py:66-75)."""
+    rng = np.random.default_rng(m + k + r + jobs)
+    X = _rand(rng, (jobs, L, m, k), 64)
+    Y = _rand(rng, (jobs, L, k, r), 64)
+    A, B, C = _rand(rng, (jobs, L, m, k), 64), _rand(rng, (jobs, L, k, r), 64), _rand(rng, (jobs, L, m, r), 64)
+    # operands as the protocol sees them: [L, rows, cols] views (transposed storage when asked)
+    Xd = _dev(np.ascontiguousarray(X.transpose(0, 1, 3, 2))).transpose(2, 3) if xt else _dev(X)
+    Yd = _dev(np.ascontiguousarray(Y.transpose(0, 1, 3, 2))).transpose(2, 3) if yt else _dev(Y)
+    Ad, Bd, Cd = _dev(A), _dev(B), _dev(C)
+    Mp, Np, Kh = K._rup(m, 128), K._rup(r, 32), K.kpad(k)
+    SA = torch.empty((jobs, 8, Mp, Kh), dtype=torch.uint8, device="cuda")
+    PA = torch.empty((jobs, L, 8, Mp, Kh), dtype=torch.uint8, device="cuda")
+    SB = torch.empty((jobs, 8, Np, Kh), dtype=torch.uint8, device="cuda")
+    PB = torch.empty((jobs, L, 8, Np, Kh), dtype=torch.uint8, device="cuda")
+    x0, y0 = Xd[0], Yd[0]
+    K.mask_limbs(SA, PA, x0.data_ptr(), x0.stride(0), x0.stride(1), x0.stride(2), Ad.data_ptr(), m * k, k, 1, L, m,
+                 k, Mp, Kh, p0, False, 64, jobs=jobs, x_js=Xd.stride(0), t_js=L * m * k)
+    K.mask_limbs(SB, PB, y0.data_ptr(), y0.stride(0), y0.stride(2), y0.stride(1), Bd.data_ptr(), k * r, 1, r, L, r,
+                 k, Np, Kh, p0, True, 64, jobs=jobs, x_js=Yd.stride(0), t_js=L * k * r)
+    Z = torch.empty((jobs, L, m, r), dtype=torch.int64, device="cuda")
+    K.gemm_limbs_split(Z, PA, SA, PB, SB, jobs * L, m, r, Mp, Np, Kh, r, m * r, 64, Cd.data_ptr(), m * r, zl=L,
+                       s_cin_j=L * m * r)
+    got = _host(Z)
+    with np.errstate(over="ignore"):
+        for j in range(jobs):
+            D = (X[j] - A[j]).sum(0, dtype=np.uint64)
+            E = (Y[j] - B[j]).sum(0, dtype=np.uint64)
+            for l in range(L):
+                Bl = B[j, l] + (E if l == p0 else np.uint64(0))
+                want = C[j, l] + _mm(D, Bl) + _mm(A[j, l], E)
+                assert np.array_equal(got[j, l], want), (j, l)
