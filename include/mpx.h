@@ -336,6 +336,15 @@ int mpx_maxlevel_fused(uint64_t* win, const uint64_t* u, const uint64_t* v, int6
 int mpx_maxtour_fused(uint64_t* y, const uint64_t* x, int64_t rows, int d0, const void* tape_host,
                       const void* levels_host, const void* params_host, void* stream);
 int mpx_fused_tour_size(int64_t* levels);
+/* softmax_parts (nn.py:115-136) in one launch, one CTA per row (d0 <= 256):
+ * [rescale by log2 e], narrow to 32 bits, max tournament, x - max - 1 ulp,
+ * attention_exp, row sum, reciprocal. `segs_host` (SoftmaxSegs) holds each
+ * stage's first tape index; the three FusedParams are the tournament's,
+ * attention-exp's and reciprocal's. Outputs e (like x) and r (one per row). */
+int mpx_softmax_fused(uint64_t* e_out, uint64_t* r_out, const uint64_t* x, int64_t rows, int d0,
+                      const void* tape_host, const void* segs_host, const void* pm_host, const void* pe_host,
+                      const void* pr_host, void* stream);
+int mpx_fused_softmax_size(int64_t* segs);
 int mpx_fused_abi_sizes(int64_t* matref, int64_t* tape, int64_t* params, int64_t* tape_max);
 
 /* ---- trusted dealer (preprocessing.py:121-174; ring.py:124-134) ----

@@ -101,7 +101,8 @@ def exported_symbols() -> list[str]:
     return sorted(list(_SIGS) + ["mpx_version", "mpx_cuda_error_string", "mpx_reciprocal_fused",
                                  "mpx_exp_fused", "mpx_log_fused", "mpx_fused_abi_sizes",
                                  "mpx_relu_fused", "mpx_maxlevel_fused", "mpx_attexp_fused",
-                                 "mpx_maxtour_fused", "mpx_fused_tour_size"])
+                                 "mpx_maxtour_fused", "mpx_fused_tour_size", "mpx_softmax_fused",
+                                 "mpx_fused_softmax_size"])
 
 
 def load() -> ctypes.CDLL:

@@ -16,7 +16,7 @@
 // local party counts with fused instantiations: every n <= 4, and n = 8
 #define FUSED_L_OK(L) (((L) >= 1 && (L) <= 4) || (L) == 8)
 
-#define TAPE_MAX 160  // a whole max_vec tournament (<= 10 levels of ~9 takes) fits one tape
+#define TAPE_MAX 160  // a whole softmax (rescale, <= 7 tournament levels, attention-exp, reciprocal) fits one tape
 
 struct MatRef {
   const u64* p0;  // triple a | bintriple a | dabit/edabit arithmetic part
@@ -502,6 +502,59 @@ __device__ __forceinline__ void store_sh(u64* y, i64 n, i64 e, const Sh<L>& s) {
 // ---------------------------------------------------------------------------
 // Reciprocal, paper Alg. 1 (nonlinear.py:146-176)
 
+// Reciprocal (Alg. 1, nonlinear.py:146-176) of one element's shares.
+template <int L>
+__device__ __forceinline__ Sh<L> d_reciprocal(const Sh<L>& x, const Tape& tape, int& ti, i64 e,
+                                              const FusedParams& P) {
+  const int w = P.w, p = P.p, p0 = P.p0;
+  const u64 msk = ring_mask(w);
+  const Sh<L> bits = d_decompose<L>(x, w, tape, ti, e, p0);
+  Sh<L> sign, mag;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    sign.v[l] = (bits.v[l] >> (w - 1)) & 1ull;
+    const u64 mm = low_bits(w - 1);
+    mag.v[l] = (bits.v[l] & mm) ^ (sign.v[l] ? mm : 0ull);
+  }
+  const MatRef& tsg = next_take<L>(tape, ti, e);
+  const u64 csg = d_bit2a_open<L>(sign, 1, tsg, e);
+  const Sh<L> s = d_bit2a_get<L>(csg, 0, 1, tsg, e, p0, msk);
+  const Sh<L> sx = d_mul<L>(s, x, next_take<L>(tape, ti, e), e, p0, msk);
+  const Sh<L> x_pos = sh_lin<L>(x, 1, sx, 0ull - 2ull, 0, p0, msk);
+  const Sh<L> onehot = d_lmo<L>(mag, w - 1, tape, ti, e, p0);
+  // reversed low 2p window -> compose (basic.py:187-196)
+  Sh<L> window;
+#pragma unroll
+  for (int l = 0; l < L; ++l) window.v[l] = __brevll(onehot.v[l] & low_bits(2 * p)) >> (64 - 2 * p);
+  const MatRef& tc = next_take<L>(tape, ti, e);
+  const u64 cw = d_bit2a_open<L>(window, 2 * p, tc, e);
+  Sh<L> t;
+#pragma unroll
+  for (int l = 0; l < L; ++l) t.v[l] = 0;
+  d_bit2a_row<L>(cw, 2 * p, 2 * p, tc, e, p0, msk, [&](int l, int j, u64 z) { t.v[l] += z << j; });
+#pragma unroll
+  for (int l = 0; l < L; ++l) t.v[l] &= msk;
+  // z = trunc(t * x_pos), Newton product (nonlinear.py:134-143), y = trunc(t * acc):
+  // a chain of 2*iters mul+trunc steps, pipelined one step ahead (A/B)
+  MTM<L> A, B;
+  mt_load<L>(A, tape, ti, e, p, w);
+  mt_load<L>(B, tape, ti, e, p, w);
+  const Sh<L> z = mt_compute<L>(t, x_pos, A, p, w, p0, msk);
+  Sh<L> q = sh_scale<L>(z, 0ull - 1ull, P.one_p, p0, msk);
+  Sh<L> acc = sh_scale<L>(q, 1, P.one_p, p0, msk);
+  for (int it = 1; it < P.iters; ++it) {
+    mt_load<L>(A, tape, ti, e, p, w);
+    q = mt_compute<L>(q, q, B, p, w, p0, msk);
+    mt_load<L>(B, tape, ti, e, p, w);
+    acc = mt_compute<L>(acc, sh_scale<L>(q, 1, P.one_p, p0, msk), A, p, w, p0, msk);
+  }
+  const Sh<L> yv = mt_compute<L>(t, acc, B, p, w, p0, msk);
+  const Sh<L> sy = d_mul<L>(s, yv, next_take<L>(tape, ti, e), e, p0, msk);
+  return sh_lin<L>(yv, 1, sy, 0ull - 2ull, 0, p0, msk);
+}
+
+// Standalone kernel keeps its own copy of the body: through d_reciprocal it
+// compiles to 72 registers + spills at L = 2 (8.3 vs 7.9 ms at 2^24).
 template <int L>
 __global__ void __launch_bounds__(128) k_reciprocal_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
                                                           const __grid_constant__ Tape tape, FusedParams P) {
@@ -566,6 +619,8 @@ __global__ void __launch_bounds__(128) k_exp_fused(u64* __restrict__ y, const u6
   const u64 msk = ring_mask(w);
   GRID_STRIDE(e, n) {
     int ti = 0;
+    if (P.pf)  // small calls are latency-bound: pull the element's whole tape towards L2 first
+      for (int i = 0; i < tape.n; ++i) prefetch_take<L>(tape.m[i], e);
     const Sh<L> x = load_sh<L>(xin, n, e);
     const Sh<L> xb = sh_scale<L>(x, P.log2e_p, P.bias_2p, p0, msk);
     const Sh<L> bits = d_decompose<L>(xb, w, tape, ti, e, p0);
@@ -606,57 +661,65 @@ __global__ void __launch_bounds__(128) k_exp_fused(u64* __restrict__ y, const u6
 // P.coef_p[0] = enc(p + delta, 32, p), coef_p[1..3] = enc(t3 | t2 | lead*t1,
 // 64, p), coef0_2p = enc(lead*t0, 64, 2p), P.bias = lead_shift, P.c = c.
 
+// attention_exp (App. E, nonlinear.py:315-356): narrow input, 64-bit output.
+template <int L>
+__device__ __forceinline__ Sh<L> d_attexp(const Sh<L>& x, const Tape& tape, int& ti, i64 e, const FusedParams& P) {
+  const int win = P.w, p = P.p, p0 = P.p0, c = P.c;
+  const u64 msk_in = ring_mask(win), msk = ring_mask(64);
+  const Sh<L> xb = sh_scale<L>(x, 1ull, P.coef_p[0], p0, msk_in);
+  const Sh<L> bits = d_decompose<L>(xb, win, tape, ti, e, p0);
+  const int k = p + c + 1;
+  Sh<L> seg;
+#pragma unroll
+  for (int l = 0; l < L; ++l)
+    seg.v[l] = (bits.v[l] & low_bits(p + c)) | (((bits.v[l] >> (win - 1)) & 1ull) << (p + c));
+  const MatRef& tc = next_take<L>(tape, ti, e);
+  const u64 cw = d_bit2a_open<L>(seg, k, tc, e);
+  Sh<L> t;
+#pragma unroll
+  for (int l = 0; l < L; ++l) t.v[l] = 0;
+  d_bit2a_row<L>(cw, p, k, tc, e, p0, msk, [&](int l, int j, u64 z) { t.v[l] += z << j; });
+  // 2^int as a product of (2^(2^i) b_i - b_i + 1) (nonlinear.py:125-131)
+  Sh<L> pw = sh_scale<L>(d_bit2a_get<L>(cw, p, k, tc, e, p0, msk), 1ull, 1ull, p0, msk);
+  for (int i = 1; i < c; ++i) {
+    const Sh<L> bi = d_bit2a_get<L>(cw, p + i, k, tc, e, p0, msk);
+    const u64 kf = (1ull << (1 << i)) - 1ull;
+    pw = d_mul<L>(pw, sh_scale<L>(bi, kf, 1ull, p0, msk), next_take<L>(tape, ti, e), e, p0, msk);
+  }
+  const Sh<L> sgn = d_bit2a_get<L>(cw, p + c, k, tc, e, p0, msk);
+  // evaluate_square_completed (derived.py:111-128)
+  const Sh<L> u = sh_scale<L>(t, 1ull, P.coef_p[1], p0, msk);
+  const Sh<L> u2 = d_mul_trunc<L>(u, u, tape, ti, e, p, 64, p0, msk);
+  const Sh<L> v = sh_scale<L>(u2, 1ull, P.coef_p[2], p0, msk);
+  const Sh<L> sq = d_mul<L>(v, v, next_take<L>(tape, ti, e), e, p0, msk);
+  Sh<L> lead = sq;  // truncate(sq, 0) is a copy (derived.py:55-57)
+  if (P.bias > 0) {
+    const MatRef& lo = next_take<L>(tape, ti, e);
+    const MatRef* hi = (64 - 1 - P.bias > 0) ? &next_take<L>(tape, ti, e) : nullptr;
+    lead = d_trunc<L>(sq, lo, hi, e, P.bias, true, 64, p0, msk);
+  }
+  Sh<L> acc = sh_lin<L>(lead, 1ull, t, P.coef_p[3], P.coef0_2p, p0, msk);
+  Sh<L> ev;
+  {
+    const MatRef& lo = next_take<L>(tape, ti, e);
+    const MatRef& hi = next_take<L>(tape, ti, e);
+    ev = d_trunc<L>(acc, lo, &hi, e, p, true, 64, p0, msk);
+  }
+  const Sh<L> yv = d_mul<L>(pw, ev, next_take<L>(tape, ti, e), e, p0, msk);
+  const Sh<L> s1 = sh_scale<L>(sgn, 0ull - 1ull, 1ull, p0, msk);
+  const Sh<L> out = d_mul_trunc<L>(s1, yv, tape, ti, e, p, 64, p0, msk);
+  return out;
+}
+
 template <int L>
 __global__ void __launch_bounds__(128) k_attexp_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
                                                       const __grid_constant__ Tape tape, FusedParams P) {
-  const int win = P.w, p = P.p, p0 = P.p0, c = P.c;
-  const u64 msk_in = ring_mask(win), msk = ring_mask(64);
   GRID_STRIDE(e, n) {
     int ti = 0;
+    if (P.pf)  // small calls are latency-bound: pull the element's whole tape towards L2 first
+      for (int i = 0; i < tape.n; ++i) prefetch_take<L>(tape.m[i], e);
     const Sh<L> x = load_sh<L>(xin, n, e);
-    const Sh<L> xb = sh_scale<L>(x, 1ull, P.coef_p[0], p0, msk_in);
-    const Sh<L> bits = d_decompose<L>(xb, win, tape, ti, e, p0);
-    const int k = p + c + 1;
-    Sh<L> seg;
-#pragma unroll
-    for (int l = 0; l < L; ++l)
-      seg.v[l] = (bits.v[l] & low_bits(p + c)) | (((bits.v[l] >> (win - 1)) & 1ull) << (p + c));
-    const MatRef& tc = next_take<L>(tape, ti, e);
-    const u64 cw = d_bit2a_open<L>(seg, k, tc, e);
-    Sh<L> t;
-#pragma unroll
-    for (int l = 0; l < L; ++l) t.v[l] = 0;
-    d_bit2a_row<L>(cw, p, k, tc, e, p0, msk, [&](int l, int j, u64 z) { t.v[l] += z << j; });
-    // 2^int as a product of (2^(2^i) b_i - b_i + 1) (nonlinear.py:125-131)
-    Sh<L> pw = sh_scale<L>(d_bit2a_get<L>(cw, p, k, tc, e, p0, msk), 1ull, 1ull, p0, msk);
-    for (int i = 1; i < c; ++i) {
-      const Sh<L> bi = d_bit2a_get<L>(cw, p + i, k, tc, e, p0, msk);
-      const u64 kf = (1ull << (1 << i)) - 1ull;
-      pw = d_mul<L>(pw, sh_scale<L>(bi, kf, 1ull, p0, msk), next_take<L>(tape, ti, e), e, p0, msk);
-    }
-    const Sh<L> sgn = d_bit2a_get<L>(cw, p + c, k, tc, e, p0, msk);
-    // evaluate_square_completed (derived.py:111-128)
-    const Sh<L> u = sh_scale<L>(t, 1ull, P.coef_p[1], p0, msk);
-    const Sh<L> u2 = d_mul_trunc<L>(u, u, tape, ti, e, p, 64, p0, msk);
-    const Sh<L> v = sh_scale<L>(u2, 1ull, P.coef_p[2], p0, msk);
-    const Sh<L> sq = d_mul<L>(v, v, next_take<L>(tape, ti, e), e, p0, msk);
-    Sh<L> lead = sq;  // truncate(sq, 0) is a copy (derived.py:55-57)
-    if (P.bias > 0) {
-      const MatRef& lo = next_take<L>(tape, ti, e);
-      const MatRef* hi = (64 - 1 - P.bias > 0) ? &next_take<L>(tape, ti, e) : nullptr;
-      lead = d_trunc<L>(sq, lo, hi, e, P.bias, true, 64, p0, msk);
-    }
-    Sh<L> acc = sh_lin<L>(lead, 1ull, t, P.coef_p[3], P.coef0_2p, p0, msk);
-    Sh<L> ev;
-    {
-      const MatRef& lo = next_take<L>(tape, ti, e);
-      const MatRef& hi = next_take<L>(tape, ti, e);
-      ev = d_trunc<L>(acc, lo, &hi, e, p, true, 64, p0, msk);
-    }
-    const Sh<L> yv = d_mul<L>(pw, ev, next_take<L>(tape, ti, e), e, p0, msk);
-    const Sh<L> s1 = sh_scale<L>(sgn, 0ull - 1ull, 1ull, p0, msk);
-    const Sh<L> out = d_mul_trunc<L>(s1, yv, tape, ti, e, p, 64, p0, msk);
-    store_sh<L>(y, n, e, out);
+    store_sh<L>(y, n, e, d_attexp<L>(x, tape, ti, e, P));
   }
 }
 
@@ -671,6 +734,8 @@ __global__ void __launch_bounds__(128, MPX_MINB_L(L, MPX_LOG_MINB)) k_log_fused(
   const int m2 = 2 * p;
   GRID_STRIDE(e, n) {
     int ti = 0;
+    if (P.pf)  // small calls are latency-bound: pull the element's whole tape towards L2 first
+      for (int i = 0; i < tape.n; ++i) prefetch_take<L>(tape.m[i], e);
     const Sh<L> x = load_sh<L>(xin, n, e);
     const Sh<L> bits = d_decompose<L>(x, w, tape, ti, e, p0);
     Sh<L> window;
@@ -867,6 +932,152 @@ __global__ void __launch_bounds__(256) k_maxtour_fused(u64* __restrict__ out, co
       for (int l = 0; l < L; ++l) out[(i64)l * rows + row] = vals[l * d0];
     __syncthreads();
   }
+}
+
+// softmax_parts (nn.py:115-136) of a row in one CTA: [rescale x = trunc(x *
+// log2 e)], narrow to 32 bits, the max_vec tournament, x - max - 1 ulp,
+// attention_exp per element, the row sum and its reciprocal. Every stage
+// reads its takes at the flat index its standalone kernel uses (rescale /
+// exp: row * d0 + j, tournament level: row * half + j, reciprocal: row), and
+// the stages' tapes are scheduled with the standalone keys in the standalone
+// order, so shares, material use and the ledger equal the per-op path.
+struct SoftmaxSegs {
+  int resc;        // tape index of the rescale truncation (-1: base-2 input)
+  int lev[17];     // tournament level starts
+  int nlev;
+  int attexp, recip, end;
+  u64 log2e_p;     // enc(log2 e, 64, p) for the rescale
+  int p, w32;
+};
+
+template <int L>
+__global__ void __launch_bounds__(256) k_softmax_fused(u64* __restrict__ eout, u64* __restrict__ rout,
+                                                       const u64* __restrict__ in, i64 rows, int d0,
+                                                       const __grid_constant__ Tape tape,
+                                                       const __grid_constant__ SoftmaxSegs sg, FusedParams Pm,
+                                                       FusedParams Pe, FusedParams Pr) {
+  extern __shared__ u64 sm_vals[];  // [L][d0] tournament values, then [L][nwarps] row-sum partials
+  const int p0 = Pm.p0;
+  const u64 m64 = ring_mask(64), m32 = ring_mask(sg.w32);
+  const int j = threadIdx.x;
+  const int nw = (blockDim.x + 31) / 32;
+  u64* part = sm_vals + L * d0;
+  for (i64 row = blockIdx.x; row < rows; row += gridDim.x) {
+    Sh<L> v;
+    if (j < d0) {
+      const i64 e = row * d0 + j;
+#pragma unroll
+      for (int l = 0; l < L; ++l) v.v[l] = in[((i64)l * rows + row) * d0 + j];
+      if (sg.resc >= 0) {  // truncate(scale_fixed(x, log2 e), p) (derived.py:55-83)
+        int ti = sg.resc;
+        const Sh<L> sc = sh_scale<L>(v, sg.log2e_p, 0ull, p0, m64);
+        const MatRef& lo = next_take<L>(tape, ti, e);
+        const MatRef& hi = next_take<L>(tape, ti, e);
+        v = d_trunc<L>(sc, lo, &hi, e, sg.p, true, 64, p0, m64);
+      }
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        v.v[l] &= m32;  // narrow (nn.py:68-74)
+        sm_vals[l * d0 + j] = v.v[l];
+      }
+    }
+    __syncthreads();
+    // max_vec tournament (derived.py:152-170)
+    int d = d0;
+    for (int lev = 0; lev < sg.nlev; ++lev) {
+      const int half = d / 2, rest = d - 2 * half;
+      Sh<L> win;
+      if (j < half) {
+        int ti = sg.lev[lev];
+        Sh<L> u, w;
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+          u.v[l] = sm_vals[l * d0 + j];
+          w.v[l] = sm_vals[l * d0 + half + j];
+        }
+        win = d_maxpair<L>(u, w, tape, ti, row * (i64)half + j, sg.w32, p0, m32);
+      }
+      Sh<L> rv;
+      if (j == 0 && rest)
+#pragma unroll
+        for (int l = 0; l < L; ++l) rv.v[l] = sm_vals[l * d0 + 2 * half];
+      __syncthreads();
+      if (j < half)
+#pragma unroll
+        for (int l = 0; l < L; ++l) sm_vals[l * d0 + j] = win.v[l];
+      if (j == 0 && rest)
+#pragma unroll
+        for (int l = 0; l < L; ++l) sm_vals[l * d0 + half] = rv.v[l];
+      __syncthreads();
+      d = half + rest;
+    }
+    // x - max - 1 ulp (nn.py:100-112), attention_exp, row sum
+    Sh<L> ev;
+#pragma unroll
+    for (int l = 0; l < L; ++l) ev.v[l] = 0;
+    if (j < d0) {
+      Sh<L> sh;
+#pragma unroll
+      for (int l = 0; l < L; ++l) sh.v[l] = (v.v[l] - sm_vals[l * d0] + (l == p0 ? m32 : 0ull)) & m32;
+      int ti = sg.attexp;
+      ev = d_attexp<L>(sh, tape, ti, row * (i64)d0 + j, Pe);
+#pragma unroll
+      for (int l = 0; l < L; ++l) eout[((i64)l * rows + row) * d0 + j] = ev.v[l];
+    }
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      u64 s = ev.v[l];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if ((j & 31) == 0) part[l * nw + (j >> 5)] = s;
+    }
+    __syncthreads();
+    if (j == 0) {
+      Sh<L> tot;
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        u64 s = 0;
+        for (int q = 0; q < nw; ++q) s += part[l * nw + q];
+        tot.v[l] = s & m64;
+      }
+      int ti = sg.recip;
+      const Sh<L> r = d_reciprocal<L>(tot, tape, ti, row, Pr);
+#pragma unroll
+      for (int l = 0; l < L; ++l) rout[(i64)l * rows + row] = r.v[l];
+    }
+    __syncthreads();
+  }
+}
+
+extern "C" int mpx_softmax_fused(uint64_t* e_out, uint64_t* r_out, const uint64_t* x, int64_t rows, int d0,
+                                 const void* tape_host, const void* segs_host, const void* pm_host,
+                                 const void* pe_host, const void* pr_host, void* stream) {
+  CHECK_ARG(e_out && r_out && x && rows >= 0 && d0 >= 2 && d0 <= 256 && tape_host && segs_host && pm_host &&
+            pe_host && pr_host);
+  const Tape& tp = *(const Tape*)tape_host;
+  const SoftmaxSegs& sg = *(const SoftmaxSegs*)segs_host;
+  const FusedParams& Pm = *(const FusedParams*)pm_host;
+  const FusedParams& Pe = *(const FusedParams*)pe_host;
+  const FusedParams& Pr = *(const FusedParams*)pr_host;
+  CHECK_ARG(tp.n >= 1 && tp.n <= TAPE_MAX && sg.nlev >= 1 && sg.nlev <= 16 && FUSED_L_OK(Pm.L));
+  if (rows == 0) return MPX_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int threads = max(32, ((d0 + 31) / 32) * 32);
+  const unsigned g = (unsigned)min(rows, (i64)(148 * 8));
+  const size_t sm = (size_t)Pm.L * (d0 + threads / 32) * 8;
+  switch (Pm.L) {
+    case 1: k_softmax_fused<1><<<g, threads, sm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr); break;
+    case 2: k_softmax_fused<2><<<g, threads, sm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr); break;
+    case 3: k_softmax_fused<3><<<g, threads, sm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr); break;
+    case 4: k_softmax_fused<4><<<g, threads, sm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr); break;
+    default: k_softmax_fused<8><<<g, threads, sm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr); break;
+  }
+  return launch_status();
+}
+
+extern "C" int mpx_fused_softmax_size(int64_t* segs) {
+  *segs = sizeof(SoftmaxSegs);
+  return MPX_OK;
 }
 
 extern "C" int mpx_maxtour_fused(uint64_t* y, const uint64_t* x, int64_t rows, int d0, const void* tape_host,

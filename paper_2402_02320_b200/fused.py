@@ -43,6 +43,12 @@ class TourLevels(ctypes.Structure):
     _fields_ = [("start", ctypes.c_int * 17), ("nlev", ctypes.c_int)]
 
 
+class SoftmaxSegs(ctypes.Structure):
+    _fields_ = [("resc", ctypes.c_int), ("lev", ctypes.c_int * 17), ("nlev", ctypes.c_int),
+                ("attexp", ctypes.c_int), ("recip", ctypes.c_int), ("end", ctypes.c_int),
+                ("log2e_p", ctypes.c_uint64), ("p", ctypes.c_int), ("w32", ctypes.c_int)]
+
+
 class FusedParams(ctypes.Structure):
     _fields_ = [("w", ctypes.c_int), ("p", ctypes.c_int), ("iters", ctypes.c_int), ("bias", ctypes.c_int),
                 ("c", ctypes.c_int), ("L", ctypes.c_int), ("p0", ctypes.c_int),
@@ -165,6 +171,14 @@ def _bind():
         lib.mpx_fused_tour_size(ctypes.byref(tsz))
         if tsz.value != ctypes.sizeof(TourLevels):
             raise _lib.MpxError(f"fused tournament ABI mismatch: C {tsz.value} vs ctypes {ctypes.sizeof(TourLevels)}")
+        lib.mpx_softmax_fused.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int64, ctypes.c_int] + \
+            [ctypes.c_void_p] * 6
+        lib.mpx_softmax_fused.restype = ctypes.c_int
+        lib.mpx_fused_softmax_size.argtypes = [ctypes.POINTER(ctypes.c_int64)]
+        ssz = ctypes.c_int64()
+        lib.mpx_fused_softmax_size(ctypes.byref(ssz))
+        if ssz.value != ctypes.sizeof(SoftmaxSegs):
+            raise _lib.MpxError(f"fused softmax ABI mismatch: C {ssz.value} vs ctypes {ctypes.sizeof(SoftmaxSegs)}")
         lib.mpx_fused_abi_sizes.argtypes = [ctypes.POINTER(ctypes.c_int64)] * 4
         sizes = [ctypes.c_int64() for _ in range(4)]
         lib.mpx_fused_abi_sizes(*[ctypes.byref(s) for s in sizes])
@@ -210,10 +224,18 @@ def fusable_cmp(session, x: AShare) -> bool:
             and 8 <= x.width <= 64 and (1 <= session.L <= 4 or session.L == 8) and x.size > 0)
 
 
+# Reciprocal / Exp / Log / attention-exp calls of at most this many elements
+# (softmax row sums, LeNet's 128 x 10 logits, attention scores) prefetch each
+# element's whole take list to L2 before the first round: they are chains of
+# dependent rounds on a few CTAs, not bandwidth-bound (env MPX_PF_SMALL).
+PF_SMALL_ELEMS = int(os.environ.get("MPX_PF_SMALL", "0"))  # measured neutral: off
+
+
 def params_for(kind: str, session, x: AShare, params) -> FusedParams:
     w, p = x.width, x.frac
     P = FusedParams()
     P.w, P.p, P.L, P.p0 = w, p, session.L, session.p0
+    P.pf = int(x.size <= PF_SMALL_ELEMS)
     P.iters = params.newton_iters
     coeffs = None
     if kind == "exp":
@@ -389,3 +411,97 @@ def maxtour_fused(session, x: AShare, protocol) -> AShare:
                                        ctypes.addressof(tape), ctypes.addressof(lv), ctypes.addressof(P)),
             ("maxtour", rows, session.L, None, 0))
     return AShare(y, x.width, x.frac, session.parties)
+
+
+SOFTMAX_FUSED_MAX_ROWS = int(os.environ.get("MPX_SOFTMAX_FUSED_ROWS", "296"))   # 2 CTAs x 148 SMs
+
+
+def softmax_fusable(session, x: AShare, cast_width) -> bool:
+    """One-kernel softmax_parts: 64-bit input narrowed to 32 bits, rows of
+    2..256 (one CTA per row), and the attention-exp / reciprocal kernels'
+    own conditions on the narrowed values / row sums."""
+    if not x.shape or cast_width != 32 or x.width != 64:
+        return False
+    d = x.shape[-1]
+    if not (2 <= d <= 256 and fusable_cmp(session, x)):
+        return False
+    # one CTA per row runs every stage's chain of rounds back to back (the
+    # reciprocal on one thread): a win only when all rows are resident at once
+    # (LeNet's 128 logit rows); the attention's 1024 rows would take several
+    # waves of the whole chain (measured 3.82 vs 3.33 ms per Transformer
+    # forward), so they keep the per-stage kernels.
+    if x.size // d > SOFTMAX_FUSED_MAX_ROWS:
+        return False
+    narrow_meta = AShare(torch.empty((session.L,) + x.shape, dtype=torch.int64, device="meta"), 32, x.frac,
+                         x.parties)
+    return fusable_attexp(session, narrow_meta) and fusable(session, x)
+
+
+def softmax_fused(session, x: AShare, params, base2: bool, protocols):
+    """softmax_parts (nn.py:115-136) in ONE kernel, one CTA per row. Each
+    stage's takes are scheduled exactly as the standalone fused kernels
+    schedule them (same keys, same scopes, same order) and concatenated into
+    one tape, so material use and the ledger equal the per-op path.
+    ``protocols``: (rescale, max_level, attention_exp, reciprocal) callables
+    for the dry passes. Returns (e, r)."""
+    lib = _bind()
+    rescale, max_level, att, recip = protocols
+    p, L = x.frac, session.L
+    d0 = x.shape[-1]
+    lead = x.shape[:-1]
+    rows = x.size // d0
+    meta = lambda shape, w, f: AShare(torch.empty((L,) + tuple(shape), dtype=torch.int64, device="meta"), w, f,  # noqa: E731
+                                      x.parties)
+    entries = []
+    sg = SoftmaxSegs()
+    sg.resc = -1
+    if not base2:
+        with session.scope("rescale"):
+            key = ("softmax_rescale", x.shape, x.width, p, L, session.n_parties, session.p0)
+            tape, _ = _schedule("softmax_rescale", session, key, x.size, rescale, (meta(x.shape, 64, p),))
+            sg.resc = len(entries)
+            entries += [tape.m[i] for i in range(tape.n)]
+    with session.scope("maxcut"):
+        d, nlev = d0, 0
+        while d > 1:
+            half = d // 2
+            shp = lead + (half,)
+            mu = meta(shp, 32, p)
+            key = ("maxlevel", shp, 32, p, L, session.n_parties, session.p0)
+            tape, _ = _schedule("maxlevel", session, key, rows * half, max_level, (mu, mu))
+            sg.lev[nlev] = len(entries)
+            nlev += 1
+            entries += [tape.m[i] for i in range(tape.n)]
+            d = half + (d - 2 * half)
+        sg.nlev = nlev
+    with session.scope("exp"):
+        xm = meta(x.shape, 32, p)
+        key = ("attexp", x.shape, 32, p, params, L, session.n_parties, session.p0)
+        tape, (_, _, ew, ef) = _schedule("attexp", session, key, x.size, att, (xm,))
+        sg.attexp = len(entries)
+        entries += [tape.m[i] for i in range(tape.n)]
+        Pe = params_for("attexp", session, xm, params)
+    with session.scope("sum_recip"):
+        rm = meta(lead, ew, ef)
+        key = ("reciprocal", tuple(lead), ew, ef, params, L, session.n_parties, session.p0)
+        tape, (_, _, rw, rf) = _schedule("reciprocal", session, key, rows, recip, (rm,))
+        sg.recip = len(entries)
+        entries += [tape.m[i] for i in range(tape.n)]
+        Pr = params_for("reciprocal", session, rm, params)
+    sg.end = len(entries)
+    if len(entries) > TAPE_MAX:
+        raise _lib.MpxError(f"softmax of width {d0}: {len(entries)} takes exceed the tape")
+    tp = Tape()
+    for i, m in enumerate(entries):
+        tp.m[i] = m
+    tp.n = len(entries)
+    sg.log2e_p = encode_scalar(math.log2(math.e), 64, p)
+    sg.p, sg.w32 = p, 32
+    Pm = _basic_params(session, meta(x.shape, 32, p))
+    Pe.pf = Pr.pf = 0
+    e = session.alloc((L,) + x.shape)
+    r = session.alloc((L,) + tuple(lead))
+    _launch(lib, "mpx_softmax_fused", (e.data_ptr(), r.data_ptr(), x.values.contiguous().data_ptr(), rows, d0,
+                                       ctypes.addressof(tp), ctypes.addressof(sg), ctypes.addressof(Pm),
+                                       ctypes.addressof(Pe), ctypes.addressof(Pr)), ("softmax", rows, L, None, 0))
+    return AShare(e, ew, ef, session.parties), AShare(r, rw, rf, session.parties)
