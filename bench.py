@@ -310,6 +310,21 @@ def alg_bytes(name, a):
             L, R, Kd, Rpad, Kp = a[10], a[11], a[12], a[13], a[14]
             jobs = a[18] if len(a) > 18 else 1
             return jobs * (2 * L * R * Kd * 8 + (1 + L) * 8 * Rpad * Kp)
+        if name == "mpx_mask_limbs2":
+            # both sides: X_l, A_l / Y_l, B_l read once; shared + per-party limb planes written
+            M, Mpad, N, Npad, L, Kd, Kp, jobs = a[10], a[11], a[22], a[23], a[24], a[25], a[26], a[29]
+            return jobs * (2 * L * (M + N) * Kd * 8 + (1 + L) * 8 * (Mpad + Npad) * Kp)
+        if name in ("mpx_beaver_gemm", "mpx_beaver_gemm_batched"):
+            # D, E read once, A_l, B_l, C_l read and Z_l written per party
+            if name == "mpx_beaver_gemm":
+                L, batch, M, Kd, N = a[10], 1, a[11], a[12], a[13]
+            else:
+                L, batch, M, Kd, N = a[14], a[15], a[16], a[17], a[18]
+            return 8 * batch * ((1 + L) * (M * Kd + Kd * N) + 2 * L * M * N)
+        if name == "mpx_beaver_gemm_sim":
+            # X_l, A_l, Y_l, B_l, C_l read once and Z_l written, per party
+            L, batch, M, Kd, N = a[22], a[23], a[24], a[25], a[26]
+            return 8 * batch * L * (2 * M * Kd + 2 * Kd * N + 2 * M * N)
         if name == "mpx_mask_sub_bs":
             L, batch, n = a[7], a[8], a[9]
             return batch * n * 8 * (2 * L + 1)

@@ -292,6 +292,31 @@ int mpx_mask_limbs(uint8_t* S8, uint8_t* P8, const uint64_t* X, int64_t x_ps, in
                    int64_t Rpad, int64_t Kp, int p0, int add_p0, int width, int jobs, int64_t x_js,
                    int64_t t_js, void* stream);
 
+/* Both sides of a sim-mode Beaver product in ONE launch (basic.py:66-70):
+ * side A = mpx_mask_limbs(SA8, PA8, X, A; R = M, Rpad = Mpad, add_p0 = 0),
+ * side B = mpx_mask_limbs(SB8, PB8, Y^T, B^T; R = N, Rpad = Npad,
+ * add_p0 = 1), same L, K, Kp, p0, width and job count (job strides
+ * x_js / a_js / y_js / b_js). */
+int mpx_mask_limbs2(uint8_t* SA8, uint8_t* PA8, const uint64_t* X, int64_t x_ps, int64_t x_sr, int64_t x_sc,
+                    const uint64_t* A, int64_t a_ps, int64_t a_sr, int64_t a_sc, int64_t M, int64_t Mpad,
+                    uint8_t* SB8, uint8_t* PB8, const uint64_t* Y, int64_t y_ps, int64_t y_sr, int64_t y_sc,
+                    const uint64_t* B, int64_t b_ps, int64_t b_sr, int64_t b_sc, int64_t N, int64_t Npad, int L,
+                    int64_t K, int64_t Kp, int p0, int width, int jobs, int64_t x_js, int64_t a_js, int64_t y_js,
+                    int64_t b_js, void* stream);
+
+/* Sim sessions (all L local parties, 2 <= L <= 4): the Beaver opening and
+ * reconstruction of `batch` equal-shape products in one launch
+ * (basic.py:66-75): D = sum_l (X_l - A_l), E = sum_l (Y_l - B_l) formed in
+ * shared memory, Z_l = C_l + D @ (B_l + [l==p0] E) + A_l @ E mod 2^width.
+ * X / Y: logical M x K / K x N views at (party, row, col, job) element
+ * strides; A_l (M x K), B_l (K x N), C_l, Z_l (M x N) row-major at party
+ * strides sA / sB / sC / sZ and job strides bA / bB / bC / bZ. */
+int mpx_beaver_gemm_sim(uint64_t* Z, int64_t sZ, int64_t bZ, const uint64_t* C, int64_t sC, int64_t bC,
+                        const uint64_t* X, int64_t x_ps, int64_t x_sr, int64_t x_sc, int64_t x_js,
+                        const uint64_t* A, int64_t sA, int64_t bA, const uint64_t* Y, int64_t y_ps, int64_t y_sr,
+                        int64_t y_sc, int64_t y_js, const uint64_t* B, int64_t sB, int64_t bB, int L,
+                        int64_t batch, int64_t M, int64_t K, int64_t N, int p0, int width, void* stream);
+
 /* Beaver matrix-product reconstruction in one launch (basic.py:72-75):
  * Z_l = C_l + D @ (B_l + [l==p0] E) + A_l @ E mod 2^width for the L local
  * parties (batch strides sZ, sC, sA, sB). Z, C: M x N; D, A: M x K; E, B:

@@ -71,6 +71,8 @@ _SIGS = {
     "mpx_beaver_gemm": [_P, _L, _P, _L, _P, _P, _P, _L, _P, _L, _I, _L, _L, _L, _I, _I, _P],
     "mpx_beaver_gemm_batched": [_P, _L, _L, _P, _L, _L, _P, _P, _P, _L, _L, _P, _L, _L, _I, _L, _L, _L, _L, _I, _I,
                                 _P],
+    "mpx_beaver_gemm_sim": [_P, _L, _L, _P, _L, _L, _P, _L, _L, _L, _L, _P, _L, _L, _P, _L, _L, _L, _L, _P, _L, _L,
+                            _I, _L, _L, _L, _L, _I, _I, _P],
     "mpx_ring_colsum": [_P, _P, _I, _L, _L, _I, _P],
     "mpx_ring_pool_sum": [_P, _P, _L, _L, _L, _L, _L, _I, _P],
     "mpx_ring_pool_scatter": [_P, _P, _L, _L, _L, _L, _L, _I, _P],
@@ -78,6 +80,8 @@ _SIGS = {
     "mpx_gemm_limbs": [_P, _P, _P, _L, _L, _L, _L, _L, _L, _L, _L, _I, _I, _I, _P, _L, _P],
     "mpx_gemm_limbs_split": [_P, _P, _P, _P, _P, _L, _L, _L, _L, _L, _L, _L, _L, _I, _I, _P, _L, _I, _L, _P],
     "mpx_mask_limbs": [_P, _P, _P, _L, _L, _L, _P, _L, _L, _L, _I, _L, _L, _L, _L, _I, _I, _I, _I, _L, _L, _P],
+    "mpx_mask_limbs2": [_P, _P, _P, _L, _L, _L, _P, _L, _L, _L, _L, _L, _P, _P, _P, _L, _L, _L, _P, _L, _L, _L,
+                        _L, _L, _I, _L, _L, _I, _I, _I, _L, _L, _L, _L, _P],
     "mpx_philox_elems": [_P, _U, _U, _L, _L, _I, _P],
     "mpx_philox_bits": [_P, _U, _U, _L, _L, _P],
     "mpx_deal_share_arith": [_P, _L, _P, _U, _U, _L, _L, _I, _I, _I, _I, _P],

@@ -18,13 +18,13 @@
 // <= 128 registers per thread (a block occupies whole warps)
 constexpr int bg_min_blocks(int nt) { return 512 / (nt < 32 ? 32 : nt); }
 
-template <int BM, int BN, int TN, bool FULL>
+template <int BM, int BN, int TN, bool FULL, int KB = BG_BK>
 __device__ __forceinline__ void bg_tile_math(u64 (&acc)[4][TN], const u64 (*Ds)[BM + 1], const u64 (*As)[BM + 1],
                                              const u64 (*Bs)[BN], const u64 (*Es)[BN], int tx, int ty, int kn,
                                              bool addE) {
   constexpr int TX = BN / TN, TY = BM / 4;
 #pragma unroll
-  for (int kk = 0; kk < BG_BK; ++kk) {
+  for (int kk = 0; kk < KB; ++kk) {
     if (!FULL && kk >= kn) break;
     u64 d[4], a[4], b[TN], e[TN];
 #pragma unroll
@@ -260,4 +260,269 @@ extern "C" int mpx_beaver_gemm(uint64_t* Z, int64_t sZ, const uint64_t* C, int64
                                const uint64_t* E, const uint64_t* A, int64_t sA, const uint64_t* B, int64_t sB,
                                int L, int64_t M, int64_t K, int64_t N, int p0, int width, void* stream) {
   return mpx_beaver_gemm_batched(Z, sZ, 0, C, sC, 0, D, E, A, sA, 0, B, sB, 0, L, 1, M, K, N, p0, width, stream);
+}
+
+// ---------------------------------------------------------------------------
+// All parties local (sim sessions): the Beaver opening folded into the
+// product. D = sum_l (X_l - A_l) and E = sum_l (Y_l - B_l) (basic.py:66-70,
+// an opening is a sum over the party axis) are formed tile by tile in shared
+// memory next to every party's A_l / B_l tile, and the CTA's L party groups
+// (NT threads each) reconstruct Z_l = C_l + D @ (B_l + [l==p0] E) + A_l @ E
+// from them. One launch replaces mask(D) + mask(E) + reconstruct; D and E
+// never reach HBM, and the operands are read once for all parties. X / Y are
+// logical M x K / K x N share views at any (party, row, col) strides (the
+// transposed im2col / activation views are read in place); material A_l,
+// B_l is row-major. Shared-memory fills walk each source along its unit
+// stride.
+struct SimOperand {
+  const u64* p;
+  i64 ps, sr, sc, js;  // party, row, col, job strides (elements)
+};
+
+#define BS_BK 8  // k-depth of one pipeline stage
+
+// Raw operand tiles of one k-step: every party's X_l, A_l, Y_l, B_l.
+template <int L, int BM, int BN>
+constexpr int bs_stage_words() {
+  return 2 * L * BS_BK * (BM + 1) + 2 * L * BS_BK * BN;
+}
+
+template <int L, int BM, int BN, int TN>
+__global__ void __launch_bounds__(L*(BM / 4) * (BN / TN))
+    k_beaver_gemm_sim(u64* __restrict__ Z, i64 sZ, i64 bZ, const u64* __restrict__ C, i64 sC, i64 bC,
+                      const __grid_constant__ SimOperand X, const u64* __restrict__ A, i64 sA, i64 bA,
+                      const __grid_constant__ SimOperand Y, const u64* __restrict__ B, i64 sB, i64 bB, int M,
+                      int K, int N, int p0, u64 msk, int ksplit, int kchunk) {
+  constexpr int TX = BN / TN, TY = BM / 4, NT = TX * TY, NTL = L * NT;
+  constexpr int STAGE = bs_stage_words<L, BM, BN>();
+  typedef u64 RowM[BM + 1];
+  typedef u64 RowN[BN];
+  extern __shared__ u64 bs_sm[];
+  // stage s: Xs[L][BK] | As[L][BK] (RowM), Ys[L][BK] | Bs[L][BK] (RowN); then D[BK] (RowM), E[BK] (RowN)
+  auto Xs = [&](int st) { return reinterpret_cast<RowM*>(bs_sm + st * STAGE); };
+  auto As = [&](int st) { return reinterpret_cast<RowM*>(bs_sm + st * STAGE) + L * BS_BK; };
+  auto Ys = [&](int st) { return reinterpret_cast<RowN*>(bs_sm + st * STAGE + 2 * L * BS_BK * (BM + 1)); };
+  auto Bs = [&](int st) { return Ys(st) + L * BS_BK; };
+  RowM* Ds = reinterpret_cast<RowM*>(bs_sm + 2 * STAGE);
+  RowN* Es = reinterpret_cast<RowN*>(bs_sm + 2 * STAGE + BS_BK * (BM + 1));
+  const int bt = blockIdx.z / ksplit, ks = blockIdx.z % ksplit;
+  Z += bt * bZ;
+  C += bt * bC;
+  A += bt * bA;
+  B += bt * bB;
+  const u64* Xp = X.p + bt * X.js;
+  const u64* Yp = Y.p + bt * Y.js;
+  const int kbeg = ks * kchunk, kend = min(K, kbeg + kchunk);
+  const int row0 = blockIdx.y * BM, col0 = blockIdx.x * BN;
+  const int tid = threadIdx.x, l = tid / NT, t = tid % NT;
+  const int tx = t % TX, ty = t / TX;
+  const bool xrow = X.sc == 1, yrow = Y.sc == 1;  // k (resp. n) is X's (Y's) unit stride
+  u64 acc[4][TN];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0;
+
+  // cp.async of one k-step's raw tiles (zero-filled outside the matrices);
+  // each source is walked along its unit stride
+  auto issue = [&](int st, int k0) {
+    RowM* xs = Xs(st);
+    RowM* as = As(st);
+    RowN* ys = Ys(st);
+    RowN* bs = Bs(st);
+    for (int idx = tid; idx < BM * BS_BK; idx += NTL) {
+      const int r = idx / BS_BK, kk = idx % BS_BK, gr = row0 + r, gk = k0 + kk;
+      const bool ok = gr < M && gk < kend;
+      const u64* src = A + (ok ? (i64)gr * K + gk : 0);
+#pragma unroll
+      for (int q = 0; q < L; ++q) cp_async8(&as[q * BS_BK + kk][r], src + (ok ? q * sA : 0), ok);
+    }
+    for (int idx = tid; idx < BM * BS_BK; idx += NTL) {
+      const int r = xrow ? idx / BS_BK : idx % BM, kk = xrow ? idx % BS_BK : idx / BM;
+      const int gr = row0 + r, gk = k0 + kk;
+      const bool ok = gr < M && gk < kend;
+      const u64* src = Xp + (ok ? (i64)gr * X.sr + (i64)gk * X.sc : 0);
+#pragma unroll
+      for (int q = 0; q < L; ++q) cp_async8(&xs[q * BS_BK + kk][r], src + (ok ? q * X.ps : 0), ok);
+    }
+    for (int idx = tid; idx < BN * BS_BK; idx += NTL) {
+      const int kk = idx / BN, c = idx % BN, gk = k0 + kk, gc = col0 + c;
+      const bool ok = gk < kend && gc < N;
+      const u64* src = B + (ok ? (i64)gk * N + gc : 0);
+#pragma unroll
+      for (int q = 0; q < L; ++q) cp_async8(&bs[q * BS_BK + kk][c], src + (ok ? q * sB : 0), ok);
+    }
+    for (int idx = tid; idx < BN * BS_BK; idx += NTL) {
+      const int c = yrow ? idx % BN : idx / BS_BK, kk = yrow ? idx / BN : idx % BS_BK;
+      const int gk = k0 + kk, gc = col0 + c;
+      const bool ok = gk < kend && gc < N;
+      const u64* src = Yp + (ok ? (i64)gk * Y.sr + (i64)gc * Y.sc : 0);
+#pragma unroll
+      for (int q = 0; q < L; ++q) cp_async8(&ys[q * BS_BK + kk][c], src + (ok ? q * Y.ps : 0), ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const int nsteps = kend > kbeg ? (kend - kbeg + BS_BK - 1) / BS_BK : 0;
+  if (nsteps > 0) issue(0, kbeg);
+  for (int step = 0; step < nsteps; ++step) {
+    const int k0 = kbeg + step * BS_BK, st = step & 1;
+    if (step + 1 < nsteps) {
+      issue(st ^ 1, k0 + BS_BK);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    {  // the opening: D = sum_l X_l - A_l, E = sum_l Y_l - B_l of this k-step
+      const RowM* xs = Xs(st);
+      const RowM* as = As(st);
+      const RowN* ys = Ys(st);
+      const RowN* bs = Bs(st);
+      for (int idx = tid; idx < BM * BS_BK; idx += NTL) {
+        const int kk = idx / BM, r = idx % BM;
+        u64 d = 0;
+#pragma unroll
+        for (int q = 0; q < L; ++q) d += xs[q * BS_BK + kk][r] - as[q * BS_BK + kk][r];
+        Ds[kk][r] = d;
+      }
+      for (int idx = tid; idx < BN * BS_BK; idx += NTL) {
+        const int kk = idx / BN, c = idx % BN;
+        u64 e = 0;
+#pragma unroll
+        for (int q = 0; q < L; ++q) e += ys[q * BS_BK + kk][c] - bs[q * BS_BK + kk][c];
+        Es[kk][c] = e;
+      }
+    }
+    __syncthreads();
+    const int kn = kend - k0;
+    if (kn >= BS_BK)
+      bg_tile_math<BM, BN, TN, true, BS_BK>(acc, Ds, As(st) + l * BS_BK, Bs(st) + l * BS_BK, Es, tx, ty, kn,
+                                            l == p0);
+    else
+      bg_tile_math<BM, BN, TN, false, BS_BK>(acc, Ds, As(st) + l * BS_BK, Bs(st) + l * BS_BK, Es, tx, ty, kn,
+                                             l == p0);
+    __syncthreads();
+  }
+  u64* Zl = Z + (i64)l * sZ;
+  const u64* Cl = C + (i64)l * sC;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gr = row0 + ty + TY * i;
+    if (gr >= M) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int gc = col0 + tx + TX * j;
+      if (gc >= N) continue;
+      const i64 o = (i64)gr * N + gc;
+      if (ksplit > 1)
+        atomicAdd(reinterpret_cast<unsigned long long*>(Zl + o), (unsigned long long)acc[i][j]);
+      else
+        Zl[o] = (Cl[o] + acc[i][j]) & msk;
+    }
+  }
+}
+
+namespace {
+template <int L, int BM, int BN>
+constexpr int bs_smem_bytes() {
+  return 8 * (2 * bs_stage_words<L, BM, BN>() + BS_BK * (BM + 1 + BN));
+}
+
+template <int L, int BM, int BN, int TN>
+int launch_sim(i64 tiles_n, i64 tiles_m, i64 batch, i64 K, cudaStream_t s, uint64_t* Z, int64_t sZ, int64_t bZ,
+               const uint64_t* C, int64_t sC, int64_t bC, const SimOperand& X, const uint64_t* A, int64_t sA,
+               int64_t bA, const SimOperand& Y, const uint64_t* B, int64_t sB, int64_t bB, int M, int N, int p0,
+               int width) {
+  constexpr int smem = bs_smem_bytes<L, BM, BN>();
+  constexpr int nthr = L * (BM / 4) * (BN / TN);
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_beaver_gemm_sim<L, BM, BN, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem) != cudaSuccess)
+      return MPX_ERR_CUDA;
+    attr = true;
+  }
+  // resident CTAs per SM of this instantiation: split K to fill exactly one wave
+  static int occ = 0;
+  if (!occ && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_beaver_gemm_sim<L, BM, BN, TN>, nthr, smem) !=
+                   cudaSuccess ||
+               occ < 1))
+    occ = 1;
+  i64 per_sm = occ;
+  if (const char* ov = getenv("MPX_BS_PER_SM")) per_sm = max(1, atoi(ov));  // sweeps
+  const i64 tiles = tiles_n * tiles_m * batch, target = 148 * per_sm;
+  int ksplit = 1;
+  if (width == 64 && tiles < target && K >= 4 * BS_BK)
+    ksplit = (int)max((i64)1, min((target + tiles - 1) / tiles, (K + 2 * BS_BK - 1) / (2 * BS_BK)));
+  const i64 kchunk = ((K + ksplit - 1) / ksplit + BS_BK - 1) / BS_BK * BS_BK;
+  ksplit = (int)((K + kchunk - 1) / kchunk);
+  if (batch * ksplit > 65535 || tiles_m > 65535) return MPX_ERR_ARG;
+  if (ksplit > 1) {
+    for (i64 b = 0; b < batch; ++b)
+      if (cudaMemcpy2DAsync(Z + b * bZ, (size_t)sZ * 8, C + b * bC, (size_t)sC * 8, (size_t)((i64)M * N * 8),
+                            (size_t)L, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        return MPX_ERR_CUDA;
+  }
+  dim3 grid((unsigned)tiles_n, (unsigned)tiles_m, (unsigned)(batch * ksplit));
+  k_beaver_gemm_sim<L, BM, BN, TN><<<grid, nthr, smem, s>>>(Z, sZ, bZ, C, sC, bC, X, A, sA, bA, Y, B, sB, bB, M,
+                                                            (int)K, N, p0, ring_mask(width), ksplit, (int)kchunk);
+  return launch_status();
+}
+
+// tiles with at most 128 threads per party group
+const Cfg kSimCfgs[] = {{32, 32, 4}, {64, 32, 4}, {128, 16, 4}, {128, 20, 5}, {128, 10, 5}, {32, 20, 5}, {32, 10, 5}};
+constexpr int kNumSimCfgs = sizeof(kSimCfgs) / sizeof(kSimCfgs[0]);
+
+template <int L>
+int dispatch_sim(int best, i64 K, i64 batch, cudaStream_t s, uint64_t* Z, int64_t sZ, int64_t bZ, const uint64_t* C,
+                 int64_t sC, int64_t bC, const SimOperand& X, const uint64_t* A, int64_t sA, int64_t bA,
+                 const SimOperand& Y, const uint64_t* B, int64_t sB, int64_t bB, int M, int N, int p0, int width) {
+#define BS_CASE(I, BM_, BN_, TN_)                                                                              \
+  case I:                                                                                                     \
+    return launch_sim<L, BM_, BN_, TN_>((N + BN_ - 1) / BN_, (M + BM_ - 1) / BM_, batch, K, s, Z, sZ, bZ, C, sC, \
+                                        bC, X, A, sA, bA, Y, B, sB, bB, M, N, p0, width);
+  switch (best) {
+    BS_CASE(0, 32, 32, 4)
+    BS_CASE(1, 64, 32, 4)
+    BS_CASE(2, 128, 16, 4)
+    BS_CASE(3, 128, 20, 5)
+    BS_CASE(4, 128, 10, 5)
+    BS_CASE(5, 32, 20, 5)
+    default:
+      BS_CASE(6, 32, 10, 5)
+  }
+#undef BS_CASE
+}
+}  // namespace
+
+extern "C" int mpx_beaver_gemm_sim(uint64_t* Z, int64_t sZ, int64_t bZ, const uint64_t* C, int64_t sC, int64_t bC,
+                                   const uint64_t* X, int64_t x_ps, int64_t x_sr, int64_t x_sc, int64_t x_js,
+                                   const uint64_t* A, int64_t sA, int64_t bA, const uint64_t* Y, int64_t y_ps,
+                                   int64_t y_sr, int64_t y_sc, int64_t y_js, const uint64_t* B, int64_t sB,
+                                   int64_t bB, int L, int64_t batch, int64_t M, int64_t K, int64_t N, int p0,
+                                   int width, void* stream) {
+  CHECK_ARG(Z && C && X && A && Y && B && M >= 1 && K >= 1 && N >= 1 && width >= 1 && width <= 64);
+  CHECK_ARG(L >= 2 && L <= 4 && p0 < L && batch >= 1);
+  CHECK_ARG(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31) && M * K < (1ll << 40) && K * N < (1ll << 40));
+  int best = 0;
+  i64 best_cost = -1, best_area = 0;
+  for (int c = 0; c < kNumSimCfgs; ++c) {
+    const i64 bm = kSimCfgs[c].bm, bn = kSimCfgs[c].bn;
+    const i64 cost = ((M + bm - 1) / bm) * bm * ((N + bn - 1) / bn) * bn;
+    if (best_cost < 0 || cost < best_cost || (cost == best_cost && bm * bn > best_area)) {
+      best = c;
+      best_cost = cost;
+      best_area = bm * bn;
+    }
+  }
+  const SimOperand xo{X, x_ps, x_sr, x_sc, x_js}, yo{Y, y_ps, y_sr, y_sc, y_js};
+  cudaStream_t s = (cudaStream_t)stream;
+  if (L == 2)
+    return dispatch_sim<2>(best, K, batch, s, Z, sZ, bZ, C, sC, bC, xo, A, sA, bA, yo, B, sB, bB, (int)M, (int)N, p0,
+                           width);
+  if (L == 3)
+    return dispatch_sim<3>(best, K, batch, s, Z, sZ, bZ, C, sC, bC, xo, A, sA, bA, yo, B, sB, bB, (int)M, (int)N, p0,
+                           width);
+  return dispatch_sim<4>(best, K, batch, s, Z, sZ, bZ, C, sC, bC, xo, A, sA, bA, yo, B, sB, bB, (int)M, (int)N, p0,
+                         width);
 }

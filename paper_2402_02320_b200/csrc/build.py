@@ -39,22 +39,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
             return OUT
     objdir = os.path.join(REPO, "build", "mpx")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
+    objs, jobs = [], []
+    hdrs = [os.path.join(HERE, "common.cuh"), os.path.join(REPO, "include", "mpx.h")]
     for src in srcs:
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
-        hdrs = [os.path.join(HERE, "common.cuh"), os.path.join(REPO, "include", "mpx.h")]
         if not force and os.path.exists(obj) and \
                 os.path.getmtime(obj) >= max(os.path.getmtime(p) for p in [src] + hdrs):
             continue  # object up to date
-        cmd = [nvcc(), "-c", src, "-o", obj] + flags()
-        res = subprocess.run(cmd, capture_output=True, text=True)
-        if res.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")
+        jobs.append((src, obj, subprocess.Popen([nvcc(), "-c", src, "-o", obj] + flags(),
+                                                stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    for src, obj, proc in jobs:  # translation units compile concurrently
+        _, err = proc.communicate()
+        if proc.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src}:\n{err}")
         if verbose:
-            print(res.stderr, file=sys.stderr)
+            print(err, file=sys.stderr)
         with open(obj + ".ptxas.txt", "w") as fh:
-            fh.write(res.stderr)
+            fh.write(err)
     tmp = OUT + ".tmp"
     cmd = [nvcc(), "-shared", "-o", tmp] + objs + ["-gencode", "arch=compute_100a,code=sm_100a",
                                                    "-lcuda"]

@@ -977,19 +977,15 @@ __device__ __forceinline__ void ml_emit(uint8_t* base, i64 plane, const u64 (&w)
 // its material tile, which keeps the register footprint small enough for
 // three CTAs per SM.
 template <bool XK, bool TK>
-__global__ void __launch_bounds__(256, 3) k_mask_limbs(MaskLimbArgs a) {
-  __shared__ u64 tile[64][33];
-  const i64 r0 = (i64)blockIdx.x * 32, k0 = (i64)blockIdx.y * 64;
+__device__ __forceinline__ void ml_tile(MaskLimbArgs a, i64 r0, i64 k0, i64 jb, u64 (*tile)[33]) {
   const int t = threadIdx.x;
   const i64 plane = a.Rpad * a.Kp;
   const bool defer = a.add_p0 && a.p0 >= 0;
-  {  // job blockIdx.z: its operands and its shared + per-party plane sets
-    const i64 jb = blockIdx.z;
-    a.X += jb * a.x_js;
-    a.T += jb * a.t_js;
-    a.S8 += jb * 8 * plane;
-    a.P8 += jb * (i64)a.L * 8 * plane;
-  }
+  // job jb: its operands and its shared + per-party plane sets
+  a.X += jb * a.x_js;
+  a.T += jb * a.t_js;
+  a.S8 += jb * 8 * plane;
+  a.P8 += jb * (i64)a.L * 8 * plane;
   u64 s[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) s[c] = 0;
@@ -1013,6 +1009,88 @@ __global__ void __launch_bounds__(256, 3) k_mask_limbs(MaskLimbArgs a) {
     for (int c = 0; c < 8; ++c) v[c] = (v[c] + s[c]) & a.msk;
     ml_emit(a.P8 + (i64)a.p0 * 8 * plane, plane, v, r0, k0, a.Kp, t);
   }
+}
+
+template <bool XK, bool TK>
+__global__ void __launch_bounds__(256, 3) k_mask_limbs(MaskLimbArgs a) {
+  __shared__ u64 tile[64][33];
+  ml_tile<XK, TK>(a, (i64)blockIdx.x * 32, (i64)blockIdx.y * 64, blockIdx.z, tile);
+}
+
+// Both operand sides of a Beaver product in one launch: blocks [0, na) do
+// side a's tiles, the rest side b's (each side's source layouts picked at run
+// time; every block takes one branch, so its barriers stay uniform).
+__device__ __forceinline__ void ml_tile_rt(const MaskLimbArgs& a, i64 r0, i64 k0, i64 jb, u64 (*tile)[33]) {
+  const bool xk = a.x_sc == 1, tk = a.t_sc == 1;
+  if (xk && tk)
+    ml_tile<true, true>(a, r0, k0, jb, tile);
+  else if (xk)
+    ml_tile<true, false>(a, r0, k0, jb, tile);
+  else if (tk)
+    ml_tile<false, true>(a, r0, k0, jb, tile);
+  else
+    ml_tile<false, false>(a, r0, k0, jb, tile);
+}
+
+__global__ void __launch_bounds__(256, 3) k_mask_limbs2(const __grid_constant__ MaskLimbArgs a,
+                                                        const __grid_constant__ MaskLimbArgs b, int ax, int na,
+                                                        int bx) {
+  __shared__ u64 tile[64][33];
+  const int id = blockIdx.x;
+  if (id < na)
+    ml_tile_rt(a, (i64)(id % ax) * 32, (i64)(id / ax) * 64, blockIdx.y, tile);
+  else
+    ml_tile_rt(b, (i64)((id - na) % bx) * 32, (i64)((id - na) / bx) * 64, blockIdx.y, tile);
+}
+
+static void ml_pack(MaskLimbArgs& a, uint8_t* S8, uint8_t* P8, const uint64_t* X, int64_t x_ps, int64_t x_sr,
+                    int64_t x_sc, const uint64_t* T, int64_t t_ps, int64_t t_sr, int64_t t_sc, int L, int64_t R,
+                    int64_t K, int64_t Rpad, int64_t Kp, int p0, int add_p0, int width, int64_t x_js, int64_t t_js) {
+  a.X = X;
+  a.x_ps = x_ps;
+  a.x_sr = x_sr;
+  a.x_sc = x_sc;
+  a.T = T;
+  a.t_ps = t_ps;
+  a.t_sr = t_sr;
+  a.t_sc = t_sc;
+  a.S8 = S8;
+  a.P8 = P8;
+  a.R = R;
+  a.K = K;
+  a.Rpad = Rpad;
+  a.Kp = Kp;
+  a.msk = ring_mask(width);
+  a.L = L;
+  a.p0 = p0;
+  a.add_p0 = add_p0;
+  a.pad = 0;
+  a.x_js = x_js;
+  a.t_js = t_js;
+}
+
+// Side A (X_l, A_l; logical m x k) and side B (Y_l^T, B_l^T; logical r x k,
+// B_l + E at p0) of `jobs` products in ONE launch (sim mode).
+extern "C" int mpx_mask_limbs2(uint8_t* SA8, uint8_t* PA8, const uint64_t* X, int64_t x_ps, int64_t x_sr,
+                               int64_t x_sc, const uint64_t* A, int64_t a_ps, int64_t a_sr, int64_t a_sc,
+                               int64_t M, int64_t Mpad, uint8_t* SB8, uint8_t* PB8, const uint64_t* Y, int64_t y_ps,
+                               int64_t y_sr, int64_t y_sc, const uint64_t* B, int64_t b_ps, int64_t b_sr,
+                               int64_t b_sc, int64_t N, int64_t Npad, int L, int64_t K, int64_t Kp, int p0,
+                               int width, int jobs, int64_t x_js, int64_t a_js, int64_t y_js, int64_t b_js,
+                               void* stream) {
+  CHECK_ARG(SA8 && PA8 && X && A && SB8 && PB8 && Y && B && L >= 1 && M >= 1 && N >= 1 && K >= 1);
+  CHECK_ARG(width >= 1 && width <= 64 && jobs >= 1 && jobs <= 65535);
+  CHECK_ARG(Mpad >= M && Mpad % 32 == 0 && Npad >= N && Npad % 32 == 0 && Kp >= K && Kp % 32 == 0);
+  MaskLimbArgs a, b;
+  ml_pack(a, SA8, PA8, X, x_ps, x_sr, x_sc, A, a_ps, a_sr, a_sc, L, M, K, Mpad, Kp, p0, 0, width, x_js, a_js);
+  ml_pack(b, SB8, PB8, Y, y_ps, y_sr, y_sc, B, b_ps, b_sr, b_sc, L, N, K, Npad, Kp, p0, 1, width, y_js, b_js);
+  const i64 ky = (Kp + 63) / 64;
+  const i64 ax = Mpad / 32, bx = Npad / 32;
+  const i64 na = ax * ky, nb = bx * ky;
+  CHECK_ARG(na + nb < (1ll << 31));
+  k_mask_limbs2<<<dim3((unsigned)(na + nb), (unsigned)jobs), 256, 0, (cudaStream_t)stream>>>(a, b, (int)ax, (int)na,
+                                                                                            (int)bx);
+  return launch_status();
 }
 
 extern "C" int mpx_mask_limbs(uint8_t* S8, uint8_t* P8, const uint64_t* X, int64_t x_ps, int64_t x_sr, int64_t x_sc,

@@ -437,6 +437,16 @@ def beaver_gemm_batched(Z, sZ, bZ, C_ptr, sC, bC, D, E, A_ptr, sA, bA, B_ptr, sB
     return Z
 
 
+def beaver_gemm_sim(Z, sZ, bZ, C_ptr, sC, bC, x_ptr, x_ps, x_sr, x_sc, x_js, A_ptr, sA, bA,
+                    y_ptr, y_ps, y_sr, y_sc, y_js, B_ptr, sB, bB, L, batch, M, K, N, p0, width):
+    """Sim sessions: Beaver opening + reconstruction of ``batch`` products in one launch."""
+    if _dry(Z):
+        return Z
+    call("mpx_beaver_gemm_sim", ptr(Z), sZ, bZ, C_ptr, sC, bC, x_ptr, x_ps, x_sr, x_sc, x_js, A_ptr, sA, bA,
+         y_ptr, y_ps, y_sr, y_sc, y_js, B_ptr, sB, bB, L, batch, M, K, N, p0, width)
+    return Z
+
+
 def beaver_gemm(Z, sZ, C_ptr, sC, D, E, A_ptr, sA, B_ptr, sB, L, M, K, N, p0, width):
     """Z_l = C_l + D @ (B_l + [l==p0] E) + A_l @ E (one SIMT launch, all local parties)."""
     if _dry(Z):
@@ -485,6 +495,18 @@ def mask_limbs(S8, P8, x_ptr, x_ps, x_sr, x_sc, t_ptr, t_ps, t_sr, t_sc, L, R, K
     call("mpx_mask_limbs", ptr(S8), ptr(P8), x_ptr, x_ps, x_sr, x_sc, t_ptr, t_ps, t_sr, t_sc, L, R, Kd, Rpad, Kp,
          p0, int(add_p0), width, jobs, x_js, t_js)
     return S8
+
+
+def mask_limbs2(SA8, PA8, x_ptr, x_ps, x_sr, x_sc, a_ptr, a_ps, a_sr, a_sc, M, Mpad,
+                SB8, PB8, y_ptr, y_ps, y_sr, y_sc, b_ptr, b_ps, b_sr, b_sc, N, Npad, L, Kd, Kp, p0, width,
+                jobs=1, x_js=0, a_js=0, y_js=0, b_js=0):
+    """Both operand sides of sim-mode Beaver products (mask_limbs twice) in one launch."""
+    if _dry(SA8):
+        return SA8
+    call("mpx_mask_limbs2", ptr(SA8), ptr(PA8), x_ptr, x_ps, x_sr, x_sc, a_ptr, a_ps, a_sr, a_sc, M, Mpad,
+         ptr(SB8), ptr(PB8), y_ptr, y_ps, y_sr, y_sc, b_ptr, b_ps, b_sr, b_sc, N, Npad, L, Kd, Kp, p0, width,
+         jobs, x_js, a_js, y_js, b_js)
+    return SA8
 
 
 def gemm_tc(C, A, B, batch, M, K, N, sA, sB, sC, accumulate, width):

@@ -75,9 +75,9 @@ def batch_matmul(session, pairs) -> list[AShare]:
     for g in groups:
         x0, y0 = pairs[g[0]]
         w, (m, k), r = x0.width, x0.shape, y0.shape[1]
-        if _fused_tc(session, m, k, r, w):
-            # sim mode: mask + open + limb split fused below (one round, same
-            # logical payload as the reference's D, E openings)
+        if _fused_tc(session, m, k, r, w) or _fused_simt(session, m, k, r, w):
+            # sim mode: mask + open + limb split (or SIMT reconstruction) fused
+            # below (one round, same logical payload as the reference's D, E openings)
             fused_payload += len(g) * (arith_payload(w, m * k) + arith_payload(w, k * r))
             continue
         D = session.alloc((len(g), m * k))
@@ -140,6 +140,13 @@ def _finish_group(session, pairs, trip, g, Zg, opened, pos, out, L) -> int:
             if len(g) == 1:
                 A, B, C = trip[i]
                 _beaver_matmul_fused_tc(session, Zg[j], x.values, y.values, A, B, C, L, m, k, r, w)
+            session.metrics.count(matmul_count=1, matmul_macs=m * k * r)
+            out[i] = AShare(Zg[j], w, x.frac + y.frac, session.parties)
+        return pos
+    if _fused_simt(session, m, k, r, w):
+        _beaver_matmul_fused_simt(session, Zg, [pairs[i] for i in g], [trip[i] for i in g], L, m, k, r, w)
+        for j, i in enumerate(g):
+            x, y = pairs[i]
             session.metrics.count(matmul_count=1, matmul_macs=m * k * r)
             out[i] = AShare(Zg[j], w, x.frac + y.frac, session.parties)
         return pos
@@ -265,6 +272,29 @@ def _fused_tc(session, m, k, r, w) -> bool:
     return session.fused and 2 * K.kpad(k) <= 1.25 * K.kpad(2 * k) and _use_tc(m, k, r, w)
 
 
+def _fused_simt(session, m, k, r, w) -> bool:
+    """Sim sessions with 2..4 local parties run the SIMT-sized products (thin
+    outputs, long weight-gradient reductions) as one fused opening +
+    reconstruction launch (D, E never materialised)."""
+    return session.fused and 2 <= session.L <= 4 and not _use_tc(m, k, r, w)
+
+
+def _beaver_matmul_fused_simt(session, Zg, pairs, trips, L, m, k, r, w):
+    """Z_l = C_l + D @ (B_l + [l==p0] E) + A_l @ E for a group of equal-shape
+    products (basic.py:66-75) with D = sum_l X_l - A_l, E = sum_l Y_l - B_l
+    formed tile by tile inside the kernel; operand views read in place."""
+    X0, Y0 = pairs[0][0].values, pairs[0][1].values
+    A0, B0, C0 = trips[0]
+    step = lambda ts: (_uniform([_ptr(t) for t in ts]) or 0) // 8  # noqa: E731
+    x_js, y_js = step([p[0].values for p in pairs]), step([p[1].values for p in pairs])
+    xps, xsr, xsc = _strides3(X0)
+    yps, ysr, ysc = _strides3(Y0)
+    K.beaver_gemm_sim(Zg, m * r, L * m * r, C0.data_ptr(), C0.stride(0), _bstride(trips, range(len(trips)), 2),
+                      _ptr(X0), xps, xsr, xsc, x_js, A0.data_ptr(), A0.stride(0),
+                      _bstride(trips, range(len(trips)), 0), _ptr(Y0), yps, ysr, ysc, y_js, B0.data_ptr(),
+                      B0.stride(0), _bstride(trips, range(len(trips)), 1), L, len(pairs), m, k, r, session.p0, w)
+
+
 def _strides3(v):
     """(party, row, col) element strides of an [L, rows, cols] view."""
     if v.dim() != 3:
@@ -287,11 +317,9 @@ def _beaver_matmul_fused_tc(session, Z, X, Y, A, B, C, L, m, k, r, w):
     xps, xsr, xsc = _strides3(X)
     yps, ysk, ysn = _strides3(Y)
     # A side: logical (m, k); material A_l row-major m x k
-    K.mask_limbs(SA, PA, _ptr(X), xps, xsr, xsc, A.data_ptr(), A.stride(0), k, 1, L, m, k, Mp, Kh, session.p0,
-                 False, w)
-    # B side: logical (r, k) = Y^T; material B_l row-major k x r
-    K.mask_limbs(SB, PB, _ptr(Y), yps, ysn, ysk, B.data_ptr(), B.stride(0), 1, r, L, r, k, Np, Kh, session.p0,
-                 True, w)
+    # B side: logical (r, k) = Y^T; material B_l row-major k x r (one launch for both sides)
+    K.mask_limbs2(SA, PA, _ptr(X), xps, xsr, xsc, A.data_ptr(), A.stride(0), k, 1, m, Mp,
+                  SB, PB, _ptr(Y), yps, ysn, ysk, B.data_ptr(), B.stride(0), 1, r, r, Np, L, k, Kh, session.p0, w)
     K.gemm_limbs_split(Z, PA, SA, PB, SB, L, m, r, Mp, Np, Kh, r, m * r, w, C.data_ptr(), C.stride(0))
 
 
@@ -314,10 +342,9 @@ def _beaver_matmul_fused_tc_group(session, Zg, pairs, trips, L, m, k, r, w):
     a_js, b_js, c_js = step([t[0] for t in trips]), step([t[1] for t in trips]), step([t[2] for t in trips])
     xps, xsr, xsc = _strides3(X0)
     yps, ysk, ysn = _strides3(Y0)
-    K.mask_limbs(SA, PA, _ptr(X0), xps, xsr, xsc, A0.data_ptr(), A0.stride(0), k, 1, L, m, k, Mp, Kh, session.p0,
-                 False, w, jobs=J, x_js=x_js, t_js=a_js)
-    K.mask_limbs(SB, PB, _ptr(Y0), yps, ysn, ysk, B0.data_ptr(), B0.stride(0), 1, r, L, r, k, Np, Kh, session.p0,
-                 True, w, jobs=J, x_js=y_js, t_js=b_js)
+    K.mask_limbs2(SA, PA, _ptr(X0), xps, xsr, xsc, A0.data_ptr(), A0.stride(0), k, 1, m, Mp,
+                  SB, PB, _ptr(Y0), yps, ysn, ysk, B0.data_ptr(), B0.stride(0), 1, r, r, Np, L, k, Kh, session.p0, w,
+                  jobs=J, x_js=x_js, a_js=a_js, y_js=y_js, b_js=b_js)
     K.gemm_limbs_split(Zg, PA, SA, PB, SB, J * L, m, r, Mp, Np, Kh, r, m * r, w, C0.data_ptr(), C0.stride(0),
                        zl=L, s_cin_j=c_js)
 

@@ -251,3 +251,70 @@ def test_mask_limbs_split_gemm_matches_numpy(K, L, p0, jobs, m, k, r, xt, yt):
                 Bl = B[j, l] + (E if l == p0 else np.uint64(0))
                 want = C[j, l] + _mm(D, Bl) + _mm(A[j, l], E)
                 assert np.array_equal(got[j, l], want), (j, l)
+
+
+@pytest.mark.parametrize("L,p0,jobs,m,k,r,xt,yt", [
+    (3, 0, 1, 300, 130, 70, False, False),
+    (2, 1, 2, 128, 64, 96, False, True),
+    (3, 2, 1, 200, 25, 20, True, False),
+])
+def test_mask_limbs2_matches_two_launches(K, L, p0, jobs, m, k, r, xt, yt):
+    """Both operand sides in one launch write exactly the planes of the two
+    per-side mask_limbs launches."""
+    rng = np.random.default_rng(m * 3 + k + r + jobs)
+    X, Y = _rand(rng, (jobs, L, m, k), 64), _rand(rng, (jobs, L, k, r), 64)
+    A, B = _rand(rng, (jobs, L, m, k), 64), _rand(rng, (jobs, L, k, r), 64)
+    Xd = _dev(np.ascontiguousarray(X.transpose(0, 1, 3, 2))).transpose(2, 3) if xt else _dev(X)
+    Yd = _dev(np.ascontiguousarray(Y.transpose(0, 1, 3, 2))).transpose(2, 3) if yt else _dev(Y)
+    Ad, Bd = _dev(A), _dev(B)
+    Mp, Np, Kh = K._rup(m, 128), K._rup(r, 32), K.kpad(k)
+    bufs = [torch.full(s, 7, dtype=torch.uint8, device="cuda") for s in
+            [(jobs, 8, Mp, Kh), (jobs, L, 8, Mp, Kh), (jobs, 8, Np, Kh), (jobs, L, 8, Np, Kh)] * 2]
+    x0, y0 = Xd[0], Yd[0]
+    K.mask_limbs(bufs[0], bufs[1], x0.data_ptr(), x0.stride(0), x0.stride(1), x0.stride(2), Ad.data_ptr(), m * k, k,
+                 1, L, m, k, Mp, Kh, p0, False, 64, jobs=jobs, x_js=Xd.stride(0), t_js=L * m * k)
+    K.mask_limbs(bufs[2], bufs[3], y0.data_ptr(), y0.stride(0), y0.stride(2), y0.stride(1), Bd.data_ptr(), k * r, 1,
+                 r, L, r, k, Np, Kh, p0, True, 64, jobs=jobs, x_js=Yd.stride(0), t_js=L * k * r)
+    K.mask_limbs2(bufs[4], bufs[5], x0.data_ptr(), x0.stride(0), x0.stride(1), x0.stride(2), Ad.data_ptr(), m * k, k,
+                  1, m, Mp, bufs[6], bufs[7], y0.data_ptr(), y0.stride(0), y0.stride(2), y0.stride(1), Bd.data_ptr(),
+                  k * r, 1, r, r, Np, L, k, Kh, p0, 64, jobs=jobs, x_js=Xd.stride(0), a_js=L * m * k,
+                  y_js=Yd.stride(0), b_js=L * k * r)
+    for i in range(4):
+        assert torch.equal(bufs[i], bufs[4 + i]), i
+
+
+@pytest.mark.parametrize("L,p0,jobs,m,k,r,xt,yt,w", [
+    (3, 0, 1, 25, 5000, 20, True, False, 64),    # conv weight gradient: tiny output, long K, X^T in place
+    (3, 1, 1, 128, 500, 10, False, False, 64),   # thin FC output (128x10 tiles)
+    (2, 0, 2, 500, 128, 10, True, False, 64),    # batched jobs
+    (4, 3, 1, 128, 10, 500, False, True, 64),    # short K, transposed Y view, p0 = last party
+    (3, 0, 1, 70, 33, 40, False, False, 32),     # narrow ring: no split
+    (2, 1, 3, 20, 3000, 10, True, True, 64),
+])
+def test_beaver_gemm_sim_matches_numpy(K, L, p0, jobs, m, k, r, xt, yt, w):
+    """Sim-mode Beaver opening + reconstruction in one launch: Z_l = C_l +
+    D @ (B_l + [l==p0] E) + A_l @ E, D = sum_l X_l - A_l, E = sum_l Y_l - B_l
+    (basic.py:66-75), mod 2^w."""
+    rng = np.random.default_rng(m * 5 + k + r + jobs + w)
+    X, Y = _rand(rng, (jobs, L, m, k), w), _rand(rng, (jobs, L, k, r), w)
+    A, B, C = _rand(rng, (jobs, L, m, k), w), _rand(rng, (jobs, L, k, r), w), _rand(rng, (jobs, L, m, r), w)
+    Xd = _dev(np.ascontiguousarray(X.transpose(0, 1, 3, 2))).transpose(2, 3) if xt else _dev(X)
+    Yd = _dev(np.ascontiguousarray(Y.transpose(0, 1, 3, 2))).transpose(2, 3) if yt else _dev(Y)
+    Ad, Bd, Cd = _dev(A), _dev(B), _dev(C)
+    Z = torch.empty((jobs, L, m, r), dtype=torch.int64, device="cuda")
+    x0, y0 = Xd[0], Yd[0]
+    K.beaver_gemm_sim(Z, m * r, L * m * r, Cd.data_ptr(), m * r, L * m * r,
+                      x0.data_ptr(), x0.stride(0), x0.stride(1), x0.stride(2), Xd.stride(0),
+                      Ad.data_ptr(), m * k, L * m * k,
+                      y0.data_ptr(), y0.stride(0), y0.stride(1), y0.stride(2), Yd.stride(0),
+                      Bd.data_ptr(), k * r, L * k * r, L, jobs, m, k, r, p0, w)
+    got = _host(Z)
+    msk = np.uint64((1 << w) - 1) if w < 64 else np.uint64(0xFFFFFFFFFFFFFFFF)
+    with np.errstate(over="ignore"):
+        for j in range(jobs):
+            D = (X[j] - A[j]).sum(0, dtype=np.uint64)
+            E = (Y[j] - B[j]).sum(0, dtype=np.uint64)
+            for l in range(L):
+                Bl = B[j, l] + (E if l == p0 else np.uint64(0))
+                want = (C[j, l] + _mm(D, Bl) + _mm(A[j, l], E)) & msk
+                assert np.array_equal(got[j, l], want), (j, l)

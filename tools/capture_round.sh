@@ -11,7 +11,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/
     > $OUT/ncu_bench_launches.log 2>&1
 python tools/bench_train.py --graph --steps 2 > $OUT/bench_train.json 2>&1 || exit 1
 # full sections for the step's tcgen05 GEMMs and fused Beaver-operand kernels
-ncu --set full --clock-control none --import-source on -k regex:"k_gemm_limbs_tc_pers|k_mask_limbs" \
+ncu --set full --clock-control none --import-source on -k regex:"k_gemm_limbs_tc_pers|k_mask_limbs|k_beaver_gemm_sim" \
     --launch-skip 30 --launch-count 20 -o $OUT/lenet_gemm_full python tools/bench_train.py --graph --steps 1 \
     > $OUT/ncu_lenet_gemm_full.log 2>&1
 ncu -i $OUT/lenet_gemm_full.ncu-rep --page details --csv > $OUT/lenet_gemm_full_details.csv 2>/dev/null
