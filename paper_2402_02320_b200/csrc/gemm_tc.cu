@@ -961,6 +961,29 @@ __device__ __forceinline__ void ml_load8(u64 (&v)[8], const u64* __restrict__ sr
   }
 }
 
+#ifndef MPX_ML_PREFETCH
+#define MPX_ML_PREFETCH 1
+#endif
+
+// Pull this thread's part of a source tile towards L2 (ml_load8's addresses).
+template <bool KFAST>
+__device__ __forceinline__ void ml_prefetch(const u64* __restrict__ src, i64 sr, i64 sc, i64 r0, i64 k0, i64 R,
+                                            i64 K, int t) {
+  if constexpr (KFAST) {
+    const i64 r = r0 + (t >> 3), k = k0 + (t & 7) * 8;
+    if (r < R && k < K) {
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(src + r * sr + k));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(src + r * sr + min(k + 7, K - 1)));
+    }
+  } else {
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      const i64 r = r0 + (t & 31), k = k0 + (t >> 5) + 8 * p;
+      if (r < R && k < K) asm volatile("prefetch.global.L2 [%0];" ::"l"(src + r * sr + k * sc));
+    }
+  }
+}
+
 __device__ __forceinline__ void ml_emit(uint8_t* base, i64 plane, const u64 (&w)[8], i64 r0, i64 k0, i64 Kp,
                                         int t) {
   const int rr = t >> 3, g = t & 7;
@@ -986,6 +1009,11 @@ __device__ __forceinline__ void ml_tile(MaskLimbArgs a, i64 r0, i64 k0, i64 jb, 
   a.T += jb * a.t_js;
   a.S8 += jb * 8 * plane;
   a.P8 += jb * (i64)a.L * 8 * plane;
+  if (MPX_ML_PREFETCH)  // every party's source tiles in flight at once (the loop below is per-party serial)
+    for (int l = 0; l < a.L; ++l) {
+      ml_prefetch<XK>(a.X + (i64)l * a.x_ps, a.x_sr, a.x_sc, r0, k0, a.R, a.K, t);
+      ml_prefetch<TK>(a.T + (i64)l * a.t_ps, a.t_sr, a.t_sc, r0, k0, a.R, a.K, t);
+    }
   u64 s[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) s[c] = 0;

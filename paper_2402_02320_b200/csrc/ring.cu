@@ -658,36 +658,6 @@ __global__ void k_im2col(u64* __restrict__ out, const u64* __restrict__ x, IT B,
   }
 }
 
-// Narrow rows (C*K*K < 64): a thread owns one output row, decomposes the row
-// index once and walks (c, kh, kw) with counters — the element-per-thread
-// kernel spent its time in six runtime integer divisions per element.
-__global__ void k_im2col_rows(u64* __restrict__ out, const u64* __restrict__ x, int L, int B, int C, int H, int W,
-                              int K, int S, int P, int OH, int OW) {
-  const int cols = C * K * K;
-  const i64 rows = (i64)B * OH * OW;
-  const i64 nrow = (i64)L * rows;
-  for (i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x; t < nrow; t += (i64)gridDim.x * blockDim.x) {
-    const i64 l = t / rows, row = t - l * rows;
-    const int ow = (int)(row % OW);
-    const i64 boh = row / OW;
-    const int oh = (int)(boh % OH), b = (int)(boh / OH);
-    const u64* img = x + ((i64)l * B + b) * C * H * W;
-    const int h0 = oh * S - P, w0 = ow * S - P;
-    u64* o = out + t * cols;
-    int col = 0;
-    for (int c = 0; c < C; ++c)
-      for (int kh = 0; kh < K; ++kh) {
-        const int h = h0 + kh;
-        const bool hin = h >= 0 && h < H;
-        const u64* rowp = img + ((i64)c * H + h) * W;
-        for (int kw = 0; kw < K; ++kw, ++col) {
-          const int w = w0 + kw;
-          o[col] = (hin && w >= 0 && w < W) ? rowp[w] : 0ull;
-        }
-      }
-  }
-}
-
 template <typename IT, bool S1>
 __global__ void k_col2im(u64* __restrict__ dx, const u64* __restrict__ colsb, IT B, IT C, IT H, IT W, IT K,
                          IT S, IT P, IT OH, IT OW, IT total, u64 msk) {
@@ -763,6 +733,52 @@ __global__ void __launch_bounds__(256) k_im2col_tab(u64* __restrict__ out, const
   }
 }
 
+// Narrow rows (C*K*K < 64, e.g. LeNet conv1's 25 columns): a block owns 256
+// consecutive output rows = one contiguous run of 256*cols output words and
+// stores it element-per-thread (coalesced); the rows' image offsets and the
+// columns' (kh, kw) offsets are decoded once into shared memory, so the
+// element loop costs one 32-bit division by cols.
+__global__ void __launch_bounds__(256) k_im2col_narrow(u64* __restrict__ out, const u64* __restrict__ x, int L,
+                                                       int B, int C, int H, int W, int K, int S, int P, int OH,
+                                                       int OW) {
+  extern __shared__ i64 nsm[];  // rbase[256] | rhw[256] (int) | tab[cols] | tabk[cols] (int)
+  i64* rbase = nsm;
+  int* rhw = reinterpret_cast<int*>(nsm + 256);
+  int* tab = rhw + 256;
+  const int cols = C * K * K;
+  int* tabk = tab + cols;
+  for (int col = threadIdx.x; col < cols; col += blockDim.x) {
+    const int c = col / (K * K), r = col - c * K * K, kh = r / K, kw = r - kh * K;
+    tab[col] = (c * H + kh) * W + kw;
+    tabk[col] = (kh << 16) | kw;
+  }
+  const i64 rows = (i64)B * OH * OW, nrow = (i64)L * rows;
+  for (i64 r0 = (i64)blockIdx.x * 256; r0 < nrow; r0 += (i64)gridDim.x * 256) {
+    __syncthreads();  // previous rows' tables consumed
+    const i64 lr = r0 + threadIdx.x;
+    if (lr < nrow) {
+      const i64 l = lr / rows, row = lr - l * rows;
+      const int ow = (int)(row % OW);
+      const i64 t = row / OW;
+      const int oh = (int)(t % OH);
+      const i64 b = t / OH;
+      const int h0 = oh * S - P, w0 = ow * S - P;
+      rbase[threadIdx.x] = (l * B + b) * (i64)C * H * W + (i64)h0 * W + w0;
+      rhw[threadIdx.x] = (int)(((unsigned)(h0 + 0x8000) << 16) | (unsigned)(w0 + 0x8000));
+    }
+    __syncthreads();
+    const int nel = (int)min((i64)256, nrow - r0) * cols;
+    u64* o = out + r0 * cols;
+    for (int idx = threadIdx.x; idx < nel; idx += blockDim.x) {
+      const int rl = idx / cols, col = idx - rl * cols;
+      const unsigned hw = (unsigned)rhw[rl];
+      const int kk = tabk[col];
+      const int h = (int)(hw >> 16) - 0x8000 + (kk >> 16), w = (int)(hw & 0xFFFF) - 0x8000 + (kk & 0xFFFF);
+      o[idx] = (h >= 0 && h < H && w >= 0 && w < W) ? x[rbase[rl] + tab[col]] : 0ull;
+    }
+  }
+}
+
 extern "C" int mpx_im2col(uint64_t* out, const uint64_t* x, int L, int64_t B, int C, int H, int W, int K,
                           int stride, int pad, void* stream) {
   CHECK_ARG(out && x && L >= 1 && B >= 1 && C >= 1 && H >= 1 && W >= 1 && K >= 1 && stride >= 1 && pad >= 0);
@@ -779,8 +795,10 @@ extern "C" int mpx_im2col(uint64_t* out, const uint64_t* x, int L, int64_t B, in
                                                                                    stride, pad, OH, OW);
     return launch_status();
   }
-  if (cols < 64 && (i64)L * B * C * H * W < (1ll << 40)) {
-    k_im2col_rows<<<grid_for((i64)L * B * OH * OW, 128), 128, 0, (cudaStream_t)stream>>>(
+  if (cols < 64 && H < 0x4000 && W < 0x4000 && pad < 0x4000) {
+    const i64 nrow = (i64)L * B * OH * OW;
+    const i64 blocks = min((nrow + 255) / 256, (i64)148 * 8);
+    k_im2col_narrow<<<(unsigned)blocks, 256, 256 * 12 + (size_t)cols * 8, (cudaStream_t)stream>>>(
         out, x, L, (int)B, C, H, W, K, stride, pad, OH, OW);
     return launch_status();
   }

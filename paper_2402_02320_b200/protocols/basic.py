@@ -253,14 +253,24 @@ def session_dry(v) -> bool:
 TC_MAX_WASTE = 2.2     # padded / useful MACs above which the SIMT kernel wins (conv1 fwd: 2.05 on TC)
 
 
-def _use_tc(m, k, r, w=64) -> bool:
+# sim sessions (2..4 local parties) compare the tcgen05 path (mask+limb pass +
+# GEMM) with the fused SIMT opening+reconstruction kernel, not with mask
+# kernels + SIMT GEMM: LeNet conv1 forward (waste 2.05) is 116 vs 148 us on SIMT
+SIM_TC_MAX_WASTE = 2.0
+
+
+def _sim_waste(session) -> float:
+    return SIM_TC_MAX_WASTE if 2 <= session.L <= 4 else TC_MAX_WASTE
+
+
+def _use_tc(m, k, r, w=64, max_waste=None) -> bool:
     """tcgen05 limb GEMM when the padded work (128-row M tiles, 32/64-wide N
     tiles, 32/64/128-byte k-blocks) stays within TC_MAX_WASTE of the useful
     MACs; thin or tiny products go to the SIMT kernel."""
     if m < 96 or r < 16 or m * 2 * k * r < K.TC_MIN_MACS or (w != 64 and 2 * k > K.TC_MAX_K):
         return False
     waste = (K._rup(m, 128) / m) * (K.npad_tiles(r) / r) * (K.kpad(2 * k) / (2 * k))
-    return waste <= TC_MAX_WASTE
+    return waste <= (TC_MAX_WASTE if max_waste is None else max_waste)
 
 
 def _fused_tc(session, m, k, r, w) -> bool:
@@ -269,14 +279,14 @@ def _fused_tc(session, m, k, r, w) -> bool:
     128-byte k-blocks) costs much more MMA work than padding the concatenated
     2K (e.g. K = 10: 2 x 32 vs 32); up to 25% more MMA work is cheaper than
     the separate mask and limb passes (VGG K = 576: 2 x 640 vs 1152)."""
-    return session.fused and 2 * K.kpad(k) <= 1.25 * K.kpad(2 * k) and _use_tc(m, k, r, w)
+    return session.fused and 2 * K.kpad(k) <= 1.25 * K.kpad(2 * k) and _use_tc(m, k, r, w, _sim_waste(session))
 
 
 def _fused_simt(session, m, k, r, w) -> bool:
     """Sim sessions with 2..4 local parties run the SIMT-sized products (thin
     outputs, long weight-gradient reductions) as one fused opening +
     reconstruction launch (D, E never materialised)."""
-    return session.fused and 2 <= session.L <= 4 and not _use_tc(m, k, r, w)
+    return session.fused and 2 <= session.L <= 4 and not _use_tc(m, k, r, w, SIM_TC_MAX_WASTE)
 
 
 def _beaver_matmul_fused_simt(session, Zg, pairs, trips, L, m, k, r, w):

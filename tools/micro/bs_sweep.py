@@ -8,7 +8,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from paper_2402_02320_b200 import kernels as K  # noqa: E402
 
-SHAPES = [(25, 73728, 20, True, False), (128, 500, 10, False, False), (500, 128, 10, True, False),
+SHAPES = [(73728, 25, 20, False, False), (25, 73728, 20, True, False), (128, 500, 10, False, False), (500, 128, 10, True, False),
           (128, 10, 500, False, True), (27, 131072, 64, True, False)]
 
 
