@@ -13,6 +13,8 @@
 // [e*per, e*per + per) — the reference's flattened C order.
 #include "common.cuh"
 
+#include <stdlib.h>
+
 // local party counts with fused instantiations: every n <= 4, and n = 8
 #define FUSED_L_OK(L) (((L) >= 1 && (L) <= 4) || (L) == 8)
 
@@ -47,6 +49,11 @@ struct Tape {
 #define MPX_MINB4 MPX_CMP_MINB
 #endif
 #define MPX_MINB_L(L, B2) ((L) <= 2 ? (B2) : (L) == 3 ? MPX_MINB3 : (L) == 4 ? MPX_MINB4 : 1)
+// n = 8 split over two lanes (4 parties per lane): 128-register cap
+#ifndef MPX_MINB_SPLIT
+#define MPX_MINB_SPLIT 4
+#endif
+#define MPX_MINB_LG(L, G, B2) ((G) > 1 && (L) >= 4 ? MPX_MINB_SPLIT : MPX_MINB_L(L, B2))
 
 #ifndef MPX_LOG_MINB
 #define MPX_LOG_MINB 6  // 80 regs, 6 blocks: 8.95 vs 9.34 ms at 2^24
@@ -58,40 +65,73 @@ struct Tape {
 
 __device__ __forceinline__ void pf_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
+// Party split: with G > 1 an element's n = L*G local parties are held by G
+// adjacent lanes, L each (lane g of the group holds parties g*L .. g*L+L-1),
+// so n = 8 needs 4 shares per value in registers instead of 8. Every opening
+// (a sum or XOR over the parties) is finished with a butterfly over the
+// group; both lanes of a group run the same element, so the same control
+// path. G = 1 is the one-lane-per-element layout.
+template <int L, int G>
+__device__ __forceinline__ int pbase() {
+  return G == 1 ? 0 : (int)(threadIdx.x & (G - 1)) * L;
+}
+#define PI(l) ((l) + pbase<L, G>())
+
+template <int G>
+__device__ __forceinline__ unsigned gmask() {
+  return G == 1 ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(unsigned)(G - 1)));
+}
+template <int G>
+__device__ __forceinline__ u64 gsum(u64 v) {
+#pragma unroll
+  for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(gmask<G>(), v, o);
+  return v;
+}
+template <int G>
+__device__ __forceinline__ u64 gxor(u64 v) {
+#pragma unroll
+  for (int o = 1; o < G; o <<= 1) v ^= __shfl_xor_sync(gmask<G>(), v, o);
+  return v;
+}
+
+// element loop with G lanes per element
+#define GRID_STRIDE_G(i, n)                                                                   \
+  for (i64 i = ((i64)blockIdx.x * blockDim.x + threadIdx.x) / G; i < (n); i += (i64)gridDim.x * blockDim.x / G)
+
 // Pull take `t`'s slice for element e towards L2 (no registers held).
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ void prefetch_take(const MatRef& t, i64 e) {
   if (t.kind == 0) {
 #pragma unroll
     for (int l = 0; l < L; ++l) {
-      pf_l2(t.p0 + l * t.ps0 + e);
-      pf_l2(t.p1 + l * t.ps1 + e);
-      pf_l2(t.p2 + l * t.ps2 + e);
+      pf_l2(t.p0 + PI(l) * t.ps0 + e);
+      pf_l2(t.p1 + PI(l) * t.ps1 + e);
+      pf_l2(t.p2 + PI(l) * t.ps2 + e);
     }
   } else if (t.kind == 1) {
     const i64 w = (t.off + e * (i64)t.per0) >> 6;
 #pragma unroll
     for (int l = 0; l < L; ++l) {
-      pf_l2(t.p0 + l * t.ps0 + w);
-      pf_l2(t.p1 + l * t.ps1 + w);
-      pf_l2(t.p2 + l * t.ps2 + w);
+      pf_l2(t.p0 + PI(l) * t.ps0 + w);
+      pf_l2(t.p1 + PI(l) * t.ps1 + w);
+      pf_l2(t.p2 + PI(l) * t.ps2 + w);
     }
   } else {
 #pragma unroll
     for (int l = 0; l < L; ++l) {
-      const u64* row = t.p0 + l * t.ps0 + e * (i64)t.per0;
+      const u64* row = t.p0 + PI(l) * t.ps0 + e * (i64)t.per0;
       for (int q = 0; q < t.per0; q += 16) pf_l2(row + q);
-      if (t.p1) pf_l2(t.p1 + l * t.ps1 + ((t.off + e * (i64)t.per1) >> 6));
+      if (t.p1) pf_l2(t.p1 + PI(l) * t.ps1 + ((t.off + e * (i64)t.per1) >> 6));
     }
   }
 }
 
 // Consume the next tape entry, prefetching the one MPX_PREFETCH_DIST ahead.
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ const MatRef& next_take(const Tape& tape, int& ti, i64 e) {
   if (MPX_PREFETCH_DIST > 0) {
     const int ahead = ti + MPX_PREFETCH_DIST;
-    if (ahead < tape.n) prefetch_take<L>(tape.m[ahead], e);
+    if (ahead < tape.n) prefetch_take<L, G>(tape.m[ahead], e);
   }
   return tape.m[ti++];
 }
@@ -115,63 +155,65 @@ struct Sh {
   u64 v[L];
 };
 
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ Sh<L> sh_lin(const Sh<L>& a, u64 ka, const Sh<L>& b, u64 kb, u64 c0, int p0, u64 msk) {
   Sh<L> o;
 #pragma unroll
-  for (int l = 0; l < L; ++l) o.v[l] = (a.v[l] * ka + b.v[l] * kb + (l == p0 ? c0 : 0ull)) & msk;
+  for (int l = 0; l < L; ++l) o.v[l] = (a.v[l] * ka + b.v[l] * kb + (PI(l) == p0 ? c0 : 0ull)) & msk;
   return o;
 }
 
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ Sh<L> sh_scale(const Sh<L>& a, u64 ka, u64 c0, int p0, u64 msk) {
   Sh<L> o;
 #pragma unroll
-  for (int l = 0; l < L; ++l) o.v[l] = (a.v[l] * ka + (l == p0 ? c0 : 0ull)) & msk;
+  for (int l = 0; l < L; ++l) o.v[l] = (a.v[l] * ka + (PI(l) == p0 ? c0 : 0ull)) & msk;
   return o;
 }
 
 // Beaver mul (basic.py:27-42), triple item e of the take
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ Sh<L> d_mul(const Sh<L>& x, const Sh<L>& y, const MatRef& t, i64 e, int p0, u64 msk) {
   u64 a[L], b[L];
   u64 d = 0, f = 0;
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    a[l] = __ldcs(t.p0 + l * t.ps0 + e);
-    b[l] = __ldcs(t.p1 + l * t.ps1 + e);
+    a[l] = __ldcs(t.p0 + PI(l) * t.ps0 + e);
+    b[l] = __ldcs(t.p1 + PI(l) * t.ps1 + e);
     d += x.v[l] - a[l];
     f += y.v[l] - b[l];
   }
+  d = gsum<G>(d);
+  f = gsum<G>(f);
   Sh<L> z;
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    u64 v = __ldcs(t.p2 + l * t.ps2 + e) + d * b[l] + f * a[l];
-    if (l == p0) v += d * f;
+    u64 v = __ldcs(t.p2 + PI(l) * t.ps2 + e) + d * b[l] + f * a[l];
+    if (PI(l) == p0) v += d * f;
     z.v[l] = v & msk;
   }
   return z;
 }
 
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ Sh<L> d_mul(const Sh<L>& x, const Sh<L>& y, const MatRef& t, i64 e, int p0, u64 msk);
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ Sh<L> d_trunc(const Sh<L>& x, const MatRef& lo, const MatRef* hi, i64 e, int f,
                                          bool sgn, int w, int p0, u64 msk);
 
 // truncate(mul(x, y), f) consuming triple, edaBit(w, f), edaBit(w, w-1-f) in order
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ Sh<L> d_mul_trunc(const Sh<L>& x, const Sh<L>& y, const Tape& tape, int& ti, i64 e,
                                              int f, int w, int p0, u64 msk) {
-  const MatRef& tm = next_take<L>(tape, ti, e);
-  const Sh<L> z = d_mul<L>(x, y, tm, e, p0, msk);
-  const MatRef& lo = next_take<L>(tape, ti, e);
-  const MatRef* hi = (w - 1 - f > 0) ? &next_take<L>(tape, ti, e) : nullptr;
-  return d_trunc<L>(z, lo, hi, e, f, true, w, p0, msk);
+  const MatRef& tm = next_take<L, G>(tape, ti, e);
+  const Sh<L> z = d_mul<L, G>(x, y, tm, e, p0, msk);
+  const MatRef& lo = next_take<L, G>(tape, ti, e);
+  const MatRef* hi = (w - 1 - f > 0) ? &next_take<L, G>(tape, ti, e) : nullptr;
+  return d_trunc<L, G>(z, lo, hi, e, f, true, w, p0, msk);
 }
 
 // probabilistic truncation (derived.py:20-70); lo/hi = edaBit(w, f), edaBit(w, w-1-f)
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ Sh<L> d_trunc(const Sh<L>& x, const MatRef& lo, const MatRef* hi, i64 e, int f,
                                          bool sgn, int w, int p0, u64 msk) {
   const u64 bias = sgn ? (1ull << (w - 2)) : 0ull;
@@ -180,17 +222,18 @@ __device__ __forceinline__ Sh<L> d_trunc(const Sh<L>& x, const MatRef& lo, const
   u64 s = 0;
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    h[l] = hi ? __ldcs(hi->p0 + l * hi->ps0 + e) : 0ull;
-    u64 v = x.v[l] + __ldcs(lo.p0 + l * lo.ps0 + e) + (h[l] << f);
-    if (l == p0) v += bias;
+    h[l] = hi ? __ldcs(hi->p0 + PI(l) * hi->ps0 + e) : 0ull;
+    u64 v = x.v[l] + __ldcs(lo.p0 + PI(l) * lo.ps0 + e) + (h[l] << f);
+    if (PI(l) == p0) v += bias;
     s += v;
   }
+  s = gsum<G>(s);
   const u64 chi = (s & msk) >> f;
   Sh<L> z;
 #pragma unroll
   for (int l = 0; l < L; ++l) {
     u64 v = 0ull - h[l];
-    if (l == p0) v += chi - unbias;
+    if (PI(l) == p0) v += chi - unbias;
     z.v[l] = v & msk;
   }
   return z;
@@ -200,8 +243,8 @@ __device__ __forceinline__ Sh<L> d_trunc(const Sh<L>& x, const MatRef& lo, const
 // entry per level; returns the sum bits P0 ^ (G << 1).
 // One Kogge-Stone level (basic.py:98-129): bintriple fields for this level's
 // G (and P, unless last) AND gates, opened across the L local parties.
-template <int L>
-__device__ __forceinline__ void d_carry_level(u64 (&G)[L], u64 (&P)[L], int m, int s, const MatRef& t, i64 e,
+template <int L, int G>
+__device__ __forceinline__ void d_carry_level(u64 (&Gk)[L], u64 (&P)[L], int m, int s, const MatRef& t, i64 e,
                                               int p0) {
   const bool last = 2 * s >= m;
   const int W = m - s;
@@ -212,26 +255,32 @@ __device__ __forceinline__ void d_carry_level(u64 (&G)[L], u64 (&P)[L], int m, i
   u64 dg = 0, eg = 0, dp = 0, ep = 0;
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    ag[l] = load_bits(t.p0 + l * t.ps0, bit, W) << s;
-    bg[l] = load_bits(t.p1 + l * t.ps1, bit, W) << s;
+    ag[l] = load_bits(t.p0 + PI(l) * t.ps0, bit, W) << s;
+    bg[l] = load_bits(t.p1 + PI(l) * t.ps1, bit, W) << s;
     const u64 left = P[l] & hi;
     dg ^= left ^ ag[l];
-    eg ^= ((G[l] << s) & hi) ^ bg[l];
+    eg ^= ((Gk[l] << s) & hi) ^ bg[l];
     if (!last) {
-      ap[l] = load_bits(t.p0 + l * t.ps0, bit + W, W) << s;
-      bp[l] = load_bits(t.p1 + l * t.ps1, bit + W, W) << s;
+      ap[l] = load_bits(t.p0 + PI(l) * t.ps0, bit + W, W) << s;
+      bp[l] = load_bits(t.p1 + PI(l) * t.ps1, bit + W, W) << s;
       dp ^= left ^ ap[l];
       ep ^= ((P[l] << s) & hi) ^ bp[l];
     }
   }
+  dg = gxor<G>(dg);
+  eg = gxor<G>(eg);
+  if (!last) {
+    dp = gxor<G>(dp);
+    ep = gxor<G>(ep);
+  }
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    u64 zg = (load_bits(t.p2 + l * t.ps2, bit, W) << s) ^ (dg & bg[l]) ^ (eg & ag[l]);
-    if (l == p0) zg ^= dg & eg;
-    G[l] ^= zg;
+    u64 zg = (load_bits(t.p2 + PI(l) * t.ps2, bit, W) << s) ^ (dg & bg[l]) ^ (eg & ag[l]);
+    if (PI(l) == p0) zg ^= dg & eg;
+    Gk[l] ^= zg;
     if (!last) {
-      u64 zp = (load_bits(t.p2 + l * t.ps2, bit + W, W) << s) ^ (dp & bp[l]) ^ (ep & ap[l]);
-      if (l == p0) zp ^= dp & ep;
+      u64 zp = (load_bits(t.p2 + PI(l) * t.ps2, bit + W, W) << s) ^ (dp & bp[l]) ^ (ep & ap[l]);
+      if (PI(l) == p0) zp ^= dp & ep;
       P[l] = (P[l] & low_bits(s)) | zp;
     }
   }
@@ -241,50 +290,51 @@ __device__ __forceinline__ void d_carry_level(u64 (&G)[L], u64 (&P)[L], int m, i
 // entry per level; returns the sum bits P0 ^ (G << 1). m = 64 (the common
 // ring) runs as a fully unrolled level sequence so independent loads of the
 // next level can be scheduled early.
-template <int L>
-__device__ __forceinline__ void d_carry_sum(u64 (&G)[L], u64 (&P)[L], const u64 (&P0)[L], int m, const Tape& tape,
+template <int L, int G>
+__device__ __forceinline__ void d_carry_sum(u64 (&Gk)[L], u64 (&P)[L], const u64 (&P0)[L], int m, const Tape& tape,
                                             int& ti, i64 e, int p0, Sh<L>& out) {
   // levels s = 1, 2, 4, ... < m, unrolled; the 64-bit ring gets its own
   // constant-m copy (measured 7.7 vs 8.9 ms for the 2^24 Reciprocal)
   if (m == 64) {
 #pragma unroll
-    for (int s = 1; s < 64; s *= 2) d_carry_level<L>(G, P, 64, s, next_take<L>(tape, ti, e), e, p0);
+    for (int s = 1; s < 64; s *= 2) d_carry_level<L, G>(Gk, P, 64, s, next_take<L, G>(tape, ti, e), e, p0);
   } else {
 #pragma unroll
     for (int s = 1; s < 64; s *= 2)
-      if (s < m) d_carry_level<L>(G, P, m, s, next_take<L>(tape, ti, e), e, p0);
+      if (s < m) d_carry_level<L, G>(Gk, P, m, s, next_take<L, G>(tape, ti, e), e, p0);
   }
 #pragma unroll
-  for (int l = 0; l < L; ++l) out.v[l] = (P0[l] ^ (G[l] << 1)) & low_bits(m);
+  for (int l = 0; l < L; ++l) out.v[l] = (P0[l] ^ (Gk[l] << 1)) & low_bits(m);
 }
 
 // bit decomposition (basic.py:199-214): edaBit(w, w) then the carry tree
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ Sh<L> d_decompose(const Sh<L>& x, int w, const Tape& tape, int& ti, i64 e, int p0) {
-  const MatRef& t = next_take<L>(tape, ti, e);
+  const MatRef& t = next_take<L, G>(tape, ti, e);
   const u64 msk = ring_mask(w);
   u64 c = 0;
   u64 rb[L];
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    c += x.v[l] - __ldcs(t.p0 + l * t.ps0 + e);
-    rb[l] = load_bits(t.p1 + l * t.ps1, t.off + e * (i64)w, w);
+    c += x.v[l] - __ldcs(t.p0 + PI(l) * t.ps0 + e);
+    rb[l] = load_bits(t.p1 + PI(l) * t.ps1, t.off + e * (i64)w, w);
   }
+  c = gsum<G>(c);
   c &= msk;
-  u64 G[L], P[L], P0[L];
+  u64 Gk[L], P[L], P0[L];
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    G[l] = rb[l] & c;
-    P[l] = (l == p0) ? (rb[l] ^ c) : rb[l];
+    Gk[l] = rb[l] & c;
+    P[l] = (PI(l) == p0) ? (rb[l] ^ c) : rb[l];
     P0[l] = P[l];
   }
   Sh<L> out;
-  d_carry_sum<L>(G, P, P0, w, tape, ti, e, p0, out);
+  d_carry_sum<L, G>(Gk, P, P0, w, tape, ti, e, p0, out);
   return out;
 }
 
 // one leftmost-one level: suffix OR via a ^ b ^ ab
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ void d_lmo_level(u64 (&Y)[L], int m, int s, const MatRef& t, i64 e, int p0) {
   const int W = m - s;
   const u64 mw = low_bits(W);
@@ -293,33 +343,35 @@ __device__ __forceinline__ void d_lmo_level(u64 (&Y)[L], int m, int s, const Mat
   u64 d = 0, f = 0;
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    a[l] = load_bits(t.p0 + l * t.ps0, bit, W);
-    b[l] = load_bits(t.p1 + l * t.ps1, bit, W);
+    a[l] = load_bits(t.p0 + PI(l) * t.ps0, bit, W);
+    b[l] = load_bits(t.p1 + PI(l) * t.ps1, bit, W);
     d ^= (Y[l] & mw) ^ a[l];
     f ^= ((Y[l] >> s) & mw) ^ b[l];
   }
+  d = gxor<G>(d);
+  f = gxor<G>(f);
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    u64 z = load_bits(t.p2 + l * t.ps2, bit, W) ^ (d & b[l]) ^ (f & a[l]);
-    if (l == p0) z ^= d & f;
+    u64 z = load_bits(t.p2 + PI(l) * t.ps2, bit, W) ^ (d & b[l]) ^ (f & a[l]);
+    if (PI(l) == p0) z ^= d & f;
     const u64 lo = Y[l] & mw, hi = (Y[l] >> s) & mw;
     Y[l] = (Y[l] & ~mw) | ((lo ^ hi ^ z) & mw);
   }
 }
 
 // leftmost one (derived.py:131-149); levels unrolled like the carries
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ Sh<L> d_lmo(const Sh<L>& bits, int m, const Tape& tape, int& ti, i64 e, int p0) {
   u64 Y[L];
 #pragma unroll
   for (int l = 0; l < L; ++l) Y[l] = bits.v[l];
   if (m == 63) {
 #pragma unroll
-    for (int s = 1; s < 63; s *= 2) d_lmo_level<L>(Y, 63, s, next_take<L>(tape, ti, e), e, p0);
+    for (int s = 1; s < 63; s *= 2) d_lmo_level<L, G>(Y, 63, s, next_take<L, G>(tape, ti, e), e, p0);
   } else {
 #pragma unroll
     for (int s = 1; s < 64; s *= 2)
-      if (s < m) d_lmo_level<L>(Y, m, s, next_take<L>(tape, ti, e), e, p0);
+      if (s < m) d_lmo_level<L, G>(Y, m, s, next_take<L, G>(tape, ti, e), e, p0);
   }
   Sh<L> o;
 #pragma unroll
@@ -328,23 +380,23 @@ __device__ __forceinline__ Sh<L> d_lmo(const Sh<L>& bits, int m, const Tape& tap
 }
 
 // bit2a opening of an m-bit row (basic.py:164-184): returns the opened c word
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ u64 d_bit2a_open(const Sh<L>& b, int m, const MatRef& t, i64 e) {
   u64 c = 0;
 #pragma unroll
-  for (int l = 0; l < L; ++l) c ^= b.v[l] ^ load_bits(t.p1 + l * t.ps1, t.off + e * (i64)m, m);
-  return c & low_bits(m);
+  for (int l = 0; l < L; ++l) c ^= b.v[l] ^ load_bits(t.p1 + PI(l) * t.ps1, t.off + e * (i64)m, m);
+  return gxor<G>(c) & low_bits(m);
 }
 
 // converted bit j of the row: r_arith * (1 - 2c_j) + [p0] c_j
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ Sh<L> d_bit2a_get(u64 c, int j, int m, const MatRef& t, i64 e, int p0, u64 msk) {
   const u64 cj = (c >> j) & 1ull;
   Sh<L> z;
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    u64 v = __ldg(t.p0 + l * t.ps0 + e * (i64)m + j) * (1ull - 2ull * cj);
-    if (l == p0) v += cj;
+    u64 v = __ldg(t.p0 + PI(l) * t.ps0 + e * (i64)m + j) * (1ull - 2ull * cj);
+    if (PI(l) == p0) v += cj;
     z.v[l] = v & msk;
   }
   return z;
@@ -353,17 +405,17 @@ __device__ __forceinline__ Sh<L> d_bit2a_get(u64 c, int j, int m, const MatRef& 
 // Stream a whole converted row z_0..z_{m-1} (per party) through `f(l, j, z)`.
 // Each party's m daBit words are contiguous (items e*m .. e*m+m-1): read them
 // with back-to-back 16-byte L1-cached vector loads so every sector is used.
-template <int L, class F>
+template <int L, int G, class F>
 __device__ __forceinline__ void d_bit2a_row(u64 c, int m, int stride, const MatRef& t, i64 e, int p0, u64 msk,
                                             F&& f) {
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    const u64* row = t.p0 + l * t.ps0 + e * (i64)stride;
+    const u64* row = t.p0 + PI(l) * t.ps0 + e * (i64)stride;
     int j = 0;
     auto emit = [&](int jj, u64 r) {
       const u64 cj = (c >> jj) & 1ull;
       u64 v = r * (1ull - 2ull * cj);
-      if (l == p0) v += cj;
+      if (PI(l) == p0) v += cj;
       f(l, jj, v & msk);
     };
     if (((uintptr_t)row & 15) != 0 && m > 0) {
@@ -393,23 +445,23 @@ struct MTM {
   u64 a[L], b[L], c[L], lo[L], hi[L];
 };
 
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ void mt_load(MTM<L>& m, const Tape& tape, int& ti, i64 e, int f, int w) {
-  const MatRef& tm = next_take<L>(tape, ti, e);
-  const MatRef& lo = next_take<L>(tape, ti, e);
+  const MatRef& tm = next_take<L, G>(tape, ti, e);
+  const MatRef& lo = next_take<L, G>(tape, ti, e);
   const bool has_hi = w - 1 - f > 0;
-  const MatRef* hi = has_hi ? &next_take<L>(tape, ti, e) : nullptr;
+  const MatRef* hi = has_hi ? &next_take<L, G>(tape, ti, e) : nullptr;
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    m.a[l] = __ldcs(tm.p0 + l * tm.ps0 + e);
-    m.b[l] = __ldcs(tm.p1 + l * tm.ps1 + e);
-    m.c[l] = __ldcs(tm.p2 + l * tm.ps2 + e);
-    m.lo[l] = __ldcs(lo.p0 + l * lo.ps0 + e);
-    m.hi[l] = hi ? __ldcs(hi->p0 + l * hi->ps0 + e) : 0ull;
+    m.a[l] = __ldcs(tm.p0 + PI(l) * tm.ps0 + e);
+    m.b[l] = __ldcs(tm.p1 + PI(l) * tm.ps1 + e);
+    m.c[l] = __ldcs(tm.p2 + PI(l) * tm.ps2 + e);
+    m.lo[l] = __ldcs(lo.p0 + PI(l) * lo.ps0 + e);
+    m.hi[l] = hi ? __ldcs(hi->p0 + PI(l) * hi->ps0 + e) : 0ull;
   }
 }
 
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ Sh<L> mt_compute(const Sh<L>& x, const Sh<L>& y, const MTM<L>& m, int f, int w, int p0,
                                             u64 msk) {
   u64 d = 0, g = 0;
@@ -418,48 +470,51 @@ __device__ __forceinline__ Sh<L> mt_compute(const Sh<L>& x, const Sh<L>& y, cons
     d += x.v[l] - m.a[l];
     g += y.v[l] - m.b[l];
   }
+  d = gsum<G>(d);
+  g = gsum<G>(g);
   const u64 bias = 1ull << (w - 2), unbias = 1ull << (w - 2 - f);
   u64 z[L];
   u64 s = 0;
 #pragma unroll
   for (int l = 0; l < L; ++l) {
     u64 v = m.c[l] + d * m.b[l] + g * m.a[l];
-    if (l == p0) v += d * g;
+    if (PI(l) == p0) v += d * g;
     z[l] = v & msk;
     u64 t = z[l] + m.lo[l] + (m.hi[l] << f);
-    if (l == p0) t += bias;
+    if (PI(l) == p0) t += bias;
     s += t;
   }
+  s = gsum<G>(s);
   const u64 chi = (s & msk) >> f;
   Sh<L> o;
 #pragma unroll
   for (int l = 0; l < L; ++l) {
     u64 v = 0ull - m.hi[l];
-    if (l == p0) v += chi - unbias;
+    if (PI(l) == p0) v += chi - unbias;
     o.v[l] = v & msk;
   }
   return o;
 }
 
 // polynomial at precision p (derived.py:86-108), coefficients pre-encoded
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ Sh<L> d_poly4(const Sh<L>& x, const FusedParams& P, const Tape& tape, int& ti, i64 e,
                                          u64 msk) {
 #ifdef MPX_POLY_PIPELINED
   MTM<L> A, B;
-  mt_load<L>(A, tape, ti, e, P.p, P.w);
-  mt_load<L>(B, tape, ti, e, P.p, P.w);
-  const Sh<L> x2 = mt_compute<L>(x, x, A, P.p, P.w, P.p0, msk);
-  mt_load<L>(A, tape, ti, e, P.p, P.w);
-  const Sh<L> x3 = mt_compute<L>(x2, x, B, P.p, P.w, P.p0, msk);
-  const Sh<L> x4 = mt_compute<L>(x3, x, A, P.p, P.w, P.p0, msk);
+  mt_load<L, G>(A, tape, ti, e, P.p, P.w);
+  mt_load<L, G>(B, tape, ti, e, P.p, P.w);
+  const Sh<L> x2 = mt_compute<L, G>(x, x, A, P.p, P.w, P.p0, msk);
+  mt_load<L, G>(A, tape, ti, e, P.p, P.w);
+  const Sh<L> x3 = mt_compute<L, G>(x2, x, B, P.p, P.w, P.p0, msk);
+  const Sh<L> x4 = mt_compute<L, G>(x3, x, A, P.p, P.w, P.p0, msk);
 #else
-  const Sh<L> x2 = d_mul_trunc<L>(x, x, tape, ti, e, P.p, P.w, P.p0, msk);
-  const Sh<L> x3 = d_mul_trunc<L>(x2, x, tape, ti, e, P.p, P.w, P.p0, msk);
-  const Sh<L> x4 = d_mul_trunc<L>(x3, x, tape, ti, e, P.p, P.w, P.p0, msk);
+  const Sh<L> x2 = d_mul_trunc<L, G>(x, x, tape, ti, e, P.p, P.w, P.p0, msk);
+  const Sh<L> x3 = d_mul_trunc<L, G>(x2, x, tape, ti, e, P.p, P.w, P.p0, msk);
+  const Sh<L> x4 = d_mul_trunc<L, G>(x3, x, tape, ti, e, P.p, P.w, P.p0, msk);
 #endif
-  const MatRef& flo = next_take<L>(tape, ti, e);
-  const MatRef& fhi = next_take<L>(tape, ti, e);
+  const MatRef& flo = next_take<L, G>(tape, ti, e);
+  const MatRef& fhi = next_take<L, G>(tape, ti, e);
   u64 acc[L];
 #pragma unroll
   for (int l = 0; l < L; ++l) acc[l] = 0;
@@ -481,34 +536,34 @@ __device__ __forceinline__ Sh<L> d_poly4(const Sh<L>& x, const FusedParams& P, c
   }
   Sh<L> a;
 #pragma unroll
-  for (int l = 0; l < L; ++l) a.v[l] = (acc[l] + (l == P.p0 ? P.coef0_2p : 0ull)) & msk;
-  return d_trunc<L>(a, flo, &fhi, e, P.p, true, P.w, P.p0, msk);
+  for (int l = 0; l < L; ++l) a.v[l] = (acc[l] + (PI(l) == P.p0 ? P.coef0_2p : 0ull)) & msk;
+  return d_trunc<L, G>(a, flo, &fhi, e, P.p, true, P.w, P.p0, msk);
 }
 
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ Sh<L> load_sh(const u64* x, i64 n, i64 e) {
   Sh<L> s;
 #pragma unroll
-  for (int l = 0; l < L; ++l) s.v[l] = __ldcs(x + l * n + e);
+  for (int l = 0; l < L; ++l) s.v[l] = __ldcs(x + PI(l) * n + e);
   return s;
 }
 
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ void store_sh(u64* y, i64 n, i64 e, const Sh<L>& s) {
 #pragma unroll
-  for (int l = 0; l < L; ++l) __stcs(y + l * n + e, s.v[l]);
+  for (int l = 0; l < L; ++l) __stcs(y + PI(l) * n + e, s.v[l]);
 }
 
 // ---------------------------------------------------------------------------
 // Reciprocal, paper Alg. 1 (nonlinear.py:146-176)
 
 // Reciprocal (Alg. 1, nonlinear.py:146-176) of one element's shares.
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ Sh<L> d_reciprocal(const Sh<L>& x, const Tape& tape, int& ti, i64 e,
                                               const FusedParams& P) {
   const int w = P.w, p = P.p, p0 = P.p0;
   const u64 msk = ring_mask(w);
-  const Sh<L> bits = d_decompose<L>(x, w, tape, ti, e, p0);
+  const Sh<L> bits = d_decompose<L, G>(x, w, tape, ti, e, p0);
   Sh<L> sign, mag;
 #pragma unroll
   for (int l = 0; l < L; ++l) {
@@ -516,54 +571,54 @@ __device__ __forceinline__ Sh<L> d_reciprocal(const Sh<L>& x, const Tape& tape, 
     const u64 mm = low_bits(w - 1);
     mag.v[l] = (bits.v[l] & mm) ^ (sign.v[l] ? mm : 0ull);
   }
-  const MatRef& tsg = next_take<L>(tape, ti, e);
-  const u64 csg = d_bit2a_open<L>(sign, 1, tsg, e);
-  const Sh<L> s = d_bit2a_get<L>(csg, 0, 1, tsg, e, p0, msk);
-  const Sh<L> sx = d_mul<L>(s, x, next_take<L>(tape, ti, e), e, p0, msk);
-  const Sh<L> x_pos = sh_lin<L>(x, 1, sx, 0ull - 2ull, 0, p0, msk);
-  const Sh<L> onehot = d_lmo<L>(mag, w - 1, tape, ti, e, p0);
+  const MatRef& tsg = next_take<L, G>(tape, ti, e);
+  const u64 csg = d_bit2a_open<L, G>(sign, 1, tsg, e);
+  const Sh<L> s = d_bit2a_get<L, G>(csg, 0, 1, tsg, e, p0, msk);
+  const Sh<L> sx = d_mul<L, G>(s, x, next_take<L, G>(tape, ti, e), e, p0, msk);
+  const Sh<L> x_pos = sh_lin<L, G>(x, 1, sx, 0ull - 2ull, 0, p0, msk);
+  const Sh<L> onehot = d_lmo<L, G>(mag, w - 1, tape, ti, e, p0);
   // reversed low 2p window -> compose (basic.py:187-196)
   Sh<L> window;
 #pragma unroll
   for (int l = 0; l < L; ++l) window.v[l] = __brevll(onehot.v[l] & low_bits(2 * p)) >> (64 - 2 * p);
-  const MatRef& tc = next_take<L>(tape, ti, e);
-  const u64 cw = d_bit2a_open<L>(window, 2 * p, tc, e);
+  const MatRef& tc = next_take<L, G>(tape, ti, e);
+  const u64 cw = d_bit2a_open<L, G>(window, 2 * p, tc, e);
   Sh<L> t;
 #pragma unroll
   for (int l = 0; l < L; ++l) t.v[l] = 0;
-  d_bit2a_row<L>(cw, 2 * p, 2 * p, tc, e, p0, msk, [&](int l, int j, u64 z) { t.v[l] += z << j; });
+  d_bit2a_row<L, G>(cw, 2 * p, 2 * p, tc, e, p0, msk, [&](int l, int j, u64 z) { t.v[l] += z << j; });
 #pragma unroll
   for (int l = 0; l < L; ++l) t.v[l] &= msk;
   // z = trunc(t * x_pos), Newton product (nonlinear.py:134-143), y = trunc(t * acc):
   // a chain of 2*iters mul+trunc steps, pipelined one step ahead (A/B)
   MTM<L> A, B;
-  mt_load<L>(A, tape, ti, e, p, w);
-  mt_load<L>(B, tape, ti, e, p, w);
-  const Sh<L> z = mt_compute<L>(t, x_pos, A, p, w, p0, msk);
-  Sh<L> q = sh_scale<L>(z, 0ull - 1ull, P.one_p, p0, msk);
-  Sh<L> acc = sh_scale<L>(q, 1, P.one_p, p0, msk);
+  mt_load<L, G>(A, tape, ti, e, p, w);
+  mt_load<L, G>(B, tape, ti, e, p, w);
+  const Sh<L> z = mt_compute<L, G>(t, x_pos, A, p, w, p0, msk);
+  Sh<L> q = sh_scale<L, G>(z, 0ull - 1ull, P.one_p, p0, msk);
+  Sh<L> acc = sh_scale<L, G>(q, 1, P.one_p, p0, msk);
   for (int it = 1; it < P.iters; ++it) {
-    mt_load<L>(A, tape, ti, e, p, w);
-    q = mt_compute<L>(q, q, B, p, w, p0, msk);
-    mt_load<L>(B, tape, ti, e, p, w);
-    acc = mt_compute<L>(acc, sh_scale<L>(q, 1, P.one_p, p0, msk), A, p, w, p0, msk);
+    mt_load<L, G>(A, tape, ti, e, p, w);
+    q = mt_compute<L, G>(q, q, B, p, w, p0, msk);
+    mt_load<L, G>(B, tape, ti, e, p, w);
+    acc = mt_compute<L, G>(acc, sh_scale<L, G>(q, 1, P.one_p, p0, msk), A, p, w, p0, msk);
   }
-  const Sh<L> yv = mt_compute<L>(t, acc, B, p, w, p0, msk);
-  const Sh<L> sy = d_mul<L>(s, yv, next_take<L>(tape, ti, e), e, p0, msk);
-  return sh_lin<L>(yv, 1, sy, 0ull - 2ull, 0, p0, msk);
+  const Sh<L> yv = mt_compute<L, G>(t, acc, B, p, w, p0, msk);
+  const Sh<L> sy = d_mul<L, G>(s, yv, next_take<L, G>(tape, ti, e), e, p0, msk);
+  return sh_lin<L, G>(yv, 1, sy, 0ull - 2ull, 0, p0, msk);
 }
 
 // Standalone kernel keeps its own copy of the body: through d_reciprocal it
 // compiles to 72 registers + spills at L = 2 (8.3 vs 7.9 ms at 2^24).
-template <int L>
+template <int L, int G>
 __global__ void __launch_bounds__(128) k_reciprocal_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
                                                           const __grid_constant__ Tape tape, FusedParams P) {
   const int w = P.w, p = P.p, p0 = P.p0;
   const u64 msk = ring_mask(w);
-  GRID_STRIDE(e, n) {
+  GRID_STRIDE_G(e, n) {
     int ti = 0;
-    const Sh<L> x = load_sh<L>(xin, n, e);
-    const Sh<L> bits = d_decompose<L>(x, w, tape, ti, e, p0);
+    const Sh<L> x = load_sh<L, G>(xin, n, e);
+    const Sh<L> bits = d_decompose<L, G>(x, w, tape, ti, e, p0);
     Sh<L> sign, mag;
 #pragma unroll
     for (int l = 0; l < L; ++l) {
@@ -571,86 +626,86 @@ __global__ void __launch_bounds__(128) k_reciprocal_fused(u64* __restrict__ y, c
       const u64 mm = low_bits(w - 1);
       mag.v[l] = (bits.v[l] & mm) ^ (sign.v[l] ? mm : 0ull);
     }
-    const MatRef& tsg = next_take<L>(tape, ti, e);
-    const u64 csg = d_bit2a_open<L>(sign, 1, tsg, e);
-    const Sh<L> s = d_bit2a_get<L>(csg, 0, 1, tsg, e, p0, msk);
-    const Sh<L> sx = d_mul<L>(s, x, next_take<L>(tape, ti, e), e, p0, msk);
-    const Sh<L> x_pos = sh_lin<L>(x, 1, sx, 0ull - 2ull, 0, p0, msk);
-    const Sh<L> onehot = d_lmo<L>(mag, w - 1, tape, ti, e, p0);
+    const MatRef& tsg = next_take<L, G>(tape, ti, e);
+    const u64 csg = d_bit2a_open<L, G>(sign, 1, tsg, e);
+    const Sh<L> s = d_bit2a_get<L, G>(csg, 0, 1, tsg, e, p0, msk);
+    const Sh<L> sx = d_mul<L, G>(s, x, next_take<L, G>(tape, ti, e), e, p0, msk);
+    const Sh<L> x_pos = sh_lin<L, G>(x, 1, sx, 0ull - 2ull, 0, p0, msk);
+    const Sh<L> onehot = d_lmo<L, G>(mag, w - 1, tape, ti, e, p0);
     // reversed low 2p window -> compose (basic.py:187-196)
     Sh<L> window;
 #pragma unroll
     for (int l = 0; l < L; ++l) window.v[l] = __brevll(onehot.v[l] & low_bits(2 * p)) >> (64 - 2 * p);
-    const MatRef& tc = next_take<L>(tape, ti, e);
-    const u64 cw = d_bit2a_open<L>(window, 2 * p, tc, e);
+    const MatRef& tc = next_take<L, G>(tape, ti, e);
+    const u64 cw = d_bit2a_open<L, G>(window, 2 * p, tc, e);
     Sh<L> t;
 #pragma unroll
     for (int l = 0; l < L; ++l) t.v[l] = 0;
-    d_bit2a_row<L>(cw, 2 * p, 2 * p, tc, e, p0, msk, [&](int l, int j, u64 z) { t.v[l] += z << j; });
+    d_bit2a_row<L, G>(cw, 2 * p, 2 * p, tc, e, p0, msk, [&](int l, int j, u64 z) { t.v[l] += z << j; });
 #pragma unroll
     for (int l = 0; l < L; ++l) t.v[l] &= msk;
     // z = trunc(t * x_pos), Newton product (nonlinear.py:134-143), y = trunc(t * acc):
     // a chain of 2*iters mul+trunc steps, pipelined one step ahead (A/B)
     MTM<L> A, B;
-    mt_load<L>(A, tape, ti, e, p, w);
-    mt_load<L>(B, tape, ti, e, p, w);
-    const Sh<L> z = mt_compute<L>(t, x_pos, A, p, w, p0, msk);
-    Sh<L> q = sh_scale<L>(z, 0ull - 1ull, P.one_p, p0, msk);
-    Sh<L> acc = sh_scale<L>(q, 1, P.one_p, p0, msk);
+    mt_load<L, G>(A, tape, ti, e, p, w);
+    mt_load<L, G>(B, tape, ti, e, p, w);
+    const Sh<L> z = mt_compute<L, G>(t, x_pos, A, p, w, p0, msk);
+    Sh<L> q = sh_scale<L, G>(z, 0ull - 1ull, P.one_p, p0, msk);
+    Sh<L> acc = sh_scale<L, G>(q, 1, P.one_p, p0, msk);
     for (int it = 1; it < P.iters; ++it) {
-      mt_load<L>(A, tape, ti, e, p, w);
-      q = mt_compute<L>(q, q, B, p, w, p0, msk);
-      mt_load<L>(B, tape, ti, e, p, w);
-      acc = mt_compute<L>(acc, sh_scale<L>(q, 1, P.one_p, p0, msk), A, p, w, p0, msk);
+      mt_load<L, G>(A, tape, ti, e, p, w);
+      q = mt_compute<L, G>(q, q, B, p, w, p0, msk);
+      mt_load<L, G>(B, tape, ti, e, p, w);
+      acc = mt_compute<L, G>(acc, sh_scale<L, G>(q, 1, P.one_p, p0, msk), A, p, w, p0, msk);
     }
-    const Sh<L> yv = mt_compute<L>(t, acc, B, p, w, p0, msk);
-    const Sh<L> sy = d_mul<L>(s, yv, next_take<L>(tape, ti, e), e, p0, msk);
-    store_sh<L>(y, n, e, sh_lin<L>(yv, 1, sy, 0ull - 2ull, 0, p0, msk));
+    const Sh<L> yv = mt_compute<L, G>(t, acc, B, p, w, p0, msk);
+    const Sh<L> sy = d_mul<L, G>(s, yv, next_take<L, G>(tape, ti, e), e, p0, msk);
+    store_sh<L, G>(y, n, e, sh_lin<L, G>(yv, 1, sy, 0ull - 2ull, 0, p0, msk));
   }
 }
 
 // ---------------------------------------------------------------------------
 // Exponentiation, paper Alg. 2 (nonlinear.py:179-213)
 
-template <int L>
+template <int L, int G>
 __global__ void __launch_bounds__(128) k_exp_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
                                                    const __grid_constant__ Tape tape, FusedParams P) {
   const int w = P.w, p = P.p, p0 = P.p0, c = P.c, bias = P.bias;
   const u64 msk = ring_mask(w);
-  GRID_STRIDE(e, n) {
+  GRID_STRIDE_G(e, n) {
     int ti = 0;
     if (P.pf)  // small calls are latency-bound: pull the element's whole tape towards L2 first
-      for (int i = 0; i < tape.n; ++i) prefetch_take<L>(tape.m[i], e);
-    const Sh<L> x = load_sh<L>(xin, n, e);
-    const Sh<L> xb = sh_scale<L>(x, P.log2e_p, P.bias_2p, p0, msk);
-    const Sh<L> bits = d_decompose<L>(xb, w, tape, ti, e, p0);
+      for (int i = 0; i < tape.n; ++i) prefetch_take<L, G>(tape.m[i], e);
+    const Sh<L> x = load_sh<L, G>(xin, n, e);
+    const Sh<L> xb = sh_scale<L, G>(x, P.log2e_p, P.bias_2p, p0, msk);
+    const Sh<L> bits = d_decompose<L, G>(xb, w, tape, ti, e, p0);
     const int k = p + c + 1;
     Sh<L> seg;
 #pragma unroll
     for (int l = 0; l < L; ++l)
       seg.v[l] = ((bits.v[l] >> p) & low_bits(p + c)) | (((bits.v[l] >> (w - 1)) & 1ull) << (p + c));
-    const MatRef& tc = next_take<L>(tape, ti, e);
-    const u64 cw = d_bit2a_open<L>(seg, k, tc, e);
+    const MatRef& tc = next_take<L, G>(tape, ti, e);
+    const u64 cw = d_bit2a_open<L, G>(seg, k, tc, e);
     Sh<L> t;
 #pragma unroll
     for (int l = 0; l < L; ++l) t.v[l] = 0;
     // fraction window: first p converted bits, streamed; the row stays in L1
-    d_bit2a_row<L>(cw, p, k, tc, e, p0, msk, [&](int l, int j, u64 z) { t.v[l] += z << j; });
+    d_bit2a_row<L, G>(cw, p, k, tc, e, p0, msk, [&](int l, int j, u64 z) { t.v[l] += z << j; });
 #pragma unroll
     for (int l = 0; l < L; ++l) t.v[l] &= msk;
     // 2^int as a product of (2^(2^i) b_i - b_i + 1) (nonlinear.py:125-131)
-    Sh<L> pw = sh_scale<L>(d_bit2a_get<L>(cw, p, k, tc, e, p0, msk), 1ull, 1ull, p0, msk);
+    Sh<L> pw = sh_scale<L, G>(d_bit2a_get<L, G>(cw, p, k, tc, e, p0, msk), 1ull, 1ull, p0, msk);
     for (int i = 1; i < c; ++i) {
-      const Sh<L> bi = d_bit2a_get<L>(cw, p + i, k, tc, e, p0, msk);
+      const Sh<L> bi = d_bit2a_get<L, G>(cw, p + i, k, tc, e, p0, msk);
       const u64 kf = (1ull << (1 << i)) - 1ull;
-      pw = d_mul<L>(pw, sh_scale<L>(bi, kf, 1ull, p0, msk), next_take<L>(tape, ti, e), e, p0, msk);
+      pw = d_mul<L, G>(pw, sh_scale<L, G>(bi, kf, 1ull, p0, msk), next_take<L, G>(tape, ti, e), e, p0, msk);
     }
-    const Sh<L> sgn = d_bit2a_get<L>(cw, p + c, k, tc, e, p0, msk);
-    const Sh<L> poly = d_poly4<L>(t, P, tape, ti, e, msk);
-    const Sh<L> yv = d_mul<L>(pw, poly, next_take<L>(tape, ti, e), e, p0, msk);
-    const Sh<L> s1 = sh_scale<L>(sgn, 0ull - 1ull, 1ull, p0, msk);
-    const Sh<L> out = d_mul_trunc<L>(s1, yv, tape, ti, e, bias, w, p0, msk);
-    store_sh<L>(y, n, e, out);
+    const Sh<L> sgn = d_bit2a_get<L, G>(cw, p + c, k, tc, e, p0, msk);
+    const Sh<L> poly = d_poly4<L, G>(t, P, tape, ti, e, msk);
+    const Sh<L> yv = d_mul<L, G>(pw, poly, next_take<L, G>(tape, ti, e), e, p0, msk);
+    const Sh<L> s1 = sh_scale<L, G>(sgn, 0ull - 1ull, 1ull, p0, msk);
+    const Sh<L> out = d_mul_trunc<L, G>(s1, yv, tape, ti, e, bias, w, p0, msk);
+    store_sh<L, G>(y, n, e, out);
   }
 }
 
@@ -662,117 +717,119 @@ __global__ void __launch_bounds__(128) k_exp_fused(u64* __restrict__ y, const u6
 // 64, p), coef0_2p = enc(lead*t0, 64, 2p), P.bias = lead_shift, P.c = c.
 
 // attention_exp (App. E, nonlinear.py:315-356): narrow input, 64-bit output.
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ Sh<L> d_attexp(const Sh<L>& x, const Tape& tape, int& ti, i64 e, const FusedParams& P) {
   const int win = P.w, p = P.p, p0 = P.p0, c = P.c;
   const u64 msk_in = ring_mask(win), msk = ring_mask(64);
-  const Sh<L> xb = sh_scale<L>(x, 1ull, P.coef_p[0], p0, msk_in);
-  const Sh<L> bits = d_decompose<L>(xb, win, tape, ti, e, p0);
+  const Sh<L> xb = sh_scale<L, G>(x, 1ull, P.coef_p[0], p0, msk_in);
+  const Sh<L> bits = d_decompose<L, G>(xb, win, tape, ti, e, p0);
   const int k = p + c + 1;
   Sh<L> seg;
 #pragma unroll
   for (int l = 0; l < L; ++l)
     seg.v[l] = (bits.v[l] & low_bits(p + c)) | (((bits.v[l] >> (win - 1)) & 1ull) << (p + c));
-  const MatRef& tc = next_take<L>(tape, ti, e);
-  const u64 cw = d_bit2a_open<L>(seg, k, tc, e);
+  const MatRef& tc = next_take<L, G>(tape, ti, e);
+  const u64 cw = d_bit2a_open<L, G>(seg, k, tc, e);
   Sh<L> t;
 #pragma unroll
   for (int l = 0; l < L; ++l) t.v[l] = 0;
-  d_bit2a_row<L>(cw, p, k, tc, e, p0, msk, [&](int l, int j, u64 z) { t.v[l] += z << j; });
+  d_bit2a_row<L, G>(cw, p, k, tc, e, p0, msk, [&](int l, int j, u64 z) { t.v[l] += z << j; });
   // 2^int as a product of (2^(2^i) b_i - b_i + 1) (nonlinear.py:125-131)
-  Sh<L> pw = sh_scale<L>(d_bit2a_get<L>(cw, p, k, tc, e, p0, msk), 1ull, 1ull, p0, msk);
+  Sh<L> pw = sh_scale<L, G>(d_bit2a_get<L, G>(cw, p, k, tc, e, p0, msk), 1ull, 1ull, p0, msk);
   for (int i = 1; i < c; ++i) {
-    const Sh<L> bi = d_bit2a_get<L>(cw, p + i, k, tc, e, p0, msk);
+    const Sh<L> bi = d_bit2a_get<L, G>(cw, p + i, k, tc, e, p0, msk);
     const u64 kf = (1ull << (1 << i)) - 1ull;
-    pw = d_mul<L>(pw, sh_scale<L>(bi, kf, 1ull, p0, msk), next_take<L>(tape, ti, e), e, p0, msk);
+    pw = d_mul<L, G>(pw, sh_scale<L, G>(bi, kf, 1ull, p0, msk), next_take<L, G>(tape, ti, e), e, p0, msk);
   }
-  const Sh<L> sgn = d_bit2a_get<L>(cw, p + c, k, tc, e, p0, msk);
+  const Sh<L> sgn = d_bit2a_get<L, G>(cw, p + c, k, tc, e, p0, msk);
   // evaluate_square_completed (derived.py:111-128)
-  const Sh<L> u = sh_scale<L>(t, 1ull, P.coef_p[1], p0, msk);
-  const Sh<L> u2 = d_mul_trunc<L>(u, u, tape, ti, e, p, 64, p0, msk);
-  const Sh<L> v = sh_scale<L>(u2, 1ull, P.coef_p[2], p0, msk);
-  const Sh<L> sq = d_mul<L>(v, v, next_take<L>(tape, ti, e), e, p0, msk);
+  const Sh<L> u = sh_scale<L, G>(t, 1ull, P.coef_p[1], p0, msk);
+  const Sh<L> u2 = d_mul_trunc<L, G>(u, u, tape, ti, e, p, 64, p0, msk);
+  const Sh<L> v = sh_scale<L, G>(u2, 1ull, P.coef_p[2], p0, msk);
+  const Sh<L> sq = d_mul<L, G>(v, v, next_take<L, G>(tape, ti, e), e, p0, msk);
   Sh<L> lead = sq;  // truncate(sq, 0) is a copy (derived.py:55-57)
   if (P.bias > 0) {
-    const MatRef& lo = next_take<L>(tape, ti, e);
-    const MatRef* hi = (64 - 1 - P.bias > 0) ? &next_take<L>(tape, ti, e) : nullptr;
-    lead = d_trunc<L>(sq, lo, hi, e, P.bias, true, 64, p0, msk);
+    const MatRef& lo = next_take<L, G>(tape, ti, e);
+    const MatRef* hi = (64 - 1 - P.bias > 0) ? &next_take<L, G>(tape, ti, e) : nullptr;
+    lead = d_trunc<L, G>(sq, lo, hi, e, P.bias, true, 64, p0, msk);
   }
-  Sh<L> acc = sh_lin<L>(lead, 1ull, t, P.coef_p[3], P.coef0_2p, p0, msk);
+  Sh<L> acc = sh_lin<L, G>(lead, 1ull, t, P.coef_p[3], P.coef0_2p, p0, msk);
   Sh<L> ev;
   {
-    const MatRef& lo = next_take<L>(tape, ti, e);
-    const MatRef& hi = next_take<L>(tape, ti, e);
-    ev = d_trunc<L>(acc, lo, &hi, e, p, true, 64, p0, msk);
+    const MatRef& lo = next_take<L, G>(tape, ti, e);
+    const MatRef& hi = next_take<L, G>(tape, ti, e);
+    ev = d_trunc<L, G>(acc, lo, &hi, e, p, true, 64, p0, msk);
   }
-  const Sh<L> yv = d_mul<L>(pw, ev, next_take<L>(tape, ti, e), e, p0, msk);
-  const Sh<L> s1 = sh_scale<L>(sgn, 0ull - 1ull, 1ull, p0, msk);
-  const Sh<L> out = d_mul_trunc<L>(s1, yv, tape, ti, e, p, 64, p0, msk);
+  const Sh<L> yv = d_mul<L, G>(pw, ev, next_take<L, G>(tape, ti, e), e, p0, msk);
+  const Sh<L> s1 = sh_scale<L, G>(sgn, 0ull - 1ull, 1ull, p0, msk);
+  const Sh<L> out = d_mul_trunc<L, G>(s1, yv, tape, ti, e, p, 64, p0, msk);
   return out;
 }
 
-template <int L>
+template <int L, int G>
 __global__ void __launch_bounds__(128) k_attexp_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
                                                       const __grid_constant__ Tape tape, FusedParams P) {
-  GRID_STRIDE(e, n) {
+  GRID_STRIDE_G(e, n) {
     int ti = 0;
     if (P.pf)  // small calls are latency-bound: pull the element's whole tape towards L2 first
-      for (int i = 0; i < tape.n; ++i) prefetch_take<L>(tape.m[i], e);
-    const Sh<L> x = load_sh<L>(xin, n, e);
-    store_sh<L>(y, n, e, d_attexp<L>(x, tape, ti, e, P));
+      for (int i = 0; i < tape.n; ++i) prefetch_take<L, G>(tape.m[i], e);
+    const Sh<L> x = load_sh<L, G>(xin, n, e);
+    store_sh<L, G>(y, n, e, d_attexp<L, G>(x, tape, ti, e, P));
   }
 }
 
 // ---------------------------------------------------------------------------
 // Logarithm, paper Alg. 3 without the big-input pre-shift (nonlinear.py:216-267)
 
-template <int L>
-__global__ void __launch_bounds__(128, MPX_MINB_L(L, MPX_LOG_MINB)) k_log_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
+template <int L, int G>
+__global__ void __launch_bounds__(128, MPX_MINB_LG(L, G, MPX_LOG_MINB)) k_log_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
                                                    const __grid_constant__ Tape tape, FusedParams P) {
   const int w = P.w, p = P.p, p0 = P.p0;
   const u64 msk = ring_mask(w);
   const int m2 = 2 * p;
-  GRID_STRIDE(e, n) {
+  GRID_STRIDE_G(e, n) {
     int ti = 0;
     if (P.pf)  // small calls are latency-bound: pull the element's whole tape towards L2 first
-      for (int i = 0; i < tape.n; ++i) prefetch_take<L>(tape.m[i], e);
-    const Sh<L> x = load_sh<L>(xin, n, e);
-    const Sh<L> bits = d_decompose<L>(x, w, tape, ti, e, p0);
+      for (int i = 0; i < tape.n; ++i) prefetch_take<L, G>(tape.m[i], e);
+    const Sh<L> x = load_sh<L, G>(xin, n, e);
+    const Sh<L> bits = d_decompose<L, G>(x, w, tape, ti, e, p0);
     Sh<L> window;
 #pragma unroll
     for (int l = 0; l < L; ++l) window.v[l] = bits.v[l] & low_bits(m2);
-    const Sh<L> onehot = d_lmo<L>(window, m2, tape, ti, e, p0);
+    const Sh<L> onehot = d_lmo<L, G>(window, m2, tape, ti, e, p0);
     // paired = AND(window, below) (basic.py:82-95), one bintriple per bit
-    const MatRef& ta = next_take<L>(tape, ti, e);
+    const MatRef& ta = next_take<L, G>(tape, ti, e);
     u64 a[L], b[L];
     u64 d = 0, f = 0;
     const i64 bit = ta.off + e * (i64)m2;
 #pragma unroll
     for (int l = 0; l < L; ++l) {
-      a[l] = load_bits(ta.p0 + l * ta.ps0, bit, m2);
-      b[l] = load_bits(ta.p1 + l * ta.ps1, bit, m2);
+      a[l] = load_bits(ta.p0 + PI(l) * ta.ps0, bit, m2);
+      b[l] = load_bits(ta.p1 + PI(l) * ta.ps1, bit, m2);
       const u64 below = onehot.v[l] >> 1;
       d ^= window.v[l] ^ a[l];
       f ^= below ^ b[l];
     }
+    d = gxor<G>(d);
+    f = gxor<G>(f);
     Sh<L> seg;
 #pragma unroll
     for (int l = 0; l < L; ++l) {
-      u64 z = load_bits(ta.p2 + l * ta.ps2, bit, m2) ^ (d & b[l]) ^ (f & a[l]);
-      if (l == p0) z ^= d & f;
+      u64 z = load_bits(ta.p2 + PI(l) * ta.ps2, bit, m2) ^ (d & b[l]) ^ (f & a[l]);
+      if (PI(l) == p0) z ^= d & f;
       const u64 r_bit = (u64)(__popcll(z & low_bits(m2)) & 1);
       seg.v[l] = (onehot.v[l] & low_bits(m2)) | (r_bit << m2);
     }
     const int k = m2 + 1;
-    const MatRef& tc = next_take<L>(tape, ti, e);
-    const u64 cw = d_bit2a_open<L>(seg, k, tc, e);
+    const MatRef& tc = next_take<L, G>(tape, ti, e);
+    const u64 cw = d_bit2a_open<L, G>(seg, k, tc, e);
     Sh<L> yl, mm, r;
 #pragma unroll
     for (int l = 0; l < L; ++l) {
       yl.v[l] = 0;
       mm.v[l] = 0;
     }
-    d_bit2a_row<L>(cw, k, k, tc, e, p0, msk, [&](int l, int j, u64 z) {
+    d_bit2a_row<L, G>(cw, k, k, tc, e, p0, msk, [&](int l, int j, u64 z) {
       if (j < m2) {
         yl.v[l] += z * (u64)(long long)(j - p);
         mm.v[l] += z << (m2 - 1 - j);
@@ -780,21 +837,21 @@ __global__ void __launch_bounds__(128, MPX_MINB_L(L, MPX_LOG_MINB)) k_log_fused(
         r.v[l] = z;
       }
     });
-    const Sh<L> xr = d_mul<L>(x, r, next_take<L>(tape, ti, e), e, p0, msk);
-    const Sh<L> doubled = sh_lin<L>(x, 2, xr, 0ull - 1ull, 0, p0, msk);
-    Sh<L> t = d_mul_trunc<L>(doubled, sh_scale<L>(mm, 1, 0, p0, msk), tape, ti, e, p, w, p0, msk);
-    t = sh_scale<L>(t, 1, P.m1_p, p0, msk);
-    const Sh<L> yr = d_poly4<L>(t, P, tape, ti, e, msk);
+    const Sh<L> xr = d_mul<L, G>(x, r, next_take<L, G>(tape, ti, e), e, p0, msk);
+    const Sh<L> doubled = sh_lin<L, G>(x, 2, xr, 0ull - 1ull, 0, p0, msk);
+    Sh<L> t = d_mul_trunc<L, G>(doubled, sh_scale<L, G>(mm, 1, 0, p0, msk), tape, ti, e, p, w, p0, msk);
+    t = sh_scale<L, G>(t, 1, P.m1_p, p0, msk);
+    const Sh<L> yr = d_poly4<L, G>(t, P, tape, ti, e, msk);
     Sh<L> pre;
 #pragma unroll
     for (int l = 0; l < L; ++l) pre.v[l] = (yr.v[l] + (yl.v[l] << p) + (r.v[l] << p)) & msk;
-    Sh<L> out = sh_scale<L>(pre, P.ln2_p, 0, p0, msk);
+    Sh<L> out = sh_scale<L, G>(pre, P.ln2_p, 0, p0, msk);
     {
-      const MatRef& lo = next_take<L>(tape, ti, e);
-      const MatRef& hi = next_take<L>(tape, ti, e);
-      out = d_trunc<L>(out, lo, &hi, e, p, true, w, p0, msk);
+      const MatRef& lo = next_take<L, G>(tape, ti, e);
+      const MatRef& hi = next_take<L, G>(tape, ti, e);
+      out = d_trunc<L, G>(out, lo, &hi, e, p, true, w, p0, msk);
     }
-    store_sh<L>(y, n, e, out);
+    store_sh<L, G>(y, n, e, out);
   }
 }
 
@@ -802,36 +859,36 @@ __global__ void __launch_bounds__(128, MPX_MINB_L(L, MPX_LOG_MINB)) k_log_fused(
 // ReLU (nn.py:92-97): s = bit2a(gt(x, 0)) = bit2a(sign(0 - x)), y = s * x.
 // Also stores s (the converted sign) for the backward pass when s_out != 0.
 
-template <int L>
-__global__ void __launch_bounds__(128, MPX_MINB_L(L, MPX_CMP_MINB)) k_relu_fused(u64* __restrict__ y, u64* __restrict__ s_out,
+template <int L, int G>
+__global__ void __launch_bounds__(128, MPX_MINB_LG(L, G, MPX_CMP_MINB)) k_relu_fused(u64* __restrict__ y, u64* __restrict__ s_out,
                                                     const u64* __restrict__ xin, i64 n,
                                                     const __grid_constant__ Tape tape, FusedParams P) {
   const int w = P.w, p0 = P.p0;
   const u64 msk = ring_mask(w);
-  GRID_STRIDE(e, n) {
+  GRID_STRIDE_G(e, n) {
     int ti = 0;
     if (P.pf)
-      for (int i = 0; i < tape.n; ++i) prefetch_take<L>(tape.m[i], e);
-    const Sh<L> x = load_sh<L>(xin, n, e);
+      for (int i = 0; i < tape.n; ++i) prefetch_take<L, G>(tape.m[i], e);
+    const Sh<L> x = load_sh<L, G>(xin, n, e);
     Sh<L> diff;
 #pragma unroll
     for (int l = 0; l < L; ++l) diff.v[l] = (0ull - x.v[l]) & msk;   // public zero (party 0) - x
-    const Sh<L> bits = d_decompose<L>(diff, w, tape, ti, e, p0);
+    const Sh<L> bits = d_decompose<L, G>(diff, w, tape, ti, e, p0);
     Sh<L> sign;
 #pragma unroll
     for (int l = 0; l < L; ++l) sign.v[l] = (bits.v[l] >> (w - 1)) & 1ull;
-    const MatRef& tb = next_take<L>(tape, ti, e);
-    const u64 c = d_bit2a_open<L>(sign, 1, tb, e);
-    const Sh<L> sa = d_bit2a_get<L>(c, 0, 1, tb, e, p0, msk);
-    const Sh<L> out = d_mul<L>(sa, x, next_take<L>(tape, ti, e), e, p0, msk);
-    store_sh<L>(y, n, e, out);
-    if (s_out) store_sh<L>(s_out, n, e, sa);
+    const MatRef& tb = next_take<L, G>(tape, ti, e);
+    const u64 c = d_bit2a_open<L, G>(sign, 1, tb, e);
+    const Sh<L> sa = d_bit2a_get<L, G>(c, 0, 1, tb, e, p0, msk);
+    const Sh<L> out = d_mul<L, G>(sa, x, next_take<L, G>(tape, ti, e), e, p0, msk);
+    store_sh<L, G>(y, n, e, out);
+    if (s_out) store_sh<L, G>(s_out, n, e, sa);
   }
 }
 
 // One max_vec tournament level (derived.py:152-170) on pairs (u, v):
 // b = gt(u, v) (sign of v - u), s = bit2a(b), winner = v + s * (u - v).
-template <int L>
+template <int L, int G>
 __device__ __forceinline__ Sh<L> d_maxpair(const Sh<L>& u, const Sh<L>& v, const Tape& tape, int& ti, i64 e, int w,
                                            int p0, u64 msk) {
   Sh<L> diff, uv;
@@ -840,33 +897,33 @@ __device__ __forceinline__ Sh<L> d_maxpair(const Sh<L>& u, const Sh<L>& v, const
     diff.v[l] = (v.v[l] - u.v[l]) & msk;
     uv.v[l] = (u.v[l] - v.v[l]) & msk;
   }
-  const Sh<L> bits = d_decompose<L>(diff, w, tape, ti, e, p0);
+  const Sh<L> bits = d_decompose<L, G>(diff, w, tape, ti, e, p0);
   Sh<L> sign;
 #pragma unroll
   for (int l = 0; l < L; ++l) sign.v[l] = (bits.v[l] >> (w - 1)) & 1ull;
-  const MatRef& tb = next_take<L>(tape, ti, e);
-  const u64 c = d_bit2a_open<L>(sign, 1, tb, e);
-  const Sh<L> sa = d_bit2a_get<L>(c, 0, 1, tb, e, p0, msk);
-  const Sh<L> m = d_mul<L>(sa, uv, next_take<L>(tape, ti, e), e, p0, msk);
+  const MatRef& tb = next_take<L, G>(tape, ti, e);
+  const u64 c = d_bit2a_open<L, G>(sign, 1, tb, e);
+  const Sh<L> sa = d_bit2a_get<L, G>(c, 0, 1, tb, e, p0, msk);
+  const Sh<L> m = d_mul<L, G>(sa, uv, next_take<L, G>(tape, ti, e), e, p0, msk);
   Sh<L> out;
 #pragma unroll
   for (int l = 0; l < L; ++l) out.v[l] = (v.v[l] + m.v[l]) & msk;
   return out;
 }
 
-template <int L>
-__global__ void __launch_bounds__(128, MPX_MINB_L(L, MPX_CMP_MINB)) k_maxlevel_fused(u64* __restrict__ win, const u64* __restrict__ uin,
+template <int L, int G>
+__global__ void __launch_bounds__(128, MPX_MINB_LG(L, G, MPX_CMP_MINB)) k_maxlevel_fused(u64* __restrict__ win, const u64* __restrict__ uin,
                                                         const u64* __restrict__ vin, i64 n,
                                                         const __grid_constant__ Tape tape, FusedParams P) {
   const int w = P.w, p0 = P.p0;
   const u64 msk = ring_mask(w);
-  GRID_STRIDE(e, n) {
+  GRID_STRIDE_G(e, n) {
     int ti = 0;
     if (P.pf)
-      for (int i = 0; i < tape.n; ++i) prefetch_take<L>(tape.m[i], e);
-    const Sh<L> u = load_sh<L>(uin, n, e);
-    const Sh<L> v = load_sh<L>(vin, n, e);
-    store_sh<L>(win, n, e, d_maxpair<L>(u, v, tape, ti, e, w, p0, msk));
+      for (int i = 0; i < tape.n; ++i) prefetch_take<L, G>(tape.m[i], e);
+    const Sh<L> u = load_sh<L, G>(uin, n, e);
+    const Sh<L> v = load_sh<L, G>(vin, n, e);
+    store_sh<L, G>(win, n, e, d_maxpair<L, G>(u, v, tape, ti, e, w, p0, msk));
   }
 }
 
@@ -881,8 +938,8 @@ struct TourLevels {
   int nlev;
 };
 
-template <int L>
-__global__ void __launch_bounds__(256) k_maxtour_fused(u64* __restrict__ out, const u64* __restrict__ in, i64 rows,
+template <int L, int G>
+__global__ void __launch_bounds__(256 * G) k_maxtour_fused(u64* __restrict__ out, const u64* __restrict__ in, i64 rows,
                                                        int d0, const __grid_constant__ Tape tape,
                                                        const __grid_constant__ TourLevels lv, FusedParams P) {
   extern __shared__ u64 vals[];  // [L][d0]
@@ -891,45 +948,45 @@ __global__ void __launch_bounds__(256) k_maxtour_fused(u64* __restrict__ out, co
   for (i64 row = blockIdx.x; row < rows; row += gridDim.x) {
     for (int c = threadIdx.x; c < d0; c += blockDim.x)
 #pragma unroll
-      for (int l = 0; l < L; ++l) vals[l * d0 + c] = in[((i64)l * rows + row) * d0 + c];
+      for (int l = 0; l < L * G; ++l) vals[l * d0 + c] = in[((i64)l * rows + row) * d0 + c];
     __syncthreads();
     int d = d0;
+    // lanes j*G .. j*G+G-1 play pair j (blockDim >= G * d0 / 2), each for its L parties
+    const int j = threadIdx.x / G;
     for (int lev = 0; lev < lv.nlev; ++lev) {
       const int half = d / 2;
       const int rest = d - 2 * half;
-      // thread j plays pair j (blockDim >= d0 / 2)
-      const int j = threadIdx.x;
       Sh<L> win;
       if (j < half) {
         int ti = lv.start[lev];
         const i64 e = row * (i64)half + j;
         if (P.pf)
-          for (int i = lv.start[lev]; i < lv.start[lev + 1]; ++i) prefetch_take<L>(tape.m[i], e);
+          for (int i = lv.start[lev]; i < lv.start[lev + 1]; ++i) prefetch_take<L, G>(tape.m[i], e);
         Sh<L> u, v;
 #pragma unroll
         for (int l = 0; l < L; ++l) {
-          u.v[l] = vals[l * d0 + j];
-          v.v[l] = vals[l * d0 + half + j];
+          u.v[l] = vals[PI(l) * d0 + j];
+          v.v[l] = vals[PI(l) * d0 + half + j];
         }
-        win = d_maxpair<L>(u, v, tape, ti, e, w, p0, msk);
+        win = d_maxpair<L, G>(u, v, tape, ti, e, w, p0, msk);
       }
       Sh<L> rv;
-      if (threadIdx.x == 0 && rest)
+      if (j == 0 && rest)
 #pragma unroll
-        for (int l = 0; l < L; ++l) rv.v[l] = vals[l * d0 + 2 * half];
+        for (int l = 0; l < L; ++l) rv.v[l] = vals[PI(l) * d0 + 2 * half];
       __syncthreads();
       if (j < half)
 #pragma unroll
-        for (int l = 0; l < L; ++l) vals[l * d0 + j] = win.v[l];
-      if (threadIdx.x == 0 && rest)
+        for (int l = 0; l < L; ++l) vals[PI(l) * d0 + j] = win.v[l];
+      if (j == 0 && rest)
 #pragma unroll
-        for (int l = 0; l < L; ++l) vals[l * d0 + half] = rv.v[l];
+        for (int l = 0; l < L; ++l) vals[PI(l) * d0 + half] = rv.v[l];
       __syncthreads();
       d = half + rest;
     }
-    if (threadIdx.x == 0)
+    if (j == 0)
 #pragma unroll
-      for (int l = 0; l < L; ++l) out[(i64)l * rows + row] = vals[l * d0];
+      for (int l = 0; l < L; ++l) out[(i64)PI(l) * rows + row] = vals[PI(l) * d0];
     __syncthreads();
   }
 }
@@ -950,8 +1007,8 @@ struct SoftmaxSegs {
   int p, w32;
 };
 
-template <int L>
-__global__ void __launch_bounds__(256) k_softmax_fused(u64* __restrict__ eout, u64* __restrict__ rout,
+template <int L, int G>
+__global__ void __launch_bounds__(256 * G) k_softmax_fused(u64* __restrict__ eout, u64* __restrict__ rout,
                                                        const u64* __restrict__ in, i64 rows, int d0,
                                                        const __grid_constant__ Tape tape,
                                                        const __grid_constant__ SoftmaxSegs sg, FusedParams Pm,
@@ -959,26 +1016,26 @@ __global__ void __launch_bounds__(256) k_softmax_fused(u64* __restrict__ eout, u
   extern __shared__ u64 sm_vals[];  // [L][d0] tournament values, then [L][nwarps] row-sum partials
   const int p0 = Pm.p0;
   const u64 m64 = ring_mask(64), m32 = ring_mask(sg.w32);
-  const int j = threadIdx.x;
+  const int j = threadIdx.x / G;  // lanes j*G .. j*G+G-1 own column j, L parties each
   const int nw = (blockDim.x + 31) / 32;
-  u64* part = sm_vals + L * d0;
+  u64* part = sm_vals + L * G * d0;
   for (i64 row = blockIdx.x; row < rows; row += gridDim.x) {
     Sh<L> v;
     if (j < d0) {
       const i64 e = row * d0 + j;
 #pragma unroll
-      for (int l = 0; l < L; ++l) v.v[l] = in[((i64)l * rows + row) * d0 + j];
+      for (int l = 0; l < L; ++l) v.v[l] = in[((i64)PI(l) * rows + row) * d0 + j];
       if (sg.resc >= 0) {  // truncate(scale_fixed(x, log2 e), p) (derived.py:55-83)
         int ti = sg.resc;
-        const Sh<L> sc = sh_scale<L>(v, sg.log2e_p, 0ull, p0, m64);
-        const MatRef& lo = next_take<L>(tape, ti, e);
-        const MatRef& hi = next_take<L>(tape, ti, e);
-        v = d_trunc<L>(sc, lo, &hi, e, sg.p, true, 64, p0, m64);
+        const Sh<L> sc = sh_scale<L, G>(v, sg.log2e_p, 0ull, p0, m64);
+        const MatRef& lo = next_take<L, G>(tape, ti, e);
+        const MatRef& hi = next_take<L, G>(tape, ti, e);
+        v = d_trunc<L, G>(sc, lo, &hi, e, sg.p, true, 64, p0, m64);
       }
 #pragma unroll
       for (int l = 0; l < L; ++l) {
         v.v[l] &= m32;  // narrow (nn.py:68-74)
-        sm_vals[l * d0 + j] = v.v[l];
+        sm_vals[PI(l) * d0 + j] = v.v[l];
       }
     }
     __syncthreads();
@@ -992,22 +1049,22 @@ __global__ void __launch_bounds__(256) k_softmax_fused(u64* __restrict__ eout, u
         Sh<L> u, w;
 #pragma unroll
         for (int l = 0; l < L; ++l) {
-          u.v[l] = sm_vals[l * d0 + j];
-          w.v[l] = sm_vals[l * d0 + half + j];
+          u.v[l] = sm_vals[PI(l) * d0 + j];
+          w.v[l] = sm_vals[PI(l) * d0 + half + j];
         }
-        win = d_maxpair<L>(u, w, tape, ti, row * (i64)half + j, sg.w32, p0, m32);
+        win = d_maxpair<L, G>(u, w, tape, ti, row * (i64)half + j, sg.w32, p0, m32);
       }
       Sh<L> rv;
       if (j == 0 && rest)
 #pragma unroll
-        for (int l = 0; l < L; ++l) rv.v[l] = sm_vals[l * d0 + 2 * half];
+        for (int l = 0; l < L; ++l) rv.v[l] = sm_vals[PI(l) * d0 + 2 * half];
       __syncthreads();
       if (j < half)
 #pragma unroll
-        for (int l = 0; l < L; ++l) sm_vals[l * d0 + j] = win.v[l];
+        for (int l = 0; l < L; ++l) sm_vals[PI(l) * d0 + j] = win.v[l];
       if (j == 0 && rest)
 #pragma unroll
-        for (int l = 0; l < L; ++l) sm_vals[l * d0 + half] = rv.v[l];
+        for (int l = 0; l < L; ++l) sm_vals[PI(l) * d0 + half] = rv.v[l];
       __syncthreads();
       d = half + rest;
     }
@@ -1018,18 +1075,18 @@ __global__ void __launch_bounds__(256) k_softmax_fused(u64* __restrict__ eout, u
     if (j < d0) {
       Sh<L> sh;
 #pragma unroll
-      for (int l = 0; l < L; ++l) sh.v[l] = (v.v[l] - sm_vals[l * d0] + (l == p0 ? m32 : 0ull)) & m32;
+      for (int l = 0; l < L; ++l) sh.v[l] = (v.v[l] - sm_vals[PI(l) * d0] + (PI(l) == p0 ? m32 : 0ull)) & m32;
       int ti = sg.attexp;
-      ev = d_attexp<L>(sh, tape, ti, row * (i64)d0 + j, Pe);
+      ev = d_attexp<L, G>(sh, tape, ti, row * (i64)d0 + j, Pe);
 #pragma unroll
-      for (int l = 0; l < L; ++l) eout[((i64)l * rows + row) * d0 + j] = ev.v[l];
+      for (int l = 0; l < L; ++l) eout[((i64)PI(l) * rows + row) * d0 + j] = ev.v[l];
     }
 #pragma unroll
     for (int l = 0; l < L; ++l) {
       u64 s = ev.v[l];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if ((j & 31) == 0) part[l * nw + (j >> 5)] = s;
+      for (int o = 16; o >= G; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if ((threadIdx.x & 31) < G) part[PI(l) * nw + (threadIdx.x >> 5)] = s;
     }
     __syncthreads();
     if (j == 0) {
@@ -1037,13 +1094,13 @@ __global__ void __launch_bounds__(256) k_softmax_fused(u64* __restrict__ eout, u
 #pragma unroll
       for (int l = 0; l < L; ++l) {
         u64 s = 0;
-        for (int q = 0; q < nw; ++q) s += part[l * nw + q];
+        for (int q = 0; q < nw; ++q) s += part[PI(l) * nw + q];
         tot.v[l] = s & m64;
       }
       int ti = sg.recip;
-      const Sh<L> r = d_reciprocal<L>(tot, tape, ti, row, Pr);
+      const Sh<L> r = d_reciprocal<L, G>(tot, tape, ti, row, Pr);
 #pragma unroll
-      for (int l = 0; l < L; ++l) rout[(i64)l * rows + row] = r.v[l];
+      for (int l = 0; l < L; ++l) rout[(i64)PI(l) * rows + row] = r.v[l];
     }
     __syncthreads();
   }
@@ -1062,15 +1119,16 @@ extern "C" int mpx_softmax_fused(uint64_t* e_out, uint64_t* r_out, const uint64_
   CHECK_ARG(tp.n >= 1 && tp.n <= TAPE_MAX && sg.nlev >= 1 && sg.nlev <= 16 && FUSED_L_OK(Pm.L));
   if (rows == 0) return MPX_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  const int threads = max(32, ((d0 + 31) / 32) * 32);
+  const int gl = Pm.L == 8 ? 2 : 1;  // lanes per column: n = 8 splits its parties over two lanes
+  const int threads = max(32, ((gl * d0 + 31) / 32) * 32);
   const unsigned g = (unsigned)min(rows, (i64)(148 * 8));
   const size_t sm = (size_t)Pm.L * (d0 + threads / 32) * 8;
   switch (Pm.L) {
-    case 1: k_softmax_fused<1><<<g, threads, sm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr); break;
-    case 2: k_softmax_fused<2><<<g, threads, sm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr); break;
-    case 3: k_softmax_fused<3><<<g, threads, sm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr); break;
-    case 4: k_softmax_fused<4><<<g, threads, sm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr); break;
-    default: k_softmax_fused<8><<<g, threads, sm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr); break;
+    case 1: k_softmax_fused<1, 1><<<g, threads, sm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr); break;
+    case 2: k_softmax_fused<2, 1><<<g, threads, sm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr); break;
+    case 3: k_softmax_fused<3, 1><<<g, threads, sm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr); break;
+    case 4: k_softmax_fused<4, 1><<<g, threads, sm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr); break;
+    default: k_softmax_fused<4, 2><<<g, threads, sm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr); break;
   }
   return launch_status();
 }
@@ -1089,25 +1147,48 @@ extern "C" int mpx_maxtour_fused(uint64_t* y, const uint64_t* x, int64_t rows, i
   CHECK_ARG(tp.n >= 1 && tp.n <= TAPE_MAX && lv.nlev >= 1 && lv.nlev <= 16 && FUSED_L_OK(P.L));
   if (rows == 0) return MPX_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  const int threads = min(256, max(32, ((d0 / 2 + 31) / 32) * 32));
+  const int gl = P.L == 8 ? 2 : 1;  // lanes per pair: n = 8 splits its parties over two lanes
+  const int threads = min(256 * gl, max(32, ((gl * (d0 / 2) + 31) / 32) * 32));
   const unsigned g = (unsigned)min(rows, (i64)(148 * 16));
   const size_t sm = (size_t)P.L * d0 * 8;
   switch (P.L) {
-    case 1: k_maxtour_fused<1><<<g, threads, sm, s>>>(y, x, rows, d0, tp, lv, P); break;
-    case 2: k_maxtour_fused<2><<<g, threads, sm, s>>>(y, x, rows, d0, tp, lv, P); break;
-    case 3: k_maxtour_fused<3><<<g, threads, sm, s>>>(y, x, rows, d0, tp, lv, P); break;
-    case 4: k_maxtour_fused<4><<<g, threads, sm, s>>>(y, x, rows, d0, tp, lv, P); break;
-    default: k_maxtour_fused<8><<<g, threads, sm, s>>>(y, x, rows, d0, tp, lv, P); break;
+    case 1: k_maxtour_fused<1, 1><<<g, threads, sm, s>>>(y, x, rows, d0, tp, lv, P); break;
+    case 2: k_maxtour_fused<2, 1><<<g, threads, sm, s>>>(y, x, rows, d0, tp, lv, P); break;
+    case 3: k_maxtour_fused<3, 1><<<g, threads, sm, s>>>(y, x, rows, d0, tp, lv, P); break;
+    case 4: k_maxtour_fused<4, 1><<<g, threads, sm, s>>>(y, x, rows, d0, tp, lv, P); break;
+    default: k_maxtour_fused<4, 2><<<g, threads, sm, s>>>(y, x, rows, d0, tp, lv, P); break;
   }
   return launch_status();
 }
 
 // ---------------------------------------------------------------------------
 
-template <template <int> class KERN>
-struct Dispatch;
 
-#define DEFINE_LAUNCH(NAME, KFN)                                                                             \
+// n = 4 split over two lanes (2 parties each) or one lane per element: the
+// per-kernel default `def` is the faster of the two at 2^22 elements
+// (Reciprocal 4.89 vs 5.08 ms, Log 5.02 vs 5.46, ReLU 1.48 vs 1.60; Exp 3.98
+// vs 3.63 stays unsplit); MPX_SPLIT4=0/1 forces one layout for A/B runs.
+static bool split4(bool def) {
+  static const int v = [] {
+    const char* e = getenv("MPX_SPLIT4");
+    return e ? atoi(e) : -1;
+  }();
+  return v < 0 ? def : v != 0;
+}
+
+// n = 8: lanes per element (2: four parties per lane, 4: two), per-kernel
+// default `def` measured at 2^22 elements: Reciprocal 10.6 (4 lanes) vs 16.5
+// ms (2), Exp 8.3 vs 10.1, Log 10.2 vs 12.7, ReLU 4.9 vs 3.4 (2 lanes kept;
+// one lane per element: 33.6 / 26.1 / 28.6 / 3.9 ms); MPX_SPLIT8=2/4 forces.
+static int split8(int def) {
+  static const int v = [] {
+    const char* e = getenv("MPX_SPLIT8");
+    return e ? atoi(e) : 0;
+  }();
+  return v ? v : def;
+}
+
+#define DEFINE_LAUNCH(NAME, KFN, S4, S8)                                                                            \
   extern "C" int NAME(uint64_t* y, const uint64_t* x, int64_t n, const void* tape_host,                    \
                       const void* params_host, void* stream) {                                             \
     CHECK_ARG(y && x && n >= 0 && tape_host && params_host);                                               \
@@ -1118,18 +1199,24 @@ struct Dispatch;
     cudaStream_t s = (cudaStream_t)stream;                                                                 \
     const unsigned g = grid_for(n, 128);                                                                   \
     switch (P.L) {                                                                                         \
-      case 1: KFN<1><<<g, 128, 0, s>>>(y, x, n, tp, P); break;                                             \
-      case 2: KFN<2><<<g, 128, 0, s>>>(y, x, n, tp, P); break;                                             \
-      case 3: KFN<3><<<g, 128, 0, s>>>(y, x, n, tp, P); break;                                             \
-      case 4: KFN<4><<<g, 128, 0, s>>>(y, x, n, tp, P); break;                                             \
-      default: KFN<8><<<g, 128, 0, s>>>(y, x, n, tp, P); break;                                            \
+      case 1: KFN<1, 1><<<g, 128, 0, s>>>(y, x, n, tp, P); break;                                             \
+      case 2: KFN<2, 1><<<g, 128, 0, s>>>(y, x, n, tp, P); break;                                             \
+      case 3: KFN<3, 1><<<g, 128, 0, s>>>(y, x, n, tp, P); break;                                             \
+      case 4:                                                                                             \
+        if (split4(S4)) KFN<2, 2><<<grid_for(2 * n, 128), 128, 0, s>>>(y, x, n, tp, P);                                   \
+        else KFN<4, 1><<<g, 128, 0, s>>>(y, x, n, tp, P);                                                               \
+        break;                                             \
+      default:  /* n = 8: two lanes per element, 4 parties each */ \
+        if (split8(S8) == 4) KFN<2, 4><<<grid_for(4 * n, 128), 128, 0, s>>>(y, x, n, tp, P);                               \
+        else KFN<4, 2><<<grid_for(2 * n, 128), 128, 0, s>>>(y, x, n, tp, P);                                            \
+        break;                                            \
     }                                                                                                      \
     return launch_status();                                                                                \
   }
 
-DEFINE_LAUNCH(mpx_reciprocal_fused, k_reciprocal_fused)
+DEFINE_LAUNCH(mpx_reciprocal_fused, k_reciprocal_fused, true, 4)
 
-#define DEFINE_LAUNCH2(NAME, KFN, T1, T2)                                                                  \
+#define DEFINE_LAUNCH2(NAME, KFN, S4, S8, T1, T2)                                                                 \
   extern "C" int NAME(uint64_t* y, T1 a1, T2 a2, int64_t n, const void* tape_host, const void* params_host,   \
                       void* stream) {                                                                      \
     CHECK_ARG(y && a2 && n >= 0 && tape_host && params_host);                                              \
@@ -1140,22 +1227,28 @@ DEFINE_LAUNCH(mpx_reciprocal_fused, k_reciprocal_fused)
     cudaStream_t s = (cudaStream_t)stream;                                                                 \
     const unsigned g = grid_for(n, 128);                                                                   \
     switch (P.L) {                                                                                         \
-      case 1: KFN<1><<<g, 128, 0, s>>>(y, a1, a2, n, tp, P); break;                                        \
-      case 2: KFN<2><<<g, 128, 0, s>>>(y, a1, a2, n, tp, P); break;                                        \
-      case 3: KFN<3><<<g, 128, 0, s>>>(y, a1, a2, n, tp, P); break;                                        \
-      case 4: KFN<4><<<g, 128, 0, s>>>(y, a1, a2, n, tp, P); break;                                        \
-      default: KFN<8><<<g, 128, 0, s>>>(y, a1, a2, n, tp, P); break;                                       \
+      case 1: KFN<1, 1><<<g, 128, 0, s>>>(y, a1, a2, n, tp, P); break;                                        \
+      case 2: KFN<2, 1><<<g, 128, 0, s>>>(y, a1, a2, n, tp, P); break;                                        \
+      case 3: KFN<3, 1><<<g, 128, 0, s>>>(y, a1, a2, n, tp, P); break;                                        \
+      case 4:                                                                                             \
+        if (split4(S4)) KFN<2, 2><<<grid_for(2 * n, 128), 128, 0, s>>>(y, a1, a2, n, tp, P);                                   \
+        else KFN<4, 1><<<g, 128, 0, s>>>(y, a1, a2, n, tp, P);                                                               \
+        break;                                        \
+      default:  /* n = 8: two lanes per element, 4 parties each */ \
+        if (split8(S8) == 4) KFN<2, 4><<<grid_for(4 * n, 128), 128, 0, s>>>(y, a1, a2, n, tp, P);                               \
+        else KFN<4, 2><<<grid_for(2 * n, 128), 128, 0, s>>>(y, a1, a2, n, tp, P);                                            \
+        break;                                       \
     }                                                                                                      \
     return launch_status();                                                                                \
   }
 
 // y, s_out (may be NULL), x
-DEFINE_LAUNCH2(mpx_relu_fused, k_relu_fused, uint64_t*, const uint64_t*)
+DEFINE_LAUNCH2(mpx_relu_fused, k_relu_fused, true, 2, uint64_t*, const uint64_t*)
 // winner, u, v
-DEFINE_LAUNCH2(mpx_maxlevel_fused, k_maxlevel_fused, const uint64_t*, const uint64_t*)
-DEFINE_LAUNCH(mpx_exp_fused, k_exp_fused)
-DEFINE_LAUNCH(mpx_log_fused, k_log_fused)
-DEFINE_LAUNCH(mpx_attexp_fused, k_attexp_fused)
+DEFINE_LAUNCH2(mpx_maxlevel_fused, k_maxlevel_fused, true, 2, const uint64_t*, const uint64_t*)
+DEFINE_LAUNCH(mpx_exp_fused, k_exp_fused, false, 4)
+DEFINE_LAUNCH(mpx_log_fused, k_log_fused, true, 4)
+DEFINE_LAUNCH(mpx_attexp_fused, k_attexp_fused, false, 4)
 
 extern "C" int mpx_fused_tour_size(int64_t* levels) {
   *levels = sizeof(TourLevels);
