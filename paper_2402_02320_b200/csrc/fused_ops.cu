@@ -53,6 +53,10 @@ struct Tape {
 #ifndef MPX_MINB_SPLIT
 #define MPX_MINB_SPLIT 4
 #endif
+// four lanes per element (n = 8 Reciprocal / Exp): resident CTAs per SM
+#ifndef MPX_MINB_G4
+#define MPX_MINB_G4 6
+#endif
 #define MPX_MINB_LG(L, G, B2) ((G) > 1 && (L) >= 4 ? MPX_MINB_SPLIT : MPX_MINB_L(L, B2))
 
 #ifndef MPX_LOG_MINB
@@ -611,7 +615,7 @@ __device__ __forceinline__ Sh<L> d_reciprocal(const Sh<L>& x, const Tape& tape, 
 // Standalone kernel keeps its own copy of the body: through d_reciprocal it
 // compiles to 72 registers + spills at L = 2 (8.3 vs 7.9 ms at 2^24).
 template <int L, int G>
-__global__ void __launch_bounds__(128) k_reciprocal_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
+__global__ void __launch_bounds__(128, G >= 4 ? MPX_MINB_G4 : 1) k_reciprocal_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
                                                           const __grid_constant__ Tape tape, FusedParams P) {
   const int w = P.w, p = P.p, p0 = P.p0;
   const u64 msk = ring_mask(w);
@@ -668,7 +672,7 @@ __global__ void __launch_bounds__(128) k_reciprocal_fused(u64* __restrict__ y, c
 // Exponentiation, paper Alg. 2 (nonlinear.py:179-213)
 
 template <int L, int G>
-__global__ void __launch_bounds__(128) k_exp_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
+__global__ void __launch_bounds__(128, G >= 4 ? MPX_MINB_G4 : 1) k_exp_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
                                                    const __grid_constant__ Tape tape, FusedParams P) {
   const int w = P.w, p = P.p, p0 = P.p0, c = P.c, bias = P.bias;
   const u64 msk = ring_mask(w);

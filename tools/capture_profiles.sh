@@ -33,4 +33,12 @@ ncu --set full --clock-control none -k regex:k_gemm_limbs_tc --launch-skip 3 --l
     -o $OUT/gemm4096_full python tools/bench_gemm.py --iters 1 > $OUT/ncu_gemm.log 2>&1
 reduce gemm4096_full
 fi
+if [ "${1:-all}" = "all" ] || [ "$1" = "split8" ]; then
+# n = 8 sim-mode fused kernels with the party split (2^22 elements)
+python tools/bench_fused.py --parties 8 --elems 4194304 --kinds reciprocal,exp,log,relu > $OUT/bench_fused8.json 2>&1 || exit 1
+ncu --set full --clock-control none -k regex:"k_(reciprocal|exp|log|relu)_fused" \
+    -o $OUT/split8_full python tools/bench_fused.py --parties 8 --elems 4194304 --kinds reciprocal,exp,log,relu --reps 1 \
+    > $OUT/ncu_split8.log 2>&1
+reduce split8_full
+fi
 echo done
