@@ -53,7 +53,7 @@ struct Tape {
 #ifndef MPX_MINB_SPLIT
 #define MPX_MINB_SPLIT 4
 #endif
-// four lanes per element (n = 8 Reciprocal / Exp): resident CTAs per SM
+// split Reciprocal / Exp (n = 4 on two lanes, n = 8 on four): resident CTAs per SM
 #ifndef MPX_MINB_G4
 #define MPX_MINB_G4 6
 #endif
@@ -615,7 +615,7 @@ __device__ __forceinline__ Sh<L> d_reciprocal(const Sh<L>& x, const Tape& tape, 
 // Standalone kernel keeps its own copy of the body: through d_reciprocal it
 // compiles to 72 registers + spills at L = 2 (8.3 vs 7.9 ms at 2^24).
 template <int L, int G>
-__global__ void __launch_bounds__(128, G >= 4 ? MPX_MINB_G4 : 1) k_reciprocal_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
+__global__ void __launch_bounds__(128, G >= 2 ? MPX_MINB_G4 : 1) k_reciprocal_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
                                                           const __grid_constant__ Tape tape, FusedParams P) {
   const int w = P.w, p = P.p, p0 = P.p0;
   const u64 msk = ring_mask(w);
@@ -672,7 +672,7 @@ __global__ void __launch_bounds__(128, G >= 4 ? MPX_MINB_G4 : 1) k_reciprocal_fu
 // Exponentiation, paper Alg. 2 (nonlinear.py:179-213)
 
 template <int L, int G>
-__global__ void __launch_bounds__(128, G >= 4 ? MPX_MINB_G4 : 1) k_exp_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
+__global__ void __launch_bounds__(128, G >= 2 ? MPX_MINB_G4 : 1) k_exp_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
                                                    const __grid_constant__ Tape tape, FusedParams P) {
   const int w = P.w, p = P.p, p0 = P.p0, c = P.c, bias = P.bias;
   const u64 msk = ring_mask(w);
@@ -1170,8 +1170,9 @@ extern "C" int mpx_maxtour_fused(uint64_t* y, const uint64_t* x, int64_t rows, i
 
 // n = 4 split over two lanes (2 parties each) or one lane per element: the
 // per-kernel default `def` is the faster of the two at 2^22 elements
-// (Reciprocal 4.89 vs 5.08 ms, Log 5.02 vs 5.46, ReLU 1.48 vs 1.60; Exp 3.98
-// vs 3.63 stays unsplit); MPX_SPLIT4=0/1 forces one layout for A/B runs.
+// (Log 5.02 vs 5.46 ms, ReLU 1.48 vs 1.60; with the 80-register cap of the
+// split Reciprocal / Exp: 4.68 vs 5.08, 3.50 vs 3.63); MPX_SPLIT4=0/1 forces
+// one layout for A/B runs.
 static bool split4(bool def) {
   static const int v = [] {
     const char* e = getenv("MPX_SPLIT4");
@@ -1250,7 +1251,7 @@ DEFINE_LAUNCH(mpx_reciprocal_fused, k_reciprocal_fused, true, 4)
 DEFINE_LAUNCH2(mpx_relu_fused, k_relu_fused, true, 2, uint64_t*, const uint64_t*)
 // winner, u, v
 DEFINE_LAUNCH2(mpx_maxlevel_fused, k_maxlevel_fused, true, 2, const uint64_t*, const uint64_t*)
-DEFINE_LAUNCH(mpx_exp_fused, k_exp_fused, false, 4)
+DEFINE_LAUNCH(mpx_exp_fused, k_exp_fused, true, 4)
 DEFINE_LAUNCH(mpx_log_fused, k_log_fused, true, 4)
 DEFINE_LAUNCH(mpx_attexp_fused, k_attexp_fused, false, 4)
 
