@@ -57,6 +57,12 @@ struct Tape {
 #ifndef MPX_MINB_G4
 #define MPX_MINB_G4 6
 #endif
+// one lane per element: caps at the register counts ptxas picks unconstrained
+// (Reciprocal 56/80/96/146, Exp 47/72/128/168 for L = 1..4); a bare
+// minBlocks = 1 lets it take 255 and halves occupancy (Reciprocal 2^24 at
+// n = 2: 11.1 vs 8.0 ms)
+#define MPX_MINB_RCP1(L) ((L) <= 2 ? 6 : (L) == 3 ? 5 : 3)
+#define MPX_MINB_EXP1(L) ((L) <= 2 ? 6 : (L) == 3 ? 4 : 3)
 #define MPX_MINB_LG(L, G, B2) ((G) > 1 && (L) >= 4 ? MPX_MINB_SPLIT : MPX_MINB_L(L, B2))
 
 #ifndef MPX_LOG_MINB
@@ -615,7 +621,7 @@ __device__ __forceinline__ Sh<L> d_reciprocal(const Sh<L>& x, const Tape& tape, 
 // Standalone kernel keeps its own copy of the body: through d_reciprocal it
 // compiles to 72 registers + spills at L = 2 (8.3 vs 7.9 ms at 2^24).
 template <int L, int G>
-__global__ void __launch_bounds__(128, G >= 2 ? MPX_MINB_G4 : 1) k_reciprocal_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
+__global__ void __launch_bounds__(128, G >= 2 ? MPX_MINB_G4 : MPX_MINB_RCP1(L)) k_reciprocal_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
                                                           const __grid_constant__ Tape tape, FusedParams P) {
   const int w = P.w, p = P.p, p0 = P.p0;
   const u64 msk = ring_mask(w);
@@ -672,7 +678,7 @@ __global__ void __launch_bounds__(128, G >= 2 ? MPX_MINB_G4 : 1) k_reciprocal_fu
 // Exponentiation, paper Alg. 2 (nonlinear.py:179-213)
 
 template <int L, int G>
-__global__ void __launch_bounds__(128, G >= 2 ? MPX_MINB_G4 : 1) k_exp_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
+__global__ void __launch_bounds__(128, G >= 2 ? MPX_MINB_G4 : MPX_MINB_EXP1(L)) k_exp_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
                                                    const __grid_constant__ Tape tape, FusedParams P) {
   const int w = P.w, p = P.p, p0 = P.p0, c = P.c, bias = P.bias;
   const u64 msk = ring_mask(w);
@@ -1170,8 +1176,8 @@ extern "C" int mpx_maxtour_fused(uint64_t* y, const uint64_t* x, int64_t rows, i
 
 // n = 4 split over two lanes (2 parties each) or one lane per element: the
 // per-kernel default `def` is the faster of the two at 2^22 elements
-// (Log 5.02 vs 5.46 ms, ReLU 1.48 vs 1.60; with the 80-register cap of the
-// split Reciprocal / Exp: 4.68 vs 5.08, 3.50 vs 3.63); MPX_SPLIT4=0/1 forces
+// (Log 5.02 vs 5.51 ms, ReLU 1.48 vs 1.60; Reciprocal / Exp under the
+// 80-register cap 4.71 / 3.51 vs 4.75 / 3.51 unsplit); MPX_SPLIT4=0/1 forces
 // one layout for A/B runs.
 static bool split4(bool def) {
   static const int v = [] {
