@@ -378,6 +378,9 @@ __device__ __forceinline__ Sh<L> d_lmo(const Sh<L>& bits, int m, const Tape& tap
   if (m == 63) {
 #pragma unroll
     for (int s = 1; s < 63; s *= 2) d_lmo_level<L, G>(Y, 63, s, next_take<L, G>(tape, ti, e), e, p0);
+  } else if (m == 46) {  // Log's 2p window at the default p = 23
+#pragma unroll
+    for (int s = 1; s < 46; s *= 2) d_lmo_level<L, G>(Y, 46, s, next_take<L, G>(tape, ti, e), e, p0);
   } else {
 #pragma unroll
     for (int s = 1; s < 64; s *= 2)
