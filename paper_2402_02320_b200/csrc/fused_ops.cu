@@ -42,8 +42,8 @@ struct Tape {
 #endif
 
 // min resident CTAs per SM (register cap) by local party count: L <= 2 / 3 / 4
-#ifndef MPX_MINB3
-#define MPX_MINB3 MPX_CMP_MINB
+#ifndef MPX_MINB3  // L = 3 at 128 regs: ReLU 0.87 / max_vec 2.65 / Log 3.35 ms at 2^22 vs 1.04 / 2.75 / 3.60
+#define MPX_MINB3 4     // at 80 regs and 0.90 / 2.67 / 3.84 at 168; LeNet n = 3 step 1.564 vs 1.583 ms
 #endif
 #ifndef MPX_MINB4
 #define MPX_MINB4 MPX_CMP_MINB
