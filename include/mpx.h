@@ -90,6 +90,8 @@ int mpx_ring_add_rowvec(uint64_t* z, const uint64_t* b, int L, int64_t rows, int
 /* ---- fixed-point codec (ring.py:76-89) ---- */
 int mpx_encode(uint64_t* out, const double* in, int64_t n, int width, int frac, void* stream);
 int mpx_decode(double* out, const uint64_t* in, int64_t n, int width, int frac, void* stream);
+/* ring.to_signed (ring.py:65-73): centered int64 representative of Z_2^w words. */
+int mpx_to_signed(int64_t* out, const uint64_t* in, int64_t n, int width, void* stream);
 
 /* ---- openings: local-party reduction of one round (session.py:71-115) ----
  * Sim mode: the reduction over all L parties IS the opening. Party mode: the

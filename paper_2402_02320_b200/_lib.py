@@ -31,6 +31,7 @@ _SIGS = {
     "mpx_ring_rowdot": [_P, _P, _P, _I, _L, _L, _I, _P],
     "mpx_encode": [_P, _P, _L, _I, _I, _P],
     "mpx_decode": [_P, _P, _L, _I, _I, _P],
+    "mpx_to_signed": [_P, _P, _L, _I, _P],
     "mpx_open_sum": [_P, _P, _I, _L, _I, _P],
     "mpx_open_xor": [_P, _P, _I, _L, _P],
     "mpx_mask_sub": [_P, _P, _P, _L, _I, _L, _I, _P],
@@ -86,9 +87,11 @@ _SIGS = {
     "mpx_philox_bits": [_P, _U, _U, _L, _L, _P],
     "mpx_deal_share_arith": [_P, _L, _P, _U, _U, _L, _L, _I, _I, _I, _I, _P],
     "mpx_deal_share_bits": [_P, _L, _P, _U, _U, _L, _L, _I, _I, _I, _P],
-    "mpx_last_cuda_error": [],
-    "mpx_device_sm_count": [_I],
 }
+
+# entry points without a stream argument (bound with their own argtypes)
+_PLAIN = {"mpx_last_cuda_error": ([], ctypes.c_int), "mpx_device_sm_count": ([_I], ctypes.c_int),
+          "mpx_version": ([], ctypes.c_char_p), "mpx_cuda_error_string": ([_I], ctypes.c_char_p)}
 
 BITS_XOR, BITS_AND, BITS_AND_PUB, BITS_XOR_PUB, BITS_XOR_SHR1, BITS_PARITY, BITS_SIGNFOLD, \
     BITS_SHL_OR, BITS_BCAST_PUB = range(9)
@@ -102,7 +105,7 @@ _lib = None
 
 
 def exported_symbols() -> list[str]:
-    return sorted(list(_SIGS) + ["mpx_version", "mpx_cuda_error_string", "mpx_reciprocal_fused",
+    return sorted(list(_SIGS) + list(_PLAIN) + ["mpx_reciprocal_fused",
                                  "mpx_exp_fused", "mpx_log_fused", "mpx_fused_abi_sizes",
                                  "mpx_relu_fused", "mpx_maxlevel_fused", "mpx_attexp_fused",
                                  "mpx_maxtour_fused", "mpx_fused_tour_size", "mpx_softmax_fused",
@@ -121,10 +124,10 @@ def load() -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = ctypes.c_int
-    lib.mpx_version.restype = ctypes.c_char_p
-    lib.mpx_version.argtypes = []
-    lib.mpx_cuda_error_string.restype = ctypes.c_char_p
-    lib.mpx_cuda_error_string.argtypes = [_I]
+    for name, (args, res) in _PLAIN.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
     _lib = lib
     return lib
 
@@ -181,12 +184,33 @@ def call(name: str, *args) -> None:
         prof.append((name, args, ev0, ev1))
     else:
         rc = getattr(lib, name)(*args, stream_ptr())
-    if rc != 0:
-        if rc == -2:
-            code = lib.mpx_last_cuda_error()
-            msg = lib.mpx_cuda_error_string(code).decode()
-            raise MpxError(f"{name}: CUDA error {code} ({msg})")
-        raise MpxError(f"{name}: returned {rc} (invalid argument)")
+    check(name, rc)
+
+
+MPX_OK, MPX_ERR_ARG, MPX_ERR_CUDA = 0, -1, -2
+
+
+def check(name: str, rc: int) -> None:
+    """Map a libmpx return code to the Python error behaviour: MPX_ERR_ARG
+    (a shape / width / pointer precondition, the C side of the reference's
+    ValueError) and MPX_ERR_CUDA both raise ``MpxError``."""
+    if rc == MPX_OK:
+        return
+    lib = load()
+    if rc == MPX_ERR_CUDA:
+        code = lib.mpx_last_cuda_error()
+        msg = lib.mpx_cuda_error_string(code).decode()
+        raise MpxError(f"{name}: CUDA error {code} ({msg})")
+    raise MpxError(f"{name}: returned {rc} (invalid argument)")
+
+
+def device_sm_count(device: int | None = None) -> int:
+    """SM count of the device (148 on B200), queried through libmpx."""
+    dev = torch.cuda.current_device() if device is None else device
+    n = load().mpx_device_sm_count(dev)
+    if n <= 0:
+        raise MpxError(f"mpx_device_sm_count({dev}) failed ({n})")
+    return n
 
 
 def is_dry(*tensors) -> bool:

@@ -248,7 +248,19 @@ __global__ void k_encode(u64* __restrict__ out, const double* __restrict__ in, i
                          u64 msk) {
   GRID_STRIDE(i, n) {
     const double s = floor(in[i] * scale);
-    out[i] = ((u64)(long long)s) & msk;
+    // numpy's float64 -> int64 cast on x86 (cvttsd2si) yields INT64_MIN for
+    // NaN and for anything outside [-2^63, 2^63); CUDA's cvt saturates, so
+    // the reference's out-of-range encodings are reproduced explicitly.
+    const bool in_range = s >= -9223372036854775808.0 && s < 9223372036854775808.0;
+    out[i] = (in_range ? (u64)(long long)s : 0x8000000000000000ull) & msk;
+  }
+}
+
+// Centered representative in [-2^(w-1), 2^(w-1)) as int64 (ring.py:65-73).
+__global__ void k_to_signed(long long* __restrict__ out, const u64* __restrict__ in, i64 n, int w) {
+  GRID_STRIDE(i, n) {
+    const u64 v = in[i] & ring_mask(w);
+    out[i] = (w == 64 || !(v >> (w - 1))) ? (long long)v : (long long)(v | ~ring_mask(w));
   }
 }
 
@@ -273,6 +285,13 @@ extern "C" int mpx_encode(uint64_t* out, const double* in, int64_t n, int width,
   if (n == 0) return MPX_OK;
   k_encode<<<grid_for(n), MPX_THREADS, 0, (cudaStream_t)stream>>>(out, in, n, ldexp(1.0, frac),
                                                                    ring_mask(width));
+  return launch_status();
+}
+
+extern "C" int mpx_to_signed(int64_t* out, const uint64_t* in, int64_t n, int width, void* stream) {
+  CHECK_ARG(out && in && n >= 0 && width >= 1 && width <= 64);
+  if (n == 0) return MPX_OK;
+  k_to_signed<<<grid_for(n), MPX_THREADS, 0, (cudaStream_t)stream>>>((long long*)out, in, n, width);
   return launch_status();
 }
 

@@ -64,6 +64,13 @@ def decode(out_f64, x, n, width, frac):
     return out_f64
 
 
+def to_signed(out, x, n, width):
+    if _dry(out):
+        return out
+    call("mpx_to_signed", ptr(out), ptr(x), n, width)
+    return out
+
+
 # ---- openings ------------------------------------------------------------
 
 def open_sum(out, x, L, n, width):
@@ -364,7 +371,6 @@ def gemm(C, A, B, batch, M, K, N, sA, sB, sC, accumulate, width, simt=False):
 
 TC_MIN_MACS = 1 << 22   # below this the SIMT tiles win (launch + split overhead)
 TC_MAX_K = 16384        # exactness bound of the u32 diagonal accumulators (per CTA)
-NUM_SMS = 148
 
 
 def tc_eligible(M, K, N, width) -> bool:

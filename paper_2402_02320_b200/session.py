@@ -70,7 +70,7 @@ class _Session:
     @property
     def fused(self) -> bool:
         """All parties local and live: an opening needs no communication."""
-        return self.world == 1 and not self.dry
+        return self.world == 1 and not self.dry and self.L == self.n_parties
 
     def alloc(self, shape) -> torch.Tensor:
         return torch.empty(tuple(shape), dtype=torch.int64, device=self.device)
@@ -98,6 +98,9 @@ class _Session:
                 sum(bits_payload(t.numel()) for t in bits)
         self._account(payload)
         outs = [t for t, _ in arith] + list(bits)
+        if self.world == 1 and not self.dry and self.L != self.n_parties:
+            raise RuntimeError(f"parties {self.parties} of {self.n_parties} hold partial shares but the session "
+                               "has no communicator: pass a mesh or init torch.distributed")
         if self.world > 1 and not self.dry:
             outs = self._collective([t for t, _ in arith], list(bits))
         return outs
@@ -332,6 +335,9 @@ class PartySession(_Session):
         self.world = mesh.world if mesh is not None else 1
         if self.world not in (1, n_parties):
             raise ValueError("one rank per party expected")
+        if mesh is None and n_parties > 1 and store is not None and not self.dry:
+            raise RuntimeError(f"party {party} of {n_parties}: no communicator (mesh=None and torch.distributed "
+                               "is not initialised); openings would silently use the local share only")
 
     def _collective(self, arith, bits):
         outs = []

@@ -406,6 +406,10 @@ class GraphedStep:
     copied back inside the graph), intermediates come from the graph's private
     pool, and the dealer re-deals fresh material into the SAME store arrays
     before each replay (``device_store(..., into=store)``, outside the graph).
+
+    Construction runs one eager warm-up step (seed0 material) and then
+    restores the weights it updated, so the model is where the caller left
+    it: the first ``step()`` is the model's first update.
     """
 
     def __init__(self, session, model: Model, x: AShare, y: AShare, lr_shift: int, demands: dict,
@@ -418,7 +422,9 @@ class GraphedStep:
         self.x, self.y = x, y
         session.store = device_store(seed0, session.n_parties, demands, parties=session.parties,
                                      device=session.device, needs_bits=needs_bits)
-        # warm-up (eager) step: first-use work (attributes, schedules) happens here
+        # warm-up (eager) step: first-use work (attributes, schedules) happens
+        # here; the weights it updates are restored afterwards
+        snapshot = [b.values.clone() for b in self.bufs]
         side = torch.cuda.Stream(session.device)
         side.wait_stream(torch.cuda.current_stream(session.device))
         with torch.cuda.stream(side):
@@ -426,6 +432,9 @@ class GraphedStep:
             self._writeback()
         torch.cuda.current_stream(session.device).wait_stream(side)
         torch.cuda.synchronize(session.device)
+        for b, v in zip(self.bufs, snapshot):
+            b.values.copy_(v)
+        del snapshot
         session.store.rewind()
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
