@@ -9,9 +9,11 @@ Beaver matmul 4096^2) and the Simple-MLP training step (configs[0]).
   training step captured once in a CUDA graph and replayed.
 * N > 1 (torchrun, one rank per GPU): N parties, one per GPU, openings over
   NCCL, eager steps.
-* ``--impl reference``: the reference algorithm's CPU implementation (the
-  numpy oracle port under ``oracle/``; the Python reference itself cannot
-  travel to the GPU box) on all host cores, same metric, bounded sample.
+* ``--impl reference``: the UNMODIFIED reference package, pip-installed in
+  ``baseline/_ref`` (git-ignored, travels to the GPU box with the repo), run
+  through its own API by ``baseline/reference_arm.py`` on all host cores:
+  same metric and config, the batch split over the cores (the oracle port
+  under ``oracle/`` only if the install is missing).
 
 A step = one secure SGD step of LeNet (forward, softmax-CE, backward, update)
 on a batch of 128 synthetic 28x28 images, weights secret-shared. The trusted
@@ -141,6 +143,7 @@ def cpu_lenet_reference(n_parties: int, cores: int | None = None):
     """The oracle port of the reference algorithm, one LeNet training step of
     batch 128 split data-parallel over all host cores (one process per core,
     batch 128 / cores each; the slowest process bounds the step).
+    Fallback when the reference install (baseline/_ref) is missing.
     Returns (steps/s, cores, seconds, per-process batch)."""
     cores = cores or os.cpu_count() or 1
     per = max(1, BATCH // cores)
@@ -150,6 +153,98 @@ def cpu_lenet_reference(n_parties: int, cores: int | None = None):
         times = pool.map(_cpu_lenet_worker, [(per, n_parties, 11 + i) for i in range(procs)])
     secs = max(times) * (-(-procs // min(cores, procs)))
     return 1.0 / secs, min(cores, procs), secs, per
+
+
+def reference_arm():
+    """baseline/reference_arm.py when the unmodified reference is installed
+    in baseline/_ref (it travels to the GPU box with the repo), else None."""
+    try:
+        from baseline import reference_arm as ra
+    except ImportError:
+        return None
+    return ra if ra.available() is None else None
+
+
+def ref_train_sampler(ra, arch: str, n_parties: int, batch: int = BATCH, sample: int | None = None):
+    """Persistent workers running the reference's online SGD step on the
+    batch (or a ``sample`` of it) split over all host cores."""
+    cores = os.cpu_count() or 1
+    if arch == "lenet":
+        x, y = lenet_data(batch)
+        keys = (label_key("share:x"), label_key("share:y"))
+    else:
+        rng = np.random.default_rng(6)
+        x, y = rng.uniform(0, 1, (batch, 3, 32, 32)), np.eye(10)[rng.integers(0, 10, batch)]
+        keys = ([2, 1], [2, 2])
+    if sample is not None:
+        x, y = x[:sample], y[:sample]
+    procs = min(cores, len(x))
+    return ra.TrainWorkers(arch, x, y, n_parties, keys, procs), procs, len(x)
+
+
+def cpu_baselines(n_parties: int, with_sweep: bool, lenet_steps: int = 2) -> dict:
+    """cpu_baseline objects, measured on the host cores before CUDA starts:
+    the unmodified reference (kind "reference") when installed, else the
+    oracle port (kind "port")."""
+    cores = os.cpu_count() or 1
+    out = {}
+    ra = reference_arm()
+    if ra is None:
+        sps, c, secs, per = cpu_lenet_reference(n_parties)
+        out["lenet"] = {"value": sps, "unit": UNIT, "cores": c, "kind": "port",
+                        "sample": f"oracle/ numpy port of the reference algorithm: one LeNet train step of batch "
+                                  f"{BATCH} split over {c} processes (batch {per} each, n={n_parties}), online phase, "
+                                  f"{secs:.1f} s"}
+        if with_sweep:
+            rate, rc, rsecs = cpu_reference(1 << 20, 2)
+            out["reciprocal"] = {"value": rate, "unit": RECIP_UNIT, "cores": rc, "kind": "port",
+                                 "sample": f"online reciprocal on 2^20 elements (n=2), slowest {rsecs:.2f} s"}
+        return out
+    w, procs, nb = ref_train_sampler(ra, "lenet", n_parties)
+    secs = min(w.step() for _ in range(lenet_steps))
+    w.close()
+    out["lenet"] = {"value": 1.0 / secs, "unit": UNIT, "cores": cores, "kind": "reference",
+                    "sample": f"unmodified reference (baseline/_ref): one LeNet SGD step of batch {nb} split over "
+                              f"{procs} processes x {n_parties} party threads, online phase {secs:.2f} s"}
+    if not with_sweep:
+        return out
+    chunk = 1 << 13
+    for op in ("reciprocal", "exp", "log"):
+        tasks = []
+        for i in range(cores):
+            rng = np.random.default_rng(100 + i)
+            xs = workload_inputs(chunk) if op == "reciprocal" else (
+                rng.uniform(-16, 16, chunk) if op == "exp" else np.exp2(rng.uniform(-8, 8, chunk)))
+            tasks.append(("op", (op, encode_np(xs), 2, label_key(f"share:{op}"))))
+        secs = ra.parallel_online(tasks, cores)
+        out[op] = {"value": chunk * cores / secs, "unit": RECIP_UNIT, "cores": cores, "kind": "reference",
+                   "sample": f"unmodified reference: online {op} on {cores} x 2^13 elements (n=2) at once, "
+                             f"slowest {secs:.2f} s"}
+    rows, D = 4, 4096
+    rng = np.random.default_rng(7)
+    b = rng.integers(0, 1 << 64, (D, D), dtype=np.uint64)
+    tasks = [("matmul", (rng.integers(0, 1 << 64, (rows, D), dtype=np.uint64), b, 2,
+                         (label_key("share:mm_a"), label_key("share:mm_b")))) for _ in range(cores)]
+    secs = ra.parallel_online(tasks, cores)
+    macs = cores * rows * D * D
+    out["matmul"] = {"value": macs / secs / 1e9, "unit": "ring GMAC/s (X@Y, 4096^2 operands)", "cores": cores,
+                     "kind": "reference",
+                     "sample": f"unmodified reference: online batch_matmul of {cores} x ({rows}x4096 @ 4096x4096) "
+                               f"(n=2) at once, slowest {secs:.2f} s"}
+    x = np.random.default_rng(3).normal(0, 1, (128, 512))
+    secs = ra.parallel_online([("transformer_layer", (x, 2))], 1)
+    out["transformer"] = {"value": 6 * secs * 1e3, "unit": "ms (latency, lower is better)", "cores": 2,
+                          "kind": "reference",
+                          "sample": f"unmodified reference: online forward of 1 of the 6 encoder layers at seq 128 "
+                                    f"(n=2, 2 party threads) = {secs:.2f} s, x 6"}
+    for arch in ("alexnet", "vgg16m"):
+        w, procs, nb = ref_train_sampler(ra, arch, 2, sample=cores)
+        secs = w.step()
+        w.close()
+        out[arch] = {"value": (nb / BATCH) / secs, "unit": UNIT, "cores": cores, "kind": "reference",
+                     "sample": f"unmodified reference: online SGD step on {nb} of the {BATCH} images "
+                               f"({procs} processes x 2 party threads) = {secs:.2f} s, scaled to batch {BATCH}"}
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -738,19 +833,11 @@ def run_b200(args, group=None):
     group = group or DistGroup(torch, dist)
     world, rank, local = group.world, group.rank, group.local
     n_parties = 3 if world == 1 else world
-    cpu = cpu_recip = None
+    cpu_all = {}
     if rank == 0 and world == 1 and not args.no_cpu:
         # before CUDA initialisation: the pools fork numpy-only workers
-        sps, cores, secs, per = cpu_lenet_reference(n_parties)
-        cpu = {"value": sps, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"oracle/ numpy port of the reference algorithm: one LeNet train step of batch {BATCH} "
-                         f"split over {cores} processes (batch {per} each, n={n_parties}), online phase, "
-                         f"{secs:.1f} s"}
-        if not args.no_sweep:
-            rate, rcores, rsecs = cpu_reference(args.cpu_sample, 2)
-            cpu_recip = {"value": rate, "unit": RECIP_UNIT, "cores": rcores, "kind": "port",
-                         "sample": f"online reciprocal on {args.cpu_sample} elements (n=2) over {rcores} "
-                                   f"processes, slowest {rsecs:.2f} s"}
+        cpu_all = cpu_baselines(n_parties, with_sweep=not args.no_sweep)
+    cpu = cpu_all.get("lenet")
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
@@ -880,7 +967,6 @@ def run_b200(args, group=None):
                 return SimSession(2, store, device=dev)
             return PartySession(rank, n_parties, group.comm(), store, device=dev)
         sweep["reciprocal"] = reciprocal_entry(torch, G, mk2, ps, np_, dev, group, 3, 2)
-        sweep["reciprocal"]["cpu_baseline"] = cpu_recip
         for nm in ("exp", "log", "matmul"):
             sweep[nm] = sweep_entry(torch, G, mk2, ps, np_, dev, nm)
         if int8_pk:
@@ -897,6 +983,10 @@ def run_b200(args, group=None):
                 sweep[f"{arch}_train"] = cifar_entry(torch, dev, arch, 3, 2)
             if not getattr(args, "no_party_sweep", False):
                 sweep["party_scaling_sim"] = party_scaling(torch, G, dev, group)
+        for nm, key in (("reciprocal", "reciprocal"), ("exp", "exp"), ("log", "log"), ("matmul", "matmul"),
+                        ("transformer", "transformer"), ("alexnet_train", "alexnet"), ("vgg16m_train", "vgg16m")):
+            if nm in sweep:
+                sweep[nm]["cpu_baseline"] = cpu_all.get(key)
 
     line = None
     if rank == 0:
@@ -935,27 +1025,45 @@ def run_b200(args, group=None):
 
 
 def run_reference(args):
+    """The reference arm: the unmodified reference (baseline/_ref) on all host
+    cores, same metric / config / unit as the B200 arm; each step = one online
+    LeNet SGD step of batch 128 split over the cores (dry run + dealer once
+    per worker, outside the timed region). Falls back to the oracle port when
+    the reference install is missing."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     n_parties = 3 if world == 1 else world
-    rates, cores, secs, per = [], None, None, None
-    for step in range(args.warmup + args.steps):
-        sps, cores, secs, per = cpu_lenet_reference(n_parties)
-        if step >= args.warmup:
-            rates.append(sps)
+    ra = reference_arm()
+    rates = []
+    if ra is not None:
+        w, procs, nb = ref_train_sampler(ra, "lenet", n_parties)
+        for step in range(args.warmup + args.steps):
+            secs = w.step()
+            if step >= args.warmup:
+                rates.append(1.0 / secs)
+        w.close()
+        cores = os.cpu_count() or 1
+        kind, mode = "reference", "CPU: unmodified reference package (baseline/_ref), all host cores"
+        sample = (f"each step: batch {nb} split over {procs} processes x {n_parties} party threads (InProcHub), "
+                  f"online phase; dry run + reference dealer once per process")
+    else:
+        cores = per = None
+        for step in range(args.warmup + args.steps):
+            sps, cores, secs, per = cpu_lenet_reference(n_parties)
+            if step >= args.warmup:
+                rates.append(sps)
+        kind, mode = "port", "CPU: reference algorithm (numpy oracle port; baseline/_ref missing), all host cores"
+        sample = f"each step: batch {BATCH} split over {cores} processes (batch {per} each), online phase"
     value = float(np.mean(rates))
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 / value, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64 (Z_2^64 fixed point, p=23)", "impl": "reference",
             "data": "synthetic: x ~ U(0,1) 128x1x28x28, uniform labels; Kaiming-init secret weights",
             "config": {"workload": "configs[1]: secure LeNet training step", "parties": n_parties,
-                       "batch": BATCH, "frac": FRAC, "ring_width": WIDTH,
-                       "mode": "CPU: reference algorithm (numpy oracle port), all host cores"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"each step: batch {BATCH} split over {cores} processes (batch {per} "
-                                       f"each), online phase"},
+                       "batch": BATCH, "frac": FRAC, "ring_width": WIDTH, "mode": mode},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
