@@ -706,7 +706,7 @@ def mlp_entry(torch, dev, steps, warmup):
                           LR_SHIFT, c.demands, c.needs_bits, seed0=70)
     times = []
     for t in range(warmup + steps):
-        device_store(71 + t, n, c.demands, device=dev, needs_bits=c.needs_bits, into=s.store)
+        g.dealer.redeal(71 + t)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -741,10 +741,12 @@ def cifar_entry(torch, dev, arch, steps, warmup, n=2):
                           LR_SHIFT, c.demands, c.needs_bits, seed0=80)
     times, deal = [], []
     for t in range(warmup + steps):
-        t0 = time.perf_counter()
-        device_store(81 + t, n, c.demands, device=dev, needs_bits=c.needs_bits, into=s.store)
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record()
+        g.dealer.redeal(81 + t)
+        d1.record()
         torch.cuda.synchronize()
-        deal.append(1e3 * (time.perf_counter() - t0))
+        deal.append(d0.elapsed_time(d1))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         g.graph.replay()
@@ -777,7 +779,7 @@ def transformer_entry(torch, dev, steps, warmup, n=2):
     g = GraphedInference(s, m, s.share_fixed(x, WIDTH, 14, [5, 5]), c.demands, c.needs_bits, seed0=90)
     times = []
     for t in range(warmup + steps):
-        device_store(91 + t, n, c.demands, device=dev, needs_bits=c.needs_bits, into=s.store)
+        g.dealer.redeal(91 + t)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -871,8 +873,11 @@ def run_b200(args, group=None):
                                   needs_bits=counter.needs_bits)
 
     def redeal(seed):
-        device_store(seed, n_parties, counter.demands, parties=parties, device=dev,
-                     needs_bits=counter.needs_bits, into=sess.store)
+        if graph is not None:          # the dealer's own CUDA graph (DealerGraph)
+            graph.dealer.redeal(seed)
+        else:
+            device_store(seed, n_parties, counter.demands, parties=parties, device=dev,
+                         needs_bits=counter.needs_bits, into=sess.store)
 
     def one_step():
         if graph is not None:
@@ -892,11 +897,14 @@ def run_b200(args, group=None):
     clocks.start()
     step_ms, deal_ms, t_window = [], [], [None, None]
     for step in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
-        torch.cuda.synchronize()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record()
         redeal(100 + step)
+        d1.record()
         torch.cuda.synchronize()
-        deal_ms.append(1e3 * (time.perf_counter() - t0))
+        deal_ms.append((d0.elapsed_time(d1), 1e3 * (time.perf_counter() - t0)))
         group.barrier()
         torch.cuda.synchronize()
         if step >= args.warmup and t_window[0] is None:
@@ -1014,7 +1022,13 @@ def run_b200(args, group=None):
             "clocks": clk,
             "roofline": roofline,
             "rounds_per_step": sd.metrics.total.rounds,
-            "dealer_ms_per_step": float(np.median(deal_ms[args.warmup:])),
+            "dealer_ms_per_step": float(np.median([d[0] for d in deal_ms[args.warmup:]])),
+            "dealer": {"gpu_ms_per_step": float(np.median([d[0] for d in deal_ms[args.warmup:]])),
+                       "host_wall_ms_per_step": float(np.median([d[1] for d in deal_ms[args.warmup:]])),
+                       "how": ("one CUDA graph of the whole re-deal (keys in device slots), CUDA events"
+                               if world == 1 else "device_store(into=...) per step, CUDA events"),
+                       "material_GB": sum(t.numel() * t.element_size() for d in sess.store._arrays.values()
+                                          for t in d.values()) / 1e9},
             "loss_first_last": losses,
             "kernels": _kernel_table(per),
             "cpu_baseline": cpu,

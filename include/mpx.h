@@ -392,6 +392,17 @@ int mpx_deal_share_arith(uint64_t* out, int64_t out_ps, const uint64_t* secret, 
 int mpx_deal_share_bits(uint64_t* out, int64_t out_ps, const uint64_t* secret_words, uint64_t k0,
                         uint64_t k1, int64_t u32_base, int64_t count, int n, int p_lo, int L,
                         void* stream);
+/* The same four draws with the Philox key read from a device slot
+ * dkey[0..1] at launch: a CUDA graph of a whole re-deal replays with fresh
+ * keys written into the slots (preprocessing.py:121-125 keys per seed). */
+int mpx_philox_elems_dk(uint64_t* out, const uint64_t* dkey, int64_t u32_off, int64_t count, int width,
+                        void* stream);
+int mpx_philox_bits_dk(uint64_t* out_words, const uint64_t* dkey, int64_t u32_off, int64_t count,
+                       void* stream);
+int mpx_deal_share_arith_dk(uint64_t* out, int64_t out_ps, const uint64_t* secret, const uint64_t* dkey,
+                            int64_t u32_base, int64_t count, int n, int p_lo, int L, int width, void* stream);
+int mpx_deal_share_bits_dk(uint64_t* out, int64_t out_ps, const uint64_t* secret_words, const uint64_t* dkey,
+                           int64_t u32_base, int64_t count, int n, int p_lo, int L, void* stream);
 
 #ifdef __cplusplus
 }

@@ -87,6 +87,10 @@ _SIGS = {
     "mpx_philox_bits": [_P, _U, _U, _L, _L, _P],
     "mpx_deal_share_arith": [_P, _L, _P, _U, _U, _L, _L, _I, _I, _I, _I, _P],
     "mpx_deal_share_bits": [_P, _L, _P, _U, _U, _L, _L, _I, _I, _I, _P],
+    "mpx_philox_elems_dk": [_P, _P, _L, _L, _I, _P],
+    "mpx_philox_bits_dk": [_P, _P, _L, _L, _P],
+    "mpx_deal_share_arith_dk": [_P, _L, _P, _P, _L, _L, _I, _I, _I, _I, _P],
+    "mpx_deal_share_bits_dk": [_P, _L, _P, _P, _L, _L, _I, _I, _I, _P],
 }
 
 # entry points without a stream argument (bound with their own argtypes)

@@ -74,7 +74,17 @@ __device__ __forceinline__ void draw_bits(u64 k0, u64 k1, i64 q, u64 (&v)[DEAL_W
   }
 }
 
-__global__ void k_philox_elems(u64* __restrict__ out, u64 k0, u64 k1, i64 u32_off, i64 count, u64 msk) {
+// Keys by value, or (dk != nullptr) from a device key slot {k0, k1}: the
+// dealer's CUDA graph replays every launch with the slot rewritten per seed.
+#define LOAD_DKEY()        \
+  if (dk != nullptr) {     \
+    k0 = __ldg(dk);        \
+    k1 = __ldg(dk + 1);    \
+  }
+
+__global__ void k_philox_elems(u64* __restrict__ out, u64 k0, u64 k1, const u64* __restrict__ dk, i64 u32_off,
+                               i64 count, u64 msk) {
+  LOAD_DKEY();
   const i64 groups = (count + DEAL_E - 1) / DEAL_E;
   GRID_STRIDE(g, groups) {
     u64 v[DEAL_E];
@@ -87,7 +97,9 @@ __global__ void k_philox_elems(u64* __restrict__ out, u64 k0, u64 k1, i64 u32_of
   }
 }
 
-__global__ void k_philox_bits(u64* __restrict__ out, u64 k0, u64 k1, i64 u32_off, i64 count) {
+__global__ void k_philox_bits(u64* __restrict__ out, u64 k0, u64 k1, const u64* __restrict__ dk, i64 u32_off,
+                              i64 count) {
+  LOAD_DKEY();
   const i64 nw = (count + 63) >> 6;
   const i64 groups = (nw + DEAL_W - 1) / DEAL_W;
   GRID_STRIDE(g, groups) {
@@ -103,30 +115,53 @@ __global__ void k_philox_bits(u64* __restrict__ out, u64 k0, u64 k1, i64 u32_off
   }
 }
 
-extern "C" int mpx_philox_elems(uint64_t* out, uint64_t k0, uint64_t k1, int64_t u32_off, int64_t count,
-                                int width, void* stream) {
+static int philox_elems(uint64_t* out, uint64_t k0, uint64_t k1, const uint64_t* dk, int64_t u32_off,
+                        int64_t count, int width, void* stream) {
   CHECK_ARG(out && u32_off >= 0 && count >= 0 && width >= 1 && width <= 64);
   if (count == 0) return MPX_OK;
   k_philox_elems<<<grid_for((count + DEAL_E - 1) / DEAL_E), MPX_THREADS, 0, (cudaStream_t)stream>>>(
-      out, k0, k1, u32_off, count, ring_mask(width));
+      out, k0, k1, dk, u32_off, count, ring_mask(width));
   return launch_status();
+}
+
+static int philox_bits(uint64_t* out_words, uint64_t k0, uint64_t k1, const uint64_t* dk, int64_t u32_off,
+                       int64_t count, void* stream) {
+  CHECK_ARG(out_words && u32_off >= 0 && count >= 0);
+  if (count == 0) return MPX_OK;
+  k_philox_bits<<<grid_for(((count + 63) / 64 + DEAL_W - 1) / DEAL_W), MPX_THREADS, 0, (cudaStream_t)stream>>>(
+      out_words, k0, k1, dk, u32_off, count);
+  return launch_status();
+}
+
+extern "C" int mpx_philox_elems(uint64_t* out, uint64_t k0, uint64_t k1, int64_t u32_off, int64_t count,
+                                int width, void* stream) {
+  return philox_elems(out, k0, k1, nullptr, u32_off, count, width, stream);
 }
 
 extern "C" int mpx_philox_bits(uint64_t* out_words, uint64_t k0, uint64_t k1, int64_t u32_off,
                                int64_t count, void* stream) {
-  CHECK_ARG(out_words && u32_off >= 0 && count >= 0);
-  if (count == 0) return MPX_OK;
-  k_philox_bits<<<grid_for(((count + 63) / 64 + DEAL_W - 1) / DEAL_W), MPX_THREADS, 0, (cudaStream_t)stream>>>(
-      out_words, k0, k1, u32_off, count);
-  return launch_status();
+  return philox_bits(out_words, k0, k1, nullptr, u32_off, count, stream);
+}
+
+extern "C" int mpx_philox_elems_dk(uint64_t* out, const uint64_t* dkey, int64_t u32_off, int64_t count, int width,
+                                   void* stream) {
+  CHECK_ARG(dkey);
+  return philox_elems(out, 0, 0, dkey, u32_off, count, width, stream);
+}
+
+extern "C" int mpx_philox_bits_dk(uint64_t* out_words, const uint64_t* dkey, int64_t u32_off, int64_t count,
+                                  void* stream) {
+  CHECK_ARG(dkey);
+  return philox_bits(out_words, 0, 0, dkey, u32_off, count, stream);
 }
 
 // Party p < n-1: draw p ; last party: secret - sum of the n-1 draws. One
 // thread covers a group for every local party, so each draw is generated
 // once even when the last party is local too (sim mode: n-1 draws, not 2(n-1)).
 __global__ void k_deal_share_arith(u64* __restrict__ out, i64 out_ps, const u64* __restrict__ secret,
-                                   u64 k0, u64 k1, i64 u32_base, i64 count, int n, int p_lo, int L,
-                                   u64 msk) {
+                                   u64 k0, u64 k1, const u64* __restrict__ dk, i64 u32_base, i64 count, int n,
+                                   int p_lo, int L, u64 msk) {
+  LOAD_DKEY();
   const i64 groups = (count + DEAL_E - 1) / DEAL_E;
   const i64 draw_u32 = 2 * count;
   const bool last_local = p_lo + L == n;
@@ -163,7 +198,9 @@ __global__ void k_deal_share_arith(u64* __restrict__ out, i64 out_ps, const u64*
 }
 
 __global__ void k_deal_share_bits(u64* __restrict__ out, i64 out_ps, const u64* __restrict__ secret,
-                                  u64 k0, u64 k1, i64 u32_base, i64 count, int n, int p_lo, int L) {
+                                  u64 k0, u64 k1, const u64* __restrict__ dk, i64 u32_base, i64 count, int n,
+                                  int p_lo, int L) {
+  LOAD_DKEY();
   const i64 nw = (count + 63) >> 6;
   const i64 groups = (nw + DEAL_W - 1) / DEAL_W;
   const i64 draw_u32 = (count + 3) >> 2;
@@ -202,27 +239,53 @@ __global__ void k_deal_share_bits(u64* __restrict__ out, i64 out_ps, const u64* 
   }
 }
 
-extern "C" int mpx_deal_share_arith(uint64_t* out, int64_t out_ps, const uint64_t* secret, uint64_t k0,
-                                    uint64_t k1, int64_t u32_base, int64_t count, int n, int p_lo, int L,
-                                    int width, void* stream) {
+static int deal_share_arith(uint64_t* out, int64_t out_ps, const uint64_t* secret, uint64_t k0, uint64_t k1,
+                            const uint64_t* dk, int64_t u32_base, int64_t count, int n, int p_lo, int L, int width,
+                            void* stream) {
   CHECK_ARG(out && u32_base >= 0 && count >= 0 && n >= 1 && p_lo >= 0 && L >= 1 && p_lo + L <= n &&
             width >= 1 && width <= 64);
   CHECK_ARG(secret || p_lo + L < n);
   if (count == 0) return MPX_OK;
   const i64 groups = (count + DEAL_E - 1) / DEAL_E;
   k_deal_share_arith<<<grid_for(groups), MPX_THREADS, 0, (cudaStream_t)stream>>>(
-      out, out_ps, secret, k0, k1, u32_base, count, n, p_lo, L, ring_mask(width));
+      out, out_ps, secret, k0, k1, dk, u32_base, count, n, p_lo, L, ring_mask(width));
   return launch_status();
 }
 
-extern "C" int mpx_deal_share_bits(uint64_t* out, int64_t out_ps, const uint64_t* secret_words,
-                                   uint64_t k0, uint64_t k1, int64_t u32_base, int64_t count, int n,
-                                   int p_lo, int L, void* stream) {
+static int deal_share_bits(uint64_t* out, int64_t out_ps, const uint64_t* secret_words, uint64_t k0, uint64_t k1,
+                           const uint64_t* dk, int64_t u32_base, int64_t count, int n, int p_lo, int L,
+                           void* stream) {
   CHECK_ARG(out && u32_base >= 0 && count >= 0 && n >= 1 && p_lo >= 0 && L >= 1 && p_lo + L <= n);
   CHECK_ARG(secret_words || p_lo + L < n);
   if (count == 0) return MPX_OK;
   const i64 groups = ((count + 63) / 64 + DEAL_W - 1) / DEAL_W;
   k_deal_share_bits<<<grid_for(groups), MPX_THREADS, 0, (cudaStream_t)stream>>>(
-      out, out_ps, secret_words, k0, k1, u32_base, count, n, p_lo, L);
+      out, out_ps, secret_words, k0, k1, dk, u32_base, count, n, p_lo, L);
   return launch_status();
+}
+
+extern "C" int mpx_deal_share_arith(uint64_t* out, int64_t out_ps, const uint64_t* secret, uint64_t k0,
+                                    uint64_t k1, int64_t u32_base, int64_t count, int n, int p_lo, int L,
+                                    int width, void* stream) {
+  return deal_share_arith(out, out_ps, secret, k0, k1, nullptr, u32_base, count, n, p_lo, L, width, stream);
+}
+
+extern "C" int mpx_deal_share_bits(uint64_t* out, int64_t out_ps, const uint64_t* secret_words,
+                                   uint64_t k0, uint64_t k1, int64_t u32_base, int64_t count, int n,
+                                   int p_lo, int L, void* stream) {
+  return deal_share_bits(out, out_ps, secret_words, k0, k1, nullptr, u32_base, count, n, p_lo, L, stream);
+}
+
+extern "C" int mpx_deal_share_arith_dk(uint64_t* out, int64_t out_ps, const uint64_t* secret, const uint64_t* dkey,
+                                       int64_t u32_base, int64_t count, int n, int p_lo, int L, int width,
+                                       void* stream) {
+  CHECK_ARG(dkey);
+  return deal_share_arith(out, out_ps, secret, 0, 0, dkey, u32_base, count, n, p_lo, L, width, stream);
+}
+
+extern "C" int mpx_deal_share_bits_dk(uint64_t* out, int64_t out_ps, const uint64_t* secret_words,
+                                      const uint64_t* dkey, int64_t u32_base, int64_t count, int n, int p_lo, int L,
+                                      void* stream) {
+  CHECK_ARG(dkey);
+  return deal_share_bits(out, out_ps, secret_words, 0, 0, dkey, u32_base, count, n, p_lo, L, stream);
 }

@@ -81,27 +81,50 @@ __device__ __forceinline__ void pf_l2(const void* p) { asm volatile("prefetch.gl
 // (a sum or XOR over the parties) is finished with a butterfly over the
 // group; both lanes of a group run the same element, so the same control
 // path. G = 1 is the one-lane-per-element layout.
+//
+// Bit 4 of the G template argument (G | MPX_STAGED) marks a kernel whose
+// material has been staged into shared memory (k_softmax_fused's staged
+// variant): material reads then use generic loads instead of the global-only
+// __ldcs / __ldg. GS(G) is the lane-group size.
+#define MPX_STAGED 16
+#define GS(G) ((G) & 15)
+
 template <int L, int G>
 __device__ __forceinline__ int pbase() {
-  return G == 1 ? 0 : (int)(threadIdx.x & (G - 1)) * L;
+  return GS(G) == 1 ? 0 : (int)(threadIdx.x & (GS(G) - 1)) * L;
 }
 #define PI(l) ((l) + pbase<L, G>())
 
 template <int G>
 __device__ __forceinline__ unsigned gmask() {
-  return G == 1 ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(unsigned)(G - 1)));
+  return GS(G) == 1 ? 0xffffffffu : (((1u << GS(G)) - 1u) << ((threadIdx.x & 31) & ~(unsigned)(GS(G) - 1)));
 }
 template <int G>
 __device__ __forceinline__ u64 gsum(u64 v) {
 #pragma unroll
-  for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(gmask<G>(), v, o);
+  for (int o = 1; o < GS(G); o <<= 1) v += __shfl_xor_sync(gmask<G>(), v, o);
   return v;
 }
 template <int G>
 __device__ __forceinline__ u64 gxor(u64 v) {
 #pragma unroll
-  for (int o = 1; o < G; o <<= 1) v ^= __shfl_xor_sync(gmask<G>(), v, o);
+  for (int o = 1; o < GS(G); o <<= 1) v ^= __shfl_xor_sync(gmask<G>(), v, o);
   return v;
+}
+
+// material loads: streaming (evict-first) / read-only cached from HBM, or
+// plain generic loads when the kernel staged its material in shared memory
+template <int G>
+__device__ __forceinline__ u64 ldm(const u64* p) {
+  if constexpr ((G & MPX_STAGED) != 0) return *p; else return __ldcs(p);
+}
+template <int G>
+__device__ __forceinline__ u64 ldr(const u64* p) {
+  if constexpr ((G & MPX_STAGED) != 0) return *p; else return __ldg(p);
+}
+template <int G>
+__device__ __forceinline__ ulonglong2 ldr2(const ulonglong2* p) {
+  if constexpr ((G & MPX_STAGED) != 0) return *p; else return __ldg(p);
 }
 
 // element loop with G lanes per element
@@ -188,8 +211,8 @@ __device__ __forceinline__ Sh<L> d_mul(const Sh<L>& x, const Sh<L>& y, const Mat
   u64 d = 0, f = 0;
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    a[l] = __ldcs(t.p0 + PI(l) * t.ps0 + e);
-    b[l] = __ldcs(t.p1 + PI(l) * t.ps1 + e);
+    a[l] = ldm<G>(t.p0 + PI(l) * t.ps0 + e);
+    b[l] = ldm<G>(t.p1 + PI(l) * t.ps1 + e);
     d += x.v[l] - a[l];
     f += y.v[l] - b[l];
   }
@@ -198,7 +221,7 @@ __device__ __forceinline__ Sh<L> d_mul(const Sh<L>& x, const Sh<L>& y, const Mat
   Sh<L> z;
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    u64 v = __ldcs(t.p2 + PI(l) * t.ps2 + e) + d * b[l] + f * a[l];
+    u64 v = ldm<G>(t.p2 + PI(l) * t.ps2 + e) + d * b[l] + f * a[l];
     if (PI(l) == p0) v += d * f;
     z.v[l] = v & msk;
   }
@@ -232,8 +255,8 @@ __device__ __forceinline__ Sh<L> d_trunc(const Sh<L>& x, const MatRef& lo, const
   u64 s = 0;
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    h[l] = hi ? __ldcs(hi->p0 + PI(l) * hi->ps0 + e) : 0ull;
-    u64 v = x.v[l] + __ldcs(lo.p0 + PI(l) * lo.ps0 + e) + (h[l] << f);
+    h[l] = hi ? ldm<G>(hi->p0 + PI(l) * hi->ps0 + e) : 0ull;
+    u64 v = x.v[l] + ldm<G>(lo.p0 + PI(l) * lo.ps0 + e) + (h[l] << f);
     if (PI(l) == p0) v += bias;
     s += v;
   }
@@ -326,7 +349,7 @@ __device__ __forceinline__ Sh<L> d_decompose(const Sh<L>& x, int w, const Tape& 
   u64 rb[L];
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    c += x.v[l] - __ldcs(t.p0 + PI(l) * t.ps0 + e);
+    c += x.v[l] - ldm<G>(t.p0 + PI(l) * t.ps0 + e);
     rb[l] = load_bits(t.p1 + PI(l) * t.ps1, t.off + e * (i64)w, w);
   }
   c = gsum<G>(c);
@@ -408,7 +431,7 @@ __device__ __forceinline__ Sh<L> d_bit2a_get(u64 c, int j, int m, const MatRef& 
   Sh<L> z;
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    u64 v = __ldg(t.p0 + PI(l) * t.ps0 + e * (i64)m + j) * (1ull - 2ull * cj);
+    u64 v = ldr<G>(t.p0 + PI(l) * t.ps0 + e * (i64)m + j) * (1ull - 2ull * cj);
     if (PI(l) == p0) v += cj;
     z.v[l] = v & msk;
   }
@@ -432,21 +455,21 @@ __device__ __forceinline__ void d_bit2a_row(u64 c, int m, int stride, const MatR
       f(l, jj, v & msk);
     };
     if (((uintptr_t)row & 15) != 0 && m > 0) {
-      emit(0, __ldg(row));
+      emit(0, ldr<G>(row));
       j = 1;
     }
     for (; j + 8 <= m; j += 8) {
       const ulonglong2* r2 = reinterpret_cast<const ulonglong2*>(row + j);
-      const ulonglong2 v0 = __ldg(r2), v1 = __ldg(r2 + 1), v2 = __ldg(r2 + 2), v3 = __ldg(r2 + 3);
+      const ulonglong2 v0 = ldr2<G>(r2), v1 = ldr2<G>(r2 + 1), v2 = ldr2<G>(r2 + 2), v3 = ldr2<G>(r2 + 3);
       emit(j, v0.x); emit(j + 1, v0.y); emit(j + 2, v1.x); emit(j + 3, v1.y);
       emit(j + 4, v2.x); emit(j + 5, v2.y); emit(j + 6, v3.x); emit(j + 7, v3.y);
     }
     for (; j + 2 <= m; j += 2) {
-      const ulonglong2 v0 = __ldg(reinterpret_cast<const ulonglong2*>(row + j));
+      const ulonglong2 v0 = ldr2<G>(reinterpret_cast<const ulonglong2*>(row + j));
       emit(j, v0.x);
       emit(j + 1, v0.y);
     }
-    if (j < m) emit(j, __ldg(row + j));
+    if (j < m) emit(j, ldr<G>(row + j));
   }
 }
 
@@ -466,11 +489,11 @@ __device__ __forceinline__ void mt_load(MTM<L>& m, const Tape& tape, int& ti, i6
   const MatRef* hi = has_hi ? &next_take<L, G>(tape, ti, e) : nullptr;
 #pragma unroll
   for (int l = 0; l < L; ++l) {
-    m.a[l] = __ldcs(tm.p0 + PI(l) * tm.ps0 + e);
-    m.b[l] = __ldcs(tm.p1 + PI(l) * tm.ps1 + e);
-    m.c[l] = __ldcs(tm.p2 + PI(l) * tm.ps2 + e);
-    m.lo[l] = __ldcs(lo.p0 + PI(l) * lo.ps0 + e);
-    m.hi[l] = hi ? __ldcs(hi->p0 + PI(l) * hi->ps0 + e) : 0ull;
+    m.a[l] = ldm<G>(tm.p0 + PI(l) * tm.ps0 + e);
+    m.b[l] = ldm<G>(tm.p1 + PI(l) * tm.ps1 + e);
+    m.c[l] = ldm<G>(tm.p2 + PI(l) * tm.ps2 + e);
+    m.lo[l] = ldm<G>(lo.p0 + PI(l) * lo.ps0 + e);
+    m.hi[l] = hi ? ldm<G>(hi->p0 + PI(l) * hi->ps0 + e) : 0ull;
   }
 }
 
@@ -1020,6 +1043,103 @@ struct SoftmaxSegs {
   int p, w32;
 };
 
+// One row of softmax_parts. `tape` is the concatenated tape (kernel
+// parameter) or its staged shadow in shared memory (G | MPX_STAGED).
+template <int L, int G>
+__device__ __forceinline__ void softmax_row(i64 row, u64* __restrict__ eout, u64* __restrict__ rout,
+                                            const u64* __restrict__ in, i64 rows, int d0, const Tape& tape,
+                                            const SoftmaxSegs& sg, const FusedParams& Pm, const FusedParams& Pe,
+                                            const FusedParams& Pr, u64* sm_vals) {
+  const int p0 = Pm.p0;
+  const u64 m64 = ring_mask(64), m32 = ring_mask(sg.w32);
+  const int j = threadIdx.x / GS(G);  // lanes j*G .. j*G+G-1 own column j, L parties each
+  const int nw = (blockDim.x + 31) / 32;
+  u64* part = sm_vals + L * GS(G) * d0;
+  Sh<L> v;
+  if (j < d0) {
+    const i64 e = row * d0 + j;
+#pragma unroll
+    for (int l = 0; l < L; ++l) v.v[l] = in[((i64)PI(l) * rows + row) * d0 + j];
+    if (sg.resc >= 0) {  // truncate(scale_fixed(x, log2 e), p) (derived.py:55-83)
+      int ti = sg.resc;
+      const Sh<L> sc = sh_scale<L, G>(v, sg.log2e_p, 0ull, p0, m64);
+      const MatRef& lo = next_take<L, G>(tape, ti, e);
+      const MatRef& hi = next_take<L, G>(tape, ti, e);
+      v = d_trunc<L, G>(sc, lo, &hi, e, sg.p, true, 64, p0, m64);
+    }
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      v.v[l] &= m32;  // narrow (nn.py:68-74)
+      sm_vals[PI(l) * d0 + j] = v.v[l];
+    }
+  }
+  __syncthreads();
+  // max_vec tournament (derived.py:152-170)
+  int d = d0;
+  for (int lev = 0; lev < sg.nlev; ++lev) {
+    const int half = d / 2, rest = d - 2 * half;
+    Sh<L> win;
+    if (j < half) {
+      int ti = sg.lev[lev];
+      Sh<L> u, w;
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        u.v[l] = sm_vals[PI(l) * d0 + j];
+        w.v[l] = sm_vals[PI(l) * d0 + half + j];
+      }
+      win = d_maxpair<L, G>(u, w, tape, ti, row * (i64)half + j, sg.w32, p0, m32);
+    }
+    Sh<L> rv;
+    if (j == 0 && rest)
+#pragma unroll
+      for (int l = 0; l < L; ++l) rv.v[l] = sm_vals[PI(l) * d0 + 2 * half];
+    __syncthreads();
+    if (j < half)
+#pragma unroll
+      for (int l = 0; l < L; ++l) sm_vals[PI(l) * d0 + j] = win.v[l];
+    if (j == 0 && rest)
+#pragma unroll
+      for (int l = 0; l < L; ++l) sm_vals[PI(l) * d0 + half] = rv.v[l];
+    __syncthreads();
+    d = half + rest;
+  }
+  // x - max - 1 ulp (nn.py:100-112), attention_exp, row sum
+  Sh<L> ev;
+#pragma unroll
+  for (int l = 0; l < L; ++l) ev.v[l] = 0;
+  if (j < d0) {
+    Sh<L> sh;
+#pragma unroll
+    for (int l = 0; l < L; ++l) sh.v[l] = (v.v[l] - sm_vals[PI(l) * d0] + (PI(l) == p0 ? m32 : 0ull)) & m32;
+    int ti = sg.attexp;
+    ev = d_attexp<L, G>(sh, tape, ti, row * (i64)d0 + j, Pe);
+#pragma unroll
+    for (int l = 0; l < L; ++l) eout[((i64)PI(l) * rows + row) * d0 + j] = ev.v[l];
+  }
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    u64 sum = ev.v[l];
+#pragma unroll
+    for (int o = 16; o >= GS(G); o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if ((threadIdx.x & 31) < GS(G)) part[PI(l) * nw + (threadIdx.x >> 5)] = sum;
+  }
+  __syncthreads();
+  if (j == 0) {
+    Sh<L> tot;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      u64 sum = 0;
+      for (int q = 0; q < nw; ++q) sum += part[PI(l) * nw + q];
+      tot.v[l] = sum & m64;
+    }
+    int ti = sg.recip;
+    const Sh<L> r = d_reciprocal<L, G>(tot, tape, ti, row, Pr);
+#pragma unroll
+    for (int l = 0; l < L; ++l) rout[(i64)PI(l) * rows + row] = r.v[l];
+  }
+  __syncthreads();
+}
+
 template <int L, int G>
 __global__ void __launch_bounds__(256 * G) k_softmax_fused(u64* __restrict__ eout, u64* __restrict__ rout,
                                                        const u64* __restrict__ in, i64 rows, int d0,
@@ -1027,95 +1147,79 @@ __global__ void __launch_bounds__(256 * G) k_softmax_fused(u64* __restrict__ eou
                                                        const __grid_constant__ SoftmaxSegs sg, FusedParams Pm,
                                                        FusedParams Pe, FusedParams Pr) {
   extern __shared__ u64 sm_vals[];  // [L][d0] tournament values, then [L][nwarps] row-sum partials
-  const int p0 = Pm.p0;
-  const u64 m64 = ring_mask(64), m32 = ring_mask(sg.w32);
-  const int j = threadIdx.x / G;  // lanes j*G .. j*G+G-1 own column j, L parties each
-  const int nw = (blockDim.x + 31) / 32;
-  u64* part = sm_vals + L * G * d0;
+  for (i64 row = blockIdx.x; row < rows; row += gridDim.x)
+    softmax_row<L, G>(row, eout, rout, in, rows, d0, tape, sg, Pm, Pe, Pr, sm_vals);
+}
+
+// Staged variant: before each row, the CTA copies every word of material the
+// row's chain will read (each take's element range for this row: d0 scores
+// for the rescale / attention-exp takes, half of the level for a tournament
+// level, one element for the reciprocal) into shared memory with all loads
+// in flight at once, and rewrites the tape to point there. The ~100
+// dependent rounds of the row then wait on shared-memory latency instead of
+// a DRAM / L2 round trip each (LeNet's 128 x 10 softmax: one warp per row).
+// Plan (row-independent, built on the host): per take and operand array, the
+// element count per row and the staged words per party.
+struct StagePlan {
+  int cnt[TAPE_MAX];        // elements of this take per row
+  int off[TAPE_MAX][3];     // word offset of (take, array) in the stage
+  int len[TAPE_MAX][3];     // words per party (0: array unused)
+  int words;                // total staged words
+  int nparties;
+};
+
+__device__ __forceinline__ i64 stage_lo(const MatRef& t, int a, i64 e_lo) {
+  if (t.kind == 0) return e_lo * (i64)max(1, t.per0);           // one word per element
+  if (t.kind == 1) return (t.off + e_lo * (i64)t.per0) >> 6;    // bit triples
+  return a == 0 ? e_lo * (i64)t.per0 : (t.off + e_lo * (i64)t.per1) >> 6;   // daBit / edaBit
+}
+
+template <int L, int G>
+__global__ void __launch_bounds__(256 * G) k_softmax_staged(u64* __restrict__ eout, u64* __restrict__ rout,
+                                                        const u64* __restrict__ in, i64 rows, int d0,
+                                                        const __grid_constant__ Tape tape,
+                                                        const __grid_constant__ SoftmaxSegs sg, FusedParams Pm,
+                                                        FusedParams Pe, FusedParams Pr,
+                                                        const __grid_constant__ StagePlan plan) {
+  extern __shared__ __align__(16) u64 smem_all[];
+  Tape& st = *reinterpret_cast<Tape*>(smem_all);
+  u64* stage = smem_all + (sizeof(Tape) + 15) / 16 * 2;
+  u64* vals = stage + plan.words;
   for (i64 row = blockIdx.x; row < rows; row += gridDim.x) {
-    Sh<L> v;
-    if (j < d0) {
-      const i64 e = row * d0 + j;
+    // shadow tape: same entries, operand pointers into the stage
+    for (int ti = threadIdx.x; ti < tape.n; ti += blockDim.x) {
+      MatRef m = tape.m[ti];
+      const i64 e_lo = row * plan.cnt[ti];
+      const u64** ps[3] = {&m.p0, &m.p1, &m.p2};
+      i64* strides[3] = {&m.ps0, &m.ps1, &m.ps2};
 #pragma unroll
-      for (int l = 0; l < L; ++l) v.v[l] = in[((i64)PI(l) * rows + row) * d0 + j];
-      if (sg.resc >= 0) {  // truncate(scale_fixed(x, log2 e), p) (derived.py:55-83)
-        int ti = sg.resc;
-        const Sh<L> sc = sh_scale<L, G>(v, sg.log2e_p, 0ull, p0, m64);
-        const MatRef& lo = next_take<L, G>(tape, ti, e);
-        const MatRef& hi = next_take<L, G>(tape, ti, e);
-        v = d_trunc<L, G>(sc, lo, &hi, e, sg.p, true, 64, p0, m64);
+      for (int a = 0; a < 3; ++a) {
+        if (plan.len[ti][a] == 0) continue;
+        *ps[a] = stage + plan.off[ti][a] - stage_lo(m, a, e_lo);
+        *strides[a] = plan.len[ti][a];
       }
-#pragma unroll
-      for (int l = 0; l < L; ++l) {
-        v.v[l] &= m32;  // narrow (nn.py:68-74)
-        sm_vals[PI(l) * d0 + j] = v.v[l];
-      }
+      st.m[ti] = m;
     }
+    if (threadIdx.x == 0) st.n = tape.n;
+    // copy: thread t takes segments (take, array, party) t, t + blockDim, ...
+    // and issues one asynchronous 8-byte copy per word (cp.async: nothing
+    // waits until every copy of the row is in flight)
+    const int nseg = tape.n * 3 * plan.nparties;
+    for (int q = threadIdx.x; q < nseg; q += blockDim.x) {
+      const int l = q % plan.nparties, ta = q / plan.nparties, ti = ta / 3, a = ta % 3;
+      const int len = plan.len[ti][a];
+      if (len == 0) continue;
+      const MatRef& m = tape.m[ti];
+      const u64* src = a == 0 ? m.p0 : (a == 1 ? m.p1 : m.p2);
+      const i64 sps = a == 0 ? m.ps0 : (a == 1 ? m.ps1 : m.ps2);
+      src += l * sps + stage_lo(m, a, row * plan.cnt[ti]);
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(stage + plan.off[ti][a] + l * len);
+      for (int i = 0; i < len; ++i)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8 * i), "l"(src + i) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
     __syncthreads();
-    // max_vec tournament (derived.py:152-170)
-    int d = d0;
-    for (int lev = 0; lev < sg.nlev; ++lev) {
-      const int half = d / 2, rest = d - 2 * half;
-      Sh<L> win;
-      if (j < half) {
-        int ti = sg.lev[lev];
-        Sh<L> u, w;
-#pragma unroll
-        for (int l = 0; l < L; ++l) {
-          u.v[l] = sm_vals[PI(l) * d0 + j];
-          w.v[l] = sm_vals[PI(l) * d0 + half + j];
-        }
-        win = d_maxpair<L, G>(u, w, tape, ti, row * (i64)half + j, sg.w32, p0, m32);
-      }
-      Sh<L> rv;
-      if (j == 0 && rest)
-#pragma unroll
-        for (int l = 0; l < L; ++l) rv.v[l] = sm_vals[PI(l) * d0 + 2 * half];
-      __syncthreads();
-      if (j < half)
-#pragma unroll
-        for (int l = 0; l < L; ++l) sm_vals[PI(l) * d0 + j] = win.v[l];
-      if (j == 0 && rest)
-#pragma unroll
-        for (int l = 0; l < L; ++l) sm_vals[PI(l) * d0 + half] = rv.v[l];
-      __syncthreads();
-      d = half + rest;
-    }
-    // x - max - 1 ulp (nn.py:100-112), attention_exp, row sum
-    Sh<L> ev;
-#pragma unroll
-    for (int l = 0; l < L; ++l) ev.v[l] = 0;
-    if (j < d0) {
-      Sh<L> sh;
-#pragma unroll
-      for (int l = 0; l < L; ++l) sh.v[l] = (v.v[l] - sm_vals[PI(l) * d0] + (PI(l) == p0 ? m32 : 0ull)) & m32;
-      int ti = sg.attexp;
-      ev = d_attexp<L, G>(sh, tape, ti, row * (i64)d0 + j, Pe);
-#pragma unroll
-      for (int l = 0; l < L; ++l) eout[((i64)PI(l) * rows + row) * d0 + j] = ev.v[l];
-    }
-#pragma unroll
-    for (int l = 0; l < L; ++l) {
-      u64 s = ev.v[l];
-#pragma unroll
-      for (int o = 16; o >= G; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if ((threadIdx.x & 31) < G) part[PI(l) * nw + (threadIdx.x >> 5)] = s;
-    }
-    __syncthreads();
-    if (j == 0) {
-      Sh<L> tot;
-#pragma unroll
-      for (int l = 0; l < L; ++l) {
-        u64 s = 0;
-        for (int q = 0; q < nw; ++q) s += part[PI(l) * nw + q];
-        tot.v[l] = s & m64;
-      }
-      int ti = sg.recip;
-      const Sh<L> r = d_reciprocal<L, G>(tot, tape, ti, row, Pr);
-#pragma unroll
-      for (int l = 0; l < L; ++l) rout[(i64)PI(l) * rows + row] = r.v[l];
-    }
-    __syncthreads();
+    softmax_row<L, G | MPX_STAGED>(row, eout, rout, in, rows, d0, st, sg, Pm, Pe, Pr, vals);
   }
 }
 
@@ -1136,6 +1240,65 @@ extern "C" int mpx_softmax_fused(uint64_t* e_out, uint64_t* r_out, const uint64_
   const int threads = max(32, ((gl * d0 + 31) / 32) * 32);
   const unsigned g = (unsigned)min(rows, (i64)(148 * 8));
   const size_t sm = (size_t)Pm.L * (d0 + threads / 32) * 8;
+  // staged plan: the row's element range per take (segments in tape order)
+  static StagePlan plan;
+  bool staged = true;
+  if (const char* e = getenv("MPX_SOFTMAX_STAGE")) staged = atoi(e) != 0;
+  if (staged) {
+    int cur = 0;
+    for (int ti = 0; ti < tp.n; ++ti) {
+      int cnt;
+      if (sg.resc >= 0 && ti < sg.lev[0]) cnt = d0;             // rescale truncation
+      else if (ti < sg.attexp) {                                 // tournament levels
+        int lev = 0;
+        while (lev + 1 < sg.nlev && ti >= sg.lev[lev + 1]) ++lev;
+        int dd = d0;
+        for (int k = 0; k < lev; ++k) dd = dd / 2 + (dd & 1);
+        cnt = dd / 2;
+      } else if (ti < sg.recip) cnt = d0;                       // attention exp
+      else cnt = 1;                                              // row-sum reciprocal
+      plan.cnt[ti] = cnt;
+      const MatRef& m = tp.m[ti];
+      for (int a = 0; a < 3; ++a) {
+        const void* ptr = a == 0 ? (const void*)m.p0 : (a == 1 ? (const void*)m.p1 : (const void*)m.p2);
+        int len = 0;
+        if (ptr) {
+          if (m.kind == 0) len = cnt * max(1, m.per0);
+          else if (m.kind == 1) len = (int)(((i64)cnt * m.per0 + 63) / 64 + 2);
+          else len = a == 0 ? cnt * m.per0 : (int)(((i64)cnt * m.per1 + 63) / 64 + 2);
+        }
+        plan.off[ti][a] = cur;
+        plan.len[ti][a] = len;
+        cur += ((len * Pm.L + 1) / 2) * 2;                      // 16-byte aligned regions
+      }
+    }
+    plan.words = cur;
+    plan.nparties = Pm.L;                                        // every local party (all lanes)
+    // at least four warps per row: the staging copy is spread over every thread
+    const int sthreads = max(threads, 128);
+    const size_t ssm = (sizeof(Tape) + 15) / 16 * 16 + (size_t)cur * 8 + (size_t)Pm.L * (d0 + sthreads / 32) * 8;
+    if (ssm > 200 * 1024) staged = false;
+    else {
+      static size_t attr_set = 0;
+      if (ssm > attr_set) {
+        const void* fns[] = {(const void*)k_softmax_staged<1, 1>, (const void*)k_softmax_staged<2, 1>,
+                             (const void*)k_softmax_staged<3, 1>, (const void*)k_softmax_staged<4, 1>,
+                             (const void*)k_softmax_staged<4, 2>};
+        for (const void* f : fns)
+          if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm) != cudaSuccess)
+            return MPX_ERR_CUDA;
+        attr_set = ssm;
+      }
+      switch (Pm.L) {
+        case 1: k_softmax_staged<1, 1><<<g, sthreads, ssm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr, plan); break;
+        case 2: k_softmax_staged<2, 1><<<g, sthreads, ssm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr, plan); break;
+        case 3: k_softmax_staged<3, 1><<<g, sthreads, ssm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr, plan); break;
+        case 4: k_softmax_staged<4, 1><<<g, sthreads, ssm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr, plan); break;
+        default: k_softmax_staged<4, 2><<<g, sthreads, ssm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr, plan); break;
+      }
+      return launch_status();
+    }
+  }
   switch (Pm.L) {
     case 1: k_softmax_fused<1, 1><<<g, threads, sm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr); break;
     case 2: k_softmax_fused<2, 1><<<g, threads, sm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr); break;

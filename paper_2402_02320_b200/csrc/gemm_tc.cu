@@ -372,9 +372,22 @@ __global__ void __launch_bounds__(192, BN == 32 ? 2 : 1)
 #define TCP_BST 2
 #define TCP_STAGE_TILE (32 * 33 * 8)  // one 32 x 32 u64 transpose tile per epilogue warp
 #define TCP_STAGED_MAX_KB 4
-constexpr int tcp_ast(int bk) { return 65536 / (TC_BM * bk); }  // 64 KB A ring
+// A ring: every byte of shared memory the B stages and the epilogue tiles
+// leave (short-K products are load-latency bound: more A tiles in flight).
+// MPX_TC_ARING_KB caps it at compile time for A/B runs (64 = the old ring).
+#ifndef MPX_TC_ARING_KB
+#define MPX_TC_ARING_KB 1024
+#endif
+constexpr int tcp_fixed_bytes(int bk, int bn, bool staged, int ew) {
+  return TCP_BST * 8 * bn * bk + (staged ? ew * TCP_STAGE_TILE : 0) + 1024 + 1024;
+}
+constexpr int tcp_ast_for(int bk, int bn, bool staged, int ew) {
+  return ((232448 - tcp_fixed_bytes(bk, bn, staged, ew)) / (TC_BM * bk)) < (MPX_TC_ARING_KB * 1024 / (TC_BM * bk))
+             ? (232448 - tcp_fixed_bytes(bk, bn, staged, ew)) / (TC_BM * bk)
+             : MPX_TC_ARING_KB * 1024 / (TC_BM * bk);
+}
 constexpr int tcp_smem_bytes(int bk, int bn, bool staged, int ew) {
-  return tcp_ast(bk) * TC_BM * bk + TCP_BST * 8 * bn * bk + (staged ? ew * TCP_STAGE_TILE : 0) + 1024 + 512;
+  return tcp_ast_for(bk, bn, staged, ew) * TC_BM * bk + tcp_fixed_bytes(bk, bn, staged, ew);
 }
 
 // K-major UMMA shared-memory descriptor for a BK-byte-row swizzled tile
@@ -437,7 +450,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
     k_gemm_limbs_tc_pers(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                          const __grid_constant__ CUtensorMap mapA2, const __grid_constant__ CUtensorMap mapB2,
                          TcArgs args, int batch) {
-  constexpr int AST = tcp_ast(BK), BST = TCP_BST;
+  constexpr int AST = tcp_ast_for(BK, BN, STAGED, EW), BST = TCP_BST;
   constexpr int A_TILE = TC_BM * BK;
   constexpr int B_TILE = BN * BK;
   constexpr int B_STAGE = 8 * B_TILE;

@@ -544,33 +544,50 @@ def gemm_tc(C, A, B, batch, M, K, N, sA, sB, sC, accumulate, width):
 
 # ---- dealer -----------------------------------------------------------------
 
+# ``key``: (k0, k1) by value, or an int64[2] device tensor (a key slot read
+# at launch: the dealer's CUDA graph, preprocessing.DealerGraph)
+
 def philox_elems(out, key, u32_off, count, width):
     if _dry(out):
         return out
-    call("mpx_philox_elems", ptr(out), _u(key[0]), _u(key[1]), u32_off, count, width)
+    if isinstance(key, torch.Tensor):
+        call("mpx_philox_elems_dk", ptr(out), ptr(key), u32_off, count, width)
+    else:
+        call("mpx_philox_elems", ptr(out), _u(key[0]), _u(key[1]), u32_off, count, width)
     return out
 
 
 def philox_bits(out, key, u32_off, count):
     if _dry(out):
         return out
-    call("mpx_philox_bits", ptr(out), _u(key[0]), _u(key[1]), u32_off, count)
+    if isinstance(key, torch.Tensor):
+        call("mpx_philox_bits_dk", ptr(out), ptr(key), u32_off, count)
+    else:
+        call("mpx_philox_bits", ptr(out), _u(key[0]), _u(key[1]), u32_off, count)
     return out
 
 
 def deal_share_arith(out, secret, key, u32_base, count, n, p_lo, L, width):
     if _dry(out):
         return out
-    call("mpx_deal_share_arith", ptr(out), out.stride(0), ptr(secret), _u(key[0]), _u(key[1]), u32_base,
-         count, n, p_lo, L, width)
+    if isinstance(key, torch.Tensor):
+        call("mpx_deal_share_arith_dk", ptr(out), out.stride(0), ptr(secret), ptr(key), u32_base, count, n, p_lo,
+             L, width)
+    else:
+        call("mpx_deal_share_arith", ptr(out), out.stride(0), ptr(secret), _u(key[0]), _u(key[1]), u32_base,
+             count, n, p_lo, L, width)
     return out
 
 
 def deal_share_bits(out, secret, key, u32_base, count, n, p_lo, L):
     if _dry(out):
         return out
-    call("mpx_deal_share_bits", ptr(out), out.stride(0), ptr(secret), _u(key[0]), _u(key[1]), u32_base,
-         count, n, p_lo, L)
+    if isinstance(key, torch.Tensor):
+        call("mpx_deal_share_bits_dk", ptr(out), out.stride(0), ptr(secret), ptr(key), u32_base, count, n, p_lo,
+             L)
+    else:
+        call("mpx_deal_share_bits", ptr(out), out.stride(0), ptr(secret), _u(key[0]), _u(key[1]), u32_base,
+             count, n, p_lo, L)
     return out
 
 

@@ -173,10 +173,11 @@ class Dealer:
     running u32 index into the key's Philox stream.
     """
 
-    def __init__(self, seed: int, n_parties: int, p_lo: int, L: int, device):
+    def __init__(self, seed: int, n_parties: int, p_lo: int, L: int, device, key_slots: dict | None = None):
         self.seed, self.n, self.p_lo, self.L = seed, n_parties, p_lo, L
         self.device = torch.device(device)
         self._out = None   # when set: write shares into these existing arrays
+        self.key_slots = key_slots   # MaterialKey -> int64[2] device slot (keys read at launch)
 
     def _e(self, *shape):
         return torch.empty(shape, dtype=torch.int64, device=self.device)
@@ -222,7 +223,7 @@ class Dealer:
             self._out = None
 
     def _generate(self, key: MaterialKey, count: int, need_bits: bool) -> dict:
-        pk = dealer_philox_key(self.seed, key)
+        pk = self.key_slots[key] if self.key_slots is not None else dealer_philox_key(self.seed, key)
         w = key.width
         q = 0
         if key.kind == KIND_TRIPLE:                       # preprocessing.py:139-145
@@ -416,3 +417,60 @@ def device_store(seed: int, n_parties: int, demands: dict, parties=None, device=
     if into is not None:
         into.rewind()
     return store
+
+
+class DealerGraph:
+    """A whole re-deal of ``store`` (every demanded key, in place) captured in
+    ONE CUDA graph.
+
+    The dealer kernels read their Philox keys from device slots, so a replay
+    for a new seed is: hash the seed's per-key keys on the host
+    (preprocessing.py:121-125), one small copy into the slots, one graph
+    launch - the same material as ``device_store(seed, ..., into=store)``,
+    bit for bit (tests/test_train.py), at device speed instead of ~100
+    Python-issued launches.
+    """
+
+    def __init__(self, store: MaterialStore, demands: dict, needs_bits: dict | None, seed0: int):
+        self.store = store
+        self.n, self.parties, self.device = store.n_parties, store.parties, store.device
+        self.keys = [k for k, c in sorted(demands.items(), key=lambda kv: kv[0].name()) if c > 0]
+        self.counts = {k: demands[k] for k in self.keys}
+        self.need = {k: (True if needs_bits is None else needs_bits.get(k, k.kind != KIND_EDABIT)) for k in self.keys}
+        self.slots = torch.zeros((max(1, len(self.keys)), 2), dtype=torch.int64, device=self.device)
+        self._host = torch.zeros(self.slots.shape, dtype=torch.int64).pin_memory()
+        self._copied = torch.cuda.Event()   # the pinned key buffer is free again
+        slot_of = {k: self.slots[i] for i, k in enumerate(self.keys)}
+        self._dealer = Dealer(seed0, self.n, self.parties[0], len(self.parties), self.device, key_slots=slot_of)
+        self._write(seed0)
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):
+            self._deal()                     # warm-up: first-use work outside the capture
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        torch.cuda.synchronize(self.device)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._deal()
+        store.rewind()
+
+    def _deal(self):
+        for k in self.keys:
+            self._dealer.generate(k, self.counts[k], need_bits=self.need[k], out=self.store._arrays[k])
+
+    def _write(self, seed: int):
+        import numpy as np
+        words = np.zeros((self.slots.shape[0], 2), dtype=np.uint64)
+        for i, k in enumerate(self.keys):
+            words[i] = dealer_philox_key(seed, k)
+        self._copied.synchronize()
+        self._host.copy_(torch.from_numpy(words.view(np.int64)))
+        self.slots.copy_(self._host, non_blocking=True)
+        self._copied.record()
+
+    def redeal(self, seed: int) -> MaterialStore:
+        """Fresh material for ``seed`` in place; cursors reset."""
+        self._write(seed)
+        self.graph.replay()
+        self.store.rewind()
+        return self.store

@@ -405,7 +405,8 @@ class GraphedStep:
     stable: inputs and weights live in static buffers (updated weights are
     copied back inside the graph), intermediates come from the graph's private
     pool, and the dealer re-deals fresh material into the SAME store arrays
-    before each replay (``device_store(..., into=store)``, outside the graph).
+    before each replay (``DealerGraph.redeal``: the whole re-deal is its own
+    CUDA graph, keys in device slots), outside the step's graph.
 
     Construction runs one eager warm-up step (seed0 material) and then
     restores the weights it updated, so the model is where the caller left
@@ -414,7 +415,7 @@ class GraphedStep:
 
     def __init__(self, session, model: Model, x: AShare, y: AShare, lr_shift: int, demands: dict,
                  needs_bits: dict, seed0: int):
-        from .preprocessing import device_store
+        from .preprocessing import DealerGraph, device_store
         self.s, self.model, self.lr_shift = session, model, lr_shift
         self.demands, self.needs_bits = demands, needs_bits
         self.params = [(layer, nm) for layer in model.layers for nm in ("W", "b") if hasattr(layer, nm)]
@@ -422,6 +423,7 @@ class GraphedStep:
         self.x, self.y = x, y
         session.store = device_store(seed0, session.n_parties, demands, parties=session.parties,
                                      device=session.device, needs_bits=needs_bits)
+        self.dealer = DealerGraph(session.store, demands, needs_bits, seed0)
         # warm-up (eager) step: first-use work (attributes, schedules) happens
         # here; the weights it updates are restored afterwards
         snapshot = [b.values.clone() for b in self.bufs]
@@ -449,9 +451,7 @@ class GraphedStep:
                 setattr(layer, nm, buf)
 
     def step(self, seed: int) -> AShare:
-        """Re-deal fresh material in place, replay the captured step."""
-        from .preprocessing import device_store
-        device_store(seed, self.s.n_parties, self.demands, parties=self.s.parties, device=self.s.device,
-                     needs_bits=self.needs_bits, into=self.s.store)
+        """Re-deal fresh material in place (the dealer's own CUDA graph), replay the captured step."""
+        self.dealer.redeal(seed)
         self.graph.replay()
         return self.logits

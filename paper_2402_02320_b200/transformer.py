@@ -115,11 +115,12 @@ class GraphedInference:
     """Forward pass captured in one CUDA graph; material re-dealt in place per call."""
 
     def __init__(self, session, model: Transformer, x: AShare, demands, needs_bits, seed0: int):
-        from .preprocessing import device_store
+        from .preprocessing import DealerGraph, device_store
         self.s, self.model, self.x = session, model, x
         self.demands, self.needs_bits = demands, needs_bits
         session.store = device_store(seed0, session.n_parties, demands, parties=session.parties,
                                      device=session.device, needs_bits=needs_bits)
+        self.dealer = DealerGraph(session.store, demands, needs_bits, seed0)
         side = torch.cuda.Stream(session.device)
         side.wait_stream(torch.cuda.current_stream(session.device))
         with torch.cuda.stream(side):
@@ -132,8 +133,6 @@ class GraphedInference:
             self.y = model.forward(session, x)
 
     def run(self, seed: int) -> AShare:
-        from .preprocessing import device_store
-        device_store(seed, self.s.n_parties, self.demands, parties=self.s.parties, device=self.s.device,
-                     needs_bits=self.needs_bits, into=self.s.store)
+        self.dealer.redeal(seed)
         self.graph.replay()
         return self.y

@@ -290,11 +290,21 @@ def test_mask_limbs2_matches_two_launches(K, L, p0, jobs, m, k, r, xt, yt):
     (4, 3, 1, 128, 10, 500, False, True, 64),    # short K, transposed Y view, p0 = last party
     (3, 0, 1, 70, 33, 40, False, False, 32),     # narrow ring: no split
     (2, 1, 3, 20, 3000, 10, True, True, 64),
+    # thin kernels: tall (huge M, K and N <= 32) and long-K (tiny output)
+    (3, 0, 1, 9000, 25, 20, False, False, 64),   # LeNet conv1 forward shape family
+    (2, 1, 2, 5000, 10, 16, False, True, 64),
+    (4, 3, 1, 4100, 32, 32, True, False, 32),
+    (3, 2, 1, 4096, 7, 5, False, False, 64),
+    (3, 0, 1, 25, 73728, 20, True, False, 64),   # LeNet conv1 weight gradient at batch 128
+    (4, 1, 1, 10, 700, 9, False, True, 64),
 ])
-def test_beaver_gemm_sim_matches_numpy(K, L, p0, jobs, m, k, r, xt, yt, w):
+@pytest.mark.parametrize("thin", ["1", "0"])
+def test_beaver_gemm_sim_matches_numpy(K, monkeypatch, thin, L, p0, jobs, m, k, r, xt, yt, w):
     """Sim-mode Beaver opening + reconstruction in one launch: Z_l = C_l +
     D @ (B_l + [l==p0] E) + A_l @ E, D = sum_l X_l - A_l, E = sum_l Y_l - B_l
-    (basic.py:66-75), mod 2^w."""
+    (basic.py:66-75), mod 2^w - on the thin kernels (tall / long-K) where
+    the shape fits them, and with them disabled (MPX_THIN=0: tiled kernel)."""
+    monkeypatch.setenv("MPX_THIN", thin)
     rng = np.random.default_rng(m * 5 + k + r + jobs + w)
     X, Y = _rand(rng, (jobs, L, m, k), w), _rand(rng, (jobs, L, k, r), w)
     A, B, C = _rand(rng, (jobs, L, m, k), w), _rand(rng, (jobs, L, k, r), w), _rand(rng, (jobs, L, m, r), w)
