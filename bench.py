@@ -796,6 +796,46 @@ def transformer_entry(torch, dev, steps, warmup, n=2):
             "max_abs_err_vs_float64": float(np.abs(y - m.plaintext(xq)).max())}
 
 
+def party_mode_entry(torch, dev, n: int = 3, steps: int = 5, warmup: int = 2):
+    """The one-party-per-GPU (L = 1) LeNet step of party 0 on this GPU with
+    the collectives elided (session.LoopbackComm): the per-party compute of
+    the north star's n-GPU deployment, captured in a CUDA graph like the sim
+    step, plus what the n-GPU run adds on top - the rounds and the bytes this
+    party's collectives move per step (all_reduce for arithmetic openings,
+    all_gather + XOR kernel for bit openings)."""
+    from paper_2402_02320_b200 import train
+    from paper_2402_02320_b200.preprocessing import DemandCounter
+    from paper_2402_02320_b200.session import LoopbackComm, PartySession
+    x, y = lenet_data(BATCH)
+    kx, ky = label_key("share:x"), label_key("share:y")
+    c = DemandCounter((0,), n)
+    sd = PartySession(0, n, LoopbackComm(n), c, device=dev)
+    train.lenet(sd).train_step(sd, sd.share_fixed(x, WIDTH, FRAC, kx), sd.share_fixed(y, WIDTH, FRAC, ky), LR_SHIFT)
+    s = PartySession(0, n, LoopbackComm(n), None, device=dev)
+    m = train.lenet(s)
+    before = s.metrics.physical_bytes
+    g = train.GraphedStep(s, m, s.share_fixed(x, WIDTH, FRAC, kx), s.share_fixed(y, WIDTH, FRAC, ky), LR_SHIFT,
+                          c.demands, c.needs_bits, seed0=300)
+    phys = (s.metrics.physical_bytes - before) // 2           # warm-up step + captured step
+    times = []
+    for t in range(warmup + steps):
+        g.dealer.redeal(301 + t)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        if t >= warmup:
+            times.append(e0.elapsed_time(e1))
+    tot = sd.metrics.total.as_dict()
+    return {"parties": n, "party": 0, "batch": BATCH, "local_compute_ms_per_step": float(np.mean(times)),
+            "rounds_per_step": tot["rounds"], "logical_bytes_sent_per_step": tot["bytes"],
+            "collective_bytes_per_step": int(phys),
+            "how": "PartySession(L=1) of party 0 with LoopbackComm (collectives elided), CUDA graph replay; "
+                   "an n-GPU run adds one NCCL collective per round on top"}
+
+
 def party_scaling(torch, G, dev, group, ns=(2, 4, 8)):
     """North-star party sweep, all n parties simulated on one GPU (one-GPU-
     per-party runs need an n-GPU box: bench.py --gpus n under torchrun):
@@ -989,6 +1029,7 @@ def run_b200(args, group=None):
             sweep["transformer"] = transformer_entry(torch, dev, 3, 2)
             for arch in ("alexnet", "vgg16m"):
                 sweep[f"{arch}_train"] = cifar_entry(torch, dev, arch, 3, 2)
+            sweep["party_mode_1gpu"] = {str(n): party_mode_entry(torch, dev, n) for n in (2, 3, 4, 8)}
             if not getattr(args, "no_party_sweep", False):
                 sweep["party_scaling_sim"] = party_scaling(torch, G, dev, group)
         for nm, key in (("reciprocal", "reciprocal"), ("exp", "exp"), ("log", "log"), ("matmul", "matmul"),

@@ -496,23 +496,15 @@ int dispatch_sim(int best, i64 K, i64 batch, cudaStream_t s, uint64_t* Z, int64_
 }  // namespace
 
 // --------------------------------------------------------------------------
-// Thin sim-mode products (all parties local), shapes the tiled kernel above
-// serves with too few threads per SM:
-//
-// * tall: huge M, K <= 32, N <= 32 (a first conv layer's forward product,
-//   73728 x 25 x 20 at LeNet batch 128). Each CTA holds E and every party's
-//   B' = B_l + [l==p0] E for the whole (tiny) K x N in shared memory, then
-//   streams 32-row groups: the rows' X_l / A_l words are read once
-//   (contiguous), D = sum_l X_l - A_l is formed in shared memory, and warp l
-//   / lane r computes party l's output row r against B'_l and E.
-// * long-K: M * N * L <= 2048 outputs, any K (a first conv layer's weight
-//   gradient, 25 x 73728 x 20). A persistent grid walks K in 32-deep chunks,
-//   staging D, A_l, E, B'_l of the chunk; each thread owns a 2 x 4 output
-//   block of one party in registers; one wrapping 64-bit atomic per output
-//   and CTA at the end (Z pre-initialised with C).
-//
-// u64 products keep the 32-bit split explicit: a*b mod 2^64 = lo(a)lo(b) +
-// 2^32 (lo(a)hi(b) + hi(a)lo(b)); the compiler emits IMAD.WIDE + 2 IMAD.
+// Tall thin sim-mode products (all parties local): huge M, K <= 32, N <= 32
+// (a first conv layer's forward product, 73728 x 25 x 20 at LeNet batch
+// 128), which the tiled kernel above serves with too few threads per SM.
+// Each CTA holds E and every party's B' = B_l + [l==p0] E for the whole
+// (tiny) K x N in shared memory, then streams 32-row groups: the rows'
+// X_l / A_l words are read once (contiguous), D = sum_l X_l - A_l is formed
+// in shared memory, and warp l / lane r computes party l's output row r
+// against B'_l and E. (A long-K / tiny-output variant for the weight
+// gradient measured slower than the tiled split-K kernel: 158 vs 127 us.)
 
 #define TALL_R 32
 
@@ -593,98 +585,6 @@ __global__ void __launch_bounds__(32 * L) k_beaver_tall(u64* __restrict__ Z, i64
   }
 }
 
-#define LK_KC 32
-
-template <int L>
-__global__ void __launch_bounds__(256) k_beaver_longk(u64* __restrict__ Z, i64 sZ, i64 bZ, const u64* __restrict__ A,
-                                                     i64 sA, i64 bA, const __grid_constant__ SimOperand X,
-                                                     const __grid_constant__ SimOperand Y,
-                                                     const u64* __restrict__ B, i64 sB, i64 bB, int M, int K, int N,
-                                                     int p0, int chunks_per_cta) {
-  extern __shared__ __align__(16) u64 lk_sm[];
-  const int MP = (M + 1) & ~1, NP = (N + 3) & ~3;     // 16-byte aligned 2- and 4-wide reads
-  u64* Ds = lk_sm;                                     // [KC][MP]
-  u64* As = Ds + LK_KC * MP;                           // [L][KC][MP]
-  u64* Es = As + L * LK_KC * MP;                       // [KC][NP]
-  u64* Bp = Es + LK_KC * NP;                           // [L][KC][NP]
-  const int bt = blockIdx.y;
-  Z += bt * bZ;
-  A += bt * bA;
-  B += bt * bB;
-  const u64* Xp = X.p + bt * X.js;
-  const u64* Yp = Y.p + bt * Y.js;
-  const int tid = threadIdx.x;
-  // thread -> (party, 2-row block, 4-column block)
-  const int ib_n = MP / 2, jb_n = NP / 4;
-  const int per_l = ib_n * jb_n;
-  const bool active = tid < L * per_l;
-  const int l = active ? tid / per_l : 0, rem = active ? tid % per_l : 0;
-  const int i0 = 2 * (rem / jb_n), j0 = 4 * (rem % jb_n);
-  u64 acc[2][4] = {};
-  const i64 nchunks = ((i64)K + LK_KC - 1) / LK_KC;
-  for (i64 c = (i64)blockIdx.x * chunks_per_cta; c < min(nchunks, (i64)(blockIdx.x + 1) * chunks_per_cta); ++c) {
-    const i64 k0 = c * LK_KC;
-    const int kc = (int)min((i64)LK_KC, (i64)K - k0);
-    __syncthreads();
-    // A_l[i][k] rows are k-contiguous; X_l is read along its own unit stride
-    for (int idx = tid; idx < LK_KC * MP; idx += 256) {
-      const int kk = idx % LK_KC, i = idx / LK_KC;
-      const bool ok = kk < kc && i < M;
-#pragma unroll
-      for (int q = 0; q < L; ++q) As[(q * LK_KC + kk) * MP + i] = ok ? A[q * sA + (i64)i * K + k0 + kk] : 0ull;
-    }
-    __syncthreads();
-    const bool xk = X.sc == 1;
-    for (int idx = tid; idx < LK_KC * MP; idx += 256) {
-      const int kk = xk ? idx % LK_KC : idx / MP, i = xk ? idx / LK_KC : idx % MP;
-      const bool ok = kk < kc && i < M;
-      u64 d = 0;
-#pragma unroll
-      for (int q = 0; q < L; ++q)
-        d += (ok ? Xp[q * X.ps + (i64)i * X.sr + (k0 + kk) * X.sc] : 0ull) - As[(q * LK_KC + kk) * MP + i];
-      Ds[kk * MP + i] = d;
-    }
-    for (int idx = tid; idx < LK_KC * NP; idx += 256) {
-      const int kk = idx / NP, j = idx % NP;
-      const bool ok = kk < kc && j < N;
-      u64 e = 0, b[L];
-#pragma unroll
-      for (int q = 0; q < L; ++q) {
-        b[q] = ok ? B[q * sB + (k0 + kk) * N + j] : 0ull;
-        e += (ok ? Yp[q * Y.ps + (k0 + kk) * Y.sr + (i64)j * Y.sc] : 0ull) - b[q];
-      }
-      Es[kk * NP + j] = e;
-#pragma unroll
-      for (int q = 0; q < L; ++q) Bp[(q * LK_KC + kk) * NP + j] = b[q] + (q == p0 ? e : 0ull);
-    }
-    __syncthreads();
-    if (active) {
-      for (int kk = 0; kk < kc; ++kk) {
-        const ulonglong2 d = *reinterpret_cast<const ulonglong2*>(Ds + kk * MP + i0);
-        const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(As + (l * LK_KC + kk) * MP + i0);
-        const ulonglong2* bp = reinterpret_cast<const ulonglong2*>(Bp + (l * LK_KC + kk) * NP + j0);
-        const ulonglong2* ep = reinterpret_cast<const ulonglong2*>(Es + kk * NP + j0);
-        const ulonglong2 b01 = bp[0], b23 = bp[1], e01 = ep[0], e23 = ep[1];
-        const u64 bv[4] = {b01.x, b01.y, b23.x, b23.y}, ev[4] = {e01.x, e01.y, e23.x, e23.y};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          acc[0][q] += d.x * bv[q] + a.x * ev[q];
-          acc[1][q] += d.y * bv[q] + a.y * ev[q];
-        }
-      }
-    }
-  }
-  if (active) {
-#pragma unroll
-    for (int ii = 0; ii < 2; ++ii)
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (i0 + ii < M && j0 + q < N)
-          atomicAdd(reinterpret_cast<unsigned long long*>(Z + l * sZ + (i64)(i0 + ii) * N + j0 + q),
-                    (unsigned long long)acc[ii][q]);
-  }
-}
-
 namespace {
 template <int L>
 int launch_thin(i64 batch, cudaStream_t s, uint64_t* Z, int64_t sZ, int64_t bZ, const uint64_t* C, int64_t sC,
@@ -713,41 +613,14 @@ int launch_thin(i64 batch, cudaStream_t s, uint64_t* Z, int64_t sZ, int64_t bZ, 
 #undef TALL_CASE
     return launch_status();
   }
-  // long-K, small output
-  const int MP = (M + 1) & ~1, NP = (N + 3) & ~3;
-  const size_t smem = 8 * ((size_t)(L + 1) * LK_KC * MP + (size_t)(L + 1) * LK_KC * NP);
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(k_beaver_longk<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
-        cudaSuccess)
-      return MPX_ERR_CUDA;
-    attr = true;
-  }
-  const i64 nchunks = ((i64)K + LK_KC - 1) / LK_KC;
-  int occ = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_beaver_longk<L>, 256, smem) != cudaSuccess || occ < 1)
-    occ = 1;
-  const i64 ctas_target = max((i64)1, (i64)148 * occ / batch);
-  const int per = (int)max((i64)1, (nchunks + ctas_target - 1) / ctas_target);
-  const i64 ctas = (nchunks + per - 1) / per;
-  for (i64 b = 0; b < batch; ++b)
-    if (cudaMemcpy2DAsync(Z + b * bZ, (size_t)sZ * 8, C + b * bC, (size_t)sC * 8, (size_t)((i64)M * N * 8),
-                          (size_t)L, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-      return MPX_ERR_CUDA;
-  k_beaver_longk<L><<<dim3((unsigned)ctas, (unsigned)batch), 256, smem, s>>>(Z, sZ, bZ, A, sA, bA, X, Y, B, sB, bB, M,
-                                                                           K, N, p0, per);
-  return launch_status();
+  return MPX_ERR_ARG;
 }
 
 // shapes the thin kernels take (MPX_THIN=0 disables them for A/B runs)
 bool thin_fits(int L, i64 M, i64 K, i64 N, int width) {
   if (const char* e = getenv("MPX_THIN"))
     if (atoi(e) == 0) return false;
-  if (width != 64 && !(K <= 32 && N <= 32)) return false;  // atomics wrap mod 2^64 only
-  if (K <= 32 && N <= 32 && M >= 4096) return true;
-  const i64 MP = (M + 1) & ~1, NP = (N + 3) & ~3;
-  return width == 64 && L * (MP / 2) * (NP / 4) <= 256 && K >= 256 &&
-         8 * (L + 1) * LK_KC * (MP + NP) <= 160 * 1024;
+  return K <= 32 && N <= 32 && M >= 4096;
 }
 }  // namespace
 

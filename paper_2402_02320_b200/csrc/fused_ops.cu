@@ -61,8 +61,14 @@ struct Tape {
 // (Reciprocal 56/80/96/146, Exp 47/72/128/168 for L = 1..4); a bare
 // minBlocks = 1 lets it take 255 and halves occupancy (Reciprocal 2^24 at
 // n = 2: 11.1 vs 8.0 ms)
-#define MPX_MINB_RCP1(L) ((L) <= 2 ? 6 : (L) == 3 ? 5 : 3)
-#define MPX_MINB_EXP1(L) ((L) <= 2 ? 6 : (L) == 3 ? 4 : 3)
+#ifndef MPX_RCP1_MINB2
+#define MPX_RCP1_MINB2 6
+#endif
+#ifndef MPX_EXP1_MINB2
+#define MPX_EXP1_MINB2 6
+#endif
+#define MPX_MINB_RCP1(L) ((L) <= 2 ? MPX_RCP1_MINB2 : (L) == 3 ? 5 : 3)
+#define MPX_MINB_EXP1(L) ((L) <= 2 ? MPX_EXP1_MINB2 : (L) == 3 ? 4 : 3)
 #define MPX_MINB_LG(L, G, B2) ((G) > 1 && (L) >= 4 ? MPX_MINB_SPLIT : MPX_MINB_L(L, B2))
 
 #ifndef MPX_LOG_MINB
@@ -1049,7 +1055,9 @@ template <int L, int G>
 __device__ __forceinline__ void softmax_row(i64 row, u64* __restrict__ eout, u64* __restrict__ rout,
                                             const u64* __restrict__ in, i64 rows, int d0, const Tape& tape,
                                             const SoftmaxSegs& sg, const FusedParams& Pm, const FusedParams& Pe,
-                                            const FusedParams& Pr, u64* sm_vals) {
+                                            const FusedParams& Pr, u64* sm_vals, int nreal = 1 << 30) {
+  // nreal < L * GS(G): trailing dummy party slots (zero shares, zero staged
+  // material) pad n = 3 to four lanes; they never touch global memory
   const int p0 = Pm.p0;
   const u64 m64 = ring_mask(64), m32 = ring_mask(sg.w32);
   const int j = threadIdx.x / GS(G);  // lanes j*G .. j*G+G-1 own column j, L parties each
@@ -1059,7 +1067,7 @@ __device__ __forceinline__ void softmax_row(i64 row, u64* __restrict__ eout, u64
   if (j < d0) {
     const i64 e = row * d0 + j;
 #pragma unroll
-    for (int l = 0; l < L; ++l) v.v[l] = in[((i64)PI(l) * rows + row) * d0 + j];
+    for (int l = 0; l < L; ++l) v.v[l] = PI(l) < nreal ? in[((i64)PI(l) * rows + row) * d0 + j] : 0ull;
     if (sg.resc >= 0) {  // truncate(scale_fixed(x, log2 e), p) (derived.py:55-83)
       int ti = sg.resc;
       const Sh<L> sc = sh_scale<L, G>(v, sg.log2e_p, 0ull, p0, m64);
@@ -1114,7 +1122,8 @@ __device__ __forceinline__ void softmax_row(i64 row, u64* __restrict__ eout, u64
     int ti = sg.attexp;
     ev = d_attexp<L, G>(sh, tape, ti, row * (i64)d0 + j, Pe);
 #pragma unroll
-    for (int l = 0; l < L; ++l) eout[((i64)PI(l) * rows + row) * d0 + j] = ev.v[l];
+    for (int l = 0; l < L; ++l)
+      if (PI(l) < nreal) eout[((i64)PI(l) * rows + row) * d0 + j] = ev.v[l];
   }
 #pragma unroll
   for (int l = 0; l < L; ++l) {
@@ -1135,7 +1144,8 @@ __device__ __forceinline__ void softmax_row(i64 row, u64* __restrict__ eout, u64
     int ti = sg.recip;
     const Sh<L> r = d_reciprocal<L, G>(tot, tape, ti, row, Pr);
 #pragma unroll
-    for (int l = 0; l < L; ++l) rout[(i64)PI(l) * rows + row] = r.v[l];
+    for (int l = 0; l < L; ++l)
+      if (PI(l) < nreal) rout[(i64)PI(l) * rows + row] = r.v[l];
   }
   __syncthreads();
 }
@@ -1165,7 +1175,8 @@ struct StagePlan {
   int off[TAPE_MAX][3];     // word offset of (take, array) in the stage
   int len[TAPE_MAX][3];     // words per party (0: array unused)
   int words;                // total staged words
-  int nparties;
+  int nparties;             // staged party slots (lanes x parties per lane)
+  int nreal;                // real parties; slots beyond hold zeros
 };
 
 __device__ __forceinline__ i64 stage_lo(const MatRef& t, int a, i64 e_lo) {
@@ -1212,14 +1223,17 @@ __global__ void __launch_bounds__(256 * G) k_softmax_staged(u64* __restrict__ eo
       const MatRef& m = tape.m[ti];
       const u64* src = a == 0 ? m.p0 : (a == 1 ? m.p1 : m.p2);
       const i64 sps = a == 0 ? m.ps0 : (a == 1 ? m.ps1 : m.ps2);
-      src += l * sps + stage_lo(m, a, row * plan.cnt[ti]);
+      const bool real = l < plan.nreal;              // dummy slots: zero fill (no global read)
+      src += (real ? l * sps : 0) + stage_lo(m, a, row * plan.cnt[ti]);
       const uint32_t dst = (uint32_t)__cvta_generic_to_shared(stage + plan.off[ti][a] + l * len);
+      const uint32_t nb = real ? 8u : 0u;
       for (int i = 0; i < len; ++i)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8 * i), "l"(src + i) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst + 8 * i), "l"(src + i), "r"(nb)
+                     : "memory");
     }
     asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
     __syncthreads();
-    softmax_row<L, G | MPX_STAGED>(row, eout, rout, in, rows, d0, st, sg, Pm, Pe, Pr, vals);
+    softmax_row<L, G | MPX_STAGED>(row, eout, rout, in, rows, d0, st, sg, Pm, Pe, Pr, vals, plan.nreal);
   }
 }
 
@@ -1244,6 +1258,11 @@ extern "C" int mpx_softmax_fused(uint64_t* e_out, uint64_t* r_out, const uint64_
   static StagePlan plan;
   bool staged = true;
   if (const char* e = getenv("MPX_SOFTMAX_STAGE")) staged = atoi(e) != 0;
+  // n = 3: one party per lane, four lanes per column (the fourth a zero
+  // dummy), so each lane carries a third of the row chain's arithmetic
+  bool split3 = Pm.L == 3;
+  if (const char* e = getenv("MPX_SOFTMAX_SPLIT3")) split3 = split3 && atoi(e) != 0;
+  const int slots = split3 ? 4 : Pm.L;
   if (staged) {
     int cur = 0;
     for (int ti = 0; ti < tp.n; ++ti) {
@@ -1269,21 +1288,23 @@ extern "C" int mpx_softmax_fused(uint64_t* e_out, uint64_t* r_out, const uint64_
         }
         plan.off[ti][a] = cur;
         plan.len[ti][a] = len;
-        cur += ((len * Pm.L + 1) / 2) * 2;                      // 16-byte aligned regions
+        cur += ((len * slots + 1) / 2) * 2;                     // 16-byte aligned regions
       }
     }
     plan.words = cur;
-    plan.nparties = Pm.L;                                        // every local party (all lanes)
+    plan.nparties = slots;                                       // every local party (all lanes)
+    plan.nreal = Pm.L;
     // at least four warps per row: the staging copy is spread over every thread
-    const int sthreads = max(threads, 128);
-    const size_t ssm = (sizeof(Tape) + 15) / 16 * 16 + (size_t)cur * 8 + (size_t)Pm.L * (d0 + sthreads / 32) * 8;
+    const int cthreads = split3 ? max(32, ((4 * d0 + 31) / 32) * 32) : threads;
+    const int sthreads = max(cthreads, 128);
+    const size_t ssm = (sizeof(Tape) + 15) / 16 * 16 + (size_t)cur * 8 + (size_t)slots * (d0 + sthreads / 32) * 8;
     if (ssm > 200 * 1024) staged = false;
     else {
       static size_t attr_set = 0;
       if (ssm > attr_set) {
         const void* fns[] = {(const void*)k_softmax_staged<1, 1>, (const void*)k_softmax_staged<2, 1>,
                              (const void*)k_softmax_staged<3, 1>, (const void*)k_softmax_staged<4, 1>,
-                             (const void*)k_softmax_staged<4, 2>};
+                             (const void*)k_softmax_staged<4, 2>, (const void*)k_softmax_staged<1, 4>};
         for (const void* f : fns)
           if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm) != cudaSuccess)
             return MPX_ERR_CUDA;
@@ -1292,7 +1313,12 @@ extern "C" int mpx_softmax_fused(uint64_t* e_out, uint64_t* r_out, const uint64_
       switch (Pm.L) {
         case 1: k_softmax_staged<1, 1><<<g, sthreads, ssm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr, plan); break;
         case 2: k_softmax_staged<2, 1><<<g, sthreads, ssm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr, plan); break;
-        case 3: k_softmax_staged<3, 1><<<g, sthreads, ssm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr, plan); break;
+        case 3:
+          if (split3)
+            k_softmax_staged<1, 4><<<g, sthreads, ssm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr, plan);
+          else
+            k_softmax_staged<3, 1><<<g, sthreads, ssm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr, plan);
+          break;
         case 4: k_softmax_staged<4, 1><<<g, sthreads, ssm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr, plan); break;
         default: k_softmax_staged<4, 2><<<g, sthreads, ssm, s>>>(e_out, r_out, x, rows, d0, tp, sg, Pm, Pe, Pr, plan); break;
       }

@@ -39,7 +39,7 @@ def mul(session, x: AShare, y: AShare) -> AShare:
         K.mul_fused(z, x.values, y.values, a.ptr, b.ptr, c.ptr, a.ps, L, n, w, session.p0)
         session.exchange(payload=2 * arith_payload(w, n))
     else:
-        d, e = session.alloc((n,)), session.alloc((n,))
+        d, e = session.alloc((2, n)).unbind(0)          # one contiguous round payload
         K.mask_sub(d, x.values, a.ptr, a.ps, L, n, w)
         K.mask_sub(e, y.values, b.ptr, b.ps, L, n, w)
         d, e = session.exchange(arith=[(d, w), (e, w)])
@@ -72,16 +72,24 @@ def batch_matmul(session, pairs) -> list[AShare]:
     groups = _groups(session, pairs, trip)
     masked = []
     fused_payload = 0
+    unfused = [g for g in groups if not (_fused_tc(session, *_gshape(pairs, g)) or
+                                          _fused_simt(session, *_gshape(pairs, g)))]
+    # every masked D, E of the round in ONE buffer: party mode opens it with a
+    # single collective, no concatenation
+    arena = session.alloc((sum(len(g) * (pairs[g[0]][0].size + pairs[g[0]][1].size) for g in unfused),))
+    at = 0
     for g in groups:
         x0, y0 = pairs[g[0]]
         w, (m, k), r = x0.width, x0.shape, y0.shape[1]
-        if _fused_tc(session, m, k, r, w) or _fused_simt(session, m, k, r, w):
+        if g not in unfused:
             # sim mode: mask + open + limb split (or SIMT reconstruction) fused
             # below (one round, same logical payload as the reference's D, E openings)
             fused_payload += len(g) * (arith_payload(w, m * k) + arith_payload(w, k * r))
             continue
-        D = session.alloc((len(g), m * k))
-        E = session.alloc((len(g), k * r))
+        D = arena[at:at + len(g) * m * k].view(len(g), m * k)
+        at += len(g) * m * k
+        E = arena[at:at + len(g) * k * r].view(len(g), k * r)
+        at += len(g) * k * r
         _mask_group(D, [pairs[i][0].values for i in g], [trip[i][0] for i in g], L, m, k, w)
         _mask_group(E, [pairs[i][1].values for i in g], [trip[i][1] for i in g], L, k, r, w)
         for j in range(len(g)):
@@ -117,6 +125,11 @@ def batch_matmul(session, pairs) -> list[AShare]:
 # — the persistent GEMM holds every SM's shared memory, so nothing co-runs
 CONCURRENT_GROUPS = os.environ.get("MPX_CONCURRENT_GROUPS", "0") != "0"
 _SIDE: dict = {}
+
+
+def _gshape(pairs, g):
+    x0, y0 = pairs[g[0]]
+    return x0.shape[0], x0.shape[1], y0.shape[1], x0.width
 
 
 def _side_stream(device, i: int):
@@ -376,7 +389,7 @@ def and_gate(session, x: BShare, y: BShare) -> BShare:
     y = y.like_layout(x)
     L, rows, m = session.L, x.rows, x.m
     t = session.store.take_bin_triples(x.size)
-    d, e = session.alloc((rows,)), session.alloc((rows,))
+    d, e = session.alloc((2, rows)).unbind(0)
     K.and_mask(d, e, x.words, y.words, t, L, rows, m)
     d, e = session.exchange(bits=[d, e], payload=2 * bits_payload(x.size))
     z = session.alloc(x.words.shape)
@@ -402,9 +415,10 @@ def _carry_prefix(session, G: torch.Tensor, P: torch.Tensor, m: int, rows: int) 
             K.carry_fused(G, P, t, L, rows, m, s, last, session.p0)
             session.exchange(payload=2 * bits_payload(cnt))
         else:
-            dg, eg = session.alloc((rows,)), session.alloc((rows,))
-            dp = None if last else session.alloc((rows,))
-            ep = None if last else session.alloc((rows,))
+            pay = session.alloc((2 if last else 4, rows)).unbind(0)
+            dg, eg = pay[0], pay[1]
+            dp = None if last else pay[2]
+            ep = None if last else pay[3]
             K.carry_mask(dg, eg, dp, ep, G, P, t, L, rows, m, s, last)
             parts = [dg, eg] if last else [dg, eg, dp, ep]
             got = session.exchange(bits=parts, payload=2 * bits_payload(cnt))

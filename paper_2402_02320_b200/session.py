@@ -312,6 +312,24 @@ class ThreadComm:
         K.open_sum(flat, g, self.world, flat.numel(), 64)
 
 
+class LoopbackComm:
+    """Timing stand-in for ONE party of an n-party deployment on one GPU: the
+    collectives keep (sum) or replicate (gather) this party's own partial, so
+    opened values are meaningless, but every kernel, tensor size and round
+    of the one-party-per-GPU (L = 1) path runs exactly as deployed; it is
+    CUDA-graph capturable. bench.py reports the party's compute time per step
+    with it (the communication is what the n-GPU run adds)."""
+
+    def __init__(self, n: int):
+        self.world = n
+
+    def allreduce_sum_(self, flat: torch.Tensor) -> None:
+        return None
+
+    def allgather(self, flat: torch.Tensor) -> torch.Tensor:
+        return flat.unsqueeze(0).expand(self.world, flat.numel()).contiguous()
+
+
 class PartySession(_Session):
     """One party per process/GPU; openings are collectives over the party group.
 
@@ -342,24 +360,53 @@ class PartySession(_Session):
     def _collective(self, arith, bits):
         outs = []
         if arith:
-            flat = torch.cat([t.reshape(-1) for t in arith]) if len(arith) > 1 else arith[0].reshape(-1)
-            self.comm.allreduce_sum_(flat)
-            self.metrics.physical_bytes += flat.numel() * 8
-            off = 0
-            for t in arith:
-                outs.append(flat[off:off + t.numel()].view(t.shape))
-                off += t.numel()
+            cover = _covering(arith)
+            if cover is not None:          # the round's payloads tile one buffer: reduce it in place
+                self.comm.allreduce_sum_(cover)
+                self.metrics.physical_bytes += cover.numel() * 8
+                outs.extend(arith)
+            else:
+                flat = torch.cat([t.reshape(-1) for t in arith])
+                self.comm.allreduce_sum_(flat)
+                self.metrics.physical_bytes += flat.numel() * 8
+                off = 0
+                for t in arith:
+                    outs.append(flat[off:off + t.numel()].view(t.shape))
+                    off += t.numel()
         if bits:
-            flat = torch.cat([t.reshape(-1) for t in bits]) if len(bits) > 1 else bits[0].reshape(-1)
+            cover = _covering(bits)
+            flat = cover if cover is not None else torch.cat([t.reshape(-1) for t in bits])
             gathered = self.comm.allgather(flat)
             self.metrics.physical_bytes += flat.numel() * 8 * (self.world - 1)
-            red = torch.empty_like(flat)
-            K.open_xor(red, gathered, self.world, flat.numel())
-            off = 0
-            for t in bits:
-                outs.append(red[off:off + t.numel()].view(t.shape))
-                off += t.numel()
+            K.open_xor(flat, gathered, self.world, flat.numel())   # XOR of every party's partial, in place
+            if cover is not None:
+                outs.extend(bits)
+            else:
+                off = 0
+                for t in bits:
+                    outs.append(flat[off:off + t.numel()].view(t.shape))
+                    off += t.numel()
         return outs
+
+
+def _covering(ts):
+    """A flat contiguous view covering exactly the tensors ``ts`` when they
+    tile one range of one storage (any order), else None."""
+    if len(ts) == 1:
+        t = ts[0]
+        return t.view(-1) if t.is_contiguous() else None
+    if any(not t.is_contiguous() or t.untyped_storage().data_ptr() != ts[0].untyped_storage().data_ptr()
+           for t in ts):
+        return None
+    spans = sorted((t.data_ptr(), t.numel()) for t in ts)
+    for (p, n), (q, _) in zip(spans, spans[1:]):
+        if p + 8 * n != q:
+            return None
+    base = ts[0].untyped_storage()
+    lo = spans[0][0]
+    total = sum(n for _, n in spans)
+    off = (lo - base.data_ptr()) // 8
+    return torch.empty(0, dtype=torch.int64, device=ts[0].device).set_(base, off, (total,), (1,))
 
 
 # ---------------------------------------------------------------------------
@@ -388,4 +435,5 @@ def demands_by_name(counter: DemandCounter) -> dict[str, int]:
     return {k.name(): c for k, c in sorted(counter.demands.items(), key=lambda kv: kv[0].name()) if c > 0}
 
 
-__all__ = ["SimSession", "PartySession", "DistComm", "ThreadHub", "run_sim", "dry_run", "demands_by_name", "MaterialKey"]
+__all__ = ["SimSession", "PartySession", "DistComm", "ThreadHub", "LoopbackComm", "run_sim", "dry_run",
+           "demands_by_name", "MaterialKey"]

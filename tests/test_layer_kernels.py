@@ -295,7 +295,7 @@ def test_mask_limbs2_matches_two_launches(K, L, p0, jobs, m, k, r, xt, yt):
     (2, 1, 2, 5000, 10, 16, False, True, 64),
     (4, 3, 1, 4100, 32, 32, True, False, 32),
     (3, 2, 1, 4096, 7, 5, False, False, 64),
-    (3, 0, 1, 25, 73728, 20, True, False, 64),   # LeNet conv1 weight gradient at batch 128
+    (3, 0, 1, 25, 73728, 20, True, False, 64),   # LeNet conv1 weight gradient at batch 128 (split-K tiles)
     (4, 1, 1, 10, 700, 9, False, True, 64),
 ])
 @pytest.mark.parametrize("thin", ["1", "0"])
