@@ -404,6 +404,48 @@ int mpx_deal_share_arith_dk(uint64_t* out, int64_t out_ps, const uint64_t* secre
 int mpx_deal_share_bits_dk(uint64_t* out, int64_t out_ps, const uint64_t* secret_words, const uint64_t* dkey,
                            int64_t u32_base, int64_t count, int n, int p_lo, int L, void* stream);
 
+/* Thin sim-mode Beaver product on tcgen05 (basic.py:66-75), operand limbs
+ * built in shared memory: Z_l = C_l + [D | A_l] @ [B_l + [l==p0] E ; E] with
+ * D = sum_l X_l - A_l, E = sum_l Y_l - B_l, for K <= 32, N <= 32, L = 2..3
+ * local parties (LeNet conv1 forward). Z, C [L][M][N], A [L][M][K],
+ * B [L][K][N] at party strides; X (M x K), Y (K x N) at (party, row, col)
+ * strides. */
+int mpx_beaver_tc_thin(uint64_t* Z, int64_t sZ, const uint64_t* C, int64_t sC, const uint64_t* X,
+                       int64_t x_ps, int64_t x_sr, int64_t x_sc, const uint64_t* A, int64_t sA,
+                       const uint64_t* Y, int64_t y_ps, int64_t y_sr, int64_t y_sc, const uint64_t* B,
+                       int64_t sB, int L, int64_t M, int64_t K, int64_t N, int p0, int width, void* stream);
+
+/* ---- fused per-kind dealer: ONE launch per material key ----
+ * Each thread draws its group's secrets straight from the key's stream (draw
+ * order SURVEY App. A4 / preprocessing.py:139-171), derives c = a*b or
+ * c = a & b in registers and writes only the local parties' shares
+ * (p_lo..p_lo+L-1; party stride `ps` elements or words). `dkey` (nullable)
+ * overrides (k0, k1) with a device key slot read at launch (CUDA-graph
+ * re-deals). Replaces the draw -> store -> share kernel chains above. */
+/* triple (preprocessing.py:139-145): out a, b, c [L][count] */
+int mpx_deal_triple(uint64_t* a, uint64_t* b, uint64_t* c, int64_t ps, uint64_t k0, uint64_t k1,
+                    const uint64_t* dkey, int64_t count, int n, int p_lo, int L, int width, void* stream);
+/* one drawn secret per element at u32 offset q_secret, masked to
+ * min(width, secret_bits) bits, optionally stored to secret_out (count
+ * elems), shared with draws at q_shares + p*2*count: mtriple A / B
+ * (preprocessing.py:146-152) and edaBit values + arithmetic shares (:165-170). */
+int mpx_deal_gen_arith(uint64_t* out, int64_t ps, uint64_t* secret_out, uint64_t k0, uint64_t k1,
+                       const uint64_t* dkey, int64_t q_secret, int64_t q_shares, int64_t count, int n,
+                       int p_lo, int L, int secret_bits, int width, void* stream);
+/* bintriple (preprocessing.py:153-159): packed bit streams a, b, c [L][words] */
+int mpx_deal_bintriple(uint64_t* a, uint64_t* b, uint64_t* c, int64_t ps, uint64_t k0, uint64_t k1,
+                       const uint64_t* dkey, int64_t count, int n, int p_lo, int L, void* stream);
+/* daBit (preprocessing.py:160-164): arithmetic shares [L][count], bit shares [L][words] */
+int mpx_deal_dabit(uint64_t* arith, int64_t arith_ps, uint64_t* bit_words, int64_t bit_ps, uint64_t k0,
+                   uint64_t k1, const uint64_t* dkey, int64_t count, int n, int p_lo, int L, int width,
+                   void* stream);
+/* edaBit bit shares (preprocessing.py:165-170): the m low bits of each value
+ * (value draw at u32 offset 0) as a packed stream, shared with draws of
+ * count*m bytes at q_shares. */
+int mpx_deal_edabit_bits(uint64_t* bit_words, int64_t ps, uint64_t k0, uint64_t k1, const uint64_t* dkey,
+                         int64_t q_shares, int64_t count, int m, int width, int n, int p_lo, int L,
+                         void* stream);
+
 #ifdef __cplusplus
 }
 #endif

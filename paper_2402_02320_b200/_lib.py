@@ -91,6 +91,13 @@ _SIGS = {
     "mpx_philox_bits_dk": [_P, _P, _L, _L, _P],
     "mpx_deal_share_arith_dk": [_P, _L, _P, _P, _L, _L, _I, _I, _I, _I, _P],
     "mpx_deal_share_bits_dk": [_P, _L, _P, _P, _L, _L, _I, _I, _I, _P],
+    "mpx_beaver_tc_thin": [_P, _L, _P, _L, _P, _L, _L, _L, _P, _L, _P, _L, _L, _L, _P, _L, _I, _L, _L, _L, _I, _I,
+                           _P],
+    "mpx_deal_triple": [_P, _P, _P, _L, _U, _U, _P, _L, _I, _I, _I, _I, _P],
+    "mpx_deal_gen_arith": [_P, _L, _P, _U, _U, _P, _L, _L, _L, _I, _I, _I, _I, _I, _P],
+    "mpx_deal_bintriple": [_P, _P, _P, _L, _U, _U, _P, _L, _I, _I, _I, _P],
+    "mpx_deal_dabit": [_P, _L, _P, _L, _U, _U, _P, _L, _I, _I, _I, _I, _P],
+    "mpx_deal_edabit_bits": [_P, _L, _U, _U, _P, _L, _L, _I, _I, _I, _I, _I, _P],
 }
 
 # entry points without a stream argument (bound with their own argtypes)

@@ -1452,3 +1452,298 @@ int mpx_gemm_tc(uint64_t*, const uint64_t*, const uint64_t*, int64_t, int64_t, i
                 int64_t, int64_t, int, int, cudaStream_t) {
   return MPX_ERR_UNSUPPORTED;  // the u64 entry point needs caller scratch: see mpx_gemm_limbs
 }
+
+// --------------------------------------------------------------------------
+// Thin sim-mode Beaver products on tcgen05 with the operand limbs built in
+// shared memory (no limb planes in HBM):
+//     Z_l = C_l + [D | A_l] @ [B_l + [l == p0] E ; E]        (basic.py:66-75)
+// with D = sum_l X_l - A_l and E = sum_l Y_l - B_l (the openings are local
+// sums: all parties live on this GPU), for K <= 32 and N <= 32 (LeNet's conv1
+// forward: 73728 x 25 x 20 at three parties). One persistent CTA per SM:
+//  * warps 0-3 own one row each of a 128-row tile. Per party they stage the
+//    32 rows of X_l, then of A_l, of their warp through shared memory (coalesced
+//    reads at any X strides), accumulate D in registers and write the u8
+//    limb tile of A_l, then D's, in the UMMA K-major 32-byte-swizzle layout
+//    (16-byte chunk c of row r at chunk c ^ bit 2 of r);
+//  * lane 0 of warp 4 issues per party the 72 limb MMAs of the two 32-byte
+//    k-blocks (D x B'_l, then A_l x E; diagonal i+j accumulates in TMEM
+//    columns 32(i+j) of the party's 256-column buffer, two buffers);
+//  * warps 0-3 drain a party's 8 diagonals (tcgen05.ld), recombine the limbs
+//    mod 2^64, hand the buffer back and store Z_l = C_l + acc through the
+//    staging tile (coalesced rows).
+// B'_l and E limb tiles (32 x 32 bytes each) are built once per CTA.
+#define THIN_TA (128 * 32)  // one limb tile of the A side: 128 rows x 32 bytes
+#define THIN_TB (32 * 32)   // one limb tile of the B side: 32 rows (N) x 32 bytes
+
+struct ThinArgs {
+  u64* Z;
+  i64 sZ;
+  const u64* C;
+  i64 sC;
+  const u64* X;
+  i64 x_ps, x_sr, x_sc;
+  const u64* A;
+  i64 sA;
+  const u64* Y;
+  i64 y_ps, y_sr, y_sc;
+  const u64* B;
+  i64 sB;
+  int M, K, N, p0, L;
+  u64 msk;
+};
+
+__device__ __forceinline__ void thin_put16(uint8_t* tile, int r, int c, u64 lo, u64 hi) {
+  const int pc = c ^ ((r >> 2) & 1);
+  *reinterpret_cast<ulonglong2*>(tile + r * 32 + pc * 16) = make_ulonglong2(lo, hi);
+}
+
+// 32 values (k = 0..31) of one row -> row r of the 8 limb tiles at `base`
+// (tile stride `ts` bytes)
+__device__ __forceinline__ void thin_emit_row(uint8_t* base, int ts, int r, const u64 (&v)[32]) {
+  u64 pl[4][8];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    u64 w[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) w[c] = v[8 * g + c];
+    bytes_transpose8(w, pl[g]);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    thin_put16(base + i * ts, r, 0, pl[0][i], pl[1][i]);
+    thin_put16(base + i * ts, r, 1, pl[2][i], pl[3][i]);
+  }
+}
+
+constexpr int thin_smem_bytes(int L) {
+  // D + L A_l tiles, L B'_l + E tiles, per-warp staging (32 x 33 u64), barriers
+  return 8 * THIN_TA * (1 + L) + 8 * THIN_TB * (L + 1) + 4 * 32 * 33 * 8 + 1024 + 1024;
+}
+
+template <int L>
+__global__ void __launch_bounds__(160, 1) k_beaver_tc_thin(const __grid_constant__ ThinArgs a) {
+  extern __shared__ __align__(1024) uint8_t thin_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)thin_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sD = smem;                          // 8 limb tiles
+  uint8_t* sA = sD + 8 * THIN_TA;              // [L][8] limb tiles
+  uint8_t* sBp = sA + L * 8 * THIN_TA;         // [L][8] B'_l limb tiles
+  uint8_t* sE = sBp + L * 8 * THIN_TB;         // [8] E limb tiles
+  u64* stg = reinterpret_cast<u64*>(sE + 8 * THIN_TB);  // [4 warps][32][33]
+  uint64_t* tf = reinterpret_cast<uint64_t*>(stg + 4 * 32 * 33);  // [2] MMA done per buffer
+  uint64_t* te = tf + 2;                                               // [2] buffer drained
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(te + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = a.K, N = a.N;
+  const int KP = 33;  // staging pitch (u64): odd, conflict-free row reads
+
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tf[b], 1);
+      mbar_init(&te[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // B side once per CTA: E = sum_l Y_l - B_l; B'_l = B_l + [l == p0] E (rows = n, bytes = k)
+  if (warp < 4) {
+    for (int job = threadIdx.x; job < (L + 1) * 32; job += 128) {
+      const int n = job & 31, which = job >> 5;  // which < L: B'_which, == L: E
+      u64 v[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        u64 e = 0, bw = 0;
+        if (k < K && n < N) {
+#pragma unroll
+          for (int l = 0; l < L; ++l) {
+            const u64 b = a.B[l * a.sB + (i64)k * N + n];
+            e += a.Y[l * a.y_ps + (i64)k * a.y_sr + (i64)n * a.y_sc] - b;
+            if (l == which) bw = b;
+          }
+        }
+        v[k] = which == L ? e : bw + (which == a.p0 ? e : 0ull);
+      }
+      thin_emit_row(which == L ? sE : sBp + which * 8 * THIN_TB, THIN_TB, n, v);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_holder;
+  const int tiles = (a.M + 127) / 128;
+  const uint32_t idesc = (2u << 4) | ((uint32_t)(32 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+
+  int job = 0;  // running (tile, party) index: TMEM buffer job & 1
+  for (int t = blockIdx.x; t < tiles; t += gridDim.x, job += L) {
+    const i64 r0 = (i64)t * 128;
+    if (warp < 4) {
+      // ---- produce: limb tiles of A_l (each party) and D ----
+      u64* sx = stg + warp * 32 * KP;
+      const i64 wr0 = r0 + warp * 32;
+      const int rows = (int)max((i64)0, min((i64)32, (i64)a.M - wr0));
+      u64 d[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) d[k] = 0;
+      for (int l = 0; l < L; ++l) {
+        const u64* Xl = a.X + l * a.x_ps + wr0 * a.x_sr;
+        const u64* Al = a.A + l * a.sA + wr0 * (i64)K;
+        // X_l rows, then A_l rows, through the warp's staging tile
+        __syncwarp();
+        for (int idx = lane; idx < 32 * K; idx += 32) {
+          const int rr = idx / K, k = idx - rr * K;
+          sx[rr * KP + k] = rr < rows ? Xl[(i64)rr * a.x_sr + (i64)k * a.x_sc] : 0ull;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          if (k < K) d[k] += sx[lane * KP + k];
+        __syncwarp();
+        for (int idx = lane; idx < 32 * K; idx += 32) {
+          const int rr = idx / K, k = idx - rr * K;
+          sx[rr * KP + k] = rr < rows ? Al[(i64)rr * K + k] : 0ull;
+        }
+        __syncwarp();
+        u64 v[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          v[k] = k < K ? sx[lane * KP + k] : 0ull;
+          d[k] -= v[k];
+        }
+        thin_emit_row(sA + l * 8 * THIN_TA, THIN_TA, warp * 32 + lane, v);
+      }
+#pragma unroll
+      for (int k = 0; k < 32; ++k) d[k] &= a.msk;
+      thin_emit_row(sD, THIN_TA, warp * 32 + lane, d);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();  // limb tiles of this tile complete
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 4) {
+      if (lane == 0) {
+        // ---- MMA issue: per party two k-blocks of 36 limb products ----
+        for (int l = 0; l < L; ++l) {
+          const int j = job + l, buf = j & 1;
+          if (j >= 2) mbar_wait(&te[buf], (uint32_t)(((j - 2) >> 1) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t dt = tmem_base + (uint32_t)(buf * 256);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint64_t ad = umma_desc_sw<32>(smem_u32(sD + i * THIN_TA));
+#pragma unroll
+            for (int jj = 0; jj <= 7 - i; ++jj)
+              mma_i8(dt + (uint32_t)((i + jj) * 32), ad,
+                     umma_desc_sw<32>(smem_u32(sBp + (l * 8 + jj) * THIN_TB)), idesc, i > 0 ? 1u : 0u);
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint64_t ad = umma_desc_sw<32>(smem_u32(sA + (l * 8 + i) * THIN_TA));
+#pragma unroll
+            for (int jj = 0; jj <= 7 - i; ++jj)
+              mma_i8(dt + (uint32_t)((i + jj) * 32), ad, umma_desc_sw<32>(smem_u32(sE + jj * THIN_TB)), idesc, 1u);
+          }
+          umma_commit(&tf[buf]);
+        }
+      }
+      __syncwarp();
+    } else {
+      // ---- epilogue: drain, recombine, Z_l = C_l + acc (coalesced via staging) ----
+      u64* st = stg + warp * 32 * KP;
+      const i64 wr0 = r0 + warp * 32;
+      const int rows = (int)max((i64)0, min((i64)32, (i64)a.M - wr0));
+      for (int l = 0; l < L; ++l) {
+        const int j = job + l, buf = j & 1;
+        mbar_wait(&tf[buf], (uint32_t)((j >> 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        u64 acc[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) acc[q] = 0;
+#pragma unroll
+        for (int dd = 0; dd < 8; ++dd) {
+          uint32_t v[32];
+          TMEM_LD32(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(buf * 256 + dd * 32), v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int q = 0; q < 32; ++q) acc[q] += (u64)v[q] << (8 * dd);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&te[buf]);
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          if (q < N) st[lane * KP + q] = acc[q];
+        __syncwarp();
+        const u64* Cl = a.C + l * a.sC + wr0 * (i64)N;
+        u64* Zl = a.Z + l * a.sZ + wr0 * (i64)N;
+        for (int idx = lane; idx < rows * N; idx += 32) {
+          const int rr = idx / N, q = idx - rr * N;
+          Zl[idx] = (Cl[idx] + st[rr * KP + q]) & a.msk;
+        }
+        __syncwarp();
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 4) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+  }
+}
+
+template <int L>
+static int thin_launch(const ThinArgs& a, cudaStream_t s) {
+  static bool attr = false;
+  constexpr int smem = thin_smem_bytes(L);
+  static_assert(smem <= 232448, "shared memory budget");
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_beaver_tc_thin<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return MPX_ERR_CUDA;
+    attr = true;
+  }
+  const int tiles = (a.M + 127) / 128;
+  k_beaver_tc_thin<L><<<min(tiles, num_sms()), 160, smem, s>>>(a);
+  return launch_status();
+}
+
+// Z [L][M][N], C [L][M][N], A [L][M][K], B [L][K][N] (party strides sZ, sC,
+// sA, sB); X, Y logical M x K and K x N share views at (party, row, col)
+// strides. K <= 32, N <= 32, 2 <= L <= 3 (all parties local), width 64.
+extern "C" int mpx_beaver_tc_thin(uint64_t* Z, int64_t sZ, const uint64_t* C, int64_t sC, const uint64_t* X,
+                                  int64_t x_ps, int64_t x_sr, int64_t x_sc, const uint64_t* A, int64_t sA,
+                                  const uint64_t* Y, int64_t y_ps, int64_t y_sr, int64_t y_sc, const uint64_t* B,
+                                  int64_t sB, int L, int64_t M, int64_t K, int64_t N, int p0, int width,
+                                  void* stream) {
+  CHECK_ARG(Z && C && X && A && Y && B && M >= 1 && K >= 1 && K <= 32 && N >= 1 && N <= 32);
+  CHECK_ARG(L >= 2 && L <= 3 && p0 >= -1 && p0 < L && width >= 1 && width <= 64 && M < (1ll << 31));
+  ThinArgs a;
+  a.Z = Z;
+  a.sZ = sZ;
+  a.C = C;
+  a.sC = sC;
+  a.X = X;
+  a.x_ps = x_ps;
+  a.x_sr = x_sr;
+  a.x_sc = x_sc;
+  a.A = A;
+  a.sA = sA;
+  a.Y = Y;
+  a.y_ps = y_ps;
+  a.y_sr = y_sr;
+  a.y_sc = y_sc;
+  a.B = B;
+  a.sB = sB;
+  a.M = (int)M;
+  a.K = (int)K;
+  a.N = (int)N;
+  a.p0 = p0;
+  a.L = L;
+  a.msk = ring_mask(width);
+  cudaStream_t s = (cudaStream_t)stream;
+  return L == 2 ? thin_launch<2>(a, s) : thin_launch<3>(a, s);
+}

@@ -453,6 +453,17 @@ def beaver_gemm_sim(Z, sZ, bZ, C_ptr, sC, bC, x_ptr, x_ps, x_sr, x_sc, x_js, A_p
     return Z
 
 
+def beaver_tc_thin(Z, sZ, C_ptr, sC, x_ptr, x_ps, x_sr, x_sc, A_ptr, sA, y_ptr, y_ps, y_sr, y_sc, B_ptr, sB,
+                   L, M, K, N, p0, width):
+    """Sim sessions, K <= 32 and N <= 32: Beaver opening + reconstruction on
+    tcgen05 with the limb operands built in shared memory (one launch)."""
+    if _dry(Z):
+        return Z
+    call("mpx_beaver_tc_thin", ptr(Z), sZ, C_ptr, sC, x_ptr, x_ps, x_sr, x_sc, A_ptr, sA, y_ptr, y_ps, y_sr, y_sc,
+         B_ptr, sB, L, M, K, N, p0, width)
+    return Z
+
+
 def beaver_gemm(Z, sZ, C_ptr, sC, D, E, A_ptr, sA, B_ptr, sB, L, M, K, N, p0, width):
     """Z_l = C_l + D @ (B_l + [l==p0] E) + A_l @ E (one SIMT launch, all local parties)."""
     if _dry(Z):
@@ -589,6 +600,58 @@ def deal_share_bits(out, secret, key, u32_base, count, n, p_lo, L):
         call("mpx_deal_share_bits", ptr(out), out.stride(0), ptr(secret), _u(key[0]), _u(key[1]), u32_base,
              count, n, p_lo, L)
     return out
+
+
+def _key_args(key):
+    """(k0, k1, dkey) for the fused dealer entry points: a key by value, or a
+    device key slot (int64[2]) read at launch."""
+    if isinstance(key, torch.Tensor):
+        return 0, 0, ptr(key)
+    return _u(key[0]), _u(key[1]), None
+
+
+def deal_triple(a, b, c, key, count, n, p_lo, L, width):
+    """Fused triple deal (preprocessing.py:139-145) into [L, count] share arrays."""
+    if _dry(a):
+        return a
+    k0, k1, dk = _key_args(key)
+    call("mpx_deal_triple", ptr(a), ptr(b), ptr(c), a.stride(0), k0, k1, dk, count, n, p_lo, L, width)
+    return a
+
+
+def deal_gen_arith(out, secret_out, key, q_secret, q_shares, count, n, p_lo, L, secret_bits, width):
+    """Draw + share one secret per element (mtriple A/B, edaBit values)."""
+    if _dry(out):
+        return out
+    k0, k1, dk = _key_args(key)
+    call("mpx_deal_gen_arith", ptr(out), out.stride(0), None if secret_out is None else ptr(secret_out), k0, k1, dk,
+         q_secret, q_shares, count, n, p_lo, L, secret_bits, width)
+    return out
+
+
+def deal_bintriple(a, b, c, key, count, n, p_lo, L):
+    if _dry(a):
+        return a
+    k0, k1, dk = _key_args(key)
+    call("mpx_deal_bintriple", ptr(a), ptr(b), ptr(c), a.stride(0), k0, k1, dk, count, n, p_lo, L)
+    return a
+
+
+def deal_dabit(arith, bits, key, count, n, p_lo, L, width):
+    if _dry(arith):
+        return arith
+    k0, k1, dk = _key_args(key)
+    call("mpx_deal_dabit", ptr(arith), arith.stride(0), ptr(bits), bits.stride(0), k0, k1, dk, count, n, p_lo, L,
+         width)
+    return arith
+
+
+def deal_edabit_bits(bits, key, q_shares, count, m, width, n, p_lo, L):
+    if _dry(bits):
+        return bits
+    k0, k1, dk = _key_args(key)
+    call("mpx_deal_edabit_bits", ptr(bits), bits.stride(0), k0, k1, dk, q_shares, count, m, width, n, p_lo, L)
+    return bits
 
 
 def empty(shape, like: torch.Tensor):

@@ -21,6 +21,7 @@ edaBit bits are only generated for keys whose consumer needs them
 from __future__ import annotations
 
 import hashlib
+import os
 from dataclasses import dataclass
 
 import torch
@@ -37,6 +38,11 @@ _KIND_NAMES = {KIND_TRIPLE: "triple", KIND_MATRIX_TRIPLE: "mtriple", KIND_BIN_TR
                KIND_DABIT: "dabit", KIND_EDABIT: "edabit"}
 _NAME_KINDS = {v: k for k, v in _KIND_NAMES.items()}
 _M64 = (1 << 64) - 1
+
+
+# MPX_DEALER_LEGACY=1: the draw -> store -> share kernel chain instead of the
+# fused per-kind kernels (A/B timing and cross-checks)
+LEGACY_DEALER = os.environ.get("MPX_DEALER_LEGACY", "0") not in ("", "0")
 
 
 class PreprocessingExhausted(RuntimeError):
@@ -224,6 +230,8 @@ class Dealer:
 
     def _generate(self, key: MaterialKey, count: int, need_bits: bool) -> dict:
         pk = self.key_slots[key] if self.key_slots is not None else dealer_philox_key(self.seed, key)
+        if not LEGACY_DEALER:
+            return self._generate_fused(key, count, need_bits, pk)
         w = key.width
         q = 0
         if key.kind == KIND_TRIPLE:                       # preprocessing.py:139-145
@@ -272,6 +280,48 @@ class Dealer:
                 flat = self._z(_words(count * m))
                 K.bits_rows_to_flat(flat, value, count, m)
                 res["bits"], q = self._share_bits(flat, pk, q, count * m, "bits")
+            return res
+        raise ValueError(f"unknown material kind {key.kind}")
+
+    def _generate_fused(self, key: MaterialKey, count: int, need_bits: bool, pk) -> dict:
+        """One fused launch per key (two for an edaBit with bits, three plus
+        the A @ B GEMM for a matrix triple); same draw order and results as
+        ``_generate``'s kernel chain (preprocessing.py:139-171)."""
+        n, p_lo, L, w = self.n, self.p_lo, self.L, key.width
+        if key.kind == KIND_TRIPLE:                       # preprocessing.py:139-145
+            sa, sb, sc = (self._dst(x, (L, count)) for x in "abc")
+            K.deal_triple(sa, sb, sc, pk, count, n, p_lo, L, w)
+            return {"a": sa, "b": sb, "c": sc}
+        if key.kind == KIND_MATRIX_TRIPLE:                # preprocessing.py:146-152
+            m, k, r = key.params
+            ca, cb, cc = count * m * k, count * k * r, count * m * r
+            a, b = self._e(ca), self._e(cb)
+            sa, sb, sc = self._dst("a", (L, ca)), self._dst("b", (L, cb)), self._dst("c", (L, cc))
+            q0 = 2 * (ca + cb)                              # after the A and B draws
+            K.deal_gen_arith(sa, a, pk, 0, q0, ca, n, p_lo, L, w, w)
+            K.deal_gen_arith(sb, b, pk, 2 * ca, q0 + (n - 1) * 2 * ca, cb, n, p_lo, L, w, w)
+            c = self._e(cc)
+            K.gemm(c, a, b, count, m, k, r, m * k, k * r, m * r, False, w)
+            K.deal_share_arith(sc, c, pk, q0 + (n - 1) * 2 * (ca + cb), cc, n, p_lo, L, w)
+            return {"a": sa.view(L, count, m, k), "b": sb.view(L, count, k, r), "c": sc.view(L, count, m, r)}
+        if key.kind == KIND_BIN_TRIPLE:                   # preprocessing.py:153-159
+            sa, sb, sc = (self._dst(x, (L, _words(count)), zero=True) for x in "abc")
+            K.deal_bintriple(sa, sb, sc, pk, count, n, p_lo, L)
+            return {"a": sa, "b": sb, "c": sc}
+        if key.kind == KIND_DABIT:                        # preprocessing.py:160-164
+            arith = self._dst("arith", (L, count))
+            bit = self._dst("bit", (L, _words(count)), zero=True)
+            K.deal_dabit(arith, bit, pk, count, n, p_lo, L, w)
+            return {"arith": arith, "bit": bit}
+        if key.kind == KIND_EDABIT:                       # preprocessing.py:165-170
+            m = key.params[0]
+            arith = self._dst("arith", (L, count))
+            K.deal_gen_arith(arith, None, pk, 0, 2 * count, count, n, p_lo, L, m, w)
+            res = {"arith": arith}
+            if need_bits:
+                bits = self._dst("bits", (L, _words(count * m)), zero=True)
+                K.deal_edabit_bits(bits, pk, 2 * count + (n - 1) * 2 * count, count, m, w, n, p_lo, L)
+                res["bits"] = bits
             return res
         raise ValueError(f"unknown material kind {key.kind}")
 

@@ -312,10 +312,23 @@ def _beaver_matmul_fused_simt(session, Zg, pairs, trips, L, m, k, r, w):
     x_js, y_js = step([p[0].values for p in pairs]), step([p[1].values for p in pairs])
     xps, xsr, xsc = _strides3(X0)
     yps, ysr, ysc = _strides3(Y0)
+    if _thin_tc(len(pairs), L, m, k, r) and A0.stride(1) == k and B0.stride(1) == r and C0.stride(1) == r:
+        K.beaver_tc_thin(Zg, m * r, C0.data_ptr(), C0.stride(0), _ptr(X0), xps, xsr, xsc, A0.data_ptr(),
+                         A0.stride(0), _ptr(Y0), yps, ysr, ysc, B0.data_ptr(), B0.stride(0), L, m, k, r, session.p0, w)
+        return
     K.beaver_gemm_sim(Zg, m * r, L * m * r, C0.data_ptr(), C0.stride(0), _bstride(trips, range(len(trips)), 2),
                       _ptr(X0), xps, xsr, xsc, x_js, A0.data_ptr(), A0.stride(0),
                       _bstride(trips, range(len(trips)), 0), _ptr(Y0), yps, ysr, ysc, y_js, B0.data_ptr(),
                       B0.stride(0), _bstride(trips, range(len(trips)), 1), L, len(pairs), m, k, r, session.p0, w)
+
+
+# thin products (K, N <= 32: LeNet conv1 forward) on tcgen05 with the limb
+# operands built in shared memory; MPX_THIN_TC=0 keeps them on the SIMT kernel
+THIN_TC = os.environ.get("MPX_THIN_TC", "1") != "0"
+
+
+def _thin_tc(batch, L, m, k, r) -> bool:
+    return THIN_TC and batch == 1 and 2 <= L <= 3 and k <= 32 and r <= 32 and m >= 1024
 
 
 def _strides3(v):

@@ -45,3 +45,15 @@ if __name__ == "__main__":
     print()
     for n, t in sorted(agg.items(), key=lambda kv: -kv[1]):
         print(f"{t:8.1f} us  {n}")
+
+
+def dealer_segments(data):
+    """Kernels between consecutive training steps that belong to the dealer."""
+    ends = [i for i, (n, _, _) in enumerate(data) if n.startswith("k_trunc_sub_multi")]
+    segs = []
+    for a, b in zip(ends[:-1], ends[1:]):
+        seg = data[a + 1:b + 1]
+        # the step starts at the first non-dealer kernel after the dealer run
+        segs.append([d for d in seg if DEALER.search(d[0]) or d[0].startswith("k_gemm_limbs_tc_pers<128, 64, 0")
+                     or (d[0].startswith("k_gemm_limbs_tc_pers") and seg.index(d) < 40)])
+    return segs
