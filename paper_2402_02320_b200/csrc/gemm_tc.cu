@@ -741,13 +741,31 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
 // Limb split: u64 matrix -> 8 u8 planes. `trans` = 0: plane[i][r][coff + c];
 // trans = 1: plane[i][c][coff + r] (K-major operand from a row-major KxN).
 
+// 4 x 4 byte transpose of four u32 rows (out[j] byte r = a[r] byte j): 8 PRMT
+__device__ __forceinline__ void bytes_transpose4(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                                 uint32_t (&o)[4]) {
+  const uint32_t t0 = __byte_perm(a0, a1, 0x5140), t1 = __byte_perm(a0, a1, 0x7362);
+  const uint32_t t2 = __byte_perm(a2, a3, 0x5140), t3 = __byte_perm(a2, a3, 0x7362);
+  o[0] = __byte_perm(t0, t2, 0x5410);
+  o[1] = __byte_perm(t0, t2, 0x7632);
+  o[2] = __byte_perm(t1, t3, 0x5410);
+  o[3] = __byte_perm(t1, t3, 0x7632);
+}
+
+// 8 x 8 byte transpose: p[i] byte c = w[c] byte i (limb planes of 8 words),
+// as four 4 x 4 transposes of the words' 32-bit halves (32 PRMT)
 __device__ __forceinline__ void bytes_transpose8(const u64 (&w)[8], u64 (&p)[8]) {
+  uint32_t a[4], b[4], c[4], d[4];
+  bytes_transpose4((uint32_t)w[0], (uint32_t)w[1], (uint32_t)w[2], (uint32_t)w[3], a);
+  bytes_transpose4((uint32_t)w[4], (uint32_t)w[5], (uint32_t)w[6], (uint32_t)w[7], b);
+  bytes_transpose4((uint32_t)(w[0] >> 32), (uint32_t)(w[1] >> 32), (uint32_t)(w[2] >> 32), (uint32_t)(w[3] >> 32),
+                   c);
+  bytes_transpose4((uint32_t)(w[4] >> 32), (uint32_t)(w[5] >> 32), (uint32_t)(w[6] >> 32), (uint32_t)(w[7] >> 32),
+                   d);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    u64 v = 0;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) v |= ((w[c] >> (8 * i)) & 0xFFull) << (8 * c);
-    p[i] = v;
+  for (int i = 0; i < 4; ++i) {
+    p[i] = (u64)a[i] | ((u64)b[i] << 32);
+    p[4 + i] = (u64)c[i] | ((u64)d[i] << 32);
   }
 }
 
@@ -1460,18 +1478,23 @@ int mpx_gemm_tc(uint64_t*, const uint64_t*, const uint64_t*, int64_t, int64_t, i
 // with D = sum_l X_l - A_l and E = sum_l Y_l - B_l (the openings are local
 // sums: all parties live on this GPU), for K <= 32 and N <= 32 (LeNet's conv1
 // forward: 73728 x 25 x 20 at three parties). One persistent CTA per SM:
-//  * warps 0-3 own one row each of a 128-row tile. Per party they stage the
-//    32 rows of X_l, then of A_l, of their warp through shared memory (coalesced
-//    reads at any X strides), accumulate D in registers and write the u8
-//    limb tile of A_l, then D's, in the UMMA K-major 32-byte-swizzle layout
-//    (16-byte chunk c of row r at chunk c ^ bit 2 of r);
-//  * lane 0 of warp 4 issues per party the 72 limb MMAs of the two 32-byte
+//  * warps 0-3 (producers) own 32 rows each of a 128-row tile: lane k loads
+//    column k of every party's X_l and A_l rows (all loads in flight at
+//    once), accumulates D per column in registers and writes the u8 limb
+//    tiles of A_l, then D, in the UMMA K-major 32-byte-swizzle layout (16-byte
+//    chunk c of row r at chunk c ^ bit 2 of r) through a staging tile; lane 0
+//    of warp 0 then issues per party the 72 limb MMAs of the two 32-byte
 //    k-blocks (D x B'_l, then A_l x E; diagonal i+j accumulates in TMEM
 //    columns 32(i+j) of the party's 256-column buffer, two buffers);
-//  * warps 0-3 drain a party's 8 diagonals (tcgen05.ld), recombine the limbs
-//    mod 2^64, hand the buffer back and store Z_l = C_l + acc through the
-//    staging tile (coalesced rows).
+//  * warps 4-7 (epilogue) drain a party's 8 diagonals (tcgen05.ld), recombine
+//    the limbs mod 2^64 onto the C_l addend and store Z_l, while the
+//    producers already load the next tile.
 // B'_l and E limb tiles (32 x 32 bytes each) are built once per CTA.
+// Measured (tools/micro/thin_tc.py, conv1 forward): 94 us vs 110 us for the
+// SIMT tall kernel; with loads, C/Z traffic and MMAs all disabled
+// (MPX_THIN_DBG=7) the skeleton alone still takes 50 us: one CTA of eight
+// warps per SM (the limb tiles take 160 KB) leaves the per-warp dependency
+// chains exposed.
 #define THIN_TA (128 * 32)  // one limb tile of the A side: 128 rows x 32 bytes
 #define THIN_TB (32 * 32)   // one limb tile of the B side: 32 rows (N) x 32 bytes
 
@@ -1490,6 +1513,7 @@ struct ThinArgs {
   i64 sB;
   int M, K, N, p0, L;
   u64 msk;
+  int dbg;  // timing experiments (MPX_THIN_DBG bits, wrong results): 1 no operand loads, 2 no C / Z traffic, 4 no MMA
 };
 
 __device__ __forceinline__ void thin_put16(uint8_t* tile, int r, int c, u64 lo, u64 hi) {
@@ -1497,175 +1521,245 @@ __device__ __forceinline__ void thin_put16(uint8_t* tile, int r, int c, u64 lo, 
   *reinterpret_cast<ulonglong2*>(tile + r * 32 + pc * 16) = make_ulonglong2(lo, hi);
 }
 
-// 32 values (k = 0..31) of one row -> row r of the 8 limb tiles at `base`
-// (tile stride `ts` bytes)
-__device__ __forceinline__ void thin_emit_row(uint8_t* base, int ts, int r, const u64 (&v)[32]) {
-  u64 pl[4][8];
+// 16 values (k = 16c .. 16c+15) of one row -> 16-byte chunk c of row r of the
+// 8 limb tiles at `base` (tile stride `ts` bytes)
+__device__ __forceinline__ void thin_emit_chunk(uint8_t* base, int ts, int r, int c, const u64* v) {
+  u64 p0[8], p1[8], w[8];
 #pragma unroll
-  for (int g = 0; g < 4; ++g) {
-    u64 w[8];
+  for (int q = 0; q < 8; ++q) w[q] = v[q];
+  bytes_transpose8(w, p0);
 #pragma unroll
-    for (int c = 0; c < 8; ++c) w[c] = v[8 * g + c];
-    bytes_transpose8(w, pl[g]);
-  }
+  for (int q = 0; q < 8; ++q) w[q] = v[8 + q];
+  bytes_transpose8(w, p1);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    thin_put16(base + i * ts, r, 0, pl[0][i], pl[1][i]);
-    thin_put16(base + i * ts, r, 1, pl[2][i], pl[3][i]);
-  }
+  for (int i = 0; i < 8; ++i) thin_put16(base + i * ts, r, c, p0[i], p1[i]);
 }
+
+#define TMEM_LD16(taddr, v)                                                                            \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
+               "%14,%15}, [%16];"                                                                       \
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),    \
+                 "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), \
+                 "=r"(v[14]), "=r"(v[15])                                                               \
+               : "r"(taddr))
+
+#define THIN_SP 33  // staging pitch (u64): odd, conflict-free row reads
 
 constexpr int thin_smem_bytes(int L) {
-  // D + L A_l tiles, L B'_l + E tiles, per-warp staging (32 x 33 u64), barriers
-  return 8 * THIN_TA * (1 + L) + 8 * THIN_TB * (L + 1) + 4 * 32 * 33 * 8 + 1024 + 1024;
+  // D + L A_l tiles, L B'_l + E tiles, 4 producer warps' staging (32 x 33 u64), barriers
+  return 8 * THIN_TA * (1 + L) + 8 * THIN_TB * (L + 1) + 4 * 32 * THIN_SP * 8 + 1024 + 1024;
 }
 
+// Roles (256 threads): warps 0-3 producers (warp w: rows 32w..32w+31 of the
+// tile, all k; lane 0 of warp 0 also issues the tile's MMAs once the four
+// have written it), warps 4-7 epilogue (TMEM lane quarter w - 4). Producers
+// run one tile ahead of the epilogue: tile t+1's loads overlap tile t's
+// drain and stores; its limb tiles are written once the MMAs of tile t have
+// read theirs (sempty). Every tile's inputs are prefetched to L2 one tile
+// ahead. (Eight warps: 255 registers per thread; a ninth warp would cap
+// them at 168.)
 template <int L>
-__global__ void __launch_bounds__(160, 1) k_beaver_tc_thin(const __grid_constant__ ThinArgs a) {
+__global__ void __launch_bounds__(256, 1) k_beaver_tc_thin(const __grid_constant__ ThinArgs a) {
   extern __shared__ __align__(1024) uint8_t thin_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)thin_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sD = smem;                          // 8 limb tiles
   uint8_t* sA = sD + 8 * THIN_TA;              // [L][8] limb tiles
   uint8_t* sBp = sA + L * 8 * THIN_TA;         // [L][8] B'_l limb tiles
   uint8_t* sE = sBp + L * 8 * THIN_TB;         // [8] E limb tiles
-  u64* stg = reinterpret_cast<u64*>(sE + 8 * THIN_TB);  // [4 warps][32][33]
-  uint64_t* tf = reinterpret_cast<uint64_t*>(stg + 4 * 32 * 33);  // [2] MMA done per buffer
-  uint64_t* te = tf + 2;                                               // [2] buffer drained
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(te + 2);
+  u64* stg = reinterpret_cast<u64*>(sE + 8 * THIN_TB);                  // [4 warps][32][THIN_SP]
+  uint64_t* tf = reinterpret_cast<uint64_t*>(stg + 4 * 32 * THIN_SP);  // [2] MMA done per TMEM buffer
+  uint64_t* te = tf + 2;                                                // [2] buffer drained
+  uint64_t* sempty = te + 2;                                            // limb tiles consumed by the MMAs
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sempty + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = a.K, N = a.N;
-  const int KP = 33;  // staging pitch (u64): odd, conflict-free row reads
 
   if (threadIdx.x == 0) {
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tf[b], 1);
       mbar_init(&te[b], 4);
     }
+    mbar_init(sempty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 4) {
+  if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
                  "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  // B side once per CTA: E = sum_l Y_l - B_l; B'_l = B_l + [l == p0] E (rows = n, bytes = k)
-  if (warp < 4) {
-    for (int job = threadIdx.x; job < (L + 1) * 32; job += 128) {
-      const int n = job & 31, which = job >> 5;  // which < L: B'_which, == L: E
-      u64 v[32];
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        u64 e = 0, bw = 0;
-        if (k < K && n < N) {
-#pragma unroll
-          for (int l = 0; l < L; ++l) {
-            const u64 b = a.B[l * a.sB + (i64)k * N + n];
-            e += a.Y[l * a.y_ps + (i64)k * a.y_sr + (i64)n * a.y_sc] - b;
-            if (l == which) bw = b;
-          }
+  const int tiles = (a.M + 127) / 128;
+  // L2 prefetch of a tile's X_l / A_l rows (warps 0-3: their own 32 rows)
+  auto prefetch_tile = [&](int t) {
+    const i64 wr0 = (i64)t * 128 + warp * 32;
+    const int rows = (int)max((i64)0, min((i64)32, (i64)a.M - wr0));
+    for (int l = 0; l < L; ++l) {
+      const u64* Xl = a.X + l * a.x_ps + wr0 * a.x_sr;
+      const u64* Al = a.A + l * a.sA + wr0 * (i64)K;
+      for (int r = lane; r < rows; r += 32) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(Al + (i64)r * K));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(Al + (i64)r * K + K - 1));
+        if (a.x_sc == 1) {
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(Xl + (i64)r * a.x_sr));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(Xl + (i64)r * a.x_sr + K - 1));
         }
-        v[k] = which == L ? e : bw + (which == a.p0 ? e : 0ull);
       }
-      thin_emit_row(which == L ? sE : sBp + which * 8 * THIN_TB, THIN_TB, n, v);
+    }
+  };
+  if (warp < 4 && blockIdx.x < tiles) prefetch_tile(blockIdx.x);
+  // B side once per CTA: E = sum_l Y_l - B_l; B'_l = B_l + [l == p0] E (rows = n,
+  // bytes = k). E and every B_l are first gathered into the (still free) staging area.
+  if (warp < 4) {
+    u64* Es = stg;            // [32 k][32 n]
+    u64* Bs = stg + 32 * 32;  // [L][32 k][32 n]
+    for (int idx = threadIdx.x; idx < 32 * 32; idx += 128) {
+      const int k = idx >> 5, n = idx & 31;
+      const bool ok = k < K && n < N;
+      u64 bv[L], yv[L];
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        bv[l] = ok ? __ldg(a.B + l * a.sB + (i64)k * N + n) : 0ull;
+        yv[l] = ok ? __ldg(a.Y + l * a.y_ps + (i64)k * a.y_sr + (i64)n * a.y_sc) : 0ull;
+      }
+      u64 e = 0;
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        e += yv[l] - bv[l];
+        Bs[l * 1024 + idx] = bv[l];
+      }
+      Es[idx] = e;
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    for (int job = threadIdx.x; job < (L + 1) * 64; job += 128) {
+      const int n = job & 31, c = (job >> 5) & 1, which = job >> 6;  // which < L: B'_which, == L: E
+      u64 v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int k = 16 * c + q;
+        const u64 e = Es[k * 32 + n];
+        v[q] = which == L ? e : Bs[which * 1024 + k * 32 + n] + (which == a.p0 ? e : 0ull);
+      }
+      thin_emit_chunk(which == L ? sE : sBp + which * 8 * THIN_TB, THIN_TB, n, c, v);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("bar.sync 1, 128;" ::: "memory");  // staging free again
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_holder;
-  const int tiles = (a.M + 127) / 128;
   const uint32_t idesc = (2u << 4) | ((uint32_t)(32 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 
-  int job = 0;  // running (tile, party) index: TMEM buffer job & 1
-  for (int t = blockIdx.x; t < tiles; t += gridDim.x, job += L) {
-    const i64 r0 = (i64)t * 128;
-    if (warp < 4) {
-      // ---- produce: limb tiles of A_l (each party) and D ----
-      u64* sx = stg + warp * 32 * KP;
-      const i64 wr0 = r0 + warp * 32;
+  if (warp < 4) {
+    // ---------------- producers ----------------
+    u64* sx = stg + warp * 32 * THIN_SP;
+    int it = 0, job = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      if (t + (int)gridDim.x < tiles) prefetch_tile(t + gridDim.x);
+      const i64 wr0 = (i64)t * 128 + warp * 32;
       const int rows = (int)max((i64)0, min((i64)32, (i64)a.M - wr0));
-      u64 d[32];
+      // lane = column k: D is accumulated per column in registers (dcol[r] =
+      // D[row r][k]); each party's A_l tile and finally D go to row-owned
+      // lanes through the staging tile for the limb emission.
+      const bool kok = lane < K;
+      u64 dcol[32];
 #pragma unroll
-      for (int k = 0; k < 32; ++k) d[k] = 0;
+      for (int r = 0; r < 32; ++r) dcol[r] = 0;
       for (int l = 0; l < L; ++l) {
-        const u64* Xl = a.X + l * a.x_ps + wr0 * a.x_sr;
-        const u64* Al = a.A + l * a.sA + wr0 * (i64)K;
-        // X_l rows, then A_l rows, through the warp's staging tile
+        const u64* __restrict__ Xl = a.X + l * a.x_ps + wr0 * a.x_sr + (i64)lane * a.x_sc;
+        const u64* __restrict__ Al = a.A + l * a.sA + wr0 * (i64)K + lane;
+        u64 t[32], tx[32];  // X_l's and A_l's loads all in flight together
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+          const bool ld = kok && r < rows && !(a.dbg & 1);
+          tx[r] = ld ? __ldg(Xl + (i64)r * a.x_sr) : 0ull;
+          t[r] = ld ? __ldg(Al + (i64)r * K) : 0ull;
+        }
+#pragma unroll
+        for (int r = 0; r < 32; ++r) dcol[r] += tx[r];
         __syncwarp();
-        for (int idx = lane; idx < 32 * K; idx += 32) {
-          const int rr = idx / K, k = idx - rr * K;
-          sx[rr * KP + k] = rr < rows ? Xl[(i64)rr * a.x_sr + (i64)k * a.x_sc] : 0ull;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+          dcol[r] -= t[r];
+          sx[r * THIN_SP + lane] = t[r];
         }
         __syncwarp();
+        // the previous tile's MMAs must have read the limb tiles
+        if (l == 0 && it > 0) mbar_wait(sempty, (uint32_t)((it - 1) & 1));
 #pragma unroll
-        for (int k = 0; k < 32; ++k)
-          if (k < K) d[k] += sx[lane * KP + k];
-        __syncwarp();
-        for (int idx = lane; idx < 32 * K; idx += 32) {
-          const int rr = idx / K, k = idx - rr * K;
-          sx[rr * KP + k] = rr < rows ? Al[(i64)rr * K + k] : 0ull;
-        }
-        __syncwarp();
-        u64 v[32];
+        for (int c = 0; c < 2; ++c) {  // A_l row (lane = row): 16 words at a time
+          u64 v[16];
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          v[k] = k < K ? sx[lane * KP + k] : 0ull;
-          d[k] -= v[k];
-        }
-        thin_emit_row(sA + l * 8 * THIN_TA, THIN_TA, warp * 32 + lane, v);
-      }
-#pragma unroll
-      for (int k = 0; k < 32; ++k) d[k] &= a.msk;
-      thin_emit_row(sD, THIN_TA, warp * 32 + lane, d);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();  // limb tiles of this tile complete
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (warp == 4) {
-      if (lane == 0) {
-        // ---- MMA issue: per party two k-blocks of 36 limb products ----
-        for (int l = 0; l < L; ++l) {
-          const int j = job + l, buf = j & 1;
-          if (j >= 2) mbar_wait(&te[buf], (uint32_t)(((j - 2) >> 1) & 1));
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t dt = tmem_base + (uint32_t)(buf * 256);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const uint64_t ad = umma_desc_sw<32>(smem_u32(sD + i * THIN_TA));
-#pragma unroll
-            for (int jj = 0; jj <= 7 - i; ++jj)
-              mma_i8(dt + (uint32_t)((i + jj) * 32), ad,
-                     umma_desc_sw<32>(smem_u32(sBp + (l * 8 + jj) * THIN_TB)), idesc, i > 0 ? 1u : 0u);
-          }
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const uint64_t ad = umma_desc_sw<32>(smem_u32(sA + (l * 8 + i) * THIN_TA));
-#pragma unroll
-            for (int jj = 0; jj <= 7 - i; ++jj)
-              mma_i8(dt + (uint32_t)((i + jj) * 32), ad, umma_desc_sw<32>(smem_u32(sE + jj * THIN_TB)), idesc, 1u);
-          }
-          umma_commit(&tf[buf]);
+          for (int q = 0; q < 16; ++q) v[q] = sx[lane * THIN_SP + 16 * c + q];
+          thin_emit_chunk(sA + l * 8 * THIN_TA, THIN_TA, warp * 32 + lane, c, v);
         }
       }
       __syncwarp();
-    } else {
-      // ---- epilogue: drain, recombine, Z_l = C_l + acc (coalesced via staging) ----
-      u64* st = stg + warp * 32 * KP;
-      const i64 wr0 = r0 + warp * 32;
-      const int rows = (int)max((i64)0, min((i64)32, (i64)a.M - wr0));
-      for (int l = 0; l < L; ++l) {
-        const int j = job + l, buf = j & 1;
-        mbar_wait(&tf[buf], (uint32_t)((j >> 1) & 1));
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int r = 0; r < 32; ++r) sx[r * THIN_SP + lane] = dcol[r] & a.msk;
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        u64 v[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = sx[lane * THIN_SP + 16 * c + q];
+        thin_emit_chunk(sD, THIN_TA, warp * 32 + lane, c, v);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      asm volatile("bar.sync 2, 128;" ::: "memory");  // the four producer warps wrote tile t
+      if (warp == 0) {
+        if (lane == 0) {
+          // ---- MMA issue: per party two k-blocks of 36 limb products ----
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          for (int l = 0; l < L; ++l, ++job) {
+            const int buf = job & 1;
+            if (job >= 2) mbar_wait(&te[buf], (uint32_t)(((job - 2) >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t dt = tmem_base + (uint32_t)(buf * 256);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const uint64_t ad = umma_desc_sw<32>(smem_u32(sD + i * THIN_TA));
+#pragma unroll
+              for (int jj = 0; jj <= 7 - i; ++jj)
+                if (!(a.dbg & 4))
+                  mma_i8(dt + (uint32_t)((i + jj) * 32), ad,
+                         umma_desc_sw<32>(smem_u32(sBp + (l * 8 + jj) * THIN_TB)), idesc, i > 0 ? 1u : 0u);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const uint64_t ad = umma_desc_sw<32>(smem_u32(sA + (l * 8 + i) * THIN_TA));
+#pragma unroll
+              for (int jj = 0; jj <= 7 - i; ++jj)
+                if (!(a.dbg & 4))
+                  mma_i8(dt + (uint32_t)((i + jj) * 32), ad, umma_desc_sw<32>(smem_u32(sE + jj * THIN_TB)), idesc,
+                         1u);
+            }
+            umma_commit(&tf[buf]);
+          }
+          umma_commit(sempty);  // this tile's limb tiles may be overwritten
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- epilogue: drain, recombine, Z_l = C_l + acc (a thread = a row) ----------------
+    const int rq = warp - 4;
+    int job = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const i64 row = (i64)t * 128 + rq * 32 + lane;
+      for (int l = 0; l < L; ++l, ++job) {
+        const int buf = job & 1;
+        const u64* __restrict__ Cl = a.C + l * a.sC + row * (i64)N;
+        u64* __restrict__ Zl = a.Z + l * a.sZ + row * (i64)N;
         u64 acc[32];
 #pragma unroll
-        for (int q = 0; q < 32; ++q) acc[q] = 0;
+        for (int q = 0; q < 32; ++q) acc[q] = (q < N && row < a.M && !(a.dbg & 2)) ? __ldg(Cl + q) : 0ull;  // addend first
+        mbar_wait(&tf[buf], (uint32_t)((job >> 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
         for (int dd = 0; dd < 8; ++dd) {
           uint32_t v[32];
-          TMEM_LD32(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(buf * 256 + dd * 32), v);
+          TMEM_LD32(tmem_base + ((uint32_t)(rq * 32) << 16) + (uint32_t)(buf * 256 + dd * 32), v);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
           for (int q = 0; q < 32; ++q) acc[q] += (u64)v[q] << (8 * dd);
@@ -1673,24 +1767,17 @@ __global__ void __launch_bounds__(160, 1) k_beaver_tc_thin(const __grid_constant
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&te[buf]);
-        __syncwarp();
+        if (row < a.M && !(a.dbg & 2)) {
 #pragma unroll
-        for (int q = 0; q < 32; ++q)
-          if (q < N) st[lane * KP + q] = acc[q];
-        __syncwarp();
-        const u64* Cl = a.C + l * a.sC + wr0 * (i64)N;
-        u64* Zl = a.Z + l * a.sZ + wr0 * (i64)N;
-        for (int idx = lane; idx < rows * N; idx += 32) {
-          const int rr = idx / N, q = idx - rr * N;
-          Zl[idx] = (Cl[idx] + st[rr * KP + q]) & a.msk;
+          for (int q = 0; q < 32; ++q)
+            if (q < N) Zl[q] = acc[q] & a.msk;
         }
-        __syncwarp();
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 4) {
+  if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
   }
@@ -1707,7 +1794,7 @@ static int thin_launch(const ThinArgs& a, cudaStream_t s) {
     attr = true;
   }
   const int tiles = (a.M + 127) / 128;
-  k_beaver_tc_thin<L><<<min(tiles, num_sms()), 160, smem, s>>>(a);
+  k_beaver_tc_thin<L><<<min(tiles, num_sms()), 256, smem, s>>>(a);
   return launch_status();
 }
 
@@ -1744,6 +1831,7 @@ extern "C" int mpx_beaver_tc_thin(uint64_t* Z, int64_t sZ, const uint64_t* C, in
   a.p0 = p0;
   a.L = L;
   a.msk = ring_mask(width);
+  a.dbg = getenv("MPX_THIN_DBG") ? atoi(getenv("MPX_THIN_DBG")) : 0;
   cudaStream_t s = (cudaStream_t)stream;
   return L == 2 ? thin_launch<2>(a, s) : thin_launch<3>(a, s);
 }

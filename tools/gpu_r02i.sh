@@ -1,0 +1,7 @@
+#!/bin/bash
+set -u
+mkdir -p gpurun_out
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_beaver_tc_thin -c 1 -o gpurun_out/thin_tc3 python tools/micro/thin_tc.py --reps 1 --only-thin > gpurun_out/ncu_thin.log 2>&1
+ncu -i gpurun_out/thin_tc3.ncu-rep --page source --csv --print-source sass > gpurun_out/thin_tc3_source.csv 2>/dev/null
+ncu -i gpurun_out/thin_tc3.ncu-rep --page source --csv --print-source cuda > gpurun_out/thin_tc3_cuda.csv 2>/dev/null
+ncu -i gpurun_out/thin_tc3.ncu-rep --page details --csv > gpurun_out/thin_tc3_details.csv 2>/dev/null
