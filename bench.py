@@ -490,6 +490,39 @@ def int8_peak_tops(torch, n=8192, iters=10):
     return 2 * n ** 3 / (best / 1e3) / 1e12
 
 
+def philox_ceiling_gblocks(torch, blocks=1 << 28, iters=5):
+    """Philox4x64-10 ALU ceiling (mpx_philox_probe: generate + XOR-fold, no
+    stores), G blocks/s, best of `iters`: the dealer's roofline denominator."""
+    from paper_2402_02320_b200 import kernels as K
+    out = torch.empty(148 * 8 * 256, dtype=torch.int64, device="cuda")
+    K.philox_probe(out, 1 << 20)
+    torch.cuda.synchronize()
+    best = None
+    for _ in range(iters):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        K.philox_probe(out, blocks)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    return blocks / (best / 1e3) / 1e9
+
+
+def dealer_roofline(torch, demands, n_parties, needs_bits, dealer_ms):
+    """The re-deal's Philox work (preprocessing.stream_blocks: every draw of
+    the reference's generate_material, 32 bytes per block) over its time,
+    against the in-run ALU ceiling."""
+    from paper_2402_02320_b200.preprocessing import stream_blocks
+    blocks = stream_blocks(demands, n_parties, needs_bits)
+    peak = philox_ceiling_gblocks(torch)
+    achieved = blocks / (dealer_ms / 1e3) / 1e9
+    return {"bound": "alu (Philox4x64-10)", "achieved": achieved, "peak": peak, "unit": "G Philox blocks/s",
+            "frac": achieved / peak, "blocks_per_deal": blocks,
+            "peak_kind": "measured in-run: mpx_philox_probe (Philox4x64-10 generate + XOR-fold, no stores)",
+            "note": "whole re-deal incl. the matrix-triple C = A @ B GEMMs and all share stores"}
+
+
 def sweep_entry(torch, G, make_session, parties, n_parties, dev, name, steps=2, warmup=1, elems=1 << 24):
     from paper_2402_02320_b200 import _lib
     from paper_2402_02320_b200.preprocessing import DemandCounter, device_store
@@ -1038,7 +1071,10 @@ def run_b200(args, group=None):
                 sweep[nm]["cpu_baseline"] = cpu_all.get(key)
 
     line = None
+    dealer_roof = None
     if rank == 0:
+        dealer_roof = dealer_roofline(torch, counter.demands, n_parties, counter.needs_bits,
+                                      float(np.median([d[0] for d in deal_ms[args.warmup:]])))
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -1050,7 +1086,7 @@ def run_b200(args, group=None):
                        "parties": n_parties, "batch": B, "frac": FRAC, "ring_width": WIDTH,
                        "mode": ("sim: all parties on 1 GPU, step captured in one CUDA graph" if world == 1
                                 else "one party per GPU, NCCL openings, eager"),
-                       "l2": "working set > L2 per step (material ~0.7 GB, re-dealt in place each step)",
+                       "l2": "working set > L2 per step (material ~1.4 GB, re-dealt in place each step)",
                        "dealer": "fresh on-device material re-dealt in place before every step, outside "
                                  "the timed region"},
             "e2e": {"value": args.steps / (e2e_total / 1e3), "unit": UNIT,
@@ -1069,7 +1105,8 @@ def run_b200(args, group=None):
                        "how": ("one CUDA graph of the whole re-deal (keys in device slots), CUDA events"
                                if world == 1 else "device_store(into=...) per step, CUDA events"),
                        "material_GB": sum(t.numel() * t.element_size() for d in sess.store._arrays.values()
-                                          for t in d.values()) / 1e9},
+                                          for t in d.values()) / 1e9,
+                       "roofline": dealer_roof},
             "loss_first_last": losses,
             "kernels": _kernel_table(per),
             "cpu_baseline": cpu,

@@ -415,6 +415,11 @@ int mpx_beaver_tc_thin(uint64_t* Z, int64_t sZ, const uint64_t* C, int64_t sC, c
                        const uint64_t* Y, int64_t y_ps, int64_t y_sr, int64_t y_sc, const uint64_t* B,
                        int64_t sB, int L, int64_t M, int64_t K, int64_t N, int p0, int width, void* stream);
 
+/* Philox4x64-10 ALU ceiling probe: `blocks` counter blocks generated and
+ * XOR-folded into out[grid*256] (out_words >= 148*8*256), no other memory
+ * traffic: the dealer's roofline denominator, measured in-run. */
+int mpx_philox_probe(uint64_t* out, int64_t out_words, int64_t blocks, void* stream);
+
 /* ---- fused per-kind dealer: ONE launch per material key ----
  * Each thread draws its group's secrets straight from the key's stream (draw
  * order SURVEY App. A4 / preprocessing.py:139-171), derives c = a*b or

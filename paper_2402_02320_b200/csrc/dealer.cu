@@ -591,3 +591,31 @@ extern "C" int mpx_deal_edabit_bits(uint64_t* bit_words, int64_t ps, uint64_t k0
                                                                 ring_mask(width) & low_bits(m), n, p_lo, L);
   return launch_status();
 }
+
+// Philox4x64-10 ALU ceiling probe (the dealer's roofline denominator):
+// `blocks` counter blocks, two independent blocks per thread iteration, keys
+// in uniform registers, the outputs XOR-folded to one word per thread (no
+// memory traffic to speak of). tools/micro/philox_bench.cu measures the same
+// loop standalone: ~100 G blocks/s on a B200.
+__global__ void __launch_bounds__(256) k_philox_probe(u64* __restrict__ out, u64 k0, u64 k1, i64 blocks) {
+  u64 acc = 0;
+  const i64 stride = (i64)gridDim.x * blockDim.x * 2;
+  for (i64 b = ((i64)blockIdx.x * blockDim.x + threadIdx.x) * 2; b < blocks; b += stride) {
+    const Philox4 r0 = philox4x64_10((u64)b + 1ull, k0, k1);
+    const Philox4 r1 = philox4x64_10((u64)b + 2ull, k0, k1);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc ^= r0.v[i] ^ r1.v[i];
+  }
+  out[(i64)blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
+extern "C" int mpx_philox_probe(uint64_t* out, int64_t out_words, int64_t blocks, void* stream) {
+  CHECK_ARG(out && blocks >= 0);
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+  const i64 grid = (i64)sms * 8;
+  CHECK_ARG(out_words >= grid * 256);
+  k_philox_probe<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(out, 0x1234567ull, 0x89abcdefull, blocks);
+  return launch_status();
+}

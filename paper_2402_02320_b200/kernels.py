@@ -602,6 +602,12 @@ def deal_share_bits(out, secret, key, u32_base, count, n, p_lo, L):
     return out
 
 
+def philox_probe(out, blocks):
+    """ALU-only Philox4x64-10 throughput probe (the dealer's roofline)."""
+    call("mpx_philox_probe", ptr(out), out.numel(), int(blocks))
+    return out
+
+
 def _key_args(key):
     """(k0, k1, dkey) for the fused dealer entry points: a key by value, or a
     device key slot (int64[2]) read at launch."""

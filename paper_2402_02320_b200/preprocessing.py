@@ -445,6 +445,39 @@ class DemandCounter(MaterialStore):
         return ArithMat(self._m(self.L, count)), (BitMat(self._m(self.L, 1), 0) if need_bits else None)
 
 
+def stream_u32(key: MaterialKey, count: int, n_parties: int, need_bits: bool = True) -> int:
+    """u32 words of the key's Philox stream one all-parties deal of ``count``
+    items draws (SURVEY App. A4 draw sizes: random_elems = 8 bytes per
+    element, random_bits = 1 byte per bit, each draw rounded up to whole u32,
+    ring.py:124-134; n-1 share draws per secret, sharing.py:124-152)."""
+    n = n_parties
+    q = lambda nbytes: (nbytes + 3) // 4  # noqa: E731
+    if count <= 0:
+        return 0
+    if key.kind == KIND_TRIPLE:
+        return (2 + 3 * (n - 1)) * q(8 * count)
+    if key.kind == KIND_MATRIX_TRIPLE:
+        m, k, r = key.params
+        return n * (q(8 * count * m * k) + q(8 * count * k * r)) + (n - 1) * q(8 * count * m * r)
+    if key.kind == KIND_BIN_TRIPLE:
+        return (2 + 3 * (n - 1)) * q(count)
+    if key.kind == KIND_DABIT:
+        return n * q(count) + (n - 1) * q(8 * count)
+    if key.kind == KIND_EDABIT:
+        return n * q(8 * count) + ((n - 1) * q(count * key.params[0]) if need_bits else 0)
+    raise ValueError(f"unknown material kind {key.kind}")
+
+
+def stream_blocks(demands: dict, n_parties: int, needs_bits: dict | None = None) -> int:
+    """Philox4x64-10 blocks (32 bytes of stream) one re-deal of ``demands``
+    generates: the dealer's algorithmic ALU work."""
+    u32 = 0
+    for key, count in demands.items():
+        nb = True if needs_bits is None else needs_bits.get(key, key.kind != KIND_EDABIT)
+        u32 += stream_u32(key, count, n_parties, nb)
+    return (u32 + 7) // 8
+
+
 def device_store(seed: int, n_parties: int, demands: dict, parties=None, device="cuda",
                  needs_bits: dict | None = None, into: MaterialStore | None = None) -> MaterialStore:
     """Deal every demanded key for the local ``parties`` (memory_stores,

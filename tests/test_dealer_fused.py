@@ -14,7 +14,6 @@ import torch
 
 import oracle as O
 
-pytestmark = pytest.mark.gpu
 
 KINDS = ["triple_w64", "triple_w32", "mtriple_w64_3x5x2", "mtriple_w64_7x9x4", "bintriple", "dabit_w64",
          "dabit_w32", "edabit_w64_m64", "edabit_w64_m23", "edabit_w32_m32", "edabit_w64_m40", "edabit_w64_m2",
@@ -48,12 +47,14 @@ def _check(key_name, count, n, p_lo, L, slot=False, seed=11):
         assert np.array_equal(_as_np(got[arr], w[p_lo:p_lo + L]), w[p_lo:p_lo + L]), (key_name, count, n, p_lo, L, arr)
 
 
+@pytest.mark.gpu
 @pytest.mark.parametrize("key_name", KINDS)
 @pytest.mark.parametrize("count", COUNTS)
 def test_fused_dealer_all_parties(key_name, count):
     _check(key_name, count, 3, 0, 3)
 
 
+@pytest.mark.gpu
 @pytest.mark.parametrize("key_name", ["triple_w64", "bintriple", "dabit_w64", "edabit_w64_m64", "edabit_w64_m23",
                                       "mtriple_w64_3x5x2"])
 @pytest.mark.parametrize("n", [2, 4, 5])
@@ -63,11 +64,13 @@ def test_fused_dealer_party_subsets(key_name, n):
             _check(key_name, 67, n, p_lo, L)
 
 
+@pytest.mark.gpu
 @pytest.mark.parametrize("key_name", ["triple_w64", "bintriple", "dabit_w32", "edabit_w64_m64", "mtriple_w64_7x9x4"])
 def test_fused_dealer_device_key_slot(key_name):
     _check(key_name, 1000, 3, 0, 3, slot=True)
 
 
+@pytest.mark.gpu
 def test_fused_dealer_equals_legacy_chain_large():
     """At a LeNet-sized count the fused kernels reproduce the legacy
     draw -> store -> share chain word for word (n = 3)."""
@@ -84,3 +87,22 @@ def test_fused_dealer_equals_legacy_chain_large():
             P.LEGACY_DEALER = False
         for k in fused:
             assert torch.equal(fused[k], legacy[k]), (name, k)
+
+
+@pytest.mark.parametrize("n", [2, 3, 5])
+def test_stream_accounting_matches_oracle_draws(n, monkeypatch):
+    """preprocessing.stream_u32 (the dealer roofline's work count) equals the
+    u32 words the restated reference dealer actually draws."""
+    from paper_2402_02320_b200.preprocessing import MaterialKey, stream_u32
+    used = {}
+    orig = O.ByteStream.take
+
+    def take(self, nbytes):
+        used[id(self)] = used.get(id(self), 0) + (nbytes + 3) // 4
+        return orig(self, nbytes)
+    monkeypatch.setattr(O.ByteStream, "take", take)
+    for name in ["triple_w64", "mtriple_w64_3x5x2", "bintriple", "dabit_w32", "edabit_w64_m23", "edabit_w32_m32"]:
+        for count in (1, 13, 66):
+            used.clear()
+            O.deal_material(11, n, name, count)
+            assert sum(used.values()) == stream_u32(MaterialKey.from_name(name), count, n, True), (name, count)

@@ -38,9 +38,10 @@ for i in range(5):
     e0.record(); g.redeal(10 + i); e1.record(); torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
 print("graph re-deal ms", [round(t, 3) for t in ts])
-buf = torch.empty(1 << 27, dtype=torch.int64, device="cuda")
-for i in range(3):
-    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-    e0.record(); K.philox_elems(buf, (1, 2), 0, buf.numel(), 64); e1.record(); torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-print(f"philox ceiling: {buf.numel() * 8 / ms / 1e6:.1f} GB/s of stream = {buf.numel() / 4 / ms / 1e6:.2f} G blocks/s")
+import bench
+from paper_2402_02320_b200.preprocessing import stream_blocks
+blocks = stream_blocks(c.demands, n, c.needs_bits)
+peak = bench.philox_ceiling_gblocks(torch)
+ms = min(ts)
+print(f"philox ceiling (mpx_philox_probe): {peak:.1f} G blocks/s; re-deal: {blocks / 1e6:.1f} M blocks in {ms:.3f} ms "
+      f"= {blocks / ms / 1e6:.1f} G blocks/s = {blocks / ms / 1e6 / peak:.2f} of the ALU ceiling")
