@@ -598,6 +598,8 @@ def sweep_entry(torch, G, make_session, parties, n_parties, dev, name, steps=2, 
 class DistGroup:
     """torch.distributed over NCCL: one rank per GPU (torchrun)."""
 
+    capturable = True   # NCCL collectives can be captured into the step's CUDA graph
+
     def __init__(self, torch, dist):
         self.torch, self.dist = torch, dist
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -606,6 +608,9 @@ class DistGroup:
 
     def init(self, dev):
         if self.world > 1:
+            # communicator init lines on stderr (one per rank) show the N-rank NCCL setup
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             self.dist.init_process_group("nccl", device_id=dev)
 
     def comm(self):
@@ -937,11 +942,24 @@ def run_b200(args, group=None):
     xs, ys = sess.share_fixed(x, WIDTH, FRAC, kx), sess.share_fixed(y, WIDTH, FRAC, ky)
     launches_per_step = None
     graph = None
-    if world == 1:
-        l0 = _lib.LAUNCHES
-        graph = train.GraphedStep(sess, model, xs, ys, LR_SHIFT, counter.demands, counter.needs_bits, seed0=1)
+    graph_note = None
+    l0 = _lib.LAUNCHES
+    try:
+        if world > 1 and not getattr(group, "capturable", False):
+            raise RuntimeError("the party group's collectives are host rendezvous (not capturable)")
+        # party mode (N > 1): the NCCL collectives of every round are captured
+        # into the step's CUDA graph too (thread-local capture: the NCCL
+        # watchdog thread keeps polling its own events)
+        graph = train.GraphedStep(sess, model, xs, ys, LR_SHIFT, counter.demands, counter.needs_bits, seed0=1,
+                                  capture_error_mode="global" if world == 1 else "thread_local")
         launches_per_step = (_lib.LAUNCHES - l0) // 2          # warm-up step + captured step
-    else:
+    except Exception as e:  # noqa: BLE001
+        if world == 1:
+            raise
+        graph_note = f"CUDA-graph capture of the NCCL step failed ({type(e).__name__}: {e}); eager steps"
+        print(f"[rank {rank}] {graph_note}", file=sys.stderr)
+        torch.cuda.synchronize(dev)
+        graph = None
         sess.store = device_store(1, n_parties, counter.demands, parties=parties, device=dev,
                                   needs_bits=counter.needs_bits)
 
@@ -1085,7 +1103,9 @@ def run_b200(args, group=None):
                                    "lr 2^-5)",
                        "parties": n_parties, "batch": B, "frac": FRAC, "ring_width": WIDTH,
                        "mode": ("sim: all parties on 1 GPU, step captured in one CUDA graph" if world == 1
-                                else "one party per GPU, NCCL openings, eager"),
+                                else "one party per GPU, NCCL openings" +
+                                (", step (kernels + collectives) captured in one CUDA graph" if graph is not None
+                                 else ", eager (" + str(graph_note) + ")")),
                        "l2": "working set > L2 per step (material ~1.4 GB, re-dealt in place each step)",
                        "dealer": "fresh on-device material re-dealt in place before every step, outside "
                                  "the timed region"},

@@ -75,9 +75,13 @@ def batch_matmul(session, pairs) -> list[AShare]:
     unfused = [g for g in groups if not (_fused_tc(session, *_gshape(pairs, g)) or
                                           _fused_simt(session, *_gshape(pairs, g)))]
     # every masked D, E of the round in ONE buffer: party mode opens it with a
-    # single collective, no concatenation
-    arena = session.alloc((sum(len(g) * (pairs[g[0]][0].size + pairs[g[0]][1].size) for g in unfused),))
-    at = 0
+    # single collective, no concatenation. Canonical layout - all D's in pair
+    # order, then all E's - so every party reduces the same element at the
+    # same offset whatever its local launch grouping (_groups depends on its
+    # own buffer addresses); a group's D's (E's) are still one run.
+    nd = sum(len(g) * pairs[g[0]][0].size for g in unfused)
+    arena = session.alloc((nd + sum(len(g) * pairs[g[0]][1].size for g in unfused),))
+    at_d, at_e = 0, nd
     for g in groups:
         x0, y0 = pairs[g[0]]
         w, (m, k), r = x0.width, x0.shape, y0.shape[1]
@@ -86,10 +90,10 @@ def batch_matmul(session, pairs) -> list[AShare]:
             # below (one round, same logical payload as the reference's D, E openings)
             fused_payload += len(g) * (arith_payload(w, m * k) + arith_payload(w, k * r))
             continue
-        D = arena[at:at + len(g) * m * k].view(len(g), m * k)
-        at += len(g) * m * k
-        E = arena[at:at + len(g) * k * r].view(len(g), k * r)
-        at += len(g) * k * r
+        D = arena[at_d:at_d + len(g) * m * k].view(len(g), m * k)
+        at_d += len(g) * m * k
+        E = arena[at_e:at_e + len(g) * k * r].view(len(g), k * r)
+        at_e += len(g) * k * r
         _mask_group(D, [pairs[i][0].values for i in g], [trip[i][0] for i in g], L, m, k, w)
         _mask_group(E, [pairs[i][1].values for i in g], [trip[i][1] for i in g], L, k, r, w)
         for j in range(len(g)):

@@ -414,7 +414,7 @@ class GraphedStep:
     """
 
     def __init__(self, session, model: Model, x: AShare, y: AShare, lr_shift: int, demands: dict,
-                 needs_bits: dict, seed0: int):
+                 needs_bits: dict, seed0: int, capture_error_mode: str = "global"):
         from .preprocessing import DealerGraph, device_store
         self.s, self.model, self.lr_shift = session, model, lr_shift
         self.demands, self.needs_bits = demands, needs_bits
@@ -439,7 +439,10 @@ class GraphedStep:
         del snapshot
         session.store.rewind()
         self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
+        # party sessions: the round's NCCL collectives are captured as graph
+        # nodes too ("thread_local": other threads, e.g. NCCL's watchdog, may
+        # keep querying their own events during the capture)
+        with torch.cuda.graph(self.graph, capture_error_mode=capture_error_mode):
             self.logits = model.train_step(session, x, y, lr_shift)
             self._writeback()
 
