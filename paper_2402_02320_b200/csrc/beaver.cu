@@ -909,7 +909,7 @@ extern "C" int mpx_bit2a_finish(uint64_t* out, const uint64_t* c, const uint64_t
   else
   {
     i64 tiles = (i64)L * ((rows + B2A_ROWS - 1) / B2A_ROWS);
-    unsigned g = (unsigned)(tiles < 148 * 8 ? tiles : 148 * 8);
+    unsigned g = (unsigned)(tiles < (i64)dev_sms() * 8 ? tiles : (i64)dev_sms() * 8);
     k_bit2a_compose<<<g, 256, 0, s>>>(out, c, rarith, ra_ps, L, rows, m, msk, p0, wts);
   }
   return launch_status();

@@ -15,6 +15,7 @@
 
 #define BG_BK 16
 
+
 // <= 128 registers per thread (a block occupies whole warps)
 constexpr int bg_min_blocks(int nt) { return 512 / (nt < 32 ? 32 : nt); }
 
@@ -217,7 +218,7 @@ extern "C" int mpx_beaver_gemm_batched(uint64_t* Z, int64_t sZ, int64_t bZ, cons
   // resident CTAs per SM at <= 128 registers per thread
   i64 per_sm = min((i64)32, (i64)(65536 / (max(nt, 32) * 128)));
   if (const char* cap = getenv("MPX_BG_PER_SM")) per_sm = min(per_sm, (i64)max(1, atoi(cap)));  // sweeps
-  const i64 target = 148 * per_sm;
+  const i64 target = (i64)dev_sms() * per_sm;
   int ksplit = 1;
   if (width == 64 && tiles < target && K >= 4 * BG_BK) {
     ksplit = (int)min((target + tiles - 1) / tiles, (K + BG_BK - 1) / BG_BK);
@@ -450,7 +451,7 @@ int launch_sim(i64 tiles_n, i64 tiles_m, i64 batch, i64 K, cudaStream_t s, uint6
     occ = 1;
   i64 per_sm = occ;
   if (const char* ov = getenv("MPX_BS_PER_SM")) per_sm = max(1, atoi(ov));  // sweeps
-  const i64 tiles = tiles_n * tiles_m * batch, target = 148 * per_sm;
+  const i64 tiles = tiles_n * tiles_m * batch, target = (i64)dev_sms() * per_sm;
   int ksplit = 1;
   if (width == 64 && tiles < target && K >= 4 * BS_BK)
     ksplit = (int)max((i64)1, min((target + tiles - 1) / tiles, (K + 2 * BS_BK - 1) / (2 * BS_BK)));
@@ -595,7 +596,7 @@ int launch_thin(i64 batch, cudaStream_t s, uint64_t* Z, int64_t sZ, int64_t bZ, 
     const int nt = N <= 16 ? 16 : (N <= 20 ? 20 : 32);
     const size_t smem = 8 * ((size_t)(L + 1) * K * nt + (size_t)(L + 1) * TALL_R * KP);
     const int groups = (M + TALL_R - 1) / TALL_R;
-    const unsigned g = (unsigned)min((i64)groups, (i64)148 * 16);
+    const unsigned g = (unsigned)min((i64)groups, (i64)dev_sms() * 16);
     dim3 grid(g, (unsigned)batch);
 #define TALL_CASE(NT_)                                                                                         \
   {                                                                                                            \

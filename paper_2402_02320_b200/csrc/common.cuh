@@ -21,7 +21,7 @@ typedef uint64_t u64;
 typedef int64_t i64;
 
 #define MPX_THREADS 256
-#define MPX_MAX_BLOCKS (148 * 16)
+
 
 __host__ __device__ __forceinline__ u64 ring_mask(int w) {
   return w >= 64 ? ~0ull : ((1ull << w) - 1ull);
@@ -44,10 +44,21 @@ __device__ __forceinline__ u64 load_bits(const u64* __restrict__ arr, i64 bit, i
   return v & low_bits(n);
 }
 
+// SM count of the current device (148 on a B200), queried once per process
+static inline int dev_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
 static inline unsigned grid_for(i64 n, int threads = MPX_THREADS) {
   i64 b = (n + threads - 1) / threads;
   if (b < 1) b = 1;
-  if (b > MPX_MAX_BLOCKS) b = MPX_MAX_BLOCKS;
+  if (b > (i64)dev_sms() * 16) b = (i64)dev_sms() * 16;
   return (unsigned)b;
 }
 

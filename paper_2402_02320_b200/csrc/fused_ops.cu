@@ -1252,7 +1252,7 @@ extern "C" int mpx_softmax_fused(uint64_t* e_out, uint64_t* r_out, const uint64_
   cudaStream_t s = (cudaStream_t)stream;
   const int gl = Pm.L == 8 ? 2 : 1;  // lanes per column: n = 8 splits its parties over two lanes
   const int threads = max(32, ((gl * d0 + 31) / 32) * 32);
-  const unsigned g = (unsigned)min(rows, (i64)(148 * 8));
+  const unsigned g = (unsigned)min(rows, (i64)dev_sms() * 8);
   const size_t sm = (size_t)Pm.L * (d0 + threads / 32) * 8;
   // staged plan: the row's element range per take (segments in tape order)
   static StagePlan plan;
@@ -1351,7 +1351,7 @@ extern "C" int mpx_maxtour_fused(uint64_t* y, const uint64_t* x, int64_t rows, i
   cudaStream_t s = (cudaStream_t)stream;
   const int gl = P.L == 8 ? 2 : 1;  // lanes per pair: n = 8 splits its parties over two lanes
   const int threads = min(256 * gl, max(32, ((gl * (d0 / 2) + 31) / 32) * 32));
-  const unsigned g = (unsigned)min(rows, (i64)(148 * 16));
+  const unsigned g = (unsigned)min(rows, (i64)dev_sms() * 16);
   const size_t sm = (size_t)P.L * d0 * 8;
   switch (P.L) {
     case 1: k_maxtour_fused<1, 1><<<g, threads, sm, s>>>(y, x, rows, d0, tp, lv, P); break;

@@ -101,8 +101,8 @@ extern "C" int mpx_gemm_simt(uint64_t* C, const uint64_t* A, const uint64_t* B, 
   // split K across CTAs when the output grid cannot fill the SMs (width 64:
   // partial sums combine with wrapping 64-bit atomics)
   int ksplit = 1;
-  if (width == 64 && tiles < 2 * 148 && K >= 4 * GT_BK) {
-    ksplit = (int)min((i64)(2 * 148 / tiles), (K + 2 * GT_BK - 1) / (2 * GT_BK));
+  if (width == 64 && tiles < 2 * dev_sms() && K >= 4 * GT_BK) {
+    ksplit = (int)min((i64)(2 * dev_sms() / tiles), (K + 2 * GT_BK - 1) / (2 * GT_BK));
     if (ksplit < 1) ksplit = 1;
   }
   const i64 kchunk = ((K + ksplit - 1) / ksplit + GT_BK - 1) / GT_BK * GT_BK;

@@ -142,7 +142,7 @@ extern "C" int mpx_ring_colsum(uint64_t* out, const uint64_t* x, int L, int64_t 
   const int threads = 256;
   // enough blocks to cover the SMs a few times, each a contiguous row band
   const i64 lanes = cols <= threads ? threads / cols : 1;
-  i64 nblk = (4 * 148 + L - 1) / L;
+  i64 nblk = (4 * (i64)dev_sms() + L - 1) / L;
   const i64 min_rows = 4 * lanes;
   nblk = max((i64)1, min(nblk, (rows + min_rows - 1) / min_rows));
   const i64 rpb = (rows + nblk - 1) / nblk;
@@ -809,7 +809,7 @@ extern "C" int mpx_im2col(uint64_t* out, const uint64_t* x, int L, int64_t B, in
   // narrow rows (< 64 columns) leave most lanes idle: element-per-thread path
   if (cols >= 64 && cols <= 8192 && (i64)C * H * W < (1ll << 31)) {
     const i64 nrow = (i64)L * B * OH * OW;
-    const i64 blocks = min((nrow + 7) / 8, (i64)148 * 16);
+    const i64 blocks = min((nrow + 7) / 8, (i64)dev_sms() * 16);
     k_im2col_tab<<<(unsigned)blocks, 256, (size_t)cols * 8, (cudaStream_t)stream>>>(out, x, L, (int)B, C, H, W, K,
                                                                                    stride, pad, OH, OW);
     return launch_status();
