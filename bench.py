@@ -1091,8 +1091,9 @@ def run_b200(args, group=None):
     line = None
     dealer_roof = None
     if rank == 0:
-        dealer_roof = dealer_roofline(torch, counter.demands, n_parties, counter.needs_bits,
-                                      float(np.median([d[0] for d in deal_ms[args.warmup:]])))
+        if world == 1:   # all parties' draws on this GPU (party mode deals one party's share of the work)
+            dealer_roof = dealer_roofline(torch, counter.demands, n_parties, counter.needs_bits,
+                                          float(np.median([d[0] for d in deal_ms[args.warmup:]])))
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,

@@ -369,7 +369,9 @@ __global__ void __launch_bounds__(192, BN == 32 ? 2 : 1)
 // Template: BK = k-block bytes (128 / 64 / 32 with the matching 128B / 64B /
 // 32B swizzle, so short reductions pad K to 32 or 64 instead of 128), BN =
 // N tile (64, or 32 for outputs at most 32 wide: 256 TMEM columns).
+#ifndef TCP_BST
 #define TCP_BST 2
+#endif
 #define TCP_STAGE_TILE (32 * 33 * 8)  // one 32 x 32 u64 transpose tile per epilogue warp
 #define TCP_STAGED_MAX_KB 4
 // A ring: every byte of shared memory the B stages and the epilogue tiles
@@ -547,7 +549,8 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
-      const uint32_t idesc = (2u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+      constexpr int MJ = 256 / BN;  // B limbs per MMA (N <= 256)
+      const uint32_t idesc_base = (2u << 4) | ((uint32_t)(TC_BM >> 4) << 24);
       const uint64_t a_desc0 = umma_desc_sw<BK>(smem_u32(sA));
       const uint64_t b_desc0 = umma_desc_sw<BK>(smem_u32(sB));
       int as = 0, gkb = 0, it = 0;
@@ -568,13 +571,20 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
             mbar_wait(&fullA[as], aph);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint64_t ad = a_desc0 + (uint64_t)((as * A_TILE) >> 4);
+            // A_i meets B_0..B_{7-i}: the B limb tiles sit back to back in the
+            // stage (rows of one K-major operand), and their diagonals i..7
+            // are adjacent TMEM column blocks, so ONE MMA of N = nj * BN
+            // covers nj limbs (N <= 256): 12 MMAs per k-step instead of 36
+            // at BN = 64, 8 at BN = 32 (same tensor work, a third of the issue)
 #pragma unroll
-            for (int j = 0; j <= 7 - i; ++j) {
-              const uint32_t d_tmem = tmem_base + (uint32_t)((i + j) * BN);
-              const uint64_t bd = bd0 + (uint64_t)((j * B_TILE) >> 4);
+            for (int j0 = 0; j0 <= 7 - i; j0 += MJ) {
+              const int nj = (8 - i - j0) < MJ ? (8 - i - j0) : MJ;
+              const uint32_t d_tmem = tmem_base + (uint32_t)((i + j0) * BN);
+              const uint64_t bd = bd0 + (uint64_t)((j0 * B_TILE) >> 4);
+              const uint32_t id = idesc_base | ((uint32_t)((nj * BN) >> 3) << 17);
 #pragma unroll
               for (int kk = 0; kk < BK / 32; ++kk)
-                if (!(args.dbg & 4)) mma_i8(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, (i > 0 || kk > 0) ? 1u : first);
+                if (!(args.dbg & 4)) mma_i8(d_tmem, ad + 2 * kk, bd + 2 * kk, id, (i > 0 || kk > 0) ? 1u : first);
             }
             umma_commit(&emptyA[as]);
             if (++as == AST) {
@@ -973,10 +983,22 @@ __device__ __forceinline__ void ml_load8(u64 (&v)[8], const u64* __restrict__ sr
   const int rr = t >> 3, g = t & 7;
   if constexpr (KFAST) {
     const i64 r = r0 + rr;
+    const i64 kb = k0 + g * 8;
+    const u64* p = src + r * sr + kb;
+    if (r < R && kb + 8 <= K && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+      // four 16-byte loads instead of eight 8-byte ones
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const i64 k = k0 + g * 8 + c;
-      v[c] = (r < R && k < K) ? src[r * sr + k] : 0ull;
+      for (int c = 0; c < 8; c += 2) {
+        const ulonglong2 q = __ldg(reinterpret_cast<const ulonglong2*>(p + c));
+        v[c] = q.x;
+        v[c + 1] = q.y;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const i64 k = kb + c;
+        v[c] = (r < R && k < K) ? src[r * sr + k] : 0ull;
+      }
     }
   } else {
 #pragma unroll
@@ -1647,7 +1669,7 @@ __global__ void __launch_bounds__(256, 1) k_beaver_tc_thin(const __grid_constant
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_holder;
-  const uint32_t idesc = (2u << 4) | ((uint32_t)(32 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  const uint32_t idesc_base = (2u << 4) | ((uint32_t)(128 >> 4) << 24);
 
   if (warp < 4) {
     // ---------------- producers ----------------
@@ -1716,23 +1738,18 @@ __global__ void __launch_bounds__(256, 1) k_beaver_tc_thin(const __grid_constant
             if (job >= 2) mbar_wait(&te[buf], (uint32_t)(((job - 2) >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t dt = tmem_base + (uint32_t)(buf * 256);
+            // A_i x [B_0 .. B_{7-i}] as ONE MMA of N = 32 (8 - i): the B limb
+            // tiles are consecutive rows of one operand and diagonals i..7
+            // adjacent TMEM column blocks
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-              const uint64_t ad = umma_desc_sw<32>(smem_u32(sD + i * THIN_TA));
-#pragma unroll
-              for (int jj = 0; jj <= 7 - i; ++jj)
-                if (!(a.dbg & 4))
-                  mma_i8(dt + (uint32_t)((i + jj) * 32), ad,
-                         umma_desc_sw<32>(smem_u32(sBp + (l * 8 + jj) * THIN_TB)), idesc, i > 0 ? 1u : 0u);
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const uint64_t ad = umma_desc_sw<32>(smem_u32(sA + (l * 8 + i) * THIN_TA));
-#pragma unroll
-              for (int jj = 0; jj <= 7 - i; ++jj)
-                if (!(a.dbg & 4))
-                  mma_i8(dt + (uint32_t)((i + jj) * 32), ad, umma_desc_sw<32>(smem_u32(sE + jj * THIN_TB)), idesc,
-                         1u);
+              const uint32_t id = idesc_base | ((uint32_t)((32 * (8 - i)) >> 3) << 17);
+              if (!(a.dbg & 4)) {
+                mma_i8(dt + (uint32_t)(i * 32), umma_desc_sw<32>(smem_u32(sD + i * THIN_TA)),
+                       umma_desc_sw<32>(smem_u32(sBp + l * 8 * THIN_TB)), id, i > 0 ? 1u : 0u);
+                mma_i8(dt + (uint32_t)(i * 32), umma_desc_sw<32>(smem_u32(sA + (l * 8 + i) * THIN_TA)),
+                       umma_desc_sw<32>(smem_u32(sE)), id, 1u);
+              }
             }
             umma_commit(&tf[buf]);
           }
