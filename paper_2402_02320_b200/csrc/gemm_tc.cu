@@ -1092,6 +1092,48 @@ __device__ __forceinline__ void ml_tile(MaskLimbArgs a, i64 r0, i64 k0, i64 jb, 
   }
 }
 
+// Row-major X and T (k contiguous) with L <= 3: every party's X_l and T_l
+// words of the thread are loaded before any is used (2L x 64 bytes in flight
+// per thread instead of 2 x 64: the party loop above is latency bound).
+template <int LP>
+__device__ __forceinline__ void ml_tile_pre(MaskLimbArgs a, i64 r0, i64 k0, i64 jb) {
+  const int t = threadIdx.x;
+  const i64 plane = a.Rpad * a.Kp;
+  const bool defer = a.add_p0 && a.p0 >= 0;
+  a.X += jb * a.x_js;
+  a.T += jb * a.t_js;
+  a.S8 += jb * 8 * plane;
+  a.P8 += jb * (i64)a.L * 8 * plane;
+  u64 xv[LP][8], tv[LP][8];
+#pragma unroll
+  for (int l = 0; l < LP; ++l) {
+    ml_load8<true>(xv[l], a.X + (i64)l * a.x_ps, a.x_sr, 1, r0, k0, a.R, a.K, nullptr, t);
+    ml_load8<true>(tv[l], a.T + (i64)l * a.t_ps, a.t_sr, 1, r0, k0, a.R, a.K, nullptr, t);
+  }
+  u64 s[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s[c] = 0;
+#pragma unroll
+  for (int l = 0; l < LP; ++l) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) s[c] += xv[l][c] - tv[l][c];
+    if (!(defer && l == a.p0)) ml_emit(a.P8 + (i64)l * 8 * plane, plane, tv[l], r0, k0, a.Kp, t);
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s[c] &= a.msk;
+  ml_emit(a.S8, plane, s, r0, k0, a.Kp, t);
+  if (defer) {
+#pragma unroll
+    for (int l = 0; l < LP; ++l)
+      if (l == a.p0) {
+        u64 v[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) v[c] = (tv[l][c] + s[c]) & a.msk;
+        ml_emit(a.P8 + (i64)l * 8 * plane, plane, v, r0, k0, a.Kp, t);
+      }
+  }
+}
+
 template <bool XK, bool TK>
 __global__ void __launch_bounds__(256, 3) k_mask_limbs(MaskLimbArgs a) {
   __shared__ u64 tile[64][33];
@@ -1113,15 +1155,26 @@ __device__ __forceinline__ void ml_tile_rt(const MaskLimbArgs& a, i64 r0, i64 k0
     ml_tile<false, false>(a, r0, k0, jb, tile);
 }
 
-__global__ void __launch_bounds__(256, 3) k_mask_limbs2(const __grid_constant__ MaskLimbArgs a,
+__device__ __forceinline__ void ml_tile_any(const MaskLimbArgs& a, i64 r0, i64 k0, i64 jb, u64 (*tile)[33]) {
+  if (a.x_sc == 1 && a.t_sc == 1 && a.L <= 3) {
+    switch (a.L) {
+      case 1: ml_tile_pre<1>(a, r0, k0, jb); return;
+      case 2: ml_tile_pre<2>(a, r0, k0, jb); return;
+      default: ml_tile_pre<3>(a, r0, k0, jb); return;
+    }
+  }
+  ml_tile_rt(a, r0, k0, jb, tile);
+}
+
+__global__ void __launch_bounds__(256, 2) k_mask_limbs2(const __grid_constant__ MaskLimbArgs a,
                                                         const __grid_constant__ MaskLimbArgs b, int ax, int na,
                                                         int bx) {
   __shared__ u64 tile[64][33];
   const int id = blockIdx.x;
   if (id < na)
-    ml_tile_rt(a, (i64)(id % ax) * 32, (i64)(id / ax) * 64, blockIdx.y, tile);
+    ml_tile_any(a, (i64)(id % ax) * 32, (i64)(id / ax) * 64, blockIdx.y, tile);
   else
-    ml_tile_rt(b, (i64)((id - na) % bx) * 32, (i64)((id - na) / bx) * 64, blockIdx.y, tile);
+    ml_tile_any(b, (i64)((id - na) % bx) * 32, (i64)((id - na) / bx) * 64, blockIdx.y, tile);
 }
 
 static void ml_pack(MaskLimbArgs& a, uint8_t* S8, uint8_t* P8, const uint64_t* X, int64_t x_ps, int64_t x_sr,
