@@ -280,7 +280,9 @@ struct SimOperand {
   i64 ps, sr, sc, js;  // party, row, col, job strides (elements)
 };
 
+#ifndef BS_BK
 #define BS_BK 8  // k-depth of one pipeline stage
+#endif
 
 // Raw operand tiles of one k-step: every party's X_l, A_l, Y_l, B_l.
 template <int L, int BM, int BN>

@@ -677,6 +677,39 @@ __global__ void k_im2col(u64* __restrict__ out, const u64* __restrict__ x, IT B,
   }
 }
 
+// Stride 1, K <= 5 (LeNet's 5 x 5): every window gather of an output is
+// issued before the sum (predicated loads instead of data-dependent
+// continues).
+template <int KM>
+__global__ void k_col2im_s1(u64* __restrict__ dx, const u64* __restrict__ colsb, uint32_t B, int C, int H, int W,
+                            int K, int P, int OH, int OW, uint32_t total, u64 msk) {
+  const uint32_t cols = (uint32_t)C * K * K;
+  const uint32_t rows = B * (uint32_t)OH * OW;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int w = (int)(t % W);
+    const uint32_t t1 = t / W;
+    const int h = (int)(t1 % H);
+    const uint32_t t2 = t1 / H;
+    const int c = (int)(t2 % C);
+    const uint32_t bl = t2 / C;
+    const uint32_t b = bl % B, l = bl / B;
+    const u64* base = colsb + ((i64)l * rows + (i64)b * OH * OW) * cols + (i64)c * K * K;
+    u64 v[KM * KM];
+#pragma unroll
+    for (int kh = 0; kh < KM; ++kh)
+#pragma unroll
+      for (int kw = 0; kw < KM; ++kw) {
+        const int oh = h + P - kh, ow = w + P - kw;
+        const bool ok = kh < K && kw < K && oh >= 0 && oh < OH && ow >= 0 && ow < OW;
+        v[kh * KM + kw] = ok ? __ldg(base + ((i64)oh * OW + ow) * cols + kh * K + kw) : 0ull;
+      }
+    u64 acc = 0;
+#pragma unroll
+    for (int q = 0; q < KM * KM; ++q) acc += v[q];
+    dx[t] = acc & msk;
+  }
+}
+
 template <typename IT, bool S1>
 __global__ void k_col2im(u64* __restrict__ dx, const u64* __restrict__ colsb, IT B, IT C, IT H, IT W, IT K,
                          IT S, IT P, IT OH, IT OW, IT total, u64 msk) {
@@ -739,15 +772,26 @@ __global__ void __launch_bounds__(256) k_im2col_tab(u64* __restrict__ out, const
     const u64* xb = x + (l * B + b) * (i64)C * H * W;
     const i64 base = (i64)h0 * W + w0;
     u64* o = out + lr * cols;
-    for (int col = lane; col < cols; col += 32) {
-      u64 v;
-      if (inside) {
-        v = xb[base + tab[col]];
-      } else {
-        const int kk = tab[cols + col], h = h0 + (kk >> 16), w = w0 + (kk & 0xFFFF);
-        v = (h >= 0 && h < H && w >= 0 && w < W) ? xb[base + tab[col]] : 0ull;
+    // four columns per lane in flight (the gathers hit L1/L2; one at a time
+    // the loop is latency bound)
+    for (int c0 = lane; c0 < cols; c0 += 128) {
+      u64 v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int col = c0 + 32 * q;
+        v[q] = 0;
+        if (col < cols) {
+          if (inside) {
+            v[q] = __ldg(xb + base + tab[col]);
+          } else {
+            const int kk = tab[cols + col], h = h0 + (kk >> 16), w = w0 + (kk & 0xFFFF);
+            if (h >= 0 && h < H && w >= 0 && w < W) v[q] = __ldg(xb + base + tab[col]);
+          }
+        }
       }
-      o[col] = v;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (c0 + 32 * q < cols) o[c0 + 32 * q] = v[q];
     }
   }
 }
@@ -788,12 +832,23 @@ __global__ void __launch_bounds__(256) k_im2col_narrow(u64* __restrict__ out, co
     __syncthreads();
     const int nel = (int)min((i64)256, nrow - r0) * cols;
     u64* o = out + r0 * cols;
-    for (int idx = threadIdx.x; idx < nel; idx += blockDim.x) {
-      const int rl = idx / cols, col = idx - rl * cols;
-      const unsigned hw = (unsigned)rhw[rl];
-      const int kk = tabk[col];
-      const int h = (int)(hw >> 16) - 0x8000 + (kk >> 16), w = (int)(hw & 0xFFFF) - 0x8000 + (kk & 0xFFFF);
-      o[idx] = (h >= 0 && h < H && w >= 0 && w < W) ? x[rbase[rl] + tab[col]] : 0ull;
+    for (int i0 = threadIdx.x; i0 < nel; i0 += 4 * blockDim.x) {
+      u64 v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int idx = i0 + q * blockDim.x;
+        v[q] = 0;
+        if (idx < nel) {
+          const int rl = idx / cols, col = idx - rl * cols;
+          const unsigned hw = (unsigned)rhw[rl];
+          const int kk = tabk[col];
+          const int h = (int)(hw >> 16) - 0x8000 + (kk >> 16), w = (int)(hw & 0xFFFF) - 0x8000 + (kk & 0xFFFF);
+          if (h >= 0 && h < H && w >= 0 && w < W) v[q] = __ldg(x + rbase[rl] + tab[col]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (i0 + q * blockDim.x < nel) o[i0 + q * blockDim.x] = v[q];
     }
   }
 }
@@ -816,7 +871,7 @@ extern "C" int mpx_im2col(uint64_t* out, const uint64_t* x, int L, int64_t B, in
   }
   if (cols < 64 && H < 0x4000 && W < 0x4000 && pad < 0x4000) {
     const i64 nrow = (i64)L * B * OH * OW;
-    const i64 blocks = min((nrow + 255) / 256, (i64)148 * 8);
+    const i64 blocks = min((nrow + 255) / 256, (i64)dev_sms() * 8);
     k_im2col_narrow<<<(unsigned)blocks, 256, 256 * 12 + (size_t)cols * 8, (cudaStream_t)stream>>>(
         out, x, L, (int)B, C, H, W, K, stride, pad, OH, OW);
     return launch_status();
@@ -838,6 +893,11 @@ extern "C" int mpx_col2im(uint64_t* dx, const uint64_t* cols, int L, int64_t B, 
   CHECK_ARG(OH >= 1 && OW >= 1);
   const i64 total = (i64)L * B * C * H * W;
   if (total == 0) return MPX_OK;
+  if (stride == 1 && K <= 5 && total < (1ll << 31) && (i64)L * B * OH * OW * C * K * K < (1ll << 31)) {
+    k_col2im_s1<5><<<grid_for(total), MPX_THREADS, 0, (cudaStream_t)stream>>>(
+        dx, cols, (uint32_t)B, C, H, W, K, pad, OH, OW, (uint32_t)total, ring_mask(width));
+    return launch_status();
+  }
   if (total < (1ll << 31) && (i64)L * B * OH * OW * C * K * K < (1ll << 32))
     if (stride == 1)
       k_col2im<uint32_t, true><<<grid_for(total), MPX_THREADS, 0, (cudaStream_t)stream>>>(
