@@ -45,8 +45,8 @@ struct Tape {
 #ifndef MPX_MINB3  // L = 3 at 128 regs: ReLU 0.87 / max_vec 2.65 / Log 3.35 ms at 2^22 vs 1.04 / 2.75 / 3.60
 #define MPX_MINB3 4     // at 80 regs and 0.90 / 2.67 / 3.84 at 168; LeNet n = 3 step 1.564 vs 1.583 ms
 #endif
-#ifndef MPX_MINB4
-#define MPX_MINB4 MPX_CMP_MINB
+#ifndef MPX_MINB4  // four parties in one lane (forced MPX_SPLIT4=1 layouts): 128 registers, no spills
+#define MPX_MINB4 4
 #endif
 #define MPX_MINB_L(L, B2) ((L) <= 2 ? (B2) : (L) == 3 ? MPX_MINB3 : (L) == 4 ? MPX_MINB4 : 1)
 // n = 8 split over two lanes (4 parties per lane): 128-register cap
@@ -653,7 +653,7 @@ __device__ __forceinline__ Sh<L> d_reciprocal(const Sh<L>& x, const Tape& tape, 
 // Standalone kernel keeps its own copy of the body: through d_reciprocal it
 // compiles to 72 registers + spills at L = 2 (8.3 vs 7.9 ms at 2^24).
 template <int L, int G>
-__global__ void __launch_bounds__(128, G >= 2 ? MPX_MINB_G4 : MPX_MINB_RCP1(L)) k_reciprocal_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
+__global__ void __launch_bounds__(128, G >= 2 ? (L >= 4 ? MPX_MINB_SPLIT : MPX_MINB_G4) : MPX_MINB_RCP1(L)) k_reciprocal_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
                                                           const __grid_constant__ Tape tape, FusedParams P) {
   const int w = P.w, p = P.p, p0 = P.p0;
   const u64 msk = ring_mask(w);
@@ -710,7 +710,7 @@ __global__ void __launch_bounds__(128, G >= 2 ? MPX_MINB_G4 : MPX_MINB_RCP1(L)) 
 // Exponentiation, paper Alg. 2 (nonlinear.py:179-213)
 
 template <int L, int G>
-__global__ void __launch_bounds__(128, G >= 2 ? MPX_MINB_G4 : MPX_MINB_EXP1(L)) k_exp_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
+__global__ void __launch_bounds__(128, G >= 2 ? (L >= 4 ? MPX_MINB_SPLIT : MPX_MINB_G4) : MPX_MINB_EXP1(L)) k_exp_fused(u64* __restrict__ y, const u64* __restrict__ xin, i64 n,
                                                    const __grid_constant__ Tape tape, FusedParams P) {
   const int w = P.w, p = P.p, p0 = P.p0, c = P.c, bias = P.bias;
   const u64 msk = ring_mask(w);
