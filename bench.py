@@ -890,7 +890,8 @@ def party_mode_entry(torch, dev, n: int = 3, steps: int = 5, warmup: int = 2):
 def party_scaling(torch, G, dev, group, ns=(2, 4, 8)):
     """North-star party sweep, all n parties simulated on one GPU (one-GPU-
     per-party runs need an n-GPU box: bench.py --gpus n under torchrun):
-    LeNet training step, 18.9M Transformer inference, Beaver matmul 4096^2,
+    LeNet / AlexNet / VGG16m training steps (configs[1], configs[2]), 18.9M
+    Transformer inference, Beaver matmul 4096^2,
     and Reciprocal / Exp / Log on 2^22 elements (2^24 x 8 parties of
     single-use material would exceed HBM)."""
     from paper_2402_02320_b200.session import SimSession
@@ -901,6 +902,17 @@ def party_scaling(torch, G, dev, group, ns=(2, 4, 8)):
         parties = tuple(range(n))
         e = {"lenet_train_ms": cifar_entry(torch, dev, "lenet", 3, 2, n=n)["ms_per_step"],
              "transformer_infer_ms": transformer_entry(torch, dev, 3, 2, n=n)["latency_ms"]}
+        # configs[2] at 2/4/8 parties: AlexNet, and VGG16m where its single-use
+        # material (~15 GB per party per step) still fits HBM next to the step
+        for arch in ("alexnet", "vgg16m"):
+            try:
+                ce = cifar_entry(torch, dev, arch, 2, 1, n=n)
+                e[f"{arch}_train_ms"] = ce["ms_per_step"]
+                e[f"{arch}_material_GB"] = ce["material_GB_per_step"]
+            except torch.cuda.OutOfMemoryError as err:
+                e[f"{arch}_train_ms"] = None
+                e[f"{arch}_skipped"] = f"out of device memory at n = {n} ({str(err).splitlines()[0][:120]})"
+            torch.cuda.empty_cache()
         mm = sweep_entry(torch, G, mk, parties, n, dev, "matmul")
         e["matmul_4096_ms"] = mm["ms_per_op"]
         r = reciprocal_entry(torch, G, mk, parties, n, dev, group, 2, 1, elems=1 << 22)
