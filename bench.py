@@ -456,6 +456,9 @@ def alg_bytes(name, a):
     return None
 
 
+INT8_SPEC_TOPS = 4500.0   # B200 nominal dense int8 (B200_PROFILING.md / the task's nominal peaks)
+
+
 def int8_alt_peak():
     """Second int8 denominator: 2 x the driver-measured bf16 burst."""
     try:
@@ -684,6 +687,7 @@ def roofline_for(per, int8_peak=None):
                     frac=(ach / int8_peak) if int8_peak else None, traffic=traffic,
                     peak_alt=alt, frac_alt=(ach / alt) if alt else None,
                     peak_alt_kind="2 x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x bf16 on B200)",
+                    peak_spec=INT8_SPEC_TOPS, frac_spec=ach / INT8_SPEC_TOPS,
                     traffic_unit="DRAM bytes per launch (ncu)", alg_ops_per_launch=dom["ops"] // dom["n"])
     peak, peak_kind = _read_peaks()
     ach = dom["bytes"] / (dom["ms"] / 1e3) / 1e9 if dom["bytes_known"] else None
@@ -1100,7 +1104,8 @@ def run_b200(args, group=None):
                               "peak_kind": "measured in-run: torch._int_mm int8 8192^3 (cuBLASLt), burst",
                               "unit": "TOPS int8",
                               "frac": (mm["gemm_int8_TOPS"] / int8_pk) if mm.get("gemm_int8_TOPS") else None,
-                              "peak_alt": int8_alt_peak(),
+                              "peak_alt": int8_alt_peak(), "peak_spec": INT8_SPEC_TOPS,
+                              "frac_spec": (mm["gemm_int8_TOPS"] / INT8_SPEC_TOPS) if mm.get("gemm_int8_TOPS") else None,
                               "frac_alt": (mm["gemm_int8_TOPS"] / int8_alt_peak())
                               if mm.get("gemm_int8_TOPS") and int8_alt_peak() else None}
         if world == 1:

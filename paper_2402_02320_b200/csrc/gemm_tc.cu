@@ -1826,13 +1826,16 @@ __global__ void __launch_bounds__(256, 1) k_beaver_tc_thin(const __grid_constant
         for (int q = 0; q < 32; ++q) acc[q] = (q < N && row < a.M && !(a.dbg & 2)) ? __ldg(Cl + q) : 0ull;  // addend first
         mbar_wait(&tf[buf], (uint32_t)((job >> 1) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        // two diagonals' TMEM loads in flight per wait (four waits per party)
 #pragma unroll
-        for (int dd = 0; dd < 8; ++dd) {
-          uint32_t v[32];
-          TMEM_LD32(tmem_base + ((uint32_t)(rq * 32) << 16) + (uint32_t)(buf * 256 + dd * 32), v);
+        for (int d0 = 0; d0 < 8; d0 += 2) {
+          uint32_t v0[32], v1[32];
+          const uint32_t ta = tmem_base + ((uint32_t)(rq * 32) << 16) + (uint32_t)(buf * 256 + d0 * 32);
+          TMEM_LD32(ta, v0);
+          TMEM_LD32(ta + 32, v1);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-          for (int q = 0; q < 32; ++q) acc[q] += (u64)v[q] << (8 * dd);
+          for (int q = 0; q < 32; ++q) acc[q] += ((u64)v0[q] << (8 * d0)) + ((u64)v1[q] << (8 * d0 + 8));
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
