@@ -1134,60 +1134,6 @@ __device__ __forceinline__ void ml_tile_pre(MaskLimbArgs a, i64 r0, i64 k0, i64 
   }
 }
 
-// Transposed X (any strides: X^T views of an im2col buffer or activations)
-// with row-major T, L <= 3: every party's raw X words (read along X's unit
-// stride, as ml_load8<false>) and T words are loaded before the per-party
-// shared-memory transposes.
-template <int LP>
-__device__ __forceinline__ void ml_tile_pre_t(MaskLimbArgs a, i64 r0, i64 k0, i64 jb, u64 (*tile)[33]) {
-  const int t = threadIdx.x;
-  const i64 plane = a.Rpad * a.Kp;
-  const bool defer = a.add_p0 && a.p0 >= 0;
-  a.X += jb * a.x_js;
-  a.T += jb * a.t_js;
-  a.S8 += jb * 8 * plane;
-  a.P8 += jb * (i64)a.L * 8 * plane;
-  u64 xr[LP][8], tv[LP][8];
-#pragma unroll
-  for (int l = 0; l < LP; ++l) {
-    const u64* src = a.X + (i64)l * a.x_ps;
-#pragma unroll
-    for (int p = 0; p < 8; ++p) {
-      const int r2 = t & 31, k2 = (t >> 5) + 8 * p;
-      const i64 r = r0 + r2, k = k0 + k2;
-      xr[l][p] = (r < a.R && k < a.K) ? __ldg(src + r * a.x_sr + k * a.x_sc) : 0ull;
-    }
-    ml_load8<true>(tv[l], a.T + (i64)l * a.t_ps, a.t_sr, 1, r0, k0, a.R, a.K, nullptr, t);
-  }
-  const int rr = t >> 3, g = t & 7;
-  u64 s[8];
-#pragma unroll
-  for (int c = 0; c < 8; ++c) s[c] = 0;
-#pragma unroll
-  for (int l = 0; l < LP; ++l) {
-#pragma unroll
-    for (int p = 0; p < 8; ++p) tile[(t >> 5) + 8 * p][t & 31] = xr[l][p];
-    __syncthreads();
-#pragma unroll
-    for (int c = 0; c < 8; ++c) s[c] += tile[g * 8 + c][rr] - tv[l][c];
-    __syncthreads();
-    if (!(defer && l == a.p0)) ml_emit(a.P8 + (i64)l * 8 * plane, plane, tv[l], r0, k0, a.Kp, t);
-  }
-#pragma unroll
-  for (int c = 0; c < 8; ++c) s[c] &= a.msk;
-  ml_emit(a.S8, plane, s, r0, k0, a.Kp, t);
-  if (defer) {
-#pragma unroll
-    for (int l = 0; l < LP; ++l)
-      if (l == a.p0) {
-        u64 v[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) v[c] = (tv[l][c] + s[c]) & a.msk;
-        ml_emit(a.P8 + (i64)l * 8 * plane, plane, v, r0, k0, a.Kp, t);
-      }
-  }
-}
-
 template <bool XK, bool TK>
 __global__ void __launch_bounds__(256, 3) k_mask_limbs(MaskLimbArgs a) {
   __shared__ u64 tile[64][33];
@@ -1216,13 +1162,6 @@ __device__ __forceinline__ void ml_tile_any(const MaskLimbArgs& a, i64 r0, i64 k
       case 2: ml_tile_pre<2>(a, r0, k0, jb); return;
       default: ml_tile_pre<3>(a, r0, k0, jb); return;
     }
-  }
-  if (a.x_sc != 1 && a.t_sc == 1 && a.L >= 2 && a.L <= 3) {
-    if (a.L == 2)
-      ml_tile_pre_t<2>(a, r0, k0, jb, tile);
-    else
-      ml_tile_pre_t<3>(a, r0, k0, jb, tile);
-    return;
   }
   ml_tile_rt(a, r0, k0, jb, tile);
 }
