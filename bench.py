@@ -398,7 +398,13 @@ def alg_bytes(name, a):
             return L * rows * cols * 8 + L * rows * 8
         if name == "mpx_bits_gather":
             return 16 * a[4]
-        if name in ("mpx_gemm_limbs", "mpx_gemm_limbs_split"):  # int8 ops, not bytes: see roofline_for
+        if name == "mpx_gemm_limbs_split":
+            # (C, PA8, SA8, PB8, SB8, batch, M, N, Mpad, Npad, Kh, ldc, sC, width, ksplit, Cin, sCin, zl, ...):
+            # shared + per-party limb planes read once, the C addend read and Z written (int8 ops: roofline_for)
+            batch, M, N, Mpad, Npad, Kh, zl = a[5], a[6], a[7], a[8], a[9], a[10], a[17]
+            jobs = batch // max(zl, 1)
+            return 8 * Kh * (Mpad + Npad) * (jobs + batch) + (2 if a[15] else 1) * batch * M * N * 8
+        if name == "mpx_gemm_limbs":  # int8 ops, not bytes: see roofline_for
             return None
         if name == "mpx_mask_limbs":
             # X_l, T_l read once; shared S limbs + per-party T limbs written
@@ -681,7 +687,14 @@ def roofline_for(per, int8_peak=None):
     if dom_name in ("mpx_gemm_limbs", "mpx_gemm_limbs_split"):
         ach = dom["ops"] / (dom["ms"] / 1e3) / 1e12
         alt = int8_alt_peak()
+        hbm_peak, _ = _read_peaks()
+        hbm = (dom["bytes"] / (dom["ms"] / 1e3) / 1e9) if dom["bytes_known"] and dom["bytes"] else None
         return dict(common, bound="tensor", achieved=ach, peak=int8_peak, unit="TOPS int8",
+                    hbm_view={"achieved_GBps": hbm, "peak_GBps": hbm_peak,
+                              "frac": (hbm / hbm_peak) if hbm else None,
+                              "alg_bytes_per_launch": (dom["bytes"] // dom["n"]) if hbm else None,
+                              "note": "limb planes read once + C addend read + Z written: the thin LeNet "
+                                      "products are operand/epilogue paced, so both views are reported"},
                     peak_kind="measured in-run: torch._int_mm int8 8192^3 (cuBLASLt), burst "
                               "(MEASURED_PEAKS.json carries bf16 only)",
                     frac=(ach / int8_peak) if int8_peak else None, traffic=traffic,
