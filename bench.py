@@ -42,6 +42,8 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 METRIC = "secure CNN train steps/s: LeNet, batch 128 (BASELINE configs[1])"
+LENET_WORKLOAD = ("configs[1]: secure LeNet training step (conv20-5x5, avgpool, ReLU, conv50-5x5, avgpool, ReLU, "
+                  "FC800x500, ReLU, FC500x10; softmax-CE; SGD lr 2^-5)")
 UNIT = "steps/s"
 RECIP_UNIT = "elements/s"
 BATCH = 128
@@ -1145,9 +1147,7 @@ def run_b200(args, group=None):
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64 (Z_2^64 fixed point, p=23)",
             "data": "synthetic: x ~ U(0,1) 128x1x28x28, uniform labels; Kaiming-init secret weights",
-            "config": {"workload": "configs[1]: secure LeNet training step (conv20-5x5, avgpool, ReLU, "
-                                   "conv50-5x5, avgpool, ReLU, FC800x500, ReLU, FC500x10; softmax-CE; SGD "
-                                   "lr 2^-5)",
+            "config": {"workload": LENET_WORKLOAD,
                        "parties": n_parties, "batch": B, "frac": FRAC, "ring_width": WIDTH,
                        "mode": ("sim: all parties on 1 GPU, step captured in one CUDA graph" if world == 1
                                 else "one party per GPU, NCCL openings" +
@@ -1220,7 +1220,7 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": 1e3 / value, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64 (Z_2^64 fixed point, p=23)", "impl": "reference",
             "data": "synthetic: x ~ U(0,1) 128x1x28x28, uniform labels; Kaiming-init secret weights",
-            "config": {"workload": "configs[1]: secure LeNet training step", "parties": n_parties,
+            "config": {"workload": LENET_WORKLOAD, "parties": n_parties,
                        "batch": BATCH, "frac": FRAC, "ring_width": WIDTH, "mode": mode},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
