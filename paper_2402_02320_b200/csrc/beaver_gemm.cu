@@ -16,6 +16,30 @@
 #define BG_BK 16
 
 
+// Z[b][l] = C[b][l] (M*N words each) for every product b and party l: the
+// split-K partial products then land on a copy of C. One 2D copy when the
+// (product, party) slabs sit at uniform pitches; else one per party (rows =
+// products) or one per product (rows = parties), whichever is fewer.
+static int batch_copy_c(u64* Z, i64 sZ, i64 bZ, const u64* C, i64 sC, i64 bC, i64 MN, int L, i64 batch,
+                        cudaStream_t s) {
+  const size_t w = (size_t)(MN * 8);
+  if (batch == 1 || (bZ == (i64)L * sZ && bC == (i64)L * sC))
+    return cudaMemcpy2DAsync(Z, (size_t)sZ * 8, C, (size_t)sC * 8, w, (size_t)(L * batch), cudaMemcpyDeviceToDevice,
+                             s) == cudaSuccess ? MPX_OK : MPX_ERR_CUDA;
+  if (L < batch && bZ >= MN && bC >= MN) {
+    for (int l = 0; l < L; ++l)
+      if (cudaMemcpy2DAsync(Z + l * sZ, (size_t)bZ * 8, C + l * sC, (size_t)bC * 8, w, (size_t)batch,
+                            cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        return MPX_ERR_CUDA;
+    return MPX_OK;
+  }
+  for (i64 b = 0; b < batch; ++b)
+    if (cudaMemcpy2DAsync(Z + b * bZ, (size_t)sZ * 8, C + b * bC, (size_t)sC * 8, w, (size_t)L,
+                          cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      return MPX_ERR_CUDA;
+  return MPX_OK;
+}
+
 // <= 128 registers per thread (a block occupies whole warps)
 constexpr int bg_min_blocks(int nt) { return 512 / (nt < 32 ? 32 : nt); }
 
@@ -230,10 +254,7 @@ extern "C" int mpx_beaver_gemm_batched(uint64_t* Z, int64_t sZ, int64_t bZ, cons
   cudaStream_t s = (cudaStream_t)stream;
   if (ksplit > 1) {
     // every party's partial products land on a copy of its C
-    for (i64 b = 0; b < batch; ++b)
-      if (cudaMemcpy2DAsync(Z + b * bZ, (size_t)sZ * 8, C + b * bC, (size_t)sC * 8, (size_t)(M * N * 8), (size_t)L,
-                            cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-        return MPX_ERR_CUDA;
+    if (batch_copy_c(Z, sZ, bZ, C, sC, bC, (i64)M * N, L, batch, s) != MPX_OK) return MPX_ERR_CUDA;
   }
   dim3 grid((unsigned)((N + bn - 1) / bn), (unsigned)((M + bm - 1) / bm), (unsigned)(L * batch * ksplit));
   const u64 msk = ring_mask(width);
@@ -461,10 +482,7 @@ int launch_sim(i64 tiles_n, i64 tiles_m, i64 batch, i64 K, cudaStream_t s, uint6
   ksplit = (int)((K + kchunk - 1) / kchunk);
   if (batch * ksplit > 65535 || tiles_m > 65535) return MPX_ERR_ARG;
   if (ksplit > 1) {
-    for (i64 b = 0; b < batch; ++b)
-      if (cudaMemcpy2DAsync(Z + b * bZ, (size_t)sZ * 8, C + b * bC, (size_t)sC * 8, (size_t)((i64)M * N * 8),
-                            (size_t)L, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-        return MPX_ERR_CUDA;
+    if (batch_copy_c(Z, sZ, bZ, C, sC, bC, (i64)M * N, L, batch, s) != MPX_OK) return MPX_ERR_CUDA;
   }
   dim3 grid((unsigned)tiles_n, (unsigned)tiles_m, (unsigned)(batch * ksplit));
   k_beaver_gemm_sim<L, BM, BN, TN><<<grid, nthr, smem, s>>>(Z, sZ, bZ, C, sC, bC, X, A, sA, bA, Y, B, sB, bB, M,

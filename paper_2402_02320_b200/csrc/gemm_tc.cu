@@ -1455,10 +1455,15 @@ static int gemm_limbs_impl(uint64_t* C, const uint8_t* A8, const uint8_t* B8, co
   if (!legacy) {
     // split slices meet in C through atomics: start from zero unless C is
     // the accumulate operand (the addend rides on slice 0)
-    if (ksplit > 1 && !accumulate)
-      for (i64 z = 0; z < batch; ++z)
-        if (cudaMemset2DAsync(C + z * sC, (size_t)ldc * 8, 0, (size_t)N * 8, (size_t)M, s) != cudaSuccess)
-          return MPX_ERR_CUDA;
+    if (ksplit > 1 && !accumulate) {
+      if (ldc == N && sC == M * N) {  // one contiguous block: one memset node instead of `batch`
+        if (cudaMemsetAsync(C, 0, (size_t)(batch * M * N * 8), s) != cudaSuccess) return MPX_ERR_CUDA;
+      } else {
+        for (i64 z = 0; z < batch; ++z)
+          if (cudaMemset2DAsync(C + z * sC, (size_t)ldc * 8, 0, (size_t)N * 8, (size_t)M, s) != cudaSuccess)
+            return MPX_ERR_CUDA;
+      }
+    }
     if (make_map(&mapA, A8, batch * 8, Mpad, kcols, TC_BM, bk) != MPX_OK ||
         make_map(&mapB, B8, batch * 8, Npad, kcols, bn, bk) != MPX_OK)
       return MPX_ERR_CUDA;
