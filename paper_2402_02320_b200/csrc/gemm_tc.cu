@@ -79,6 +79,16 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// 3D box: consecutive limb planes land in consecutive 2D tiles of the stage
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                        uint32_t accumulate) {
   const uint32_t z = 0;
@@ -380,13 +390,20 @@ __global__ void __launch_bounds__(192, BN == 32 ? 2 : 1)
 #ifndef MPX_TC_ARING_KB
 #define MPX_TC_ARING_KB 1024
 #endif
+// A limb tiles per TMA box / ring slot (one 3D box of AP consecutive limb
+// planes); the B stage is one 3D box of all 8 limbs
+#ifndef MPX_TC_AP
+#define MPX_TC_AP 2
+#endif
 constexpr int tcp_fixed_bytes(int bk, int bn, bool staged, int ew) {
   return TCP_BST * 8 * bn * bk + (staged ? ew * TCP_STAGE_TILE : 0) + 1024 + 1024;
 }
 constexpr int tcp_ast_for(int bk, int bn, bool staged, int ew) {
-  return ((232448 - tcp_fixed_bytes(bk, bn, staged, ew)) / (TC_BM * bk)) < (MPX_TC_ARING_KB * 1024 / (TC_BM * bk))
-             ? (232448 - tcp_fixed_bytes(bk, bn, staged, ew)) / (TC_BM * bk)
-             : MPX_TC_ARING_KB * 1024 / (TC_BM * bk);
+  // limb tiles, rounded down to whole AP-tile ring slots
+  return (((232448 - tcp_fixed_bytes(bk, bn, staged, ew)) / (TC_BM * bk)) < (MPX_TC_ARING_KB * 1024 / (TC_BM * bk))
+              ? (232448 - tcp_fixed_bytes(bk, bn, staged, ew)) / (TC_BM * bk)
+              : MPX_TC_ARING_KB * 1024 / (TC_BM * bk)) /
+         MPX_TC_AP * MPX_TC_AP;
 }
 constexpr int tcp_smem_bytes(int bk, int bn, bool staged, int ew) {
   return tcp_ast_for(bk, bn, staged, ew) * TC_BM * bk + tcp_fixed_bytes(bk, bn, staged, ew);
@@ -452,8 +469,9 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
     k_gemm_limbs_tc_pers(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                          const __grid_constant__ CUtensorMap mapA2, const __grid_constant__ CUtensorMap mapB2,
                          TcArgs args, int batch) {
-  constexpr int AST = tcp_ast_for(BK, BN, STAGED, EW), BST = TCP_BST;
-  constexpr int A_TILE = TC_BM * BK;
+  constexpr int AST = tcp_ast_for(BK, BN, STAGED, EW) / MPX_TC_AP, BST = TCP_BST;  // AST: ring slots
+  constexpr int AP = MPX_TC_AP;
+  constexpr int A_TILE = TC_BM * BK;      // one limb tile; a ring slot holds AP of them
   constexpr int B_TILE = BN * BK;
   constexpr int B_STAGE = 8 * B_TILE;
   constexpr int NC = BN / 32;             // 32-column epilogue chunks
@@ -461,7 +479,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
-  uint8_t* sB = smem + AST * A_TILE;
+  uint8_t* sB = smem + AST * AP * A_TILE;
   u64* stage_all = reinterpret_cast<u64*>(sB + BST * B_STAGE);
   uint64_t* bars =
       reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stage_all) + (STAGED ? EW * TCP_STAGE_TILE : 0));
@@ -530,14 +548,13 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
           const int zA = lo ? zs : t.z, zB = hi ? zs : t.z;
           mbar_wait(&emptyB[bs], bph ^ 1);
           mbar_expect_tx(&fullB[bs], B_STAGE);
-          for (int j = 0; j < 8; ++j)
-            tma_load_2d(sB + bs * B_STAGE + j * B_TILE, mB, &fullB[bs], kx % args.tw,
-                        ((zB * 8 + j) * args.nkt + kx / args.tw) * args.Npad + t.n0);
-          for (int i = 0; i < 8; ++i) {
+          // all 8 B limb planes of the k-block in one 3D box
+          tma_load_3d(sB + bs * B_STAGE, mB, &fullB[bs], kx % args.tw, (kx / args.tw) * args.Npad + t.n0, zB * 8);
+          for (int i = 0; i < 8; i += AP) {
             mbar_wait(&emptyA[as], aph ^ 1);
-            mbar_expect_tx(&fullA[as], A_TILE);
-            tma_load_2d(sA + as * A_TILE, mA, &fullA[as], kx % args.tw,
-                        ((zA * 8 + i) * args.nkt + kx / args.tw) * args.Mpad + t.m0);
+            mbar_expect_tx(&fullA[as], AP * A_TILE);
+            tma_load_3d(sA + as * AP * A_TILE, mA, &fullA[as], kx % args.tw, (kx / args.tw) * args.Mpad + t.m0,
+                        zA * 8 + i);
             if (++as == AST) {
               as = 0;
               aph ^= 1;
@@ -568,9 +585,11 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
           const uint32_t first = kb == 0 ? 0u : 1u;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            mbar_wait(&fullA[as], aph);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint64_t ad = a_desc0 + (uint64_t)((as * A_TILE) >> 4);
+            if (i % AP == 0) {
+              mbar_wait(&fullA[as], aph);  // limbs i .. i + AP - 1 landed
+              asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            }
+            const uint64_t ad = a_desc0 + (uint64_t)(((as * AP + i % AP) * A_TILE) >> 4);
             // A_i meets B_0..B_{7-i}: the B limb tiles sit back to back in the
             // stage (rows of one K-major operand), and their diagonals i..7
             // are adjacent TMEM column blocks, so ONE MMA of N = nj * BN
@@ -586,10 +605,12 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
               for (int kk = 0; kk < BK / 32; ++kk)
                 if (!(args.dbg & 4)) mma_i8(d_tmem, ad + 2 * kk, bd + 2 * kk, id, (i > 0 || kk > 0) ? 1u : first);
             }
-            umma_commit(&emptyA[as]);
-            if (++as == AST) {
-              as = 0;
-              aph ^= 1;
+            if (i % AP == AP - 1) {
+              umma_commit(&emptyA[as]);  // slot free once these MMAs retire
+              if (++as == AST) {
+                as = 0;
+                aph ^= 1;
+              }
             }
           }
           umma_commit(&emptyB[bs]);
@@ -1293,6 +1314,29 @@ static PFN_encodeTiled get_encode() {
 
 // `planes` K-block-tiled [Rpad][kbytes] limb planes (limb_off) as one 2D
 // tensor of (planes * kbytes / tw * Rpad) rows of tw bytes.
+// 3D map over K-block-tiled limb planes: (k within the tile, tile * Rpad +
+// row, plane), box (bk, box_rows, box_planes) - consecutive limb planes of
+// one k-block and row block in one TMA.
+static int make_map3(CUtensorMap* map, const uint8_t* base, i64 planes, i64 Rpad, i64 kbytes, int box_rows, int bk,
+                     int box_planes) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return MPX_ERR_CUDA;
+  const int tw = limb_tw(kbytes);
+  if (kbytes % tw != 0 || tw % bk != 0) return MPX_ERR_ARG;
+  const i64 rows = (kbytes / tw) * Rpad;
+  if (rows >= (1ll << 31) || planes >= (1ll << 31)) return MPX_ERR_ARG;
+  cuuint64_t dims[3] = {(cuuint64_t)tw, (cuuint64_t)rows, (cuuint64_t)planes};
+  cuuint64_t strides[2] = {(cuuint64_t)tw, (cuuint64_t)(rows * tw)};
+  cuuint32_t box[3] = {(cuuint32_t)bk, (cuuint32_t)box_rows, (cuuint32_t)box_planes};
+  cuuint32_t estr[3] = {1, 1, 1};
+  const CUtensorMapSwizzle sw = bk == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                          : (bk == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? MPX_OK : MPX_ERR_CUDA;
+}
+
 static int make_map(CUtensorMap* map, const uint8_t* base, i64 planes, i64 Rpad, i64 kbytes, int box_rows,
                     int bk = TC_BK) {
   PFN_encodeTiled enc = get_encode();
@@ -1464,13 +1508,13 @@ static int gemm_limbs_impl(uint64_t* C, const uint8_t* A8, const uint8_t* B8, co
             return MPX_ERR_CUDA;
       }
     }
-    if (make_map(&mapA, A8, batch * 8, Mpad, kcols, TC_BM, bk) != MPX_OK ||
-        make_map(&mapB, B8, batch * 8, Npad, kcols, bn, bk) != MPX_OK)
+    if (make_map3(&mapA, A8, batch * 8, Mpad, kcols, TC_BM, bk, MPX_TC_AP) != MPX_OK ||
+        make_map3(&mapB, B8, batch * 8, Npad, kcols, bn, bk, 8) != MPX_OK)
       return MPX_ERR_CUDA;
     if (split_ops) {
       const i64 jobs = batch / zl;
-      if (make_map(&mapA2, A8s, jobs * 8, Mpad, kcols, TC_BM, bk) != MPX_OK ||
-          make_map(&mapB2, B8s, jobs * 8, Npad, kcols, bn, bk) != MPX_OK)
+      if (make_map3(&mapA2, A8s, jobs * 8, Mpad, kcols, TC_BM, bk, MPX_TC_AP) != MPX_OK ||
+          make_map3(&mapB2, B8s, jobs * 8, Npad, kcols, bn, bk, 8) != MPX_OK)
         return MPX_ERR_CUDA;
     } else {
       mapA2 = mapA;
