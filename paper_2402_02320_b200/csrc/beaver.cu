@@ -16,7 +16,7 @@ __global__ void k_mul_finish(u64* __restrict__ z, const u64* __restrict__ d, con
                              const u64* __restrict__ c, i64 t_ps, int L, i64 n, u64 msk, int p0) {
   const i64 total = (i64)L * n;
   GRID_STRIDE(t, total) {
-    const i64 l = t / n;
+    const i64 l = L == 1 ? 0 : t / n;  // party mode (L = 1): no 64-bit division
     const i64 i = t - l * n;
     const i64 m = l * t_ps + i;
     const u64 dv = d[i], ev = e[i];
@@ -63,6 +63,45 @@ __global__ void k_mul_fused(u64* __restrict__ z, const u64* __restrict__ x, cons
   }
 }
 
+// Two elements per thread with 16-byte accesses (every party's array 16-byte
+// aligned, n and t_ps even).
+template <int LMAX>
+__global__ void k_mul_fused2(u64* __restrict__ z, const u64* __restrict__ x, const u64* __restrict__ y,
+                             const u64* __restrict__ a, const u64* __restrict__ b,
+                             const u64* __restrict__ c, i64 t_ps, int L, i64 n, u64 msk, int p0) {
+  typedef ulonglong2 V;
+  GRID_STRIDE(i2, n / 2) {
+    const i64 i = 2 * i2;
+    V av[LMAX], bv[LMAX];
+    u64 d0 = 0, d1 = 0, e0 = 0, e1 = 0;
+#pragma unroll
+    for (int l = 0; l < LMAX; ++l) {
+      if (l < L) {
+        av[l] = __ldg(reinterpret_cast<const V*>(a + l * t_ps + i));
+        bv[l] = __ldg(reinterpret_cast<const V*>(b + l * t_ps + i));
+        const V xv = __ldg(reinterpret_cast<const V*>(x + l * n + i));
+        const V yv = __ldg(reinterpret_cast<const V*>(y + l * n + i));
+        d0 += xv.x - av[l].x;
+        d1 += xv.y - av[l].y;
+        e0 += yv.x - bv[l].x;
+        e1 += yv.y - bv[l].y;
+      }
+    }
+#pragma unroll
+    for (int l = 0; l < LMAX; ++l) {
+      if (l < L) {
+        const V cv = __ldg(reinterpret_cast<const V*>(c + l * t_ps + i));
+        u64 v0 = cv.x + d0 * bv[l].x + e0 * av[l].x, v1 = cv.y + d1 * bv[l].y + e1 * av[l].y;
+        if (l == p0) {
+          v0 += d0 * e0;
+          v1 += d1 * e1;
+        }
+        *reinterpret_cast<V*>(z + l * n + i) = make_ulonglong2(v0 & msk, v1 & msk);
+      }
+    }
+  }
+}
+
 extern "C" int mpx_mul_fused(uint64_t* z, const uint64_t* x, const uint64_t* y, const uint64_t* a,
                              const uint64_t* b, const uint64_t* c, int64_t t_ps, int L, int64_t n,
                              int width, int p0, void* stream) {
@@ -70,6 +109,15 @@ extern "C" int mpx_mul_fused(uint64_t* z, const uint64_t* x, const uint64_t* y, 
   if (n == 0) return MPX_OK;
   const u64 msk = ring_mask(width);
   cudaStream_t s = (cudaStream_t)stream;
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (L <= 4 && n >= 1024 && n % 2 == 0 && t_ps % 2 == 0 && al16(z) && al16(x) && al16(y) && al16(a) && al16(b) &&
+      al16(c)) {
+    if (L <= 2)
+      k_mul_fused2<2><<<grid_for(n / 2), MPX_THREADS, 0, s>>>(z, x, y, a, b, c, t_ps, L, n, msk, p0);
+    else
+      k_mul_fused2<4><<<grid_for(n / 2), MPX_THREADS, 0, s>>>(z, x, y, a, b, c, t_ps, L, n, msk, p0);
+    return launch_status();
+  }
   if (L <= 2)
     k_mul_fused<2><<<grid_for(n), MPX_THREADS, 0, s>>>(z, x, y, a, b, c, t_ps, L, n, msk, p0);
   else if (L <= 4)
@@ -109,7 +157,7 @@ __global__ void k_trunc_finish(u64* __restrict__ z, const u64* __restrict__ c, c
                                i64 hi_ps, int L, i64 n, u64 msk, int f, u64 unbias, int p0) {
   const i64 total = (i64)L * n;
   GRID_STRIDE(t, total) {
-    const i64 l = t / n;
+    const i64 l = L == 1 ? 0 : t / n;  // party mode (L = 1): no 64-bit division
     const i64 i = t - l * n;
     u64 v = r_hi ? (0ull - r_hi[l * hi_ps + i]) : 0ull;
     if (l == p0) v += ((c[i] & msk) >> f) - unbias;
@@ -501,7 +549,7 @@ __global__ void k_and_finish(u64* __restrict__ z, const u64* __restrict__ d, con
                              int p0) {
   const i64 total = (i64)L * rows;
   GRID_STRIDE(t, total) {
-    const i64 l = t / rows;
+    const i64 l = L == 1 ? 0 : t / rows;
     const i64 r = t - l * rows;
     const i64 bit = t_bit + r * (i64)m;
     const u64 av = load_bits(ta + l * t_ps, bit, m);
@@ -609,7 +657,7 @@ __global__ void k_carry_finish(u64* __restrict__ G, u64* __restrict__ P, const u
   const int RW = last ? W : 2 * W;
   const i64 total = (i64)L * rows;
   GRID_STRIDE(t, total) {
-    const i64 l = t / rows;
+    const i64 l = L == 1 ? 0 : t / rows;
     const i64 r = t - l * rows;
     CarryMat M;
     carry_load(M, ta + l * t_ps, tb + l * t_ps, tc + l * t_ps, t_bit + r * (i64)RW, W, s, last, true);
@@ -709,7 +757,7 @@ __global__ void k_pubadd_init(u64* __restrict__ G, u64* __restrict__ P, u64* __r
   const i64 total = (i64)L * rows;
   const u64 mm = low_bits(m);
   GRID_STRIDE(t, total) {
-    const i64 l = t / rows;
+    const i64 l = L == 1 ? 0 : t / rows;
     const i64 r = t - l * rows;
     const u64 xv = x ? (x[t] & mm) : load_bits(xb + l * xb_ps, xb_bit + r * (i64)m, m);
     const u64 pv = pub[r] & mm;
@@ -784,7 +832,7 @@ __global__ void k_lmo_finish(u64* __restrict__ Y, const u64* __restrict__ d, con
   const int W = m - s;
   const i64 total = (i64)L * rows;
   GRID_STRIDE(t, total) {
-    const i64 l = t / rows;
+    const i64 l = L == 1 ? 0 : t / rows;
     const i64 r = t - l * rows;
     const i64 bit = t_bit + r * (i64)W;
     Y[t] = lmo_apply(Y[t], load_bits(ta + l * t_ps, bit, W), load_bits(tb + l * t_ps, bit, W),
@@ -887,7 +935,7 @@ __global__ void k_bit2a_expand(u64* __restrict__ out, const u64* __restrict__ c,
   const i64 per = rows * m;
   const i64 total = (i64)L * per;
   GRID_STRIDE(t, total) {
-    const i64 l = t / per;
+    const i64 l = L == 1 ? 0 : t / per;
     const i64 k = t - l * per;
     const i64 r = k / m;
     const int j = (int)(k - r * m);
@@ -915,7 +963,7 @@ __global__ void __launch_bounds__(256) k_bit2a_compose(u64* __restrict__ out, co
   const int sub = threadIdx.x & 3;
   const int lr = threadIdx.x >> 2;  // local row 0..63
   for (i64 t = blockIdx.x; t < total; t += gridDim.x) {
-    const i64 l = t / tiles;
+    const i64 l = L == 1 ? 0 : t / tiles;
     const i64 r0 = (t - l * tiles) * B2A_ROWS;
     const int nr = (int)min((i64)B2A_ROWS, rows - r0);
     const u64* src = ra + l * ra_ps + r0 * (i64)m;

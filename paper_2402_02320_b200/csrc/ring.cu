@@ -11,17 +11,18 @@
 __global__ void k_ring_lin(u64* __restrict__ out, const u64* __restrict__ a, u64 ka,
                            const u64* __restrict__ b, u64 kb, u64 c0, const u64* __restrict__ cv,
                            i64 cv_len, int L, i64 n, u64 msk, int p0) {
-  const i64 total = (i64)L * n;
-  GRID_STRIDE(t, total) {
-    const i64 l = t / n;
-    const i64 i = t - l * n;
-    u64 v = a ? a[t] * ka : 0ull;
-    if (b) v += b[t] * kb;
-    if (l == p0) {
-      v += c0;
-      if (cv) v += cv[cv_len == n ? i : i % cv_len];
+  // element-major with the party loop inside: no 64-bit division per word
+  GRID_STRIDE(i, n) {
+    for (int l = 0; l < L; ++l) {
+      const i64 t = (i64)l * n + i;
+      u64 v = a ? a[t] * ka : 0ull;
+      if (b) v += b[t] * kb;
+      if (l == p0) {
+        v += c0;
+        if (cv) v += cv[cv_len == n ? i : i % cv_len];
+      }
+      out[t] = v & msk;
     }
-    out[t] = v & msk;
   }
 }
 
@@ -31,7 +32,7 @@ extern "C" int mpx_ring_lin(uint64_t* out, const uint64_t* a, uint64_t ka, const
   CHECK_ARG(out && L >= 1 && n >= 0 && width >= 1 && width <= 64);
   CHECK_ARG(!cv || cv_len >= 1);
   if (n == 0) return MPX_OK;
-  k_ring_lin<<<grid_for((i64)L * n), MPX_THREADS, 0, (cudaStream_t)stream>>>(
+  k_ring_lin<<<grid_for(n), MPX_THREADS, 0, (cudaStream_t)stream>>>(
       out, a, ka, b, kb, c0, cv, cv_len, L, n, ring_mask(width), p0);
   return launch_status();
 }
@@ -434,7 +435,7 @@ __global__ void k_bits_op(u64* __restrict__ out, const u64* __restrict__ a, cons
   const i64 total = (i64)L * rows;
   const u64 mm = low_bits(m);
   GRID_STRIDE(t, total) {
-    const i64 l = t / rows;
+    const i64 l = L == 1 ? 0 : t / rows;
     const i64 r = t - l * rows;
     const u64 x = a[t];
     u64 v;
