@@ -506,6 +506,51 @@ __global__ void k_trunc_expand_rows(u64* __restrict__ z, const u64* __restrict__
   }
 }
 
+// Tiled variant: a CTA owns one (image b, source row hs): it truncates the
+// row's C x Ws dy elements (all parties) into a shared tile, then writes the
+// k output rows h = hs*k + a, all W = Ws*k columns and C channels in the
+// output's own order (c fastest: coalesced stores, where the element-per-
+// thread kernel above scatters 8-byte words C words apart).
+template <int LMAX>
+__global__ void __launch_bounds__(256) k_trunc_expand_rows_tiled(u64* __restrict__ z, const u64* __restrict__ x,
+                                                                 const u64* __restrict__ r_lo, i64 lo_ps,
+                                                                 const u64* __restrict__ r_hi, i64 hi_ps, int L,
+                                                                 i64 B, int C, int Hs, int Ws, int k, u64 msk, int f,
+                                                                 u64 bias, u64 unbias, int p0) {
+  extern __shared__ u64 te_tile[];  // [LMAX][C][Ws]
+  const i64 n = B * C * Hs * Ws;
+  const int H = Hs * k, W = Ws * k;
+  const i64 total = n * k * k;
+  const int per = C * Ws;
+  for (i64 bh = blockIdx.x; bh < B * Hs; bh += gridDim.x) {
+    const i64 b = bh / Hs;
+    const int hs = (int)(bh - b * Hs);
+    for (int q = threadIdx.x; q < per; q += blockDim.x) {
+      const int c = q / Ws, ws = q - c * Ws;
+      const i64 i = ((b * C + c) * Hs + hs) * Ws + ws;
+      u64 xv[LMAX], o[LMAX];
+#pragma unroll
+      for (int l = 0; l < LMAX; ++l) xv[l] = l < L ? __ldg(x + l * n + i) : 0ull;
+      trunc_elem<LMAX>(o, xv, r_lo, lo_ps, r_hi, hi_ps, L, i, msk, f, bias, unbias, p0);
+#pragma unroll
+      for (int l = 0; l < LMAX; ++l)
+        if (l < L) te_tile[(l * C + c) * Ws + ws] = o[l];
+    }
+    __syncthreads();
+    const int outw = k * W * C;  // k output rows x W columns x C channels
+    const i64 o0 = ((b * H + (i64)hs * k) * W) * C;
+    for (int q = threadIdx.x; q < outw; q += blockDim.x) {
+      const int c = q % C, rw = q / C;   // rw = a * W + w
+      const int w = rw % W;
+      const u64* tl = te_tile + c * Ws + w / k;
+#pragma unroll
+      for (int l = 0; l < LMAX; ++l)
+        if (l < L) z[(i64)l * total + o0 + q] = tl[l * C * Ws];
+    }
+    __syncthreads();
+  }
+}
+
 extern "C" int mpx_trunc_expand_rows(uint64_t* z, const uint64_t* x, const uint64_t* r_lo, int64_t lo_ps,
                                      const uint64_t* r_hi, int64_t hi_ps, int L, int64_t B, int64_t C, int64_t Hs,
                                      int64_t Ws, int64_t k, int width, int f, uint64_t bias, uint64_t unbias, int p0,
@@ -515,6 +560,13 @@ extern "C" int mpx_trunc_expand_rows(uint64_t* z, const uint64_t* x, const uint6
             f < width);
   const i64 n = B * C * Hs * Ws;
   if (n == 0) return MPX_OK;
+  const size_t tsm = (size_t)4 * C * Ws * 8;
+  if (L <= 4 && tsm <= 48 * 1024 && B * Hs < (1ll << 31)) {
+    const unsigned g = (unsigned)min(B * Hs, (i64)dev_sms() * 8);
+    k_trunc_expand_rows_tiled<4><<<g, 256, tsm, (cudaStream_t)stream>>>(
+        z, x, r_lo, lo_ps, r_hi, hi_ps, L, B, (int)C, (int)Hs, (int)Ws, (int)k, ring_mask(width), f, bias, unbias, p0);
+    return launch_status();
+  }
   if (L <= 4)
     k_trunc_expand_rows<4><<<grid_for(n), MPX_THREADS, 0, (cudaStream_t)stream>>>(
         z, x, r_lo, lo_ps, r_hi, hi_ps, L, B, (int)C, (int)Hs, (int)Ws, (int)k, ring_mask(width), f, bias, unbias, p0);
