@@ -415,6 +415,19 @@ int mpx_beaver_tc_thin(uint64_t* Z, int64_t sZ, const uint64_t* C, int64_t sC, c
                        const uint64_t* Y, int64_t y_ps, int64_t y_sr, int64_t y_sc, const uint64_t* B,
                        int64_t sB, int L, int64_t M, int64_t K, int64_t N, int p0, int width, void* stream);
 
+/* Long-K small sim-mode Beaver product on tcgen05 (basic.py:66-75): same
+ * operands and result as mpx_beaver_tc_thin, for M <= 32, N <= 32, any K,
+ * L = 2..3 local parties, width 64 (LeNet conv1 weight gradient, K = 73728).
+ * Split-K over the SMs: every CTA writes its partial product into the scratch
+ * W (at least max(SMs, ceil(K / 16384)) * L * M * N words) and a second
+ * launch sums the partials onto C. Shared-memory budget:
+ * 1024 + 81920 + 16 L (2M + 2N) * 34 + 64 <= 232448. */
+int mpx_beaver_tc_long(uint64_t* Z, int64_t sZ, const uint64_t* C, int64_t sC, const uint64_t* X,
+                       int64_t x_ps, int64_t x_sr, int64_t x_sc, const uint64_t* A, int64_t sA,
+                       const uint64_t* Y, int64_t y_ps, int64_t y_sr, int64_t y_sc, const uint64_t* B,
+                       int64_t sB, int L, int64_t M, int64_t K, int64_t N, int p0, int width, uint64_t* W,
+                       int64_t w_words, void* stream);
+
 /* Philox4x64-10 ALU ceiling probe: `blocks` counter blocks generated and
  * XOR-folded into out[grid*256] (out_words >= 148*8*256), no other memory
  * traffic: the dealer's roofline denominator, measured in-run. */

@@ -93,6 +93,8 @@ _SIGS = {
     "mpx_deal_share_bits_dk": [_P, _L, _P, _P, _L, _L, _I, _I, _I, _P],
     "mpx_beaver_tc_thin": [_P, _L, _P, _L, _P, _L, _L, _L, _P, _L, _P, _L, _L, _L, _P, _L, _I, _L, _L, _L, _I, _I,
                            _P],
+    "mpx_beaver_tc_long": [_P, _L, _P, _L, _P, _L, _L, _L, _P, _L, _P, _L, _L, _L, _P, _L, _I, _L, _L, _L, _I, _I,
+                           _P, _L, _P],
     "mpx_philox_probe": [_P, _L, _L, _P],
     "mpx_deal_triple": [_P, _P, _P, _L, _U, _U, _P, _L, _I, _I, _I, _I, _P],
     "mpx_deal_gen_arith": [_P, _L, _P, _U, _U, _P, _L, _L, _L, _I, _I, _I, _I, _I, _P],

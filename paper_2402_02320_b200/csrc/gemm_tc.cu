@@ -17,6 +17,7 @@
 // w2..w5 epilogue (TMEM -> registers -> limb recombination -> global).
 // Operand tiles are TMA-loaded with 128-byte swizzle; UMMA smem descriptors
 // are K-major SWIZZLE_128B.
+#include <cstdio>
 #include <cuda.h>
 #include <stdlib.h>
 
@@ -1956,4 +1957,503 @@ extern "C" int mpx_beaver_tc_thin(uint64_t* Z, int64_t sZ, const uint64_t* C, in
   a.dbg = getenv("MPX_THIN_DBG") ? atoi(getenv("MPX_THIN_DBG")) : 0;
   cudaStream_t s = (cudaStream_t)stream;
   return L == 2 ? thin_launch<2>(a, s) : thin_launch<3>(a, s);
+}
+
+// --------------------------------------------------------------------------
+// Long-K small sim-mode Beaver products on tcgen05 (weight gradients of thin
+// layers: LeNet conv1 dW = cols^T @ dZ, 25 x 73728 x 20 at three parties):
+//     Z_l = C_l + D @ B_l + A_l @ E + [l == p0] D @ E        (basic.py:66-75)
+// for M, N <= 32 and any K. The K range is split over one CTA per SM. Each
+// CTA streams its k-blocks (32 k) of every party's X_l, A_l (M side) and
+// Y_l, B_l (N side) into shared memory -- TMA bulk copies (one per party for
+// a contiguous run, one per 256-byte row otherwise), two raw buffers so block
+// t + 2 lands while block t is converted -- forms D and E, and writes the u8
+// limb tiles of two 128-row MMA families that stack the parties along M:
+//   F1: [A_0; A_1; A_2; D]          x E      -> A_l @ E and D @ E
+//   F2: [B_0^T; B_1^T; B_2^T; -]    x D^T    -> (D @ B_l)^T
+// (32 rows per group; limb i of the stack times B limbs 0 .. 7-i as one MMA of
+// N = 32 (8 - i), diagonal i + j accumulating in TMEM columns 32 (i + j):
+// F1 in columns 0-255, F2 in 256-511). The accumulators stay in TMEM over the
+// CTA's whole K range (at most 512 blocks per CTA keeps every diagonal exact
+// in the bits it contributes mod 2^64); the epilogue recombines the limbs,
+// transposes F2 through shared memory and writes the CTA's partial product;
+// a second kernel sums the partials onto C_l. Width 64 only. Unused stack rows
+// / columns carry garbage that only reaches ignored accumulator entries.
+#define LONG_KMAJ 0   // the block is one contiguous run: (row, k) at (kb0 + k) R + row -> [k][R]
+#define LONG_ROW16 1  // k is the unit stride, rows 16-byte aligned -> [row][LONG_RP]
+#define LONG_ROW8 2   // anything else (8-byte copies) -> [row][LONG_RP]
+#define LONG_ROWT 3   // k is the unit stride, one 3D tensor-map TMA box per 16-k half -> [half][party][row][16], 128B swizzle
+#define LONG_RP 34    // row pitch (words): 16-byte rows, conflict-free 16-byte reads down a column
+
+struct LongArgs {
+  u64* W;  // partial products [grid][L][M][N]
+  const u64* X;
+  i64 x_ps, x_sr, x_sc;
+  const u64* A;
+  i64 sA;
+  const u64* Y;
+  i64 y_ps, y_sr, y_sc;
+  const u64* B;
+  i64 sB;
+  int M, K, N, p0, L;
+  int nkb, per;  // k-blocks in total / per CTA
+  int mode[4];   // layout / fill per family X, A, Y, B
+  int off[4];    // word offset of each family in a raw buffer
+  int rw;        // words per raw buffer
+  int txb;       // bytes the bulk copies of one full block deliver
+  int tma;       // full blocks arrive by bulk / tensor copies (no ROW8 family)
+  int hb;        // LONG_ROWT: words per half box (1024-byte padded)
+  int dbg;       // timing experiments (MPX_LONG_DBG bits, wrong results): 1 no operand loads, 2 no conversion, 4 no MMA
+};
+
+#define LONG_TA 4096  // one 128-row limb tile (32 bytes of k per row)
+#define LONG_TB 1024  // one 32-row limb tile
+#define LONG_LIMB_BYTES (2 * 8 * LONG_TA + 2 * 8 * LONG_TB)
+
+static int long_hb_words(int L, int R) { return (L * R * 128 + 1023) / 1024 * 128; }
+static int long_fam_words(int mode, int L, int R) {
+  return mode == LONG_ROWT ? 2 * long_hb_words(L, R) : L * R * (mode == LONG_KMAJ ? 32 : LONG_RP);
+}
+static int long_smem_bytes(int rw) { return 1024 + LONG_LIMB_BYTES + 2 * rw * 8 + 64; }
+
+// word of element (party l, row, k) within a family's region
+__device__ __forceinline__ int long_idx(int mode, int R, int hb, int l, int row, int k) {
+  const int g = l * R + row;
+  if (mode == LONG_KMAJ) return l * R * 32 + k * R + row;
+  if (mode == LONG_ROWT) return (k >> 4) * hb + g * 16 + ((((k & 15) >> 1) ^ (g & 7)) << 1) + (k & 1);
+  return g * LONG_RP + k;
+}
+
+__device__ __forceinline__ void cp_async8z(uint32_t dst, const void* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(ok ? 8u : 0u) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// Bulk-copy fill of one family for a full k-block, by warp 0's lanes (the
+// expect_tx was posted before).
+template <int L>
+__device__ __forceinline__ void long_bulk(int mode, uint32_t dst, const u64* __restrict__ g, i64 ps, i64 sr, int R,
+                                          int kb0, uint64_t* bar, int lane) {
+  if (mode == LONG_KMAJ) {
+    if (lane < L) bulk_g2s(dst + 8u * (uint32_t)(lane * R * 32), g + lane * ps + (i64)kb0 * R, (uint32_t)(R * 256), bar);
+  } else {
+    for (int q = lane; q < L * R; q += 32) {
+      const int l = q / R, row = q - l * R;
+      bulk_g2s(dst + 8u * (uint32_t)(q * LONG_RP), g + l * ps + row * sr + kb0, 256u, bar);
+    }
+  }
+}
+
+// cp.async fill of one family (partial last block, or ROW8 families), all
+// threads; words past K are zero-filled. Element (row, k) of party l is at
+// g + l ps + row sr + k sk.
+template <int L>
+__device__ __forceinline__ void long_fill(int mode, uint32_t dst, const u64* __restrict__ g, i64 ps, i64 sr, i64 sk,
+                                          int R, int kb0, int K, int hb) {
+#pragma unroll
+  for (int l = 0; l < L; ++l)
+    for (int q = threadIdx.x; q < 32 * R; q += 256) {
+      int row, k;
+      if (mode == LONG_KMAJ) k = q / R, row = q - k * R;
+      else row = q >> 5, k = q & 31;
+      const int gk = kb0 + k;
+      const bool ok = gk < K;
+      cp_async8z(dst + 8u * (uint32_t)long_idx(mode, R, hb, l, row, k),
+                 ok ? g + l * ps + row * sr + (i64)gk * sk : g, ok);
+    }
+}
+
+template <int L>
+__global__ void __launch_bounds__(256, 1) k_beaver_tc_long(const __grid_constant__ LongArgs a,
+                                                         const __grid_constant__ CUtensorMap mapA) {
+  extern __shared__ __align__(1024) uint8_t long_raw_sm[];
+  // 1024-aligned, derived from the shared array (keeps ld / st.shared)
+  uint8_t* smem = long_raw_sm + ((1024u - (smem_u32(long_raw_sm) & 1023u)) & 1023u);
+  uint8_t* f1a = smem;                 // [8] 128-row limb tiles: A_0 | A_1 | A_2 | D
+  uint8_t* f2a = f1a + 8 * LONG_TA;    // [8] 128-row limb tiles: B_0^T | B_1^T | B_2^T | -
+  uint8_t* f1b = f2a + 8 * LONG_TA;    // [8] 32-row limb tiles: E^T (rows n)
+  uint8_t* f2b = f1b + 8 * LONG_TB;    // [8] 32-row limb tiles: D (rows m)
+  u64* raw0 = reinterpret_cast<u64*>(f2b + 8 * LONG_TB);
+  const int m = a.M, n = a.N, RW = a.rw;
+  uint64_t* sdone = reinterpret_cast<uint64_t*>(raw0 + 2 * RW);
+  uint64_t* full = sdone + 1;  // [2] bulk copies of raw buffer b landed
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(full + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // k-blocks blockIdx.x, + gridDim.x, ...: at any moment the CTAs stream
+  // neighbouring blocks (spread over the DRAM channels, no camping on one stride)
+  const int G = gridDim.x;
+  const int nb = blockIdx.x < a.nkb ? (a.nkb - 1 - blockIdx.x) / G + 1 : 0;
+  const int mx = a.mode[0], ma = a.mode[1], my = a.mode[2], mb = a.mode[3];
+#ifdef MPX_LONG_CHECK
+  if (threadIdx.x == 0) printf("cta %d start nb %d rw %d\n", blockIdx.x, nb, RW);
+  if (threadIdx.x == 0 && a.dbg == 99) return;
+#endif
+
+  if (threadIdx.x == 0) {
+    mbar_init(sdone, 1);
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  __syncthreads();
+  auto is_bulk = [&](int t) { return a.tma && ((int)blockIdx.x + t * G + 1) * 32 <= a.K; };
+  auto issue = [&](int t) {
+    if (a.dbg & 1) return;
+    const uint32_t base = smem_u32(raw0 + (t & 1) * RW);
+    const int kb0 = ((int)blockIdx.x + t * G) * 32;
+    if (is_bulk(t)) {
+      if (warp == 0) {
+        uint64_t* bar = &full[t & 1];
+        if (lane == 0) mbar_expect_tx(bar, (uint32_t)a.txb);
+        __syncwarp();
+        long_bulk<L>(mx, base + 8u * a.off[0], a.X, a.x_ps, a.x_sr, m, kb0, bar, lane);
+        if (ma == LONG_ROWT) {
+          if (lane == 0) {
+            u64* fa = raw0 + (t & 1) * RW + a.off[1];
+            tma_load_3d(fa, &mapA, bar, kb0, 0, 0);
+            tma_load_3d(fa + a.hb, &mapA, bar, kb0 + 16, 0, 0);
+          }
+        } else {
+          long_bulk<L>(ma, base + 8u * a.off[1], a.A, a.sA, a.K, m, kb0, bar, lane);
+        }
+        long_bulk<L>(my, base + 8u * a.off[2], a.Y, a.y_ps, a.y_sc, n, kb0, bar, lane);
+        long_bulk<L>(mb, base + 8u * a.off[3], a.B, a.sB, 1, n, kb0, bar, lane);
+      }
+    } else {
+      long_fill<L>(mx, base + 8u * a.off[0], a.X, a.x_ps, a.x_sr, a.x_sc, m, kb0, a.K, a.hb);
+      long_fill<L>(ma, base + 8u * a.off[1], a.A, a.sA, a.K, 1, m, kb0, a.K, a.hb);
+      long_fill<L>(my, base + 8u * a.off[2], a.Y, a.y_ps, a.y_sc, a.y_sr, n, kb0, a.K, a.hb);
+      long_fill<L>(mb, base + 8u * a.off[3], a.B, a.sB, 1, a.N, n, kb0, a.K, a.hb);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+  };
+  if (nb > 0) issue(0);
+  if (nb > 1) issue(1);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_holder;
+#ifdef MPX_LONG_CHECK
+  if (threadIdx.x == 0)
+    printf("cta %d nb %d rw %d off %d %d %d %d modes %d %d %d %d txb %d tma %d tmem %u smem %u raw0 %u\n", blockIdx.x,
+           nb, RW, a.off[0], a.off[1], a.off[2], a.off[3], mx, ma, my, mb, a.txb, a.tma, tmem_base,
+           smem_u32(smem), smem_u32(raw0));
+#endif
+  const uint32_t idesc_base = (2u << 4) | ((uint32_t)(128 >> 4) << 24);
+  // conversion units: (row of an operand family, 16-k chunk); rows enumerate
+  // A_l (L m), D (m, in party 0's X slot), E^T (n, in party 0's Y slot), B_l^T (L n)
+  const int urows = L * m + m + n + L * n;
+  for (int t = 0; t < nb; ++t) {
+    if (is_bulk(t)) {
+      if (!(a.dbg & 1)) mbar_wait(&full[t & 1], (uint32_t)((t >> 1) & 1));
+    } else {
+      asm volatile("cp.async.wait_all;" ::: "memory");
+    }
+    __syncthreads();
+    u64* rb = raw0 + (t & 1) * RW;
+    u64* rX = rb + a.off[0];
+    const u64* rA = rb + a.off[1];
+    u64* rY = rb + a.off[2];
+    const u64* rB = rb + a.off[3];
+    // openings, element-wise: D = sum_l X_l - A_l over X_0, E = sum_l Y_l - B_l
+    // over Y_0 (in X's / Y's layout). Warp w: k = w, w + 8, w + 16, w + 24; lane = row.
+    if (!(a.dbg & 2)) {
+#pragma unroll
+      for (int f = 0; f < 2; ++f) {
+        const int R = f ? n : m, fx = f ? my : mx, fa = f ? mb : ma;
+        u64* xs = f ? rY : rX;
+        const u64* as = f ? rB : rA;
+        if (lane < R) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int k = warp + 8 * j;
+            u64 d = 0;
+#pragma unroll
+            for (int l = 0; l < L; ++l)
+              d += xs[long_idx(fx, R, a.hb, l, lane, k)] - as[long_idx(fa, R, a.hb, l, lane, k)];
+            xs[long_idx(fx, R, a.hb, 0, lane, k)] = d;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (t > 0) mbar_wait(sdone, (uint32_t)((t - 1) & 1));  // the previous block's MMAs read their tiles
+    for (int u = threadIdx.x; u < ((a.dbg & 2) ? 0 : 2 * urows); u += 256) {
+      const int c = u >= urows ? 1 : 0, row = u - c * urows;
+      const u64* src;
+      uint8_t* dst;
+      int ts, r, tr, md, R, l = 0;
+      if (row < L * m) {  // A_l row -> F1 group l
+        l = row / m;
+        r = row - l * m;
+        src = rA, dst = f1a, ts = LONG_TA, tr = 32 * l + r, md = ma, R = m;
+      } else if (row < L * m + m) {  // D row -> F1 group 3 (and F2's B operand below)
+        r = row - L * m;
+        src = rX, dst = f1a, ts = LONG_TA, tr = 96 + r, md = mx, R = m;
+      } else if (row < L * m + m + n) {  // E^T row -> F1's B operand
+        r = row - L * m - m;
+        src = rY, dst = f1b, ts = LONG_TB, tr = r, md = my, R = n;
+      } else {  // B_l^T row -> F2 group l
+        const int rr = row - L * m - m - n;
+        l = rr / n;
+        r = rr - l * n;
+        src = rB, dst = f2a, ts = LONG_TA, tr = 32 * l + r, md = mb, R = n;
+      }
+      u64 v[16];
+      if (md == LONG_KMAJ) {
+        const u64* sp = src + l * R * 32 + r;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = sp[(16 * c + q) * R];
+      } else if (md == LONG_ROWT) {
+        const int g = l * R + r;
+        const ulonglong2* sr = reinterpret_cast<const ulonglong2*>(src + c * a.hb + g * 16);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const ulonglong2 p = sr[q ^ (g & 7)];
+          v[2 * q] = p.x;
+          v[2 * q + 1] = p.y;
+        }
+      } else {
+        const ulonglong2* sr = reinterpret_cast<const ulonglong2*>(src + (l * R + r) * LONG_RP + 16 * c);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const ulonglong2 p = sr[q];
+          v[2 * q] = p.x;
+          v[2 * q + 1] = p.y;
+        }
+      }
+      thin_emit_chunk(dst, ts, tr, c, v);
+      if (row >= L * m && row < L * m + m) thin_emit_chunk(f2b, LONG_TB, r, c, v);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();  // tiles written; raw buffer t & 1 consumed
+    if (t + 2 < nb) issue(t + 2);
+    if (threadIdx.x == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int i = 0; i < ((a.dbg & 4) ? 0 : 8); ++i) {
+        const uint32_t id = idesc_base | ((uint32_t)((32 * (8 - i)) >> 3) << 17);
+        const uint32_t acc = (t > 0 || i > 0) ? 1u : 0u;
+        mma_i8(tmem_base + (uint32_t)(i * 32), umma_desc_sw<32>(smem_u32(f1a + i * LONG_TA)),
+               umma_desc_sw<32>(smem_u32(f1b)), id, acc);
+        mma_i8(tmem_base + (uint32_t)(256 + i * 32), umma_desc_sw<32>(smem_u32(f2a + i * LONG_TA)),
+               umma_desc_sw<32>(smem_u32(f2b)), id, acc);
+      }
+      umma_commit(sdone);
+    }
+  }
+#ifdef MPX_LONG_CHECK
+  if (threadIdx.x == 0) printf("cta %d loop done\n", blockIdx.x);
+#endif
+  if (nb > 0) {
+    mbar_wait(sdone, (uint32_t)((nb - 1) & 1));
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // F2 (rows n) and D @ E (rows 96..) through shared memory (the limb
+    // tiles: every MMA has completed)
+    u64* S2 = reinterpret_cast<u64*>(smem);   // [L][32 m][33]
+    u64* SDE = S2 + L * 32 * 33;              // [32 m][33]
+    auto drain = [&](uint32_t col0, u64 (&val)[32]) {
+#pragma unroll
+      for (int q = 0; q < 32; ++q) val[q] = 0;
+      const uint32_t ta = tmem_base + ((uint32_t)(warp * 32) << 16) + col0;
+#pragma unroll
+      for (int d0 = 0; d0 < 8; d0 += 2) {
+        uint32_t v0[32], v1[32];
+        TMEM_LD32(ta + (uint32_t)(d0 * 32), v0);
+        TMEM_LD32(ta + (uint32_t)(d0 * 32 + 32), v1);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < 32; ++q) val[q] += ((u64)v0[q] << (8 * d0)) + ((u64)v1[q] << (8 * d0 + 8));
+      }
+    };
+    if (warp < L) {  // lane = column n of (D B_l)^T
+      u64 val[32];
+      drain(256, val);
+      if (lane < n) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          if (q < m) S2[(warp * 32 + q) * 33 + lane] = val[q];
+      }
+    } else if (warp == 3 && a.p0 >= 0) {  // lane = row m of D @ E
+      u64 val[32];
+      drain(0, val);
+#pragma unroll
+      for (int q = 0; q < 32; ++q) SDE[lane * 33 + q] = val[q];
+    }
+    __syncthreads();
+    if (warp < L) {  // lane = row m of A_l @ E -> this CTA's partial of Z_l
+      u64 val[32];
+      drain(0, val);
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        u64 v = val[q] + S2[(warp * 32 + lane) * 33 + q];
+        if (warp == a.p0) v += SDE[lane * 33 + q];
+        S2[(warp * 32 + lane) * 33 + q] = v;
+      }
+      __syncwarp();
+      u64* wp = a.W + ((i64)blockIdx.x * L + warp) * m * n;  // row-major m x n, coalesced
+      for (int e = lane; e < m * n; e += 32) {
+        const int r = e / n, cc = e - r * n;
+        wp[e] = S2[(warp * 32 + r) * 33 + cc];
+      }
+    }
+  }
+#ifdef MPX_LONG_CHECK
+  if (threadIdx.x == 0) printf("cta %d epilogue done\n", blockIdx.x);
+#endif
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+  }
+}
+
+// Z_l = C_l + sum over the CTAs' partials: a CTA takes 32 output words, its
+// eight warps every eighth partial (all loads of a warp in flight together),
+// then a shared-memory sum across the warps
+__global__ void __launch_bounds__(256) k_long_reduce(u64* __restrict__ Z, i64 sZ, const u64* __restrict__ C, i64 sC,
+                                                     const u64* __restrict__ W, int L, int mn, int parts) {
+  __shared__ u64 red[8][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int o = blockIdx.x * 32 + lane, outs = L * mn;
+  u64 acc[4] = {0, 0, 0, 0};
+  if (o < outs) {
+    const u64* w = W + o;
+    const i64 step = (i64)outs;
+    int p = warp, j = 0;
+#pragma unroll 4
+    for (; p < parts; p += 8, ++j) acc[j & 3] += __ldg(w + p * step);
+  }
+  red[warp][lane] = acc[0] + acc[1] + acc[2] + acc[3];
+  __syncthreads();
+  if (warp == 0 && o < outs) {
+    const int l = o / mn, i = o - l * mn;
+    u64 v = C[l * sC + i];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v += red[q][lane];
+    Z[l * sZ + i] = v;
+  }
+}
+
+// shapes mpx_beaver_tc_long takes (protocols/basic.py _long_tc mirrors this:
+// the budget assumes the larger row layout for every family)
+static bool long_ok(int L, int64_t M, int64_t K, int64_t N, int width) {
+  return L >= 2 && L <= 3 && M >= 1 && M <= 32 && N >= 1 && N <= 32 && K >= 1 && K < (1ll << 31) && width == 64 &&
+         long_smem_bytes((L * (2 * (int)M + 2 * (int)N) * LONG_RP + 127) / 128 * 128) <= 232448;
+}
+
+static int long_grid(int64_t K, int* per_out) {
+  const int nkb = (int)((K + 31) / 32);
+  // one CTA per SM; at most 512 k-blocks (16384 k) per CTA keeps the diagonals exact
+  const int per = min((nkb + num_sms() - 1) / num_sms(), 512);
+  *per_out = per;
+  return (nkb + per - 1) / per;
+}
+
+// Z [L][M][N], C [L][M][N], A [L][M][K], B [L][K][N] (party strides sZ, sC,
+// sA, sB); X, Y logical M x K and K x N share views at (party, row, col)
+// strides; W scratch of at least max(SMs, ceil(K / 16384)) * L * M * N words.
+// M, N <= 32, 2 <= L <= 3 (all parties local), width 64.
+extern "C" int mpx_beaver_tc_long(uint64_t* Z, int64_t sZ, const uint64_t* C, int64_t sC, const uint64_t* X,
+                                  int64_t x_ps, int64_t x_sr, int64_t x_sc, const uint64_t* A, int64_t sA,
+                                  const uint64_t* Y, int64_t y_ps, int64_t y_sr, int64_t y_sc, const uint64_t* B,
+                                  int64_t sB, int L, int64_t M, int64_t K, int64_t N, int p0, int width,
+                                  uint64_t* W, int64_t w_words, void* stream) {
+  CHECK_ARG(Z && C && X && A && Y && B && W && p0 >= -1 && p0 < L);
+  CHECK_ARG(long_ok(L, M, K, N, width));
+  cudaStream_t s = (cudaStream_t)stream;
+  LongArgs a;
+  a.W = W;
+  a.X = X;
+  a.x_ps = x_ps;
+  a.x_sr = x_sr;
+  a.x_sc = x_sc;
+  a.A = A;
+  a.sA = sA;
+  a.Y = Y;
+  a.y_ps = y_ps;
+  a.y_sr = y_sr;
+  a.y_sc = y_sc;
+  a.B = B;
+  a.sB = sB;
+  a.M = (int)M;
+  a.K = (int)K;
+  a.N = (int)N;
+  a.p0 = p0;
+  a.L = L;
+  a.nkb = (int)((K + 31) / 32);
+  const int grid = long_grid(K, &a.per);
+  CHECK_ARG(w_words >= (int64_t)grid * L * M * N);
+  a.dbg = getenv("MPX_LONG_DBG") ? atoi(getenv("MPX_LONG_DBG")) : 0;
+  // per-family layout: contiguous runs and 16-byte alignment allow bulk copies
+  auto al16 = [](const void* p, i64 ps) { return ((uintptr_t)p & 15) == 0 && (ps & 1) == 0; };
+  auto fam_mode = [&](const void* g, i64 ps, i64 sr, i64 sk, i64 R) {
+    if (!al16(g, ps)) return LONG_ROW8;
+    if (sr == 1 && sk == R) return LONG_KMAJ;
+    if (sk == 1 && (sr & 1) == 0) return LONG_ROW16;
+    return LONG_ROW8;
+  };
+  a.mode[0] = fam_mode(X, x_ps, x_sr, x_sc, M);
+  a.mode[1] = fam_mode(A, sA, K, 1, M);
+  // A_l (row-major material) by one 3D tensor-map box per 16-k half: two TMA
+  // requests per block instead of one bulk copy per 256-byte row
+  CUtensorMap mapA;
+  memset(&mapA, 0, sizeof(mapA));
+  if (a.mode[1] == LONG_ROW16 && !getenv("MPX_LONG_NO_TMAP")) {
+    PFN_encodeTiled enc = get_encode();
+    cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)M, (cuuint64_t)L};
+    cuuint64_t strides[2] = {(cuuint64_t)K * 8, (cuuint64_t)sA * 8};
+    cuuint32_t box[3] = {16, (cuuint32_t)M, (cuuint32_t)L};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (enc && enc(&mapA, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, (void*)A, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+      a.mode[1] = LONG_ROWT;
+  }
+  a.mode[2] = fam_mode(Y, y_ps, y_sc, y_sr, N);
+  a.mode[3] = fam_mode(B, sB, 1, N, N);
+  if (const char* e = getenv("MPX_LONG_ROW8"))  // tests: force the generic fill
+    if (atoi(e)) a.mode[0] = a.mode[1] = a.mode[2] = a.mode[3] = LONG_ROW8;
+  a.tma = 1;
+  a.hb = long_hb_words(L, (int)M);
+  // the tensor-map family first (its half boxes need 1024-byte alignment)
+  int off = 0;
+  const int rows[4] = {(int)M, (int)M, (int)N, (int)N};
+  const int order[4] = {1, 0, 2, 3};
+  for (int f : order) {
+    a.off[f] = off;
+    off += long_fam_words(a.mode[f], L, rows[f]);
+    off = (off + 1) & ~1;
+    if (a.mode[f] == LONG_ROW8) a.tma = 0;
+  }
+  a.rw = (off + 127) & ~127;  // raw buffers 1024-byte aligned
+  a.txb = L * (int)(2 * M + 2 * N) * 256;  // 32 words per (party, row): row pads are not copied
+  const int smem = long_smem_bytes(a.rw);
+  CHECK_ARG(smem <= 232448);
+  static int attr[4] = {0, 0, 0, 0};
+  const void* fn = L == 2 ? (const void*)k_beaver_tc_long<2> : (const void*)k_beaver_tc_long<3>;
+  if (smem > attr[L]) {
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return MPX_ERR_CUDA;
+    attr[L] = smem;
+  }
+  if (L == 2) k_beaver_tc_long<2><<<grid, 256, smem, s>>>(a, mapA);
+  else k_beaver_tc_long<3><<<grid, 256, smem, s>>>(a, mapA);
+  if (cudaGetLastError() != cudaSuccess) return MPX_ERR_CUDA;
+  const int outs = L * (int)(M * N);
+  k_long_reduce<<<(outs + 31) / 32, 256, 0, s>>>(Z, sZ, C, sC, W, L, (int)(M * N), grid);
+  return launch_status();
 }

@@ -464,6 +464,33 @@ def beaver_tc_thin(Z, sZ, C_ptr, sC, x_ptr, x_ps, x_sr, x_sc, A_ptr, sA, y_ptr, 
     return Z
 
 
+def beaver_tc_long(Z, sZ, C_ptr, sC, x_ptr, x_ps, x_sr, x_sc, A_ptr, sA, y_ptr, y_ps, y_sr, y_sc, B_ptr, sB,
+                   L, M, K, N, p0, width, W=None):
+    """Sim sessions, M <= 32 and N <= 32, long K (weight gradients of thin
+    layers): split-K Beaver opening + reconstruction on tcgen05 (partials in
+    the scratch W, then one launch sums them onto C)."""
+    if _dry(Z):
+        return Z
+    need = long_tc_scratch(L, M, K, N, Z.device)
+    if W is None:
+        W = torch.empty(need, dtype=torch.int64, device=Z.device)
+    call("mpx_beaver_tc_long", ptr(Z), sZ, C_ptr, sC, x_ptr, x_ps, x_sr, x_sc, A_ptr, sA, y_ptr, y_ps, y_sr, y_sc,
+         B_ptr, sB, L, M, K, N, p0, width, ptr(W), W.numel())
+    return Z
+
+
+def long_tc_ok(L, M, K, N, width) -> bool:
+    """Shapes mpx_beaver_tc_long takes (gemm_tc.cu long_ok)."""
+    return (2 <= L <= 3 and 1 <= M <= 32 and 1 <= N <= 32 and 1 <= K < 2**31 and width == 64
+            and 1024 + 81920 + 2 * L * (2 * M + 2 * N) * 34 * 8 + 64 <= 232448)
+
+
+def long_tc_scratch(L, M, K, N, device) -> int:
+    """Words of partial-product scratch mpx_beaver_tc_long needs."""
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    return max(sms, -(-((K + 31) // 32) // 512)) * L * M * N
+
+
 def beaver_gemm(Z, sZ, C_ptr, sC, D, E, A_ptr, sA, B_ptr, sB, L, M, K, N, p0, width):
     """Z_l = C_l + D @ (B_l + [l==p0] E) + A_l @ E (one SIMT launch, all local parties)."""
     if _dry(Z):

@@ -320,6 +320,10 @@ def _beaver_matmul_fused_simt(session, Zg, pairs, trips, L, m, k, r, w):
         K.beaver_tc_thin(Zg, m * r, C0.data_ptr(), C0.stride(0), _ptr(X0), xps, xsr, xsc, A0.data_ptr(),
                          A0.stride(0), _ptr(Y0), yps, ysr, ysc, B0.data_ptr(), B0.stride(0), L, m, k, r, session.p0, w)
         return
+    if _long_tc(len(pairs), L, m, k, r, w) and A0.stride(1) == k and B0.stride(1) == r and C0.stride(1) == r:
+        K.beaver_tc_long(Zg, m * r, C0.data_ptr(), C0.stride(0), _ptr(X0), xps, xsr, xsc, A0.data_ptr(),
+                         A0.stride(0), _ptr(Y0), yps, ysr, ysc, B0.data_ptr(), B0.stride(0), L, m, k, r, session.p0, w)
+        return
     K.beaver_gemm_sim(Zg, m * r, L * m * r, C0.data_ptr(), C0.stride(0), _bstride(trips, range(len(trips)), 2),
                       _ptr(X0), xps, xsr, xsc, x_js, A0.data_ptr(), A0.stride(0),
                       _bstride(trips, range(len(trips)), 0), _ptr(Y0), yps, ysr, ysc, y_js, B0.data_ptr(),
@@ -333,6 +337,16 @@ THIN_TC = os.environ.get("MPX_THIN_TC", "1") != "0"
 
 def _thin_tc(batch, L, m, k, r) -> bool:
     return THIN_TC and batch == 1 and 2 <= L <= 3 and k <= 32 and r <= 32 and m >= 1024
+
+
+# long-K small products (M, N <= 32: LeNet conv1 weight gradient) on tcgen05,
+# split-K over the SMs; MPX_LONG_TC=0 keeps them on the SIMT kernel
+LONG_TC = os.environ.get("MPX_LONG_TC", "1") != "0"
+LONG_TC_MIN_K = 4096
+
+
+def _long_tc(batch, L, m, k, r, w) -> bool:
+    return LONG_TC and batch == 1 and k >= LONG_TC_MIN_K and K.long_tc_ok(L, m, k, r, w)
 
 
 def _strides3(v):
