@@ -41,7 +41,7 @@ lng = lambda: Kn.beaver_tc_long(Z, M * N, C.data_ptr(), M * N, XT.data_ptr(), K 
 byts = 8 * L * (2 * M * K + 2 * K * N)
 t = ev(lng, a.reps)
 print(f"long tc: {t:.1f} us, {byts / t / 1e3:.0f} GB/s of X, A, Y, B")
-for dbg in ((1, 2, 4, 3, 5, 6, 7) if "MPX_LONG_DBG" not in os.environ else ()):
+for dbg in ((1, 2, 4, 3, 5, 6, 7) if "MPX_LONG_DBG" not in os.environ and a.reps > 1 else ()):
     os.environ["MPX_LONG_DBG"] = str(dbg)
     print(f"  dbg {dbg}: {ev(lng, a.reps):.1f} us")
 os.environ.pop("MPX_LONG_DBG", None)
