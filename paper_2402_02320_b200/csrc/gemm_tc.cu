@@ -17,7 +17,6 @@
 // w2..w5 epilogue (TMEM -> registers -> limb recombination -> global).
 // Operand tiles are TMA-loaded with 128-byte swizzle; UMMA smem descriptors
 // are K-major SWIZZLE_128B.
-#include <cstdio>
 #include <cuda.h>
 #include <stdlib.h>
 
@@ -2089,10 +2088,6 @@ __global__ void __launch_bounds__(256, 1) k_beaver_tc_long(const __grid_constant
   const int G = gridDim.x;
   const int nb = blockIdx.x < a.nkb ? (a.nkb - 1 - blockIdx.x) / G + 1 : 0;
   const int mx = a.mode[0], ma = a.mode[1], my = a.mode[2], mb = a.mode[3];
-#ifdef MPX_LONG_CHECK
-  if (threadIdx.x == 0) printf("cta %d start nb %d rw %d\n", blockIdx.x, nb, RW);
-  if (threadIdx.x == 0 && a.dbg == 99) return;
-#endif
 
   if (threadIdx.x == 0) {
     mbar_init(sdone, 1);
@@ -2104,8 +2099,13 @@ __global__ void __launch_bounds__(256, 1) k_beaver_tc_long(const __grid_constant
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
                  "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  } else if (warp == 1 && lane == 0 && ma == LONG_ROWT) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
   }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_holder;
   auto is_bulk = [&](int t) { return a.tma && ((int)blockIdx.x + t * G + 1) * 32 <= a.K; };
   auto issue = [&](int t) {
     if (a.dbg & 1) return;
@@ -2137,18 +2137,10 @@ __global__ void __launch_bounds__(256, 1) k_beaver_tc_long(const __grid_constant
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
   };
+  // the first two blocks' copies; the other warps go straight to block 0's
+  // full barrier (cp.async blocks are waited for by every thread below)
   if (nb > 0) issue(0);
   if (nb > 1) issue(1);
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem_base = *tmem_holder;
-#ifdef MPX_LONG_CHECK
-  if (threadIdx.x == 0)
-    printf("cta %d nb %d rw %d off %d %d %d %d modes %d %d %d %d txb %d tma %d tmem %u smem %u raw0 %u\n", blockIdx.x,
-           nb, RW, a.off[0], a.off[1], a.off[2], a.off[3], mx, ma, my, mb, a.txb, a.tma, tmem_base,
-           smem_u32(smem), smem_u32(raw0));
-#endif
   const uint32_t idesc_base = (2u << 4) | ((uint32_t)(128 >> 4) << 24);
   // conversion units: (row of an operand family, 16-k chunk); rows enumerate
   // A_l (L m), D (m, in party 0's X slot), E^T (n, in party 0's Y slot), B_l^T (L n)
@@ -2253,9 +2245,6 @@ __global__ void __launch_bounds__(256, 1) k_beaver_tc_long(const __grid_constant
       umma_commit(sdone);
     }
   }
-#ifdef MPX_LONG_CHECK
-  if (threadIdx.x == 0) printf("cta %d loop done\n", blockIdx.x);
-#endif
   if (nb > 0) {
     mbar_wait(sdone, (uint32_t)((nb - 1) & 1));
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -2310,9 +2299,6 @@ __global__ void __launch_bounds__(256, 1) k_beaver_tc_long(const __grid_constant
       }
     }
   }
-#ifdef MPX_LONG_CHECK
-  if (threadIdx.x == 0) printf("cta %d epilogue done\n", blockIdx.x);
-#endif
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) {
