@@ -654,17 +654,24 @@ extern "C" int mpx_beaver_gemm_sim(uint64_t* Z, int64_t sZ, int64_t bZ, const ui
   CHECK_ARG(Z && C && X && A && Y && B && M >= 1 && K >= 1 && N >= 1 && width >= 1 && width <= 64);
   CHECK_ARG(L >= 2 && L <= 4 && p0 < L && batch >= 1);
   CHECK_ARG(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31) && M * K < (1ll << 40) && K * N < (1ll << 40));
+  // least padded output area; on a tie the larger tile, unless the product
+  // is too small to fill the SMs (small outputs: the split-K grid is
+  // tiles x at most K / 16 chunks), where more, smaller tiles spread the
+  // per-CTA reduction over more SMs (LeNet fc2: 128 x 500 x 10 on 32 vs 124 CTAs)
+  const bool small = (M * N * batch) / 1024 * max((i64)1, K / (2 * BS_BK)) < (i64)dev_sms() * 4;
   int best = 0;
   i64 best_cost = -1, best_area = 0;
   for (int c = 0; c < kNumSimCfgs; ++c) {
     const i64 bm = kSimCfgs[c].bm, bn = kSimCfgs[c].bn;
     const i64 cost = ((M + bm - 1) / bm) * bm * ((N + bn - 1) / bn) * bn;
-    if (best_cost < 0 || cost < best_cost || (cost == best_cost && bm * bn > best_area)) {
+    const bool tie_better = small ? bm * bn < best_area : bm * bn > best_area;
+    if (best_cost < 0 || cost < best_cost || (cost == best_cost && tie_better)) {
       best = c;
       best_cost = cost;
       best_area = bm * bn;
     }
   }
+  if (const char* e = getenv("MPX_BS_CFG")) best = min(max(atoi(e), 0), kNumSimCfgs - 1);  // sweeps
   const SimOperand xo{X, x_ps, x_sr, x_sc, x_js}, yo{Y, y_ps, y_sr, y_sc, y_js};
   cudaStream_t s = (cudaStream_t)stream;
   if (thin_fits(L, M, K, N, width) && batch <= 65535) {
