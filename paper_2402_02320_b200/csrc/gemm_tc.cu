@@ -1694,7 +1694,8 @@ __global__ void __launch_bounds__(256, 1) k_beaver_tc_thin(const __grid_constant
   uint64_t* tf = reinterpret_cast<uint64_t*>(stg + 4 * 32 * THIN_SP);  // [2] MMA done per TMEM buffer
   uint64_t* te = tf + 2;                                                // [2] buffer drained
   uint64_t* sempty = te + 2;                                            // limb tiles consumed by the MMAs
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sempty + 1);
+  uint64_t* tready = sempty + 1;                                        // the producers wrote a tile's limb tiles
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tready + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = a.K, N = a.N;
 
@@ -1704,6 +1705,7 @@ __global__ void __launch_bounds__(256, 1) k_beaver_tc_thin(const __grid_constant
       mbar_init(&te[b], 4);
     }
     mbar_init(sempty, 1);
+    mbar_init(tready, 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -1776,7 +1778,7 @@ __global__ void __launch_bounds__(256, 1) k_beaver_tc_thin(const __grid_constant
   if (warp < 4) {
     // ---------------- producers ----------------
     u64* sx = stg + warp * 32 * THIN_SP;
-    int it = 0, job = 0;
+    int it = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       if (t + (int)gridDim.x < tiles) prefetch_tile(t + gridDim.x);
       const i64 wr0 = (i64)t * 128 + warp * 32;
@@ -1830,42 +1832,43 @@ __global__ void __launch_bounds__(256, 1) k_beaver_tc_thin(const __grid_constant
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      asm volatile("bar.sync 2, 128;" ::: "memory");  // the four producer warps wrote tile t
-      if (warp == 0) {
-        if (lane == 0) {
-          // ---- MMA issue: per party two k-blocks of 36 limb products ----
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          for (int l = 0; l < L; ++l, ++job) {
-            const int buf = job & 1;
-            if (job >= 2) mbar_wait(&te[buf], (uint32_t)(((job - 2) >> 1) & 1));
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t dt = tmem_base + (uint32_t)(buf * 256);
-            // A_i x [B_0 .. B_{7-i}] as ONE MMA of N = 32 (8 - i): the B limb
-            // tiles are consecutive rows of one operand and diagonals i..7
-            // adjacent TMEM column blocks
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const uint32_t id = idesc_base | ((uint32_t)((32 * (8 - i)) >> 3) << 17);
-              if (!(a.dbg & 4)) {
-                mma_i8(dt + (uint32_t)(i * 32), umma_desc_sw<32>(smem_u32(sD + i * THIN_TA)),
-                       umma_desc_sw<32>(smem_u32(sBp + l * 8 * THIN_TB)), id, i > 0 ? 1u : 0u);
-                mma_i8(dt + (uint32_t)(i * 32), umma_desc_sw<32>(smem_u32(sA + (l * 8 + i) * THIN_TA)),
-                       umma_desc_sw<32>(smem_u32(sE)), id, 1u);
-              }
-            }
-            umma_commit(&tf[buf]);
-          }
-          umma_commit(sempty);  // this tile's limb tiles may be overwritten
-        }
-        __syncwarp();
-      }
+      mbar_arrive(tready);  // the MMAs are issued by the epilogue side (warp 4)
     }
   } else {
     // ---------------- epilogue: drain, recombine, Z_l = C_l + acc (a thread = a row) ----------------
     const int rq = warp - 4;
-    int job = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    int job = 0, it = 0;
+    // ---- MMA issue (warp 4, lane 0): per party two k-blocks of 36 limb products.
+    // A_i x [B_0 .. B_{7-i}] is ONE MMA of N = 32 (8 - i): the B limb tiles are
+    // consecutive rows of one operand and diagonals i..7 adjacent TMEM column
+    // blocks. Issuing from the epilogue side keeps the producers loading the
+    // next tile while a TMEM buffer waits to be drained.
+    auto issue = [&](int jb, int l) {
+      const int buf = jb & 1;
+      if (jb >= 2) mbar_wait(&te[buf], (uint32_t)(((jb - 2) >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t dt = tmem_base + (uint32_t)(buf * 256);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t id = idesc_base | ((uint32_t)((32 * (8 - i)) >> 3) << 17);
+        if (!(a.dbg & 4)) {
+          mma_i8(dt + (uint32_t)(i * 32), umma_desc_sw<32>(smem_u32(sD + i * THIN_TA)),
+                 umma_desc_sw<32>(smem_u32(sBp + l * 8 * THIN_TB)), id, i > 0 ? 1u : 0u);
+          mma_i8(dt + (uint32_t)(i * 32), umma_desc_sw<32>(smem_u32(sA + (l * 8 + i) * THIN_TA)),
+                 umma_desc_sw<32>(smem_u32(sE)), id, 1u);
+        }
+      }
+      umma_commit(&tf[buf]);
+      if (l == L - 1) umma_commit(sempty);  // this tile's limb tiles may be overwritten
+    };
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       const i64 row = (i64)t * 128 + rq * 32 + lane;
+      if (rq == 0 && lane == 0) {  // the tile's first party, once the producers wrote it
+        mbar_wait(tready, (uint32_t)(it & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        issue(job, 0);
+      }
+      __syncwarp();
       for (int l = 0; l < L; ++l, ++job) {
         const int buf = job & 1;
         const u64* __restrict__ Cl = a.C + l * a.sC + row * (i64)N;
@@ -1875,6 +1878,8 @@ __global__ void __launch_bounds__(256, 1) k_beaver_tc_thin(const __grid_constant
         for (int q = 0; q < 32; ++q) acc[q] = (q < N && row < a.M && !(a.dbg & 2)) ? __ldg(Cl + q) : 0ull;  // addend first
         mbar_wait(&tf[buf], (uint32_t)((job >> 1) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (rq == 0 && lane == 0 && l + 1 < L) issue(job + 1, l + 1);  // next party's MMAs under this drain
+        __syncwarp();
         // two diagonals' TMEM loads in flight per wait (four waits per party)
 #pragma unroll
         for (int d0 = 0; d0 < 8; d0 += 2) {
