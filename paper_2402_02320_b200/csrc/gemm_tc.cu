@@ -2000,7 +2000,7 @@ struct LongArgs {
   const u64* B;
   i64 sB;
   int M, K, N, p0, L;
-  int nkb, per;  // k-blocks in total / per CTA
+  int nkb;       // k-blocks in total (CTA b takes blocks b, b + grid, ...)
   int mode[4];   // layout / fill per family X, A, Y, B
   int off[4];    // word offset of each family in a raw buffer
   int rw;        // words per raw buffer
@@ -2346,11 +2346,10 @@ static bool long_ok(int L, int64_t M, int64_t K, int64_t N, int width) {
          long_smem_bytes((L * (2 * (int)M + 2 * (int)N) * LONG_RP + 127) / 128 * 128) <= 232448;
 }
 
-static int long_grid(int64_t K, int* per_out) {
+static int long_grid(int64_t K) {
   const int nkb = (int)((K + 31) / 32);
   // one CTA per SM; at most 512 k-blocks (16384 k) per CTA keeps the diagonals exact
   const int per = min((nkb + num_sms() - 1) / num_sms(), 512);
-  *per_out = per;
   return (nkb + per - 1) / per;
 }
 
@@ -2386,7 +2385,7 @@ extern "C" int mpx_beaver_tc_long(uint64_t* Z, int64_t sZ, const uint64_t* C, in
   a.p0 = p0;
   a.L = L;
   a.nkb = (int)((K + 31) / 32);
-  const int grid = long_grid(K, &a.per);
+  const int grid = long_grid(K);
   CHECK_ARG(w_words >= (int64_t)grid * L * M * N);
   a.dbg = getenv("MPX_LONG_DBG") ? atoi(getenv("MPX_LONG_DBG")) : 0;
   // per-family layout: contiguous runs and 16-byte alignment allow bulk copies
