@@ -1693,8 +1693,8 @@ __global__ void __launch_bounds__(256, 1) k_beaver_tc_thin(const __grid_constant
   u64* stg = reinterpret_cast<u64*>(sE + 8 * THIN_TB);                  // [4 warps][32][THIN_SP]
   uint64_t* tf = reinterpret_cast<uint64_t*>(stg + 4 * 32 * THIN_SP);  // [2] MMA done per TMEM buffer
   uint64_t* te = tf + 2;                                                // [2] buffer drained
-  uint64_t* sempty = te + 2;                                            // limb tiles consumed by the MMAs
-  uint64_t* tready = sempty + 1;                                        // the producers wrote a tile's limb tiles
+  uint64_t* sempty = te + 2;  // [3] party l's MMAs done: its A_l limb tiles (and, for the last, D's) are free
+  uint64_t* tready = sempty + 3;                                        // the producers wrote a tile's limb tiles
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tready + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = a.K, N = a.N;
@@ -1704,7 +1704,7 @@ __global__ void __launch_bounds__(256, 1) k_beaver_tc_thin(const __grid_constant
       mbar_init(&tf[b], 1);
       mbar_init(&te[b], 4);
     }
-    mbar_init(sempty, 1);
+    for (int l = 0; l < 3; ++l) mbar_init(&sempty[l], 1);
     mbar_init(tready, 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1810,7 +1810,7 @@ __global__ void __launch_bounds__(256, 1) k_beaver_tc_thin(const __grid_constant
         }
         __syncwarp();
         // the previous tile's MMAs must have read the limb tiles
-        if (l == 0 && it > 0) mbar_wait(sempty, (uint32_t)((it - 1) & 1));
+        if (it > 0) mbar_wait(&sempty[l], (uint32_t)((it - 1) & 1));  // the previous tile's party-l MMAs read theirs
 #pragma unroll
         for (int c = 0; c < 2; ++c) {  // A_l row (lane = row): 16 words at a time
           u64 v[16];
@@ -1859,7 +1859,7 @@ __global__ void __launch_bounds__(256, 1) k_beaver_tc_thin(const __grid_constant
         }
       }
       umma_commit(&tf[buf]);
-      if (l == L - 1) umma_commit(sempty);  // this tile's limb tiles may be overwritten
+      umma_commit(&sempty[l]);  // party l's A_l tiles (after the last party: D's too) may be overwritten
     };
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       const i64 row = (i64)t * 128 + rq * 32 + lane;
