@@ -93,6 +93,9 @@ __device__ __forceinline__ void pf_l2(const void* p) { asm volatile("prefetch.gl
 // variant): material reads then use generic loads instead of the global-only
 // __ldcs / __ldg. GS(G) is the lane-group size.
 #define MPX_STAGED 16
+#ifndef MPX_STAGED_ROLLED
+#define MPX_STAGED_ROLLED 1  // staged kernels keep the carry levels rolled (code size / icache)
+#endif
 #define GS(G) ((G) & 15)
 
 template <int L, int G>
@@ -334,7 +337,12 @@ __device__ __forceinline__ void d_carry_sum(u64 (&Gk)[L], u64 (&P)[L], const u64
                                             int& ti, i64 e, int p0, Sh<L>& out) {
   // levels s = 1, 2, 4, ... < m, unrolled; the 64-bit ring gets its own
   // constant-m copy (measured 7.7 vs 8.9 ms for the 2^24 Reciprocal)
-  if (m == 64) {
+  if constexpr ((G & MPX_STAGED) != 0 && MPX_STAGED_ROLLED) {
+    // staged (latency-bound, single-row) kernels: one rolled copy keeps the
+    // chain's code in the instruction cache
+#pragma unroll 1
+    for (int s = 1; s < m; s *= 2) d_carry_level<L, G>(Gk, P, m, s, next_take<L, G>(tape, ti, e), e, p0);
+  } else if (m == 64) {
 #pragma unroll
     for (int s = 1; s < 64; s *= 2) d_carry_level<L, G>(Gk, P, 64, s, next_take<L, G>(tape, ti, e), e, p0);
   } else {
