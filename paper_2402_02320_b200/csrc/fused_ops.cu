@@ -412,7 +412,10 @@ __device__ __forceinline__ Sh<L> d_lmo(const Sh<L>& bits, int m, const Tape& tap
   u64 Y[L];
 #pragma unroll
   for (int l = 0; l < L; ++l) Y[l] = bits.v[l];
-  if (m == 63) {
+  if constexpr ((G & MPX_STAGED) != 0 && MPX_STAGED_ROLLED) {  // one rolled copy (see d_carry_sum)
+#pragma unroll 1
+    for (int s = 1; s < m; s *= 2) d_lmo_level<L, G>(Y, m, s, next_take<L, G>(tape, ti, e), e, p0);
+  } else if (m == 63) {
 #pragma unroll
     for (int s = 1; s < 63; s *= 2) d_lmo_level<L, G>(Y, 63, s, next_take<L, G>(tape, ti, e), e, p0);
   } else if (m == 46) {  // Log's 2p window at the default p = 23
