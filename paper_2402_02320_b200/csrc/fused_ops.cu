@@ -96,6 +96,10 @@ __device__ __forceinline__ void pf_l2(const void* p) { asm volatile("prefetch.gl
 #ifndef MPX_STAGED_ROLLED
 #define MPX_STAGED_ROLLED 1  // staged kernels keep the carry levels rolled (code size / icache)
 #endif
+#ifndef MPX_ROLL_ALL
+#define MPX_ROLL_ALL 0  // every fused kernel rolled (sweeps)
+#endif
+#define MPX_ROLLED(G) ((((G) & MPX_STAGED) != 0 && MPX_STAGED_ROLLED) || MPX_ROLL_ALL)
 #define GS(G) ((G) & 15)
 
 template <int L, int G>
@@ -337,7 +341,7 @@ __device__ __forceinline__ void d_carry_sum(u64 (&Gk)[L], u64 (&P)[L], const u64
                                             int& ti, i64 e, int p0, Sh<L>& out) {
   // levels s = 1, 2, 4, ... < m, unrolled; the 64-bit ring gets its own
   // constant-m copy (measured 7.7 vs 8.9 ms for the 2^24 Reciprocal)
-  if constexpr ((G & MPX_STAGED) != 0 && MPX_STAGED_ROLLED) {
+  if constexpr (MPX_ROLLED(G)) {
     // staged (latency-bound, single-row) kernels: one rolled copy keeps the
     // chain's code in the instruction cache
 #pragma unroll 1
@@ -412,7 +416,7 @@ __device__ __forceinline__ Sh<L> d_lmo(const Sh<L>& bits, int m, const Tape& tap
   u64 Y[L];
 #pragma unroll
   for (int l = 0; l < L; ++l) Y[l] = bits.v[l];
-  if constexpr ((G & MPX_STAGED) != 0 && MPX_STAGED_ROLLED) {  // one rolled copy (see d_carry_sum)
+  if constexpr (MPX_ROLLED(G)) {  // one rolled copy (see d_carry_sum)
 #pragma unroll 1
     for (int s = 1; s < m; s *= 2) d_lmo_level<L, G>(Y, m, s, next_take<L, G>(tape, ti, e), e, p0);
   } else if (m == 63) {
