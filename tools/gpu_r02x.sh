@@ -1,7 +1,3 @@
-for v in "" roll; do
-  if [ -n "$v" ]; then export MPX_LIB=$PWD/paper_2402_02320_b200/libmpx_$v.so; else unset MPX_LIB; fi
-  echo "== ${v:-default}"
-  timeout 300 python tools/bench_fused.py --kinds reciprocal,exp,log,relu 2>&1 | tail -1
-  timeout 300 python tools/bench_fused.py --kinds reciprocal,exp,log --parties 3 --elems 4194304 2>&1 | tail -1
-  timeout 300 python tools/micro/graph_gaps.py 2>&1 | grep -i "kernels, span\|relu_fused"
-done
+timeout 900 python -m pytest -q -x tests/test_fused_ops.py tests/test_train.py tests/test_gpu_parity.py tests/test_transformer.py > gpurun_out/x_tests.log 2>&1; echo rc=$? >> gpurun_out/x_tests.log; tail -2 gpurun_out/x_tests.log
+timeout 300 python tools/micro/graph_gaps.py 2>&1 | grep -i "kernels, span\|relu_fused"
+timeout 300 python tools/bench_fused.py --kinds relu --elems 65536 2>&1 | tail -1
